@@ -1,0 +1,517 @@
+// Synthetic workload generator: 3-D hex meshes (natural,
+// scrambled, anisotropic) and the two block systems the hot path solves.
+//
+//   * 5x5 density-based Jacobian  — restates euler.cpp:390-455
+//     (assembleJacobian: first-order approximate Jacobian, Roe-averaged
+//     spectral radius, pseudo-time diagonal) and its RHS, the steady residual
+//     euler.cpp:361-389 with the Roe flux euler.cpp:116-150.
+//   * 4x4 pressure-based coupled p-U system — restates incompressible.cpp:
+//     momentumDiagCoeff :57-89, pressureGradients :91-126, rhieChowFlux
+//     :128-141, assembleCoupled :143-250, pinPressure :252-264.
+//
+// This is NOT the hot path (the matrix producers are out of scope);
+// it is the input side of the benchmark.  It reproduces the reference
+// producers bit for bit (same operation order, no FMA contraction: built with
+// -ffp-contract=off), which tests/test_generator.py checks against the
+// reference compiled in oracle/_ref.  Layouts are the reference's: int32
+// owner/neighbour per internal face (owner < neighbour), row-major n x n
+// blocks per cell/face, AoS vectors.
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <random>
+#include <vector>
+
+namespace {
+
+struct V3 {
+    double x, y, z;
+};
+inline V3 add(V3 a, V3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+inline V3 sub(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+inline V3 scl(V3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+inline V3 dvd(V3 a, double s) { return {a.x / s, a.y / s, a.z / s}; }
+inline double dot3(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+inline double len3(V3 a) { return std::sqrt(dot3(a, a)); }
+inline double comp(V3 a, int i) { return i == 0 ? a.x : (i == 1 ? a.y : a.z); }
+
+struct BFace {
+    int cell;
+    V3 area;  // outward
+};
+
+// Hex box: cells (k*ny + j)*nx + i before the optional scramble permutation.
+struct Hex {
+    int nc = 0;
+    std::vector<int> owner, neigh;
+    std::vector<V3> area;
+    std::vector<double> fx;
+    std::vector<double> vol;
+    std::vector<V3> cen;
+    std::vector<std::vector<BFace>> patches;  // xmin xmax ymin ymax zmin zmax
+};
+
+Hex buildHex(int nx, int ny, int nz, double aspect, long long scrambleSeed) {
+    Hex h;
+    const double lx = 1.0, ly = 1.0 * ny / nx;
+    const double hx = lx / nx, hy = ly / ny, hz = hx / aspect;
+    h.nc = nx * ny * nz;
+    std::vector<int> perm(h.nc);
+    for (int c = 0; c < h.nc; ++c) perm[c] = c;
+    if (scrambleSeed >= 0) {  // seeded Fisher-Yates on mt19937_64
+        std::mt19937_64 rng(static_cast<std::uint64_t>(scrambleSeed));
+        for (int i = h.nc - 1; i > 0; --i) {
+            const int j = static_cast<int>(rng() % static_cast<std::uint64_t>(i + 1));
+            std::swap(perm[i], perm[j]);
+        }
+    }
+    auto id = [&](int i, int j, int k) { return perm[(k * ny + j) * nx + i]; };
+    h.vol.assign(h.nc, hx * hy * hz);
+    h.cen.resize(h.nc);
+    for (int k = 0; k < nz; ++k)
+        for (int j = 0; j < ny; ++j)
+            for (int i = 0; i < nx; ++i) h.cen[id(i, j, k)] = {(i + 0.5) * hx, (j + 0.5) * hy, (k + 0.5) * hz};
+    auto face = [&](int a, int b, V3 s) {
+        if (a > b) {  // owner < neighbour convention (mesh.cpp:84-89)
+            std::swap(a, b);
+            s = {-s.x, -s.y, -s.z};
+            h.fx.push_back(1.0 - 0.5);
+        } else {
+            h.fx.push_back(0.5);
+        }
+        h.owner.push_back(a);
+        h.neigh.push_back(b);
+        h.area.push_back(s);
+    };
+    for (int k = 0; k < nz; ++k)
+        for (int j = 0; j < ny; ++j)
+            for (int i = 0; i < nx; ++i) {
+                if (i + 1 < nx) face(id(i, j, k), id(i + 1, j, k), {hy * hz, 0.0, 0.0});
+                if (j + 1 < ny) face(id(i, j, k), id(i, j + 1, k), {0.0, hx * hz, 0.0});
+                if (k + 1 < nz) face(id(i, j, k), id(i, j, k + 1), {0.0, 0.0, hx * hy});
+            }
+    h.patches.resize(6);
+    for (int k = 0; k < nz; ++k) for (int j = 0; j < ny; ++j) h.patches[0].push_back({id(0, j, k), {-hy * hz, 0.0, 0.0}});
+    for (int k = 0; k < nz; ++k) for (int j = 0; j < ny; ++j) h.patches[1].push_back({id(nx - 1, j, k), {hy * hz, 0.0, 0.0}});
+    for (int k = 0; k < nz; ++k) for (int i = 0; i < nx; ++i) h.patches[2].push_back({id(i, 0, k), {0.0, -hx * hz, 0.0}});
+    for (int k = 0; k < nz; ++k) for (int i = 0; i < nx; ++i) h.patches[3].push_back({id(i, ny - 1, k), {0.0, hx * hz, 0.0}});
+    for (int j = 0; j < ny; ++j) for (int i = 0; i < nx; ++i) h.patches[4].push_back({id(i, j, 0), {0.0, 0.0, -hx * hy}});
+    for (int j = 0; j < ny; ++j) for (int i = 0; i < nx; ++i) h.patches[5].push_back({id(i, j, nz - 1), {0.0, 0.0, hx * hy}});
+    return h;
+}
+
+// ---------------------------------------------------------------- Euler 5x5
+constexpr double kGamma = 1.4;
+// natural component [rho, m, E] -> block slot in the vector-first layout
+constexpr int kSlot[5] = {3, 0, 1, 2, 4};
+
+struct Prim {
+    double v[5];  // rho, ux, uy, uz, p
+};
+inline V3 vel(const Prim& q) { return {q.v[1], q.v[2], q.v[3]}; }
+
+struct RoeAvg {
+    double rho;
+    V3 u;
+    double H, c;
+};
+
+RoeAvg roeAvg(const Prim& L, const Prim& R) {
+    const double sL = std::sqrt(L.v[0]), sR = std::sqrt(R.v[0]);
+    const double w = 1.0 / (sL + sR);
+    RoeAvg a;
+    a.rho = sL * sR;
+    a.u = scl(add(scl(vel(L), sL), scl(vel(R), sR)), w);
+    const double HL = kGamma / (kGamma - 1.0) * L.v[4] / L.v[0] + 0.5 * dot3(vel(L), vel(L));
+    const double HR = kGamma / (kGamma - 1.0) * R.v[4] / R.v[0] + 0.5 * dot3(vel(R), vel(R));
+    a.H = (sL * HL + sR * HR) * w;
+    a.c = std::sqrt((kGamma - 1.0) * (a.H - 0.5 * dot3(a.u, a.u)));
+    return a;
+}
+
+void physFlux(const Prim& q, V3 n, double* f) {
+    const V3 u = vel(q);
+    const double un = dot3(u, n);
+    const double rhoE = q.v[4] / (kGamma - 1.0) + 0.5 * q.v[0] * dot3(u, u);
+    f[0] = q.v[0] * un;
+    f[1] = q.v[0] * u.x * un + q.v[4] * n.x;
+    f[2] = q.v[0] * u.y * un + q.v[4] * n.y;
+    f[3] = q.v[0] * u.z * un + q.v[4] * n.z;
+    f[4] = (rhoE + q.v[4]) * un;
+}
+
+// convective Jacobian d(F.n)/dQ in [rho, m, E] order
+void convJac(const Prim& q, V3 n, double* J) {
+    const V3 u = vel(q);
+    const double un = dot3(u, n);
+    const double g1 = kGamma - 1.0;
+    const double ek = 0.5 * dot3(u, u);
+    const double c = std::sqrt(kGamma * q.v[4] / q.v[0]);
+    const double H = c * c / g1 + ek;
+    const double nv[3] = {n.x, n.y, n.z};
+    const double uv[3] = {u.x, u.y, u.z};
+    J[0] = 0.0;
+    J[1] = nv[0];
+    J[2] = nv[1];
+    J[3] = nv[2];
+    J[4] = 0.0;
+    for (int i = 0; i < 3; ++i) {
+        double* row = J + 5 * (i + 1);
+        row[0] = g1 * ek * nv[i] - uv[i] * un;
+        for (int j = 0; j < 3; ++j) row[1 + j] = uv[i] * nv[j] - g1 * uv[j] * nv[i] + (i == j ? un : 0.0);
+        row[4] = g1 * nv[i];
+    }
+    double* e = J + 20;
+    e[0] = (g1 * ek - H) * un;
+    for (int j = 0; j < 3; ++j) e[1 + j] = H * nv[j] - g1 * uv[j] * un;
+    e[4] = kGamma * un;
+}
+
+void roe(const Prim& L, const Prim& R, V3 n, double* flux) {
+    double fL[5], fR[5];
+    physFlux(L, n, fL);
+    physFlux(R, n, fR);
+    const RoeAvg a = roeAvg(L, R);
+    const double un = dot3(a.u, n);
+    const double c = a.c;
+    const double dRho = R.v[0] - L.v[0];
+    const V3 dU = sub(vel(R), vel(L));
+    const double dUn = dot3(dU, n);
+    const double dP = R.v[4] - L.v[4];
+    const double a1 = (dP - a.rho * c * dUn) / (2.0 * c * c);
+    const double a5 = (dP + a.rho * c * dUn) / (2.0 * c * c);
+    const double a2 = dRho - dP / (c * c);
+    const double delta = 0.1 * (std::fabs(un) + c);
+    auto entropyFix = [delta](double lam) {
+        const double m = std::fabs(lam);
+        return m < delta ? (lam * lam + delta * delta) / (2.0 * delta) : m;
+    };
+    const double l1 = entropyFix(un - c);
+    const double l2 = std::fabs(un);
+    const double l5 = entropyFix(un + c);
+    double diss[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    auto wave = [&](double strength, double lam, double k0, V3 kU, double kE) {
+        const double w = strength * lam;
+        diss[0] += w * k0;
+        diss[1] += w * kU.x;
+        diss[2] += w * kU.y;
+        diss[3] += w * kU.z;
+        diss[4] += w * kE;
+    };
+    wave(a1, l1, 1.0, sub(a.u, scl(n, c)), a.H - c * un);
+    wave(a2, l2, 1.0, a.u, 0.5 * dot3(a.u, a.u));
+    wave(a5, l5, 1.0, add(a.u, scl(n, c)), a.H + c * un);
+    const V3 dUt = sub(dU, scl(n, dUn));
+    wave(a.rho, l2, 0.0, dUt, dot3(a.u, dU) - un * dUn);
+    for (int i = 0; i < 5; ++i) flux[i] = 0.5 * (fL[i] + fR[i]) - 0.5 * diss[i];
+}
+
+// dst(block order) += scale * J + lamScale * I
+void accumulate(double* dst, double scale, const double* J, double lamScale) {
+    for (int r = 0; r < 5; ++r)
+        for (int c = 0; c < 5; ++c) dst[kSlot[r] * 5 + kSlot[c]] += scale * J[r * 5 + c] + (r == c ? lamScale : 0.0);
+}
+
+void euler(const Hex& h, double* diag, double* upper, double* lower, double* rhs) {
+    const int nc = h.nc;
+    const int nf = static_cast<int>(h.owner.size());
+    std::mt19937 gen(2);
+    std::uniform_real_distribution<double> U(-0.05, 0.05);
+    std::vector<Prim> q(nc);
+    for (int c = 0; c < nc; ++c) {
+        const double d0 = U(gen);
+        const double d1 = U(gen);
+        const double d2 = U(gen);
+        const double d4 = U(gen);
+        q[c] = {{1.0 * (1.0 + d0), 0.5 + d1, 0.1 + d2, 0.0, (1.0 / 1.4) * (1.0 + d4)}};
+    }
+    const Prim farfield{{1.0, 0.5, 0.1, 0.0, 1.0 / 1.4}};
+    std::memset(diag, 0, sizeof(double) * 25 * nc);
+    std::memset(upper, 0, sizeof(double) * 25 * nf);
+    std::memset(lower, 0, sizeof(double) * 25 * nf);
+    std::vector<double> lamSum(nc, 0.0);
+    double J[25];
+    for (int f = 0; f < nf; ++f) {
+        const int o = h.owner[f], nb = h.neigh[f];
+        const double S = len3(h.area[f]);
+        const V3 n = dvd(h.area[f], S);
+        const RoeAvg a = roeAvg(q[o], q[nb]);
+        const double lam = std::fabs(dot3(a.u, n)) + a.c;
+        convJac(q[o], n, J);
+        accumulate(diag + 25 * static_cast<std::size_t>(o), 0.5 * S, J, 0.5 * S * lam);
+        accumulate(lower + 25 * static_cast<std::size_t>(f), -0.5 * S, J, -0.5 * S * lam);
+        convJac(q[nb], n, J);
+        accumulate(upper + 25 * static_cast<std::size_t>(f), 0.5 * S, J, -0.5 * S * lam);
+        accumulate(diag + 25 * static_cast<std::size_t>(nb), -0.5 * S, J, 0.5 * S * lam);
+        lamSum[o] += lam * S;
+        lamSum[nb] += lam * S;
+    }
+    for (const auto& patch : h.patches)
+        for (const BFace& bf : patch) {
+            const double S = len3(bf.area);
+            const V3 n = dvd(bf.area, S);
+            const RoeAvg a = roeAvg(q[bf.cell], farfield);
+            const double lam = std::fabs(dot3(a.u, n)) + a.c;
+            convJac(q[bf.cell], n, J);
+            accumulate(diag + 25 * static_cast<std::size_t>(bf.cell), 0.5 * S, J, 0.5 * S * lam);
+            lamSum[bf.cell] += lam * S;
+        }
+    const double cfl = 50.0;
+    for (int c = 0; c < nc; ++c) {
+        const double vOverDtau = lamSum[c] / cfl;
+        for (int r = 0; r < 5; ++r) diag[25 * static_cast<std::size_t>(c) + r * 5 + r] += vOverDtau;
+    }
+    // steady residual, natural component order, then permuted into the RHS
+    std::vector<double> res(5 * static_cast<std::size_t>(nc), 0.0);
+    double fl[5];
+    for (int f = 0; f < nf; ++f) {
+        const int o = h.owner[f], nb = h.neigh[f];
+        const double S = len3(h.area[f]);
+        const V3 n = dvd(h.area[f], S);
+        roe(q[o], q[nb], n, fl);
+        for (int k = 0; k < 5; ++k) {
+            res[5 * static_cast<std::size_t>(o) + k] -= S * fl[k];
+            res[5 * static_cast<std::size_t>(nb) + k] += S * fl[k];
+        }
+    }
+    for (const auto& patch : h.patches)
+        for (const BFace& bf : patch) {
+            const double S = len3(bf.area);
+            const V3 n = dvd(bf.area, S);
+            roe(q[bf.cell], farfield, n, fl);
+            for (int k = 0; k < 5; ++k) res[5 * static_cast<std::size_t>(bf.cell) + k] -= S * fl[k];
+        }
+    for (int c = 0; c < nc; ++c)
+        for (int k = 0; k < 5; ++k) rhs[5 * static_cast<std::size_t>(c) + kSlot[k]] = res[5 * static_cast<std::size_t>(c) + k];
+}
+
+// -------------------------------------------------------- coupled p-U 4x4
+// in-place partial-pivot LU + solve of a 3x3 (smallmat.hpp:67-108 semantics)
+void lu3Solve(double* a, double* x) {
+    int piv[3];
+    for (int k = 0; k < 3; ++k) {
+        int p = k;
+        double best = std::fabs(a[k * 3 + k]);
+        for (int i = k + 1; i < 3; ++i)
+            if (std::fabs(a[i * 3 + k]) > best) {
+                best = std::fabs(a[i * 3 + k]);
+                p = i;
+            }
+        piv[k] = p;
+        if (p != k)
+            for (int j = 0; j < 3; ++j) std::swap(a[k * 3 + j], a[p * 3 + j]);
+        const double d = a[k * 3 + k];
+        for (int i = k + 1; i < 3; ++i) {
+            a[i * 3 + k] /= d;
+            for (int j = k + 1; j < 3; ++j) a[i * 3 + j] -= a[i * 3 + k] * a[k * 3 + j];
+        }
+    }
+    for (int k = 0; k < 3; ++k)
+        if (piv[k] != k) std::swap(x[k], x[piv[k]]);
+    for (int i = 1; i < 3; ++i)
+        for (int j = 0; j < i; ++j) x[i] -= a[i * 3 + j] * x[j];
+    for (int i = 2; i >= 0; --i) {
+        for (int j = i + 1; j < 3; ++j) x[i] -= a[i * 3 + j] * x[j];
+        x[i] /= a[i * 3 + i];
+    }
+}
+
+std::vector<V3> lsqPressureGrad(const Hex& h, const std::vector<double>& s) {
+    const int nc = h.nc;
+    std::vector<double> G(9 * static_cast<std::size_t>(nc), 0.0);
+    std::vector<V3> b(nc, V3{0.0, 0.0, 0.0});
+    auto acc = [&](int i, int j) {
+        const V3 d = sub(h.cen[j], h.cen[i]);
+        const double w = 1.0 / dot3(d, d);
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) G[9 * static_cast<std::size_t>(i) + r * 3 + c] += w * comp(d, r) * comp(d, c);
+        const double t = w * (s[4 * static_cast<std::size_t>(j) + 3] - s[4 * static_cast<std::size_t>(i) + 3]);
+        b[i] = add(b[i], scl(d, t));
+    };
+    for (std::size_t f = 0; f < h.owner.size(); ++f) {
+        acc(h.owner[f], h.neigh[f]);
+        acc(h.neigh[f], h.owner[f]);
+    }
+    std::vector<V3> g(nc);
+    for (int i = 0; i < nc; ++i) {
+        double* Gi = &G[9 * static_cast<std::size_t>(i)];
+        double rv[3] = {b[i].x, b[i].y, b[i].z};
+        double scale = 0.0;
+        for (int r = 0; r < 3; ++r) scale = std::max(scale, Gi[r * 3 + r]);
+        for (int r = 0; r < 3; ++r)
+            if (Gi[r * 3 + r] <= 1e-12 * scale) {
+                for (int c = 0; c < 3; ++c) Gi[r * 3 + c] = Gi[c * 3 + r] = 0.0;
+                Gi[r * 3 + r] = 1.0;
+                rv[r] = 0.0;
+            }
+        lu3Solve(Gi, rv);
+        g[i] = {rv[0], rv[1], rv[2]};
+    }
+    return g;
+}
+
+void coupled(const Hex& h, double* diag, double* upper, double* lower, double* rhs, double* x0) {
+    const int nc = h.nc;
+    const int nf = static_cast<int>(h.owner.size());
+    const double nu = 0.01;
+    std::vector<double> s(4 * static_cast<std::size_t>(nc));
+    {
+        std::mt19937 gen(1);
+        std::uniform_real_distribution<double> U(-0.1, 0.1);
+        for (double& v : s) v = U(gen);
+    }
+    std::memcpy(x0, s.data(), sizeof(double) * s.size());
+    struct Geo {
+        double S, nd;
+    };
+    std::vector<Geo> geo(nf);
+    for (int f = 0; f < nf; ++f) {
+        const double S = len3(h.area[f]);
+        const V3 n = dvd(h.area[f], S);
+        geo[f] = {S, dot3(n, sub(h.cen[h.neigh[f]], h.cen[h.owner[f]]))};
+    }
+    auto wallDist = [&](const BFace& bf) { return h.vol[bf.cell] / (2.0 * len3(bf.area)); };
+    // momentum diagonal with phi = 0 (moving/static walls only contribute diffusion)
+    std::vector<double> aP(nc, 0.0);
+    for (int f = 0; f < nf; ++f) {
+        const double gDiff = nu * geo[f].S / geo[f].nd;
+        aP[h.owner[f]] += std::max(0.0, 0.0) + gDiff;
+        aP[h.neigh[f]] += -std::min(0.0, 0.0) + gDiff;
+    }
+    for (const auto& patch : h.patches)
+        for (const BFace& bf : patch) aP[bf.cell] += nu * len3(bf.area) / wallDist(bf);
+    std::vector<double> D(nc);
+    for (int i = 0; i < nc; ++i) D[i] = h.vol[i] / aP[i];
+    const std::vector<V3> gp = lsqPressureGrad(h, s);
+    auto Ucell = [&](int c) { return V3{s[4 * static_cast<std::size_t>(c)], s[4 * static_cast<std::size_t>(c) + 1], s[4 * static_cast<std::size_t>(c) + 2]}; };
+    std::vector<double> phi(nf);
+    for (int f = 0; f < nf; ++f) {
+        const int o = h.owner[f], nb = h.neigh[f];
+        const double fx = h.fx[f];
+        const V3 uBar = add(scl(Ucell(o), fx), scl(Ucell(nb), 1.0 - fx));
+        const double dBar = fx * D[o] + (1.0 - fx) * D[nb];
+        const double dpc = (s[4 * static_cast<std::size_t>(nb) + 3] - s[4 * static_cast<std::size_t>(o) + 3]) / geo[f].nd;
+        const V3 gpBar = add(scl(gp[o], fx), scl(gp[nb], 1.0 - fx));
+        phi[f] = dot3(h.area[f], uBar) - dBar * (geo[f].S * dpc - dot3(h.area[f], gpBar));
+    }
+    // assembleCoupled recomputes aP from the new fluxes
+    std::vector<double> aP2(nc, 0.0);
+    for (int f = 0; f < nf; ++f) {
+        const double gDiff = nu * geo[f].S / geo[f].nd;
+        aP2[h.owner[f]] += std::max(phi[f], 0.0) + gDiff;
+        aP2[h.neigh[f]] += -std::min(phi[f], 0.0) + gDiff;
+    }
+    for (const auto& patch : h.patches)
+        for (const BFace& bf : patch) aP2[bf.cell] += nu * len3(bf.area) / wallDist(bf);
+    for (int i = 0; i < nc; ++i) D[i] = h.vol[i] / aP2[i];
+    // (pressure gradients of the unchanged state are recomputed identically)
+    std::memset(diag, 0, sizeof(double) * 16 * nc);
+    std::memset(upper, 0, sizeof(double) * 16 * nf);
+    std::memset(lower, 0, sizeof(double) * 16 * nf);
+    std::memset(rhs, 0, sizeof(double) * 4 * nc);
+    constexpr int P = 3;
+    for (int f = 0; f < nf; ++f) {
+        const int o = h.owner[f], nb = h.neigh[f];
+        const double fx = h.fx[f];
+        const double gDiff = nu * geo[f].S / geo[f].nd;
+        const V3 Sf = h.area[f];
+        const double dBar = fx * D[o] + (1.0 - fx) * D[nb];
+        const double cc = dBar * geo[f].S / geo[f].nd;
+        double* dO = diag + 16 * static_cast<std::size_t>(o);
+        double* dN = diag + 16 * static_cast<std::size_t>(nb);
+        double* up = upper + 16 * static_cast<std::size_t>(f);
+        double* lo = lower + 16 * static_cast<std::size_t>(f);
+        for (int r = 0; r < 3; ++r) {
+            const double sr = comp(Sf, r);
+            dO[r * 4 + r] += std::max(phi[f], 0.0) + gDiff;
+            up[r * 4 + r] += std::min(phi[f], 0.0) - gDiff;
+            dN[r * 4 + r] += -std::min(phi[f], 0.0) + gDiff;
+            lo[r * 4 + r] += -std::max(phi[f], 0.0) - gDiff;
+            dO[r * 4 + P] += fx * sr;
+            up[r * 4 + P] += (1.0 - fx) * sr;
+            dN[r * 4 + P] -= (1.0 - fx) * sr;
+            lo[r * 4 + P] -= fx * sr;
+            dO[P * 4 + r] -= fx * sr;
+            up[P * 4 + r] -= (1.0 - fx) * sr;
+            dN[P * 4 + r] += (1.0 - fx) * sr;
+            lo[P * 4 + r] += fx * sr;
+        }
+        dO[P * 4 + P] -= cc;
+        up[P * 4 + P] += cc;
+        dN[P * 4 + P] -= cc;
+        lo[P * 4 + P] += cc;
+        const V3 gpBar = add(scl(gp[o], fx), scl(gp[nb], 1.0 - fx));
+        const double e = dBar * dot3(Sf, gpBar);
+        rhs[4 * static_cast<std::size_t>(o) + P] += e;
+        rhs[4 * static_cast<std::size_t>(nb) + P] -= e;
+    }
+    const V3 lid{1.0, 0.0, 0.0}, still{0.0, 0.0, 0.0};
+    for (int p = 0; p < 6; ++p) {
+        const V3 ub = p == 5 ? lid : still;
+        for (const BFace& bf : h.patches[p]) {
+            const double S = len3(bf.area);
+            const double gb = nu * S / wallDist(bf);
+            double* dP = diag + 16 * static_cast<std::size_t>(bf.cell);
+            for (int r = 0; r < 3; ++r) {
+                dP[r * 4 + r] += gb;
+                rhs[4 * static_cast<std::size_t>(bf.cell) + r] += gb * comp(ub, r);
+                dP[r * 4 + P] += comp(bf.area, r);
+            }
+        }
+    }
+    // pin p in cell 0
+    double* d0 = diag;
+    for (int c = 0; c < 4; ++c) d0[P * 4 + c] = 0.0;
+    d0[P * 4 + P] = 1.0;
+    for (int f = 0; f < nf; ++f) {
+        if (h.owner[f] == 0)
+            for (int c = 0; c < 4; ++c) upper[16 * static_cast<std::size_t>(f) + P * 4 + c] = 0.0;
+        if (h.neigh[f] == 0)
+            for (int c = 0; c < 4; ++c) lower[16 * static_cast<std::size_t>(f) + P * 4 + c] = 0.0;
+    }
+    rhs[P] = 0.0;
+}
+
+void exportTopo(const Hex& h, int* owner, int* neigh, double* centroids) {
+    std::memcpy(owner, h.owner.data(), sizeof(int) * h.owner.size());
+    std::memcpy(neigh, h.neigh.data(), sizeof(int) * h.neigh.size());
+    if (centroids)
+        for (int c = 0; c < h.nc; ++c) {
+            centroids[3 * c] = h.cen[c].x;
+            centroids[3 * c + 1] = h.cen[c].y;
+            centroids[3 * c + 2] = h.cen[c].z;
+        }
+}
+
+} // namespace
+
+extern "C" {
+
+void bcsgen_hex_sizes(int nx, int ny, int nz, int* nCells, int* nFaces) {
+    *nCells = nx * ny * nz;
+    *nFaces = (nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1);
+}
+
+// 5x5 density-based system. scrambleSeed < 0 keeps natural order.
+int bcsgen_hex_euler(int nx, int ny, int nz, double aspect, long long scrambleSeed, int* owner, int* neigh,
+                     double* diag, double* upper, double* lower, double* rhs, double* centroids) {
+    if (nx < 1 || ny < 1 || nz < 1 || !(aspect > 0.0)) return 1;
+    const Hex h = buildHex(nx, ny, nz, aspect, scrambleSeed);
+    exportTopo(h, owner, neigh, centroids);
+    euler(h, diag, upper, lower, rhs);
+    return 0;
+}
+
+// 4x4 pressure-based coupled system; x0 = the seeded state.
+int bcsgen_hex_coupled(int nx, int ny, int nz, double aspect, long long scrambleSeed, int* owner, int* neigh,
+                       double* diag, double* upper, double* lower, double* rhs, double* x0, double* centroids) {
+    if (nx < 1 || ny < 1 || nz < 1 || !(aspect > 0.0)) return 1;
+    const Hex h = buildHex(nx, ny, nz, aspect, scrambleSeed);
+    exportTopo(h, owner, neigh, centroids);
+    coupled(h, diag, upper, lower, rhs, x0);
+    return 0;
+}
+
+} // extern "C"
