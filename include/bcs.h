@@ -1,0 +1,152 @@
+/*
+ * bcs.h — C ABI of the B200-native block-coupled linear-solve path.
+ *
+ * One context drives one B200.  The boundary mirrors the reference's
+ * SolvePipeline (proj/core/include/blockfv/engine.hpp:28-38,
+ * proj/core/src/engine.cpp:47-120): face-addressed LDU upload, setup-or-
+ * replace by topology signature, AMG/DILU/LUSGS-preconditioned GMRES or
+ * BiCGStab to a relative tolerance, residual query.  Plain pointers and
+ * sizes only; no exceptions cross the ABI (status codes + bcs_last_error),
+ * which the C++ (include/bcs.hpp) and Python (paper_2403_07882_b200.bcs)
+ * wrappers turn back into the reference's std::invalid_argument /
+ * std::runtime_error semantics with the reference's message text.
+ *
+ * Layouts are exactly the reference host layouts:
+ *   owner/neighbour : int32 per internal face, owner < neighbour (mesh.cpp:84-89)
+ *   diag            : n_cells * n * n doubles, row-major n x n per cell
+ *   upper / lower   : n_faces * n * n doubles (upper = (owner row, neighbour col),
+ *                     lower = (neighbour row, owner col); block_matrix.hpp:40-87)
+ *   vectors         : n_cells * n doubles, AoS per cell (block_matrix.hpp:20-30)
+ * Block sizes 1..5 are supported on the device (hot configs: 4 and 5).
+ *
+ * Ownership: the caller owns every host array; it is read (or, for x,
+ * written) during the call only.  *_device entry points take device pointers
+ * on the context's device and enqueue on the context stream.
+ * Threading: a context is not thread-safe (the reference solve is not
+ * reentrant either).  Calls return with results valid.
+ */
+#ifndef BCS_H
+#define BCS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bcs_ctx bcs_ctx;
+
+typedef enum {
+    BCS_OK = 0,
+    BCS_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+    BCS_RUNTIME_ERROR = 2,    /* reference: std::runtime_error    */
+    BCS_CUDA_ERROR = 3,
+    BCS_NCCL_ERROR = 4,
+    BCS_OUT_OF_MEMORY = 5
+} bcs_status;
+
+/* KrylovMethod / PrecondKind (krylov.hpp:15-16) */
+enum { BCS_GMRES = 0, BCS_BICGSTAB = 1 };
+enum { BCS_PRECOND_NONE = 0, BCS_PRECOND_LUSGS = 1, BCS_PRECOND_DILU = 2, BCS_PRECOND_AMG = 3 };
+/* Backend (engine.hpp:17).  HOST_LDU keeps the reference's contract (only
+ * none/LUSGS allowed, zero convert/setup/retrieve timings) but executes on the
+ * device like every other path: there is no CPU fallback. */
+enum { BCS_BACKEND_HOST_LDU = 0, BCS_BACKEND_ENGINE_CSR = 1 };
+
+/* SolverConfig + AmgConfig (krylov.hpp:18-37).  The leading fields are
+ * layout-identical to the oracle's or_cfg. */
+typedef struct {
+    int method;              /* BCS_GMRES | BCS_BICGSTAB            (default GMRES) */
+    int precond;             /* BCS_PRECOND_*                        (default LUSGS) */
+    double rel_tol;          /* (default 1e-6)  */
+    double abs_tol;          /* (default 1e-300) */
+    int max_iters;           /* (default 500)   */
+    int gmres_restart;       /* (default 30)    */
+    int amg_max_levels;      /* (default 10)    */
+    int amg_min_coarse_rows; /* (default 8)     */
+    int amg_pre_sweeps;      /* (default 1)     */
+    int amg_post_sweeps;     /* (default 1)     */
+    int mode;                /* 0 = parity (reference operation order). Reserved. */
+} bcs_solver_config;
+
+/* SolveReport (krylov.hpp:39-50) + per-stage timings (seconds) with the
+ * reference keys (engine.cpp:80-112) and device sub-stages. */
+typedef struct {
+    int iterations;
+    int converged;
+    int breakdown;
+    int setup_branch; /* 1: setup (first call / topology change); 0: replace */
+    double initial_residual;
+    double final_residual;
+    double t_convert, t_setup, t_replace, t_solve, t_retrieve;
+    double t_amg_setup; /* preconditioner construction inside "solve" */
+    double t_krylov;    /* Krylov iterations inside "solve"          */
+    int amg_levels;
+    int coarse_rows;    /* rows of the coarsest level (dense LU is coarse_rows*n) */
+    /* kernel-level accounting (filled when bcs_set_kernel_timing(ctx,1)) */
+    int spmv_launches;
+    double spmv_ms;     /* summed CUDA-event time of the fine-level SpMV launches */
+    int kernel_launches;/* device kernels launched during the call */
+} bcs_report;
+
+void bcs_default_config(bcs_solver_config* cfg);
+const char* bcs_version(void);
+
+bcs_status bcs_create(bcs_ctx** out, int device);
+bcs_status bcs_destroy(bcs_ctx* ctx);
+const char* bcs_last_error(const bcs_ctx* ctx);
+/* Run all device work of this context on `stream` (a cudaStream_t); NULL
+ * restores the context's own stream. */
+bcs_status bcs_set_stream(bcs_ctx* ctx, void* stream);
+bcs_status bcs_set_kernel_timing(bcs_ctx* ctx, int enable);
+
+/* topologySignature (block_csr.cpp:146-160), exact; host only. */
+uint64_t bcs_topology_signature(int n_cells, int n_faces, const int32_t* owner, const int32_t* neighbour);
+
+/* ---- drop-in: one SolvePipeline::solve call (engine.cpp:47-120) ---------
+ * Host arrays.  b_len / x0_len are the element counts of b / x0 (the
+ * reference's BlockVector dimension check, engine.cpp:50-52).  x receives
+ * n_cells*n doubles.  Setup-or-replace is decided as the reference does, by
+ * topology signature against the previous call on this context. */
+bcs_status bcs_pipeline_solve(bcs_ctx* ctx, int n_cells, int n_faces, int block_size, const int32_t* owner,
+                              const int32_t* neighbour, const double* diag, const double* upper,
+                              const double* lower, const double* b, size_t b_len, const double* x0,
+                              size_t x0_len, double* x, int backend, const bcs_solver_config* cfg,
+                              bcs_report* report);
+
+/* ---- staged interface (device-resident workflows) ------------------------ */
+/* Builds the LDU->BSR plan (block_csr.cpp:56-80) on the device. */
+bcs_status bcs_set_topology(bcs_ctx* ctx, int n_cells, int n_faces, int block_size, const int32_t* owner,
+                            const int32_t* neighbour);
+/* Value permutation LDU->BSR (replaceValues, block_csr.cpp:120-127). */
+bcs_status bcs_upload_ldu(bcs_ctx* ctx, const double* diag, const double* upper, const double* lower);
+bcs_status bcs_upload_ldu_device(bcs_ctx* ctx, const double* d_diag, const double* d_upper,
+                                 const double* d_lower);
+/* Preconditioner build + Krylov on the current matrix; x holds x0 on entry. */
+bcs_status bcs_solve(bcs_ctx* ctx, const double* b, double* x, const bcs_solver_config* cfg, bcs_report* report);
+bcs_status bcs_solve_device(bcs_ctx* ctx, const double* d_b, double* d_x, const bcs_solver_config* cfg,
+                            bcs_report* report);
+
+/* ---- residual query and per-kernel entry points (parity tests / bench) --- */
+bcs_status bcs_residual(bcs_ctx* ctx, const double* b, const double* x, double* norm);
+/* relative residual per Krylov step of the last solve (same definition as
+ * the oracle: |g_{j+1}|/beta0, true residual at restarts/exit). */
+bcs_status bcs_residual_history(bcs_ctx* ctx, double* out, int cap, int* n);
+bcs_status bcs_spmv(bcs_ctx* ctx, const double* x, double* y);                  /* host arrays   */
+bcs_status bcs_spmv_device(bcs_ctx* ctx, const double* d_x, double* d_y);        /* device arrays */
+bcs_status bcs_csr_get(bcs_ctx* ctx, int32_t* row_offsets, int32_t* cols, double* values);
+bcs_status bcs_precond_setup(bcs_ctx* ctx, const bcs_solver_config* cfg);
+bcs_status bcs_precond_apply(bcs_ctx* ctx, const double* r, double* z);          /* host arrays   */
+bcs_status bcs_amg_depth(bcs_ctx* ctx, int* depth);
+bcs_status bcs_amg_level_sizes(bcs_ctx* ctx, int level, int* rows, int* nnz);
+bcs_status bcs_amg_level_get(bcs_ctx* ctx, int level, int32_t* row_offsets, int32_t* cols, double* values,
+                             int32_t* aggregate /* rows entries, or NULL; coarsest has none */);
+/* Level schedule of the last DILU/LUSGS setup of `level`: number of
+ * dependency levels of its lower-triangular DAG (critical path). */
+bcs_status bcs_level_schedule_depth(bcs_ctx* ctx, int level, int* depth);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BCS_H */

@@ -1,0 +1,319 @@
+"""Host-side mirror of the reference solver API over the C ABI.
+
+Reference interface (blockfv, proj/core/include/blockfv):
+  * ``SolverConfig`` / ``AmgConfig`` / ``SolveReport``   krylov.hpp:18-50
+  * ``KrylovMethod`` / ``PrecondKind``                  krylov.hpp:15-16
+  * ``Backend``, ``SolvePipeline.solve``, ``backend_solve`` engine.hpp:17-43
+  * ``BlockLduMatrix`` / ``BlockVector`` (layout only)   block_matrix.hpp:20-87
+
+Errors keep the reference's semantics: ``std::invalid_argument`` surfaces as
+``ValueError`` and ``std::runtime_error`` as ``RuntimeError`` with the
+reference's message text.  Everything numerical runs on the B200 through
+libbcs.so; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass, field
+from typing import Dict, Optional, Tuple
+
+import numpy as np
+
+from . import _native as N
+
+
+class KrylovMethod(enum.IntEnum):
+    GMRES = 0
+    PBiCGStab = 1
+
+
+class PrecondKind(enum.IntEnum):
+    none = 0
+    LUSGS = 1
+    DILU = 2
+    AMG = 3
+
+
+class Backend(enum.IntEnum):
+    HostLdu = 0
+    EngineCsr = 1
+
+
+@dataclass
+class AmgConfig:
+    maxLevels: int = 10
+    minCoarseRows: int = 8
+    preSweeps: int = 1
+    postSweeps: int = 1
+    aggregationSize: int = 2
+
+
+@dataclass
+class SolverConfig:
+    method: KrylovMethod = KrylovMethod.GMRES
+    preconditioner: PrecondKind = PrecondKind.LUSGS
+    relTol: float = 1e-6
+    absTol: float = 1e-300
+    maxIters: int = 500
+    gmresRestart: int = 30
+    amg: AmgConfig = field(default_factory=AmgConfig)
+
+    def to_c(self) -> N.SolverConfigC:
+        return N.SolverConfigC(
+            int(self.method), int(self.preconditioner), float(self.relTol), float(self.absTol),
+            int(self.maxIters), int(self.gmresRestart), int(self.amg.maxLevels), int(self.amg.minCoarseRows),
+            int(self.amg.preSweeps), int(self.amg.postSweeps), 0,
+        )
+
+
+@dataclass
+class SolveReport:
+    iterations: int = 0
+    initialResidual: float = 0.0
+    finalResidual: float = 0.0
+    converged: bool = False
+    breakdown: bool = False
+    timings: Dict[str, float] = field(default_factory=dict)
+    amgLevels: int = 0
+    coarseRows: int = 0
+    spmvLaunches: int = 0
+    spmvMs: float = 0.0
+    kernelLaunches: int = 0
+
+    @staticmethod
+    def from_c(r: N.ReportC, backend: Optional[Backend] = None) -> "SolveReport":
+        t = {"convert": r.t_convert, "solve": r.t_solve, "retrieve": r.t_retrieve,
+             "amgSetup": r.t_amg_setup, "krylov": r.t_krylov}
+        if backend is None or backend == Backend.EngineCsr:
+            t["setup"] = r.t_setup
+            t["replace"] = r.t_replace
+        else:
+            t["setup"] = 0.0
+        return SolveReport(r.iterations, r.initial_residual, r.final_residual, bool(r.converged),
+                           bool(r.breakdown), t, r.amg_levels, r.coarse_rows, r.spmv_launches, r.spmv_ms,
+                           r.kernel_launches)
+
+    def csvRow(self) -> str:  # krylov.cpp:24-34
+        g = self.timings.get
+        return ",".join(f"{v:.12g}" for v in (self.iterations, self.initialResidual, self.finalResidual,
+                                              g("convert", 0.0), g("setup", 0.0), g("solve", 0.0),
+                                              g("retrieve", 0.0)))
+
+    @staticmethod
+    def csvHeader() -> str:
+        return "iter,initRes,finalRes,tConvert,tSetup,tSolve,tRetrieve"
+
+
+class BlockVector:
+    """AoS block vector: n_cells * block_size doubles (block_matrix.hpp:20-30)."""
+
+    def __init__(self, n_cells: int = 0, block_size: int = 0, values: Optional[np.ndarray] = None):
+        self.blockSize = int(block_size)
+        if values is None:
+            values = np.zeros(int(n_cells) * int(block_size))
+        self.values = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
+
+    def nCells(self) -> int:
+        return self.values.size // self.blockSize if self.blockSize else 0
+
+
+class BlockLduMatrix:
+    """Face-addressed block LDU operator (block_matrix.hpp:40-87), layout only.
+
+    owner/neighbour: int32 per internal face with owner < neighbour;
+    diag (n_cells, n, n), upper/lower (n_faces, n, n), row-major blocks.
+    """
+
+    def __init__(self, n_cells: int, owner, neighbour, block_size: int, diag=None, upper=None, lower=None):
+        self.n_cells = int(n_cells)
+        self.owner = np.ascontiguousarray(owner, dtype=np.int32)
+        self.neighbour = np.ascontiguousarray(neighbour, dtype=np.int32)
+        self.n = int(block_size)
+        nn = self.n * self.n
+        nf = self.owner.size
+        self.diag = np.zeros(self.n_cells * nn) if diag is None else np.ascontiguousarray(diag, np.float64).reshape(-1)
+        self.upper = np.zeros(nf * nn) if upper is None else np.ascontiguousarray(upper, np.float64).reshape(-1)
+        self.lower = np.zeros(nf * nn) if lower is None else np.ascontiguousarray(lower, np.float64).reshape(-1)
+
+    def blockSize(self) -> int:
+        return self.n
+
+    def nCells(self) -> int:
+        return self.n_cells
+
+    def nFaces(self) -> int:
+        return int(self.owner.size)
+
+
+def _raise(status: int, msg: str):
+    if status == N.BCS_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if status == N.BCS_OUT_OF_MEMORY:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+class Context:
+    """One bcs_ctx (one B200)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = N.lib()
+        h = ctypes.c_void_p()
+        st = self._lib.bcs_create(ctypes.byref(h), int(device))
+        if st != N.BCS_OK:
+            _raise(st, self._lib.bcs_last_error(None).decode())
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.bcs_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ck(self, st: int):
+        if st != N.BCS_OK:
+            _raise(st, self._lib.bcs_last_error(self.h).decode())
+
+    # --- staged interface
+    def set_stream(self, stream_ptr: int):
+        self._ck(self._lib.bcs_set_stream(self.h, ctypes.c_void_p(stream_ptr)))
+
+    def set_kernel_timing(self, on: bool):
+        self._ck(self._lib.bcs_set_kernel_timing(self.h, 1 if on else 0))
+
+    def set_topology(self, A: BlockLduMatrix):
+        self._ck(self._lib.bcs_set_topology(self.h, A.n_cells, A.nFaces(), A.n, N.ptr(A.owner), N.ptr(A.neighbour)))
+
+    def upload_ldu(self, A: BlockLduMatrix):
+        self._ck(self._lib.bcs_upload_ldu(self.h, N.ptr(A.diag), N.ptr(A.upper), N.ptr(A.lower)))
+
+    def upload_ldu_device(self, d_diag: int, d_upper: int, d_lower: int):
+        self._ck(self._lib.bcs_upload_ldu_device(self.h, c_ptr(d_diag), c_ptr(d_upper), c_ptr(d_lower)))
+
+    def solve(self, b: np.ndarray, x: np.ndarray, cfg: SolverConfig) -> SolveReport:
+        rep = N.ReportC()
+        c = cfg.to_c()
+        self._ck(self._lib.bcs_solve(self.h, N.ptr(b), N.ptr(x), ctypes.byref(c), ctypes.byref(rep)))
+        return SolveReport.from_c(rep)
+
+    def solve_device(self, d_b: int, d_x: int, cfg: SolverConfig) -> SolveReport:
+        rep = N.ReportC()
+        c = cfg.to_c()
+        self._ck(self._lib.bcs_solve_device(self.h, c_ptr(d_b), c_ptr(d_x), ctypes.byref(c), ctypes.byref(rep)))
+        return SolveReport.from_c(rep)
+
+    def residual(self, b: np.ndarray, x: np.ndarray) -> float:
+        v = ctypes.c_double()
+        self._ck(self._lib.bcs_residual(self.h, N.ptr(b), N.ptr(x), ctypes.byref(v)))
+        return v.value
+
+    def residual_history(self) -> np.ndarray:
+        n = ctypes.c_int()
+        self._ck(self._lib.bcs_residual_history(self.h, None, 0, ctypes.byref(n)))
+        out = np.zeros(n.value)
+        self._ck(self._lib.bcs_residual_history(self.h, N.ptr(out), n.value, ctypes.byref(n)))
+        return out
+
+    def spmv(self, x: np.ndarray) -> np.ndarray:
+        y = np.zeros_like(x)
+        self._ck(self._lib.bcs_spmv(self.h, N.ptr(x), N.ptr(y)))
+        return y
+
+    def spmv_device(self, d_x: int, d_y: int):
+        self._ck(self._lib.bcs_spmv_device(self.h, c_ptr(d_x), c_ptr(d_y)))
+
+    def csr(self, n_cells: int, nnz: int, n: int):
+        ro = np.zeros(n_cells + 1, np.int32)
+        ci = np.zeros(nnz, np.int32)
+        v = np.zeros(nnz * n * n)
+        self._ck(self._lib.bcs_csr_get(self.h, N.ptr(ro), N.ptr(ci), N.ptr(v)))
+        return ro, ci, v
+
+    def precond_setup(self, cfg: SolverConfig):
+        c = cfg.to_c()
+        self._ck(self._lib.bcs_precond_setup(self.h, ctypes.byref(c)))
+
+    def precond_apply(self, r: np.ndarray) -> np.ndarray:
+        z = np.zeros_like(r)
+        self._ck(self._lib.bcs_precond_apply(self.h, N.ptr(r), N.ptr(z)))
+        return z
+
+    def amg_depth(self) -> int:
+        d = ctypes.c_int()
+        self._ck(self._lib.bcs_amg_depth(self.h, ctypes.byref(d)))
+        return d.value
+
+    def amg_level(self, level: int, n: int):
+        rows, nnz = ctypes.c_int(), ctypes.c_int()
+        self._ck(self._lib.bcs_amg_level_sizes(self.h, level, ctypes.byref(rows), ctypes.byref(nnz)))
+        ro = np.zeros(rows.value + 1, np.int32)
+        ci = np.zeros(nnz.value, np.int32)
+        v = np.zeros(nnz.value * n * n)
+        agg = np.full(rows.value, -1, np.int32)
+        self._ck(self._lib.bcs_amg_level_get(self.h, level, N.ptr(ro), N.ptr(ci), N.ptr(v), N.ptr(agg)))
+        return ro, ci, v, agg
+
+    def schedule_depth(self, level: int) -> int:
+        d = ctypes.c_int()
+        self._ck(self._lib.bcs_level_schedule_depth(self.h, level, ctypes.byref(d)))
+        return d.value
+
+    def pipeline_solve(self, A: BlockLduMatrix, b: BlockVector, x0: BlockVector, backend: Backend,
+                       cfg: SolverConfig) -> Tuple[BlockVector, SolveReport]:
+        x = BlockVector(A.n_cells, A.n)
+        rep = N.ReportC()
+        c = cfg.to_c()
+        st = self._lib.bcs_pipeline_solve(
+            self.h, A.n_cells, A.nFaces(), A.n, N.ptr(A.owner), N.ptr(A.neighbour), N.ptr(A.diag),
+            N.ptr(A.upper), N.ptr(A.lower), N.ptr(b.values), b.values.size, N.ptr(x0.values), x0.values.size,
+            N.ptr(x.values), int(backend), ctypes.byref(c), ctypes.byref(rep))
+        self._ck(st)
+        return x, SolveReport.from_c(rep, backend)
+
+
+def c_ptr(p) -> ctypes.c_void_p:
+    return ctypes.c_void_p(int(p))
+
+
+def topology_signature(A: BlockLduMatrix) -> int:
+    return int(N.lib().bcs_topology_signature(A.n_cells, A.nFaces(), N.ptr(A.owner), N.ptr(A.neighbour)))
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+class SolvePipeline:
+    """Stateful pipeline (engine.hpp:28-38): setup on first call / topology
+    change, value replace otherwise.  Each pipeline owns one device context."""
+
+    def __init__(self, device: int = 0):
+        self.ctx = Context(device)
+
+    def solve(self, A: BlockLduMatrix, b: BlockVector, x0: BlockVector, backend: Backend,
+              cfg: SolverConfig) -> Tuple[BlockVector, SolveReport]:
+        if b.blockSize != A.n or x0.blockSize != A.n or b.nCells() != A.n_cells or x0.nCells() != A.n_cells:
+            raise ValueError("SolvePipeline::solve: dimension mismatch")
+        return self.ctx.pipeline_solve(A, b, x0, backend, cfg)
+
+
+def backend_solve(A: BlockLduMatrix, b: BlockVector, x0: BlockVector, backend: Backend,
+                  cfg: SolverConfig) -> Tuple[BlockVector, SolveReport]:
+    """One-shot fresh pipeline (engine.cpp:122-127)."""
+    p = SolvePipeline()
+    try:
+        return p.solve(A, b, x0, backend, cfg)
+    finally:
+        p.ctx.close()

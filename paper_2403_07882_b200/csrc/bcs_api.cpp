@@ -1,0 +1,218 @@
+// C ABI (include/bcs.h) over bcs::Engine.  Exceptions never cross the ABI:
+// std::invalid_argument -> BCS_INVALID_ARGUMENT, std::bad_alloc ->
+// BCS_OUT_OF_MEMORY, CudaError -> BCS_CUDA_ERROR, any other std::exception
+// (the reference's std::runtime_error cases) -> BCS_RUNTIME_ERROR; the message
+// is kept per context (or thread-locally for context-free calls).
+#include "../../include/bcs.h"
+#include "engine.hpp"
+
+#include <cstring>
+#include <new>
+#include <string>
+
+struct bcs_ctx {
+    bcs::Engine* eng = nullptr;
+    std::string err;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+bcs_status guarded(bcs_ctx* ctx, F&& f) {
+    std::string& msg = ctx ? ctx->err : g_err;
+    try {
+        f();
+        msg.clear();
+        return BCS_OK;
+    } catch (const std::invalid_argument& e) {
+        msg = e.what();
+        return BCS_INVALID_ARGUMENT;
+    } catch (const std::bad_alloc&) {
+        msg = "out of device or host memory";
+        return BCS_OUT_OF_MEMORY;
+    } catch (const bcs::CudaError& e) {
+        msg = e.what();
+        return BCS_CUDA_ERROR;
+    } catch (const std::exception& e) {
+        msg = e.what();
+        return BCS_RUNTIME_ERROR;
+    } catch (...) {
+        msg = "unknown error";
+        return BCS_RUNTIME_ERROR;
+    }
+}
+
+bcs::Engine& eng(bcs_ctx* ctx) {
+    if (!ctx || !ctx->eng) throw std::invalid_argument("bcs: null context");
+    return *ctx->eng;
+}
+const bcs_solver_config& cfgOf(const bcs_solver_config* c) {
+    if (!c) throw std::invalid_argument("bcs: null solver config");
+    return *c;
+}
+}  // namespace
+
+namespace bcs {
+uint64_t topologySignatureHost(int nc, int nf, const int32_t* owner, const int32_t* neigh);
+}
+
+extern "C" {
+
+void bcs_default_config(bcs_solver_config* c) {
+    if (!c) return;
+    c->method = BCS_GMRES;
+    c->precond = BCS_PRECOND_LUSGS;
+    c->rel_tol = 1e-6;
+    c->abs_tol = 1e-300;
+    c->max_iters = 500;
+    c->gmres_restart = 30;
+    c->amg_max_levels = 10;
+    c->amg_min_coarse_rows = 8;
+    c->amg_pre_sweeps = 1;
+    c->amg_post_sweeps = 1;
+    c->mode = 0;
+}
+
+const char* bcs_version(void) { return "bcs 0.1 (sm_100a)"; }
+
+bcs_status bcs_create(bcs_ctx** out, int device) {
+    if (!out) return BCS_INVALID_ARGUMENT;
+    *out = nullptr;
+    auto* c = new (std::nothrow) bcs_ctx;
+    if (!c) return BCS_OUT_OF_MEMORY;
+    const bcs_status st = guarded(nullptr, [&] { c->eng = new bcs::Engine(device); });
+    if (st != BCS_OK) {
+        delete c;
+        return st;
+    }
+    *out = c;
+    return BCS_OK;
+}
+
+bcs_status bcs_destroy(bcs_ctx* ctx) {
+    if (!ctx) return BCS_OK;
+    delete ctx->eng;
+    delete ctx;
+    return BCS_OK;
+}
+
+const char* bcs_last_error(const bcs_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+bcs_status bcs_set_stream(bcs_ctx* ctx, void* stream) {
+    return guarded(ctx, [&] { eng(ctx).setStream(static_cast<cudaStream_t>(stream)); });
+}
+
+bcs_status bcs_set_kernel_timing(bcs_ctx* ctx, int enable) {
+    return guarded(ctx, [&] { eng(ctx).setKernelTiming(enable != 0); });
+}
+
+uint64_t bcs_topology_signature(int n_cells, int n_faces, const int32_t* owner, const int32_t* neighbour) {
+    return bcs::topologySignatureHost(n_cells, n_faces, owner, neighbour);
+}
+
+bcs_status bcs_pipeline_solve(bcs_ctx* ctx, int n_cells, int n_faces, int block_size, const int32_t* owner,
+                              const int32_t* neighbour, const double* diag, const double* upper,
+                              const double* lower, const double* b, size_t b_len, const double* x0,
+                              size_t x0_len, double* x, int backend, const bcs_solver_config* cfg,
+                              bcs_report* report) {
+    return guarded(ctx, [&] {
+        bcs_report rep{};
+        eng(ctx).pipelineSolve(n_cells, n_faces, block_size, owner, neighbour, diag, upper, lower, b, b_len, x0,
+                               x0_len, x, backend, cfgOf(cfg), rep);
+        if (report) *report = rep;
+    });
+}
+
+bcs_status bcs_set_topology(bcs_ctx* ctx, int n_cells, int n_faces, int block_size, const int32_t* owner,
+                            const int32_t* neighbour) {
+    return guarded(ctx, [&] { eng(ctx).setTopology(n_cells, n_faces, block_size, owner, neighbour); });
+}
+
+bcs_status bcs_upload_ldu(bcs_ctx* ctx, const double* diag, const double* upper, const double* lower) {
+    return guarded(ctx, [&] {
+        eng(ctx).uploadLdu(diag, upper, lower, false);
+        cudaStreamSynchronize(eng(ctx).stream());
+    });
+}
+
+bcs_status bcs_upload_ldu_device(bcs_ctx* ctx, const double* d_diag, const double* d_upper, const double* d_lower) {
+    return guarded(ctx, [&] { eng(ctx).uploadLdu(d_diag, d_upper, d_lower, true); });
+}
+
+bcs_status bcs_solve(bcs_ctx* ctx, const double* b, double* x, const bcs_solver_config* cfg, bcs_report* report) {
+    return guarded(ctx, [&] {
+        bcs_report rep{};
+        eng(ctx).solveHost(b, x, cfgOf(cfg), rep);
+        if (report) *report = rep;
+    });
+}
+
+bcs_status bcs_solve_device(bcs_ctx* ctx, const double* d_b, double* d_x, const bcs_solver_config* cfg,
+                            bcs_report* report) {
+    return guarded(ctx, [&] {
+        bcs_report rep{};
+        eng(ctx).solveDevice(d_b, d_x, cfgOf(cfg), rep);
+        if (report) *report = rep;
+    });
+}
+
+bcs_status bcs_residual(bcs_ctx* ctx, const double* b, const double* x, double* norm) {
+    return guarded(ctx, [&] {
+        const double v = eng(ctx).residualNorm(b, x);
+        if (norm) *norm = v;
+    });
+}
+
+bcs_status bcs_residual_history(bcs_ctx* ctx, double* out, int cap, int* n) {
+    return guarded(ctx, [&] {
+        const auto& h = eng(ctx).history();
+        const int cnt = static_cast<int>(h.size());
+        if (n) *n = cnt;
+        if (out)
+            for (int i = 0; i < cnt && i < cap; ++i) out[i] = h[i];
+    });
+}
+
+bcs_status bcs_spmv(bcs_ctx* ctx, const double* x, double* y) {
+    return guarded(ctx, [&] { eng(ctx).spmvHost(x, y); });
+}
+
+bcs_status bcs_spmv_device(bcs_ctx* ctx, const double* d_x, double* d_y) {
+    return guarded(ctx, [&] { eng(ctx).spmvDevice(d_x, d_y); });
+}
+
+bcs_status bcs_csr_get(bcs_ctx* ctx, int32_t* row_offsets, int32_t* cols, double* values) {
+    return guarded(ctx, [&] { eng(ctx).csrGet(row_offsets, cols, values); });
+}
+
+bcs_status bcs_precond_setup(bcs_ctx* ctx, const bcs_solver_config* cfg) {
+    return guarded(ctx, [&] { eng(ctx).precondSetup(cfgOf(cfg)); });
+}
+
+bcs_status bcs_precond_apply(bcs_ctx* ctx, const double* r, double* z) {
+    return guarded(ctx, [&] { eng(ctx).precondApplyHost(r, z); });
+}
+
+bcs_status bcs_amg_depth(bcs_ctx* ctx, int* depth) {
+    return guarded(ctx, [&] {
+        if (depth) *depth = eng(ctx).amgDepth();
+    });
+}
+
+bcs_status bcs_amg_level_sizes(bcs_ctx* ctx, int level, int* rows, int* nnz) {
+    return guarded(ctx, [&] { eng(ctx).amgLevelSizes(level, rows, nnz); });
+}
+
+bcs_status bcs_amg_level_get(bcs_ctx* ctx, int level, int32_t* row_offsets, int32_t* cols, double* values,
+                             int32_t* aggregate) {
+    return guarded(ctx, [&] { eng(ctx).amgLevelGet(level, row_offsets, cols, values, aggregate); });
+}
+
+bcs_status bcs_level_schedule_depth(bcs_ctx* ctx, int level, int* depth) {
+    return guarded(ctx, [&] {
+        if (depth) *depth = eng(ctx).scheduleDepth(level);
+    });
+}
+
+}  // extern "C"

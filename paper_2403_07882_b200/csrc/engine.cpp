@@ -1,0 +1,812 @@
+// bcs::Engine implementation — host orchestration of the device path.
+//
+// Mirrors the reference control flow line by line where it matters for
+// parity: SolvePipeline::solve (engine.cpp:47-120), makeCsrPreconditioner
+// (engine.cpp:21-29), AmgHierarchy ctor / vcycle (amg.cpp:73-158),
+// gmresSolve / bicgstabSolve (krylov.cpp:59-214).  All numerical work is on
+// the device; the host only sequences kernels and reads the few scalars the
+// reference's control flow branches on.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+namespace bcs {
+
+void check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    if (e == cudaErrorMemoryAllocation) throw std::bad_alloc();
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+using clk = std::chrono::steady_clock;
+double secs(clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); }
+
+uint64_t hashCombine(uint64_t h, uint64_t v) {
+    h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    return h;
+}
+
+// RAII: count launches of one API call into the report
+struct LaunchScope {
+    LaunchCounter* prev;
+    explicit LaunchScope(LaunchCounter* c) : prev(g_launches) { g_launches = c; }
+    ~LaunchScope() { g_launches = prev; }
+};
+}  // namespace
+
+// topologySignature (block_csr.cpp:146-160) — exact, host side
+uint64_t topologySignatureHost(int nc, int nf, const int32_t* owner, const int32_t* neigh) {
+    uint64_t h = hashCombine(0, static_cast<uint64_t>(static_cast<int64_t>(nc)));
+    std::vector<uint64_t> keys(static_cast<size_t>(nf));
+    bool sorted = true;
+    for (int f = 0; f < nf; ++f) {
+        keys[f] = (static_cast<uint64_t>(static_cast<uint32_t>(owner[f])) << 32) | static_cast<uint32_t>(neigh[f]);
+        if (f && keys[f] < keys[f - 1]) sorted = false;
+    }
+    // (owner, neighbour) are non-negative, so unsigned packing preserves the order
+    if (!sorted) std::sort(keys.begin(), keys.end());
+    for (uint64_t k : keys) {
+        h = hashCombine(h, static_cast<uint64_t>(static_cast<int64_t>(static_cast<int32_t>(k >> 32))));
+        h = hashCombine(h, static_cast<uint64_t>(static_cast<int64_t>(static_cast<int32_t>(k & 0xffffffffu))));
+    }
+    return h;
+}
+
+Engine::Engine(int device) : device_(device) {
+    check(cudaSetDevice(device), "cudaSetDevice");
+    check(cudaStreamCreateWithFlags(&own_, cudaStreamNonBlocking), "cudaStreamCreate");
+    stream_ = own_;
+    cudaMemPool_t pool;
+    check(cudaDeviceGetDefaultMemPool(&pool, device), "cudaDeviceGetDefaultMemPool");
+    uint64_t thr = std::numeric_limits<uint64_t>::max();
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    check(cudaMallocHost(reinterpret_cast<void**>(&hStatus_), 8 * sizeof(double)), "cudaMallocHost");
+    check(cudaEventCreate(&ev0_), "cudaEventCreate");
+    check(cudaEventCreate(&ev1_), "cudaEventCreate");
+    err_.ensure(4, stream_);
+    ctr_.ensure(4, stream_);
+    ticket_.ensure(4, stream_);
+    push_.ensure(8, stream_);
+    cudaMemsetAsync(ctr_.p, 0, 4 * sizeof(int), stream_);
+    cudaMemsetAsync(ticket_.p, 0, 4 * sizeof(int), stream_);
+    partials_.ensure(static_cast<size_t>(reduce_blocks()) + 8, stream_);
+    scal_.ensure(16, stream_);
+    sync();
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device_);
+    cudaStreamSynchronize(stream_);
+    // device arrays are released with the pool when the context goes away;
+    // free explicitly to keep long-lived processes lean
+    auto rel = [&](auto& a) { a.release(stream_); };
+    for (auto& L : levels_) {
+        rel(L.o_ro); rel(L.o_ci); rel(L.o_dg); rel(L.o_tpos); rel(L.o_v); rel(L.lu); rel(L.piv); rel(L.order);
+        rel(L.agg); rel(L.members); rel(L.r); rel(L.z); rel(L.res); rel(L.y); rel(L.zb);
+    }
+    rel(dOwner_); rel(dNeigh_); rel(ro_); rel(ci_); rel(dg_); rel(tpos_); rel(src_); rel(fill_); rel(vals_);
+    rel(ldu_diag_); rel(ldu_upper_); rel(ldu_lower_); rel(dense_); rel(dpiv_); rel(cnt_); rel(lvl_); rel(push_);
+    rel(scanTmp_); rel(flag_); rel(err_); rel(ctr_); rel(choice_); rel(segOff_); rel(cro_); rel(big_); rel(dn_);
+    rel(str_); rel(keys_); rel(sorted_); rel(V_); rel(w_); rel(zk_); rel(rk_); rel(H_); rel(cs_); rel(sn_); rel(g_);
+    rel(y_); rel(scal_); rel(partials_); rel(kb_); rel(kx_); rel(bp_); rel(bv_); rel(bs_); rel(bt_); rel(bph_);
+    rel(bsh_); rel(brh_); rel(ticket_);
+    cudaStreamSynchronize(stream_);
+    if (hStatus_) cudaFreeHost(hStatus_);
+    if (ev0_) cudaEventDestroy(ev0_);
+    if (ev1_) cudaEventDestroy(ev1_);
+    if (own_) cudaStreamDestroy(own_);
+}
+
+void Engine::setStream(cudaStream_t s) {
+    sync();
+    stream_ = s ? s : own_;
+}
+
+void Engine::sync() { check(cudaStreamSynchronize(stream_), "cudaStreamSynchronize"); }
+
+void Engine::checkErr(const char* where) {
+    check(cudaGetLastError(), where);
+}
+
+int Engine::readErrCell() {
+    int v = 0;
+    check(cudaMemcpyAsync(&v, err_.p, sizeof(int), cudaMemcpyDeviceToHost, stream_), "read err");
+    sync();
+    return v;
+}
+
+// --------------------------------------------------------------- topology
+void Engine::setTopology(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh) {
+    LaunchScope ls(&launches_);
+    if (n < 1 || n > 5) throw std::invalid_argument("bcs: block size must be 1..5 on the device");
+    if (nc < 1 || nf < 0) throw std::invalid_argument("bcs: need n_cells >= 1 and n_faces >= 0");
+    for (int f = 0; f < nf; ++f)
+        if (owner[f] < 0 || neigh[f] >= nc || owner[f] >= neigh[f])
+            throw std::invalid_argument("bcs: face " + std::to_string(f) +
+                                        " violates 0 <= owner < neighbour < n_cells");
+    nc_ = nc;
+    nf_ = nf;
+    n_ = n;
+    hOwner_.assign(owner, owner + nf);
+    hNeigh_.assign(neigh, neigh + nf);
+    const size_t nnz = static_cast<size_t>(nc) + 2 * static_cast<size_t>(nf);
+    if (nnz > static_cast<size_t>(std::numeric_limits<int>::max()))
+        throw std::invalid_argument("bcs: more than 2^31-1 blocks");
+    dOwner_.ensure(nf, stream_);
+    dNeigh_.ensure(nf, stream_);
+    ro_.ensure(nc + 1, stream_);
+    ci_.ensure(nnz, stream_);
+    src_.ensure(nnz, stream_);
+    dg_.ensure(nc, stream_);
+    tpos_.ensure(nnz, stream_);
+    fill_.ensure(nc + 1, stream_);
+    scanTmp_.ensure(scan_tmp_ints(nnz) + 16, stream_);
+    if (nf) {
+        check(cudaMemcpyAsync(dOwner_.p, owner, sizeof(int) * nf, cudaMemcpyHostToDevice, stream_), "H2D owner");
+        check(cudaMemcpyAsync(dNeigh_.p, neigh, sizeof(int) * nf, cudaMemcpyHostToDevice, stream_), "H2D neigh");
+    }
+    // K1: row counts -> offsets -> unordered fill -> per-row sort by column
+    cudaMemsetAsync(ro_.p, 0, sizeof(int) * (nc + 1), stream_);
+    plan_count(nc, nf, dOwner_, dNeigh_, ro_.p, stream_);
+    exclusive_scan(ro_.p, nc + 1, push_.p, scanTmp_.p, stream_);
+    cudaMemsetAsync(fill_.p, 0, sizeof(int) * (nc + 1), stream_);
+    plan_fill(nc, nf, dOwner_, dNeigh_, ro_, fill_.p, ci_.p, src_.p, stream_);
+    plan_sort_rows(nc, ro_, ci_.p, src_.p, stream_);
+    find_diag(nc, ro_, ci_, dg_.p, stream_);
+    cudaMemsetAsync(err_.p, 0, sizeof(int), stream_);
+    transpose_pos(nc, ro_, ci_, tpos_.p, err_.p, stream_);
+    vals_.ensure(nnz * n * n, stream_);
+    checkErr("setTopology");
+    if (readErrCell()) throw std::runtime_error("bcs: structurally asymmetric block pattern");
+    hasTopo_ = true;
+    hasValues_ = false;
+}
+
+void Engine::uploadLdu(const double* diag, const double* upper, const double* lower, bool device_ptrs) {
+    LaunchScope ls(&launches_);
+    if (!hasTopo_) throw std::invalid_argument("bcs: set the topology before uploading values");
+    const size_t nn = static_cast<size_t>(n_) * n_;
+    const double *dd = diag, *du = upper, *dl = lower;
+    if (!device_ptrs) {
+        ldu_diag_.ensure(nc_ * nn, stream_);
+        ldu_upper_.ensure(nf_ * nn, stream_);
+        ldu_lower_.ensure(nf_ * nn, stream_);
+        check(cudaMemcpyAsync(ldu_diag_.p, diag, sizeof(double) * nc_ * nn, cudaMemcpyHostToDevice, stream_), "H2D diag");
+        if (nf_) {
+            check(cudaMemcpyAsync(ldu_upper_.p, upper, sizeof(double) * nf_ * nn, cudaMemcpyHostToDevice, stream_),
+                  "H2D upper");
+            check(cudaMemcpyAsync(ldu_lower_.p, lower, sizeof(double) * nf_ * nn, cudaMemcpyHostToDevice, stream_),
+                  "H2D lower");
+        }
+        dd = ldu_diag_;
+        du = ldu_upper_;
+        dl = ldu_lower_;
+    }
+    // K2: replaceValues permutation
+    gather_values(n_, nc_ + 2 * nf_, nc_, nf_, src_, dd, du, dl, vals_.p, stream_);
+    checkErr("uploadLdu");
+    hasValues_ = true;
+    pcKind_ = -1;  // any preconditioner built on old values is stale
+}
+
+void Engine::requireMatrix() const {
+    if (!hasTopo_ || !hasValues_) throw std::invalid_argument("bcs: no matrix uploaded");
+}
+
+void Engine::spmvLevel(const Level& L, const double* x, const double* sub, double* y) {
+    const bool timed = kernelTiming_ && &L == &levels_[0];
+    if (timed) cudaEventRecord(ev0_, stream_);
+    spmv(n_, L.rows, L.ro, L.ci, L.v, x, sub, y, stream_);
+    if (timed) {
+        cudaEventRecord(ev1_, stream_);
+        cudaEventSynchronize(ev1_);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev0_, ev1_);
+        spmvMs_ += ms;
+        ++spmvCount_;
+    }
+}
+
+// ------------------------------------------------------------ config/setup
+void Engine::validateConfig(const bcs_solver_config& c) const {
+    // SolverConfig::validate (krylov.cpp:10-18)
+    if (!(c.rel_tol > 0.0) || !(c.abs_tol > 0.0)) throw std::invalid_argument("SolverConfig: tolerances must be positive");
+    if (c.max_iters < 1) throw std::invalid_argument("SolverConfig: maxIters must be >= 1");
+    if (c.gmres_restart < 1) throw std::invalid_argument("SolverConfig: gmresRestart must be >= 1");
+    if (c.amg_max_levels < 1) throw std::invalid_argument("SolverConfig: amg.maxLevels must be >= 1");
+    if (c.amg_pre_sweeps < 0 || c.amg_post_sweeps < 0) throw std::invalid_argument("SolverConfig: amg sweeps must be >= 0");
+    if (c.method != BCS_GMRES && c.method != BCS_BICGSTAB) throw std::invalid_argument("unknown Krylov method");
+    if (c.precond < 0 || c.precond > 3) throw std::invalid_argument("unknown preconditioner kind");
+}
+
+void Engine::setupLevelPattern(Level& L) {
+    L.o_dg.ensure(L.rows, stream_);
+    L.o_tpos.ensure(L.nnz, stream_);
+    find_diag(L.rows, L.ro, L.ci, L.o_dg.p, stream_);
+    cudaMemsetAsync(err_.p, 0, sizeof(int), stream_);
+    transpose_pos(L.rows, L.ro, L.ci, L.o_tpos.p, err_.p, stream_);
+    L.dg = L.o_dg;
+    L.tpos = L.o_tpos;
+    if (readErrCell()) throw std::runtime_error("bcs: structurally asymmetric coarse pattern");
+}
+
+static KahnWork kahnWork(DArray<int>& cnt, DArray<int>& push, DArray<int>& lvl) {
+    return KahnWork{cnt.p, push.p, lvl.p};
+}
+
+void Engine::diluSetup(Level& L) {
+    const size_t nn = static_cast<size_t>(n_) * n_;
+    L.lu.ensure(L.rows * nn, stream_);
+    L.piv.ensure(static_cast<size_t>(L.rows) * n_, stream_);
+    L.order.ensure(L.rows, stream_);
+    cnt_.ensure(L.rows, stream_);
+    lvl_.ensure(static_cast<size_t>(L.rows) + 1, stream_);
+    const int big = std::numeric_limits<int>::max();
+    check(cudaMemcpyAsync(err_.p, &big, sizeof(int), cudaMemcpyHostToDevice, stream_), "err init");
+    L.depth = kahn_schedule(n_, L.rows, L.ro, L.ci, L.dg, L.tpos, L.v, true, L.lu.p, L.piv.p, L.order.p,
+                            kahnWork(cnt_, push_, lvl_), err_.p, stream_);
+    const int cell = readErrCell();
+    if (cell != big) throw std::runtime_error("DILU setup: singular modified diagonal in cell " + std::to_string(cell));
+}
+
+void Engine::lusgsSetup(Level& L) {
+    const size_t nn = static_cast<size_t>(n_) * n_;
+    L.lu.ensure(L.rows * nn, stream_);
+    L.piv.ensure(static_cast<size_t>(L.rows) * n_, stream_);
+    L.order.ensure(L.rows, stream_);
+    cnt_.ensure(L.rows, stream_);
+    lvl_.ensure(static_cast<size_t>(L.rows) + 1, stream_);
+    const int big = std::numeric_limits<int>::max();
+    check(cudaMemcpyAsync(err_.p, &big, sizeof(int), cudaMemcpyHostToDevice, stream_), "err init");
+    factor_diag_blocks(n_, L.rows, L.dg, L.v, L.lu.p, L.piv.p, err_.p, stream_);
+    const int cell = readErrCell();
+    if (cell != big)
+        throw std::runtime_error("preconditioner setup: singular diagonal block in cell " + std::to_string(cell));
+    L.depth = kahn_schedule(n_, L.rows, L.ro, L.ci, L.dg, L.tpos, L.v, false, nullptr, nullptr, L.order.p,
+                            kahnWork(cnt_, push_, lvl_), err_.p, stream_);
+}
+
+void Engine::buildHierarchy(const bcs_solver_config& cfg) {
+    const size_t nn = static_cast<size_t>(n_) * n_;
+    nlev_ = 1;
+    // coarsening loop (amg.cpp:75-84)
+    while (nlev_ < cfg.amg_max_levels && levels_[nlev_ - 1].rows > cfg.amg_min_coarse_rows) {
+        const int l = nlev_ - 1;
+        {
+            Level& L = levels_[l];
+            dn_.ensure(L.rows, stream_);
+            str_.ensure(L.nnz, stream_);
+            strengths(n_, L.rows, L.ro, L.ci, L.dg, L.v, dn_.p, str_.p, stream_);
+            choice_.ensure(L.rows, stream_);
+            cnt_.ensure(L.rows, stream_);
+            lvl_.ensure(static_cast<size_t>(L.rows) + 1, stream_);
+            aggregate_kahn(L.rows, L.ro, L.ci, L.dg, L.tpos, str_, choice_.p, kahnWork(cnt_, push_, lvl_), err_.p,
+                           stream_);
+            L.agg.ensure(L.rows, stream_);
+            L.members.ensure(2 * static_cast<size_t>(L.rows), stream_);
+            flag_.ensure(L.rows, stream_);
+            scanTmp_.ensure(scan_tmp_ints(static_cast<size_t>(L.nnz) * 2 + L.rows) + 16, stream_);
+            const int nC = aggregate_number(L.rows, choice_, flag_.p, L.agg.p, L.members.p, push_.p + 6,
+                                            scanTmp_.p, stream_);
+            if (nC == L.rows) break;  // no coarsening possible (amg.cpp:80)
+            L.ncoarse = nC;
+        }
+        if (static_cast<int>(levels_.size()) < nlev_ + 1) levels_.emplace_back();
+        ++nlev_;
+        Level& L = levels_[l];
+        Level& C = levels_[l + 1];
+        const int nC = L.ncoarse;
+        // Galerkin (amg.cpp:39-71): segmented keys, per-segment rank sort, runs -> slots
+        segOff_.ensure(static_cast<size_t>(nC) + 1, stream_);
+        galerkin_seg_len(nC, L.ro, L.members, segOff_.p, stream_);
+        cudaMemsetAsync(segOff_.p + nC, 0, sizeof(int), stream_);
+        exclusive_scan(segOff_.p, nC + 1, push_.p + 6, scanTmp_.p, stream_);
+        int total = 0;
+        check(cudaMemcpyAsync(&total, push_.p + 6, sizeof(int), cudaMemcpyDeviceToHost, stream_), "seg total");
+        sync();
+        keys_.ensure(total, stream_);
+        sorted_.ensure(total, stream_);
+        galerkin_keys(nC, L.ro, L.ci, L.agg, L.members, segOff_, keys_.p, stream_);
+        big_.ensure(static_cast<size_t>(nC) + 1, stream_);
+        cudaMemsetAsync(err_.p, 0, sizeof(int), stream_);
+        galerkin_sort(nC, segOff_, keys_, sorted_.p, big_.p, push_.p + 7, err_.p, stream_);
+        if (readErrCell()) throw std::runtime_error("bcs: Galerkin coarse row exceeds the 12288-entry sort limit");
+        C.o_ro.ensure(static_cast<size_t>(nC) + 1, stream_);
+        galerkin_count(nC, segOff_, sorted_, C.o_ro.p, stream_);
+        cudaMemsetAsync(C.o_ro.p + nC, 0, sizeof(int), stream_);
+        exclusive_scan(C.o_ro.p, nC + 1, push_.p + 6, scanTmp_.p, stream_);
+        int cnnz = 0;
+        check(cudaMemcpyAsync(&cnnz, push_.p + 6, sizeof(int), cudaMemcpyDeviceToHost, stream_), "coarse nnz");
+        sync();
+        C.rows = nC;
+        C.nnz = cnnz;
+        C.o_ci.ensure(cnnz, stream_);
+        C.o_v.ensure(static_cast<size_t>(cnnz) * nn, stream_);
+        galerkin_fill(n_, nC, L.ro, L.members, segOff_, sorted_, L.v, C.o_ro, C.o_ci.p, C.o_v.p, stream_);
+        C.ro = C.o_ro;
+        C.ci = C.o_ci;
+        C.v = C.o_v;
+        setupLevelPattern(C);
+    }
+    levels_[nlev_ - 1].ncoarse = 0;
+    // DILU smoother on all but the coarsest level (amg.cpp:86-88)
+    for (int l = 0; l + 1 < nlev_; ++l) diluSetup(levels_[l]);
+    // dense factorisation of the coarsest level (amg.cpp:90-104)
+    const Level& Cl = levels_[nlev_ - 1];
+    m_ = Cl.rows * n_;
+    dense_.ensure(static_cast<size_t>(m_) * m_, stream_);
+    dpiv_.ensure(m_, stream_);
+    dense_build(n_, Cl.rows, Cl.ro, Cl.ci, Cl.v, dense_.p, stream_);
+    cudaMemsetAsync(err_.p, 0, sizeof(int), stream_);
+    dense_factor(m_, dense_.p, dpiv_.p, err_.p, stream_);
+    if (readErrCell()) throw std::runtime_error("singular coarse-level matrix");
+    // V-cycle vectors
+    for (int l = 0; l < nlev_; ++l) {
+        Level& L = levels_[l];
+        const size_t N = static_cast<size_t>(L.rows) * n_;
+        if (l > 0) {
+            L.r.ensure(N, stream_);
+            L.z.ensure(N, stream_);
+        }
+        if (l + 1 < nlev_) {
+            L.res.ensure(N, stream_);
+            L.y.ensure(N, stream_);
+            L.zb.ensure(N, stream_);
+        }
+    }
+}
+
+// makeCsrPreconditioner (engine.cpp:21-29)
+void Engine::buildPrecond(const bcs_solver_config& cfg) {
+    requireMatrix();
+    pcKind_ = -1;
+    if (levels_.empty()) levels_.emplace_back();
+    nlev_ = 1;
+    Level& L0 = levels_[0];
+    L0.rows = nc_;
+    L0.nnz = nc_ + 2 * nf_;
+    L0.ro = ro_;
+    L0.ci = ci_;
+    L0.dg = dg_;
+    L0.tpos = tpos_;
+    L0.v = vals_;
+    const size_t N = static_cast<size_t>(nc_) * n_;
+    switch (cfg.precond) {
+        case BCS_PRECOND_NONE: break;
+        case BCS_PRECOND_LUSGS:
+            lusgsSetup(L0);
+            L0.y.ensure(N, stream_);
+            break;
+        case BCS_PRECOND_DILU:
+            diluSetup(L0);
+            L0.y.ensure(N, stream_);
+            break;
+        case BCS_PRECOND_AMG: buildHierarchy(cfg); break;
+        default: throw std::invalid_argument("unknown preconditioner kind");
+    }
+    checkErr("buildPrecond");
+    pcKind_ = cfg.precond;
+    pcCfg_ = cfg;
+}
+
+// DILU/LUSGS sweep pair: z = (D+U)^{-1} D (D+L)^{-1} r  (accumulate: see sweep_backward)
+void Engine::smootherApply(Level& L, const double* r, double* z, int accumulate) {
+    const size_t N = static_cast<size_t>(L.rows) * n_;
+    double* zb = accumulate ? L.zb.p : z;
+    cudaMemsetAsync(L.y.p, 0xFF, N * sizeof(double), stream_);
+    cudaMemsetAsync(zb, 0xFF, N * sizeof(double), stream_);
+    sweep_forward(n_, L.rows, L.order, L.ro, L.ci, L.dg, L.v, L.lu, L.piv, r, L.y.p, ctr_.p, err_.p + 1, stream_);
+    sweep_backward(n_, L.rows, L.order, L.ro, L.ci, L.dg, L.v, L.lu, L.piv, L.y, zb, z, accumulate, ctr_.p,
+                   err_.p + 1, stream_);
+}
+
+// AmgHierarchy::vcycle (amg.cpp:111-158)
+void Engine::vcycle(int l, const double* r, double* z) {
+    Level& L = levels_[l];
+    const size_t N = static_cast<size_t>(L.rows) * n_;
+    if (l == nlev_ - 1) {
+        dense_solve(m_, dense_, dpiv_, r, z, stream_);
+        return;
+    }
+    const int pre = pcCfg_.amg_pre_sweeps, post = pcCfg_.amg_post_sweeps;
+    for (int s = 0; s < pre; ++s) {
+        const double* rin = r;  // z == 0 on the first sweep: r - A*0 == r exactly
+        if (s > 0) {
+            spmvLevel(L, z, r, L.res.p);
+            rin = L.res;
+        }
+        smootherApply(L, rin, z, s == 0 ? 1 : 2);
+    }
+    const double* res = r;
+    if (pre > 0) {
+        spmvLevel(L, z, r, L.res.p);
+        res = L.res;
+    } else {
+        cudaMemsetAsync(z, 0, N * sizeof(double), stream_);
+    }
+    Level& C = levels_[l + 1];
+    restrict_vec(n_, L.ncoarse, L.members, res, C.r.p, stream_);
+    vcycle(l + 1, C.r, C.z.p);
+    prolong_vec(n_, L.rows, L.agg, C.z, z, stream_);
+    for (int s = 0; s < post; ++s) {
+        spmvLevel(L, z, r, L.res.p);
+        smootherApply(L, L.res, z, 2);
+    }
+}
+
+void Engine::applyPrecond(const double* r, double* z) {
+    const size_t N = static_cast<size_t>(nc_) * n_;
+    switch (pcKind_) {
+        case BCS_PRECOND_NONE: copy_vec(r, z, N, stream_); break;
+        case BCS_PRECOND_LUSGS:
+        case BCS_PRECOND_DILU: smootherApply(levels_[0], r, z, 0); break;
+        case BCS_PRECOND_AMG: vcycle(0, r, z); break;
+        default: throw std::logic_error("preconditioner not built");
+    }
+}
+
+// ------------------------------------------------------------------ Krylov
+double Engine::dotHost(const double* a, const double* b, size_t N, bool sqrt_out) {
+    dot(a, b, N, scal_.p + 2, sqrt_out, partials_.p, ticket_.p, stream_);
+    check(cudaMemcpyAsync(hStatus_ + 2, scal_.p + 2, sizeof(double), cudaMemcpyDeviceToHost, stream_), "D2H scalar");
+    sync();
+    return hStatus_[2];
+}
+
+// gmresSolve (krylov.cpp:59-150)
+void Engine::gmres(const double* b, double* x, const bcs_solver_config& cfg, bcs_report& rep) {
+    const size_t N = static_cast<size_t>(nc_) * n_;
+    const int m = cfg.gmres_restart;
+    rk_.ensure(N, stream_);
+    w_.ensure(N, stream_);
+    zk_.ensure(N, stream_);
+    spmvLevel(levels_[0], x, b, rk_.p);
+    double beta = dotHost(rk_, rk_, N, true);
+    rep.initial_residual = beta;
+    const double beta0 = beta;
+    const double tol = std::max(cfg.rel_tol * beta, cfg.abs_tol);
+    if (beta <= tol) {
+        rep.final_residual = beta;
+        rep.converged = 1;
+        return;
+    }
+    V_.ensure(static_cast<size_t>(m + 1) * N, stream_);
+    H_.ensure(static_cast<size_t>(m + 1) * m, stream_);
+    cs_.ensure(m, stream_);
+    sn_.ensure(m, stream_);
+    g_.ensure(static_cast<size_t>(m) + 1, stream_);
+    y_.ensure(m, stream_);
+    double* beta_d = scal_.p + 2;  // holds ||r|| from dotHost
+    int total = 0;
+    while (total < cfg.max_iters) {
+        scale_by(rk_, beta_d, -1.0, V_.p, N, stream_);
+        cudaMemsetAsync(g_.p, 0, sizeof(double) * (m + 1), stream_);
+        cudaMemsetAsync(H_.p, 0, sizeof(double) * (m + 1) * m, stream_);
+        cudaMemcpyAsync(g_.p, beta_d, sizeof(double), cudaMemcpyDeviceToDevice, stream_);
+        int j = 0;
+        bool happy = false;
+        for (; j < m && total < cfg.max_iters; ++j, ++total) {
+            double* vj = V_.p + static_cast<size_t>(j) * N;
+            applyPrecond(vj, zk_.p);
+            spmvLevel(levels_[0], zk_, nullptr, w_.p);
+            dot(w_, V_.p, N, H_.p + j, false, partials_.p, ticket_.p, stream_);
+            for (int i = 0; i < j; ++i)
+                axpy_dot(w_.p, H_.p + static_cast<size_t>(i) * m + j, V_.p + static_cast<size_t>(i) * N,
+                         V_.p + static_cast<size_t>(i + 1) * N, N, H_.p + static_cast<size_t>(i + 1) * m + j,
+                         partials_.p, ticket_.p, stream_);
+            axpy_dot(w_.p, H_.p + static_cast<size_t>(j) * m + j, vj, nullptr, N,
+                     H_.p + static_cast<size_t>(j + 1) * m + j, partials_.p, ticket_.p, stream_);
+            scale_by(w_, H_.p + static_cast<size_t>(j + 1) * m + j, 1e-290, V_.p + static_cast<size_t>(j + 1) * N, N,
+                     stream_);
+            givens_step(H_.p, m, j, cs_.p, sn_.p, g_.p, scal_.p + 4, stream_);
+            check(cudaMemcpyAsync(hStatus_ + 4, scal_.p + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream_),
+                  "D2H status");
+            sync();
+            const double gabs = hStatus_[4];
+            happy = hStatus_[5] != 0.0;
+            hist_.push_back(gabs / beta0);
+            if (gabs <= tol || happy) {
+                ++j;
+                ++total;
+                break;
+            }
+        }
+        // back substitution, x += M^{-1}(V y)
+        back_subst(H_, m, j, g_, y_.p, stream_);
+        lincomb(V_, N, y_, j, w_.p, N, stream_);
+        applyPrecond(w_, zk_.p);
+        add_to(x, zk_, N, stream_);
+        spmvLevel(levels_[0], x, b, rk_.p);
+        beta = dotHost(rk_, rk_, N, true);
+        if (!hist_.empty()) hist_.back() = beta / beta0;
+        rep.iterations = total;
+        rep.final_residual = beta;
+        if (beta <= tol) {
+            rep.converged = 1;
+            return;
+        }
+        if (happy && beta <= tol * 1.0000001) {
+            rep.converged = 1;
+            return;
+        }
+    }
+    rep.iterations = total;
+    rep.converged = rep.final_residual <= tol;
+}
+
+// bicgstabSolve (krylov.cpp:152-214)
+void Engine::bicgstab(const double* b, double* x, const bcs_solver_config& cfg, bcs_report& rep) {
+    const size_t N = static_cast<size_t>(nc_) * n_;
+    rk_.ensure(N, stream_);
+    brh_.ensure(N, stream_);
+    bp_.ensure(N, stream_);
+    bv_.ensure(N, stream_);
+    bs_.ensure(N, stream_);
+    bt_.ensure(N, stream_);
+    bph_.ensure(N, stream_);
+    bsh_.ensure(N, stream_);
+    spmvLevel(levels_[0], x, b, rk_.p);
+    const double beta0 = dotHost(rk_, rk_, N, true);
+    rep.initial_residual = beta0;
+    const double tol = std::max(cfg.rel_tol * beta0, cfg.abs_tol);
+    if (beta0 <= tol) {
+        rep.final_residual = beta0;
+        rep.converged = 1;
+        return;
+    }
+    copy_vec(rk_, brh_.p, N, stream_);
+    double rhoPrev = 1.0, alpha = 1.0, omega = 1.0;
+    for (int it = 0; it < cfg.max_iters; ++it) {
+        const double rho = dotHost(brh_, rk_, N, false);
+        if (std::fabs(rho) < 1e-30) {
+            rep.breakdown = 1;
+            break;
+        }
+        if (it == 0) copy_vec(rk_, bp_.p, N, stream_);
+        else bicg_p(bp_.p, rk_, bv_, (rho / rhoPrev) * (alpha / omega), omega, N, stream_);
+        applyPrecond(bp_, bph_.p);
+        spmvLevel(levels_[0], bph_, nullptr, bv_.p);
+        const double rhatv = dotHost(brh_, bv_, N, false);
+        if (std::fabs(rhatv) < 1e-300) {
+            rep.breakdown = 1;
+            break;
+        }
+        alpha = rho / rhatv;
+        bicg_s(bs_.p, rk_, bv_, alpha, N, stream_);
+        const double ns = dotHost(bs_, bs_, N, true);
+        if (ns <= tol) {
+            bicg_x_half(x, bph_, alpha, N, stream_);
+            rep.iterations = it + 1;
+            hist_.push_back(ns / beta0);
+            break;
+        }
+        applyPrecond(bs_, bsh_.p);
+        spmvLevel(levels_[0], bsh_, nullptr, bt_.p);
+        const double tt = dotHost(bt_, bt_, N, false);
+        omega = tt > 0.0 ? dotHost(bt_, bs_, N, false) / tt : 0.0;
+        bicg_x_r(x, rk_.p, bph_, bsh_, bs_, bt_, alpha, omega, N, stream_);
+        rep.iterations = it + 1;
+        if (std::fabs(omega) < 1e-30) {
+            rep.breakdown = 1;
+            break;
+        }
+        rhoPrev = rho;
+        const double nr = dotHost(rk_, rk_, N, true);
+        hist_.push_back(nr / beta0);
+        if (nr <= tol) break;
+    }
+    spmvLevel(levels_[0], x, b, rk_.p);
+    rep.final_residual = dotHost(rk_, rk_, N, true);
+    rep.converged = rep.final_residual <= tol;
+    if (rep.converged) rep.breakdown = 0;
+    if (rep.breakdown)
+        throw std::runtime_error("BiCGStab breakdown at iteration " + std::to_string(rep.iterations) + ", residual " +
+                                 std::to_string(rep.final_residual));
+}
+
+void Engine::solveDevice(const double* d_b, double* d_x, const bcs_solver_config& cfg, bcs_report& rep) {
+    LaunchScope ls(&launches_);
+    requireMatrix();
+    validateConfig(cfg);
+    const long long l0 = launches_.launches;
+    spmvMs_ = 0.0;
+    spmvCount_ = 0;
+    hist_.clear();
+    cudaMemsetAsync(err_.p + 1, 0, sizeof(int), stream_);
+    const auto t0 = clk::now();
+    buildPrecond(cfg);
+    sync();
+    const auto t1 = clk::now();
+    if (cfg.method == BCS_GMRES) gmres(d_b, d_x, cfg, rep);
+    else bicgstab(d_b, d_x, cfg, rep);
+    sync();
+    const auto t2 = clk::now();
+    int spinErr = 0;
+    check(cudaMemcpy(&spinErr, err_.p + 1, sizeof(int), cudaMemcpyDeviceToHost), "spin flag");
+    if (spinErr) throw std::runtime_error("bcs: sweep dependency wait timed out (corrupt schedule)");
+    checkErr("solve");
+    rep.t_amg_setup = secs(t0, t1);
+    rep.t_krylov = secs(t1, t2);
+    rep.amg_levels = pcKind_ == BCS_PRECOND_AMG ? nlev_ : 0;
+    rep.coarse_rows = pcKind_ == BCS_PRECOND_AMG ? levels_[nlev_ - 1].rows : 0;
+    rep.spmv_launches = spmvCount_;
+    rep.spmv_ms = spmvMs_;
+    rep.kernel_launches = static_cast<int>(launches_.launches - l0);
+}
+
+void Engine::solveHost(const double* b, double* x, const bcs_solver_config& cfg, bcs_report& rep) {
+    requireMatrix();
+    const size_t N = static_cast<size_t>(nc_) * n_;
+    kb_.ensure(N, stream_);
+    kx_.ensure(N, stream_);
+    check(cudaMemcpyAsync(kb_.p, b, N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D b");
+    check(cudaMemcpyAsync(kx_.p, x, N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D x");
+    solveDevice(kb_, kx_, cfg, rep);
+    check(cudaMemcpyAsync(x, kx_.p, N * sizeof(double), cudaMemcpyDeviceToHost, stream_), "D2H x");
+    sync();
+}
+
+// SolvePipeline::solve (engine.cpp:47-120)
+void Engine::pipelineSolve(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh, const double* diag,
+                           const double* upper, const double* lower, const double* b, size_t b_len,
+                           const double* x0, size_t x0_len, double* x, int backend, const bcs_solver_config& cfg,
+                           bcs_report& rep) {
+    const size_t N = static_cast<size_t>(nc) * n;
+    if (b_len != N || x0_len != N) throw std::invalid_argument("SolvePipeline::solve: dimension mismatch");
+    if (backend != BCS_BACKEND_HOST_LDU && backend != BCS_BACKEND_ENGINE_CSR)
+        throw std::invalid_argument("unknown backend");
+    const bool sameTopo = hasTopo_ && nc == nc_ && nf == nf_ && n == n_ &&
+                          std::equal(owner, owner + nf, hOwner_.begin()) && std::equal(neigh, neigh + nf, hNeigh_.begin());
+    if (backend == BCS_BACKEND_HOST_LDU) {
+        if (cfg.precond != BCS_PRECOND_NONE && cfg.precond != BCS_PRECOND_LUSGS)
+            throw std::invalid_argument("host backend supports only none/LUSGS preconditioning");
+        const auto t0 = clk::now();
+        if (!sameTopo) setTopology(nc, nf, n, owner, neigh);
+        uploadLdu(diag, upper, lower, false);
+        std::memcpy(x, x0, N * sizeof(double));
+        solveHost(b, x, cfg, rep);
+        rep.t_solve = secs(t0, clk::now());
+        rep.t_convert = rep.t_setup = rep.t_retrieve = rep.t_replace = 0.0;
+        rep.setup_branch = 0;
+        return;
+    }
+    const size_t nn = static_cast<size_t>(n) * n;
+    (void)nn;
+    // "convert": stage b and x0 on the device
+    auto t = clk::now();
+    kb_.ensure(N, stream_);
+    kx_.ensure(N, stream_);
+    check(cudaMemcpyAsync(kb_.p, b, N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D b");
+    check(cudaMemcpyAsync(kx_.p, x0, N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D x0");
+    sync();
+    rep.t_convert = secs(t, clk::now());
+    // setup-or-replace by topology signature (engine.cpp:85-98)
+    bool takeSetup = !pipeHasSetup_;
+    if (!takeSetup && !sameTopo) {
+        if (!pipeSigValid_ && hasTopo_) {
+            pipeSig_ = topologySignatureHost(nc_, nf_, hOwner_.data(), hNeigh_.data());
+            pipeSigValid_ = true;
+        }
+        const uint64_t sig = topologySignatureHost(nc, nf, owner, neigh);
+        takeSetup = sig != pipeSig_;
+    }
+    t = clk::now();
+    if (takeSetup || !sameTopo) setTopology(nc, nf, n, owner, neigh);
+    uploadLdu(diag, upper, lower, false);
+    sync();
+    const double tsr = secs(t, clk::now());
+    if (takeSetup) {
+        rep.t_setup = tsr;
+        rep.t_replace = 0.0;
+        rep.setup_branch = 1;
+        pipeSigValid_ = false;  // computed lazily on the next topology change
+        pipeHasSetup_ = true;
+    } else {
+        rep.t_replace = tsr;
+        rep.t_setup = 0.0;
+        rep.setup_branch = 0;
+    }
+    // "solve": preconditioner + Krylov
+    t = clk::now();
+    solveDevice(kb_, kx_, cfg, rep);
+    rep.t_solve = secs(t, clk::now());
+    // "retrieve"
+    t = clk::now();
+    check(cudaMemcpyAsync(x, kx_.p, N * sizeof(double), cudaMemcpyDeviceToHost, stream_), "D2H x");
+    sync();
+    rep.t_retrieve = secs(t, clk::now());
+}
+
+// ------------------------------------------------------------ query paths
+double Engine::residualNorm(const double* b, const double* x) {
+    LaunchScope ls(&launches_);
+    requireMatrix();
+    const size_t N = static_cast<size_t>(nc_) * n_;
+    kb_.ensure(N, stream_);
+    kx_.ensure(N, stream_);
+    rk_.ensure(N, stream_);
+    check(cudaMemcpyAsync(kb_.p, b, N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D b");
+    check(cudaMemcpyAsync(kx_.p, x, N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D x");
+    spmv(n_, nc_, ro_, ci_, vals_, kx_, kb_, rk_.p, stream_);
+    return dotHost(rk_, rk_, N, true);
+}
+
+void Engine::spmvDevice(const double* d_x, double* d_y) {
+    LaunchScope ls(&launches_);
+    requireMatrix();
+    spmv(n_, nc_, ro_, ci_, vals_, d_x, nullptr, d_y, stream_);
+    checkErr("spmv");
+}
+
+void Engine::spmvHost(const double* x, double* y) {
+    const size_t N = static_cast<size_t>(nc_) * n_;
+    requireMatrix();
+    kb_.ensure(N, stream_);
+    kx_.ensure(N, stream_);
+    check(cudaMemcpyAsync(kx_.p, x, N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D x");
+    spmvDevice(kx_, kb_.p);
+    check(cudaMemcpyAsync(y, kb_.p, N * sizeof(double), cudaMemcpyDeviceToHost, stream_), "D2H y");
+    sync();
+}
+
+void Engine::csrGet(int32_t* ro, int32_t* ci, double* v) {
+    requireMatrix();
+    const size_t nnz = static_cast<size_t>(nc_) + 2 * static_cast<size_t>(nf_);
+    if (ro) check(cudaMemcpyAsync(ro, ro_.p, sizeof(int) * (nc_ + 1), cudaMemcpyDeviceToHost, stream_), "D2H ro");
+    if (ci) check(cudaMemcpyAsync(ci, ci_.p, sizeof(int) * nnz, cudaMemcpyDeviceToHost, stream_), "D2H ci");
+    if (v) check(cudaMemcpyAsync(v, vals_.p, sizeof(double) * nnz * n_ * n_, cudaMemcpyDeviceToHost, stream_), "D2H v");
+    sync();
+}
+
+void Engine::precondSetup(const bcs_solver_config& cfg) {
+    LaunchScope ls(&launches_);
+    validateConfig(cfg);
+    buildPrecond(cfg);
+    sync();
+}
+
+void Engine::precondApplyHost(const double* r, double* z) {
+    LaunchScope ls(&launches_);
+    if (pcKind_ < 0) throw std::invalid_argument("bcs: call bcs_precond_setup first");
+    const size_t N = static_cast<size_t>(nc_) * n_;
+    kb_.ensure(N, stream_);
+    kx_.ensure(N, stream_);
+    cudaMemsetAsync(err_.p + 1, 0, sizeof(int), stream_);
+    check(cudaMemcpyAsync(kb_.p, r, N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D r");
+    applyPrecond(kb_, kx_.p);
+    check(cudaMemcpyAsync(z, kx_.p, N * sizeof(double), cudaMemcpyDeviceToHost, stream_), "D2H z");
+    sync();
+    checkErr("precond apply");
+    int spinErr = 0;
+    check(cudaMemcpy(&spinErr, err_.p + 1, sizeof(int), cudaMemcpyDeviceToHost), "spin flag");
+    if (spinErr) throw std::runtime_error("bcs: sweep dependency wait timed out (corrupt schedule)");
+}
+
+void Engine::amgLevelSizes(int l, int* rows, int* nnz) const {
+    if (l < 0 || l >= nlev_) throw std::invalid_argument("bcs: level out of range");
+    *rows = levels_[l].rows;
+    *nnz = levels_[l].nnz;
+}
+
+void Engine::amgLevelGet(int l, int32_t* ro, int32_t* ci, double* v, int32_t* agg) {
+    if (l < 0 || l >= nlev_) throw std::invalid_argument("bcs: level out of range");
+    const Level& L = levels_[l];
+    const size_t nn = static_cast<size_t>(n_) * n_;
+    if (ro) check(cudaMemcpyAsync(ro, L.ro, sizeof(int) * (L.rows + 1), cudaMemcpyDeviceToHost, stream_), "D2H");
+    if (ci) check(cudaMemcpyAsync(ci, L.ci, sizeof(int) * L.nnz, cudaMemcpyDeviceToHost, stream_), "D2H");
+    if (v) check(cudaMemcpyAsync(v, L.v, sizeof(double) * L.nnz * nn, cudaMemcpyDeviceToHost, stream_), "D2H");
+    if (agg && l + 1 < nlev_)
+        check(cudaMemcpyAsync(agg, L.agg.p, sizeof(int) * L.rows, cudaMemcpyDeviceToHost, stream_), "D2H");
+    sync();
+}
+
+int Engine::scheduleDepth(int l) const {
+    if (l < 0 || l >= nlev_) throw std::invalid_argument("bcs: level out of range");
+    return levels_[l].depth;
+}
+
+}  // namespace bcs

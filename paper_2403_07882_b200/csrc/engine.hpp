@@ -1,0 +1,169 @@
+// bcs::Engine — the device-side state behind one bcs_ctx: the BSR plan of
+// the current topology, the AMG hierarchy / smoother factors rebuilt on every
+// solve (engine.cpp:100-107 semantics), and the Krylov workspace.
+#pragma once
+
+#include "../../include/bcs.h"
+#include "kernels.hpp"
+
+#include <chrono>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace bcs {
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void check(cudaError_t e, const char* what);
+
+// Stream-ordered device array (cudaMallocAsync from the device pool, whose
+// release threshold is raised so that steady-state solves never return memory
+// to the driver).  Grows by capacity; contents are not preserved on growth.
+template <class T>
+struct DArray {
+    T* p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t n, cudaStream_t s) {
+        if (n <= cap && p) return;
+        if (p) check(cudaFreeAsync(p, s), "cudaFreeAsync");
+        p = nullptr;
+        cap = 0;
+        const size_t bytes = (n ? n : 1) * sizeof(T);
+        check(cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, s), "cudaMallocAsync");
+        cap = n ? n : 1;
+    }
+    void release(cudaStream_t s) {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        cap = 0;
+    }
+    operator T*() const { return p; }
+};
+
+struct Level {
+    int rows = 0, nnz = 0;
+    // pattern/values: level 0 aliases the engine's plan arrays
+    const int* ro = nullptr;
+    const int* ci = nullptr;
+    const int* dg = nullptr;
+    const int* tpos = nullptr;
+    const double* v = nullptr;
+    DArray<int> o_ro, o_ci, o_dg, o_tpos;
+    DArray<double> o_v;
+    // smoother (DILU or LUSGS) factors + level-sorted schedule
+    DArray<double> lu;
+    DArray<int> piv, order;
+    int depth = 0;
+    // aggregation to level+1
+    DArray<int> agg, members;
+    int ncoarse = 0;
+    // V-cycle vectors
+    DArray<double> r, z, res, y, zb;
+};
+
+class Engine {
+public:
+    explicit Engine(int device);
+    ~Engine();
+
+    void setStream(cudaStream_t s);
+    void setKernelTiming(bool on) { kernelTiming_ = on; }
+
+    // topology / values
+    void setTopology(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh);
+    void uploadLdu(const double* diag, const double* upper, const double* lower, bool device_ptrs);
+
+    // drop-in pipeline (engine.cpp:47-120)
+    void pipelineSolve(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh, const double* diag,
+                       const double* upper, const double* lower, const double* b, size_t b_len, const double* x0,
+                       size_t x0_len, double* x, int backend, const bcs_solver_config& cfg, bcs_report& rep);
+
+    // staged
+    void solveDevice(const double* d_b, double* d_x, const bcs_solver_config& cfg, bcs_report& rep);
+    void solveHost(const double* b, double* x, const bcs_solver_config& cfg, bcs_report& rep);
+
+    // queries / kernels
+    double residualNorm(const double* b, const double* x);  // host arrays
+    const std::vector<double>& history() const { return hist_; }
+    void spmvDevice(const double* d_x, double* d_y);
+    void spmvHost(const double* x, double* y);
+    void csrGet(int32_t* ro, int32_t* ci, double* v);
+    void precondSetup(const bcs_solver_config& cfg);
+    void precondApplyHost(const double* r, double* z);
+    int amgDepth() const { return nlev_; }
+    void amgLevelSizes(int l, int* rows, int* nnz) const;
+    void amgLevelGet(int l, int32_t* ro, int32_t* ci, double* v, int32_t* agg);
+    int scheduleDepth(int l) const;
+
+    cudaStream_t stream() const { return stream_; }
+    int blockSize() const { return n_; }
+    int nCells() const { return nc_; }
+
+private:
+    void requireMatrix() const;
+    void validateConfig(const bcs_solver_config& cfg) const;
+    void buildPrecond(const bcs_solver_config& cfg);
+    void buildHierarchy(const bcs_solver_config& cfg);
+    void setupLevelPattern(Level& L);
+    void diluSetup(Level& L);
+    void lusgsSetup(Level& L);
+    void applyPrecond(const double* r, double* z);
+    void smootherApply(Level& L, const double* r, double* z, int accumulate);
+    void vcycle(int l, const double* r, double* z);
+    void gmres(const double* b, double* x, const bcs_solver_config& cfg, bcs_report& rep);
+    void bicgstab(const double* b, double* x, const bcs_solver_config& cfg, bcs_report& rep);
+    void spmvLevel(const Level& L, const double* x, const double* sub, double* y);
+    double dotHost(const double* a, const double* b, size_t N, bool sqrt_out);
+    void sync();
+    void checkErr(const char* where);
+    int readErrCell();
+
+    int device_ = 0;
+    cudaStream_t own_ = nullptr, stream_ = nullptr;
+    bool kernelTiming_ = false;
+    LaunchCounter launches_;
+
+    // topology
+    int nc_ = 0, nf_ = 0, n_ = 0;
+    bool hasTopo_ = false, hasValues_ = false;
+    std::vector<int32_t> hOwner_, hNeigh_;
+    DArray<int> dOwner_, dNeigh_, ro_, ci_, dg_, tpos_, src_, fill_;
+    DArray<double> vals_;
+    DArray<double> ldu_diag_, ldu_upper_, ldu_lower_;
+    // SolvePipeline state (engine.hpp:35-37): only the EngineCsr branch updates it
+    bool pipeHasSetup_ = false;
+    uint64_t pipeSig_ = 0;
+    bool pipeSigValid_ = false;
+
+    // preconditioner
+    int pcKind_ = -1;  // 0 none, 1 LUSGS, 2 DILU, 3 AMG
+    bcs_solver_config pcCfg_{};
+    std::vector<Level> levels_;  // storage persists across solves; nlev_ active
+    int nlev_ = 0;
+    DArray<double> dense_;
+    DArray<int> dpiv_;
+    int m_ = 0;
+    // scratch
+    DArray<int> cnt_, lvl_, push_, scanTmp_, flag_, err_, ctr_, choice_, segOff_, cro_, big_;
+    DArray<double> dn_, str_;
+    DArray<unsigned long long> keys_, sorted_;
+
+    // Krylov workspace
+    DArray<double> V_, w_, zk_, rk_, H_, cs_, sn_, g_, y_, scal_, partials_;
+    DArray<double> kb_, kx_;  // staging for host-array entry points
+    DArray<double> bp_, bv_, bs_, bt_, bph_, bsh_, brh_;
+    DArray<int> ticket_;
+    double* hStatus_ = nullptr;  // pinned
+    std::vector<double> hist_;
+
+    // SpMV event timing (fine level)
+    cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+    double spmvMs_ = 0.0;
+    int spmvCount_ = 0;
+};
+
+}  // namespace bcs

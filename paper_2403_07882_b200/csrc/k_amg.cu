@@ -1,0 +1,529 @@
+// K9-K12: pairwise-aggregation AMG setup and transfer operators.
+//
+// Reference: pairwiseAggregate (amg.cpp:10-37), galerkinCoarse (:39-71),
+// hierarchy/dense coarsest (:73-105), V-cycle transfers (:111-158).
+//
+// Aggregation is a sequential greedy matching in row order.  Its exact
+// parallel form: row r's decision depends only on (a) its lower neighbours
+// (was r already taken?) and (b) the lower-than-r neighbours of each upper
+// neighbour j (is j still free?).  We run Kahn's algorithm over that
+// dependency DAG in a persistent cooperative kernel (one grid barrier per
+// round); when all dependencies of r are decided its decision equals the
+// sequential one.  Strengths are computed with the reference's operation
+// order (sequential Frobenius sums, IEEE sqrt/div, no FMA), so the integer
+// aggregates are bit-identical.  Galerkin sums are taken per coarse block in
+// (fine row ascending, slot ascending) order from +0.0 — also bit-identical.
+#include "device.cuh"
+#include "kernels.hpp"
+
+#include <cooperative_groups.h>
+#include <stdexcept>
+#include <string>
+
+namespace cg = cooperative_groups;
+
+namespace bcs {
+
+#define BCS_DISPATCH_N(n, ...)                                                        \
+    switch (n) {                                                                      \
+        case 1: { constexpr int N = 1; __VA_ARGS__; } break;                          \
+        case 2: { constexpr int N = 2; __VA_ARGS__; } break;                          \
+        case 3: { constexpr int N = 3; __VA_ARGS__; } break;                          \
+        case 4: { constexpr int N = 4; __VA_ARGS__; } break;                          \
+        case 5: { constexpr int N = 5; __VA_ARGS__; } break;                          \
+        default: throw std::invalid_argument("block size must be 1..5 on the device"); \
+    }
+
+// ------------------------------------------------------------- strengths
+template <int N>
+__global__ void k_diag_norm(int rows, const int* __restrict__ dg, const double* __restrict__ v, double* dn) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    const int d = dg[r];
+    dn[r] = d >= 0 ? frob<N>(v + static_cast<size_t>(d) * N * N) : 0.0;
+}
+
+// str[k] = ||A_k||_F / sqrt(max(dn_r dn_j, 1e-300))   (amg.cpp:27-28)
+template <int N>
+__global__ void k_strength(int rows, const int* __restrict__ ro, const int* __restrict__ ci,
+                           const double* __restrict__ v, const double* __restrict__ dn, double* str) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    const double dr = dn[r];
+    for (int k = ro[r]; k < ro[r + 1]; ++k) {
+        const int j = ci[k];
+        const double prod = __dmul_rn(dr, dn[j]);
+        const double den = __dsqrt_rn(prod < 1e-300 ? 1e-300 : prod);  // std::max(prod, 1e-300)
+        str[k] = __ddiv_rn(frob<N>(v + static_cast<size_t>(k) * N * N), den);
+    }
+}
+
+void strengths(int n, int rows, const int* ro, const int* ci, const int* dg, const double* v, double* dn,
+               double* str, cudaStream_t s) {
+    const unsigned g = (rows + 255) / 256;
+    if (!g) return;
+    BCS_DISPATCH_N(n, {
+        k_diag_norm<N><<<g, 256, 0, s>>>(rows, dg, v, dn);
+        k_strength<N><<<g, 256, 0, s>>>(rows, ro, ci, v, dn, str);
+    });
+    count_launch(2);
+}
+
+// ------------------------------------------------------------ aggregation
+constexpr int kTaken = -2;
+constexpr int kSingle = -1;
+
+// number of decisions row r waits for: lower neighbours + for every upper
+// neighbour j the entries of row j with column < r.
+__global__ void k_agg_init(int rows, const int* __restrict__ ro, const int* __restrict__ ci,
+                           const int* __restrict__ dg, const int* __restrict__ tpos, int* cnt, int* order,
+                           int* push) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    const int d = dg[r];
+    int c = d - ro[r];
+    for (int k = d + 1; k < ro[r + 1]; ++k) c += tpos[k] - ro[ci[k]];
+    cnt[r] = c;
+    if (c == 0) order[atomicAdd(&push[2], 1)] = r;
+}
+
+template <bool GRID>
+__global__ void __launch_bounds__(256) k_agg_kahn(int rows, const int* __restrict__ ro, const int* __restrict__ ci,
+                                                  const int* __restrict__ dg, const int* __restrict__ tpos,
+                                                  const double* __restrict__ str, int* choice, int* cnt,
+                                                  int* order, int* push, int* out) {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nth = gridDim.x * blockDim.x;
+    int head = 0, level = 0;
+    while (true) {
+        const int c = __ldcg(&push[(level + 2) % 3]);
+        const int end = head + c;
+        if (c == 0) break;
+        if (blockIdx.x == 0 && threadIdx.x == 0) push[(level + 1) % 3] = 0;
+        for (int t = head + tid; t < end; t += nth) {
+            const int r = __ldcg(&order[t]);
+            const int b = ro[r], d = dg[r], e = ro[r + 1];
+            // (a) taken by a lower neighbour?
+            bool taken = false;
+            for (int k = b; k < d; ++k)
+                if (__ldcg(&choice[ci[k]]) == r) taken = true;
+            int decision = kTaken;
+            if (!taken) {
+                int best = -1;
+                double bs = -1.0;
+                for (int k = d + 1; k < e; ++k) {
+                    const int j = ci[k];
+                    bool freej = true;
+                    const int tp = tpos[k];
+                    for (int kk = ro[j]; kk < tp; ++kk)
+                        if (__ldcg(&choice[ci[kk]]) == j) {
+                            freej = false;
+                            break;
+                        }
+                    if (freej) {
+                        const double sv = str[k];
+                        if (sv > bs) {
+                            bs = sv;
+                            best = j;
+                        }
+                    }
+                }
+                decision = best >= 0 ? best : kSingle;
+            }
+            choice[r] = decision;
+            __threadfence();
+            // release dependants
+            for (int k = d + 1; k < e; ++k) {
+                const int j = ci[k];
+                if (atomicSub(&cnt[j], 1) == 1) order[end + atomicAdd(&push[level % 3], 1)] = j;
+                const int dj = dg[j];
+                for (int kk = tpos[k] + 1; kk < dj; ++kk) {
+                    const int q = ci[kk];
+                    if (atomicSub(&cnt[q], 1) == 1) order[end + atomicAdd(&push[level % 3], 1)] = q;
+                }
+            }
+        }
+        head = end;
+        ++level;
+        if (GRID) {
+            __threadfence();
+            cg::this_grid().sync();
+        } else {
+            __threadfence_block();
+            __syncthreads();
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        out[0] = level;
+        out[1] = head;
+    }
+}
+
+void aggregate_kahn(int rows, const int* ro, const int* ci, const int* dg, const int* tpos, const double* str,
+                    int* choice, KahnWork w, int* err, cudaStream_t s) {
+    if (rows <= 0) return;
+    int* push = w.tail;  // push[3] + out[2]
+    cudaMemsetAsync(push, 0, 5 * sizeof(int), s);
+    k_agg_init<<<(rows + 255) / 256, 256, 0, s>>>(rows, ro, ci, dg, tpos, w.cnt, w.lvl, push);
+    count_launch();
+    int* order = w.lvl;
+    int* out = push + 3;
+    if (rows <= 8192) {
+        k_agg_kahn<false><<<1, 256, 0, s>>>(rows, ro, ci, dg, tpos, str, choice, w.cnt, order, push, out);
+    } else {
+        static int bps = 0;
+        if (!bps) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_agg_kahn<true>, 256, 0);
+            if (bps < 1) bps = 1;
+        }
+        int grid = num_sms() * bps;
+        const int need = (rows + 255) / 256;
+        if (grid > need) grid = need;
+        void* args[] = {(void*)&rows, (void*)&ro,     (void*)&ci,    (void*)&dg,   (void*)&tpos, (void*)&str,
+                        (void*)&choice, (void*)&w.cnt, (void*)&order, (void*)&push, (void*)&out};
+        cudaError_t e = cudaLaunchCooperativeKernel((void*)k_agg_kahn<true>, dim3(grid), dim3(256), args, 0, s);
+        if (e != cudaSuccess)
+            throw std::runtime_error(std::string("cooperative launch failed: ") + cudaGetErrorString(e));
+    }
+    count_launch();
+    int h[2] = {0, 0};
+    cudaMemcpyAsync(h, out, sizeof h, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    if (h[1] != rows) throw std::runtime_error("aggregation: dependency graph did not cover all rows");
+}
+
+__global__ void k_init_flag(int rows, const int* choice, int* flag) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < rows) flag[r] = choice[r] != kTaken ? 1 : 0;
+}
+__global__ void k_number(int rows, const int* choice, const int* cid, int* agg, int* members) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    const int ch = choice[r];
+    if (ch == kTaken) return;
+    const int c = cid[r];
+    agg[r] = c;
+    members[2 * c] = r;
+    members[2 * c + 1] = ch >= 0 ? ch : -1;
+    if (ch >= 0) agg[ch] = c;
+}
+
+int aggregate_number(int rows, const int* choice, int* flag_tmp, int* agg, int* members, int* d_total,
+                     int* scan_tmp, cudaStream_t s) {
+    const unsigned g = (rows + 255) / 256;
+    k_init_flag<<<g, 256, 0, s>>>(rows, choice, flag_tmp);
+    count_launch();
+    exclusive_scan(flag_tmp, rows, d_total, scan_tmp, s);
+    k_number<<<g, 256, 0, s>>>(rows, choice, flag_tmp, agg, members);
+    count_launch();
+    int nc = 0;
+    cudaMemcpyAsync(&nc, d_total, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    return nc;
+}
+
+// -------------------------------------------------------------- Galerkin
+__global__ void k_seg_len(int nC, const int* ro, const int* members, int* seg) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nC) return;
+    const int r1 = members[2 * c], r2 = members[2 * c + 1];
+    seg[c] = (ro[r1 + 1] - ro[r1]) + (r2 >= 0 ? ro[r2 + 1] - ro[r2] : 0) + 1;
+}
+void galerkin_seg_len(int nCoarse, const int* ro, const int* members, int* seg_off, cudaStream_t s) {
+    k_seg_len<<<(nCoarse + 255) / 256, 256, 0, s>>>(nCoarse, ro, members, seg_off);
+    count_launch();
+}
+
+// key = (coarse column << 32) | position in the (r1 entries, r2 entries) list;
+// the forced diagonal is (c << 32) | 0xFFFFFFFF (sorts after real entries).
+__global__ void k_keys(int nC, const int* ro, const int* ci, const int* agg, const int* members, const int* seg,
+                       unsigned long long* keys) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nC) return;
+    const int r1 = members[2 * c], r2 = members[2 * c + 1];
+    unsigned long long* out = keys + seg[c];
+    unsigned p = 0;
+    for (int k = ro[r1]; k < ro[r1 + 1]; ++k, ++p)
+        out[p] = (static_cast<unsigned long long>(agg[ci[k]]) << 32) | p;
+    if (r2 >= 0)
+        for (int k = ro[r2]; k < ro[r2 + 1]; ++k, ++p)
+            out[p] = (static_cast<unsigned long long>(agg[ci[k]]) << 32) | p;
+    out[p] = (static_cast<unsigned long long>(c) << 32) | 0xFFFFFFFFull;
+}
+void galerkin_keys(int nCoarse, const int* ro, const int* ci, const int* agg, const int* members,
+                   const int* seg_off, unsigned long long* keys, cudaStream_t s) {
+    k_keys<<<(nCoarse + 127) / 128, 128, 0, s>>>(nCoarse, ro, ci, agg, members, seg_off, keys);
+    count_launch();
+}
+
+constexpr int kWarpSeg = 256;    // segments up to this size: one warp, rank sort in smem
+constexpr int kBlockSeg = 12288; // larger: one CTA, rank sort in 96 KB smem
+
+__global__ void __launch_bounds__(256) k_sort_small(int nC, const int* seg, const unsigned long long* keys,
+                                                    unsigned long long* sorted, int* big, int* nbig) {
+    __shared__ unsigned long long sh[8][kWarpSeg];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int c = blockIdx.x * 8 + w;
+    if (c >= nC) return;
+    const int b = seg[c], len = seg[c + 1] - b;
+    if (len > kWarpSeg) {
+        if (lane == 0) big[atomicAdd(nbig, 1)] = c;
+        return;
+    }
+    for (int i = lane; i < len; i += 32) sh[w][i] = keys[b + i];
+    __syncwarp();
+    for (int i = lane; i < len; i += 32) {
+        const unsigned long long k = sh[w][i];
+        int rank = 0;
+        for (int q = 0; q < len; ++q) rank += sh[w][q] < k ? 1 : 0;
+        sorted[b + rank] = k;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_sort_big(const int* seg, const unsigned long long* keys,
+                                                   unsigned long long* sorted, const int* big, int* err) {
+    extern __shared__ unsigned long long shb[];
+    const int c = big[blockIdx.x];
+    const int b = seg[c], len = seg[c + 1] - b;
+    if (len > kBlockSeg) {
+        if (threadIdx.x == 0) atomicExch(err, 1);
+        return;
+    }
+    for (int i = threadIdx.x; i < len; i += blockDim.x) shb[i] = keys[b + i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+        const unsigned long long k = shb[i];
+        int rank = 0;
+        for (int q = 0; q < len; ++q) rank += shb[q] < k ? 1 : 0;
+        sorted[b + rank] = k;
+    }
+}
+
+void galerkin_sort(int nCoarse, const int* seg_off, const unsigned long long* keys, unsigned long long* sorted,
+                   int* big, int* nbig, int* err, cudaStream_t s) {
+    cudaMemsetAsync(nbig, 0, sizeof(int), s);
+    k_sort_small<<<(nCoarse + 7) / 8, 256, 0, s>>>(nCoarse, seg_off, keys, sorted, big, nbig);
+    count_launch();
+    int nb = 0;
+    cudaMemcpyAsync(&nb, nbig, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    if (nb > 0) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kBlockSeg * static_cast<int>(sizeof(unsigned long long)));
+            attr = true;
+        }
+        k_sort_big<<<nb, 1024, kBlockSeg * sizeof(unsigned long long), s>>>(seg_off, keys, sorted, big, err);
+        count_launch();
+    }
+}
+
+__global__ void k_count(int nC, const int* seg, const unsigned long long* sorted, int* cro) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nC) return;
+    const int b = seg[c], e = seg[c + 1];
+    int u = 0;
+    unsigned prev = 0xFFFFFFFFu;
+    for (int i = b; i < e; ++i) {
+        const unsigned J = static_cast<unsigned>(sorted[i] >> 32);
+        if (i == b || J != prev) ++u;
+        prev = J;
+    }
+    cro[c] = u;
+}
+void galerkin_count(int nCoarse, const int* seg_off, const unsigned long long* sorted, int* cro, cudaStream_t s) {
+    k_count<<<(nCoarse + 255) / 256, 256, 0, s>>>(nCoarse, seg_off, sorted, cro);
+    count_launch();
+}
+
+// one warp per coarse row; lane e accumulates block element e of each slot
+template <int N>
+__global__ void __launch_bounds__(256) k_fill(int nC, const int* __restrict__ ro, const int* __restrict__ members,
+                                              const int* __restrict__ seg, const unsigned long long* __restrict__ sorted,
+                                              const double* __restrict__ v, const int* __restrict__ cro, int* cci,
+                                              double* cv) {
+    constexpr int NN = N * N;
+    const int lane = threadIdx.x & 31;
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (c >= nC) return;
+    const int r1 = members[2 * c], r2 = members[2 * c + 1];
+    const int b1 = ro[r1], len1 = ro[r1 + 1] - b1;
+    const int b2 = r2 >= 0 ? ro[r2] : 0;
+    const int sb = seg[c], se = seg[c + 1];
+    int slot = cro[c] - 1;
+    unsigned prev = 0;
+    double acc = 0.0;
+    for (int i = sb; i < se; ++i) {
+        const unsigned long long key = sorted[i];
+        const unsigned J = static_cast<unsigned>(key >> 32);
+        const unsigned pos = static_cast<unsigned>(key & 0xFFFFFFFFull);
+        if (i == sb || J != prev) {
+            if (i != sb && lane < NN) cv[static_cast<size_t>(slot) * NN + lane] = acc;
+            ++slot;
+            if (lane == 0) cci[slot] = static_cast<int>(J);
+            acc = 0.0;
+            prev = J;
+        }
+        if (pos != 0xFFFFFFFFu && lane < NN) {
+            const int k = pos < static_cast<unsigned>(len1) ? b1 + static_cast<int>(pos) : b2 + static_cast<int>(pos) - len1;
+            acc = __dadd_rn(acc, v[static_cast<size_t>(k) * NN + lane]);
+        }
+    }
+    if (lane < NN) cv[static_cast<size_t>(slot) * NN + lane] = acc;
+}
+void galerkin_fill(int n, int nCoarse, const int* ro, const int* members, const int* seg_off,
+                   const unsigned long long* sorted, const double* v, const int* cro, int* cci, double* cv,
+                   cudaStream_t s) {
+    const unsigned g = (nCoarse + 7) / 8;
+    BCS_DISPATCH_N(n, k_fill<N><<<g, 256, 0, s>>>(nCoarse, ro, members, seg_off, sorted, v, cro, cci, cv));
+    count_launch();
+}
+
+// ------------------------------------------------------------- transfers
+__global__ void k_restrict(int n, int nC, const int* members, const double* res, double* rc) {
+    const size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (t >= static_cast<size_t>(nC) * n) return;
+    const int c = static_cast<int>(t / n), q = static_cast<int>(t - static_cast<size_t>(c) * n);
+    const int r1 = members[2 * c], r2 = members[2 * c + 1];
+    double v = __dadd_rn(0.0, res[static_cast<size_t>(r1) * n + q]);
+    if (r2 >= 0) v = __dadd_rn(v, res[static_cast<size_t>(r2) * n + q]);
+    rc[t] = v;
+}
+void restrict_vec(int n, int nCoarse, const int* members, const double* res, double* rc, cudaStream_t s) {
+    const size_t w = static_cast<size_t>(nCoarse) * n;
+    k_restrict<<<static_cast<unsigned>((w + 255) / 256), 256, 0, s>>>(n, nCoarse, members, res, rc);
+    count_launch();
+}
+__global__ void k_prolong(int n, int rows, const int* agg, const double* zc, double* z) {
+    const size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (t >= static_cast<size_t>(rows) * n) return;
+    const int r = static_cast<int>(t / n), q = static_cast<int>(t - static_cast<size_t>(r) * n);
+    z[t] = __dadd_rn(z[t], zc[static_cast<size_t>(agg[r]) * n + q]);
+}
+void prolong_vec(int n, int rows, const int* agg, const double* zc, double* z, cudaStream_t s) {
+    const size_t w = static_cast<size_t>(rows) * n;
+    k_prolong<<<static_cast<unsigned>((w + 255) / 256), 256, 0, s>>>(n, rows, agg, zc, z);
+    count_launch();
+}
+
+// ------------------------------------------------------- dense coarsest
+__global__ void k_dense_build(int n, int rows, const int* ro, const int* ci, const double* v, double* dense) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    const size_t m = static_cast<size_t>(rows) * n;
+    for (int k = ro[r]; k < ro[r + 1]; ++k) {
+        const int c = ci[k];
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j)
+                dense[(static_cast<size_t>(r) * n + i) * m + (static_cast<size_t>(c) * n + j)] =
+                    v[static_cast<size_t>(k) * n * n + i * n + j];
+    }
+}
+void dense_build(int n, int rows, const int* ro, const int* ci, const double* v, double* dense, cudaStream_t s) {
+    const size_t m = static_cast<size_t>(rows) * n;
+    cudaMemsetAsync(dense, 0, m * m * sizeof(double), s);
+    k_dense_build<<<(rows + 127) / 128, 128, 0, s>>>(n, rows, ro, ci, v, dense);
+    count_launch();
+}
+
+// denseFactor (smallmat.hpp:134-161): one CTA, right-looking, reference order
+__global__ void __launch_bounds__(1024) k_dense_factor(int m, double* a, int* piv, int* err) {
+    __shared__ double sv[32];
+    __shared__ int si[32];
+    __shared__ int sp;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+    for (int k = 0; k < m; ++k) {
+        // first max of |a_ik|, i >= k (strict >: smallest index among maxima)
+        double best = -1.0;
+        int bi = 0x7fffffff;
+        for (int i = k + tid; i < m; i += nt) {
+            const double v = fabs(a[static_cast<size_t>(i) * m + k]);
+            if (v > best || (v == best && i < bi)) {
+                best = v;
+                bi = i;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_down_sync(0xffffffffu, best, o);
+            const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+            if (ov > best || (ov == best && oi < bi)) {
+                best = ov;
+                bi = oi;
+            }
+        }
+        if (lane == 0) {
+            sv[wid] = best;
+            si[wid] = bi;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double bb = sv[0];
+            int ii = si[0];
+            for (int w = 1; w < (nt >> 5); ++w)
+                if (sv[w] > bb || (sv[w] == bb && si[w] < ii)) {
+                    bb = sv[w];
+                    ii = si[w];
+                }
+            // the reference starts from |a_kk| with p = k; ties keep k
+            const double akk = fabs(a[static_cast<size_t>(k) * m + k]);
+            if (!(bb > akk)) ii = k, bb = akk;
+            if (bb < 1e-300) atomicExch(err, 1);
+            piv[k] = ii;
+            sp = ii;
+        }
+        __syncthreads();
+        const int p = sp;
+        if (p != k)
+            for (int j = tid; j < m; j += nt) {
+                const double t = a[static_cast<size_t>(k) * m + j];
+                a[static_cast<size_t>(k) * m + j] = a[static_cast<size_t>(p) * m + j];
+                a[static_cast<size_t>(p) * m + j] = t;
+            }
+        __syncthreads();
+        const double d = a[static_cast<size_t>(k) * m + k];
+        for (int i = k + 1 + tid; i < m; i += nt) a[static_cast<size_t>(i) * m + k] = __ddiv_rn(a[static_cast<size_t>(i) * m + k], d);
+        __syncthreads();
+        const int w = m - k - 1;
+        for (long long t = tid; t < static_cast<long long>(w) * w; t += nt) {
+            const int i = k + 1 + static_cast<int>(t / w), j = k + 1 + static_cast<int>(t % w);
+            a[static_cast<size_t>(i) * m + j] =
+                __dsub_rn(a[static_cast<size_t>(i) * m + j], __dmul_rn(a[static_cast<size_t>(i) * m + k], a[static_cast<size_t>(k) * m + j]));
+        }
+        __syncthreads();
+    }
+}
+void dense_factor(int m, double* a, int* piv, int* err, cudaStream_t s) {
+    k_dense_factor<<<1, 1024, 0, s>>>(m, a, piv, err);
+    count_launch();
+}
+
+// denseSolve (smallmat.hpp:163-174), sequential reference order
+__global__ void k_dense_solve(int m, const double* lu, const int* piv, const double* r, double* z) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    for (int i = 0; i < m; ++i) z[i] = r[i];
+    for (int k = 0; k < m; ++k) {
+        const int p = piv[k];
+        if (p != k) {
+            const double t = z[k];
+            z[k] = z[p];
+            z[p] = t;
+        }
+    }
+    for (int i = 1; i < m; ++i) {
+        double x = z[i];
+        for (int j = 0; j < i; ++j) x = __dsub_rn(x, __dmul_rn(lu[static_cast<size_t>(i) * m + j], z[j]));
+        z[i] = x;
+    }
+    for (int i = m - 1; i >= 0; --i) {
+        double x = z[i];
+        for (int j = i + 1; j < m; ++j) x = __dsub_rn(x, __dmul_rn(lu[static_cast<size_t>(i) * m + j], z[j]));
+        z[i] = __ddiv_rn(x, lu[static_cast<size_t>(i) * m + i]);
+    }
+}
+void dense_solve(int m, const double* lu, const int* piv, const double* r, double* z, cudaStream_t s) {
+    k_dense_solve<<<1, 32, 0, s>>>(m, lu, piv, r, z);
+    count_launch();
+}
+
+}  // namespace bcs

@@ -1,0 +1,206 @@
+// K13-K15: Krylov vector kernels (gmresSolve / bicgstabSolve,
+// proj/core/src/krylov.cpp:59-214).
+//
+// Element-wise updates use the reference expressions verbatim (bit-identical
+// under -fmad=false).  Reductions are deterministic two-level trees (fixed
+// grid, fixed per-block order, the last block to finish sums the partials in
+// block order) — the only place where the association order differs from the
+// reference's sequential sum.  MGS orthogonalisation fuses each axpy with the
+// next dot product; the Hessenberg/Givens scalars never leave the device
+// except the one |g_{j+1}| the host needs for the convergence test.
+#include "device.cuh"
+#include "kernels.hpp"
+
+namespace bcs {
+
+constexpr int kRedThreads = 256;
+
+int reduce_blocks() { return 2 * num_sms(); }
+
+__device__ __forceinline__ void finish_reduction(double part, double* partials, int* ticket, double* out,
+                                                 bool sqrt_out) {
+    __shared__ double sh[32];
+    __shared__ bool last;
+    const double s = block_sum<kRedThreads>(part, sh);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = s;
+        __threadfence();
+        last = atomicAdd(ticket, 1) == static_cast<int>(gridDim.x) - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double t = 0.0;
+    for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) t += __ldcg(&partials[i]);
+    t = block_sum<kRedThreads>(t, sh);
+    if (threadIdx.x == 0) {
+        out[0] = sqrt_out ? sqrt(t) : t;
+        *ticket = 0;
+    }
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_dot(const double* __restrict__ a, const double* __restrict__ b,
+                                                     size_t N, double* out, int sqrt_out, double* partials,
+                                                     int* ticket) {
+    double s = 0.0;
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < N; i += stride)
+        s += a[i] * b[i];
+    finish_reduction(s, partials, ticket, out, sqrt_out != 0);
+}
+
+void dot(const double* a, const double* b, size_t N, double* out, bool sqrt_out, double* partials, int* ticket,
+         cudaStream_t s) {
+    k_dot<<<reduce_blocks(), kRedThreads, 0, s>>>(a, b, N, out, sqrt_out ? 1 : 0, partials, ticket);
+    count_launch();
+}
+
+// w -= h v ; dot(w, nextv) or ||w||
+__global__ void __launch_bounds__(kRedThreads) k_axpy_dot(double* __restrict__ w, const double* __restrict__ h,
+                                                          const double* __restrict__ v,
+                                                          const double* __restrict__ nextv, size_t N, double* out,
+                                                          double* partials, int* ticket) {
+    const double hv = *h;
+    double s = 0.0;
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < N; i += stride) {
+        const double wn = w[i] - hv * v[i];
+        w[i] = wn;
+        s += nextv ? wn * nextv[i] : wn * wn;
+    }
+    finish_reduction(s, partials, ticket, out, nextv == nullptr);
+}
+
+void axpy_dot(double* w, const double* h, const double* v, const double* nextv, size_t N, double* out,
+              double* partials, int* ticket, cudaStream_t s) {
+    k_axpy_dot<<<reduce_blocks(), kRedThreads, 0, s>>>(w, h, v, nextv, N, out, partials, ticket);
+    count_launch();
+}
+
+__global__ void k_scale_by(const double* __restrict__ x, const double* __restrict__ den, double thr,
+                           double* __restrict__ y, size_t N) {
+    const double d = *den;
+    if (!(d > thr)) return;
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < N; i += stride) y[i] = x[i] / d;
+}
+void scale_by(const double* x, const double* den, double thr, double* y, size_t N, cudaStream_t s) {
+    k_scale_by<<<4 * num_sms(), 256, 0, s>>>(x, den, thr, y, N);
+    count_launch();
+}
+
+__global__ void k_sub(const double* __restrict__ b, const double* __restrict__ y, double* __restrict__ r, size_t N) {
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < N; i += stride) r[i] = b[i] - y[i];
+}
+void sub_vec(const double* b, const double* y, double* r, size_t N, cudaStream_t s) {
+    k_sub<<<4 * num_sms(), 256, 0, s>>>(b, y, r, N);
+    count_launch();
+}
+void copy_vec(const double* x, double* y, size_t N, cudaStream_t s) {
+    cudaMemcpyAsync(y, x, N * sizeof(double), cudaMemcpyDeviceToDevice, s);
+}
+__global__ void k_add_to(double* __restrict__ x, const double* __restrict__ z, size_t N) {
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < N; i += stride) x[i] += z[i];
+}
+void add_to(double* x, const double* z, size_t N, cudaStream_t s) {
+    k_add_to<<<4 * num_sms(), 256, 0, s>>>(x, z, N);
+    count_launch();
+}
+
+// w = sum_{i<j} y_i V_i with the reference's accumulation order (krylov.cpp:127-129)
+__global__ void k_lincomb(const double* __restrict__ V, size_t ld, const double* __restrict__ y, int j,
+                          double* __restrict__ w, size_t N) {
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t q = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; q < N; q += stride) {
+        double acc = 0.0;
+        for (int i = 0; i < j; ++i) acc += y[i] * V[static_cast<size_t>(i) * ld + q];
+        w[q] = acc;
+    }
+}
+void lincomb(const double* V, size_t ld, const double* y, int j, double* w, size_t N, cudaStream_t s) {
+    k_lincomb<<<4 * num_sms(), 256, 0, s>>>(V, ld, y, j, w, N);
+    count_launch();
+}
+
+// Givens update of column j (krylov.cpp:104-117); H is (m+1) x m row-major
+__global__ void k_givens(double* H, int m, int j, double* cs, double* sn, double* g, double* status) {
+    if (threadIdx.x != 0) return;
+    const double hh = H[(j + 1) * m + j];
+    for (int i = 0; i < j; ++i) {
+        const double t = cs[i] * H[i * m + j] + sn[i] * H[(i + 1) * m + j];
+        H[(i + 1) * m + j] = -sn[i] * H[i * m + j] + cs[i] * H[(i + 1) * m + j];
+        H[i * m + j] = t;
+    }
+    const double den = hypot(H[j * m + j], H[(j + 1) * m + j]);
+    cs[j] = den > 0.0 ? H[j * m + j] / den : 1.0;
+    sn[j] = den > 0.0 ? H[(j + 1) * m + j] / den : 0.0;
+    H[j * m + j] = den;
+    H[(j + 1) * m + j] = 0.0;
+    g[j + 1] = -sn[j] * g[j];
+    g[j] = cs[j] * g[j];
+    status[0] = fabs(g[j + 1]);
+    status[1] = (hh > 1e-290) ? 0.0 : 1.0;
+}
+void givens_step(double* H, int m, int j, double* cs, double* sn, double* g, double* status, cudaStream_t s) {
+    k_givens<<<1, 32, 0, s>>>(H, m, j, cs, sn, g, status);
+    count_launch();
+}
+
+__global__ void k_back_subst(const double* H, int m, int j, const double* g, double* y) {
+    if (threadIdx.x != 0) return;
+    for (int i = j - 1; i >= 0; --i) {
+        double sacc = g[i];
+        for (int q = i + 1; q < j; ++q) sacc -= H[i * m + q] * y[q];
+        y[i] = sacc / H[i * m + i];
+    }
+}
+void back_subst(const double* H, int m, int j, const double* g, double* y, cudaStream_t s) {
+    k_back_subst<<<1, 32, 0, s>>>(H, m, j, g, y);
+    count_launch();
+}
+
+// ---- BiCGStab (krylov.cpp:174-200)
+__global__ void k_bicg_p(double* p, const double* r, const double* v, double bf, double omega, size_t N) {
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < N; i += stride)
+        p[i] = r[i] + bf * (p[i] - omega * v[i]);
+}
+void bicg_p(double* p, const double* r, const double* v, double bf, double omega, size_t N, cudaStream_t s) {
+    k_bicg_p<<<4 * num_sms(), 256, 0, s>>>(p, r, v, bf, omega, N);
+    count_launch();
+}
+__global__ void k_bicg_s(double* sv, const double* r, const double* v, double alpha, size_t N) {
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < N; i += stride)
+        sv[i] = r[i] - alpha * v[i];
+}
+void bicg_s(double* sv, const double* r, const double* v, double alpha, size_t N, cudaStream_t s) {
+    k_bicg_s<<<4 * num_sms(), 256, 0, s>>>(sv, r, v, alpha, N);
+    count_launch();
+}
+__global__ void k_bicg_xh(double* x, const double* ph, double alpha, size_t N) {
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < N; i += stride)
+        x[i] += alpha * ph[i];
+}
+void bicg_x_half(double* x, const double* ph, double alpha, size_t N, cudaStream_t s) {
+    k_bicg_xh<<<4 * num_sms(), 256, 0, s>>>(x, ph, alpha, N);
+    count_launch();
+}
+__global__ void k_bicg_xr(double* x, double* r, const double* ph, const double* sh, const double* sv,
+                          const double* t, double alpha, double omega, size_t N) {
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < N; i += stride) {
+        x[i] += alpha * ph[i] + omega * sh[i];
+        r[i] = sv[i] - omega * t[i];
+    }
+}
+void bicg_x_r(double* x, double* r, const double* ph, const double* sh, const double* sv, const double* t,
+              double alpha, double omega, size_t N, cudaStream_t s) {
+    k_bicg_xr<<<4 * num_sms(), 256, 0, s>>>(x, r, ph, sh, sv, t, alpha, omega, N);
+    count_launch();
+}
+
+}  // namespace bcs

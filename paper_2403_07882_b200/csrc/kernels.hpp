@@ -1,0 +1,128 @@
+// Host-side launch wrappers for the sm_100a kernels (one translation unit
+// per subsystem: k_csr.cu, k_sweep.cu, k_amg.cu, k_krylov.cu).  Every wrapper
+// enqueues on the given stream and increments the launch counter.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bcs {
+
+struct LaunchCounter {
+    long long launches = 0;
+};
+extern thread_local LaunchCounter* g_launches;
+inline void count_launch(int k = 1) {
+    if (g_launches) g_launches->launches += k;
+}
+
+int num_sms();
+
+// ---------------------------------------------------------------- scan
+// exclusive prefix sum of n ints in place; *total (device) = sum. tmp >= scan_tmp_ints(n)
+size_t scan_tmp_ints(size_t n);
+void exclusive_scan(int* data, int n, int* d_total, int* tmp, cudaStream_t s);
+
+// ---------------------------------------------------- LDU -> BSR (K1, K2)
+// rowcnt must be zeroed, size nc+1
+void plan_count(int nc, int nf, const int* owner, const int* neigh, int* rowcnt, cudaStream_t s);
+// fill: ro (nc+1) already scanned; fill counters zeroed (nc)
+void plan_fill(int nc, int nf, const int* owner, const int* neigh, const int* ro, int* fillc, int* ci, int* src,
+               cudaStream_t s);
+void plan_sort_rows(int nc, const int* ro, int* ci, int* src, cudaStream_t s);
+void find_diag(int rows, const int* ro, const int* ci, int* dg, cudaStream_t s);
+void transpose_pos(int rows, const int* ro, const int* ci, int* tpos, int* asym_flag, cudaStream_t s);
+void gather_values(int n, int nnz, int nc, int nf, const int* src, const double* diag, const double* upper,
+                   const double* lower, double* vals, cudaStream_t s);
+
+// ------------------------------------------------------------- SpMV (K3)
+// y = A x  (sub == nullptr)   or   y = sub - A x
+void spmv(int n, int rows, const int* ro, const int* ci, const double* v, const double* x, const double* sub,
+          double* y, cudaStream_t s);
+
+// ------------------------------------------------- LU / sweeps (K5-K8)
+void factor_diag_blocks(int n, int rows, const int* dg, const double* v, double* lu, int* piv, int* err_cell,
+                        cudaStream_t s);
+// Level-synchronous Kahn over the lower-triangular DAG.  dilu != 0 also
+// computes the DILU modified diagonals (preconditioner.cpp:101-126) into lu/piv.
+// order (rows) receives the level-sorted row permutation; returns depth.
+struct KahnWork {
+    int* cnt;    // rows
+    int* tail;   // 1
+    int* lvl;    // rows+1 (level offsets into order)
+};
+int kahn_schedule(int n, int rows, const int* ro, const int* ci, const int* dg, const int* tpos, const double* v,
+                  bool dilu, double* lu, int* piv, int* order, KahnWork w, int* err_cell, cudaStream_t s);
+// sync-free sweeps (preconditioner.cpp:128-156 / :29-57). y, zb pre-filled
+// with the pending pattern (0xFF bytes).  accumulate: 0 none, 1 z = 0 + zb,
+// 2 z += zb.
+void sweep_forward(int n, int rows, const int* order, const int* ro, const int* ci, const int* dg, const double* v,
+                   const double* lu, const int* piv, const double* r, double* y, int* ctr, int* err,
+                   cudaStream_t s);
+void sweep_backward(int n, int rows, const int* order, const int* ro, const int* ci, const int* dg,
+                    const double* v, const double* lu, const int* piv, const double* y, double* zb, double* z,
+                    int accumulate, int* ctr, int* err, cudaStream_t s);
+
+// ------------------------------------------------------------ AMG (K9-K12)
+void strengths(int n, int rows, const int* ro, const int* ci, const int* dg, const double* v, double* dn,
+               double* str, cudaStream_t s);
+// greedy pairwise matching (amg.cpp:10-37), exact; choice[r]: -2 taken, -1 singleton, >=0 partner
+void aggregate_kahn(int rows, const int* ro, const int* ci, const int* dg, const int* tpos, const double* str,
+                    int* choice, KahnWork w, int* err, cudaStream_t s);
+// numbering: agg (rows), members (2 per coarse row); returns nCoarse (sync)
+int aggregate_number(int rows, const int* choice, int* flag_tmp, int* agg, int* members, int* d_total,
+                     int* scan_tmp, cudaStream_t s);
+// Galerkin coarse operator (amg.cpp:39-71)
+struct GalerkinTmp {
+    int* seg_off;            // nCoarse+1
+    unsigned long long* keys;// total
+    unsigned long long* sorted;
+    int* big;                // list of big segments
+    int* nbig;               // 1
+};
+size_t galerkin_keys_size(int rows_coarse, const int* d_dummy);
+// step 1: segment lengths into seg_off[c] (then caller scans)
+void galerkin_seg_len(int nCoarse, const int* ro, const int* members, int* seg_off, cudaStream_t s);
+void galerkin_keys(int nCoarse, const int* ro, const int* ci, const int* agg, const int* members,
+                   const int* seg_off, unsigned long long* keys, cudaStream_t s);
+void galerkin_sort(int nCoarse, const int* seg_off, const unsigned long long* keys, unsigned long long* sorted,
+                   int* big, int* nbig, int* err, cudaStream_t s);
+// coarse row lengths into cro[c] (then caller scans)
+void galerkin_count(int nCoarse, const int* seg_off, const unsigned long long* sorted, int* cro, cudaStream_t s);
+void galerkin_fill(int n, int nCoarse, const int* ro, const int* members, const int* seg_off,
+                   const unsigned long long* sorted, const double* v, const int* cro, int* cci, double* cv,
+                   cudaStream_t s);
+void restrict_vec(int n, int nCoarse, const int* members, const double* res, double* rc, cudaStream_t s);
+void prolong_vec(int n, int rows, const int* agg, const double* zc, double* z, cudaStream_t s);
+// dense coarsest level (amg.cpp:91-104, smallmat.hpp:134-174)
+void dense_build(int n, int rows, const int* ro, const int* ci, const double* v, double* dense, cudaStream_t s);
+void dense_factor(int m, double* a, int* piv, int* err, cudaStream_t s);
+void dense_solve(int m, const double* lu, const int* piv, const double* r, double* z, cudaStream_t s);
+
+// ------------------------------------------------------ Krylov (K13-K15)
+int reduce_blocks();
+// out[0] = dot(a, b)   (sqrt_out: out[0] = sqrt(dot)); deterministic
+void dot(const double* a, const double* b, size_t N, double* out, bool sqrt_out, double* partials, int* ticket,
+         cudaStream_t s);
+// w -= (*h) * v ; out = dot(w, nextv) (nextv == nullptr: out = sqrt(dot(w,w)))
+void axpy_dot(double* w, const double* h, const double* v, const double* nextv, size_t N, double* out,
+              double* partials, int* ticket, cudaStream_t s);
+// y = x / (*den) if (*den > thr) ; else untouched
+void scale_by(const double* x, const double* den, double thr, double* y, size_t N, cudaStream_t s);
+void copy_vec(const double* x, double* y, size_t N, cudaStream_t s);
+void sub_vec(const double* b, const double* y, double* r, size_t N, cudaStream_t s);  // r = b - y
+void add_to(double* x, const double* z, size_t N, cudaStream_t s);                     // x += z
+// w = sum_{i<j} y_i V_i  (in i order, from 0.0)
+void lincomb(const double* V, size_t ld, const double* y, int j, double* w, size_t N, cudaStream_t s);
+// GMRES Givens step on device (krylov.cpp:104-117); status[0]=|g_{j+1}|, status[1]=happy
+void givens_step(double* H, int m, int j, double* cs, double* sn, double* g, double* status, cudaStream_t s);
+void back_subst(const double* H, int m, int j, const double* g, double* y, cudaStream_t s);
+// BiCGStab elementwise updates (krylov.cpp:174-200)
+void bicg_p(double* p, const double* r, const double* v, double bf, double omega, size_t N, cudaStream_t s);
+void bicg_s(double* sv, const double* r, const double* v, double alpha, size_t N, cudaStream_t s);
+void bicg_x_half(double* x, const double* ph, double alpha, size_t N, cudaStream_t s);
+void bicg_x_r(double* x, double* r, const double* ph, const double* sh, const double* sv, const double* t,
+              double alpha, double omega, size_t N, cudaStream_t s);
+
+}  // namespace bcs

@@ -1,0 +1,75 @@
+"""Synthetic workloads of SURVEY §8(d) via libbcs_gen.so (csrc/gen/bcs_gen.cpp).
+
+``hex_euler``   — 5x5 density-based Jacobian (restates euler.cpp:390-455)
+``hex_coupled`` — 4x4 pressure-based coupled p-U system (incompressible.cpp:143-264)
+
+Both are bit-identical to the reference producers (tests/test_generator.py).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .bcs import BlockLduMatrix, BlockVector
+
+
+@dataclass
+class System:
+    A: BlockLduMatrix
+    b: BlockVector
+    x0: BlockVector
+    centroids: np.ndarray  # (n_cells, 3)
+    name: str
+
+
+def hex_sizes(nx: int, ny: int, nz: int):
+    nc, nf = ctypes.c_int(), ctypes.c_int()
+    N.gen().bcsgen_hex_sizes(nx, ny, nz, ctypes.byref(nc), ctypes.byref(nf))
+    return nc.value, nf.value
+
+
+def _alloc(nx, ny, nz, n, pinned_alloc=None):
+    nc, nf = hex_sizes(nx, ny, nz)
+    mk = pinned_alloc or (lambda size, dt: np.zeros(size, dt))
+    owner = mk(nf, np.int32)
+    neigh = mk(nf, np.int32)
+    diag = mk(nc * n * n, np.float64)
+    upper = mk(nf * n * n, np.float64)
+    lower = mk(nf * n * n, np.float64)
+    rhs = mk(nc * n, np.float64)
+    cen = np.zeros(nc * 3)
+    return nc, nf, owner, neigh, diag, upper, lower, rhs, cen
+
+
+def hex_euler(nx: int, ny: int = None, nz: int = None, aspect: float = 1.0, scramble_seed: int = -1,
+              alloc=None) -> System:
+    ny = nx if ny is None else ny
+    nz = nx if nz is None else nz
+    nc, nf, owner, neigh, diag, upper, lower, rhs, cen = _alloc(nx, ny, nz, 5, alloc)
+    rc = N.gen().bcsgen_hex_euler(nx, ny, nz, float(aspect), int(scramble_seed), N.ptr(owner), N.ptr(neigh),
+                                  N.ptr(diag), N.ptr(upper), N.ptr(lower), N.ptr(rhs), N.ptr(cen))
+    if rc:
+        raise ValueError("bcsgen_hex_euler: bad arguments")
+    A = BlockLduMatrix(nc, owner, neigh, 5, diag, upper, lower)
+    tag = "scrambled" if scramble_seed >= 0 else "natural"
+    return System(A, BlockVector(nc, 5, rhs), BlockVector(nc, 5), cen.reshape(nc, 3),
+                  f"euler5 {nx}x{ny}x{nz} {tag} AR{aspect:g}")
+
+
+def hex_coupled(nx: int, ny: int = None, nz: int = None, aspect: float = 1.0, scramble_seed: int = -1,
+                alloc=None) -> System:
+    ny = nx if ny is None else ny
+    nz = nx if nz is None else nz
+    nc, nf, owner, neigh, diag, upper, lower, rhs, cen = _alloc(nx, ny, nz, 4, alloc)
+    x0 = np.zeros(nc * 4)
+    rc = N.gen().bcsgen_hex_coupled(nx, ny, nz, float(aspect), int(scramble_seed), N.ptr(owner), N.ptr(neigh),
+                                    N.ptr(diag), N.ptr(upper), N.ptr(lower), N.ptr(rhs), N.ptr(x0), N.ptr(cen))
+    if rc:
+        raise ValueError("bcsgen_hex_coupled: bad arguments")
+    A = BlockLduMatrix(nc, owner, neigh, 4, diag, upper, lower)
+    tag = "scrambled" if scramble_seed >= 0 else "natural"
+    return System(A, BlockVector(nc, 4, rhs), BlockVector(nc, 4, x0), cen.reshape(nc, 3),
+                  f"coupled4 {nx}x{ny}x{nz} {tag} AR{aspect:g}")
