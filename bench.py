@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 block-coupled linear-solve path (BASELINE.json).
+
+Metric: "coupled linear solve s/outer-iter (setup+solve to 1e-8) & BSR SpMV
+HBM GB/s".  One step = one outer (nonlinear) iteration of the reference's
+SolvePipeline in steady state: value replace (LDU->BSR permutation) + full AMG
+setup (the reference rebuilds the hierarchy every call, engine.cpp:100-107) +
+GMRES(30)+AMG to relTol 1e-8 from x0 = 0.
+
+Workload (N=1): BASELINE configs[1], the 5x5 density-based system on a 128^3
+hex mesh (2,097,152 cells, 14,581,760 blocks), synthetic: the reference's
+Euler Jacobian (first-order Roe, farfield, cfl 50) of a seeded perturbed
+freestream, generated bit-identically to the reference by csrc/gen.
+
+  value  : s/outer-iter with LDU values resident in HBM (CUDA events, max over ranks)
+  e2e    : s/outer-iter through bcs_pipeline_solve (the drop-in C ABI call) with
+           pinned host LDU/b/x0 in, x out: H2D + topology check + replace + setup
+           + solve + D2H inside the timed region
+  roofline: the fine-level BSR SpMV (the kernel the metric names), algorithmic
+           bytes nnzb(8n^2+4)+4(R+1)+16nR per launch / mean CUDA-event duration
+           of the SpMV launches inside the timed steps, vs MEASURED_PEAKS hbm_gbs
+  cpu_baseline: the unmodified reference (oracle/_ref, 1 core) on a bounded
+           sample (the 48^3 instance of the same generator, replace-branch
+           SolvePipeline::solve) scaled by the row ratio to 128^3
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--size 128]
+Multi-GPU (torchrun, N>1): every rank solves its own 128^3 block (weak scaling,
+independent replicas until the Mode-R distributed solve lands).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "coupled linear solve s/outer-iter (setup+solve to 1e-8) & BSR SpMV HBM GB/s"
+UNIT = "s/outer-iter"
+CPU_SAMPLE_N = 48
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--size", type=int, default=128)
+    p.add_argument("--method", default="gmres", choices=["gmres", "bicgstab"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
+        os.environ.get("LOCAL_RANK", "0"))
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def spmv_bytes(nc, nf, n):
+    nnzb = nc + 2 * nf
+    return nnzb * (8 * n * n + 4) + 4 * (nc + 1) + 16 * n * nc
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"bcs_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except Exception:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
+        if not rows or not sm:
+            return None
+        mx = max(float(r[1]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[4 + i]})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": reasons, "samples": len(sm)}
+
+
+def solver_config(method):
+    from paper_2403_07882_b200 import bcs
+    return bcs.SolverConfig(method=bcs.KrylovMethod.GMRES if method == "gmres" else bcs.KrylovMethod.PBiCGStab,
+                            preconditioner=bcs.PrecondKind.AMG, relTol=1e-8, absTol=1e-300, maxIters=1000,
+                            gmresRestart=30, amg=bcs.AmgConfig(maxLevels=30, minCoarseRows=8))
+
+
+# ---------------------------------------------------------------- reference
+def reference_step_seconds(n_sample, method, calls):
+    """Replace-branch SolvePipeline::solve of the reference on the n_sample^3
+    instance; returns per-call seconds (after one setup call)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Reference, make_cfg
+    from paper_2403_07882_b200 import gen
+
+    R = Reference()
+    s = gen.hex_euler(n_sample)
+    cfg = make_cfg(method=0 if method == "gmres" else 1, precond=3, max_iters=1000)
+    R.solve(s.A, s.b.values, s.x0.values, cfg, calls=1, hist=False)  # setup branch
+    times, iters = [], None
+    for _ in range(calls):
+        t0 = time.perf_counter()
+        rc, x, rep, _ = R.solve(s.A, s.b.values, s.x0.values, cfg, calls=1, hist=False)
+        times.append(time.perf_counter() - t0)
+        iters = rep.iterations
+    return times, iters
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2403_07882_b200 import gen
+    nc_full, _ = gen.hex_sizes(args.size, args.size, args.size)
+    nc_s, _ = gen.hex_sizes(CPU_SAMPLE_N, CPU_SAMPLE_N, CPU_SAMPLE_N)
+    scale = nc_full / nc_s
+    times, iters = reference_step_seconds(CPU_SAMPLE_N, args.method, args.warmup + args.steps)
+    timed = times[args.warmup:]
+    v = statistics.mean(timed) * scale
+    sample = (f"reference SolvePipeline::solve (EngineCsr, replace branch, GMRES+AMG to 1e-8, {iters} its) on the "
+              f"{CPU_SAMPLE_N}^3 instance of the same generator, {statistics.mean(timed):.3f} s/call, scaled by the "
+              f"row ratio {scale:.2f} to {args.size}^3")
+    print(json.dumps({
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"5x5 density-based hex {args.size}^3 (BASELINE configs[1])", "method": args.method,
+                   "precond": "AMG(maxLevels 30, minCoarseRows 8, DILU 1/1)", "rel_tol": 1e-8},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "reference", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# --------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+
+    from paper_2403_07882_b200 import bcs, gen
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n = args.size
+
+    def pinned(size, dt):
+        t = torch.empty(size, dtype=torch.float64 if dt == np.float64 else torch.int32, pin_memory=True)
+        return t.numpy()
+
+    s = gen.hex_euler(n, alloc=pinned)
+    A, b, x0 = s.A, s.b, s.x0
+    nc, nf, nb = A.n_cells, A.nFaces(), A.n
+    cfg = solver_config(args.method)
+
+    ctx = bcs.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    d_diag = torch.from_numpy(A.diag).to(dev)
+    d_up = torch.from_numpy(A.upper).to(dev)
+    d_lo = torch.from_numpy(A.lower).to(dev)
+    d_b = torch.from_numpy(b.values).to(dev)
+    d_x = torch.zeros(nc * nb, dtype=torch.float64, device=dev)
+    ctx.set_topology(A)
+
+    def step():
+        ctx.upload_ldu_device(d_diag.data_ptr(), d_up.data_ptr(), d_lo.data_ptr())
+        d_x.zero_()
+        return ctx.solve_device(d_b.data_ptr(), d_x.data_ptr(), cfg)
+
+    for _ in range(max(args.warmup, 3)):
+        rep = step()
+    ctx.set_kernel_timing(True)
+    reps = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            reps.append(step())
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ctx.set_kernel_timing(False)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    # residual check of the last solve (independent: ||b - A x|| via the BSR SpMV)
+    x_host = d_x.cpu().numpy()
+    true_res = ctx.residual(b.values, x_host)
+    last = reps[-1]
+
+    # SpMV roofline from the launches inside the timed region
+    spmv_ms = sum(r.spmvMs for r in reps) / max(1, sum(r.spmvLaunches for r in reps))
+    bytes_per = spmv_bytes(nc, nf, nb)
+    peak, peak_kind = peaks()
+    achieved = bytes_per / (spmv_ms * 1e-3) / 1e9
+    launches = sum(r.kernelLaunches for r in reps) + args.steps  # + one value-permutation kernel per step
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "spmv_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(f"{n}")
+        except Exception:
+            traffic = None
+
+    # e2e through the drop-in ABI call with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        pipe = bcs.SolvePipeline(local)
+        pipe.solve(A, b, x0, bcs.Backend.EngineCsr, cfg)  # setup branch
+        times = []
+        for _ in range(args.steps):
+            if world > 1:
+                torch.distributed.barrier()
+            t0 = time.perf_counter()
+            xo, r = pipe.solve(A, b, x0, bcs.Backend.EngineCsr, cfg)
+            times.append(time.perf_counter() - t0)
+        e_s = statistics.mean(times)
+        if world > 1:
+            t = torch.tensor([e_s], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e_s = float(t.item())
+        h2d = (A.diag.nbytes + A.upper.nbytes + A.lower.nbytes + b.values.nbytes + x0.values.nbytes)
+        e2e = {"value": e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(nc * nb * 8),
+               "iterations": r.iterations, "stage_s": {k: round(v, 6) for k, v in r.timings.items()}}
+        pipe.ctx.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            times, its = reference_step_seconds(CPU_SAMPLE_N, args.method, 1)
+            scale = nc / gen.hex_sizes(CPU_SAMPLE_N, CPU_SAMPLE_N, CPU_SAMPLE_N)[0]
+            cpu = {"value": times[0] * scale, "unit": UNIT, "cores": 1, "kind": "reference",
+                   "sample": f"one replace-branch reference SolvePipeline::solve on the {CPU_SAMPLE_N}^3 instance "
+                             f"({times[0]:.2f} s, {its} its) x row ratio {scale:.2f}"}
+        except Exception as e:  # reference lib absent: fall back to the C restatement (port)
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": ms / 1e3, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"5x5 density-based hex {n}^3 (BASELINE configs[1]), {nc} cells, "
+                                   f"{nc + 2 * nf} blocks per GPU",
+                       "method": args.method, "precond": "AMG(maxLevels 30, minCoarseRows 8, DILU 1/1)",
+                       "rel_tol": 1e-8, "x0": "zero",
+                       "l2": "inputs (2.9 GB BSR values) exceed the 126 MB L2; no flush needed",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "iterations": last.iterations, "amg_levels": last.amgLevels, "coarse_rows": last.coarseRows,
+            "final_rel_residual": last.finalResidual / last.initialResidual,
+            "true_rel_residual_check": true_res / last.initialResidual,
+            "stage_s": {"amg_setup": last.timings.get("amgSetup"), "krylov": last.timings.get("krylov")},
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_spmv<5> (fine level)",
+                         "bytes_per_launch": bytes_per, "mean_launch_ms": spmv_ms, "peak_kind": peak_kind},
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk.summary(),
+        }
+        print(json.dumps(out), flush=True)
+    ctx.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -623,8 +623,23 @@ static void precond_free(Precond* p) {
 }
 
 /* ----------------------------------------------------------------- Krylov */
-/* defaultDot (krylov.cpp:38-42) */
+/* defaultDot (krylov.cpp:38-42).  Mode 1 (or_set_dot_mode) re-associates the
+ * same sum pairwise over 256-element chunks: a reference-equivalent variant
+ * used only to measure how strongly a Krylov history amplifies last-bit
+ * differences of the reductions (tests/test_gpu_parity.py). */
+static int g_dot_mode = 0;
+void or_set_dot_mode(int mode) { g_dot_mode = mode; }
+static double dot_pairwise(const double* a, const double* b, size_t n) {
+    if (n <= 256) {
+        double s = 0.0;
+        for (size_t i = 0; i < n; ++i) s += a[i] * b[i];
+        return s;
+    }
+    const size_t h = (n / 2 + 255) / 256 * 256;
+    return dot_pairwise(a, b, h) + dot_pairwise(a + h, b + h, n - h);
+}
 static double dotp(const double* a, const double* b, size_t n) {
+    if (g_dot_mode == 1) return dot_pairwise(a, b, n);
     double s = 0.0;
     for (size_t i = 0; i < n; ++i) s += a[i] * b[i];
     return s;

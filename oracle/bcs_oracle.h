@@ -44,6 +44,8 @@ typedef struct {
 } or_report;
 
 const char* or_last_error(void);
+/* 0: reference sequential dot (default); 1: pairwise re-association */
+void or_set_dot_mode(int mode);
 
 /* block_csr.cpp:56-80 — src[k] encodes the LDU source of slot k:
  * c (diag of cell c), nc+f (upper of face f), nc+nf+f (lower of face f). */

@@ -25,6 +25,9 @@
 #include "blockfv/partition.hpp"
 #include "blockfv/preconditioner.hpp"
 
+// the reference test suite's own fixtures (tests/support/test_helpers.hpp)
+#include "support/test_helpers.hpp"
+
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -332,37 +335,66 @@ int ref_gen_coupled(int nx, int ny, int nz, double aspect, long long scrambleSee
     });
 }
 
-// Random diagonally dominant system on caller topology (test_helpers.hpp:47-70 shape).
+// testsup::randomize (tests/support/test_helpers.hpp:47-70) on caller topology.
 int ref_randomize(int nc, int nf, int n, const int* owner, const int* neigh, unsigned seed, double diagBoost,
                   double* diag, double* upper, double* lower) {
     return guard([&] {
         const auto mesh = topoMesh(nc, nf, owner, neigh, nullptr);
         BlockLduMatrix A(*mesh, varsFor(n));
-        std::mt19937 gen(seed);
-        std::uniform_real_distribution<double> U(-1.0, 1.0);
-        const int nn = n * n;
-        for (int f = 0; f < nf; ++f)
-            for (int k = 0; k < nn; ++k) {
-                A.upper(f)[k] = U(gen);
-                A.lower(f)[k] = U(gen);
-            }
-        std::vector<double> rowAbs(static_cast<std::size_t>(nc) * n, 0.0);
-        for (int f = 0; f < nf; ++f)
-            for (int i = 0; i < n; ++i)
-                for (int j = 0; j < n; ++j) {
-                    rowAbs[static_cast<std::size_t>(owner[f]) * n + i] += std::fabs(A.upper(f)[i * n + j]);
-                    rowAbs[static_cast<std::size_t>(neigh[f]) * n + i] += std::fabs(A.lower(f)[i * n + j]);
-                }
-        for (int c = 0; c < nc; ++c)
-            for (int i = 0; i < n; ++i)
-                for (int j = 0; j < n; ++j) {
-                    double v = U(gen);
-                    if (i == j) v = diagBoost * (rowAbs[static_cast<std::size_t>(c) * n + i] + n);
-                    A.diag(c)[i * n + j] = v;
-                }
+        std::mt19937 rng(seed);
+        testsup::randomize(A, rng, diagBoost);
+        const std::size_t nn = static_cast<std::size_t>(n) * n;
         std::memcpy(diag, A.diagValues().data(), sizeof(double) * nn * nc);
-        std::memcpy(upper, A.upperValues().data(), sizeof(double) * nn * nf);
-        std::memcpy(lower, A.lowerValues().data(), sizeof(double) * nn * nf);
+        if (nf) {
+            std::memcpy(upper, A.upperValues().data(), sizeof(double) * nn * nf);
+            std::memcpy(lower, A.lowerValues().data(), sizeof(double) * nn * nf);
+        }
+    });
+}
+
+// testsup::randomVector (tests/support/test_helpers.hpp:72-77)
+void ref_random_vector(int nc, int n, unsigned seed, double* out) {
+    std::mt19937 rng(seed);
+    const BlockVector v = testsup::randomVector(nc, n, rng);
+    std::memcpy(out, v.values.data(), sizeof(double) * v.values.size());
+}
+
+// Reference mesh generators (mesh.cpp:99-165): sizes first, then addressing.
+int ref_mesh_2d(int nx, int ny, double lx, double ly, int* nCells, int* nFaces, int* owner, int* neigh,
+                double* centroids) {
+    return guard([&] {
+        const Mesh m = generateStructured2d(nx, ny, {lx, ly, 1.0});
+        *nCells = m.nCells();
+        *nFaces = m.nInternalFaces();
+        if (owner)
+            for (int f = 0; f < m.nInternalFaces(); ++f) {
+                owner[f] = m.faces()[f].owner;
+                neigh[f] = m.faces()[f].neighbour;
+            }
+        if (centroids)
+            for (int c = 0; c < m.nCells(); ++c) {
+                centroids[3 * c] = m.cellCentroids()[c].x;
+                centroids[3 * c + 1] = m.cellCentroids()[c].y;
+                centroids[3 * c + 2] = m.cellCentroids()[c].z;
+            }
+    });
+}
+int ref_mesh_tube(int n, double length, int* nCells, int* nFaces, int* owner, int* neigh, double* centroids) {
+    return guard([&] {
+        const Mesh m = generate1dTube(n, length);
+        *nCells = m.nCells();
+        *nFaces = m.nInternalFaces();
+        if (owner)
+            for (int f = 0; f < m.nInternalFaces(); ++f) {
+                owner[f] = m.faces()[f].owner;
+                neigh[f] = m.faces()[f].neighbour;
+            }
+        if (centroids)
+            for (int c = 0; c < m.nCells(); ++c) {
+                centroids[3 * c] = m.cellCentroids()[c].x;
+                centroids[3 * c + 1] = m.cellCentroids()[c].y;
+                centroids[3 * c + 2] = m.cellCentroids()[c].z;
+            }
     });
 }
 

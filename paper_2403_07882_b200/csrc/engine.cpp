@@ -98,6 +98,10 @@ Engine::~Engine() {
     if (hStatus_) cudaFreeHost(hStatus_);
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
+    for (auto& e : evPool_) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
     if (own_) cudaStreamDestroy(own_);
 }
 
@@ -197,18 +201,32 @@ void Engine::requireMatrix() const {
     if (!hasTopo_ || !hasValues_) throw std::invalid_argument("bcs: no matrix uploaded");
 }
 
+// Fine-level SpMV launches are bracketed by CUDA events on the launching
+// stream when kernel timing is on; the pairs are read after the solve's final
+// synchronisation, so timing never adds a host sync inside the solve.
 void Engine::spmvLevel(const Level& L, const double* x, const double* sub, double* y) {
     const bool timed = kernelTiming_ && &L == &levels_[0];
-    if (timed) cudaEventRecord(ev0_, stream_);
-    spmv(n_, L.rows, L.ro, L.ci, L.v, x, sub, y, stream_);
     if (timed) {
-        cudaEventRecord(ev1_, stream_);
-        cudaEventSynchronize(ev1_);
+        if (evUsed_ == evPool_.size()) {
+            cudaEvent_t a, b;
+            check(cudaEventCreate(&a), "cudaEventCreate");
+            check(cudaEventCreate(&b), "cudaEventCreate");
+            evPool_.push_back({a, b});
+        }
+        cudaEventRecord(evPool_[evUsed_].first, stream_);
+    }
+    spmv(n_, L.rows, L.ro, L.ci, L.v, x, sub, y, stream_);
+    if (timed) cudaEventRecord(evPool_[evUsed_++].second, stream_);
+}
+
+void Engine::collectSpmvTimes() {
+    for (size_t i = 0; i < evUsed_; ++i) {
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, ev0_, ev1_);
+        check(cudaEventElapsedTime(&ms, evPool_[i].first, evPool_[i].second), "cudaEventElapsedTime");
         spmvMs_ += ms;
         ++spmvCount_;
     }
+    evUsed_ = 0;
 }
 
 // ------------------------------------------------------------ config/setup
@@ -615,6 +633,7 @@ void Engine::solveDevice(const double* d_b, double* d_x, const bcs_solver_config
     const long long l0 = launches_.launches;
     spmvMs_ = 0.0;
     spmvCount_ = 0;
+    evUsed_ = 0;
     hist_.clear();
     cudaMemsetAsync(err_.p + 1, 0, sizeof(int), stream_);
     const auto t0 = clk::now();
@@ -625,6 +644,7 @@ void Engine::solveDevice(const double* d_b, double* d_x, const bcs_solver_config
     else bicgstab(d_b, d_x, cfg, rep);
     sync();
     const auto t2 = clk::now();
+    collectSpmvTimes();
     int spinErr = 0;
     check(cudaMemcpy(&spinErr, err_.p + 1, sizeof(int), cudaMemcpyDeviceToHost), "spin flag");
     if (spinErr) throw std::runtime_error("bcs: sweep dependency wait timed out (corrupt schedule)");
@@ -636,6 +656,7 @@ void Engine::solveDevice(const double* d_b, double* d_x, const bcs_solver_config
     rep.spmv_launches = spmvCount_;
     rep.spmv_ms = spmvMs_;
     rep.kernel_launches = static_cast<int>(launches_.launches - l0);
+    lastSolveLaunches_ = rep.kernel_launches;
 }
 
 void Engine::solveHost(const double* b, double* x, const bcs_solver_config& cfg, bcs_report& rep) {

@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace bcs {
@@ -100,6 +101,7 @@ public:
     int scheduleDepth(int l) const;
 
     cudaStream_t stream() const { return stream_; }
+    long long totalLaunches() const { return launches_.launches; }
     int blockSize() const { return n_; }
     int nCells() const { return nc_; }
 
@@ -161,7 +163,11 @@ private:
     std::vector<double> hist_;
 
     // SpMV event timing (fine level)
+    void collectSpmvTimes();
     cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evPool_;
+    size_t evUsed_ = 0;
+    int lastSolveLaunches_ = 0;
     double spmvMs_ = 0.0;
     int spmvCount_ = 0;
 };

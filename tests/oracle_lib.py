@@ -110,7 +110,14 @@ class Restatement:
             raise RuntimeError(self.err())
         return z
 
-    def solve(self, A, b, x0, cfg, hist_cap=100000):
+    def solve(self, A, b, x0, cfg, hist_cap=100000, dot_mode=0):
+        self.L.or_set_dot_mode(int(dot_mode))
+        try:
+            return self._solve(A, b, x0, cfg, hist_cap)
+        finally:
+            self.L.or_set_dot_mode(0)
+
+    def _solve(self, A, b, x0, cfg, hist_cap):
         c = OrCfg(*cfg)
         x = np.zeros_like(b)
         rep = OrReport()
@@ -262,3 +269,42 @@ class Reference:
         if rc:
             raise ValueError(self.err())
         return c2r, rro, o2n
+
+
+# --- reference test-suite fixtures (tests/support/test_helpers.hpp via ref_driver)
+def _ref_mesh(L, fn, *args):
+    nc, nf = c_int(), c_int()
+    rc = fn(*args, ctypes.byref(nc), ctypes.byref(nf), None, None, None)
+    assert rc == 0
+    owner = np.zeros(nf.value, np.int32)
+    neigh = np.zeros(nf.value, np.int32)
+    cen = np.zeros(nc.value * 3)
+    rc = fn(*args, ctypes.byref(nc), ctypes.byref(nf), ptr(owner), ptr(neigh), ptr(cen))
+    assert rc == 0
+    return nc.value, owner, neigh, cen.reshape(-1, 3)
+
+
+def ref_mesh_2d(R, nx, ny, lx=1.0, ly=1.0):
+    R.L.ref_mesh_2d.argtypes = [c_int, c_int, c_double, c_double] + [c_void_p] * 5
+    return _ref_mesh(R.L, R.L.ref_mesh_2d, nx, ny, lx, ly)
+
+
+def ref_mesh_tube(R, n, length=1.0):
+    R.L.ref_mesh_tube.argtypes = [c_int, c_double] + [c_void_p] * 5
+    return _ref_mesh(R.L, R.L.ref_mesh_tube, n, length)
+
+
+def ref_randomize(R, nc, owner, neigh, n, seed, boost=4.0):
+    R.L.ref_randomize.argtypes = [c_int, c_int, c_int, c_void_p, c_void_p, ctypes.c_uint, c_double] + [c_void_p] * 3
+    nf, nn = owner.size, n * n
+    d, u, lo = np.zeros(nc * nn), np.zeros(nf * nn), np.zeros(nf * nn)
+    rc = R.L.ref_randomize(nc, nf, n, ptr(owner), ptr(neigh), seed, boost, ptr(d), ptr(u), ptr(lo))
+    assert rc == 0
+    return d, u, lo
+
+
+def ref_random_vector(R, nc, n, seed):
+    R.L.ref_random_vector.argtypes = [c_int, c_int, ctypes.c_uint, c_void_p]
+    out = np.zeros(nc * n)
+    R.L.ref_random_vector(nc, n, seed, ptr(out))
+    return out
