@@ -11,7 +11,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdio>
+#include <cstdlib>
 #include <limits>
+#include <map>
 
 namespace bcs {
 
@@ -56,7 +59,29 @@ uint64_t topologySignatureHost(int nc, int nf, const int32_t* owner, const int32
     return h;
 }
 
+void Engine::profMark(const std::string& what) {
+    if (!prof_) return;
+    sync();
+    const auto now = clk::now();
+    profRec_.emplace_back(what, secs(profT_, now));
+    profT_ = now;
+}
+
+void Engine::profDump() {
+    if (!prof_ || profRec_.empty()) return;
+    std::map<std::string, double> agg;
+    std::map<std::string, int> cnt;
+    for (auto& [k, v] : profRec_) {
+        agg[k] += v;
+        cnt[k]++;
+    }
+    std::fprintf(stderr, "[bcs-profile] %zu marks\n", profRec_.size());
+    for (auto& [k, v] : agg) std::fprintf(stderr, "[bcs-profile] %-28s %10.3f ms  (x%d)\n", k.c_str(), v * 1e3, cnt[k]);
+    profRec_.clear();
+}
+
 Engine::Engine(int device) : device_(device) {
+    prof_ = std::getenv("BCS_PROFILE") != nullptr;
     check(cudaSetDevice(device), "cudaSetDevice");
     check(cudaStreamCreateWithFlags(&own_, cudaStreamNonBlocking), "cudaStreamCreate");
     stream_ = own_;
@@ -90,7 +115,7 @@ Engine::~Engine() {
     }
     rel(dOwner_); rel(dNeigh_); rel(ro_); rel(ci_); rel(dg_); rel(tpos_); rel(src_); rel(fill_); rel(vals_);
     rel(ldu_diag_); rel(ldu_upper_); rel(ldu_lower_); rel(dense_); rel(dpiv_); rel(cnt_); rel(lvl_); rel(push_);
-    rel(scanTmp_); rel(flag_); rel(err_); rel(ctr_); rel(choice_); rel(segOff_); rel(cro_); rel(big_); rel(dn_);
+    rel(scanTmp_); rel(act2_); rel(flag_); rel(err_); rel(ctr_); rel(choice_); rel(segOff_); rel(cro_); rel(big_); rel(dn_); rel(tblk_);
     rel(str_); rel(keys_); rel(sorted_); rel(V_); rel(w_); rel(zk_); rel(rk_); rel(H_); rel(cs_); rel(sn_); rel(g_);
     rel(y_); rel(scal_); rel(partials_); rel(kb_); rel(kx_); rel(bp_); rel(bv_); rel(bs_); rel(bt_); rel(bph_);
     rel(bsh_); rel(brh_); rel(ticket_);
@@ -252,8 +277,8 @@ void Engine::setupLevelPattern(Level& L) {
     if (readErrCell()) throw std::runtime_error("bcs: structurally asymmetric coarse pattern");
 }
 
-static KahnWork kahnWork(DArray<int>& cnt, DArray<int>& push, DArray<int>& lvl) {
-    return KahnWork{cnt.p, push.p, lvl.p};
+static KahnWork kahnWork(DArray<int>& cnt, DArray<int>& push, DArray<int>& lvl, int* lvl2 = nullptr) {
+    return KahnWork{cnt.p, push.p, lvl.p, lvl2};
 }
 
 void Engine::diluSetup(Level& L) {
@@ -265,7 +290,8 @@ void Engine::diluSetup(Level& L) {
     lvl_.ensure(static_cast<size_t>(L.rows) + 1, stream_);
     const int big = std::numeric_limits<int>::max();
     check(cudaMemcpyAsync(err_.p, &big, sizeof(int), cudaMemcpyHostToDevice, stream_), "err init");
-    L.depth = kahn_schedule(n_, L.rows, L.ro, L.ci, L.dg, L.tpos, L.v, true, L.lu.p, L.piv.p, L.order.p,
+    tblk_.ensure(static_cast<size_t>(L.nnz) * nn, stream_);
+    L.depth = kahn_schedule(n_, L.rows, L.ro, L.ci, L.dg, L.tpos, L.v, true, L.lu.p, L.piv.p, tblk_.p, L.order.p,
                             kahnWork(cnt_, push_, lvl_), err_.p, stream_);
     const int cell = readErrCell();
     if (cell != big) throw std::runtime_error("DILU setup: singular modified diagonal in cell " + std::to_string(cell));
@@ -284,8 +310,8 @@ void Engine::lusgsSetup(Level& L) {
     const int cell = readErrCell();
     if (cell != big)
         throw std::runtime_error("preconditioner setup: singular diagonal block in cell " + std::to_string(cell));
-    L.depth = kahn_schedule(n_, L.rows, L.ro, L.ci, L.dg, L.tpos, L.v, false, nullptr, nullptr, L.order.p,
-                            kahnWork(cnt_, push_, lvl_), err_.p, stream_);
+    L.depth = kahn_schedule(n_, L.rows, L.ro, L.ci, L.dg, L.tpos, L.v, false, nullptr, nullptr, nullptr,
+                            L.order.p, kahnWork(cnt_, push_, lvl_), err_.p, stream_);
 }
 
 void Engine::buildHierarchy(const bcs_solver_config& cfg) {
@@ -298,18 +324,23 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
             Level& L = levels_[l];
             dn_.ensure(L.rows, stream_);
             str_.ensure(L.nnz, stream_);
+            profMark("setup:other");
             strengths(n_, L.rows, L.ro, L.ci, L.dg, L.v, dn_.p, str_.p, stream_);
+            profMark("setup:strength");
             choice_.ensure(L.rows, stream_);
             cnt_.ensure(L.rows, stream_);
             lvl_.ensure(static_cast<size_t>(L.rows) + 1, stream_);
-            aggregate_kahn(L.rows, L.ro, L.ci, L.dg, L.tpos, str_, choice_.p, kahnWork(cnt_, push_, lvl_), err_.p,
-                           stream_);
+            act2_.ensure(static_cast<size_t>(L.rows) + 1, stream_);
+            aggregate_kahn(L.rows, L.ro, L.ci, L.dg, L.tpos, str_, choice_.p, kahnWork(cnt_, push_, lvl_, act2_.p),
+                           err_.p, stream_);
+            profMark("setup:aggregate L" + std::to_string(l) + " rounds " + std::to_string(last_agg_rounds));
             L.agg.ensure(L.rows, stream_);
             L.members.ensure(2 * static_cast<size_t>(L.rows), stream_);
             flag_.ensure(L.rows, stream_);
             scanTmp_.ensure(scan_tmp_ints(static_cast<size_t>(L.nnz) * 2 + L.rows) + 16, stream_);
             const int nC = aggregate_number(L.rows, choice_, flag_.p, L.agg.p, L.members.p, push_.p + 6,
                                             scanTmp_.p, stream_);
+            profMark("setup:aggregate_number");
             if (nC == L.rows) break;  // no coarsening possible (amg.cpp:80)
             L.ncoarse = nC;
         }
@@ -328,11 +359,14 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
         sync();
         keys_.ensure(total, stream_);
         sorted_.ensure(total, stream_);
+        profMark("galerkin:seglen+scan");
         galerkin_keys(nC, L.ro, L.ci, L.agg, L.members, segOff_, keys_.p, stream_);
+        profMark("galerkin:keys");
         big_.ensure(static_cast<size_t>(nC) + 1, stream_);
         cudaMemsetAsync(err_.p, 0, sizeof(int), stream_);
         galerkin_sort(nC, segOff_, keys_, sorted_.p, big_.p, push_.p + 7, err_.p, stream_);
         if (readErrCell()) throw std::runtime_error("bcs: Galerkin coarse row exceeds the 12288-entry sort limit");
+        profMark("galerkin:sort");
         C.o_ro.ensure(static_cast<size_t>(nC) + 1, stream_);
         galerkin_count(nC, segOff_, sorted_, C.o_ro.p, stream_);
         cudaMemsetAsync(C.o_ro.p + nC, 0, sizeof(int), stream_);
@@ -342,17 +376,24 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
         sync();
         C.rows = nC;
         C.nnz = cnnz;
+        profMark("galerkin:count+scan");
         C.o_ci.ensure(cnnz, stream_);
         C.o_v.ensure(static_cast<size_t>(cnnz) * nn, stream_);
         galerkin_fill(n_, nC, L.ro, L.members, segOff_, sorted_, L.v, C.o_ro, C.o_ci.p, C.o_v.p, stream_);
         C.ro = C.o_ro;
         C.ci = C.o_ci;
         C.v = C.o_v;
+        profMark("galerkin:fill");
         setupLevelPattern(C);
+        profMark("setup:pattern");
     }
     levels_[nlev_ - 1].ncoarse = 0;
     // DILU smoother on all but the coarsest level (amg.cpp:86-88)
-    for (int l = 0; l + 1 < nlev_; ++l) diluSetup(levels_[l]);
+    for (int l = 0; l + 1 < nlev_; ++l) {
+        diluSetup(levels_[l]);
+        profMark("setup:dilu L" + std::to_string(l) + " rows " + std::to_string(levels_[l].rows) + " depth " +
+                 std::to_string(levels_[l].depth));
+    }
     // dense factorisation of the coarsest level (amg.cpp:90-104)
     const Level& Cl = levels_[nlev_ - 1];
     m_ = Cl.rows * n_;
@@ -362,6 +403,7 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
     cudaMemsetAsync(err_.p, 0, sizeof(int), stream_);
     dense_factor(m_, dense_.p, dpiv_.p, err_.p, stream_);
     if (readErrCell()) throw std::runtime_error("singular coarse-level matrix");
+    profMark("setup:dense");
     // V-cycle vectors
     for (int l = 0; l < nlev_; ++l) {
         Level& L = levels_[l];
@@ -428,6 +470,7 @@ void Engine::vcycle(int l, const double* r, double* z) {
     const size_t N = static_cast<size_t>(L.rows) * n_;
     if (l == nlev_ - 1) {
         dense_solve(m_, dense_, dpiv_, r, z, stream_);
+        profMark("vcycle:dense_solve");
         return;
     }
     const int pre = pcCfg_.amg_pre_sweeps, post = pcCfg_.amg_post_sweeps;
@@ -438,6 +481,7 @@ void Engine::vcycle(int l, const double* r, double* z) {
             rin = L.res;
         }
         smootherApply(L, rin, z, s == 0 ? 1 : 2);
+        profMark("vcycle:presmooth L" + std::to_string(l));
     }
     const double* res = r;
     if (pre > 0) {
@@ -448,11 +492,15 @@ void Engine::vcycle(int l, const double* r, double* z) {
     }
     Level& C = levels_[l + 1];
     restrict_vec(n_, L.ncoarse, L.members, res, C.r.p, stream_);
+    profMark("vcycle:residual+restrict");
     vcycle(l + 1, C.r, C.z.p);
     prolong_vec(n_, L.rows, L.agg, C.z, z, stream_);
+    profMark("vcycle:prolong");
     for (int s = 0; s < post; ++s) {
         spmvLevel(L, z, r, L.res.p);
+        profMark("vcycle:post-spmv");
         smootherApply(L, L.res, z, 2);
+        profMark("vcycle:postsmooth L" + std::to_string(l));
     }
 }
 
@@ -637,6 +685,7 @@ void Engine::solveDevice(const double* d_b, double* d_x, const bcs_solver_config
     hist_.clear();
     cudaMemsetAsync(err_.p + 1, 0, sizeof(int), stream_);
     const auto t0 = clk::now();
+    profT_ = t0;
     buildPrecond(cfg);
     sync();
     const auto t1 = clk::now();
@@ -645,6 +694,7 @@ void Engine::solveDevice(const double* d_b, double* d_x, const bcs_solver_config
     sync();
     const auto t2 = clk::now();
     collectSpmvTimes();
+    profDump();
     int spinErr = 0;
     check(cudaMemcpy(&spinErr, err_.p + 1, sizeof(int), cudaMemcpyDeviceToHost), "spin flag");
     if (spinErr) throw std::runtime_error("bcs: sweep dependency wait timed out (corrupt schedule)");

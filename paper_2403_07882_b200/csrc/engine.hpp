@@ -150,8 +150,8 @@ private:
     DArray<int> dpiv_;
     int m_ = 0;
     // scratch
-    DArray<int> cnt_, lvl_, push_, scanTmp_, flag_, err_, ctr_, choice_, segOff_, cro_, big_;
-    DArray<double> dn_, str_;
+    DArray<int> cnt_, lvl_, act2_, push_, scanTmp_, flag_, err_, ctr_, choice_, segOff_, cro_, big_;
+    DArray<double> dn_, str_, tblk_;
     DArray<unsigned long long> keys_, sorted_;
 
     // Krylov workspace
@@ -164,6 +164,12 @@ private:
 
     // SpMV event timing (fine level)
     void collectSpmvTimes();
+    // BCS_PROFILE=1: per-phase / per-level wall times (with syncs) to stderr
+    bool prof_ = false;
+    std::vector<std::pair<std::string, double>> profRec_;
+    std::chrono::steady_clock::time_point profT_;
+    void profMark(const std::string& what);
+    void profDump();
     cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evPool_;
     size_t evUsed_ = 0;

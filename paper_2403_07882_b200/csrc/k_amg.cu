@@ -72,91 +72,147 @@ void strengths(int n, int rows, const int* ro, const int* ci, const int* dg, con
 // ------------------------------------------------------------ aggregation
 constexpr int kTaken = -2;
 constexpr int kSingle = -1;
+int last_agg_rounds = 0;
 
-// number of decisions row r waits for: lower neighbours + for every upper
-// neighbour j the entries of row j with column < r.
-__global__ void k_agg_init(int rows, const int* __restrict__ ro, const int* __restrict__ ci,
-                           const int* __restrict__ dg, const int* __restrict__ tpos, int* cnt, int* order,
-                           int* push) {
+// Exact parallel greedy (lazy readiness).  A row becomes *active* once all
+// its lower neighbours are decided (1-hop Kahn counter).  An active row then
+// tries to decide with the decisions visible so far:
+//   * taken   iff a lower neighbour chose it (all of them are decided);
+//   * else it walks its upper neighbours in the reference's preference order
+//     (strength descending, column ascending == the first max of the
+//     sequential scan) and for each inspects the lower-than-r entries of that
+//     neighbour's row: if one of them chose it, it is taken (skip); if one is
+//     still undecided, the outcome is unknown and the row retries next round;
+//     otherwise it is free and becomes the partner.
+// Every conclusion drawn is one the sequential algorithm draws at time r, so
+// the result is bit-identical; the smallest undecided row always decides, so
+// the rounds terminate.  choice[r]: -3 undecided, -2 taken, -1 singleton,
+// >= 0 partner.
+constexpr int kUndecided = -3;
+
+__global__ void k_agg_init(int rows, const int* __restrict__ ro, const int* __restrict__ dg, int* cnt, int* choice,
+                           int* act, int* push) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rows) return;
-    const int d = dg[r];
-    int c = d - ro[r];
-    for (int k = d + 1; k < ro[r + 1]; ++k) c += tpos[k] - ro[ci[k]];
+    const int c = dg[r] - ro[r];
     cnt[r] = c;
-    if (c == 0) order[atomicAdd(&push[2], 1)] = r;
+    choice[r] = kUndecided;
+    if (c == 0) act[atomicAdd(&push[2], 1)] = r;
+}
+
+constexpr unsigned kAll = 0xffffffffu;
+
+// (s, k) is preferred over (s2, k2): larger strength, ties by smaller slot
+__device__ __forceinline__ bool preferred(double s, int k, double s2, int k2) {
+    return k2 < 0 || (k >= 0 && (s > s2 || (s == s2 && k < k2)));
+}
+
+// One warp decides row r (lane-parallel scans; see the comment above).
+__device__ __forceinline__ int agg_try_warp(int r, int lane, const int* __restrict__ ro, const int* __restrict__ ci,
+                                            const int* __restrict__ dg, const int* __restrict__ tpos,
+                                            const double* __restrict__ str, const int* choice) {
+    const int b = __ldg(&ro[r]), d = __ldg(&dg[r]), e = __ldg(&ro[r + 1]);
+    bool taken = false;
+    for (int k = b + lane; k < d; k += 32) taken |= __ldcg(&choice[__ldg(&ci[k])]) == r;
+    if (__any_sync(kAll, taken)) return kTaken;
+    double lastS = 0.0;
+    int lastK = -1;  // -1: nothing excluded yet
+    while (true) {
+        double bs = 0.0;
+        int bk = -1;
+        for (int k = d + 1 + lane; k < e; k += 32) {
+            const double sv = __ldg(&str[k]);
+            if (!(sv > -1.0)) continue;  // NaN never wins (reference: s > best)
+            if (lastK >= 0 && !(sv < lastS || (sv == lastS && k > lastK))) continue;
+            if (preferred(sv, k, bs, bk)) {
+                bs = sv;
+                bk = k;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double os = __shfl_xor_sync(kAll, bs, o);
+            const int ok = __shfl_xor_sync(kAll, bk, o);
+            if (preferred(os, ok, bs, bk)) {
+                bs = os;
+                bk = ok;
+            }
+        }
+        if (bk < 0) return kSingle;
+        lastS = bs;
+        lastK = bk;
+        const int j = __ldg(&ci[bk]);
+        const int tp = __ldg(&tpos[bk]);
+        bool tk = false, unk = false;
+        for (int kk = __ldg(&ro[j]) + lane; kk < tp; kk += 32) {
+            const int c = __ldcg(&choice[__ldg(&ci[kk])]);
+            tk |= c == j;
+            unk |= c == kUndecided;
+        }
+        if (__any_sync(kAll, tk)) continue;
+        if (__any_sync(kAll, unk)) return kUndecided;
+        return j;
+    }
 }
 
 template <bool GRID>
-__global__ void __launch_bounds__(256) k_agg_kahn(int rows, const int* __restrict__ ro, const int* __restrict__ ci,
-                                                  const int* __restrict__ dg, const int* __restrict__ tpos,
-                                                  const double* __restrict__ str, int* choice, int* cnt,
-                                                  int* order, int* push, int* out) {
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int nth = gridDim.x * blockDim.x;
-    int head = 0, level = 0;
+__global__ void __launch_bounds__(256) k_agg_rounds(int rows, const int* __restrict__ ro, const int* __restrict__ ci,
+                                                    const int* __restrict__ dg, const int* __restrict__ tpos,
+                                                    const double* __restrict__ str, int* choice, int* cnt,
+                                                    int* actA, int* actB, int* push, int* out) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    int round = 0;
+    int* cur = actA;
+    int* nxt = actB;
     while (true) {
-        const int c = __ldcg(&push[(level + 2) % 3]);
-        const int end = head + c;
+        const int c = __ldcg(&push[(round + 2) % 3]);
         if (c == 0) break;
-        if (blockIdx.x == 0 && threadIdx.x == 0) push[(level + 1) % 3] = 0;
-        for (int t = head + tid; t < end; t += nth) {
-            const int r = __ldcg(&order[t]);
-            const int b = ro[r], d = dg[r], e = ro[r + 1];
-            // (a) taken by a lower neighbour?
-            bool taken = false;
-            for (int k = b; k < d; ++k)
-                if (__ldcg(&choice[ci[k]]) == r) taken = true;
-            int decision = kTaken;
-            if (!taken) {
-                int best = -1;
-                double bs = -1.0;
-                for (int k = d + 1; k < e; ++k) {
-                    const int j = ci[k];
-                    bool freej = true;
-                    const int tp = tpos[k];
-                    for (int kk = ro[j]; kk < tp; ++kk)
-                        if (__ldcg(&choice[ci[kk]]) == j) {
-                            freej = false;
-                            break;
-                        }
-                    if (freej) {
-                        const double sv = str[k];
-                        if (sv > bs) {
-                            bs = sv;
-                            best = j;
-                        }
-                    }
-                }
-                decision = best >= 0 ? best : kSingle;
+        if (blockIdx.x == 0 && threadIdx.x == 0) push[(round + 1) % 3] = 0;
+        int* pc = &push[round % 3];
+        for (int t = warp; t < c; t += nw) {
+            const int r = __ldcg(&cur[t]);
+            const int dec = agg_try_warp(r, lane, ro, ci, dg, tpos, str, choice);
+            if (dec == kUndecided) {
+                if (lane == 0) nxt[atomicAdd(pc, 1)] = r;
+                continue;
             }
-            choice[r] = decision;
-            __threadfence();
-            // release dependants
-            for (int k = d + 1; k < e; ++k) {
-                const int j = ci[k];
-                if (atomicSub(&cnt[j], 1) == 1) order[end + atomicAdd(&push[level % 3], 1)] = j;
-                const int dj = dg[j];
-                for (int kk = tpos[k] + 1; kk < dj; ++kk) {
-                    const int q = ci[kk];
-                    if (atomicSub(&cnt[q], 1) == 1) order[end + atomicAdd(&push[level % 3], 1)] = q;
+            if (lane == 0) atomicExch(&choice[r], dec);
+            const int ub = __ldg(&dg[r]) + 1, ue = __ldg(&ro[r + 1]);
+            for (int kb = ub; kb < ue; kb += 32) {
+                const int k = kb + lane;
+                bool ready = false;
+                int j = 0;
+                if (k < ue) {
+                    j = __ldg(&ci[k]);
+                    ready = atomicSub(&cnt[j], 1) == 1;
+                }
+                const unsigned m = __ballot_sync(kAll, ready);
+                if (m) {
+                    int base = 0;
+                    if (lane == 0) base = atomicAdd(pc, __popc(m));
+                    base = __shfl_sync(kAll, base, 0);
+                    if (ready) nxt[base + __popc(m & ((1u << lane) - 1u))] = j;
                 }
             }
         }
-        head = end;
-        ++level;
+        int* tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+        ++round;
         if (GRID) {
-            __threadfence();
             cg::this_grid().sync();
         } else {
-            __threadfence_block();
             __syncthreads();
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        out[0] = level;
-        out[1] = head;
-    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = round;
+}
+
+__global__ void k_agg_check(int rows, const int* choice, int* out) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < rows && choice[r] == kUndecided) atomicAdd(&out[1], 1);
 }
 
 void aggregate_kahn(int rows, const int* ro, const int* ci, const int* dg, const int* tpos, const double* str,
@@ -164,32 +220,36 @@ void aggregate_kahn(int rows, const int* ro, const int* ci, const int* dg, const
     if (rows <= 0) return;
     int* push = w.tail;  // push[3] + out[2]
     cudaMemsetAsync(push, 0, 5 * sizeof(int), s);
-    k_agg_init<<<(rows + 255) / 256, 256, 0, s>>>(rows, ro, ci, dg, tpos, w.cnt, w.lvl, push);
+    int* actA = w.lvl;
+    int* actB = w.lvl2;
+    k_agg_init<<<(rows + 255) / 256, 256, 0, s>>>(rows, ro, dg, w.cnt, choice, actA, push);
     count_launch();
-    int* order = w.lvl;
     int* out = push + 3;
     if (rows <= 8192) {
-        k_agg_kahn<false><<<1, 256, 0, s>>>(rows, ro, ci, dg, tpos, str, choice, w.cnt, order, push, out);
+        k_agg_rounds<false><<<1, 256, 0, s>>>(rows, ro, ci, dg, tpos, str, choice, w.cnt, actA, actB, push, out);
     } else {
         static int bps = 0;
         if (!bps) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_agg_kahn<true>, 256, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_agg_rounds<true>, 256, 0);
             if (bps < 1) bps = 1;
         }
         int grid = num_sms() * bps;
-        const int need = (rows + 255) / 256;
+        const int need = (rows + 7) / 8;
         if (grid > need) grid = need;
-        void* args[] = {(void*)&rows, (void*)&ro,     (void*)&ci,    (void*)&dg,   (void*)&tpos, (void*)&str,
-                        (void*)&choice, (void*)&w.cnt, (void*)&order, (void*)&push, (void*)&out};
-        cudaError_t e = cudaLaunchCooperativeKernel((void*)k_agg_kahn<true>, dim3(grid), dim3(256), args, 0, s);
+        void* args[] = {(void*)&rows, (void*)&ro,   (void*)&ci,   (void*)&dg,   (void*)&tpos, (void*)&str,
+                        (void*)&choice, (void*)&w.cnt, (void*)&actA, (void*)&actB, (void*)&push, (void*)&out};
+        cudaError_t e = cudaLaunchCooperativeKernel((void*)k_agg_rounds<true>, dim3(grid), dim3(256), args, 0, s);
         if (e != cudaSuccess)
             throw std::runtime_error(std::string("cooperative launch failed: ") + cudaGetErrorString(e));
     }
     count_launch();
+    k_agg_check<<<(rows + 255) / 256, 256, 0, s>>>(rows, choice, out);
+    count_launch();
     int h[2] = {0, 0};
     cudaMemcpyAsync(h, out, sizeof h, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
-    if (h[1] != rows) throw std::runtime_error("aggregation: dependency graph did not cover all rows");
+    if (h[1] != 0) throw std::runtime_error("aggregation: rows left undecided (broken pattern)");
+    last_agg_rounds = h[0];
 }
 
 __global__ void k_init_flag(int rows, const int* choice, int* flag) {

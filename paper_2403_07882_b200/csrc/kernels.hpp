@@ -49,11 +49,15 @@ void factor_diag_blocks(int n, int rows, const int* dg, const double* v, double*
 // order (rows) receives the level-sorted row permutation; returns depth.
 struct KahnWork {
     int* cnt;    // rows
-    int* tail;   // 1
-    int* lvl;    // rows+1 (level offsets into order)
+    int* tail;   // >= 5 ints of counters
+    int* lvl;    // rows+1 (level offsets into order / active list A)
+    int* lvl2;   // rows (active list B, aggregation only)
 };
+extern int last_agg_rounds;  // rounds of the last aggregation (diagnostics)
+// T: scratch of nnz*n*n doubles (producer-side D~_j^{-1} A_ji blocks), DILU only
 int kahn_schedule(int n, int rows, const int* ro, const int* ci, const int* dg, const int* tpos, const double* v,
-                  bool dilu, double* lu, int* piv, int* order, KahnWork w, int* err_cell, cudaStream_t s);
+                  bool dilu, double* lu, int* piv, double* T, int* order, KahnWork w, int* err_cell,
+                  cudaStream_t s);
 // sync-free sweeps (preconditioner.cpp:128-156 / :29-57). y, zb pre-filled
 // with the pending pattern (0xFF bytes).  accumulate: 0 none, 1 z = 0 + zb,
 // 2 z += zb.
