@@ -146,6 +146,11 @@ bcs_status bcs_amg_level_get(bcs_ctx* ctx, int level, int32_t* row_offsets, int3
  * dependency levels of its lower-triangular DAG (critical path). */
 bcs_status bcs_level_schedule_depth(bcs_ctx* ctx, int level, int* depth);
 
+/* Device self-tests (diagnostics).  what = 0: the sweeps' reciprocal-based
+ * exact division against IEEE __ddiv_rn on n random operand pairs; *result =
+ * number of bit mismatches (must be 0). */
+bcs_status bcs_selftest(int what, unsigned long long n, unsigned long long seed, unsigned long long* result);
+
 #ifdef __cplusplus
 }
 #endif

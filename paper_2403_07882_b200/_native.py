@@ -103,6 +103,7 @@ SIGNATURES = {
     "bcs_amg_level_sizes": (c_int, [c_void_p, c_int, P(c_int), P(c_int)]),
     "bcs_amg_level_get": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "bcs_level_schedule_depth": (c_int, [c_void_p, c_int, P(c_int)]),
+    "bcs_selftest": (c_int, [c_int, ctypes.c_ulonglong, ctypes.c_ulonglong, P(ctypes.c_ulonglong)]),
 }
 
 GEN_SIGNATURES = {

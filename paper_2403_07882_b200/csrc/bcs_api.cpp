@@ -215,4 +215,13 @@ bcs_status bcs_level_schedule_depth(bcs_ctx* ctx, int level, int* depth) {
     });
 }
 
+bcs_status bcs_selftest(int what, unsigned long long n, unsigned long long seed, unsigned long long* result) {
+    return guarded(nullptr, [&] {
+        if (what != 0) throw std::invalid_argument("bcs_selftest: unknown test");
+        const unsigned long long bad = bcs::selftest_division(n, seed);
+        bcs::check(cudaDeviceSynchronize(), "selftest");
+        if (result) *result = bad;
+    });
+}
+
 }  // extern "C"

@@ -56,7 +56,7 @@ struct Level {
     DArray<int> o_ro, o_ci, o_dg, o_tpos;
     DArray<double> o_v;
     // smoother (DILU or LUSGS) factors + level-sorted schedule
-    DArray<double> lu;
+    DArray<double> lu, rcp;
     DArray<int> piv, order;
     int depth = 0;
     // aggregation to level+1

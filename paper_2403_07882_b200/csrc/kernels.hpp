@@ -60,13 +60,16 @@ int kahn_schedule(int n, int rows, const int* ro, const int* ci, const int* dg, 
                   cudaStream_t s);
 // sync-free sweeps (preconditioner.cpp:128-156 / :29-57). y, zb pre-filled
 // with the pending pattern (0xFF bytes).  accumulate: 0 none, 1 z = 0 + zb,
-// 2 z += zb.
-void sweep_forward(int n, int rows, const int* order, const int* ro, const int* ci, const int* dg, const double* v,
-                   const double* lu, const int* piv, const double* r, double* y, int* ctr, int* err,
-                   cudaStream_t s);
-void sweep_backward(int n, int rows, const int* order, const int* ro, const int* ci, const int* dg,
-                    const double* v, const double* lu, const int* piv, const double* y, double* zb, double* z,
-                    int accumulate, int* ctr, int* err, cudaStream_t s);
+// 2 z += zb.  rcp: per-row diagonal reciprocals (make_reciprocals).
+void make_reciprocals(int n, int rows, const double* lu, double* rcp, cudaStream_t s);
+void sweep_forward(int n, int rows, int depth, const int* order, const int* ro, const int* ci, const int* dg,
+                   const double* v, const double* lu, const int* piv, const double* rcp, const double* r, double* y,
+                   int* err, cudaStream_t s);
+void sweep_backward(int n, int rows, int depth, const int* order, const int* ro, const int* ci, const int* dg,
+                    const double* v, const double* lu, const int* piv, const double* rcp, const double* y,
+                    double* zb, double* z, int accumulate, int* err, cudaStream_t s);
+// number of mismatches of the reciprocal-based division against __ddiv_rn
+unsigned long long selftest_division(unsigned long long n, unsigned long long seed);
 
 // ------------------------------------------------------------ AMG (K9-K12)
 void strengths(int n, int rows, const int* ro, const int* ci, const int* dg, const double* v, double* dn,
