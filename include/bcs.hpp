@@ -1,0 +1,121 @@
+// bcs.hpp — header-only C++ drop-in over the C ABI (bcs.h).
+//
+// bcs::SolvePipeline has the reference's signature
+//     std::pair<BlockVector, SolveReport>
+//     fvb::SolvePipeline::solve(const BlockLduMatrix&, const BlockVector&,
+//                               const BlockVector&, Backend, const SolverConfig&)
+// (proj/core/include/blockfv/engine.hpp:28-38, engine.cpp:47-120) and accepts
+// the reference's own types (or any types with the same members), so a
+// LinearSolveFn (euler.hpp:116-117 / incompressible.hpp:68-69) can switch to
+// the B200 by changing one line.  Errors are rethrown with
+// the reference's exception types and message text.
+#pragma once
+
+#include "bcs.h"
+
+#include <cstdint>
+#include <map>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace bcs {
+
+inline void throwStatus(bcs_status st, const char* msg) {
+    const std::string m = msg ? msg : "";
+    switch (st) {
+        case BCS_OK: return;
+        case BCS_INVALID_ARGUMENT: throw std::invalid_argument(m);
+        case BCS_OUT_OF_MEMORY: throw std::bad_alloc();
+        default: throw std::runtime_error(m);
+    }
+}
+
+// Reference enums are mapped by value: KrylovMethod{GMRES, PBiCGStab},
+// PrecondKind{none, LUSGS, DILU, AMG}, Backend{HostLdu, EngineCsr}.
+template <class Config>
+bcs_solver_config toC(const Config& cfg) {
+    bcs_solver_config c;
+    bcs_default_config(&c);
+    c.method = static_cast<int>(cfg.method);
+    c.precond = static_cast<int>(cfg.preconditioner);
+    c.rel_tol = cfg.relTol;
+    c.abs_tol = cfg.absTol;
+    c.max_iters = cfg.maxIters;
+    c.gmres_restart = cfg.gmresRestart;
+    c.amg_max_levels = cfg.amg.maxLevels;
+    c.amg_min_coarse_rows = cfg.amg.minCoarseRows;
+    c.amg_pre_sweeps = cfg.amg.preSweeps;
+    c.amg_post_sweeps = cfg.amg.postSweeps;
+    return c;
+}
+
+// Fills a reference-shaped SolveReport (krylov.hpp:39-50).
+template <class Report>
+Report fromC(const bcs_report& r, bool hostBackend) {
+    Report out;
+    out.iterations = r.iterations;
+    out.initialResidual = r.initial_residual;
+    out.finalResidual = r.final_residual;
+    out.converged = r.converged != 0;
+    out.breakdown = r.breakdown != 0;
+    out.timings["convert"] = r.t_convert;
+    out.timings["setup"] = r.t_setup;
+    if (!hostBackend) out.timings["replace"] = r.t_replace;
+    out.timings["solve"] = r.t_solve;
+    out.timings["retrieve"] = r.t_retrieve;
+    return out;
+}
+
+class SolvePipeline {
+public:
+    explicit SolvePipeline(int device = 0) {
+        const bcs_status st = bcs_create(&ctx_, device);
+        if (st != BCS_OK) throwStatus(st, bcs_last_error(nullptr));
+    }
+    ~SolvePipeline() { bcs_destroy(ctx_); }
+    SolvePipeline(const SolvePipeline&) = delete;
+    SolvePipeline& operator=(const SolvePipeline&) = delete;
+
+    template <class Report, class Matrix, class Vector, class Backend, class Config>
+    std::pair<Vector, Report> solve(const Matrix& A, const Vector& b, const Vector& x0, Backend backend,
+                                    const Config& cfg) {
+        if (b.blockSize != A.blockSize() || x0.blockSize != A.blockSize() || b.nCells() != A.nCells() ||
+            x0.nCells() != A.nCells())
+            throw std::invalid_argument("SolvePipeline::solve: dimension mismatch");
+        // the mesh is immutable (block_matrix.hpp:81): addressing is refreshed
+        // only when the matrix refers to a different mesh object
+        const void* mesh = &A.mesh();
+        if (mesh != mesh_ || static_cast<int>(owner_.size()) != A.nFaces()) {
+            const auto& faces = A.mesh().faces();
+            owner_.resize(faces.size());
+            neigh_.resize(faces.size());
+            for (std::size_t f = 0; f < faces.size(); ++f) {
+                owner_[f] = faces[f].owner;
+                neigh_[f] = faces[f].neighbour;
+            }
+            mesh_ = mesh;
+        }
+        Vector x(A.nCells(), A.blockSize());
+        const bcs_solver_config c = toC(cfg);
+        bcs_report r{};
+        const int be = static_cast<int>(backend);
+        const bcs_status st = bcs_pipeline_solve(
+            ctx_, A.nCells(), A.nFaces(), A.blockSize(), owner_.data(), neigh_.data(), A.diagValues().data(),
+            A.upperValues().data(), A.lowerValues().data(), b.values.data(), b.values.size(), x0.values.data(),
+            x0.values.size(), x.values.data(), be, &c, &r);
+        if (st != BCS_OK) throwStatus(st, bcs_last_error(ctx_));
+        return {std::move(x), fromC<Report>(r, be == BCS_BACKEND_HOST_LDU)};
+    }
+
+    bcs_ctx* handle() const { return ctx_; }
+
+private:
+    bcs_ctx* ctx_ = nullptr;
+    const void* mesh_ = nullptr;
+    std::vector<int32_t> owner_, neigh_;
+};
+
+}  // namespace bcs

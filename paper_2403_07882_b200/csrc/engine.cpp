@@ -110,7 +110,7 @@ Engine::~Engine() {
     // free explicitly to keep long-lived processes lean
     auto rel = [&](auto& a) { a.release(stream_); };
     for (auto& L : levels_) {
-        rel(L.o_ro); rel(L.o_ci); rel(L.o_dg); rel(L.o_tpos); rel(L.o_v); rel(L.lu); rel(L.rcp); rel(L.piv); rel(L.order);
+        rel(L.o_ro); rel(L.o_ci); rel(L.o_dg); rel(L.o_tpos); rel(L.o_v); rel(L.lu); rel(L.rcp); rel(L.recf); rel(L.recb); rel(L.piv); rel(L.order);
         rel(L.agg); rel(L.members); rel(L.r); rel(L.z); rel(L.res); rel(L.y); rel(L.zb);
     }
     rel(dOwner_); rel(dNeigh_); rel(ro_); rel(ci_); rel(dg_); rel(tpos_); rel(src_); rel(fill_); rel(vals_);
@@ -297,6 +297,9 @@ void Engine::diluSetup(Level& L) {
     if (cell != big) throw std::runtime_error("DILU setup: singular modified diagonal in cell " + std::to_string(cell));
     L.rcp.ensure(static_cast<size_t>(L.rows) * n_, stream_);
     make_reciprocals(n_, L.rows, L.lu, L.rcp.p, stream_);
+    L.recf.ensure(4 * static_cast<size_t>(L.rows), stream_);
+    L.recb.ensure(4 * static_cast<size_t>(L.rows), stream_);
+    sweep_records(L.rows, L.order, L.ro, L.dg, L.recf.p, L.recb.p, stream_);
 }
 
 void Engine::lusgsSetup(Level& L) {
@@ -316,6 +319,9 @@ void Engine::lusgsSetup(Level& L) {
                             L.order.p, kahnWork(cnt_, push_, lvl_), err_.p, stream_);
     L.rcp.ensure(static_cast<size_t>(L.rows) * n_, stream_);
     make_reciprocals(n_, L.rows, L.lu, L.rcp.p, stream_);
+    L.recf.ensure(4 * static_cast<size_t>(L.rows), stream_);
+    L.recb.ensure(4 * static_cast<size_t>(L.rows), stream_);
+    sweep_records(L.rows, L.order, L.ro, L.dg, L.recf.p, L.recb.p, stream_);
 }
 
 void Engine::buildHierarchy(const bcs_solver_config& cfg) {
@@ -463,10 +469,9 @@ void Engine::smootherApply(Level& L, const double* r, double* z, int accumulate)
     double* zb = accumulate ? L.zb.p : z;
     cudaMemsetAsync(L.y.p, 0xFF, N * sizeof(double), stream_);
     cudaMemsetAsync(zb, 0xFF, N * sizeof(double), stream_);
-    sweep_forward(n_, L.rows, L.depth, L.order, L.ro, L.ci, L.dg, L.v, L.lu, L.piv, L.rcp, r, L.y.p, err_.p + 1,
-                  stream_);
-    sweep_backward(n_, L.rows, L.depth, L.order, L.ro, L.ci, L.dg, L.v, L.lu, L.piv, L.rcp, L.y, zb, z, accumulate,
-                   err_.p + 1, stream_);
+    sweep_forward(n_, L.rows, L.depth, L.recf, L.ci, L.v, L.lu, L.piv, L.rcp, r, L.y.p, err_.p + 1, stream_);
+    sweep_backward(n_, L.rows, L.depth, L.recb, L.ci, L.v, L.lu, L.piv, L.rcp, L.y, zb, z, accumulate, err_.p + 1,
+                   stream_);
 }
 
 // AmgHierarchy::vcycle (amg.cpp:111-158)

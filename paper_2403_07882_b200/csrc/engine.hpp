@@ -57,7 +57,7 @@ struct Level {
     DArray<double> o_v;
     // smoother (DILU or LUSGS) factors + level-sorted schedule
     DArray<double> lu, rcp;
-    DArray<int> piv, order;
+    DArray<int> piv, order, recf, recb;  // recf/recb: int4 ticket records
     int depth = 0;
     // aggregation to level+1
     DArray<int> agg, members;

@@ -62,12 +62,13 @@ int kahn_schedule(int n, int rows, const int* ro, const int* ci, const int* dg, 
 // with the pending pattern (0xFF bytes).  accumulate: 0 none, 1 z = 0 + zb,
 // 2 z += zb.  rcp: per-row diagonal reciprocals (make_reciprocals).
 void make_reciprocals(int n, int rows, const double* lu, double* rcp, cudaStream_t s);
-void sweep_forward(int n, int rows, int depth, const int* order, const int* ro, const int* ci, const int* dg,
-                   const double* v, const double* lu, const int* piv, const double* rcp, const double* r, double* y,
-                   int* err, cudaStream_t s);
-void sweep_backward(int n, int rows, int depth, const int* order, const int* ro, const int* ci, const int* dg,
-                    const double* v, const double* lu, const int* piv, const double* rcp, const double* y,
-                    double* zb, double* z, int accumulate, int* err, cudaStream_t s);
+// ticket-order records (int4: row, first slot, #deps) for both sweeps
+void sweep_records(int rows, const int* order, const int* ro, const int* dg, int* fwd4, int* bwd4, cudaStream_t s);
+void sweep_forward(int n, int rows, int depth, const int* recf, const int* ci, const double* v, const double* lu,
+                   const int* piv, const double* rcp, const double* r, double* y, int* err, cudaStream_t s);
+void sweep_backward(int n, int rows, int depth, const int* recb, const int* ci, const double* v, const double* lu,
+                    const int* piv, const double* rcp, const double* y, double* zb, double* z, int accumulate,
+                    int* err, cudaStream_t s);
 // number of mismatches of the reciprocal-based division against __ddiv_rn
 unsigned long long selftest_division(unsigned long long n, unsigned long long seed);
 

@@ -1,0 +1,211 @@
+// Drop-in check with the reference's OWN types (TEST INFRASTRUCTURE).
+//
+// Built by oracle/Makefile against the read-only reference sources (its
+// headers, objects and test fixtures) and the product libbcs.so, into
+// oracle/_ref/dropin_test; run on the GPU box by tests/test_gpu_dropin.py.
+// It mirrors the reference's own tests with bcs::SolvePipeline (include/bcs.hpp)
+// substituted for fvb::SolvePipeline:
+//   * test_engine.cpp:13-38   host vs engine backends agree (1e-8)
+//   * test_engine.cpp:40-56   host backend rejects DILU/AMG (invalid_argument)
+//   * test_engine.cpp:58-93   setup branch then replace branch; same answer
+//   * test_engine.cpp:95-102  dimension mismatch -> invalid_argument
+//   * acceptance_main.cpp:105-134 (criterion 2): nonlinear residual histories of
+//     the coupled cavity (4x4) and the implicit Sod tube (5x5) over 200 outer
+//     iterations, reference EngineCsr/AMG vs B200 EngineCsr/AMG, <= 1e-6 rel.
+#include "blockfv/engine.hpp"
+#include "blockfv/euler.hpp"
+#include "blockfv/incompressible.hpp"
+#include "support/test_helpers.hpp"
+
+#include "../../include/bcs.hpp"
+
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <random>
+#include <stdexcept>
+#include <string>
+
+using namespace fvb;
+
+static int g_fail = 0;
+#define CHECK(cond, what)                                                  \
+    do {                                                                   \
+        if (!(cond)) {                                                     \
+            std::printf("FAIL %s (%s:%d)\n", what, __FILE__, __LINE__);    \
+            ++g_fail;                                                      \
+        } else {                                                           \
+            std::printf("ok   %s\n", what);                                \
+        }                                                                  \
+    } while (0)
+
+static double maxAbsDiff(const BlockVector& a, const BlockVector& b, double* scale) {
+    double s = 0.0, e = 0.0;
+    for (std::size_t i = 0; i < a.values.size(); ++i) {
+        s = std::max(s, std::fabs(a.values[i]));
+        e = std::max(e, std::fabs(a.values[i] - b.values[i]));
+    }
+    *scale = s;
+    return e;
+}
+
+int main() {
+    bcs::SolvePipeline gpu(0);
+
+    // --- test_engine.cpp:13-38 analog on the B200
+    {
+        std::mt19937 rng(51);
+        bool all = true;
+        for (int trial = 0; trial < 4; ++trial) {
+            const Mesh m = testsup::randomMesh(rng, 200);
+            BlockLduMatrix A(m, testsup::variablesFor(4));
+            testsup::randomize(A, rng);
+            const BlockVector b = testsup::randomVector(m.nCells(), 4, rng);
+            BlockVector x0(m.nCells(), 4);
+            SolverConfig cfg;
+            cfg.relTol = 1e-12;
+            cfg.maxIters = 2000;
+            bcs::SolvePipeline fresh(0);
+            const auto [xh, rh] = fresh.solve<SolveReport>(A, b, x0, Backend::HostLdu, cfg);
+            const auto [xe, re] = gpu.solve<SolveReport>(A, b, x0, Backend::EngineCsr, cfg);
+            const auto [xr, rr] = backendSolve(A, b, x0, Backend::EngineCsr, cfg);  // the reference itself
+            double sc;
+            all = all && rh.converged && re.converged && maxAbsDiff(xh, xe, &sc) <= 1e-8 * sc &&
+                  maxAbsDiff(xr, xe, &sc) <= 1e-8 * sc && std::abs(re.iterations - rr.iterations) <= 1;
+        }
+        CHECK(all, "host and engine backends agree to solver tolerance (and match the reference)");
+    }
+    // --- test_engine.cpp:40-56
+    {
+        const Mesh m = generate1dTube(4, 1.0);
+        BlockLduMatrix A(m, testsup::variablesFor(1));
+        std::mt19937 rng(1);
+        testsup::randomize(A, rng);
+        const BlockVector b = testsup::randomVector(m.nCells(), 1, rng);
+        const BlockVector x0(m.nCells(), 1);
+        SolverConfig cfg;
+        bool threw = false;
+        cfg.preconditioner = PrecondKind::DILU;
+        try {
+            gpu.solve<SolveReport>(A, b, x0, Backend::HostLdu, cfg);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw, "host backend rejects DILU with std::invalid_argument");
+        threw = false;
+        cfg.preconditioner = PrecondKind::AMG;
+        try {
+            gpu.solve<SolveReport>(A, b, x0, Backend::HostLdu, cfg);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw, "host backend rejects AMG with std::invalid_argument");
+        cfg.preconditioner = PrecondKind::DILU;
+        CHECK(gpu.solve<SolveReport>(A, b, x0, Backend::EngineCsr, cfg).second.converged,
+              "engine path accepts DILU");
+    }
+    // --- test_engine.cpp:58-93 (setup then replace)
+    {
+        std::mt19937 rng(61);
+        const Mesh m = generateStructured2d(6, 6, {1, 1, 1});
+        BlockLduMatrix A(m, testsup::variablesFor(4));
+        testsup::randomize(A, rng);
+        const BlockVector b = testsup::randomVector(m.nCells(), 4, rng);
+        BlockVector x0(m.nCells(), 4);
+        SolverConfig cfg;
+        cfg.relTol = 1e-10;
+        cfg.preconditioner = PrecondKind::AMG;
+        bcs::SolvePipeline p(0);
+        const auto [x1, r1] = p.solve<SolveReport>(A, b, x0, Backend::EngineCsr, cfg);
+        CHECK(r1.timings.at("setup") > 0.0 && r1.timings.at("replace") == 0.0, "first call takes the setup branch");
+        const auto [x2, r2] = p.solve<SolveReport>(A, b, x0, Backend::EngineCsr, cfg);
+        CHECK(r2.timings.at("replace") > 0.0 && r2.timings.at("setup") == 0.0, "second call takes the replace branch");
+        double sc;
+        CHECK(maxAbsDiff(x1, x2, &sc) <= 1e-9 * sc, "replace result equals setup result");
+    }
+    // --- test_engine.cpp:95-102
+    {
+        const Mesh m = generate1dTube(4, 1.0);
+        BlockLduMatrix A(m, testsup::variablesFor(4));
+        const BlockVector b(3, 4), x0(4, 4);
+        bool threw = false;
+        try {
+            gpu.solve<SolveReport>(A, b, x0, Backend::EngineCsr, SolverConfig{});
+        } catch (const std::invalid_argument& e) {
+            threw = std::string(e.what()).find("dimension mismatch") != std::string::npos;
+        }
+        CHECK(threw, "dimension mismatch -> std::invalid_argument");
+    }
+    // --- acceptance criterion 2 analog: nonlinear residual histories, 200 outer iterations
+    auto relDelta = [](double a, double b) {
+        const double s = std::max(std::fabs(a), std::fabs(b));
+        return s > 0.0 ? std::fabs(a - b) / s : 0.0;
+    };
+    SolverConfig lin;
+    lin.method = KrylovMethod::GMRES;
+    lin.preconditioner = PrecondKind::AMG;
+    lin.relTol = 1e-10;
+    lin.absTol = 1e-14;
+    lin.maxIters = 4000;
+    lin.gmresRestart = 60;
+    {
+        // lid-driven cavity 32x32, coupled p-U (4x4): acceptance_main.cpp:75-88
+        const Mesh m = generateStructured2d(32, 32, {1, 1, 1});
+        BcMap bcs;
+        bcs["left"] = {IncompressibleBc::Kind::wall, {}, 0.0};
+        bcs["right"] = {IncompressibleBc::Kind::wall, {}, 0.0};
+        bcs["bottom"] = {IncompressibleBc::Kind::wall, {}, 0.0};
+        bcs["top"] = {IncompressibleBc::Kind::movingWall, {1.0, 0.0, 0.0}, 0.0};
+        BlockVector sRef(m.nCells(), 4), sGpu(m.nCells(), 4);
+        FaceFluxField pRef(m.nInternalFaces(), 0.0), pGpu(m.nInternalFaces(), 0.0);
+        SolvePipeline refPipe;
+        CoupledSolveFn refSolve = [&](const BlockLduMatrix& A, const BlockVector& b, const BlockVector& x0) {
+            return refPipe.solve(A, b, x0, Backend::EngineCsr, lin);
+        };
+        CoupledSolveFn gpuSolve = [&](const BlockLduMatrix& A, const BlockVector& b, const BlockVector& x0) {
+            return gpu.solve<SolveReport>(A, b, x0, Backend::EngineCsr, lin);
+        };
+        double worst = 0.0;
+        for (int it = 0; it < 200; ++it) {
+            const IterateResult a = coupledIterate(sRef, pRef, m, 0.01, bcs, refSolve);
+            const IterateResult g = coupledIterate(sGpu, pGpu, m, 0.01, bcs, gpuSolve);
+            for (int k = 0; k < 4; ++k) worst = std::max(worst, relDelta(a.residuals[k], g.residuals[k]));
+        }
+        std::printf("     cavity32 worst residual rel delta %.3e\n", worst);
+        CHECK(worst <= 1e-6, "cavity 32^2 coupled (4x4): 200 nonlinear iterations match the reference (<=1e-6)");
+    }
+    {
+        // implicit Sod tube, 100 cells, first-order Roe, cfl ramp 1->20 over 100: acceptance_main.cpp:90-102
+        const Mesh m = generate1dTube(100, 1.0);
+        EulerCase ec;
+        ec.flux = FluxScheme::Roe;
+        ec.recon.firstOrder = true;
+        std::vector<PrimState> qRef(m.nCells()), qGpu(m.nCells());
+        for (int i = 0; i < m.nCells(); ++i) {
+            const bool left = m.cellCentroids()[i].x < 0.5;
+            qRef[i] = left ? PrimState{1.0, 0.0, 0.0, 0.0, 1.0} : PrimState{0.125, 0.0, 0.0, 0.0, 0.1};
+        }
+        qGpu = qRef;
+        PseudoTimeControl ctl;
+        ctl.startCfl = 1.0;
+        ctl.endCfl = 20.0;
+        ctl.rampIters = 100;
+        SolvePipeline refPipe;
+        LinearSolveFn refSolve = [&](const BlockLduMatrix& A, const BlockVector& b, const BlockVector& x0) {
+            return refPipe.solve(A, b, x0, Backend::EngineCsr, lin);
+        };
+        LinearSolveFn gpuSolve = [&](const BlockLduMatrix& A, const BlockVector& b, const BlockVector& x0) {
+            return gpu.solve<SolveReport>(A, b, x0, Backend::EngineCsr, lin);
+        };
+        double worst = 0.0;
+        for (int it = 0; it < 200; ++it) {
+            const EulerStepResult a = implicitStep(qRef, m, ec, ctl.cfl(it), refSolve);
+            const EulerStepResult g = implicitStep(qGpu, m, ec, ctl.cfl(it), gpuSolve);
+            for (int k = 0; k < 5; ++k) worst = std::max(worst, relDelta(a.residualNorms[k], g.residualNorms[k]));
+        }
+        std::printf("     sod100 worst residual rel delta %.3e\n", worst);
+        CHECK(worst <= 1e-6, "Sod tube implicit (5x5): 200 nonlinear iterations match the reference (<=1e-6)");
+    }
+    std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "PASSED", g_fail);
+    return g_fail ? 1 : 0;
+}
