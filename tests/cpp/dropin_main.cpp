@@ -12,6 +12,7 @@
 //   * acceptance_main.cpp:105-134 (criterion 2): nonlinear residual histories of
 //     the coupled cavity (4x4) and the implicit Sod tube (5x5) over 200 outer
 //     iterations, reference EngineCsr/AMG vs B200 EngineCsr/AMG, <= 1e-6 rel.
+#include "blockfv/case_runner.hpp"
 #include "blockfv/engine.hpp"
 #include "blockfv/euler.hpp"
 #include "blockfv/incompressible.hpp"
@@ -137,9 +138,13 @@ int main() {
         CHECK(threw, "dimension mismatch -> std::invalid_argument");
     }
     // --- acceptance criterion 2 analog: nonlinear residual histories, 200 outer iterations
-    auto relDelta = [](double a, double b) {
-        const double s = std::max(std::fabs(a), std::fabs(b));
-        return s > 0.0 ? std::fabs(a - b) / s : 0.0;
+    // histories are compared with the reference's own compareRuns
+    // (case_runner.cpp:631-676), exactly as acceptance criterion 2 does
+    auto record = [](RunReport& rr, int iter, const double* res, int n) {
+        IterationRecord rec;
+        rec.iter = iter;
+        rec.residuals.assign(res, res + n);
+        rr.history.push_back(std::move(rec));
     };
     SolverConfig lin;
     lin.method = KrylovMethod::GMRES;
@@ -165,13 +170,17 @@ int main() {
         CoupledSolveFn gpuSolve = [&](const BlockLduMatrix& A, const BlockVector& b, const BlockVector& x0) {
             return gpu.solve<SolveReport>(A, b, x0, Backend::EngineCsr, lin);
         };
-        double worst = 0.0;
+        RunReport ra, rg;
+        ra.residualNames = rg.residualNames = {"Ux", "Uy", "Uz", "p"};
         for (int it = 0; it < 200; ++it) {
             const IterateResult a = coupledIterate(sRef, pRef, m, 0.01, bcs, refSolve);
             const IterateResult g = coupledIterate(sGpu, pGpu, m, 0.01, bcs, gpuSolve);
-            for (int k = 0; k < 4; ++k) worst = std::max(worst, relDelta(a.residuals[k], g.residuals[k]));
+            record(ra, it + 1, a.residuals.data(), 4);
+            record(rg, it + 1, g.residuals.data(), 4);
         }
-        std::printf("     cavity32 worst residual rel delta %.3e\n", worst);
+        const ComparisonSummary cs = compareRuns(ra, rg);
+        const double worst = cs.maxResidualRelDelta;
+        std::printf("     cavity32 worst residual rel delta %.3e (overlap %d)\n", worst, cs.overlapIters);
         CHECK(worst <= 1e-6, "cavity 32^2 coupled (4x4): 200 nonlinear iterations match the reference (<=1e-6)");
     }
     {
@@ -197,13 +206,17 @@ int main() {
         LinearSolveFn gpuSolve = [&](const BlockLduMatrix& A, const BlockVector& b, const BlockVector& x0) {
             return gpu.solve<SolveReport>(A, b, x0, Backend::EngineCsr, lin);
         };
-        double worst = 0.0;
+        RunReport ra, rg;
+        ra.residualNames = rg.residualNames = {"rho", "rhoUx", "rhoUy", "rhoUz", "rhoE"};
         for (int it = 0; it < 200; ++it) {
             const EulerStepResult a = implicitStep(qRef, m, ec, ctl.cfl(it), refSolve);
             const EulerStepResult g = implicitStep(qGpu, m, ec, ctl.cfl(it), gpuSolve);
-            for (int k = 0; k < 5; ++k) worst = std::max(worst, relDelta(a.residualNorms[k], g.residualNorms[k]));
+            record(ra, it + 1, a.residualNorms.data(), 5);
+            record(rg, it + 1, g.residualNorms.data(), 5);
         }
-        std::printf("     sod100 worst residual rel delta %.3e\n", worst);
+        const ComparisonSummary cs = compareRuns(ra, rg);
+        const double worst = cs.maxResidualRelDelta;
+        std::printf("     sod100 worst residual rel delta %.3e (overlap %d)\n", worst, cs.overlapIters);
         CHECK(worst <= 1e-6, "Sod tube implicit (5x5): 200 nonlinear iterations match the reference (<=1e-6)");
     }
     std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "PASSED", g_fail);
