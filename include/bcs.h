@@ -148,7 +148,9 @@ bcs_status bcs_level_schedule_depth(bcs_ctx* ctx, int level, int* depth);
 
 /* Device self-tests (diagnostics).  what = 0: the sweeps' reciprocal-based
  * exact division against IEEE __ddiv_rn on n random operand pairs; *result =
- * number of bit mismatches (must be 0). */
+ * number of bit mismatches (must be 0).  what = 10..14: total ns of n cross-SM
+ * ping-pong round trips with signalling flavour what-10 (0 relaxed, 1 relaxed +
+ * fence, 2 atomic exchange, 3 volatile, 4 release/acquire). */
 bcs_status bcs_selftest(int what, unsigned long long n, unsigned long long seed, unsigned long long* result);
 
 #ifdef __cplusplus

@@ -217,6 +217,12 @@ bcs_status bcs_level_schedule_depth(bcs_ctx* ctx, int level, int* depth) {
 
 bcs_status bcs_selftest(int what, unsigned long long n, unsigned long long seed, unsigned long long* result) {
     return guarded(nullptr, [&] {
+        if (what >= 10 && what <= 14) {  // ping-pong latency, flavour what-10
+            const unsigned long long ns = bcs::selftest_pingpong(what - 10, static_cast<int>(n));
+            bcs::check(cudaDeviceSynchronize(), "selftest");
+            if (result) *result = ns;
+            return;
+        }
         if (what != 0) throw std::invalid_argument("bcs_selftest: unknown test");
         const unsigned long long bad = bcs::selftest_division(n, seed);
         bcs::check(cudaDeviceSynchronize(), "selftest");

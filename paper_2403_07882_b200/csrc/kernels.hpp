@@ -71,6 +71,8 @@ void sweep_backward(int n, int rows, int depth, const int* recb, const int* ci, 
                     int* err, cudaStream_t s);
 // number of mismatches of the reciprocal-based division against __ddiv_rn
 unsigned long long selftest_division(unsigned long long n, unsigned long long seed);
+// total ns of n ping-pong round trips between two SMs (signalling flavour `mode`)
+unsigned long long selftest_pingpong(int mode, int n);
 
 // ------------------------------------------------------------ AMG (K9-K12)
 void strengths(int n, int rows, const int* ro, const int* ci, const int* dg, const double* v, double* dn,
