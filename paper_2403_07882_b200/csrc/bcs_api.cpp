@@ -223,6 +223,10 @@ bcs_status bcs_selftest(int what, unsigned long long n, unsigned long long seed,
             if (result) *result = ns;
             return;
         }
+        if (what == 20) {  // install (n != 0: device buffer address in seed) / remove the sweep trace
+            bcs::set_sweep_trace(n ? reinterpret_cast<unsigned long long*>(seed) : nullptr);
+            return;
+        }
         if (what != 0) throw std::invalid_argument("bcs_selftest: unknown test");
         const unsigned long long bad = bcs::selftest_division(n, seed);
         bcs::check(cudaDeviceSynchronize(), "selftest");
