@@ -223,6 +223,12 @@ bcs_status bcs_selftest(int what, unsigned long long n, unsigned long long seed,
             if (result) *result = ns;
             return;
         }
+        if (what == 30 || what == 31) {  // minimal chain: n = steps, seed = warps
+            const unsigned long long ns = bcs::selftest_chain(what - 30, static_cast<int>(n), static_cast<int>(seed));
+            bcs::check(cudaDeviceSynchronize(), "selftest");
+            if (result) *result = ns;
+            return;
+        }
         if (what == 20) {  // install (n != 0: device buffer address in seed) / remove the sweep trace
             bcs::set_sweep_trace(n ? reinterpret_cast<unsigned long long*>(seed) : nullptr);
             return;
