@@ -82,6 +82,8 @@ void Engine::profDump() {
 
 Engine::Engine(int device) : device_(device) {
     prof_ = std::getenv("BCS_PROFILE") != nullptr;
+    if (const char* m = std::getenv("BCS_AGG_MODE")) aggMode_ = std::atoi(m);    // 1: barrier rounds
+    if (const char* m = std::getenv("BCS_DILU_MODE")) diluMode_ = std::atoi(m);  // 1: Kahn levels
     check(cudaSetDevice(device), "cudaSetDevice");
     check(cudaStreamCreateWithFlags(&own_, cudaStreamNonBlocking), "cudaStreamCreate");
     stream_ = own_;
@@ -286,13 +288,27 @@ void Engine::diluSetup(Level& L) {
     L.lu.ensure(L.rows * nn, stream_);
     L.piv.ensure(static_cast<size_t>(L.rows) * n_, stream_);
     L.order.ensure(L.rows, stream_);
-    cnt_.ensure(L.rows, stream_);
+    cnt_.ensure(static_cast<size_t>(L.rows) + 2, stream_);
     lvl_.ensure(static_cast<size_t>(L.rows) + 1, stream_);
+    tblk_.ensure(static_cast<size_t>(L.nnz) * nn, stream_);
     const int big = std::numeric_limits<int>::max();
     check(cudaMemcpyAsync(err_.p, &big, sizeof(int), cudaMemcpyHostToDevice, stream_), "err init");
-    tblk_.ensure(static_cast<size_t>(L.nnz) * nn, stream_);
-    L.depth = kahn_schedule(n_, L.rows, L.ro, L.ci, L.dg, L.tpos, L.v, true, L.lu.p, L.piv.p, tblk_.p, L.order.p,
-                            kahnWork(cnt_, push_, lvl_), err_.p, stream_);
+    if (diluMode_ == 0) {
+        // sync-free: dependency levels, then the factorisation in level order
+        scanTmp_.ensure(scan_tmp_ints(static_cast<size_t>(L.rows) + 2) + 16, stream_);
+        cudaMemsetAsync(err_.p + 2, 0, sizeof(int), stream_);
+        L.depth = level_schedule(L.rows, L.ro, L.ci, L.dg, L.order.p, lvl_.p, cnt_.p, scanTmp_.p, push_.p,
+                                 err_.p + 2, stream_);
+        dilu_setup_syncfree(n_, L.rows, L.order, L.ro, L.ci, L.dg, L.tpos, L.v, L.lu.p, L.piv.p, tblk_.p,
+                            static_cast<size_t>(L.nnz) * nn, err_.p, err_.p + 2, stream_);
+        int e2 = 0;
+        check(cudaMemcpyAsync(&e2, err_.p + 2, sizeof(int), cudaMemcpyDeviceToHost, stream_), "err");
+        sync();
+        if (e2) throw std::runtime_error("bcs: DILU setup dependency wait timed out");
+    } else {
+        L.depth = kahn_schedule(n_, L.rows, L.ro, L.ci, L.dg, L.tpos, L.v, true, L.lu.p, L.piv.p, tblk_.p,
+                                L.order.p, kahnWork(cnt_, push_, lvl_), err_.p, stream_);
+    }
     const int cell = readErrCell();
     if (cell != big) throw std::runtime_error("DILU setup: singular modified diagonal in cell " + std::to_string(cell));
     L.rcp.ensure(static_cast<size_t>(L.rows) * n_, stream_);
@@ -315,8 +331,11 @@ void Engine::lusgsSetup(Level& L) {
     const int cell = readErrCell();
     if (cell != big)
         throw std::runtime_error("preconditioner setup: singular diagonal block in cell " + std::to_string(cell));
-    L.depth = kahn_schedule(n_, L.rows, L.ro, L.ci, L.dg, L.tpos, L.v, false, nullptr, nullptr, nullptr,
-                            L.order.p, kahnWork(cnt_, push_, lvl_), err_.p, stream_);
+    cnt_.ensure(static_cast<size_t>(L.rows) + 2, stream_);
+    scanTmp_.ensure(scan_tmp_ints(static_cast<size_t>(L.rows) + 2) + 16, stream_);
+    cudaMemsetAsync(err_.p + 2, 0, sizeof(int), stream_);
+    L.depth = level_schedule(L.rows, L.ro, L.ci, L.dg, L.order.p, lvl_.p, cnt_.p, scanTmp_.p, push_.p, err_.p + 2,
+                             stream_);
     L.rcp.ensure(static_cast<size_t>(L.rows) * n_, stream_);
     make_reciprocals(n_, L.rows, L.lu, L.rcp.p, stream_);
     L.recf.ensure(4 * static_cast<size_t>(L.rows), stream_);
@@ -340,10 +359,17 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
             choice_.ensure(L.rows, stream_);
             cnt_.ensure(L.rows, stream_);
             lvl_.ensure(static_cast<size_t>(L.rows) + 1, stream_);
-            act2_.ensure(static_cast<size_t>(L.rows) + 1, stream_);
-            aggregate_kahn(L.rows, L.ro, L.ci, L.dg, L.tpos, str_, choice_.p, kahnWork(cnt_, push_, lvl_, act2_.p),
-                           err_.p, stream_);
-            profMark("setup:aggregate L" + std::to_string(l) + " rounds " + std::to_string(last_agg_rounds));
+            if (aggMode_ == 0) {
+                cudaMemsetAsync(err_.p, 0, sizeof(int), stream_);
+                aggregate_syncfree(L.rows, L.ro, L.ci, L.dg, L.tpos, str_, choice_.p, err_.p, stream_);
+                if (readErrCell()) throw std::runtime_error("aggregation: rows left undecided (broken pattern)");
+                profMark("setup:aggregate L" + std::to_string(l));
+            } else {
+                act2_.ensure(static_cast<size_t>(L.rows) + 1, stream_);
+                aggregate_kahn(L.rows, L.ro, L.ci, L.dg, L.tpos, str_, choice_.p,
+                               kahnWork(cnt_, push_, lvl_, act2_.p), err_.p, stream_);
+                profMark("setup:aggregate L" + std::to_string(l) + " rounds " + std::to_string(last_agg_rounds));
+            }
             L.agg.ensure(L.rows, stream_);
             L.members.ensure(2 * static_cast<size_t>(L.rows), stream_);
             flag_.ensure(L.rows, stream_);

@@ -166,6 +166,8 @@ private:
     void collectSpmvTimes();
     // BCS_PROFILE=1: per-phase / per-level wall times (with syncs) to stderr
     bool prof_ = false;
+    int aggMode_ = 0;   // 0 sync-free aggregation, 1 cooperative rounds
+    int diluMode_ = 0;  // 0 sync-free level-ordered DILU setup, 1 Kahn levels
     std::vector<std::pair<std::string, double>> profRec_;
     std::chrono::steady_clock::time_point profT_;
     void profMark(const std::string& what);

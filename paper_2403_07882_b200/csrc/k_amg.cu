@@ -210,6 +210,112 @@ __global__ void __launch_bounds__(256) k_agg_rounds(int rows, const int* __restr
     if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = round;
 }
 
+// ---- sync-free variant: thread per row, rows statically in index order.
+// Each warp loops until all of its lanes have decided; an undecided lane
+// re-evaluates with the decisions visible so far (relaxed loads).  Deadlock
+// freedom: the globally smallest undecided row sits in the current batch of
+// its (co-resident) warp and all its dependencies are decided.
+__device__ __forceinline__ int ld_choice(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ int agg_try_thread(int r, const int* __restrict__ ro, const int* __restrict__ ci,
+                                              const int* __restrict__ dg, const int* __restrict__ tpos,
+                                              const double* __restrict__ str, const int* choice) {
+    const int b = __ldg(&ro[r]), d = __ldg(&dg[r]), e = __ldg(&ro[r + 1]);
+    bool lowUndecided = false;
+    for (int k = b; k < d; ++k) {
+        const int c = ld_choice(&choice[__ldg(&ci[k])]);
+        if (c == r) return kTaken;
+        lowUndecided |= c == kUndecided;
+    }
+    if (lowUndecided) return kUndecided;
+    double lastS = 0.0;
+    int lastK = -1;
+    while (true) {
+        double bs = 0.0;
+        int bk = -1;
+        for (int k = d + 1; k < e; ++k) {
+            const double sv = __ldg(&str[k]);
+            if (!(sv > -1.0)) continue;
+            if (lastK >= 0 && !(sv < lastS || (sv == lastS && k > lastK))) continue;
+            if (bk < 0 || sv > bs) {
+                bs = sv;
+                bk = k;
+            }
+        }
+        if (bk < 0) return kSingle;
+        lastS = bs;
+        lastK = bk;
+        const int j = __ldg(&ci[bk]);
+        const int tp = __ldg(&tpos[bk]);
+        bool tk = false, unk = false;
+        for (int kk = __ldg(&ro[j]); kk < tp; ++kk) {
+            const int c = ld_choice(&choice[__ldg(&ci[kk])]);
+            if (c == j) {
+                tk = true;
+                break;
+            }
+            unk |= c == kUndecided;
+        }
+        if (tk) continue;
+        if (unk) return kUndecided;
+        return j;
+    }
+}
+
+__global__ void k_agg_fill(int rows, int* choice) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < rows) choice[r] = kUndecided;
+}
+
+__global__ void __launch_bounds__(256) k_agg_syncfree(int rows, const int* __restrict__ ro, const int* __restrict__ ci,
+                                                      const int* __restrict__ dg, const int* __restrict__ tpos,
+                                                      const double* __restrict__ str, int* choice, int* err) {
+    const int T = gridDim.x * blockDim.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int base0 = tid - (threadIdx.x & 31);
+    for (int base = base0; base < rows; base += T) {
+        const int r = base + (threadIdx.x & 31);
+        bool done = r >= rows;
+        unsigned spins = 0;
+        while (!__all_sync(0xffffffffu, done)) {
+            if (!done) {
+                const int dec = agg_try_thread(r, ro, ci, dg, tpos, str, choice);
+                if (dec != kUndecided) {
+                    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(&choice[r]), "r"(dec) : "memory");
+                    done = true;
+                }
+            }
+            if (++spins > (1u << 24)) {
+                if (!done) atomicExch(err, 1);
+                break;
+            }
+        }
+    }
+}
+
+void aggregate_syncfree(int rows, const int* ro, const int* ci, const int* dg, const int* tpos, const double* str,
+                        int* choice, int* err, cudaStream_t s) {
+    if (rows <= 0) return;
+    k_agg_fill<<<(rows + 255) / 256, 256, 0, s>>>(rows, choice);
+    static int cap = 0;
+    if (!cap) {
+        int bps = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_agg_syncfree, 256, 0);
+        cap = num_sms() * (bps < 1 ? 1 : bps);
+    }
+    int g = (rows + 255) / 256;
+    if (g > cap) g = cap;
+    void* args[] = {(void*)&rows, (void*)&ro, (void*)&ci, (void*)&dg, (void*)&tpos, (void*)&str, (void*)&choice,
+                    (void*)&err};
+    const cudaError_t e = cudaLaunchCooperativeKernel((void*)k_agg_syncfree, dim3(g), dim3(256), args, 0, s);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("aggregation launch failed: ") + cudaGetErrorString(e));
+    count_launch(2);
+}
+
 __global__ void k_agg_check(int rows, const int* choice, int* out) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r < rows && choice[r] == kUndecided) atomicAdd(&out[1], 1);

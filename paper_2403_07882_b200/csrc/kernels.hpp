@@ -58,6 +58,14 @@ extern int last_agg_rounds;  // rounds of the last aggregation (diagnostics)
 int kahn_schedule(int n, int rows, const int* ro, const int* ci, const int* dg, const int* tpos, const double* v,
                   bool dilu, double* lu, int* piv, double* T, int* order, KahnWork w, int* err_cell,
                   cudaStream_t s);
+// sync-free level schedule (rows bucketed by dependency level); returns depth.
+// level: rows ints, cnt: rows+2 ints, small: >= 3 ints
+int level_schedule(int rows, const int* ro, const int* ci, const int* dg, int* order, int* level, int* cnt,
+                   int* scan_tmp, int* small, int* err, cudaStream_t s);
+// DILU setup (preconditioner.cpp:101-126), sync-free in level order; T: tcount doubles scratch
+void dilu_setup_syncfree(int n, int rows, const int* order, const int* ro, const int* ci, const int* dg,
+                         const int* tpos, const double* v, double* lu, int* piv, double* T, size_t tcount,
+                         int* err_cell, int* err, cudaStream_t s);
 // sync-free sweeps (preconditioner.cpp:128-156 / :29-57). y, zb pre-filled
 // with the pending pattern (0xFF bytes).  accumulate: 0 none, 1 z = 0 + zb,
 // 2 z += zb.  rcp: per-row diagonal reciprocals (make_reciprocals).
@@ -82,6 +90,9 @@ void strengths(int n, int rows, const int* ro, const int* ci, const int* dg, con
 // greedy pairwise matching (amg.cpp:10-37), exact; choice[r]: -2 taken, -1 singleton, >=0 partner
 void aggregate_kahn(int rows, const int* ro, const int* ci, const int* dg, const int* tpos, const double* str,
                     int* choice, KahnWork w, int* err, cudaStream_t s);
+// same result, sync-free (no grid barriers); err set if a row could not decide
+void aggregate_syncfree(int rows, const int* ro, const int* ci, const int* dg, const int* tpos, const double* str,
+                        int* choice, int* err, cudaStream_t s);
 // numbering: agg (rows), members (2 per coarse row); returns nCoarse (sync)
 int aggregate_number(int rows, const int* choice, int* flag_tmp, int* agg, int* members, int* d_total,
                      int* scan_tmp, cudaStream_t s);
