@@ -115,6 +115,37 @@ bcs_status bcs_pipeline_solve(bcs_ctx* ctx, int n_cells, int n_faces, int block_
                               size_t x0_len, double* x, int backend, const bcs_solver_config* cfg,
                               bcs_report* report);
 
+/* ---- Mode R: the reference's distributed semantics --------------------------
+ * distributedSolve(buildPartitioned(A, decompose(mesh, n_ranks)), ...) with
+ * makeConsolidationPlan(dec, n_engines) (partition.cpp:21-479): RCB on the
+ * cell centroids (n_cells*3 doubles), rank-major renumbering, ranks
+ * consolidated onto engines, one local preconditioner per engine, global
+ * Krylov with halo couplings and the fixed pairwise engine tree for dot
+ * products.  All engines run on this context's device; b, x0 and x are in
+ * the original cell order.  Timings use the reference keys convert / setup /
+ * solve / retrieve (partition.cpp:474-477). */
+bcs_status bcs_dist_solve(bcs_ctx* ctx, int n_cells, int n_faces, int block_size, const int32_t* owner,
+                          const int32_t* neighbour, const double* centroids, const double* diag, const double* upper,
+                          const double* lower, const double* b, const double* x0, double* x, int n_ranks,
+                          int n_engines, const bcs_solver_config* cfg, bcs_report* report);
+
+/* Host-side partition layer (no device needed): decompose + buildPartitioned
+ * (+ consolidate when n_engines > 0).  Local slots and halo entries carry the
+ * id of their LDU source block: cell c -> c, upper of face f -> n_cells + f,
+ * lower of face f -> n_cells + n_faces + f. */
+typedef struct bcs_partition bcs_partition;
+bcs_status bcs_partition_create(bcs_partition** out, int n_cells, int n_faces, const int32_t* owner,
+                                const int32_t* neighbour, const double* centroids, int n_ranks, int n_engines);
+void bcs_partition_destroy(bcs_partition* p);
+int bcs_partition_count(const bcs_partition* p);
+bcs_status bcs_partition_decomposition(const bcs_partition* p, int32_t* cell_to_rank, int32_t* rank_row_offset,
+                                       int32_t* old_to_new);
+bcs_status bcs_partition_sizes(const bcs_partition* p, int part, int* row_start, int* row_end, int* nnz, int* n_halo,
+                               int* n_send);
+bcs_status bcs_partition_get(const bcs_partition* p, int part, int32_t* row_offsets, int32_t* cols, int32_t* src,
+                             int32_t* halo_row, int32_t* halo_col, int32_t* halo_peer, int32_t* halo_src,
+                             int32_t* send_peer, int32_t* send_row);
+
 /* ---- staged interface (device-resident workflows) ------------------------ */
 /* Builds the LDU->BSR plan (block_csr.cpp:56-80) on the device. */
 bcs_status bcs_set_topology(bcs_ctx* ctx, int n_cells, int n_faces, int block_size, const int32_t* owner,

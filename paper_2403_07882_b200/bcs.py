@@ -277,6 +277,72 @@ class Context:
         return x, SolveReport.from_c(rep, backend)
 
 
+    def dist_solve(self, A: BlockLduMatrix, b: BlockVector, x0: BlockVector, centroids: np.ndarray, n_ranks: int,
+                   n_engines: int, cfg: SolverConfig) -> Tuple[BlockVector, SolveReport]:
+        """Mode R: the reference's distributedSolve (partition.cpp:370-479) on this device."""
+        x = BlockVector(A.n_cells, A.n)
+        cen = np.ascontiguousarray(centroids, dtype=np.float64).reshape(-1)
+        rep = N.ReportC()
+        c = cfg.to_c()
+        self._ck(self._lib.bcs_dist_solve(self.h, A.n_cells, A.nFaces(), A.n, N.ptr(A.owner), N.ptr(A.neighbour),
+                                          N.ptr(cen), N.ptr(A.diag), N.ptr(A.upper), N.ptr(A.lower),
+                                          N.ptr(b.values), N.ptr(x0.values), N.ptr(x.values), int(n_ranks),
+                                          int(n_engines), ctypes.byref(c), ctypes.byref(rep)))
+        r = SolveReport.from_c(rep)
+        r.timings = {"convert": rep.t_convert, "setup": rep.t_setup, "solve": rep.t_solve, "retrieve": rep.t_retrieve}
+        return x, r
+
+
+class Partition:
+    """Host partition layer (decompose + buildPartitioned [+ consolidate]); no device needed."""
+
+    def __init__(self, n_cells, owner, neighbour, centroids, n_ranks, n_engines=0):
+        self._lib = N.lib()
+        self.n_cells = int(n_cells)
+        self.n_ranks = int(n_ranks)
+        o = np.ascontiguousarray(owner, np.int32)
+        nb = np.ascontiguousarray(neighbour, np.int32)
+        cen = np.ascontiguousarray(centroids, np.float64).reshape(-1)
+        h = ctypes.c_void_p()
+        st = self._lib.bcs_partition_create(ctypes.byref(h), self.n_cells, o.size, N.ptr(o), N.ptr(nb), N.ptr(cen),
+                                            self.n_ranks, int(n_engines))
+        if st != N.BCS_OK:
+            _raise(st, self._lib.bcs_last_error(None).decode())
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._lib.bcs_partition_destroy(self.h)
+            self.h = None
+
+    def count(self) -> int:
+        return int(self._lib.bcs_partition_count(self.h))
+
+    def decomposition(self):
+        c2r = np.zeros(self.n_cells, np.int32)
+        rro = np.zeros(self.n_ranks + 1, np.int32)
+        o2n = np.zeros(self.n_cells, np.int32)
+        self._lib.bcs_partition_decomposition(self.h, N.ptr(c2r), N.ptr(rro), N.ptr(o2n))
+        return c2r, rro, o2n
+
+    def part(self, i: int) -> dict:
+        rs, re, nnz, nh, ns = (ctypes.c_int() for _ in range(5))
+        st = self._lib.bcs_partition_sizes(self.h, i, ctypes.byref(rs), ctypes.byref(re), ctypes.byref(nnz),
+                                           ctypes.byref(nh), ctypes.byref(ns))
+        if st != N.BCS_OK:
+            _raise(st, self._lib.bcs_last_error(None).decode())
+        d = {"row_start": rs.value, "row_end": re.value,
+             "ro": np.zeros(re.value - rs.value + 1, np.int32), "ci": np.zeros(nnz.value, np.int32),
+             "src": np.zeros(nnz.value, np.int32), "halo_row": np.zeros(nh.value, np.int32),
+             "halo_col": np.zeros(nh.value, np.int32), "halo_peer": np.zeros(nh.value, np.int32),
+             "halo_src": np.zeros(nh.value, np.int32), "send_peer": np.zeros(ns.value, np.int32),
+             "send_row": np.zeros(ns.value, np.int32)}
+        self._lib.bcs_partition_get(self.h, i, *(N.ptr(d[k]) for k in ("ro", "ci", "src", "halo_row", "halo_col",
+                                                                        "halo_peer", "halo_src", "send_peer",
+                                                                        "send_row")))
+        return d
+
+
 def c_ptr(p) -> ctypes.c_void_p:
     return ctypes.c_void_p(int(p))
 

@@ -6,9 +6,15 @@
 #include "../../include/bcs.h"
 #include "engine.hpp"
 
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <string>
+
+struct bcs_partition {
+    bcs::Decomposition dec;
+    std::vector<bcs::Partition> parts;
+};
 
 struct bcs_ctx {
     bcs::Engine* eng = nullptr;
@@ -121,6 +127,75 @@ bcs_status bcs_pipeline_solve(bcs_ctx* ctx, int n_cells, int n_faces, int block_
         eng(ctx).pipelineSolve(n_cells, n_faces, block_size, owner, neighbour, diag, upper, lower, b, b_len, x0,
                                x0_len, x, backend, cfgOf(cfg), rep);
         if (report) *report = rep;
+    });
+}
+
+bcs_status bcs_dist_solve(bcs_ctx* ctx, int n_cells, int n_faces, int block_size, const int32_t* owner,
+                          const int32_t* neighbour, const double* centroids, const double* diag, const double* upper,
+                          const double* lower, const double* b, const double* x0, double* x, int n_ranks,
+                          int n_engines, const bcs_solver_config* cfg, bcs_report* report) {
+    return guarded(ctx, [&] {
+        bcs_report rep{};
+        eng(ctx).distSolve(n_cells, n_faces, block_size, owner, neighbour, centroids, diag, upper, lower, b, x0, x,
+                           n_ranks, n_engines, cfgOf(cfg), rep);
+        if (report) *report = rep;
+    });
+}
+
+bcs_status bcs_partition_create(bcs_partition** out, int n_cells, int n_faces, const int32_t* owner,
+                                const int32_t* neighbour, const double* centroids, int n_ranks, int n_engines) {
+    return guarded(nullptr, [&] {
+        if (!out) throw std::invalid_argument("bcs_partition_create: null output");
+        auto* p = new bcs_partition;
+        try {
+            p->dec = bcs::decompose(n_cells, centroids, n_ranks);
+            p->parts = bcs::buildPartitioned(n_cells, n_faces, owner, neighbour, p->dec);
+            if (n_engines > 0)
+                p->parts = bcs::consolidate(p->parts, bcs::makeConsolidationPlan(p->dec, n_engines), p->dec);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+void bcs_partition_destroy(bcs_partition* p) { delete p; }
+int bcs_partition_count(const bcs_partition* p) { return p ? static_cast<int>(p->parts.size()) : 0; }
+bcs_status bcs_partition_decomposition(const bcs_partition* p, int32_t* c2r, int32_t* rro, int32_t* o2n) {
+    return guarded(nullptr, [&] {
+        if (!p) throw std::invalid_argument("null partition");
+        if (c2r) std::copy(p->dec.cellToRank.begin(), p->dec.cellToRank.end(), c2r);
+        if (rro) std::copy(p->dec.rankRowOffset.begin(), p->dec.rankRowOffset.end(), rro);
+        if (o2n) std::copy(p->dec.oldToNew.begin(), p->dec.oldToNew.end(), o2n);
+    });
+}
+bcs_status bcs_partition_sizes(const bcs_partition* p, int part, int* rs, int* re, int* nnz, int* nh, int* ns) {
+    return guarded(nullptr, [&] {
+        if (!p || part < 0 || part >= static_cast<int>(p->parts.size())) throw std::invalid_argument("bad partition index");
+        const auto& q = p->parts[part];
+        if (rs) *rs = q.rowStart;
+        if (re) *re = q.rowEnd;
+        if (nnz) *nnz = static_cast<int>(q.ci.size());
+        if (nh) *nh = static_cast<int>(q.haloRow.size());
+        if (ns) *ns = static_cast<int>(q.sendPlan.size());
+    });
+}
+bcs_status bcs_partition_get(const bcs_partition* p, int part, int32_t* ro, int32_t* ci, int32_t* src, int32_t* hr,
+                             int32_t* hc, int32_t* hp, int32_t* hs, int32_t* sp, int32_t* sr) {
+    return guarded(nullptr, [&] {
+        if (!p || part < 0 || part >= static_cast<int>(p->parts.size())) throw std::invalid_argument("bad partition index");
+        const auto& q = p->parts[part];
+        if (ro) std::copy(q.ro.begin(), q.ro.end(), ro);
+        if (ci) std::copy(q.ci.begin(), q.ci.end(), ci);
+        if (src) std::copy(q.src.begin(), q.src.end(), src);
+        if (hr) std::copy(q.haloRow.begin(), q.haloRow.end(), hr);
+        if (hc) std::copy(q.haloCol.begin(), q.haloCol.end(), hc);
+        if (hp) std::copy(q.haloPeer.begin(), q.haloPeer.end(), hp);
+        if (hs) std::copy(q.haloSrc.begin(), q.haloSrc.end(), hs);
+        for (size_t i = 0; i < q.sendPlan.size(); ++i) {
+            if (sp) sp[i] = q.sendPlan[i].first;
+            if (sr) sr[i] = q.sendPlan[i].second;
+        }
     });
 }
 

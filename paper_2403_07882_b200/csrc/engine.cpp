@@ -100,7 +100,8 @@ Engine::Engine(int device) : device_(device) {
     push_.ensure(8, stream_);
     cudaMemsetAsync(ctr_.p, 0, 4 * sizeof(int), stream_);
     cudaMemsetAsync(ticket_.p, 0, 4 * sizeof(int), stream_);
-    partials_.ensure(static_cast<size_t>(reduce_blocks()) + 8, stream_);
+    partials_.ensure(static_cast<size_t>(reduce_blocks()) + 512, stream_);
+    seg_.ensure(65, stream_);
     scal_.ensure(16, stream_);
     sync();
 }
@@ -111,16 +112,26 @@ Engine::~Engine() {
     // device arrays are released with the pool when the context goes away;
     // free explicitly to keep long-lived processes lean
     auto rel = [&](auto& a) { a.release(stream_); };
-    for (auto& L : levels_) {
+    for (auto& L : main_.levels) {
         rel(L.o_ro); rel(L.o_ci); rel(L.o_dg); rel(L.o_tpos); rel(L.o_v); rel(L.lu); rel(L.rcp); rel(L.recf); rel(L.recb); rel(L.piv); rel(L.order);
         rel(L.agg); rel(L.members); rel(L.r); rel(L.z); rel(L.res); rel(L.y); rel(L.zb);
     }
     rel(dOwner_); rel(dNeigh_); rel(ro_); rel(ci_); rel(dg_); rel(tpos_); rel(src_); rel(fill_); rel(vals_);
-    rel(ldu_diag_); rel(ldu_upper_); rel(ldu_lower_); rel(dense_); rel(dpiv_); rel(cnt_); rel(lvl_); rel(push_);
+    rel(ldu_diag_); rel(ldu_upper_); rel(ldu_lower_); rel(main_.dense); rel(main_.dpiv); rel(cnt_); rel(lvl_); rel(push_);
     rel(scanTmp_); rel(act2_); rel(flag_); rel(err_); rel(ctr_); rel(choice_); rel(segOff_); rel(cro_); rel(big_); rel(dn_); rel(tblk_);
-    rel(str_); rel(keys_); rel(sorted_); rel(V_); rel(w_); rel(zk_); rel(rk_); rel(H_); rel(cs_); rel(sn_); rel(g_);
+    rel(str_); rel(keys_); rel(sorted_); rel(V_); rel(w_); rel(zk_); rel(rk_); rel(Hm_); rel(cs_); rel(sn_); rel(g_);
     rel(y_); rel(scal_); rel(partials_); rel(kb_); rel(kx_); rel(bp_); rel(bv_); rel(bs_); rel(bt_); rel(bph_);
-    rel(bsh_); rel(brh_); rel(ticket_);
+    rel(bsh_); rel(brh_); rel(ticket_); rel(seg_); rel(distTmp_);
+    for (auto& P : dist_) {
+        rel(P.ro); rel(P.ci); rel(P.src); rel(P.dg); rel(P.tpos); rel(P.vals); rel(P.hrow); rel(P.hoff);
+        rel(P.hcol); rel(P.hsrc); rel(P.hvals);
+        for (auto& L : P.H.levels) {
+            rel(L.o_ro); rel(L.o_ci); rel(L.o_dg); rel(L.o_tpos); rel(L.o_v); rel(L.lu); rel(L.rcp); rel(L.recf);
+            rel(L.recb); rel(L.piv); rel(L.order); rel(L.agg); rel(L.members); rel(L.r); rel(L.z); rel(L.res);
+            rel(L.y); rel(L.zb);
+        }
+        rel(P.H.dense); rel(P.H.dpiv);
+    }
     cudaStreamSynchronize(stream_);
     if (hStatus_) cudaFreeHost(hStatus_);
     if (ev0_) cudaEventDestroy(ev0_);
@@ -221,7 +232,7 @@ void Engine::uploadLdu(const double* diag, const double* upper, const double* lo
     gather_values(n_, nc_ + 2 * nf_, nc_, nf_, src_, dd, du, dl, vals_.p, stream_);
     checkErr("uploadLdu");
     hasValues_ = true;
-    pcKind_ = -1;  // any preconditioner built on old values is stale
+    H_->pcKind = -1;  // any preconditioner built on old values is stale
 }
 
 void Engine::requireMatrix() const {
@@ -232,7 +243,7 @@ void Engine::requireMatrix() const {
 // stream when kernel timing is on; the pairs are read after the solve's final
 // synchronisation, so timing never adds a host sync inside the solve.
 void Engine::spmvLevel(const Level& L, const double* x, const double* sub, double* y) {
-    const bool timed = kernelTiming_ && &L == &levels_[0];
+    const bool timed = kernelTiming_ && &L == &H_->levels[0];
     if (timed) {
         if (evUsed_ == evPool_.size()) {
             cudaEvent_t a, b;
@@ -345,12 +356,12 @@ void Engine::lusgsSetup(Level& L) {
 
 void Engine::buildHierarchy(const bcs_solver_config& cfg) {
     const size_t nn = static_cast<size_t>(n_) * n_;
-    nlev_ = 1;
+    H_->nlev = 1;
     // coarsening loop (amg.cpp:75-84)
-    while (nlev_ < cfg.amg_max_levels && levels_[nlev_ - 1].rows > cfg.amg_min_coarse_rows) {
-        const int l = nlev_ - 1;
+    while (H_->nlev < cfg.amg_max_levels && H_->levels[H_->nlev - 1].rows > cfg.amg_min_coarse_rows) {
+        const int l = H_->nlev - 1;
         {
-            Level& L = levels_[l];
+            Level& L = H_->levels[l];
             dn_.ensure(L.rows, stream_);
             str_.ensure(L.nnz, stream_);
             profMark("setup:other");
@@ -380,10 +391,10 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
             if (nC == L.rows) break;  // no coarsening possible (amg.cpp:80)
             L.ncoarse = nC;
         }
-        if (static_cast<int>(levels_.size()) < nlev_ + 1) levels_.emplace_back();
-        ++nlev_;
-        Level& L = levels_[l];
-        Level& C = levels_[l + 1];
+        if (static_cast<int>(H_->levels.size()) < H_->nlev + 1) H_->levels.emplace_back();
+        ++H_->nlev;
+        Level& L = H_->levels[l];
+        Level& C = H_->levels[l + 1];
         const int nC = L.ncoarse;
         // Galerkin (amg.cpp:39-71): segmented keys, per-segment rank sort, runs -> slots
         segOff_.ensure(static_cast<size_t>(nC) + 1, stream_);
@@ -423,32 +434,32 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
         setupLevelPattern(C);
         profMark("setup:pattern");
     }
-    levels_[nlev_ - 1].ncoarse = 0;
+    H_->levels[H_->nlev - 1].ncoarse = 0;
     // DILU smoother on all but the coarsest level (amg.cpp:86-88)
-    for (int l = 0; l + 1 < nlev_; ++l) {
-        diluSetup(levels_[l]);
-        profMark("setup:dilu L" + std::to_string(l) + " rows " + std::to_string(levels_[l].rows) + " depth " +
-                 std::to_string(levels_[l].depth));
+    for (int l = 0; l + 1 < H_->nlev; ++l) {
+        diluSetup(H_->levels[l]);
+        profMark("setup:dilu L" + std::to_string(l) + " rows " + std::to_string(H_->levels[l].rows) + " depth " +
+                 std::to_string(H_->levels[l].depth));
     }
     // dense factorisation of the coarsest level (amg.cpp:90-104)
-    const Level& Cl = levels_[nlev_ - 1];
-    m_ = Cl.rows * n_;
-    dense_.ensure(static_cast<size_t>(m_) * m_, stream_);
-    dpiv_.ensure(m_, stream_);
-    dense_build(n_, Cl.rows, Cl.ro, Cl.ci, Cl.v, dense_.p, stream_);
+    const Level& Cl = H_->levels[H_->nlev - 1];
+    H_->m = Cl.rows * n_;
+    H_->dense.ensure(static_cast<size_t>(H_->m) * H_->m, stream_);
+    H_->dpiv.ensure(H_->m, stream_);
+    dense_build(n_, Cl.rows, Cl.ro, Cl.ci, Cl.v, H_->dense.p, stream_);
     cudaMemsetAsync(err_.p, 0, sizeof(int), stream_);
-    dense_factor(m_, dense_.p, dpiv_.p, err_.p, stream_);
+    dense_factor(H_->m, H_->dense.p, H_->dpiv.p, err_.p, stream_);
     if (readErrCell()) throw std::runtime_error("singular coarse-level matrix");
     profMark("setup:dense");
     // V-cycle vectors
-    for (int l = 0; l < nlev_; ++l) {
-        Level& L = levels_[l];
+    for (int l = 0; l < H_->nlev; ++l) {
+        Level& L = H_->levels[l];
         const size_t N = static_cast<size_t>(L.rows) * n_;
         if (l > 0) {
             L.r.ensure(N, stream_);
             L.z.ensure(N, stream_);
         }
-        if (l + 1 < nlev_) {
+        if (l + 1 < H_->nlev) {
             L.res.ensure(N, stream_);
             L.y.ensure(N, stream_);
             L.zb.ensure(N, stream_);
@@ -456,21 +467,37 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
     }
 }
 
+FineMatrix Engine::serialFine() const {
+    FineMatrix F;
+    F.rows = nc_;
+    F.nnz = nc_ + 2 * nf_;
+    F.ro = ro_;
+    F.ci = ci_;
+    F.dg = dg_;
+    F.tpos = tpos_;
+    F.v = vals_;
+    return F;
+}
+
 // makeCsrPreconditioner (engine.cpp:21-29)
 void Engine::buildPrecond(const bcs_solver_config& cfg) {
     requireMatrix();
-    pcKind_ = -1;
-    if (levels_.empty()) levels_.emplace_back();
-    nlev_ = 1;
-    Level& L0 = levels_[0];
-    L0.rows = nc_;
-    L0.nnz = nc_ + 2 * nf_;
-    L0.ro = ro_;
-    L0.ci = ci_;
-    L0.dg = dg_;
-    L0.tpos = tpos_;
-    L0.v = vals_;
-    const size_t N = static_cast<size_t>(nc_) * n_;
+    buildPrecondOn(serialFine(), cfg);
+}
+
+void Engine::buildPrecondOn(const FineMatrix& F, const bcs_solver_config& cfg) {
+    H_->pcKind = -1;
+    if (H_->levels.empty()) H_->levels.emplace_back();
+    H_->nlev = 1;
+    Level& L0 = H_->levels[0];
+    L0.rows = F.rows;
+    L0.nnz = F.nnz;
+    L0.ro = F.ro;
+    L0.ci = F.ci;
+    L0.dg = F.dg;
+    L0.tpos = F.tpos;
+    L0.v = F.v;
+    const size_t N = static_cast<size_t>(F.rows) * n_;
     switch (cfg.precond) {
         case BCS_PRECOND_NONE: break;
         case BCS_PRECOND_LUSGS:
@@ -485,8 +512,8 @@ void Engine::buildPrecond(const bcs_solver_config& cfg) {
         default: throw std::invalid_argument("unknown preconditioner kind");
     }
     checkErr("buildPrecond");
-    pcKind_ = cfg.precond;
-    pcCfg_ = cfg;
+    H_->pcKind = cfg.precond;
+    H_->pcCfg = cfg;
 }
 
 // DILU/LUSGS sweep pair: z = (D+U)^{-1} D (D+L)^{-1} r  (accumulate: see sweep_backward)
@@ -502,14 +529,14 @@ void Engine::smootherApply(Level& L, const double* r, double* z, int accumulate)
 
 // AmgHierarchy::vcycle (amg.cpp:111-158)
 void Engine::vcycle(int l, const double* r, double* z) {
-    Level& L = levels_[l];
+    Level& L = H_->levels[l];
     const size_t N = static_cast<size_t>(L.rows) * n_;
-    if (l == nlev_ - 1) {
-        dense_solve(m_, dense_, dpiv_, r, z, stream_);
+    if (l == H_->nlev - 1) {
+        dense_solve(H_->m, H_->dense, H_->dpiv, r, z, stream_);
         profMark("vcycle:dense_solve");
         return;
     }
-    const int pre = pcCfg_.amg_pre_sweeps, post = pcCfg_.amg_post_sweeps;
+    const int pre = H_->pcCfg.amg_pre_sweeps, post = H_->pcCfg.amg_post_sweeps;
     for (int s = 0; s < pre; ++s) {
         const double* rin = r;  // z == 0 on the first sweep: r - A*0 == r exactly
         if (s > 0) {
@@ -526,7 +553,7 @@ void Engine::vcycle(int l, const double* r, double* z) {
     } else {
         cudaMemsetAsync(z, 0, N * sizeof(double), stream_);
     }
-    Level& C = levels_[l + 1];
+    Level& C = H_->levels[l + 1];
     restrict_vec(n_, L.ncoarse, L.members, res, C.r.p, stream_);
     profMark("vcycle:residual+restrict");
     vcycle(l + 1, C.r, C.z.p);
@@ -541,11 +568,11 @@ void Engine::vcycle(int l, const double* r, double* z) {
 }
 
 void Engine::applyPrecond(const double* r, double* z) {
-    const size_t N = static_cast<size_t>(nc_) * n_;
-    switch (pcKind_) {
+    const size_t N = static_cast<size_t>(H_->levels[0].rows) * n_;
+    switch (H_->pcKind) {
         case BCS_PRECOND_NONE: copy_vec(r, z, N, stream_); break;
         case BCS_PRECOND_LUSGS:
-        case BCS_PRECOND_DILU: smootherApply(levels_[0], r, z, 0); break;
+        case BCS_PRECOND_DILU: smootherApply(H_->levels[0], r, z, 0); break;
         case BCS_PRECOND_AMG: vcycle(0, r, z); break;
         default: throw std::logic_error("preconditioner not built");
     }
@@ -553,7 +580,8 @@ void Engine::applyPrecond(const double* r, double* z) {
 
 // ------------------------------------------------------------------ Krylov
 double Engine::dotHost(const double* a, const double* b, size_t N, bool sqrt_out) {
-    dot(a, b, N, scal_.p + 2, sqrt_out, partials_.p, ticket_.p, stream_);
+    (void)N;
+    opDot(a, b, scal_.p + 2, sqrt_out);
     check(cudaMemcpyAsync(hStatus_ + 2, scal_.p + 2, sizeof(double), cudaMemcpyDeviceToHost, stream_), "D2H scalar");
     sync();
     return hStatus_[2];
@@ -566,7 +594,7 @@ void Engine::gmres(const double* b, double* x, const bcs_solver_config& cfg, bcs
     rk_.ensure(N, stream_);
     w_.ensure(N, stream_);
     zk_.ensure(N, stream_);
-    spmvLevel(levels_[0], x, b, rk_.p);
+    opResidual(x, b, rk_.p);
     double beta = dotHost(rk_, rk_, N, true);
     rep.initial_residual = beta;
     const double beta0 = beta;
@@ -577,7 +605,7 @@ void Engine::gmres(const double* b, double* x, const bcs_solver_config& cfg, bcs
         return;
     }
     V_.ensure(static_cast<size_t>(m + 1) * N, stream_);
-    H_.ensure(static_cast<size_t>(m + 1) * m, stream_);
+    Hm_.ensure(static_cast<size_t>(m + 1) * m, stream_);
     cs_.ensure(m, stream_);
     sn_.ensure(m, stream_);
     g_.ensure(static_cast<size_t>(m) + 1, stream_);
@@ -587,24 +615,23 @@ void Engine::gmres(const double* b, double* x, const bcs_solver_config& cfg, bcs
     while (total < cfg.max_iters) {
         scale_by(rk_, beta_d, -1.0, V_.p, N, stream_);
         cudaMemsetAsync(g_.p, 0, sizeof(double) * (m + 1), stream_);
-        cudaMemsetAsync(H_.p, 0, sizeof(double) * (m + 1) * m, stream_);
+        cudaMemsetAsync(Hm_.p, 0, sizeof(double) * (m + 1) * m, stream_);
         cudaMemcpyAsync(g_.p, beta_d, sizeof(double), cudaMemcpyDeviceToDevice, stream_);
         int j = 0;
         bool happy = false;
         for (; j < m && total < cfg.max_iters; ++j, ++total) {
             double* vj = V_.p + static_cast<size_t>(j) * N;
-            applyPrecond(vj, zk_.p);
-            spmvLevel(levels_[0], zk_, nullptr, w_.p);
-            dot(w_, V_.p, N, H_.p + j, false, partials_.p, ticket_.p, stream_);
+            opPrecond(vj, zk_.p);
+            opSpmv(zk_, w_.p);
+            opDot(w_, V_.p, Hm_.p + j, false);
             for (int i = 0; i < j; ++i)
-                axpy_dot(w_.p, H_.p + static_cast<size_t>(i) * m + j, V_.p + static_cast<size_t>(i) * N,
-                         V_.p + static_cast<size_t>(i + 1) * N, N, H_.p + static_cast<size_t>(i + 1) * m + j,
-                         partials_.p, ticket_.p, stream_);
-            axpy_dot(w_.p, H_.p + static_cast<size_t>(j) * m + j, vj, nullptr, N,
-                     H_.p + static_cast<size_t>(j + 1) * m + j, partials_.p, ticket_.p, stream_);
-            scale_by(w_, H_.p + static_cast<size_t>(j + 1) * m + j, 1e-290, V_.p + static_cast<size_t>(j + 1) * N, N,
+                opAxpyDot(w_.p, Hm_.p + static_cast<size_t>(i) * m + j, V_.p + static_cast<size_t>(i) * N,
+                          V_.p + static_cast<size_t>(i + 1) * N, Hm_.p + static_cast<size_t>(i + 1) * m + j);
+            opAxpyDot(w_.p, Hm_.p + static_cast<size_t>(j) * m + j, vj, nullptr,
+                      Hm_.p + static_cast<size_t>(j + 1) * m + j);
+            scale_by(w_, Hm_.p + static_cast<size_t>(j + 1) * m + j, 1e-290, V_.p + static_cast<size_t>(j + 1) * N, N,
                      stream_);
-            givens_step(H_.p, m, j, cs_.p, sn_.p, g_.p, scal_.p + 4, stream_);
+            givens_step(Hm_.p, m, j, cs_.p, sn_.p, g_.p, scal_.p + 4, stream_);
             check(cudaMemcpyAsync(hStatus_ + 4, scal_.p + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream_),
                   "D2H status");
             sync();
@@ -618,11 +645,11 @@ void Engine::gmres(const double* b, double* x, const bcs_solver_config& cfg, bcs
             }
         }
         // back substitution, x += M^{-1}(V y)
-        back_subst(H_, m, j, g_, y_.p, stream_);
+        back_subst(Hm_, m, j, g_, y_.p, stream_);
         lincomb(V_, N, y_, j, w_.p, N, stream_);
-        applyPrecond(w_, zk_.p);
+        opPrecond(w_, zk_.p);
         add_to(x, zk_, N, stream_);
-        spmvLevel(levels_[0], x, b, rk_.p);
+        opResidual(x, b, rk_.p);
         beta = dotHost(rk_, rk_, N, true);
         if (!hist_.empty()) hist_.back() = beta / beta0;
         rep.iterations = total;
@@ -651,7 +678,7 @@ void Engine::bicgstab(const double* b, double* x, const bcs_solver_config& cfg, 
     bt_.ensure(N, stream_);
     bph_.ensure(N, stream_);
     bsh_.ensure(N, stream_);
-    spmvLevel(levels_[0], x, b, rk_.p);
+    opResidual(x, b, rk_.p);
     const double beta0 = dotHost(rk_, rk_, N, true);
     rep.initial_residual = beta0;
     const double tol = std::max(cfg.rel_tol * beta0, cfg.abs_tol);
@@ -670,8 +697,8 @@ void Engine::bicgstab(const double* b, double* x, const bcs_solver_config& cfg, 
         }
         if (it == 0) copy_vec(rk_, bp_.p, N, stream_);
         else bicg_p(bp_.p, rk_, bv_, (rho / rhoPrev) * (alpha / omega), omega, N, stream_);
-        applyPrecond(bp_, bph_.p);
-        spmvLevel(levels_[0], bph_, nullptr, bv_.p);
+        opPrecond(bp_, bph_.p);
+        opSpmv(bph_, bv_.p);
         const double rhatv = dotHost(brh_, bv_, N, false);
         if (std::fabs(rhatv) < 1e-300) {
             rep.breakdown = 1;
@@ -686,8 +713,8 @@ void Engine::bicgstab(const double* b, double* x, const bcs_solver_config& cfg, 
             hist_.push_back(ns / beta0);
             break;
         }
-        applyPrecond(bs_, bsh_.p);
-        spmvLevel(levels_[0], bsh_, nullptr, bt_.p);
+        opPrecond(bs_, bsh_.p);
+        opSpmv(bsh_, bt_.p);
         const double tt = dotHost(bt_, bt_, N, false);
         omega = tt > 0.0 ? dotHost(bt_, bs_, N, false) / tt : 0.0;
         bicg_x_r(x, rk_.p, bph_, bsh_, bs_, bt_, alpha, omega, N, stream_);
@@ -701,7 +728,7 @@ void Engine::bicgstab(const double* b, double* x, const bcs_solver_config& cfg, 
         hist_.push_back(nr / beta0);
         if (nr <= tol) break;
     }
-    spmvLevel(levels_[0], x, b, rk_.p);
+    opResidual(x, b, rk_.p);
     rep.final_residual = dotHost(rk_, rk_, N, true);
     rep.converged = rep.final_residual <= tol;
     if (rep.converged) rep.breakdown = 0;
@@ -714,6 +741,11 @@ void Engine::solveDevice(const double* d_b, double* d_x, const bcs_solver_config
     LaunchScope ls(&launches_);
     requireMatrix();
     validateConfig(cfg);
+    distActive_ = false;
+    H_ = &main_;
+    nseg_ = 1;
+    const long long segh[2] = {0, static_cast<long long>(nc_) * n_};
+    check(cudaMemcpyAsync(seg_.p, segh, sizeof segh, cudaMemcpyHostToDevice, stream_), "seg");
     const long long l0 = launches_.launches;
     spmvMs_ = 0.0;
     spmvCount_ = 0;
@@ -725,24 +757,236 @@ void Engine::solveDevice(const double* d_b, double* d_x, const bcs_solver_config
     buildPrecond(cfg);
     sync();
     const auto t1 = clk::now();
+    solveKrylov(d_b, d_x, cfg, rep);
+    const auto t2 = clk::now();
+    rep.t_amg_setup = secs(t0, t1);
+    rep.t_krylov = secs(t1, t2);
+    rep.amg_levels = H_->pcKind == BCS_PRECOND_AMG ? H_->nlev : 0;
+    rep.coarse_rows = H_->pcKind == BCS_PRECOND_AMG ? H_->levels[H_->nlev - 1].rows : 0;
+    rep.spmv_launches = spmvCount_;
+    rep.spmv_ms = spmvMs_;
+    rep.kernel_launches = static_cast<int>(launches_.launches - l0);
+    lastSolveLaunches_ = rep.kernel_launches;
+}
+
+void Engine::solveKrylov(const double* d_b, double* d_x, const bcs_solver_config& cfg, bcs_report& rep) {
     if (cfg.method == BCS_GMRES) gmres(d_b, d_x, cfg, rep);
     else bicgstab(d_b, d_x, cfg, rep);
     sync();
-    const auto t2 = clk::now();
     collectSpmvTimes();
     profDump();
     int spinErr = 0;
     check(cudaMemcpy(&spinErr, err_.p + 1, sizeof(int), cudaMemcpyDeviceToHost), "spin flag");
     if (spinErr) throw std::runtime_error("bcs: sweep dependency wait timed out (corrupt schedule)");
     checkErr("solve");
-    rep.t_amg_setup = secs(t0, t1);
-    rep.t_krylov = secs(t1, t2);
-    rep.amg_levels = pcKind_ == BCS_PRECOND_AMG ? nlev_ : 0;
-    rep.coarse_rows = pcKind_ == BCS_PRECOND_AMG ? levels_[nlev_ - 1].rows : 0;
-    rep.spmv_launches = spmvCount_;
-    rep.spmv_ms = spmvMs_;
-    rep.kernel_launches = static_cast<int>(launches_.launches - l0);
-    lastSolveLaunches_ = rep.kernel_launches;
+}
+
+// ------------------------------------------------------- Krylov operators
+void Engine::opResidual(const double* x, const double* b, double* r) {
+    if (!distActive_) {
+        spmvLevel(H_->levels[0], x, b, r);
+        return;
+    }
+    opSpmv(x, distTmp_.p);
+    sub_vec(b, distTmp_, r, static_cast<size_t>(distNc_) * n_, stream_);
+}
+
+// partitionedMatvec (partition.cpp:298-352): every engine's local product on
+// its row slice, then its halo couplings (the exchange is implicit: all engine
+// slices live in one device vector on this GPU)
+void Engine::opSpmv(const double* x, double* y) {
+    if (!distActive_) {
+        spmvLevel(H_->levels[0], x, nullptr, y);
+        return;
+    }
+    for (auto& P : dist_) {
+        const size_t off = static_cast<size_t>(P.rowStart) * n_;
+        spmv(n_, P.rows, P.ro, P.ci, P.vals, x + off, nullptr, y + off, stream_);
+        halo_spmv(n_, P.nhr, P.hrow, P.hoff, P.hcol, P.hvals, x, y, P.rowStart, stream_);
+    }
+}
+
+// per-engine local preconditioners (partition.cpp:427-431), block Jacobi across engines
+void Engine::opPrecond(const double* r, double* z) {
+    if (!distActive_) {
+        applyPrecond(r, z);
+        return;
+    }
+    for (auto& P : dist_) {
+        H_ = &P.H;
+        const size_t off = static_cast<size_t>(P.rowStart) * n_;
+        applyPrecond(r + off, z + off);
+    }
+    H_ = &main_;
+}
+
+void Engine::opDot(const double* a, const double* b, double* out, bool sqrt_out) {
+    dot(a, b, seg_, nseg_, out, sqrt_out, partials_.p, ticket_.p, stream_);
+}
+
+void Engine::opAxpyDot(double* w, const double* h, const double* v, const double* nextv, double* out) {
+    axpy_dot(w, h, v, nextv, seg_, nseg_, out, partials_.p, ticket_.p, stream_);
+}
+
+// ------------------------------------------------------------------ Mode R
+void Engine::distSetupTopology(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh,
+                               const double* centroids, int nRanks, int nEngines) {
+    if (nEngines > 64) throw std::invalid_argument("bcs: at most 64 engines per device");
+    const Decomposition dec = decompose(nc, centroids, nRanks);
+    const std::vector<Partition> parts = buildPartitioned(nc, nf, owner, neigh, dec);
+    const ConsolidationPlan plan = makeConsolidationPlan(dec, nEngines);
+    const std::vector<Partition> eng = consolidate(parts, plan, dec);
+    dist_.resize(eng.size());
+    std::vector<long long> segh(eng.size() + 1, 0);
+    for (size_t e = 0; e < eng.size(); ++e) {
+        const Partition& p = eng[e];
+        DistPart& P = dist_[e];
+        P.rowStart = p.rowStart;
+        P.rows = p.nLocalRows();
+        P.nnz = static_cast<int>(p.ci.size());
+        P.nh = static_cast<int>(p.haloRow.size());
+        P.ro.ensure(p.ro.size(), stream_);
+        P.ci.ensure(p.ci.size(), stream_);
+        P.src.ensure(p.src.size(), stream_);
+        P.dg.ensure(P.rows, stream_);
+        P.tpos.ensure(p.ci.size(), stream_);
+        P.vals.ensure(static_cast<size_t>(P.nnz) * n * n, stream_);
+        check(cudaMemcpyAsync(P.ro.p, p.ro.data(), sizeof(int) * p.ro.size(), cudaMemcpyHostToDevice, stream_), "H2D");
+        check(cudaMemcpyAsync(P.ci.p, p.ci.data(), sizeof(int) * p.ci.size(), cudaMemcpyHostToDevice, stream_), "H2D");
+        check(cudaMemcpyAsync(P.src.p, p.src.data(), sizeof(int) * p.src.size(), cudaMemcpyHostToDevice, stream_), "H2D");
+        find_diag(P.rows, P.ro, P.ci, P.dg.p, stream_);
+        cudaMemsetAsync(err_.p, 0, sizeof(int), stream_);
+        transpose_pos(P.rows, P.ro, P.ci, P.tpos.p, err_.p, stream_);
+        if (readErrCell()) throw std::runtime_error("bcs: structurally asymmetric engine pattern");
+        // halo rows: distinct local rows of the (row, col)-sorted entries
+        std::vector<int> hrow, hoff;
+        for (int h = 0; h < P.nh; ++h)
+            if (h == 0 || p.haloRow[h] != p.haloRow[h - 1]) {
+                hrow.push_back(p.haloRow[h]);
+                hoff.push_back(h);
+            }
+        hoff.push_back(P.nh);
+        P.nhr = static_cast<int>(hrow.size());
+        P.hrow.ensure(hrow.size(), stream_);
+        P.hoff.ensure(hoff.size(), stream_);
+        P.hcol.ensure(P.nh, stream_);
+        P.hsrc.ensure(P.nh, stream_);
+        P.hvals.ensure(static_cast<size_t>(P.nh) * n * n, stream_);
+        if (P.nh) {
+            check(cudaMemcpyAsync(P.hrow.p, hrow.data(), sizeof(int) * hrow.size(), cudaMemcpyHostToDevice, stream_), "H2D");
+            check(cudaMemcpyAsync(P.hoff.p, hoff.data(), sizeof(int) * hoff.size(), cudaMemcpyHostToDevice, stream_), "H2D");
+            check(cudaMemcpyAsync(P.hcol.p, p.haloCol.data(), sizeof(int) * P.nh, cudaMemcpyHostToDevice, stream_), "H2D");
+            check(cudaMemcpyAsync(P.hsrc.p, p.haloSrc.data(), sizeof(int) * P.nh, cudaMemcpyHostToDevice, stream_), "H2D");
+        }
+        segh[e + 1] = static_cast<long long>(p.rowEnd) * n;
+        segh[e] = static_cast<long long>(p.rowStart) * n;
+        sync();  // host vectors die at the end of this iteration
+    }
+    nseg_ = static_cast<int>(eng.size());
+    seg_.ensure(eng.size() + 1, stream_);
+    check(cudaMemcpyAsync(seg_.p, segh.data(), sizeof(long long) * segh.size(), cudaMemcpyHostToDevice, stream_), "H2D");
+    distNewToOld_ = dec.newToOld;
+    distOwner_.assign(owner, owner + nf);
+    distNeigh_.assign(neigh, neigh + nf);
+    distCen_.assign(centroids, centroids + 3 * static_cast<size_t>(nc));
+    distRanks_ = nRanks;
+    distEngines_ = nEngines;
+    distNc_ = nc;
+    distNf_ = nf;
+    distN_ = n;
+    sync();
+}
+
+void Engine::distSolve(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh, const double* centroids,
+                       const double* diag, const double* upper, const double* lower, const double* b,
+                       const double* x0, double* x, int nRanks, int nEngines, const bcs_solver_config& cfg,
+                       bcs_report& rep) {
+    LaunchScope ls(&launches_);
+    if (n < 1 || n > 5) throw std::invalid_argument("bcs: block size must be 1..5 on the device");
+    if (nEngines < 1 || nEngines > nRanks) throw std::invalid_argument("makeConsolidationPlan: need 1 <= nEngines <= nRanks");
+    validateConfig(cfg);
+    const auto t0 = clk::now();
+    const bool same = distNc_ == nc && distNf_ == nf && distN_ == n && distRanks_ == nRanks && distEngines_ == nEngines &&
+                      std::equal(owner, owner + nf, distOwner_.begin()) && std::equal(neigh, neigh + nf, distNeigh_.begin()) &&
+                      std::equal(centroids, centroids + 3 * static_cast<size_t>(nc), distCen_.begin());
+    if (!same) distSetupTopology(nc, nf, n, owner, neigh, centroids, nRanks, nEngines);
+    n_ = n;
+    // upload: LDU values -> engine slots and halo blocks (replace semantics)
+    const size_t nn = static_cast<size_t>(n) * n;
+    ldu_diag_.ensure(nc * nn, stream_);
+    ldu_upper_.ensure(nf * nn, stream_);
+    ldu_lower_.ensure(nf * nn, stream_);
+    check(cudaMemcpyAsync(ldu_diag_.p, diag, sizeof(double) * nc * nn, cudaMemcpyHostToDevice, stream_), "H2D");
+    if (nf) {
+        check(cudaMemcpyAsync(ldu_upper_.p, upper, sizeof(double) * nf * nn, cudaMemcpyHostToDevice, stream_), "H2D");
+        check(cudaMemcpyAsync(ldu_lower_.p, lower, sizeof(double) * nf * nn, cudaMemcpyHostToDevice, stream_), "H2D");
+    }
+    for (auto& P : dist_) {
+        gather_values(n, P.nnz, nc, nf, P.src, ldu_diag_, ldu_upper_, ldu_lower_, P.vals.p, stream_);
+        if (P.nh) gather_values(n, P.nh, nc, nf, P.hsrc, ldu_diag_, ldu_upper_, ldu_lower_, P.hvals.p, stream_);
+    }
+    // scatterVector: rank-major renumbering (partition.cpp:269-280)
+    const size_t N = static_cast<size_t>(nc) * n;
+    std::vector<double> hb(N), hx(N);
+    for (int g = 0; g < nc; ++g) {
+        const int old = distNewToOld_[g];
+        std::copy(b + static_cast<size_t>(old) * n, b + static_cast<size_t>(old + 1) * n, hb.begin() + static_cast<size_t>(g) * n);
+        std::copy(x0 + static_cast<size_t>(old) * n, x0 + static_cast<size_t>(old + 1) * n, hx.begin() + static_cast<size_t>(g) * n);
+    }
+    kb_.ensure(N, stream_);
+    kx_.ensure(N, stream_);
+    distTmp_.ensure(N, stream_);
+    check(cudaMemcpyAsync(kb_.p, hb.data(), N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D b");
+    check(cudaMemcpyAsync(kx_.p, hx.data(), N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D x0");
+    sync();
+    const auto t1 = clk::now();
+    // per-engine preconditioners (partition.cpp:411-412)
+    hist_.clear();
+    spmvMs_ = 0.0;
+    spmvCount_ = 0;
+    evUsed_ = 0;
+    cudaMemsetAsync(err_.p + 1, 0, sizeof(int), stream_);
+    nc_ = nc;
+    for (auto& P : dist_) {
+        H_ = &P.H;
+        FineMatrix F;
+        F.rows = P.rows;
+        F.nnz = P.nnz;
+        F.ro = P.ro;
+        F.ci = P.ci;
+        F.dg = P.dg;
+        F.tpos = P.tpos;
+        F.v = P.vals;
+        buildPrecondOn(F, cfg);
+    }
+    H_ = &main_;
+    sync();
+    const auto t2 = clk::now();
+    distActive_ = true;
+    try {
+        solveKrylov(kb_, kx_.p, cfg, rep);
+    } catch (...) {
+        distActive_ = false;
+        nseg_ = 1;
+        throw;
+    }
+    distActive_ = false;
+    const auto t3 = clk::now();
+    check(cudaMemcpyAsync(hx.data(), kx_.p, N * sizeof(double), cudaMemcpyDeviceToHost, stream_), "D2H x");
+    sync();
+    for (int g = 0; g < nc; ++g) {  // gatherVector (partition.cpp:282-296)
+        const int old = distNewToOld_[g];
+        std::copy(hx.begin() + static_cast<size_t>(g) * n, hx.begin() + static_cast<size_t>(g + 1) * n,
+                  x + static_cast<size_t>(old) * n);
+    }
+    const auto t4 = clk::now();
+    rep.t_convert = secs(t0, t1);  // partition.cpp:474-477 keys
+    rep.t_setup = secs(t1, t2);
+    rep.t_solve = secs(t2, t3);
+    rep.t_retrieve = secs(t3, t4);
+    rep.t_amg_setup = rep.t_setup;
+    rep.t_krylov = rep.t_solve;
+    rep.amg_levels = static_cast<int>(dist_.size());
 }
 
 void Engine::solveHost(const double* b, double* x, const bcs_solver_config& cfg, bcs_report& rep) {
@@ -832,6 +1076,9 @@ void Engine::pipelineSolve(int nc, int nf, int n, const int32_t* owner, const in
 double Engine::residualNorm(const double* b, const double* x) {
     LaunchScope ls(&launches_);
     requireMatrix();
+    nseg_ = 1;
+    const long long segh[2] = {0, static_cast<long long>(nc_) * n_};
+    check(cudaMemcpyAsync(seg_.p, segh, sizeof segh, cudaMemcpyHostToDevice, stream_), "seg");
     const size_t N = static_cast<size_t>(nc_) * n_;
     kb_.ensure(N, stream_);
     kx_.ensure(N, stream_);
@@ -878,7 +1125,7 @@ void Engine::precondSetup(const bcs_solver_config& cfg) {
 
 void Engine::precondApplyHost(const double* r, double* z) {
     LaunchScope ls(&launches_);
-    if (pcKind_ < 0) throw std::invalid_argument("bcs: call bcs_precond_setup first");
+    if (H_->pcKind < 0) throw std::invalid_argument("bcs: call bcs_precond_setup first");
     const size_t N = static_cast<size_t>(nc_) * n_;
     kb_.ensure(N, stream_);
     kx_.ensure(N, stream_);
@@ -894,26 +1141,26 @@ void Engine::precondApplyHost(const double* r, double* z) {
 }
 
 void Engine::amgLevelSizes(int l, int* rows, int* nnz) const {
-    if (l < 0 || l >= nlev_) throw std::invalid_argument("bcs: level out of range");
-    *rows = levels_[l].rows;
-    *nnz = levels_[l].nnz;
+    if (l < 0 || l >= H_->nlev) throw std::invalid_argument("bcs: level out of range");
+    *rows = H_->levels[l].rows;
+    *nnz = H_->levels[l].nnz;
 }
 
 void Engine::amgLevelGet(int l, int32_t* ro, int32_t* ci, double* v, int32_t* agg) {
-    if (l < 0 || l >= nlev_) throw std::invalid_argument("bcs: level out of range");
-    const Level& L = levels_[l];
+    if (l < 0 || l >= H_->nlev) throw std::invalid_argument("bcs: level out of range");
+    const Level& L = H_->levels[l];
     const size_t nn = static_cast<size_t>(n_) * n_;
     if (ro) check(cudaMemcpyAsync(ro, L.ro, sizeof(int) * (L.rows + 1), cudaMemcpyDeviceToHost, stream_), "D2H");
     if (ci) check(cudaMemcpyAsync(ci, L.ci, sizeof(int) * L.nnz, cudaMemcpyDeviceToHost, stream_), "D2H");
     if (v) check(cudaMemcpyAsync(v, L.v, sizeof(double) * L.nnz * nn, cudaMemcpyDeviceToHost, stream_), "D2H");
-    if (agg && l + 1 < nlev_)
+    if (agg && l + 1 < H_->nlev)
         check(cudaMemcpyAsync(agg, L.agg.p, sizeof(int) * L.rows, cudaMemcpyDeviceToHost, stream_), "D2H");
     sync();
 }
 
 int Engine::scheduleDepth(int l) const {
-    if (l < 0 || l >= nlev_) throw std::invalid_argument("bcs: level out of range");
-    return levels_[l].depth;
+    if (l < 0 || l >= H_->nlev) throw std::invalid_argument("bcs: level out of range");
+    return H_->levels[l].depth;
 }
 
 }  // namespace bcs

@@ -5,6 +5,7 @@
 
 #include "../../include/bcs.h"
 #include "kernels.hpp"
+#include "partition.hpp"
 
 #include <chrono>
 #include <cstdint>
@@ -66,6 +67,35 @@ struct Level {
     DArray<double> r, z, res, y, zb;
 };
 
+// Preconditioner state of one matrix (the serial system or one Mode-R engine)
+struct Hier {
+    std::vector<Level> levels;  // storage persists across solves; nlev active
+    int nlev = 0;
+    DArray<double> dense;
+    DArray<int> dpiv;
+    int m = 0;
+    int pcKind = -1;  // 0 none, 1 LUSGS, 2 DILU, 3 AMG
+    bcs_solver_config pcCfg{};
+};
+
+// One Mode-R engine on the device: its consolidated local BSR (local
+// numbering, LDU source ids), halo couplings and its own preconditioner.
+struct DistPart {
+    int rowStart = 0, rows = 0, nnz = 0, nh = 0, nhr = 0;
+    DArray<int> ro, ci, src, dg, tpos;
+    DArray<double> vals;
+    DArray<int> hrow, hoff, hcol, hsrc;  // halo rows (local), CSR offsets, global cols, LDU source ids
+    DArray<double> hvals;
+    Hier H;
+};
+
+// Fine-level matrix a preconditioner is built on
+struct FineMatrix {
+    int rows = 0, nnz = 0;
+    const int *ro = nullptr, *ci = nullptr, *dg = nullptr, *tpos = nullptr;
+    const double* v = nullptr;
+};
+
 class Engine {
 public:
     explicit Engine(int device);
@@ -83,6 +113,14 @@ public:
                        const double* upper, const double* lower, const double* b, size_t b_len, const double* x0,
                        size_t x0_len, double* x, int backend, const bcs_solver_config& cfg, bcs_report& rep);
 
+    // Mode R: the reference's distributedSolve semantics (partition.cpp:370-479)
+    // on this device — ranks decomposed by RCB, consolidated onto engines, one
+    // local preconditioner per engine, global Krylov with halo couplings and
+    // the fixed engine-order tree for dot products.
+    void distSolve(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh, const double* centroids,
+                   const double* diag, const double* upper, const double* lower, const double* b, const double* x0,
+                   double* x, int nRanks, int nEngines, const bcs_solver_config& cfg, bcs_report& rep);
+
     // staged
     void solveDevice(const double* d_b, double* d_x, const bcs_solver_config& cfg, bcs_report& rep);
     void solveHost(const double* b, double* x, const bcs_solver_config& cfg, bcs_report& rep);
@@ -95,7 +133,7 @@ public:
     void csrGet(int32_t* ro, int32_t* ci, double* v);
     void precondSetup(const bcs_solver_config& cfg);
     void precondApplyHost(const double* r, double* z);
-    int amgDepth() const { return nlev_; }
+    int amgDepth() const { return H_->nlev; }
     void amgLevelSizes(int l, int* rows, int* nnz) const;
     void amgLevelGet(int l, int32_t* ro, int32_t* ci, double* v, int32_t* agg);
     int scheduleDepth(int l) const;
@@ -109,6 +147,8 @@ private:
     void requireMatrix() const;
     void validateConfig(const bcs_solver_config& cfg) const;
     void buildPrecond(const bcs_solver_config& cfg);
+    void buildPrecondOn(const FineMatrix& F, const bcs_solver_config& cfg);
+    FineMatrix serialFine() const;
     void buildHierarchy(const bcs_solver_config& cfg);
     void setupLevelPattern(Level& L);
     void diluSetup(Level& L);
@@ -119,6 +159,15 @@ private:
     void gmres(const double* b, double* x, const bcs_solver_config& cfg, bcs_report& rep);
     void bicgstab(const double* b, double* x, const bcs_solver_config& cfg, bcs_report& rep);
     void spmvLevel(const Level& L, const double* x, const double* sub, double* y);
+    // Krylov operators: serial system or Mode-R engines (distActive_)
+    void opResidual(const double* x, const double* b, double* r);  // r = b - A x
+    void opSpmv(const double* x, double* y);
+    void opPrecond(const double* r, double* z);
+    void opDot(const double* a, const double* b, double* out, bool sqrt_out);
+    void opAxpyDot(double* w, const double* h, const double* v, const double* nextv, double* out);
+    void distSetupTopology(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh,
+                           const double* centroids, int nRanks, int nEngines);
+    void solveKrylov(const double* d_b, double* d_x, const bcs_solver_config& cfg, bcs_report& rep);
     double dotHost(const double* a, const double* b, size_t N, bool sqrt_out);
     void sync();
     void checkErr(const char* where);
@@ -141,21 +190,17 @@ private:
     uint64_t pipeSig_ = 0;
     bool pipeSigValid_ = false;
 
-    // preconditioner
-    int pcKind_ = -1;  // 0 none, 1 LUSGS, 2 DILU, 3 AMG
-    bcs_solver_config pcCfg_{};
-    std::vector<Level> levels_;  // storage persists across solves; nlev_ active
-    int nlev_ = 0;
-    DArray<double> dense_;
-    DArray<int> dpiv_;
-    int m_ = 0;
+    // preconditioner of the serial system; H_ points at the hierarchy being
+    // built/applied (the serial one or a Mode-R engine's)
+    Hier main_;
+    Hier* H_ = &main_;
     // scratch
     DArray<int> cnt_, lvl_, act2_, push_, scanTmp_, flag_, err_, ctr_, choice_, segOff_, cro_, big_;
     DArray<double> dn_, str_, tblk_;
     DArray<unsigned long long> keys_, sorted_;
 
     // Krylov workspace
-    DArray<double> V_, w_, zk_, rk_, H_, cs_, sn_, g_, y_, scal_, partials_;
+    DArray<double> V_, w_, zk_, rk_, Hm_, cs_, sn_, g_, y_, scal_, partials_;
     DArray<double> kb_, kx_;  // staging for host-array entry points
     DArray<double> bp_, bv_, bs_, bt_, bph_, bsh_, brh_;
     DArray<int> ticket_;
@@ -164,6 +209,16 @@ private:
 
     // SpMV event timing (fine level)
     void collectSpmvTimes();
+    // Mode R state
+    bool distActive_ = false;
+    std::vector<DistPart> dist_;
+    std::vector<int32_t> distOwner_, distNeigh_;
+    std::vector<double> distCen_;
+    int distRanks_ = 0, distEngines_ = 0, distNc_ = 0, distNf_ = 0, distN_ = 0;
+    std::vector<int> distNewToOld_;
+    DArray<long long> seg_;  // segment offsets for reductions (1 segment serial, E for Mode R)
+    int nseg_ = 1;
+    DArray<double> distTmp_;
     // BCS_PROFILE=1: per-phase / per-level wall times (with syncs) to stderr
     bool prof_ = false;
     int aggMode_ = 0;   // 0 sync-free aggregation, 1 cooperative rounds

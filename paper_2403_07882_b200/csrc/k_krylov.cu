@@ -17,10 +17,16 @@ constexpr int kRedThreads = 256;
 
 int reduce_blocks() { return 2 * num_sms(); }
 
-__device__ __forceinline__ void finish_reduction(double part, double* partials, int* ticket, double* out,
+// Segmented deterministic reduction.  The vector is split into nseg
+// contiguous segments (Mode-R engines; 1 for a serial solve); B blocks reduce
+// each segment (fixed per-block order), the last block to finish sums every
+// segment's block partials in block order and folds the segment sums with
+// the reference's pairwise tree in engine order (partition.cpp:433-450).
+__device__ __forceinline__ void finish_reduction(double part, int nseg, double* partials, int* ticket, double* out,
                                                  bool sqrt_out) {
     __shared__ double sh[32];
     __shared__ bool last;
+    __shared__ double segsum[64];
     const double s = block_sum<kRedThreads>(part, sh);
     if (threadIdx.x == 0) {
         partials[blockIdx.x] = s;
@@ -30,50 +36,109 @@ __device__ __forceinline__ void finish_reduction(double part, double* partials, 
     __syncthreads();
     if (!last) return;
     __threadfence();
-    double t = 0.0;
-    for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) t += __ldcg(&partials[i]);
-    t = block_sum<kRedThreads>(t, sh);
+    const int B = gridDim.x / nseg;
+    for (int e = 0; e < nseg; ++e) {
+        double t = 0.0;
+        for (int i = threadIdx.x; i < B; i += blockDim.x) t += __ldcg(&partials[e * B + i]);
+        t = block_sum<kRedThreads>(t, sh);
+        if (threadIdx.x == 0) segsum[e] = t;
+    }
     if (threadIdx.x == 0) {
+        int m = nseg;
+        while (m > 1) {  // pairwise tree, engine order
+            int w = 0;
+            for (int i = 0; i + 1 < m; i += 2) segsum[w++] = segsum[i] + segsum[i + 1];
+            if (m % 2) segsum[w++] = segsum[m - 1];
+            m = w;
+        }
+        const double t = segsum[0];
         out[0] = sqrt_out ? sqrt(t) : t;
         *ticket = 0;
     }
 }
 
-__global__ void __launch_bounds__(kRedThreads) k_dot(const double* __restrict__ a, const double* __restrict__ b,
-                                                     size_t N, double* out, int sqrt_out, double* partials,
-                                                     int* ticket) {
-    double s = 0.0;
-    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < N; i += stride)
-        s += a[i] * b[i];
-    finish_reduction(s, partials, ticket, out, sqrt_out != 0);
+struct SegRange {
+    size_t b, e, i0, stride;
+};
+__device__ __forceinline__ SegRange seg_range(const long long* seg, int nseg) {
+    const int B = gridDim.x / nseg;
+    const int e = blockIdx.x / B, bi = blockIdx.x - e * B;
+    SegRange r;
+    r.b = static_cast<size_t>(seg[e]);
+    r.e = static_cast<size_t>(seg[e + 1]);
+    r.i0 = r.b + static_cast<size_t>(bi) * blockDim.x + threadIdx.x;
+    r.stride = static_cast<size_t>(B) * blockDim.x;
+    return r;
 }
 
-void dot(const double* a, const double* b, size_t N, double* out, bool sqrt_out, double* partials, int* ticket,
-         cudaStream_t s) {
-    k_dot<<<reduce_blocks(), kRedThreads, 0, s>>>(a, b, N, out, sqrt_out ? 1 : 0, partials, ticket);
+__global__ void __launch_bounds__(kRedThreads) k_dot(const double* __restrict__ a, const double* __restrict__ b,
+                                                     const long long* __restrict__ seg, int nseg, double* out,
+                                                     int sqrt_out, double* partials, int* ticket) {
+    const SegRange R = seg_range(seg, nseg);
+    double s = 0.0;
+    for (size_t i = R.i0; i < R.e; i += R.stride) s += a[i] * b[i];
+    finish_reduction(s, nseg, partials, ticket, out, sqrt_out != 0);
+}
+
+static int seg_grid(int nseg) {
+    int B = reduce_blocks() / nseg;
+    if (B < 4) B = 4;
+    return B * nseg;
+}
+
+void dot(const double* a, const double* b, const long long* seg, int nseg, double* out, bool sqrt_out,
+         double* partials, int* ticket, cudaStream_t s) {
+    k_dot<<<seg_grid(nseg), kRedThreads, 0, s>>>(a, b, seg, nseg, out, sqrt_out ? 1 : 0, partials, ticket);
     count_launch();
 }
 
 // w -= h v ; dot(w, nextv) or ||w||
 __global__ void __launch_bounds__(kRedThreads) k_axpy_dot(double* __restrict__ w, const double* __restrict__ h,
                                                           const double* __restrict__ v,
-                                                          const double* __restrict__ nextv, size_t N, double* out,
+                                                          const double* __restrict__ nextv,
+                                                          const long long* __restrict__ seg, int nseg, double* out,
                                                           double* partials, int* ticket) {
     const double hv = *h;
+    const SegRange R = seg_range(seg, nseg);
     double s = 0.0;
-    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < N; i += stride) {
+    for (size_t i = R.i0; i < R.e; i += R.stride) {
         const double wn = w[i] - hv * v[i];
         w[i] = wn;
         s += nextv ? wn * nextv[i] : wn * wn;
     }
-    finish_reduction(s, partials, ticket, out, nextv == nullptr);
+    finish_reduction(s, nseg, partials, ticket, out, nextv == nullptr);
 }
 
-void axpy_dot(double* w, const double* h, const double* v, const double* nextv, size_t N, double* out,
-              double* partials, int* ticket, cudaStream_t s) {
-    k_axpy_dot<<<reduce_blocks(), kRedThreads, 0, s>>>(w, h, v, nextv, N, out, partials, ticket);
+void axpy_dot(double* w, const double* h, const double* v, const double* nextv, const long long* seg, int nseg,
+              double* out, double* partials, int* ticket, cudaStream_t s) {
+    k_axpy_dot<<<seg_grid(nseg), kRedThreads, 0, s>>>(w, h, v, nextv, seg, nseg, out, partials, ticket);
+    count_launch();
+}
+
+// Mode-R halo couplings (partitionedMatvec, partition.cpp:335-350): after the
+// local product, y[row] += sum over the row's halo entries in (localRow,
+// globalCol) order of matvecAdd(block, x[globalCol]).
+__global__ void k_halo(int n, int nhr, const int* __restrict__ hrow, const int* __restrict__ hoff,
+                       const int* __restrict__ hcol, const double* __restrict__ hv, const double* __restrict__ x,
+                       double* __restrict__ y, int rowStart) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nhr * n) return;
+    const int hr = t / n, q = t - hr * n;
+    const size_t o = static_cast<size_t>(rowStart + hrow[hr]) * n + q;
+    double acc = y[o];
+    for (int h = hoff[hr]; h < hoff[hr + 1]; ++h) {
+        const double* blk = hv + static_cast<size_t>(h) * n * n + q * n;
+        const double* xc = x + static_cast<size_t>(hcol[h]) * n;
+        double sb = 0.0;
+        for (int p = 0; p < n; ++p) sb = __dadd_rn(sb, __dmul_rn(blk[p], xc[p]));
+        acc = __dadd_rn(acc, sb);
+    }
+    y[o] = acc;
+}
+void halo_spmv(int n, int nhr, const int* hrow, const int* hoff, const int* hcol, const double* hv, const double* x,
+               double* y, int rowStart, cudaStream_t s) {
+    if (nhr <= 0) return;
+    k_halo<<<(nhr * n + 127) / 128, 128, 0, s>>>(n, nhr, hrow, hoff, hcol, hv, x, y, rowStart);
     count_launch();
 }
 

@@ -125,12 +125,18 @@ void dense_solve(int m, const double* lu, const int* piv, const double* r, doubl
 
 // ------------------------------------------------------ Krylov (K13-K15)
 int reduce_blocks();
-// out[0] = dot(a, b)   (sqrt_out: out[0] = sqrt(dot)); deterministic
-void dot(const double* a, const double* b, size_t N, double* out, bool sqrt_out, double* partials, int* ticket,
-         cudaStream_t s);
+// out[0] = dot(a, b)   (sqrt_out: out[0] = sqrt(dot)); deterministic.  The
+// vector is nseg contiguous segments seg[0..nseg] (device int64 offsets);
+// segment sums are folded with the reference's pairwise engine tree.
+// partials >= reduce_blocks() + 4*nseg doubles.
+void dot(const double* a, const double* b, const long long* seg, int nseg, double* out, bool sqrt_out,
+         double* partials, int* ticket, cudaStream_t s);
 // w -= (*h) * v ; out = dot(w, nextv) (nextv == nullptr: out = sqrt(dot(w,w)))
-void axpy_dot(double* w, const double* h, const double* v, const double* nextv, size_t N, double* out,
-              double* partials, int* ticket, cudaStream_t s);
+void axpy_dot(double* w, const double* h, const double* v, const double* nextv, const long long* seg, int nseg,
+              double* out, double* partials, int* ticket, cudaStream_t s);
+// Mode-R halo adds after the local product (partition.cpp:335-350)
+void halo_spmv(int n, int nhr, const int* hrow, const int* hoff, const int* hcol, const double* hv, const double* x,
+               double* y, int rowStart, cudaStream_t s);
 // y = x / (*den) if (*den > thr) ; else untouched
 void scale_by(const double* x, const double* den, double thr, double* y, size_t N, cudaStream_t s);
 void copy_vec(const double* x, double* y, size_t N, cudaStream_t s);

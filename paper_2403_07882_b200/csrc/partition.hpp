@@ -1,0 +1,53 @@
+// Domain decomposition for Mode R (the reference's distributed semantics,
+// proj/core/src/partition.cpp): RCB on centroids with rank-major renumbering,
+// per-rank local BSR + halo couplings + send plans, consolidation of ranks
+// onto engines.  Integer work, bit-exact with the reference (pinned by
+// tests/test_partition.py).  Values are not copied here: every local slot and
+// halo entry carries the id of its LDU source block (c, nc+f, nc+nf+f) so a
+// value replace is a device gather.
+#pragma once
+
+#include <cstdint>
+#include <utility>
+#include <vector>
+
+namespace bcs {
+
+struct Decomposition {
+    int nRanks = 0;
+    std::vector<int> cellToRank;     // by original cell
+    std::vector<int> rankRowOffset;  // nRanks + 1
+    std::vector<int> oldToNew, newToOld;
+    int rankOfRow(int globalRow) const;
+    int nLocalRows(int r) const { return rankRowOffset[r + 1] - rankRowOffset[r]; }
+};
+
+// partition.cpp:21-85
+Decomposition decompose(int nCells, const double* centroids, int nRanks);
+
+struct Partition {
+    int id = 0;
+    int rowStart = 0, rowEnd = 0;                 // owned global rows (new numbering)
+    std::vector<int> ro, ci, src;                 // local BSR (local numbering) + LDU source ids
+    std::vector<int> haloRow, haloCol, haloPeer;  // sorted by (localRow, globalCol)
+    std::vector<int> haloSrc;
+    std::vector<std::pair<int, int>> sendPlan;    // (peer, localRow), sorted unique
+    std::vector<int> memberRanks;                 // engines only
+    int nLocalRows() const { return rowEnd - rowStart; }
+};
+
+// partition.cpp:123-165 (values by source id)
+std::vector<Partition> buildPartitioned(int nCells, int nFaces, const int32_t* owner, const int32_t* neigh,
+                                        const Decomposition& dec);
+
+struct ConsolidationPlan {
+    int nEngines = 0;
+    std::vector<int> rankToEngine, engineRowOffset;
+};
+// partition.cpp:184-199
+ConsolidationPlan makeConsolidationPlan(const Decomposition& dec, int nEngines);
+// partition.cpp:201-248
+std::vector<Partition> consolidate(const std::vector<Partition>& parts, const ConsolidationPlan& plan,
+                                   const Decomposition& dec);
+
+}  // namespace bcs

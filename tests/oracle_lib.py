@@ -308,3 +308,43 @@ def ref_random_vector(R, nc, n, seed):
     out = np.zeros(nc * n)
     R.L.ref_random_vector(nc, n, seed, ptr(out))
     return out
+
+
+def ref_partition(R, A, centroids, n_ranks, n_engines):
+    """The reference's buildPartitioned (+consolidate when n_engines > 0) as a list of dicts."""
+    L = R.L
+    cen = np.ascontiguousarray(centroids, np.float64).reshape(-1)
+    h = L.ref_partition(A.n_cells, A.nFaces(), A.n, ptr(A.owner), ptr(A.neighbour), ptr(cen), ptr(A.diag),
+                        ptr(A.upper), ptr(A.lower), n_ranks, n_engines)
+    assert h, R.err()
+    out = []
+    try:
+        for p in range(L.ref_part_count(h)):
+            rs, re, nnz, nh, ns = (c_int() for _ in range(5))
+            L.ref_part_sizes(h, p, *(ctypes.byref(x) for x in (rs, re, nnz, nh, ns)))
+            nb = A.n * A.n
+            d = {"row_start": rs.value, "row_end": re.value, "ro": np.zeros(re.value - rs.value + 1, np.int32),
+                 "ci": np.zeros(nnz.value, np.int32), "vals": np.zeros(nnz.value * nb),
+                 "halo_row": np.zeros(nh.value, np.int32), "halo_col": np.zeros(nh.value, np.int32),
+                 "halo_peer": np.zeros(nh.value, np.int32), "halo_vals": np.zeros(nh.value * nb),
+                 "send_peer": np.zeros(ns.value, np.int32), "send_row": np.zeros(ns.value, np.int32)}
+            L.ref_part_get(h, p, *(ptr(d[k]) for k in ("ro", "ci", "vals", "halo_row", "halo_col", "halo_peer",
+                                                        "halo_vals", "send_peer", "send_row")))
+            out.append(d)
+    finally:
+        L.ref_part_free(h)
+    return out
+
+
+def ref_distributed_solve(R, A, b, x0, centroids, n_ranks, n_engines, cfg):
+    L = R.L
+    L.ref_distributed_solve.argtypes = [c_int, c_int, c_int] + [c_void_p] * 8 + [c_int, c_int, c_void_p, c_void_p,
+                                                                                  c_void_p]
+    cen = np.ascontiguousarray(centroids, np.float64).reshape(-1)
+    c = OrCfg(*cfg)
+    x = np.zeros_like(b)
+    rep = RefReport()
+    rc = L.ref_distributed_solve(A.n_cells, A.nFaces(), A.n, ptr(A.owner), ptr(A.neighbour), ptr(cen), ptr(A.diag),
+                                 ptr(A.upper), ptr(A.lower), ptr(b), ptr(x0), n_ranks, n_engines, ctypes.byref(c),
+                                 ptr(x), ctypes.byref(rep))
+    return rc, x, rep

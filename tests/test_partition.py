@@ -1,0 +1,115 @@
+"""Mode-R partition layer (host C++ in libbcs, no device): decompose /
+buildPartitioned / consolidate against the reference (partition.cpp:21-248)
+and the oracle; plus a world-size-2 gloo check that every rank's send plan
+matches its peers' halo columns."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle_lib import ref_mesh_2d, ref_mesh_tube, ref_partition
+from paper_2403_07882_b200 import bcs, gen
+
+
+def gather_src(A, src):
+    nn = A.n * A.n
+    allv = np.concatenate([A.diag.reshape(-1, nn), A.upper.reshape(-1, nn), A.lower.reshape(-1, nn)])
+    return allv[src].reshape(-1)
+
+
+CASES = [("hex", lambda: gen.hex_euler(6, 5, 4)), ("hex_scr", lambda: gen.hex_euler(5, 5, 5, scramble_seed=4)),
+         ("coupled", lambda: gen.hex_coupled(4, 6, 3))]
+
+
+@pytest.mark.parametrize("name,maker", CASES)
+@pytest.mark.parametrize("ranks,engines", [(1, 0), (2, 0), (3, 0), (4, 0), (8, 0), (2, 1), (4, 2), (4, 4), (3, 2),
+                                           (8, 3)])
+def test_partition_matches_reference(ref, name, maker, ranks, engines):
+    s = maker()
+    A = s.A
+    P = bcs.Partition(A.n_cells, A.owner, A.neighbour, s.centroids, ranks, engines)
+    refparts = ref_partition(ref, A, s.centroids, ranks, engines)
+    assert P.count() == len(refparts) == (engines if engines else ranks)
+    for i, rp in enumerate(refparts):
+        p = P.part(i)
+        for k in ("row_start", "row_end"):
+            assert p[k] == rp[k]
+        for k in ("ro", "ci", "halo_row", "halo_col", "halo_peer", "send_peer", "send_row"):
+            assert np.array_equal(p[k], rp[k]), k
+        assert gather_src(A, p["src"]).tobytes() == rp["vals"].tobytes()
+        assert gather_src(A, p["halo_src"]).tobytes() == rp["halo_vals"].tobytes()
+
+
+@pytest.mark.parametrize("ranks", [1, 2, 3, 4, 5, 8])
+def test_decomposition_matches_oracle(oracle, ranks):
+    s = gen.hex_euler(7, 6, 5, scramble_seed=2)
+    P = bcs.Partition(s.A.n_cells, s.A.owner, s.A.neighbour, s.centroids, ranks)
+    a = P.decomposition()
+    b = oracle.decompose(s.centroids, ranks)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+def test_known_answer_decompositions(ref):
+    # test_partition.cpp:48-73: 3x3 mesh on 3 ranks -> rows [0,3,6,9]; tube 100 on 4 -> 25 each
+    nc, o, ne, cen = ref_mesh_2d(ref, 3, 3)
+    P = bcs.Partition(nc, o, ne, cen, 3)
+    assert P.decomposition()[1].tolist() == [0, 3, 6, 9]
+    nc, o, ne, cen = ref_mesh_tube(ref, 100)
+    P = bcs.Partition(nc, o, ne, cen, 4)
+    assert P.decomposition()[1].tolist() == [0, 25, 50, 75, 100]
+
+
+def test_single_rank_has_no_halo():
+    s = gen.hex_euler(4)
+    p = bcs.Partition(s.A.n_cells, s.A.owner, s.A.neighbour, s.centroids, 1).part(0)
+    assert p["halo_row"].size == 0 and p["send_row"].size == 0
+
+
+def test_bad_rank_count_is_invalid_argument():
+    s = gen.hex_euler(2)
+    with pytest.raises(ValueError, match="1 <= nRanks <= nCells"):
+        bcs.Partition(s.A.n_cells, s.A.owner, s.A.neighbour, s.centroids, 9)
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        s = gen.hex_euler(6, 6, 6, scramble_seed=9)
+        P = bcs.Partition(s.A.n_cells, s.A.owner, s.A.neighbour, s.centroids, world)
+        mine = P.part(rank)
+        # what I send to each peer (global rows) and which global columns I need from each peer
+        sends = {int(pp): sorted(set((mine["row_start"] + mine["send_row"][mine["send_peer"] == pp]).tolist()))
+                 for pp in set(mine["send_peer"].tolist())}
+        needs = {int(pp): sorted(set(mine["halo_col"][mine["halo_peer"] == pp].tolist()))
+                 for pp in set(mine["halo_peer"].tolist())}
+        allsends = [None] * world
+        allneeds = [None] * world
+        dist.all_gather_object(allsends, sends)
+        dist.all_gather_object(allneeds, needs)
+        ok = all(allsends[src].get(dst, []) == allneeds[dst].get(src, []) for src in range(world) for dst in range(world)
+                 if src != dst)
+        q.put((rank, ok, sum(len(v) for v in needs.values())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_send_plans_match_halos():
+    import multiprocessing as mp
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _ in res), res
+    assert all(n > 0 for _, _, n in res)
