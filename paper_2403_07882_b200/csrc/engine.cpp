@@ -113,7 +113,7 @@ Engine::~Engine() {
     // free explicitly to keep long-lived processes lean
     auto rel = [&](auto& a) { a.release(stream_); };
     for (auto& L : main_.levels) {
-        rel(L.o_ro); rel(L.o_ci); rel(L.o_dg); rel(L.o_tpos); rel(L.o_v); rel(L.lu); rel(L.rcp); rel(L.recf); rel(L.recb); rel(L.piv); rel(L.order);
+        rel(L.o_ro); rel(L.o_ci); rel(L.o_dg); rel(L.o_tpos); rel(L.o_v); rel(L.lu); rel(L.rcp); rel(L.perm); rel(L.recf); rel(L.recb); rel(L.piv); rel(L.order);
         rel(L.agg); rel(L.members); rel(L.r); rel(L.z); rel(L.res); rel(L.y); rel(L.zb);
     }
     rel(dOwner_); rel(dNeigh_); rel(ro_); rel(ci_); rel(dg_); rel(tpos_); rel(src_); rel(fill_); rel(vals_);
@@ -126,7 +126,7 @@ Engine::~Engine() {
         rel(P.ro); rel(P.ci); rel(P.src); rel(P.dg); rel(P.tpos); rel(P.vals); rel(P.hrow); rel(P.hoff);
         rel(P.hcol); rel(P.hsrc); rel(P.hvals);
         for (auto& L : P.H.levels) {
-            rel(L.o_ro); rel(L.o_ci); rel(L.o_dg); rel(L.o_tpos); rel(L.o_v); rel(L.lu); rel(L.rcp); rel(L.recf);
+            rel(L.o_ro); rel(L.o_ci); rel(L.o_dg); rel(L.o_tpos); rel(L.o_v); rel(L.lu); rel(L.rcp); rel(L.perm); rel(L.recf);
             rel(L.recb); rel(L.piv); rel(L.order); rel(L.agg); rel(L.members); rel(L.r); rel(L.z); rel(L.res);
             rel(L.y); rel(L.zb);
         }
@@ -323,7 +323,8 @@ void Engine::diluSetup(Level& L) {
     const int cell = readErrCell();
     if (cell != big) throw std::runtime_error("DILU setup: singular modified diagonal in cell " + std::to_string(cell));
     L.rcp.ensure(static_cast<size_t>(L.rows) * n_, stream_);
-    make_reciprocals(n_, L.rows, L.lu, L.rcp.p, stream_);
+    L.perm.ensure(static_cast<size_t>(L.rows) * n_, stream_);
+    make_reciprocals(n_, L.rows, L.lu, L.piv, L.rcp.p, L.perm.p, stream_);
     L.recf.ensure(4 * static_cast<size_t>(L.rows), stream_);
     L.recb.ensure(4 * static_cast<size_t>(L.rows), stream_);
     sweep_records(L.rows, L.order, L.ro, L.dg, L.recf.p, L.recb.p, stream_);
@@ -348,7 +349,8 @@ void Engine::lusgsSetup(Level& L) {
     L.depth = level_schedule(L.rows, L.ro, L.ci, L.dg, L.order.p, lvl_.p, cnt_.p, scanTmp_.p, push_.p, err_.p + 2,
                              stream_);
     L.rcp.ensure(static_cast<size_t>(L.rows) * n_, stream_);
-    make_reciprocals(n_, L.rows, L.lu, L.rcp.p, stream_);
+    L.perm.ensure(static_cast<size_t>(L.rows) * n_, stream_);
+    make_reciprocals(n_, L.rows, L.lu, L.piv, L.rcp.p, L.perm.p, stream_);
     L.recf.ensure(4 * static_cast<size_t>(L.rows), stream_);
     L.recb.ensure(4 * static_cast<size_t>(L.rows), stream_);
     sweep_records(L.rows, L.order, L.ro, L.dg, L.recf.p, L.recb.p, stream_);
@@ -522,8 +524,8 @@ void Engine::smootherApply(Level& L, const double* r, double* z, int accumulate)
     double* zb = accumulate ? L.zb.p : z;
     cudaMemsetAsync(L.y.p, 0xFF, N * sizeof(double), stream_);
     cudaMemsetAsync(zb, 0xFF, N * sizeof(double), stream_);
-    sweep_forward(n_, L.rows, L.depth, L.recf, L.ci, L.v, L.lu, L.piv, L.rcp, r, L.y.p, err_.p + 1, stream_);
-    sweep_backward(n_, L.rows, L.depth, L.recb, L.ci, L.v, L.lu, L.piv, L.rcp, L.y, zb, z, accumulate, err_.p + 1,
+    sweep_forward(n_, L.rows, L.depth, L.recf, L.ci, L.v, L.lu, L.perm, L.rcp, r, L.y.p, err_.p + 1, stream_);
+    sweep_backward(n_, L.rows, L.depth, L.recb, L.ci, L.v, L.lu, L.perm, L.rcp, L.y, zb, z, accumulate, err_.p + 1,
                    stream_);
 }
 

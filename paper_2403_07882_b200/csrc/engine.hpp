@@ -58,7 +58,7 @@ struct Level {
     DArray<double> o_v;
     // smoother (DILU or LUSGS) factors + level-sorted schedule
     DArray<double> lu, rcp;
-    DArray<int> piv, order, recf, recb;  // recf/recb: int4 ticket records
+    DArray<int> piv, perm, order, recf, recb;  // perm: composed pivot permutation; recf/recb: int4 records
     int depth = 0;
     // aggregation to level+1
     DArray<int> agg, members;

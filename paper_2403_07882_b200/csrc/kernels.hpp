@@ -69,7 +69,7 @@ void dilu_setup_syncfree(int n, int rows, const int* order, const int* ro, const
 // sync-free sweeps (preconditioner.cpp:128-156 / :29-57). y, zb pre-filled
 // with the pending pattern (0xFF bytes).  accumulate: 0 none, 1 z = 0 + zb,
 // 2 z += zb.  rcp: per-row diagonal reciprocals (make_reciprocals).
-void make_reciprocals(int n, int rows, const double* lu, double* rcp, cudaStream_t s);
+void make_reciprocals(int n, int rows, const double* lu, const int* piv, double* rcp, int* perm, cudaStream_t s);
 // ticket-order records (int4: row, first slot, #deps) for both sweeps
 void sweep_records(int rows, const int* order, const int* ro, const int* dg, int* fwd4, int* bwd4, cudaStream_t s);
 void sweep_forward(int n, int rows, int depth, const int* recf, const int* ci, const double* v, const double* lu,
