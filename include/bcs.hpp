@@ -110,6 +110,42 @@ public:
         return {std::move(x), fromC<Report>(r, be == BCS_BACKEND_HOST_LDU)};
     }
 
+    // Mode R: the multi-rank branch of LinearDispatch::solve
+    // (case_runner.cpp:329-343) — decompose + buildPartitioned +
+    // makeConsolidationPlan + distributedSolve + gatherVector in one call.
+    // b, x0 and the returned x are in the original cell order.
+    template <class Report, class Matrix, class Vector, class Config>
+    std::pair<Vector, Report> distributedSolve(const Matrix& A, const Vector& b, const Vector& x0,
+                                               const Config& cfg, int nRanks, int nEngines) {
+        if (b.blockSize != A.blockSize() || x0.blockSize != A.blockSize() || b.nCells() != A.nCells() ||
+            x0.nCells() != A.nCells())
+            throw std::invalid_argument("distributedSolve: dimension mismatch");
+        const auto& faces = A.mesh().faces();
+        const int nf = A.nFaces();
+        std::vector<int32_t> own(nf), nei(nf);
+        for (int f = 0; f < nf; ++f) {
+            own[f] = faces[f].owner;
+            nei[f] = faces[f].neighbour;
+        }
+        const auto& cen = A.mesh().cellCentroids();
+        std::vector<double> c(3 * cen.size());
+        for (std::size_t i = 0; i < cen.size(); ++i) {
+            c[3 * i] = cen[i].x;
+            c[3 * i + 1] = cen[i].y;
+            c[3 * i + 2] = cen[i].z;
+        }
+        Vector x(A.nCells(), A.blockSize());
+        const bcs_solver_config cc = toC(cfg);
+        bcs_report r{};
+        const bcs_status st = bcs_dist_solve(ctx_, A.nCells(), nf, A.blockSize(), own.data(), nei.data(), c.data(),
+                                             A.diagValues().data(), A.upperValues().data(), A.lowerValues().data(),
+                                             b.values.data(), x0.values.data(), x.values.data(), nRanks, nEngines,
+                                             &cc, &r);
+        if (st != BCS_OK) throwStatus(st, bcs_last_error(ctx_));
+        Report out = fromC<Report>(r, true);
+        return {std::move(x), std::move(out)};
+    }
+
     bcs_ctx* handle() const { return ctx_; }
 
 private:

@@ -304,8 +304,8 @@ bcs_status bcs_selftest(int what, unsigned long long n, unsigned long long seed,
             if (result) *result = ns;
             return;
         }
-        if (what == 20) {  // install (n != 0: device buffer address in seed) / remove the sweep trace
-            bcs::set_sweep_trace(n ? reinterpret_cast<unsigned long long*>(seed) : nullptr);
+        if (what == 20) {  // install (n != 0: device buffer address in seed; n > 1: only sweeps with rows*2+fwd == n) / remove
+            bcs::set_sweep_trace(n ? reinterpret_cast<unsigned long long*>(seed) : nullptr, n > 1 ? static_cast<long long>(n) : 0);
             return;
         }
         if (what != 0) throw std::invalid_argument("bcs_selftest: unknown test");

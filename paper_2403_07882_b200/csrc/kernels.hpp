@@ -81,7 +81,7 @@ void sweep_backward(int n, int rows, int depth, const int* recb, const int* ci, 
 unsigned long long selftest_division(unsigned long long n, unsigned long long seed);
 // total ns of n ping-pong round trips between two SMs (signalling flavour `mode`)
 unsigned long long selftest_pingpong(int mode, int n);
-void set_sweep_trace(unsigned long long* d);
+void set_sweep_trace(unsigned long long* d, long long filter);  // filter: 0 any, else rows*2+fwd
 unsigned long long selftest_chain(int variant, int L, int warps);  // total ns  // diagnostics: per-ticket timing trace
 
 // ------------------------------------------------------------ AMG (K9-K12)
