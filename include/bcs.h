@@ -182,7 +182,7 @@ bcs_status bcs_level_schedule_depth(bcs_ctx* ctx, int level, int* depth);
  * number of bit mismatches (must be 0).  what = 10..14: total ns of n cross-SM
  * ping-pong round trips with signalling flavour what-10 (0 relaxed, 1 relaxed +
  * fence, 2 atomic exchange, 3 volatile, 4 release/acquire).  what = 20: per-row
- * sweep trace into the device buffer at address seed (5 u64 per ticket), n = 0
+ * sweep trace into the device buffer at address seed (8 u64 per ticket), n = 0
  * removes it, n = 1 traces every sweep, n > 1 only sweeps with rows*2+fwd == n.
  * what = 30/31: n-hop minimal chain, total ns. */
 bcs_status bcs_selftest(int what, unsigned long long n, unsigned long long seed, unsigned long long* result);

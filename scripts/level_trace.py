@@ -28,14 +28,14 @@ for i in range(rows):
     if js.size: depth[i] = depth[js].max() + 1
 order = np.lexsort((np.arange(rows), depth))
 nlev = depth.max() + 1
-r = np.random.default_rng(0).uniform(-1, 1, s.A.nCells * N)
+r = np.random.default_rng(0).uniform(-1, 1, s.A.n_cells * N)
 ctx.precond_apply(r)
-buf = torch.zeros(5 * rows, dtype=torch.int64, device="cuda")
+buf = torch.zeros(8 * rows, dtype=torch.int64, device="cuda")
 res = ctypes.c_ulonglong()
 _native.lib().bcs_selftest(20, 2 * rows + 1, buf.data_ptr(), ctypes.byref(res))
 ctx.precond_apply(r)
 _native.lib().bcs_selftest(20, 0, 0, ctypes.byref(res))
-tr = buf.cpu().numpy().reshape(rows, 5).astype(np.float64)
+tr = buf.cpu().numpy().reshape(rows, 8).astype(np.float64)
 ready, stored, cy0, cy1, start = tr[:, 0], tr[:, 1], tr[:, 2], tr[:, 3], tr[:, 4]
 t0 = start.min()
 dl = depth[order]  # ticket -> dependency level
@@ -68,3 +68,15 @@ for d in range(1, min(nlev, 400)):
 lag = np.array(lag)
 print(f"  last row of a level: ready - max(dep stored) median {np.median(lag[:,0]):.0f} ns, "
       f"start - max(dep stored) median {np.median(lag[:,1]):.0f} ns, deps median {np.median(lag[:,2]):.0f}")
+cys = tr[:, 5]
+w6 = buf.cpu().numpy().reshape(rows, 8)[:, 6]
+issue = (w6 & 0xFFFFFFFF).astype(np.float64); fac = (w6 >> 32).astype(np.float64)
+w7 = buf.cpu().numpy().reshape(rows, 8)[:, 7]
+spins = (w7 & 0xFFFFFFFF).astype(np.float64); poll1 = (w7 >> 32).astype(np.float64)
+print(f"  cycles: start->issued median {np.median(issue):.0f} p90 {np.percentile(issue,90):.0f}; "
+      f"start->factors {np.median(fac):.0f}; start->ready {np.median(cy0-cys):.0f} p90 {np.percentile(cy0-cys,90):.0f}")
+print(f"  poll spins: share with 0 {np.mean(spins==0):.2f}, median {np.median(spins):.0f}, p90 {np.percentile(spins,90):.0f}")
+z = spins == 0
+print(f"  rows with no spin: start->ready cycles median {np.median((cy0-cys)[z]):.0f}  (pure overhead: issue+factors+one poll pass per 6 deps)")
+print(f"  no-spin rows: start->first poll returned median {np.median(poll1[z]):.0f} (factors at {np.median(fac[z]):.0f}); "
+      f"first poll -> ready {np.median((cy0-cys)[z]-poll1[z]):.0f} cycles")
