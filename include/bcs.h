@@ -88,6 +88,9 @@ typedef struct {
     int spmv_launches;
     double spmv_ms;     /* summed CUDA-event time of the fine-level SpMV launches */
     int kernel_launches;/* device kernels launched during the call */
+    int sweep_launches; /* smoother sweeps (every level) bracketed by events */
+    double sweep_ms;    /* their summed CUDA-event time */
+    double sweep_bytes; /* their summed algorithmic bytes (sweeps) */
 } bcs_report;
 
 void bcs_default_config(bcs_solver_config* cfg);
@@ -182,7 +185,7 @@ bcs_status bcs_level_schedule_depth(bcs_ctx* ctx, int level, int* depth);
  * number of bit mismatches (must be 0).  what = 10..14: total ns of n cross-SM
  * ping-pong round trips with signalling flavour what-10 (0 relaxed, 1 relaxed +
  * fence, 2 atomic exchange, 3 volatile, 4 release/acquire).  what = 20: per-row
- * sweep trace into the device buffer at address seed (8 u64 per ticket), n = 0
+ * sweep trace into the device buffer at address seed (10 u64 per ticket), n = 0
  * removes it, n = 1 traces every sweep, n > 1 only sweeps with rows*2+fwd == n.
  * what = 30/31: n-hop minimal chain, total ns. */
 bcs_status bcs_selftest(int what, unsigned long long n, unsigned long long seed, unsigned long long* result);

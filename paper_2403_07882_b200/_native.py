@@ -69,6 +69,9 @@ class ReportC(ctypes.Structure):
         ("spmv_launches", c_int),
         ("spmv_ms", c_double),
         ("kernel_launches", c_int),
+        ("sweep_launches", c_int),
+        ("sweep_ms", c_double),
+        ("sweep_bytes", c_double),
     ]
 
 

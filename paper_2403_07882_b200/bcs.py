@@ -80,6 +80,9 @@ class SolveReport:
     spmvLaunches: int = 0
     spmvMs: float = 0.0
     kernelLaunches: int = 0
+    sweepLaunches: int = 0
+    sweepMs: float = 0.0
+    sweepBytes: float = 0.0
 
     @staticmethod
     def from_c(r: N.ReportC, backend: Optional[Backend] = None) -> "SolveReport":
@@ -92,7 +95,7 @@ class SolveReport:
             t["setup"] = 0.0
         return SolveReport(r.iterations, r.initial_residual, r.final_residual, bool(r.converged),
                            bool(r.breakdown), t, r.amg_levels, r.coarse_rows, r.spmv_launches, r.spmv_ms,
-                           r.kernel_launches)
+                           r.kernel_launches, r.sweep_launches, r.sweep_ms, r.sweep_bytes)
 
     def csvRow(self) -> str:  # krylov.cpp:24-34
         g = self.timings.get

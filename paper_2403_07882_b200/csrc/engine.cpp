@@ -97,7 +97,7 @@ Engine::Engine(int device) : device_(device) {
     err_.ensure(4, stream_);
     ctr_.ensure(4, stream_);
     ticket_.ensure(4, stream_);
-    push_.ensure(8, stream_);
+    push_.ensure(16, stream_);
     cudaMemsetAsync(ctr_.p, 0, 4 * sizeof(int), stream_);
     cudaMemsetAsync(ticket_.p, 0, 4 * sizeof(int), stream_);
     partials_.ensure(static_cast<size_t>(reduce_blocks()) + 512, stream_);
@@ -113,12 +113,12 @@ Engine::~Engine() {
     // free explicitly to keep long-lived processes lean
     auto rel = [&](auto& a) { a.release(stream_); };
     for (auto& L : main_.levels) {
-        rel(L.o_ro); rel(L.o_ci); rel(L.o_dg); rel(L.o_tpos); rel(L.o_v); rel(L.lu); rel(L.rcp); rel(L.perm); rel(L.recf); rel(L.recb); rel(L.piv); rel(L.order);
+        rel(L.o_ro); rel(L.o_ci); rel(L.o_dg); rel(L.o_tpos); rel(L.o_v); rel(L.lu); rel(L.rcp); rel(L.perm); rel(L.recf); rel(L.recb); rel(L.dlev); rel(L.offf); rel(L.offb); rel(L.pkf); rel(L.pkb); rel(L.piv); rel(L.order);
         rel(L.agg); rel(L.members); rel(L.r); rel(L.z); rel(L.res); rel(L.y); rel(L.zb);
     }
     rel(dOwner_); rel(dNeigh_); rel(ro_); rel(ci_); rel(dg_); rel(tpos_); rel(src_); rel(fill_); rel(vals_);
     rel(ldu_diag_); rel(ldu_upper_); rel(ldu_lower_); rel(main_.dense); rel(main_.dpiv); rel(cnt_); rel(lvl_); rel(push_);
-    rel(scanTmp_); rel(act2_); rel(flag_); rel(err_); rel(ctr_); rel(choice_); rel(segOff_); rel(cro_); rel(big_); rel(dn_); rel(tblk_);
+    rel(scanTmp_); rel(dkeys_); rel(dorder_); rel(ddesc_); rel(act2_); rel(flag_); rel(err_); rel(ctr_); rel(choice_); rel(segOff_); rel(cro_); rel(big_); rel(dn_); rel(tblk_);
     rel(str_); rel(keys_); rel(sorted_); rel(V_); rel(w_); rel(zk_); rel(rk_); rel(Hm_); rel(cs_); rel(sn_); rel(g_);
     rel(y_); rel(scal_); rel(partials_); rel(kb_); rel(kx_); rel(bp_); rel(bv_); rel(bs_); rel(bt_); rel(bph_);
     rel(bsh_); rel(brh_); rel(ticket_); rel(seg_); rel(distTmp_);
@@ -127,7 +127,7 @@ Engine::~Engine() {
         rel(P.hcol); rel(P.hsrc); rel(P.hvals);
         for (auto& L : P.H.levels) {
             rel(L.o_ro); rel(L.o_ci); rel(L.o_dg); rel(L.o_tpos); rel(L.o_v); rel(L.lu); rel(L.rcp); rel(L.perm); rel(L.recf);
-            rel(L.recb); rel(L.piv); rel(L.order); rel(L.agg); rel(L.members); rel(L.r); rel(L.z); rel(L.res);
+            rel(L.recb); rel(L.dlev); rel(L.offf); rel(L.offb); rel(L.pkf); rel(L.pkb); rel(L.piv); rel(L.order); rel(L.agg); rel(L.members); rel(L.r); rel(L.z); rel(L.res);
             rel(L.y); rel(L.zb);
         }
         rel(P.H.dense); rel(P.H.dpiv);
@@ -244,25 +244,42 @@ void Engine::requireMatrix() const {
 // synchronisation, so timing never adds a host sync inside the solve.
 void Engine::spmvLevel(const Level& L, const double* x, const double* sub, double* y) {
     const bool timed = kernelTiming_ && &L == &H_->levels[0];
-    if (timed) {
-        if (evUsed_ == evPool_.size()) {
-            cudaEvent_t a, b;
-            check(cudaEventCreate(&a), "cudaEventCreate");
-            check(cudaEventCreate(&b), "cudaEventCreate");
-            evPool_.push_back({a, b});
-        }
-        cudaEventRecord(evPool_[evUsed_].first, stream_);
-    }
+    if (timed) timerBegin();
     spmv(n_, L.rows, L.ro, L.ci, L.v, x, sub, y, stream_);
-    if (timed) cudaEventRecord(evPool_[evUsed_++].second, stream_);
+    if (timed) timerEnd(0, 0.0);
+}
+
+void Engine::timerBegin() {
+    if (evUsed_ == evPool_.size()) {
+        cudaEvent_t a, b;
+        check(cudaEventCreate(&a), "cudaEventCreate");
+        check(cudaEventCreate(&b), "cudaEventCreate");
+        evPool_.push_back({a, b});
+        evKind_.push_back(0);
+        evBytes_.push_back(0.0);
+    }
+    cudaEventRecord(evPool_[evUsed_].first, stream_);
+}
+
+void Engine::timerEnd(int kind, double bytes) {
+    cudaEventRecord(evPool_[evUsed_].second, stream_);
+    evKind_[evUsed_] = kind;
+    evBytes_[evUsed_] = bytes;
+    ++evUsed_;
 }
 
 void Engine::collectSpmvTimes() {
     for (size_t i = 0; i < evUsed_; ++i) {
         float ms = 0.f;
         check(cudaEventElapsedTime(&ms, evPool_[i].first, evPool_[i].second), "cudaEventElapsedTime");
-        spmvMs_ += ms;
-        ++spmvCount_;
+        if (evKind_[i] == 0) {
+            spmvMs_ += ms;
+            ++spmvCount_;
+        } else {
+            sweepMs_ += ms;
+            sweepBytes_ += evBytes_[i];
+            ++sweepCount_;
+        }
     }
     evUsed_ = 0;
 }
@@ -294,40 +311,108 @@ static KahnWork kahnWork(DArray<int>& cnt, DArray<int>& push, DArray<int>& lvl, 
     return KahnWork{cnt.p, push.p, lvl.p, lvl2};
 }
 
-void Engine::diluSetup(Level& L) {
+// DILU smoothers of levels [0, nl) (preconditioner.cpp:101-126): dependency
+// levels per matrix, then ONE sync-free factorisation over all of them
+// (tickets ordered by dependency level, then matrix), then the sweeps' data.
+void Engine::diluSetupAll(int nl) {
     const size_t nn = static_cast<size_t>(n_) * n_;
-    L.lu.ensure(L.rows * nn, stream_);
-    L.piv.ensure(static_cast<size_t>(L.rows) * n_, stream_);
-    L.order.ensure(L.rows, stream_);
-    cnt_.ensure(static_cast<size_t>(L.rows) + 2, stream_);
-    lvl_.ensure(static_cast<size_t>(L.rows) + 1, stream_);
-    tblk_.ensure(static_cast<size_t>(L.nnz) * nn, stream_);
     const int big = std::numeric_limits<int>::max();
-    check(cudaMemcpyAsync(err_.p, &big, sizeof(int), cudaMemcpyHostToDevice, stream_), "err init");
-    if (diluMode_ == 0) {
-        // sync-free: dependency levels, then the factorisation in level order
-        scanTmp_.ensure(scan_tmp_ints(static_cast<size_t>(L.rows) + 2) + 16, stream_);
-        cudaMemsetAsync(err_.p + 2, 0, sizeof(int), stream_);
-        L.depth = level_schedule(L.rows, L.ro, L.ci, L.dg, L.order.p, lvl_.p, cnt_.p, scanTmp_.p, push_.p,
-                                 err_.p + 2, stream_);
-        dilu_setup_syncfree(n_, L.rows, L.order, L.ro, L.ci, L.dg, L.tpos, L.v, L.lu.p, L.piv.p, tblk_.p,
-                            static_cast<size_t>(L.nnz) * nn, err_.p, err_.p + 2, stream_);
-        int e2 = 0;
-        check(cudaMemcpyAsync(&e2, err_.p + 2, sizeof(int), cudaMemcpyDeviceToHost, stream_), "err");
-        sync();
-        if (e2) throw std::runtime_error("bcs: DILU setup dependency wait timed out");
-    } else {
-        L.depth = kahn_schedule(n_, L.rows, L.ro, L.ci, L.dg, L.tpos, L.v, true, L.lu.p, L.piv.p, tblk_.p,
-                                L.order.p, kahnWork(cnt_, push_, lvl_), err_.p, stream_);
+    if (diluMode_ != 0) {  // Kahn-rounds variant (BCS_DILU_MODE=1), level by level
+        for (int l = 0; l < nl; ++l) {
+            Level& L = H_->levels[l];
+            L.lu.ensure(L.rows * nn, stream_);
+            L.piv.ensure(static_cast<size_t>(L.rows) * n_, stream_);
+            L.order.ensure(L.rows, stream_);
+            cnt_.ensure(static_cast<size_t>(L.rows) + 2, stream_);
+            lvl_.ensure(static_cast<size_t>(L.rows) + 1, stream_);
+            tblk_.ensure(static_cast<size_t>(L.nnz) * nn, stream_);
+            check(cudaMemcpyAsync(err_.p, &big, sizeof(int), cudaMemcpyHostToDevice, stream_), "err init");
+            L.depth = kahn_schedule(n_, L.rows, L.ro, L.ci, L.dg, L.tpos, L.v, true, L.lu.p, L.piv.p, tblk_.p,
+                                    L.order.p, kahnWork(cnt_, push_, lvl_), err_.p, stream_);
+            const int cell = readErrCell();
+            if (cell != big)
+                throw std::runtime_error("DILU setup: singular modified diagonal in cell " + std::to_string(cell));
+            finishSmoother(L);
+        }
+        return;
     }
-    const int cell = readErrCell();
-    if (cell != big) throw std::runtime_error("DILU setup: singular modified diagonal in cell " + std::to_string(cell));
+    size_t totalRows = 0, totalT = 0;
+    int maxdepth = 0;
+    cudaMemsetAsync(err_.p + 2, 0, sizeof(int), stream_);
+    for (int l = 0; l < nl; ++l) {
+        Level& L = H_->levels[l];
+        L.lu.ensure(L.rows * nn, stream_);
+        L.piv.ensure(static_cast<size_t>(L.rows) * n_, stream_);
+        L.order.ensure(L.rows, stream_);
+        L.dlev.ensure(L.rows, stream_);
+        cnt_.ensure(static_cast<size_t>(L.rows) + 2, stream_);
+        scanTmp_.ensure(scan_tmp_ints(static_cast<size_t>(L.rows) + 2) + 16, stream_);
+        L.depth = level_schedule(L.rows, L.ro, L.ci, L.dg, L.order.p, L.dlev.p, cnt_.p, scanTmp_.p, push_.p,
+                                 err_.p + 2, stream_);
+        totalRows += L.rows;
+        totalT += static_cast<size_t>(L.nnz) * nn;
+        maxdepth = std::max(maxdepth, L.depth);
+    }
+    profMark("dilu:levels");
+    std::vector<DiluLevelHost> desc(nl);
+    size_t toff = 0;
+    for (int l = 0; l < nl; ++l) {
+        Level& L = H_->levels[l];
+        desc[l] = {L.rows, L.ro, L.dg, L.tpos, L.dlev.p, L.v, L.lu.p, L.piv.p, toff};
+        toff += static_cast<size_t>(L.nnz) * nn;
+    }
+    const size_t buckets = static_cast<size_t>(maxdepth) * nl + 1;
+    dkeys_.ensure(totalRows, stream_);
+    dorder_.ensure(totalRows, stream_);
+    cnt_.ensure(buckets + 1, stream_);
+    scanTmp_.ensure(scan_tmp_ints(buckets + 1) + 16, stream_);
+    tblk_.ensure(totalT, stream_);
+    ddesc_.ensure(dilu_desc_bytes(), stream_);
+    check(cudaMemcpyAsync(err_.p, &big, sizeof(int), cudaMemcpyHostToDevice, stream_), "err init");
+    dilu_setup_multi(n_, nl, desc.data(), maxdepth, dkeys_.p, dorder_.p, cnt_.p, scanTmp_.p, push_.p + 8, ddesc_.p,
+                     tblk_.p, totalT, err_.p, err_.p + 2, stream_);
+    int e2 = 0;
+    check(cudaMemcpyAsync(&e2, err_.p + 2, sizeof(int), cudaMemcpyDeviceToHost, stream_), "err");
+    const int cell = readErrCell();  // syncs
+    if (e2) throw std::runtime_error("bcs: DILU setup dependency wait timed out");
+    if (cell != big)
+        throw std::runtime_error("DILU setup: singular modified diagonal in cell " + std::to_string(cell & ((1 << 26) - 1)));
+    profMark("dilu:factor");
+    for (int l = 0; l < nl; ++l) finishSmoother(H_->levels[l]);
+}
+
+// reciprocals, composed permutations, ticket records and packed slots
+void Engine::finishSmoother(Level& L) {
     L.rcp.ensure(static_cast<size_t>(L.rows) * n_, stream_);
     L.perm.ensure(static_cast<size_t>(L.rows) * n_, stream_);
     make_reciprocals(n_, L.rows, L.lu, L.piv, L.rcp.p, L.perm.p, stream_);
     L.recf.ensure(4 * static_cast<size_t>(L.rows), stream_);
     L.recb.ensure(4 * static_cast<size_t>(L.rows), stream_);
     sweep_records(L.rows, L.order, L.ro, L.dg, L.recf.p, L.recb.p, stream_);
+    profMark("dilu:rcp+records");
+    packSweeps(L);
+    profMark("dilu:pack");
+}
+
+// the two sweeps' per-ticket slots (k_sweep.cu: slot layout)
+void Engine::packSweeps(Level& L) {
+    const size_t n1 = static_cast<size_t>(L.rows) + 1;
+    scanTmp_.ensure(scan_tmp_ints(n1) + 16, stream_);
+    int tot[2] = {0, 0};
+    for (int d = 0; d < 2; ++d) {
+        DArray<int>& off = d == 0 ? L.offf : L.offb;
+        off.ensure(n1, stream_);
+        sweep_slot_sizes(n_, L.rows, d == 0 ? L.recf : L.recb, off.p, stream_);
+        exclusive_scan(off.p, L.rows, off.p + L.rows, scanTmp_.p, stream_);
+        check(cudaMemcpyAsync(&tot[d], off.p + L.rows, sizeof(int), cudaMemcpyDeviceToHost, stream_), "slot total");
+    }
+    sync();
+    for (int d = 0; d < 2; ++d) {
+        DArray<unsigned char>& pk = d == 0 ? L.pkf : L.pkb;
+        pk.ensure(16 * static_cast<size_t>(tot[d]), stream_);
+        sweep_pack(n_, d == 0, L.rows, L.depth, d == 0 ? L.recf : L.recb, L.ci, L.v, L.lu, L.perm, L.rcp,
+                   d == 0 ? L.offf : L.offb, pk.p, stream_);
+    }
 }
 
 void Engine::lusgsSetup(Level& L) {
@@ -348,12 +433,7 @@ void Engine::lusgsSetup(Level& L) {
     cudaMemsetAsync(err_.p + 2, 0, sizeof(int), stream_);
     L.depth = level_schedule(L.rows, L.ro, L.ci, L.dg, L.order.p, lvl_.p, cnt_.p, scanTmp_.p, push_.p, err_.p + 2,
                              stream_);
-    L.rcp.ensure(static_cast<size_t>(L.rows) * n_, stream_);
-    L.perm.ensure(static_cast<size_t>(L.rows) * n_, stream_);
-    make_reciprocals(n_, L.rows, L.lu, L.piv, L.rcp.p, L.perm.p, stream_);
-    L.recf.ensure(4 * static_cast<size_t>(L.rows), stream_);
-    L.recb.ensure(4 * static_cast<size_t>(L.rows), stream_);
-    sweep_records(L.rows, L.order, L.ro, L.dg, L.recf.p, L.recb.p, stream_);
+    finishSmoother(L);
 }
 
 void Engine::buildHierarchy(const bcs_solver_config& cfg) {
@@ -438,11 +518,7 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
     }
     H_->levels[H_->nlev - 1].ncoarse = 0;
     // DILU smoother on all but the coarsest level (amg.cpp:86-88)
-    for (int l = 0; l + 1 < H_->nlev; ++l) {
-        diluSetup(H_->levels[l]);
-        profMark("setup:dilu L" + std::to_string(l) + " rows " + std::to_string(H_->levels[l].rows) + " depth " +
-                 std::to_string(H_->levels[l].depth));
-    }
+    diluSetupAll(H_->nlev - 1);
     // dense factorisation of the coarsest level (amg.cpp:90-104)
     const Level& Cl = H_->levels[H_->nlev - 1];
     H_->m = Cl.rows * n_;
@@ -507,7 +583,7 @@ void Engine::buildPrecondOn(const FineMatrix& F, const bcs_solver_config& cfg) {
             L0.y.ensure(N, stream_);
             break;
         case BCS_PRECOND_DILU:
-            diluSetup(L0);
+            diluSetupAll(1);
             L0.y.ensure(N, stream_);
             break;
         case BCS_PRECOND_AMG: buildHierarchy(cfg); break;
@@ -524,9 +600,19 @@ void Engine::smootherApply(Level& L, const double* r, double* z, int accumulate)
     double* zb = accumulate ? L.zb.p : z;
     cudaMemsetAsync(L.y.p, 0xFF, N * sizeof(double), stream_);
     cudaMemsetAsync(zb, 0xFF, N * sizeof(double), stream_);
-    sweep_forward(n_, L.rows, L.depth, L.recf, L.ci, L.v, L.lu, L.perm, L.rcp, r, L.y.p, err_.p + 1, stream_);
-    sweep_backward(n_, L.rows, L.depth, L.recb, L.ci, L.v, L.lu, L.perm, L.rcp, L.y, zb, z, accumulate, err_.p + 1,
-                   stream_);
+    // algorithmic bytes of one sweep: the dependency blocks
+    // + column ids of its triangle, the row's LU/reciprocals/permutation and
+    // record, the input vector read and the output written (+ z update)
+    const double nb = static_cast<double>(n_), R = static_cast<double>(L.rows);
+    const double tri = 0.5 * (static_cast<double>(L.nnz) - R) * (8.0 * nb * nb + 4.0);
+    const double per = tri + R * (8.0 * nb * nb + 8.0 * nb + 4.0 * nb + 16.0) + 2.0 * R * 8.0 * nb;
+    const bool timed = kernelTiming_;
+    if (timed) timerBegin();
+    sweep_forward(n_, L.rows, L.depth, L.offf, L.pkf, L.ci, L.v, r, L.y.p, err_.p + 1, stream_);
+    if (timed) timerEnd(1, per);
+    if (timed) timerBegin();
+    sweep_backward(n_, L.rows, L.depth, L.offb, L.pkb, L.ci, L.v, L.y, zb, z, accumulate, err_.p + 1, stream_);
+    if (timed) timerEnd(1, per + (accumulate == 2 ? 2.0 : accumulate == 1 ? 1.0 : 0.0) * R * 8.0 * nb);
 }
 
 // AmgHierarchy::vcycle (amg.cpp:111-158)
@@ -751,6 +837,9 @@ void Engine::solveDevice(const double* d_b, double* d_x, const bcs_solver_config
     const long long l0 = launches_.launches;
     spmvMs_ = 0.0;
     spmvCount_ = 0;
+    sweepMs_ = 0.0;
+    sweepBytes_ = 0.0;
+    sweepCount_ = 0;
     evUsed_ = 0;
     hist_.clear();
     cudaMemsetAsync(err_.p + 1, 0, sizeof(int), stream_);
@@ -767,6 +856,9 @@ void Engine::solveDevice(const double* d_b, double* d_x, const bcs_solver_config
     rep.coarse_rows = H_->pcKind == BCS_PRECOND_AMG ? H_->levels[H_->nlev - 1].rows : 0;
     rep.spmv_launches = spmvCount_;
     rep.spmv_ms = spmvMs_;
+    rep.sweep_launches = sweepCount_;
+    rep.sweep_ms = sweepMs_;
+    rep.sweep_bytes = sweepBytes_;
     rep.kernel_launches = static_cast<int>(launches_.launches - l0);
     lastSolveLaunches_ = rep.kernel_launches;
 }
@@ -946,6 +1038,9 @@ void Engine::distSolve(int nc, int nf, int n, const int32_t* owner, const int32_
     hist_.clear();
     spmvMs_ = 0.0;
     spmvCount_ = 0;
+    sweepMs_ = 0.0;
+    sweepBytes_ = 0.0;
+    sweepCount_ = 0;
     evUsed_ = 0;
     cudaMemsetAsync(err_.p + 1, 0, sizeof(int), stream_);
     nc_ = nc;

@@ -59,6 +59,9 @@ struct Level {
     // smoother (DILU or LUSGS) factors + level-sorted schedule
     DArray<double> lu, rcp;
     DArray<int> piv, perm, order, recf, recb;  // perm: composed pivot permutation; recf/recb: int4 records
+    DArray<int> offf, offb;                    // per-ticket slot offsets (16-byte units), rows + 1
+    DArray<int> dlev;                          // dependency level of every row
+    DArray<unsigned char> pkf, pkb;            // packed per-ticket slots of the two sweeps
     int depth = 0;
     // aggregation to level+1
     DArray<int> agg, members;
@@ -151,8 +154,10 @@ private:
     FineMatrix serialFine() const;
     void buildHierarchy(const bcs_solver_config& cfg);
     void setupLevelPattern(Level& L);
-    void diluSetup(Level& L);
+    void diluSetupAll(int nl);
+    void finishSmoother(Level& L);
     void lusgsSetup(Level& L);
+    void packSweeps(Level& L);
     void applyPrecond(const double* r, double* z);
     void smootherApply(Level& L, const double* r, double* z, int accumulate);
     void vcycle(int l, const double* r, double* z);
@@ -197,6 +202,8 @@ private:
     // scratch
     DArray<int> cnt_, lvl_, act2_, push_, scanTmp_, flag_, err_, ctr_, choice_, segOff_, cro_, big_;
     DArray<double> dn_, str_, tblk_;
+    DArray<int> dkeys_, dorder_;       // combined DILU tickets
+    DArray<unsigned char> ddesc_;      // device level descriptors of the combined DILU setup
     DArray<unsigned long long> keys_, sorted_;
 
     // Krylov workspace
@@ -233,6 +240,12 @@ private:
     int lastSolveLaunches_ = 0;
     double spmvMs_ = 0.0;
     int spmvCount_ = 0;
+    std::vector<int> evKind_;      // 0: fine-level SpMV, 1: sweep (any level)
+    std::vector<double> evBytes_;  // algorithmic bytes of the timed launch
+    double sweepMs_ = 0.0, sweepBytes_ = 0.0;
+    int sweepCount_ = 0;
+    void timerBegin();
+    void timerEnd(int kind, double bytes);
 };
 
 }  // namespace bcs

@@ -62,21 +62,42 @@ int kahn_schedule(int n, int rows, const int* ro, const int* ci, const int* dg, 
 // level: rows ints, cnt: rows+2 ints, small: >= 3 ints
 int level_schedule(int rows, const int* ro, const int* ci, const int* dg, int* order, int* level, int* cnt,
                    int* scan_tmp, int* small, int* err, cudaStream_t s);
-// DILU setup (preconditioner.cpp:101-126), sync-free in level order; T: tcount doubles scratch
-void dilu_setup_syncfree(int n, int rows, const int* order, const int* ro, const int* ci, const int* dg,
-                         const int* tpos, const double* v, double* lu, int* piv, double* T, size_t tcount,
-                         int* err_cell, int* err, cudaStream_t s);
+// DILU setup (preconditioner.cpp:101-126) of several matrices at once (the
+// AMG levels but the coarsest), sync-free: tickets ordered by (dependency
+// level, matrix).  dlev: the matrix's dependency levels (level_schedule);
+// T: scratch of sum(nnz)*n*n doubles, matrix l at Tbase + tOff; keys/order:
+// sum(rows) ints; cnt: maxdepth*nl+1 ints; desc_dev: dilu_desc_bytes().
+// *err_cell = min over singular rows of (matrix << 26 | row).
+struct DiluLevelHost {
+    int rows;
+    const int *ro, *dg, *tpos, *dlev;
+    const double* v;
+    double* lu;
+    int* piv;
+    size_t tOff;
+};
+void dilu_setup_multi(int n, int nl, const DiluLevelHost* levels, int maxdepth, int* keys, int* order, int* cnt,
+                      int* scan_tmp, int* small, void* desc_dev, double* Tbase, size_t tcount, int* err_cell,
+                      int* err, cudaStream_t s);
+size_t dilu_desc_bytes();
 // sync-free sweeps (preconditioner.cpp:128-156 / :29-57). y, zb pre-filled
 // with the pending pattern (0xFF bytes).  accumulate: 0 none, 1 z = 0 + zb,
 // 2 z += zb.  rcp: per-row diagonal reciprocals (make_reciprocals).
 void make_reciprocals(int n, int rows, const double* lu, const int* piv, double* rcp, int* perm, cudaStream_t s);
 // ticket-order records (int4: row, first slot, #deps) for both sweeps
 void sweep_records(int rows, const int* order, const int* ro, const int* dg, int* fwd4, int* bwd4, cudaStream_t s);
-void sweep_forward(int n, int rows, int depth, const int* recf, const int* ci, const double* v, const double* lu,
-                   const int* piv, const double* rcp, const double* r, double* y, int* err, cudaStream_t s);
-void sweep_backward(int n, int rows, int depth, const int* recb, const int* ci, const double* v, const double* lu,
-                    const int* piv, const double* rcp, const double* y, double* zb, double* z, int accumulate,
-                    int* err, cudaStream_t s);
+// per-ticket slots (the sweep program): slot sizes in 16-byte units into
+// off16 (rows entries; the caller scans them, off16[rows] = total), then the
+// packed slots of one direction (rec4 = that direction's records).
+void sweep_slot_sizes(int n, int rows, const int* rec4, int* off16, cudaStream_t s);
+void sweep_pack(int n, bool fwd, int rows, int depth, const int* rec4, const int* ci, const double* v,
+                const double* lu, const int* perm, const double* rcp, const int* off16, unsigned char* pk,
+                cudaStream_t s);
+void sweep_forward(int n, int rows, int depth, const int* off16, const unsigned char* pk, const int* ci,
+                   const double* v, const double* r, double* y, int* err, cudaStream_t s);
+void sweep_backward(int n, int rows, int depth, const int* off16, const unsigned char* pk, const int* ci,
+                    const double* v, const double* y, double* zb, double* z, int accumulate, int* err,
+                    cudaStream_t s);
 // number of mismatches of the reciprocal-based division against __ddiv_rn
 unsigned long long selftest_division(unsigned long long n, unsigned long long seed);
 // total ns of n ping-pong round trips between two SMs (signalling flavour `mode`)

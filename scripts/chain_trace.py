@@ -14,12 +14,12 @@ ctx = bcs.Context(0); ctx.set_topology(A); ctx.upload_ldu(A)
 ctx.precond_setup(bcs.SolverConfig(preconditioner=bcs.PrecondKind.DILU))
 r = rng.uniform(-1, 1, L * 5)
 ctx.precond_apply(r)
-buf = torch.zeros(8 * L, dtype=torch.int64, device="cuda")
+buf = torch.zeros(10 * L, dtype=torch.int64, device="cuda")
 res = ctypes.c_ulonglong()
 _native.lib().bcs_selftest(20, 1, buf.data_ptr(), ctypes.byref(res))
 ctx.precond_apply(r)   # fwd then bwd: trace holds the bwd sweep (last writer)
 _native.lib().bcs_selftest(20, 0, 0, ctypes.byref(res))
-tr = buf.cpu().numpy().reshape(L, 8).astype(np.float64)
+tr = buf.cpu().numpy().reshape(L, 10).astype(np.float64)
 gt0, gt1, cy0, cy1, gts = tr[:, 0], tr[:, 1], tr[:, 2], tr[:, 3], tr[:, 4]
 comp = cy1 - cy0
 sig = gt0[1:] - gt1[:-1]

@@ -30,12 +30,12 @@ order = np.lexsort((np.arange(rows), depth))
 nlev = depth.max() + 1
 r = np.random.default_rng(0).uniform(-1, 1, s.A.n_cells * N)
 ctx.precond_apply(r)
-buf = torch.zeros(8 * rows, dtype=torch.int64, device="cuda")
+buf = torch.zeros(10 * rows, dtype=torch.int64, device="cuda")
 res = ctypes.c_ulonglong()
 _native.lib().bcs_selftest(20, 2 * rows + 1, buf.data_ptr(), ctypes.byref(res))
 ctx.precond_apply(r)
 _native.lib().bcs_selftest(20, 0, 0, ctypes.byref(res))
-tr = buf.cpu().numpy().reshape(rows, 8).astype(np.float64)
+tr = buf.cpu().numpy().reshape(rows, 10).astype(np.float64)
 ready, stored, cy0, cy1, start = tr[:, 0], tr[:, 1], tr[:, 2], tr[:, 3], tr[:, 4]
 t0 = start.min()
 dl = depth[order]  # ticket -> dependency level
@@ -69,9 +69,9 @@ lag = np.array(lag)
 print(f"  last row of a level: ready - max(dep stored) median {np.median(lag[:,0]):.0f} ns, "
       f"start - max(dep stored) median {np.median(lag[:,1]):.0f} ns, deps median {np.median(lag[:,2]):.0f}")
 cys = tr[:, 5]
-w6 = buf.cpu().numpy().reshape(rows, 8)[:, 6]
+w6 = buf.cpu().numpy().reshape(rows, 10)[:, 6]
 issue = (w6 & 0xFFFFFFFF).astype(np.float64); fac = (w6 >> 32).astype(np.float64)
-w7 = buf.cpu().numpy().reshape(rows, 8)[:, 7]
+w7 = buf.cpu().numpy().reshape(rows, 10)[:, 7]
 spins = (w7 & 0xFFFFFFFF).astype(np.float64); poll1 = (w7 >> 32).astype(np.float64)
 print(f"  cycles: start->issued median {np.median(issue):.0f} p90 {np.percentile(issue,90):.0f}; "
       f"start->factors {np.median(fac):.0f}; start->ready {np.median(cy0-cys):.0f} p90 {np.percentile(cy0-cys,90):.0f}")
@@ -80,3 +80,8 @@ z = spins == 0
 print(f"  rows with no spin: start->ready cycles median {np.median((cy0-cys)[z]):.0f}  (pure overhead: issue+factors+one poll pass per 6 deps)")
 print(f"  no-spin rows: start->first poll returned median {np.median(poll1[z]):.0f} (factors at {np.median(fac[z]):.0f}); "
       f"first poll -> ready {np.median((cy0-cys)[z]-poll1[z]):.0f} cycles")
+w9 = buf.cpu().numpy().reshape(rows, 10)[:, 9]
+plain = (w9 & 0xFFFFFFFF).astype(np.float64); ry = (w9 >> 32).astype(np.float64)
+print(f"  probe RTT (settled rin line): strong median {np.median(tr[:,8]):.0f} p90 {np.percentile(tr[:,8],90):.0f}; "
+      f"ld.cg median {np.median(plain):.0f} p90 {np.percentile(plain,90):.0f} cycles")
+print(f"  first dependency poll RTT (no-spin rows): median {np.median(ry[z]):.0f} p90 {np.percentile(ry[z],90):.0f}; all rows median {np.median(ry):.0f}")

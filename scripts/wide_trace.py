@@ -20,12 +20,12 @@ for K, L in [(1, 4000), (2048, 200), (8192, 64)]:
     ctx.precond_setup(bcs.SolverConfig(preconditioner=bcs.PrecondKind.DILU))
     r = rng.uniform(-1, 1, rows * 5)
     ctx.precond_apply(r)
-    buf = torch.zeros(8 * rows, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(10 * rows, dtype=torch.int64, device="cuda")
     res = ctypes.c_ulonglong()
     _native.lib().bcs_selftest(20, 1, buf.data_ptr(), ctypes.byref(res))
     ctx.precond_apply(r)
     _native.lib().bcs_selftest(20, 0, 0, ctypes.byref(res))
-    tr = buf.cpu().numpy().reshape(rows, 8).astype(np.float64)
+    tr = buf.cpu().numpy().reshape(rows, 10).astype(np.float64)
     ready, stored, cy0, cy1, start = tr[:, 0], tr[:, 1], tr[:, 2], tr[:, 3], tr[:, 4]
     t0 = start.min()
     span = stored.max() - t0
