@@ -187,7 +187,8 @@ bcs_status bcs_level_schedule_depth(bcs_ctx* ctx, int level, int* depth);
  * fence, 2 atomic exchange, 3 volatile, 4 release/acquire).  what = 20: per-row
  * sweep trace into the device buffer at address seed (10 u64 per ticket), n = 0
  * removes it, n = 1 traces every sweep, n > 1 only sweeps with rows*2+fwd == n.
- * what = 30/31: n-hop minimal chain, total ns. */
+ * what = 30/31: n-hop minimal chain, total ns.  what = 40..44: cycles of n
+ * dependent dadd / dmul / dfma / f64 shuffle / b32 shuffle on one warp. */
 bcs_status bcs_selftest(int what, unsigned long long n, unsigned long long seed, unsigned long long* result);
 
 #ifdef __cplusplus

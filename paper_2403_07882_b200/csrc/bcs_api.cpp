@@ -298,6 +298,11 @@ bcs_status bcs_selftest(int what, unsigned long long n, unsigned long long seed,
             if (result) *result = ns;
             return;
         }
+        if (what >= 40 && what <= 44) {  // dependent-op latency: cycles of n ops
+            const unsigned long long c = bcs::selftest_latency(what - 40, static_cast<int>(n));
+            if (result) *result = c;
+            return;
+        }
         if (what == 30 || what == 31) {  // minimal chain: n = steps, seed = warps
             const unsigned long long ns = bcs::selftest_chain(what - 30, static_cast<int>(n), static_cast<int>(seed));
             bcs::check(cudaDeviceSynchronize(), "selftest");

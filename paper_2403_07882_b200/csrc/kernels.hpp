@@ -100,6 +100,7 @@ void sweep_backward(int n, int rows, int depth, const int* off16, const unsigned
                     cudaStream_t s);
 // number of mismatches of the reciprocal-based division against __ddiv_rn
 unsigned long long selftest_division(unsigned long long n, unsigned long long seed);
+unsigned long long selftest_latency(int op, int n);  // cycles of n dependent ops (0 dadd 1 dmul 2 dfma 3 shfl.f64 4 shfl.b32)
 // total ns of n ping-pong round trips between two SMs (signalling flavour `mode`)
 unsigned long long selftest_pingpong(int mode, int n);
 void set_sweep_trace(unsigned long long* d, long long filter);  // filter: 0 any, else rows*2+fwd
