@@ -97,7 +97,7 @@ Engine::Engine(int device) : device_(device) {
     err_.ensure(4, stream_);
     ctr_.ensure(4, stream_);
     ticket_.ensure(4, stream_);
-    push_.ensure(16, stream_);
+    push_.ensure(64, stream_);
     cudaMemsetAsync(ctr_.p, 0, 4 * sizeof(int), stream_);
     cudaMemsetAsync(ticket_.p, 0, 4 * sizeof(int), stream_);
     partials_.ensure(static_cast<size_t>(reduce_blocks()) + 512, stream_);
@@ -336,22 +336,29 @@ void Engine::diluSetupAll(int nl) {
         }
         return;
     }
-    size_t totalRows = 0, totalT = 0;
+    size_t totalRows = 0, totalT = 0, maxRows = 0;
     int maxdepth = 0;
     cudaMemsetAsync(err_.p + 2, 0, sizeof(int), stream_);
+    std::vector<LevelsHost> lh(nl);
     for (int l = 0; l < nl; ++l) {
         Level& L = H_->levels[l];
         L.lu.ensure(L.rows * nn, stream_);
         L.piv.ensure(static_cast<size_t>(L.rows) * n_, stream_);
         L.order.ensure(L.rows, stream_);
         L.dlev.ensure(L.rows, stream_);
-        cnt_.ensure(static_cast<size_t>(L.rows) + 2, stream_);
-        scanTmp_.ensure(scan_tmp_ints(static_cast<size_t>(L.rows) + 2) + 16, stream_);
-        L.depth = level_schedule(L.rows, L.ro, L.ci, L.dg, L.order.p, L.dlev.p, cnt_.p, scanTmp_.p, push_.p,
-                                 err_.p + 2, stream_);
+        lh[l] = {L.rows, L.ro, L.ci, L.dg, L.dlev.p, L.order.p};
         totalRows += L.rows;
         totalT += static_cast<size_t>(L.nnz) * nn;
-        maxdepth = std::max(maxdepth, L.depth);
+        maxRows = std::max(maxRows, static_cast<size_t>(L.rows));
+    }
+    cnt_.ensure(maxRows + 2, stream_);
+    scanTmp_.ensure(scan_tmp_ints(maxRows + 2) + 16, stream_);
+    ddesc_.ensure(dilu_desc_bytes(), stream_);
+    std::vector<int> depth(nl, 0);
+    level_schedule_multi(nl, lh.data(), depth.data(), cnt_.p, scanTmp_.p, push_.p, ddesc_.p, err_.p + 2, stream_);
+    for (int l = 0; l < nl; ++l) {
+        H_->levels[l].depth = depth[l];
+        maxdepth = std::max(maxdepth, depth[l]);
     }
     profMark("dilu:levels");
     std::vector<DiluLevelHost> desc(nl);

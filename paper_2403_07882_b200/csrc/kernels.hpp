@@ -80,6 +80,16 @@ void dilu_setup_multi(int n, int nl, const DiluLevelHost* levels, int maxdepth, 
                       int* scan_tmp, int* small, void* desc_dev, double* Tbase, size_t tcount, int* err_cell,
                       int* err, cudaStream_t s);
 size_t dilu_desc_bytes();
+// dependency levels + level-ordered schedules of several matrices in one
+// sync-free pass; depth[l] out; small >= 2 + nl ints; cnt >= max depth + 2.
+struct LevelsHost {
+    int rows;
+    const int *ro, *ci, *dg;
+    int* level;
+    int* order;
+};
+void level_schedule_multi(int nl, const LevelsHost* lv, int* depth, int* cnt, int* scan_tmp, int* small,
+                          void* desc_dev, int* err, cudaStream_t s);
 // sync-free sweeps (preconditioner.cpp:128-156 / :29-57). y, zb pre-filled
 // with the pending pattern (0xFF bytes).  accumulate: 0 none, 1 z = 0 + zb,
 // 2 z += zb.  rcp: per-row diagonal reciprocals (make_reciprocals).
