@@ -271,6 +271,9 @@ __global__ void k_agg_fill(int rows, int* choice) {
     if (r < rows) choice[r] = kUndecided;
 }
 
+// Resumable per-row state of the lazy greedy decision: every attempt
+// continues from the first input that was still undecided, so a row issues
+// one dependent load chain over its whole lifetime instead of one per attempt.
 __global__ void __launch_bounds__(256) k_agg_syncfree(int rows, const int* __restrict__ ro, const int* __restrict__ ci,
                                                       const int* __restrict__ dg, const int* __restrict__ tpos,
                                                       const double* __restrict__ str, int* choice, int* err) {
@@ -280,10 +283,72 @@ __global__ void __launch_bounds__(256) k_agg_syncfree(int rows, const int* __res
     for (int base = base0; base < rows; base += T) {
         const int r = base + (threadIdx.x & 31);
         bool done = r >= rows;
+        // phase A: lower neighbours of r (was r taken by one of them?)
+        int k = done ? 0 : __ldg(&ro[r]);
+        const int d = done ? 0 : __ldg(&dg[r]);
+        const int e = done ? 0 : __ldg(&ro[r + 1]);
+        bool phaseB = false;
+        // phase B: current candidate (preference order: strength desc, slot asc)
+        double lastS = 0.0;
+        int lastK = -1, j = -1, kk = 0, tp = 0;
         unsigned spins = 0;
         while (!__all_sync(0xffffffffu, done)) {
             if (!done) {
-                const int dec = agg_try_thread(r, ro, ci, dg, tpos, str, choice);
+                int dec = kUndecided;
+                if (!phaseB) {
+                    for (; k < d; ++k) {
+                        const int c = ld_choice(&choice[__ldg(&ci[k])]);
+                        if (c == kUndecided) break;
+                        if (c == r) {
+                            dec = kTaken;
+                            break;
+                        }
+                    }
+                    if (dec == kUndecided && k == d) phaseB = true;
+                }
+                while (phaseB && dec == kUndecided) {
+                    if (j < 0) {  // next candidate after (lastS, lastK)
+                        double bs = 0.0;
+                        int bk = -1;
+                        for (int q = d + 1; q < e; ++q) {
+                            const double sv = __ldg(&str[q]);
+                            if (!(sv > -1.0)) continue;
+                            if (lastK >= 0 && !(sv < lastS || (sv == lastS && q > lastK))) continue;
+                            if (bk < 0 || sv > bs) {
+                                bs = sv;
+                                bk = q;
+                            }
+                        }
+                        if (bk < 0) {
+                            dec = kSingle;
+                            break;
+                        }
+                        lastS = bs;
+                        lastK = bk;
+                        j = __ldg(&ci[bk]);
+                        tp = __ldg(&tpos[bk]);
+                        kk = __ldg(&ro[j]);
+                    }
+                    // was j taken by one of its lower neighbours below r?
+                    bool taken = false, wait = false;
+                    for (; kk < tp; ++kk) {
+                        const int c = ld_choice(&choice[__ldg(&ci[kk])]);
+                        if (c == kUndecided) {
+                            wait = true;
+                            break;
+                        }
+                        if (c == j) {
+                            taken = true;
+                            break;
+                        }
+                    }
+                    if (wait) break;
+                    if (taken) {
+                        j = -1;
+                        continue;
+                    }
+                    dec = j;
+                }
                 if (dec != kUndecided) {
                     asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(&choice[r]), "r"(dec) : "memory");
                     done = true;
