@@ -84,6 +84,7 @@ Engine::Engine(int device) : device_(device) {
     prof_ = std::getenv("BCS_PROFILE") != nullptr;
     if (const char* m = std::getenv("BCS_AGG_MODE")) aggMode_ = std::atoi(m);    // 1: barrier rounds
     if (const char* m = std::getenv("BCS_DILU_MODE")) diluMode_ = std::atoi(m);  // 1: Kahn levels
+    if (const char* m = std::getenv("BCS_DENSE_BLOCKED_MIN")) denseBlockedMin_ = std::atoi(m);
     check(cudaSetDevice(device), "cudaSetDevice");
     check(cudaStreamCreateWithFlags(&own_, cudaStreamNonBlocking), "cudaStreamCreate");
     stream_ = own_;
@@ -530,10 +531,11 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
     const Level& Cl = H_->levels[H_->nlev - 1];
     H_->m = Cl.rows * n_;
     H_->dense.ensure(static_cast<size_t>(H_->m) * H_->m, stream_);
-    H_->dpiv.ensure(H_->m, stream_);
+    H_->dpiv.ensure(2 * static_cast<size_t>(H_->m), stream_);
     dense_build(n_, Cl.rows, Cl.ro, Cl.ci, Cl.v, H_->dense.p, stream_);
     cudaMemsetAsync(err_.p, 0, sizeof(int), stream_);
-    dense_factor(H_->m, H_->dense.p, H_->dpiv.p, err_.p, stream_);
+    if (H_->m >= denseBlockedMin_) dense_factor_blocked(H_->m, H_->dense.p, H_->dpiv.p, err_.p, stream_);
+    else dense_factor(H_->m, H_->dense.p, H_->dpiv.p, err_.p, stream_);
     if (readErrCell()) throw std::runtime_error("singular coarse-level matrix");
     profMark("setup:dense");
     // V-cycle vectors
@@ -627,7 +629,8 @@ void Engine::vcycle(int l, const double* r, double* z) {
     Level& L = H_->levels[l];
     const size_t N = static_cast<size_t>(L.rows) * n_;
     if (l == H_->nlev - 1) {
-        dense_solve(H_->m, H_->dense, H_->dpiv, r, z, stream_);
+        if (H_->m >= denseBlockedMin_) dense_solve_big(H_->m, H_->dense, H_->dpiv, r, z, stream_);
+        else dense_solve(H_->m, H_->dense, H_->dpiv, r, z, stream_);
         profMark("vcycle:dense_solve");
         return;
     }

@@ -230,6 +230,7 @@ private:
     bool prof_ = false;
     int aggMode_ = 0;   // 0 sync-free aggregation, 1 cooperative rounds
     int diluMode_ = 0;  // 0 sync-free level-ordered DILU setup, 1 Kahn levels
+    int denseBlockedMin_ = kDenseBlockedMin;  // coarsest m from which the blocked dense LU/solve run
     std::vector<std::pair<std::string, double>> profRec_;
     std::chrono::steady_clock::time_point profT_;
     void profMark(const std::string& what);

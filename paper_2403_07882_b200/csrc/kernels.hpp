@@ -154,6 +154,11 @@ void prolong_vec(int n, int rows, const int* agg, const double* zc, double* z, c
 void dense_build(int n, int rows, const int* ro, const int* ci, const double* v, double* dense, cudaStream_t s);
 void dense_factor(int m, double* a, int* piv, int* err, cudaStream_t s);
 void dense_solve(int m, const double* lu, const int* piv, const double* r, double* z, cudaStream_t s);
+// blocked variants for large coarsest levels (k_dense.cu); piv: 2m ints
+// (pivots, then the composed permutation the solve uses)
+constexpr int kDenseBlockedMin = 256;
+void dense_factor_blocked(int m, double* a, int* piv, int* err, cudaStream_t s);
+void dense_solve_big(int m, const double* lu, const int* piv, const double* r, double* z, cudaStream_t s);
 
 // ------------------------------------------------------ Krylov (K13-K15)
 int reduce_blocks();

@@ -1,0 +1,54 @@
+"""Large coarsest levels (scrambled inputs): the blocked
+dense LU and solve (csrc/k_dense.cu) against the oracle's denseFactor /
+denseSolve restatement through whole V-cycle applications, bit for bit."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle_lib import make_cfg
+from paper_2403_07882_b200 import bcs, gen
+
+pytestmark = pytest.mark.gpu
+
+
+def _apply(ctx, s, cfg_t, r):
+    ctx.set_topology(s.A)
+    ctx.upload_ldu(s.A)
+    ctx.precond_setup(bcs.SolverConfig(preconditioner=bcs.PrecondKind.AMG,
+                                       amg=bcs.AmgConfig(maxLevels=cfg_t[6], minCoarseRows=cfg_t[7])))
+    return ctx.precond_apply(r)
+
+
+@pytest.mark.parametrize("threshold", ["1", "64", "65"])
+def test_blocked_dense_forced_small(oracle, threshold, monkeypatch):
+    """Scrambled 32^3: the blocked path forced on a small coarsest level
+    (threshold 1 / 64 / 65 covers one- and two-panel factorisations)."""
+    monkeypatch.setenv("BCS_DENSE_BLOCKED_MIN", threshold)
+    ctx = bcs.Context(0)
+    try:
+        s = gen.hex_euler(32, scramble_seed=7)
+        cfg = make_cfg(precond=3, max_levels=30, min_coarse=8)
+        r = np.random.default_rng(5).uniform(-1, 1, s.A.n_cells * s.A.n)
+        z = _apply(ctx, s, cfg, r)
+        zo = oracle.precond_apply(s.A, cfg, r)
+        assert z.tobytes() == zo.tobytes()
+    finally:
+        ctx.close()
+
+
+def test_blocked_dense_scrambled64(oracle):
+    """Scrambled 64^3 hits the 30-level cap with m = 665: the blocked path by default."""
+    ctx = bcs.Context(0)
+    try:
+        s = gen.hex_euler(64, scramble_seed=7)
+        cfg = make_cfg(precond=3, max_levels=30, min_coarse=8)
+        r = np.random.default_rng(6).uniform(-1, 1, s.A.n_cells * s.A.n)
+        z = _apply(ctx, s, cfg, r)
+        assert ctx.amg_depth() == 30
+        rows, _ = ctx.amg_level(29, s.A.n)[0].size - 1, None
+        assert rows * s.A.n >= 256, "expected a coarsest level large enough for the blocked path"
+        zo = oracle.precond_apply(s.A, cfg, r)
+        assert z.tobytes() == zo.tobytes()
+    finally:
+        ctx.close()
