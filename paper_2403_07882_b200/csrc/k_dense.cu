@@ -426,23 +426,39 @@ __global__ void __launch_bounds__(1024) k_dense_solve_big(int m, const double* _
     // precompute row i-1's products t_q = RN(U_{i-1,i-1+q} x_{i-1+q}) for
     // q >= 2 (those x are final) while row i is processed, so the chain is
     // one rounded subtraction per step read from shared memory
+    // (zero padding to the next multiple of 16 plus one block: x - (+0) == x
+    // exactly, so the chain runs in whole blocks)
     auto stage = [&](int i, double* dst) {
         const double* row = lu + static_cast<size_t>(i) * m;
         if (tid - 32 == 0) dst[0] = row[i];
-        for (int j = i + 2 + (tid - 32); j < m; j += nt - 32) dst[j - i] = __dmul_rn(row[j], x[j]);
+        const int pad = ((m - i + 15) & ~15) + 48;  // every index the chain loads
+        for (int q = 2 + (tid - 32); q < pad; q += nt - 32) dst[q] = i + q < m ? __dmul_rn(row[i + q], x[i + q]) : 0.0;
     };
-    if (SX && wid > 0) stage(m - 1, ub);
+    if (SX && wid > 0) stage(m - 1, ub);  // two buffers of m + 64
     __syncthreads();
     for (int i = m - 1; i >= 0; --i) {
-        double* nxt = ub + ((m - i) & 1) * m;
+        double* nxt = ub + ((m - i) & 1) * (m + 64);
         if (tid == 0) {
             double xi = x[i];
             const int len = m - i;
             if (SX) {
-                const double* t = ub + ((m - 1 - i) & 1) * m;  // t[0] = U_ii, t[q >= 2] = products
+                const double* t = ub + ((m - 1 - i) & 1) * (m + 64);  // t[0] = U_ii, t[q >= 2] = products
                 if (len > 1) xi = __dsub_rn(xi, __dmul_rn(lu[static_cast<size_t>(i) * m + i + 1], x[i + 1]));
-#pragma unroll 16
-                for (int q = 2; q < len; ++q) xi = __dsub_rn(xi, t[q]);
+                // blocks of 16: the next block's loads are in flight while
+                // the current one is folded
+                double A[16], B[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) A[q] = q >= 2 ? t[q] : 0.0;
+                for (int q0 = 16; q0 < len + 16; q0 += 32) {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) B[q] = t[q0 + q];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) xi = __dsub_rn(xi, A[q]);
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) A[q] = t[q0 + 16 + q];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) xi = __dsub_rn(xi, B[q]);
+                }
                 x[i] = __ddiv_rn(xi, t[0]);
             } else {
                 const double* cur = lu + static_cast<size_t>(i) * m + i;
@@ -462,7 +478,7 @@ __global__ void __launch_bounds__(1024) k_dense_solve_big(int m, const double* _
 constexpr size_t kDenseSmemMax = 200 * 1024;
 
 void dense_solve_big(int m, const double* lu, const int* piv, const double* r, double* z, cudaStream_t s) {
-    const size_t full = (static_cast<size_t>(32) * 33 + 3 * static_cast<size_t>(m)) * sizeof(double);
+    const size_t full = (static_cast<size_t>(32) * 33 + 3 * static_cast<size_t>(m) + 128) * sizeof(double);
     const bool sx = full <= kDenseSmemMax;
     const size_t smem = sx ? full : static_cast<size_t>(32) * 33 * sizeof(double);
     static bool attr = false;

@@ -20,4 +20,4 @@ for i in range(2):
     t = time.perf_counter()
     r = ctx.solve(s.b.values, x, cfg)
     print(f"solve {i}: {time.perf_counter()-t:.3f}s iters={r.iterations} levels={r.amgLevels} "
-          f"setup={r.timings['amgSetup']:.3f} krylov={r.timings['krylov']:.3f}", file=sys.stderr, flush=True)
+          f"setup={r.timings['amgSetup']:.3f} krylov={r.timings['krylov']:.3f} coarse_rows={r.coarseRows}", file=sys.stderr, flush=True)
