@@ -52,3 +52,21 @@ def test_blocked_dense_scrambled64(oracle):
         assert z.tobytes() == zo.tobytes()
     finally:
         ctx.close()
+
+
+def test_sweep_variants_bit_exact(oracle):
+    """Natural 64^3 (fine level ~1.4 K rows per dependency level: the medium
+    sweep variant) and scrambled 48^3 (shallow fine level, thousands of rows per
+    level: the wide cp.async variant), V-cycle applications bit for bit."""
+    ctx = bcs.Context(0)
+    try:
+        for s in (gen.hex_euler(64), gen.hex_euler(48, scramble_seed=11)):
+            cfg = make_cfg(precond=3, max_levels=30, min_coarse=8)
+            r = np.random.default_rng(8).uniform(-1, 1, s.A.n_cells * s.A.n)
+            z = _apply(ctx, s, cfg, r)
+            width = s.A.n_cells / max(1, ctx.schedule_depth(0))
+            assert width > 1184, f"{s.name}: fine-level width {width:.0f} too narrow for the variants under test"
+            zo = oracle.precond_apply(s.A, cfg, r)
+            assert z.tobytes() == zo.tobytes(), s.name
+    finally:
+        ctx.close()
