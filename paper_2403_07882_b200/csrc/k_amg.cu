@@ -274,6 +274,7 @@ __global__ void k_agg_fill(int rows, int* choice) {
 // Resumable per-row state of the lazy greedy decision: every attempt
 // continues from the first input that was still undecided, so a row issues
 // one dependent load chain over its whole lifetime instead of one per attempt.
+template <int AL>
 __global__ void __launch_bounds__(256) k_agg_syncfree(int rows, const int* __restrict__ ro, const int* __restrict__ ci,
                                                       const int* __restrict__ dg, const int* __restrict__ tpos,
                                                       const double* __restrict__ str, int* choice, int* err) {
@@ -291,9 +292,115 @@ __global__ void __launch_bounds__(256) k_agg_syncfree(int rows, const int* __res
         // phase B: current candidate (preference order: strength desc, slot asc)
         double lastS = 0.0;
         int lastK = -1, j = -1, kk = 0, tp = 0;
+        // fast path: the row's lower columns and its two preferred candidates
+        // (with their lower-than-r columns) are static, so every input of a
+        // decision is loaded in one round of independent loads
+        constexpr int AJ = AL;  // AL: static lower / candidate columns kept per row
+        int lc[AL], jc0[AJ], jc1[AJ];
+        int c0 = -1, c1 = -1, j0 = -1, j1 = -1, n0 = 0, n1 = 0;
+        double s0 = 0.0, s1 = 0.0;
+        bool fast = false;
+        if (!done) {
+            const int nl = d - k;
+            double bs0 = 0.0, bs1 = 0.0;
+            for (int q = d + 1; q < e; ++q) {
+                const double sv = __ldg(&str[q]);
+                if (!(sv > -1.0)) continue;
+                if (c0 < 0 || sv > bs0) {
+                    bs1 = bs0;
+                    c1 = c0;
+                    bs0 = sv;
+                    c0 = q;
+                } else if (c1 < 0 || sv > bs1) {
+                    bs1 = sv;
+                    c1 = q;
+                }
+            }
+            s0 = bs0;
+            s1 = bs1;
+            int t0 = 0, t1 = 0;
+            if (c0 >= 0) {
+                j0 = __ldg(&ci[c0]);
+                t0 = __ldg(&tpos[c0]);
+                n0 = t0 - __ldg(&ro[j0]);
+            }
+            if (c1 >= 0) {
+                j1 = __ldg(&ci[c1]);
+                t1 = __ldg(&tpos[c1]);
+                n1 = t1 - __ldg(&ro[j1]);
+            }
+            fast = nl <= AL && n0 <= AJ && n1 <= AJ;
+            if (fast) {
+#pragma unroll
+                for (int q = 0; q < AL; ++q) lc[q] = q < nl ? __ldg(&ci[k + q]) : -1;
+#pragma unroll
+                for (int q = 0; q < AJ; ++q) {
+                    jc0[q] = q < n0 ? __ldg(&ci[t0 - n0 + q]) : -1;
+                    jc1[q] = q < n1 ? __ldg(&ci[t1 - n1 + q]) : -1;
+                }
+            }
+        }
         unsigned spins = 0;
         while (!__all_sync(0xffffffffu, done)) {
-            if (!done) {
+            if (!done && fast) {
+                int a[AL], b0[AJ], b1[AJ];
+#pragma unroll
+                for (int q = 0; q < AL; ++q) a[q] = lc[q] >= 0 ? ld_choice(&choice[lc[q]]) : kSingle;
+#pragma unroll
+                for (int q = 0; q < AJ; ++q) {
+                    b0[q] = jc0[q] >= 0 ? ld_choice(&choice[jc0[q]]) : kSingle;
+                    b1[q] = jc1[q] >= 0 ? ld_choice(&choice[jc1[q]]) : kSingle;
+                }
+                bool tk = false, un = false;
+#pragma unroll
+                for (int q = 0; q < AL; ++q) {
+                    tk |= a[q] == r;
+                    un |= a[q] == kUndecided;
+                }
+                int dec = kUndecided;
+                if (tk) {
+                    dec = kTaken;
+                } else if (!un) {
+                    if (c0 < 0) {
+                        dec = kSingle;
+                    } else {
+                        bool t0k = false, u0 = false;
+#pragma unroll
+                        for (int q = 0; q < AJ; ++q) {
+                            t0k |= b0[q] == j0;
+                            u0 |= b0[q] == kUndecided;
+                        }
+                        if (!t0k) {
+                            if (!u0) dec = j0;
+                        } else if (c1 < 0) {
+                            dec = kSingle;
+                        } else {
+                            bool t1k = false, u1 = false;
+#pragma unroll
+                            for (int q = 0; q < AJ; ++q) {
+                                t1k |= b1[q] == j1;
+                                u1 |= b1[q] == kUndecided;
+                            }
+                            if (!t1k) {
+                                if (!u1) dec = j1;
+                            } else {
+                                // both preferred candidates taken: continue in the
+                                // general walk after the second one
+                                fast = false;
+                                phaseB = true;
+                                k = d;
+                                lastS = s1;
+                                lastK = c1;
+                                j = -1;
+                            }
+                        }
+                    }
+                }
+                if (dec != kUndecided) {
+                    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(&choice[r]), "r"(dec) : "memory");
+                    done = true;
+                }
+            } else if (!done) {
                 int dec = kUndecided;
                 if (!phaseB) {
                     for (; k < d; ++k) {
@@ -366,17 +473,24 @@ void aggregate_syncfree(int rows, const int* ro, const int* ci, const int* dg, c
                         int* choice, int* err, cudaStream_t s) {
     if (rows <= 0) return;
     k_agg_fill<<<(rows + 255) / 256, 256, 0, s>>>(rows, choice);
-    static int cap = 0;
-    if (!cap) {
+    // big fine levels (low degree): the lean variant, more threads in flight;
+    // coarse levels (higher degree): more columns kept per row
+    const bool lean = rows >= (1 << 20);
+    static int cap[2] = {0, 0};
+    if (!cap[0]) {
         int bps = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_agg_syncfree, 256, 0);
-        cap = num_sms() * (bps < 1 ? 1 : bps);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_agg_syncfree<6>, 256, 0);
+        cap[0] = num_sms() * (bps < 1 ? 1 : bps);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_agg_syncfree<10>, 256, 0);
+        cap[1] = num_sms() * (bps < 1 ? 1 : bps);
     }
     int g = (rows + 255) / 256;
-    if (g > cap) g = cap;
+    const int c = cap[lean ? 0 : 1];
+    if (g > c) g = c;
     void* args[] = {(void*)&rows, (void*)&ro, (void*)&ci, (void*)&dg, (void*)&tpos, (void*)&str, (void*)&choice,
                     (void*)&err};
-    const cudaError_t e = cudaLaunchCooperativeKernel((void*)k_agg_syncfree, dim3(g), dim3(256), args, 0, s);
+    const cudaError_t e = cudaLaunchCooperativeKernel(lean ? (void*)k_agg_syncfree<6> : (void*)k_agg_syncfree<10>,
+                                                      dim3(g), dim3(256), args, 0, s);
     if (e != cudaSuccess) throw std::runtime_error(std::string("aggregation launch failed: ") + cudaGetErrorString(e));
     count_launch(2);
 }
