@@ -149,6 +149,31 @@ bcs_status bcs_partition_get(const bcs_partition* p, int part, int32_t* row_offs
                              int32_t* halo_row, int32_t* halo_col, int32_t* halo_peer, int32_t* halo_src,
                              int32_t* send_peer, int32_t* send_row);
 
+/* Exchange plan of engine `part` for one process per engine (host only):
+ * n_send rows it packs (send_row, local rows; send_count[peer], peers
+ * ascending), n_recv rows it receives (recv_global_row, renumbered global
+ * rows; recv_count[peer]) and, per halo entry, the position of its column
+ * in the receive buffer.  Counts arrays have count() entries. */
+bcs_status bcs_partition_exchange_sizes(const bcs_partition* p, int part, int* n_send, int* n_recv);
+bcs_status bcs_partition_exchange_get(const bcs_partition* p, int part, int32_t* send_row, int32_t* send_count,
+                                      int32_t* recv_global_row, int32_t* recv_count, int32_t* halo_recv_idx);
+
+/* ---- Mode R with one process per GPU (NCCL) -------------------------------
+ * bcs_comm_unique_id fills 128 bytes on one rank; every rank passes them to
+ * bcs_comm_init (collective).  bcs_dist_solve_mp is then called collectively
+ * with the whole system on every rank (LinearDispatch's inputs): rank r owns
+ * engine r (n_engines = number of processes), builds its local matrix,
+ * halo plan and preconditioner, and the global Krylov exchanges halos with
+ * NCCL send/recv and folds per-engine dot partials (NCCL all-gather) in the
+ * reference's engine tree — the same arithmetic as bcs_dist_solve with the
+ * engines on one device.  x (original cell order) is complete on every rank. */
+bcs_status bcs_comm_unique_id(unsigned char id[128]);
+bcs_status bcs_comm_init(bcs_ctx* ctx, int rank, int n_ranks_total, const unsigned char id[128]);
+bcs_status bcs_dist_solve_mp(bcs_ctx* ctx, int n_cells, int n_faces, int block_size, const int32_t* owner,
+                             const int32_t* neighbour, const double* centroids, const double* diag,
+                             const double* upper, const double* lower, const double* b, const double* x0, double* x,
+                             int n_ranks, const bcs_solver_config* cfg, bcs_report* report);
+
 /* ---- staged interface (device-resident workflows) ------------------------ */
 /* Builds the LDU->BSR plan (block_csr.cpp:56-80) on the device. */
 bcs_status bcs_set_topology(bcs_ctx* ctx, int n_cells, int n_faces, int block_size, const int32_t* owner,

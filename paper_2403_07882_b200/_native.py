@@ -113,6 +113,11 @@ SIGNATURES = {
     "bcs_partition_decomposition": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "bcs_partition_sizes": (c_int, [c_void_p, c_int, P(c_int), P(c_int), P(c_int), P(c_int), P(c_int)]),
     "bcs_partition_get": (c_int, [c_void_p, c_int] + [c_void_p] * 9),
+    "bcs_partition_exchange_sizes": (c_int, [c_void_p, c_int, P(c_int), P(c_int)]),
+    "bcs_partition_exchange_get": (c_int, [c_void_p, c_int] + [c_void_p] * 5),
+    "bcs_comm_unique_id": (c_int, [c_void_p]),
+    "bcs_comm_init": (c_int, [c_void_p, c_int, c_int, c_void_p]),
+    "bcs_dist_solve_mp": (c_int, [c_void_p, c_int, c_int, c_int] + [c_void_p] * 9 + [c_int, P(SolverConfigC), P(ReportC)]),
     "bcs_selftest": (c_int, [c_int, ctypes.c_ulonglong, ctypes.c_ulonglong, P(ctypes.c_ulonglong)]),
 }
 

@@ -295,6 +295,27 @@ class Context:
         r.timings = {"convert": rep.t_convert, "setup": rep.t_setup, "solve": rep.t_solve, "retrieve": rep.t_retrieve}
         return x, r
 
+    def comm_init(self, rank: int, size: int, uid: bytes):
+        """Collective: this context joins an NCCL communicator of `size` processes (one per GPU)."""
+        buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
+        self._ck(self._lib.bcs_comm_init(self.h, int(rank), int(size), buf))
+
+    def dist_solve_mp(self, A: BlockLduMatrix, b: BlockVector, x0: BlockVector, centroids: np.ndarray, n_ranks: int,
+                      cfg: SolverConfig) -> Tuple[BlockVector, SolveReport]:
+        """Collective Mode R over processes: this process solves engine `rank` (comm_init), exchanging halos and
+        dot partials with NCCL; returns the whole solution (original cell order) on every rank."""
+        x = BlockVector(A.n_cells, A.n)
+        cen = np.ascontiguousarray(centroids, dtype=np.float64).reshape(-1)
+        rep = N.ReportC()
+        c = cfg.to_c()
+        self._ck(self._lib.bcs_dist_solve_mp(self.h, A.n_cells, A.nFaces(), A.n, N.ptr(A.owner), N.ptr(A.neighbour),
+                                             N.ptr(cen), N.ptr(A.diag), N.ptr(A.upper), N.ptr(A.lower),
+                                             N.ptr(b.values), N.ptr(x0.values), N.ptr(x.values), int(n_ranks),
+                                             ctypes.byref(c), ctypes.byref(rep)))
+        r = SolveReport.from_c(rep)
+        r.timings = {"convert": rep.t_convert, "setup": rep.t_setup, "solve": rep.t_solve, "retrieve": rep.t_retrieve}
+        return x, r
+
 
 class Partition:
     """Host partition layer (decompose + buildPartitioned [+ consolidate]); no device needed."""
@@ -344,6 +365,32 @@ class Partition:
                                                                         "halo_peer", "halo_src", "send_peer",
                                                                         "send_row")))
         return d
+
+    def exchange(self, i: int) -> dict:
+        """Per-process halo exchange plan of engine i (see bcs_partition_exchange_get)."""
+        ns, nr = ctypes.c_int(), ctypes.c_int()
+        st = self._lib.bcs_partition_exchange_sizes(self.h, i, ctypes.byref(ns), ctypes.byref(nr))
+        if st != N.BCS_OK:
+            _raise(st, self._lib.bcs_last_error(None).decode())
+        G = self.count()
+        nh = self.part(i)["halo_col"].size
+        d = {"send_row": np.zeros(ns.value, np.int32), "send_count": np.zeros(G, np.int32),
+             "recv_global_row": np.zeros(nr.value, np.int32), "recv_count": np.zeros(G, np.int32),
+             "halo_recv_idx": np.zeros(nh, np.int32)}
+        st = self._lib.bcs_partition_exchange_get(self.h, i, *(N.ptr(d[k]) for k in (
+            "send_row", "send_count", "recv_global_row", "recv_count", "halo_recv_idx")))
+        if st != N.BCS_OK:
+            _raise(st, self._lib.bcs_last_error(None).decode())
+        return d
+
+
+def comm_unique_id() -> bytes:
+    """128-byte NCCL unique id for bcs_comm_init (create on one rank, broadcast)."""
+    buf = (ctypes.c_ubyte * 128)()
+    st = N.lib().bcs_comm_unique_id(buf)
+    if st != N.BCS_OK:
+        _raise(st, N.lib().bcs_last_error(None).decode())
+    return bytes(buf)
 
 
 def c_ptr(p) -> ctypes.c_void_p:

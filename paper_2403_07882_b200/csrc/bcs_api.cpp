@@ -199,6 +199,45 @@ bcs_status bcs_partition_get(const bcs_partition* p, int part, int32_t* ro, int3
     });
 }
 
+bcs_status bcs_partition_exchange_sizes(const bcs_partition* p, int part, int* n_send, int* n_recv) {
+    return guarded(nullptr, [&] {
+        if (!p || part < 0 || part >= static_cast<int>(p->parts.size())) throw std::invalid_argument("bad partition index");
+        const bcs::ExchangePlan x = bcs::makeExchangePlan(p->parts, part);
+        if (n_send) *n_send = static_cast<int>(x.sendRows.size());
+        if (n_recv) *n_recv = static_cast<int>(x.recvGlobalRow.size());
+    });
+}
+bcs_status bcs_partition_exchange_get(const bcs_partition* p, int part, int32_t* send_row, int32_t* send_count,
+                                      int32_t* recv_global_row, int32_t* recv_count, int32_t* halo_recv_idx) {
+    return guarded(nullptr, [&] {
+        if (!p || part < 0 || part >= static_cast<int>(p->parts.size())) throw std::invalid_argument("bad partition index");
+        const bcs::ExchangePlan x = bcs::makeExchangePlan(p->parts, part);
+        if (send_row) std::copy(x.sendRows.begin(), x.sendRows.end(), send_row);
+        if (send_count) std::copy(x.sendCount.begin(), x.sendCount.end(), send_count);
+        if (recv_global_row) std::copy(x.recvGlobalRow.begin(), x.recvGlobalRow.end(), recv_global_row);
+        if (recv_count) std::copy(x.recvCount.begin(), x.recvCount.end(), recv_count);
+        if (halo_recv_idx) std::copy(x.haloRecvIdx.begin(), x.haloRecvIdx.end(), halo_recv_idx);
+    });
+}
+
+bcs_status bcs_comm_unique_id(unsigned char id[128]) {
+    return guarded(nullptr, [&] { bcs::Engine::commUniqueId(id); });
+}
+bcs_status bcs_comm_init(bcs_ctx* ctx, int rank, int n_ranks_total, const unsigned char id[128]) {
+    return guarded(ctx, [&] { eng(ctx).commInit(rank, n_ranks_total, id); });
+}
+bcs_status bcs_dist_solve_mp(bcs_ctx* ctx, int n_cells, int n_faces, int block_size, const int32_t* owner,
+                             const int32_t* neighbour, const double* centroids, const double* diag,
+                             const double* upper, const double* lower, const double* b, const double* x0, double* x,
+                             int n_ranks, const bcs_solver_config* cfg, bcs_report* report) {
+    return guarded(ctx, [&] {
+        bcs_report rep{};
+        eng(ctx).distSolveMP(n_cells, n_faces, block_size, owner, neighbour, centroids, diag, upper, lower, b, x0, x,
+                             n_ranks, cfgOf(cfg), rep);
+        if (report) *report = rep;
+    });
+}
+
 bcs_status bcs_set_topology(bcs_ctx* ctx, int n_cells, int n_faces, int block_size, const int32_t* owner,
                             const int32_t* neighbour) {
     return guarded(ctx, [&] { eng(ctx).setTopology(n_cells, n_faces, block_size, owner, neighbour); });

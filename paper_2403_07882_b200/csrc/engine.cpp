@@ -8,6 +8,9 @@
 // reference's control flow branches on.
 #include "engine.hpp"
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -17,6 +20,57 @@
 #include <map>
 
 namespace bcs {
+
+// ------------------------------------------------------------------ NCCL
+// Loaded at run time (dlopen) so libbcs.so has no link-time dependency on
+// it: only the multi-process Mode R entry points need it, and they fail with
+// a clear error when it is missing.  Search: $BCS_NCCL_LIB, the soname (the
+// copy torch already loaded), the venv's nvidia-nccl wheel.
+namespace nccl {
+struct Api {
+    decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+    decltype(&ncclCommInitRank) commInitRank = nullptr;
+    decltype(&ncclCommDestroy) commDestroy = nullptr;
+    decltype(&ncclAllGather) allGather = nullptr;
+    decltype(&ncclSend) send = nullptr;
+    decltype(&ncclRecv) recv = nullptr;
+    decltype(&ncclGroupStart) groupStart = nullptr;
+    decltype(&ncclGroupEnd) groupEnd = nullptr;
+    decltype(&ncclGetErrorString) errorString = nullptr;
+};
+const Api& api() {
+    static Api a;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        std::vector<std::string> names;
+        if (const char* e = std::getenv("BCS_NCCL_LIB")) names.emplace_back(e);
+        names.emplace_back("libnccl.so.2");
+        names.emplace_back("/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2");
+        void* h = nullptr;
+        for (const auto& n : names)
+            if ((h = dlopen(n.c_str(), RTLD_NOW | RTLD_GLOBAL))) break;
+        if (h) {
+            a.getUniqueId = reinterpret_cast<decltype(a.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+            a.commInitRank = reinterpret_cast<decltype(a.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+            a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+            a.allGather = reinterpret_cast<decltype(a.allGather)>(dlsym(h, "ncclAllGather"));
+            a.send = reinterpret_cast<decltype(a.send)>(dlsym(h, "ncclSend"));
+            a.recv = reinterpret_cast<decltype(a.recv)>(dlsym(h, "ncclRecv"));
+            a.groupStart = reinterpret_cast<decltype(a.groupStart)>(dlsym(h, "ncclGroupStart"));
+            a.groupEnd = reinterpret_cast<decltype(a.groupEnd)>(dlsym(h, "ncclGroupEnd"));
+            a.errorString = reinterpret_cast<decltype(a.errorString)>(dlsym(h, "ncclGetErrorString"));
+        }
+    }
+    if (!a.getUniqueId || !a.commInitRank || !a.allGather || !a.send || !a.recv || !a.groupStart || !a.groupEnd)
+        throw std::runtime_error("bcs: NCCL (libnccl.so.2) not found; set BCS_NCCL_LIB");
+    return a;
+}
+void ck(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        throw std::runtime_error(std::string("bcs: NCCL ") + what + ": " + (api().errorString ? api().errorString(r) : "error"));
+}
+}  // namespace nccl
 
 void check(cudaError_t e, const char* what) {
     if (e == cudaSuccess) return;
@@ -892,7 +946,27 @@ void Engine::opResidual(const double* x, const double* b, double* r) {
         return;
     }
     opSpmv(x, distTmp_.p);
-    sub_vec(b, distTmp_, r, static_cast<size_t>(distNc_) * n_, stream_);
+    sub_vec(b, distTmp_, r, static_cast<size_t>(mpActive_ ? mpRows_ : distNc_) * n_, stream_);
+}
+
+// halo exchange of the multi-process Mode R: pack the rows peers need, one
+// grouped NCCL send/recv per peer (peers ascending), values land in mpRecv_
+void Engine::mpExchange(const double* x) {
+    const auto& A = nccl::api();
+    pack_rows(n_, mpSendRows_, mpSendIdx_, x, mpSend_.p, stream_);
+    nccl::ck(A.groupStart(), "group start");
+    size_t so = 0, ro = 0;
+    for (int q = 0; q < mpSize_; ++q) {
+        if (mpSendCnt_[q])
+            nccl::ck(A.send(mpSend_.p + so * n_, static_cast<size_t>(mpSendCnt_[q]) * n_, ncclDouble, q,
+                            static_cast<ncclComm_t>(comm_), stream_), "send");
+        if (mpRecvCnt_[q])
+            nccl::ck(A.recv(mpRecv_.p + ro * n_, static_cast<size_t>(mpRecvCnt_[q]) * n_, ncclDouble, q,
+                            static_cast<ncclComm_t>(comm_), stream_), "recv");
+        so += mpSendCnt_[q];
+        ro += mpRecvCnt_[q];
+    }
+    nccl::ck(A.groupEnd(), "group end");
 }
 
 // partitionedMatvec (partition.cpp:298-352): every engine's local product on
@@ -901,6 +975,13 @@ void Engine::opResidual(const double* x, const double* b, double* r) {
 void Engine::opSpmv(const double* x, double* y) {
     if (!distActive_) {
         spmvLevel(H_->levels[0], x, nullptr, y);
+        return;
+    }
+    if (mpActive_) {  // this process's engine; halo columns index the receive buffer
+        DistPart& P = dist_[0];
+        mpExchange(x);
+        spmv(n_, P.rows, P.ro, P.ci, P.vals, x, nullptr, y, stream_);
+        halo_spmv(n_, P.nhr, P.hrow, P.hoff, P.hcol, P.hvals, mpRecv_, y, 0, stream_);
         return;
     }
     for (auto& P : dist_) {
@@ -924,15 +1005,75 @@ void Engine::opPrecond(const double* r, double* z) {
     H_ = &main_;
 }
 
+// multi-process: this engine's partial with the block layout the one-device
+// Mode R uses for an engine segment, all-gathered, folded in engine order
 void Engine::opDot(const double* a, const double* b, double* out, bool sqrt_out) {
+    if (mpActive_) {
+        dot(a, b, seg_, 1, mpPart_.p, false, partials_.p, ticket_.p, stream_, mpBps_);
+        nccl::ck(nccl::api().allGather(mpPart_.p, mpGath_.p, 1, ncclDouble, static_cast<ncclComm_t>(comm_), stream_),
+                 "allgather");
+        fold_engines(mpGath_, mpSize_, out, sqrt_out, stream_);
+        return;
+    }
     dot(a, b, seg_, nseg_, out, sqrt_out, partials_.p, ticket_.p, stream_);
 }
 
 void Engine::opAxpyDot(double* w, const double* h, const double* v, const double* nextv, double* out) {
+    if (mpActive_) {
+        axpy_dot(w, h, v, nextv, seg_, 1, mpPart_.p, partials_.p, ticket_.p, stream_, mpBps_, 0);
+        nccl::ck(nccl::api().allGather(mpPart_.p, mpGath_.p, 1, ncclDouble, static_cast<ncclComm_t>(comm_), stream_),
+                 "allgather");
+        fold_engines(mpGath_, mpSize_, out, nextv == nullptr, stream_);
+        return;
+    }
     axpy_dot(w, h, v, nextv, seg_, nseg_, out, partials_.p, ticket_.p, stream_);
 }
 
 // ------------------------------------------------------------------ Mode R
+// one engine's local BSR, LDU source ids, diagonal/transpose positions and
+// halo CSR (halo columns: global rows, or hcolOverride = receive-buffer rows)
+void Engine::uploadEnginePart(DistPart& P, const Partition& p, int n, const std::vector<int>* hcolOverride) {
+    P.rowStart = 0;
+    P.rows = p.nLocalRows();
+    P.nnz = static_cast<int>(p.ci.size());
+    P.nh = static_cast<int>(p.haloRow.size());
+    P.ro.ensure(p.ro.size(), stream_);
+    P.ci.ensure(p.ci.size(), stream_);
+    P.src.ensure(p.src.size(), stream_);
+    P.dg.ensure(P.rows, stream_);
+    P.tpos.ensure(p.ci.size(), stream_);
+    P.vals.ensure(static_cast<size_t>(P.nnz) * n * n, stream_);
+    check(cudaMemcpyAsync(P.ro.p, p.ro.data(), sizeof(int) * p.ro.size(), cudaMemcpyHostToDevice, stream_), "H2D");
+    check(cudaMemcpyAsync(P.ci.p, p.ci.data(), sizeof(int) * p.ci.size(), cudaMemcpyHostToDevice, stream_), "H2D");
+    check(cudaMemcpyAsync(P.src.p, p.src.data(), sizeof(int) * p.src.size(), cudaMemcpyHostToDevice, stream_), "H2D");
+    find_diag(P.rows, P.ro, P.ci, P.dg.p, stream_);
+    cudaMemsetAsync(err_.p, 0, sizeof(int), stream_);
+    transpose_pos(P.rows, P.ro, P.ci, P.tpos.p, err_.p, stream_);
+    if (readErrCell()) throw std::runtime_error("bcs: structurally asymmetric engine pattern");
+    // halo rows: distinct local rows of the (row, col)-sorted entries
+    std::vector<int> hrow, hoff;
+    for (int h = 0; h < P.nh; ++h)
+        if (h == 0 || p.haloRow[h] != p.haloRow[h - 1]) {
+            hrow.push_back(p.haloRow[h]);
+            hoff.push_back(h);
+        }
+    hoff.push_back(P.nh);
+    P.nhr = static_cast<int>(hrow.size());
+    P.hrow.ensure(hrow.size(), stream_);
+    P.hoff.ensure(hoff.size(), stream_);
+    P.hcol.ensure(P.nh, stream_);
+    P.hsrc.ensure(P.nh, stream_);
+    P.hvals.ensure(static_cast<size_t>(P.nh) * n * n, stream_);
+    const std::vector<int>& hc = hcolOverride ? *hcolOverride : p.haloCol;
+    if (P.nh) {
+        check(cudaMemcpyAsync(P.hrow.p, hrow.data(), sizeof(int) * hrow.size(), cudaMemcpyHostToDevice, stream_), "H2D");
+        check(cudaMemcpyAsync(P.hoff.p, hoff.data(), sizeof(int) * hoff.size(), cudaMemcpyHostToDevice, stream_), "H2D");
+        check(cudaMemcpyAsync(P.hcol.p, hc.data(), sizeof(int) * P.nh, cudaMemcpyHostToDevice, stream_), "H2D");
+        check(cudaMemcpyAsync(P.hsrc.p, p.haloSrc.data(), sizeof(int) * P.nh, cudaMemcpyHostToDevice, stream_), "H2D");
+    }
+    sync();  // host vectors die with the caller's iteration
+}
+
 void Engine::distSetupTopology(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh,
                                const double* centroids, int nRanks, int nEngines) {
     if (nEngines > 64) throw std::invalid_argument("bcs: at most 64 engines per device");
@@ -944,47 +1085,10 @@ void Engine::distSetupTopology(int nc, int nf, int n, const int32_t* owner, cons
     std::vector<long long> segh(eng.size() + 1, 0);
     for (size_t e = 0; e < eng.size(); ++e) {
         const Partition& p = eng[e];
-        DistPart& P = dist_[e];
-        P.rowStart = p.rowStart;
-        P.rows = p.nLocalRows();
-        P.nnz = static_cast<int>(p.ci.size());
-        P.nh = static_cast<int>(p.haloRow.size());
-        P.ro.ensure(p.ro.size(), stream_);
-        P.ci.ensure(p.ci.size(), stream_);
-        P.src.ensure(p.src.size(), stream_);
-        P.dg.ensure(P.rows, stream_);
-        P.tpos.ensure(p.ci.size(), stream_);
-        P.vals.ensure(static_cast<size_t>(P.nnz) * n * n, stream_);
-        check(cudaMemcpyAsync(P.ro.p, p.ro.data(), sizeof(int) * p.ro.size(), cudaMemcpyHostToDevice, stream_), "H2D");
-        check(cudaMemcpyAsync(P.ci.p, p.ci.data(), sizeof(int) * p.ci.size(), cudaMemcpyHostToDevice, stream_), "H2D");
-        check(cudaMemcpyAsync(P.src.p, p.src.data(), sizeof(int) * p.src.size(), cudaMemcpyHostToDevice, stream_), "H2D");
-        find_diag(P.rows, P.ro, P.ci, P.dg.p, stream_);
-        cudaMemsetAsync(err_.p, 0, sizeof(int), stream_);
-        transpose_pos(P.rows, P.ro, P.ci, P.tpos.p, err_.p, stream_);
-        if (readErrCell()) throw std::runtime_error("bcs: structurally asymmetric engine pattern");
-        // halo rows: distinct local rows of the (row, col)-sorted entries
-        std::vector<int> hrow, hoff;
-        for (int h = 0; h < P.nh; ++h)
-            if (h == 0 || p.haloRow[h] != p.haloRow[h - 1]) {
-                hrow.push_back(p.haloRow[h]);
-                hoff.push_back(h);
-            }
-        hoff.push_back(P.nh);
-        P.nhr = static_cast<int>(hrow.size());
-        P.hrow.ensure(hrow.size(), stream_);
-        P.hoff.ensure(hoff.size(), stream_);
-        P.hcol.ensure(P.nh, stream_);
-        P.hsrc.ensure(P.nh, stream_);
-        P.hvals.ensure(static_cast<size_t>(P.nh) * n * n, stream_);
-        if (P.nh) {
-            check(cudaMemcpyAsync(P.hrow.p, hrow.data(), sizeof(int) * hrow.size(), cudaMemcpyHostToDevice, stream_), "H2D");
-            check(cudaMemcpyAsync(P.hoff.p, hoff.data(), sizeof(int) * hoff.size(), cudaMemcpyHostToDevice, stream_), "H2D");
-            check(cudaMemcpyAsync(P.hcol.p, p.haloCol.data(), sizeof(int) * P.nh, cudaMemcpyHostToDevice, stream_), "H2D");
-            check(cudaMemcpyAsync(P.hsrc.p, p.haloSrc.data(), sizeof(int) * P.nh, cudaMemcpyHostToDevice, stream_), "H2D");
-        }
+        uploadEnginePart(dist_[e], p, n, nullptr);
+        dist_[e].rowStart = p.rowStart;
         segh[e + 1] = static_cast<long long>(p.rowEnd) * n;
         segh[e] = static_cast<long long>(p.rowStart) * n;
-        sync();  // host vectors die at the end of this iteration
     }
     nseg_ = static_cast<int>(eng.size());
     seg_.ensure(eng.size() + 1, stream_);
@@ -1094,6 +1198,190 @@ void Engine::distSolve(int nc, int nf, int n, const int32_t* owner, const int32_
     rep.t_amg_setup = rep.t_setup;
     rep.t_krylov = rep.t_solve;
     rep.amg_levels = static_cast<int>(dist_.size());
+}
+
+// ------------------------------------------------- Mode R, one process per GPU
+void Engine::commUniqueId(unsigned char id[128]) {
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+    ncclUniqueId u;
+    nccl::ck(nccl::api().getUniqueId(&u), "unique id");
+    std::memcpy(id, &u, sizeof u);
+}
+
+void Engine::commInit(int rank, int size, const unsigned char id[128]) {
+    if (size < 1 || rank < 0 || rank >= size) throw std::invalid_argument("bcs_comm_init: bad rank / size");
+    if (size > 64) throw std::invalid_argument("bcs_comm_init: at most 64 processes");
+    const auto& A = nccl::api();
+    cudaSetDevice(device_);
+    if (comm_ && A.commDestroy) A.commDestroy(static_cast<ncclComm_t>(comm_));
+    comm_ = nullptr;
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof u);
+    ncclComm_t c = nullptr;
+    nccl::ck(A.commInitRank(&c, size, u, rank), "comm init");
+    comm_ = c;
+    mpRank_ = rank;
+    mpSize_ = size;
+    mpNc_ = -1;  // topology cache belongs to the previous communicator
+}
+
+// this process's engine of the consolidated decomposition (engines = processes)
+void Engine::mpSetupTopology(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh,
+                             const double* centroids, int nRanks) {
+    const Decomposition dec = decompose(nc, centroids, nRanks);
+    const std::vector<Partition> parts = buildPartitioned(nc, nf, owner, neigh, dec);
+    const ConsolidationPlan plan = makeConsolidationPlan(dec, mpSize_);
+    const std::vector<Partition> eng = consolidate(parts, plan, dec);
+    const ExchangePlan xp = makeExchangePlan(eng, mpRank_);
+    dist_.resize(1);
+    uploadEnginePart(dist_[0], eng[mpRank_], n, &xp.haloRecvIdx);
+    mpRows_ = dist_[0].rows;
+    mpSendCnt_ = xp.sendCount;
+    mpRecvCnt_ = xp.recvCount;
+    mpSendRows_ = static_cast<int>(xp.sendRows.size());
+    mpRecvRows_ = static_cast<int>(xp.recvGlobalRow.size());
+    mpSendIdx_.ensure(std::max(1, mpSendRows_), stream_);
+    if (mpSendRows_)
+        check(cudaMemcpyAsync(mpSendIdx_.p, xp.sendRows.data(), sizeof(int) * mpSendRows_, cudaMemcpyHostToDevice,
+                              stream_), "H2D");
+    mpSend_.ensure(static_cast<size_t>(std::max(1, mpSendRows_)) * n, stream_);
+    mpRecv_.ensure(static_cast<size_t>(std::max(1, mpRecvRows_)) * n, stream_);
+    mpPart_.ensure(1, stream_);
+    mpGath_.ensure(mpSize_, stream_);
+    mpEngStart_.assign(mpSize_, 0);
+    mpEngRows_.assign(mpSize_, 0);
+    mpMaxRows_ = 0;
+    for (int e = 0; e < mpSize_; ++e) {
+        mpEngStart_[e] = eng[e].rowStart;
+        mpEngRows_[e] = eng[e].nLocalRows();
+        mpMaxRows_ = std::max(mpMaxRows_, mpEngRows_[e]);
+    }
+    mpXall_.ensure(static_cast<size_t>(mpMaxRows_) * n * (mpSize_ + 1), stream_);
+    // reductions: the block layout of an engine segment in the one-device Mode R
+    mpBps_ = seg_blocks(mpSize_);
+    const long long segh[2] = {0, static_cast<long long>(mpRows_) * n};
+    seg_.ensure(2, stream_);
+    check(cudaMemcpyAsync(seg_.p, segh, sizeof segh, cudaMemcpyHostToDevice, stream_), "H2D");
+    mpNewToOld_ = dec.newToOld;
+    mpOwner_.assign(owner, owner + nf);
+    mpNeigh_.assign(neigh, neigh + nf);
+    mpCen_.assign(centroids, centroids + 3 * static_cast<size_t>(nc));
+    mpRanks_ = nRanks;
+    mpNc_ = nc;
+    mpNf_ = nf;
+    mpN_ = n;
+    distNc_ = -1;  // the one-device Mode R cache no longer describes dist_
+    sync();
+}
+
+void Engine::distSolveMP(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh, const double* centroids,
+                         const double* diag, const double* upper, const double* lower, const double* b,
+                         const double* x0, double* x, int nRanks, const bcs_solver_config& cfg, bcs_report& rep) {
+    LaunchScope ls(&launches_);
+    if (!comm_) throw std::invalid_argument("bcs_dist_solve_mp: call bcs_comm_init first");
+    if (n < 1 || n > 5) throw std::invalid_argument("bcs: block size must be 1..5 on the device");
+    if (mpSize_ < 1 || mpSize_ > nRanks) throw std::invalid_argument("makeConsolidationPlan: need 1 <= nEngines <= nRanks");
+    validateConfig(cfg);
+    const auto t0 = clk::now();
+    const bool same = mpNc_ == nc && mpNf_ == nf && mpN_ == n && mpRanks_ == nRanks &&
+                      std::equal(owner, owner + nf, mpOwner_.begin()) && std::equal(neigh, neigh + nf, mpNeigh_.begin()) &&
+                      std::equal(centroids, centroids + 3 * static_cast<size_t>(nc), mpCen_.begin());
+    if (!same) mpSetupTopology(nc, nf, n, owner, neigh, centroids, nRanks);
+    n_ = n;
+    DistPart& P = dist_[0];
+    const size_t nn = static_cast<size_t>(n) * n;
+    ldu_diag_.ensure(nc * nn, stream_);
+    ldu_upper_.ensure(nf * nn, stream_);
+    ldu_lower_.ensure(nf * nn, stream_);
+    check(cudaMemcpyAsync(ldu_diag_.p, diag, sizeof(double) * nc * nn, cudaMemcpyHostToDevice, stream_), "H2D");
+    if (nf) {
+        check(cudaMemcpyAsync(ldu_upper_.p, upper, sizeof(double) * nf * nn, cudaMemcpyHostToDevice, stream_), "H2D");
+        check(cudaMemcpyAsync(ldu_lower_.p, lower, sizeof(double) * nf * nn, cudaMemcpyHostToDevice, stream_), "H2D");
+    }
+    gather_values(n, P.nnz, nc, nf, P.src, ldu_diag_, ldu_upper_, ldu_lower_, P.vals.p, stream_);
+    if (P.nh) gather_values(n, P.nh, nc, nf, P.hsrc, ldu_diag_, ldu_upper_, ldu_lower_, P.hvals.p, stream_);
+    // this engine's slice of scatterVector (partition.cpp:269-280)
+    const size_t Nl = static_cast<size_t>(mpRows_) * n;
+    std::vector<double> hb(Nl), hx(Nl);
+    const int g0 = mpEngStart_[mpRank_];
+    for (int r = 0; r < mpRows_; ++r) {
+        const int old = mpNewToOld_[g0 + r];
+        std::copy(b + static_cast<size_t>(old) * n, b + static_cast<size_t>(old + 1) * n, hb.begin() + static_cast<size_t>(r) * n);
+        std::copy(x0 + static_cast<size_t>(old) * n, x0 + static_cast<size_t>(old + 1) * n, hx.begin() + static_cast<size_t>(r) * n);
+    }
+    kb_.ensure(Nl, stream_);
+    kx_.ensure(Nl, stream_);
+    distTmp_.ensure(Nl, stream_);
+    check(cudaMemcpyAsync(kb_.p, hb.data(), Nl * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D b");
+    check(cudaMemcpyAsync(kx_.p, hx.data(), Nl * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D x0");
+    sync();
+    const auto t1 = clk::now();
+    hist_.clear();
+    spmvMs_ = 0.0;
+    spmvCount_ = 0;
+    sweepMs_ = 0.0;
+    sweepBytes_ = 0.0;
+    sweepCount_ = 0;
+    evUsed_ = 0;
+    cudaMemsetAsync(err_.p + 1, 0, sizeof(int), stream_);
+    const int ncSerial = nc_;
+    nc_ = mpRows_;
+    H_ = &P.H;
+    FineMatrix F;
+    F.rows = P.rows;
+    F.nnz = P.nnz;
+    F.ro = P.ro;
+    F.ci = P.ci;
+    F.dg = P.dg;
+    F.tpos = P.tpos;
+    F.v = P.vals;
+    try {
+        buildPrecondOn(F, cfg);
+    } catch (...) {
+        H_ = &main_;
+        nc_ = ncSerial;
+        throw;
+    }
+    H_ = &main_;
+    sync();
+    const auto t2 = clk::now();
+    distActive_ = true;
+    mpActive_ = true;
+    nseg_ = 1;
+    try {
+        solveKrylov(kb_, kx_.p, cfg, rep);
+    } catch (...) {
+        distActive_ = mpActive_ = false;
+        nc_ = ncSerial;
+        throw;
+    }
+    distActive_ = mpActive_ = false;
+    const auto t3 = clk::now();
+    // gatherVector (partition.cpp:282-296): padded all-gather of the slices
+    const size_t pad = static_cast<size_t>(mpMaxRows_) * n;
+    double* mine = mpXall_.p + pad * mpSize_;
+    check(cudaMemsetAsync(mine, 0, pad * sizeof(double), stream_), "memset");
+    check(cudaMemcpyAsync(mine, kx_.p, Nl * sizeof(double), cudaMemcpyDeviceToDevice, stream_), "D2D");
+    nccl::ck(nccl::api().allGather(mine, mpXall_.p, pad, ncclDouble, static_cast<ncclComm_t>(comm_), stream_),
+             "allgather x");
+    std::vector<double> all(pad * mpSize_);
+    check(cudaMemcpyAsync(all.data(), mpXall_.p, all.size() * sizeof(double), cudaMemcpyDeviceToHost, stream_), "D2H x");
+    sync();
+    for (int e = 0; e < mpSize_; ++e)
+        for (int r = 0; r < mpEngRows_[e]; ++r) {
+            const int old = mpNewToOld_[mpEngStart_[e] + r];
+            std::copy(all.begin() + pad * e + static_cast<size_t>(r) * n, all.begin() + pad * e + static_cast<size_t>(r + 1) * n,
+                      x + static_cast<size_t>(old) * n);
+        }
+    nc_ = ncSerial;
+    const auto t4 = clk::now();
+    rep.t_convert = secs(t0, t1);  // partition.cpp:474-477 keys
+    rep.t_setup = secs(t1, t2);
+    rep.t_solve = secs(t2, t3);
+    rep.t_retrieve = secs(t3, t4);
+    rep.t_amg_setup = rep.t_setup;
+    rep.t_krylov = rep.t_solve;
+    rep.amg_levels = 1;
 }
 
 void Engine::solveHost(const double* b, double* x, const bcs_solver_config& cfg, bcs_report& rep) {

@@ -120,6 +120,12 @@ public:
     // on this device — ranks decomposed by RCB, consolidated onto engines, one
     // local preconditioner per engine, global Krylov with halo couplings and
     // the fixed engine-order tree for dot products.
+    // Mode R with one process per GPU (NCCL, loaded at run time)
+    static void commUniqueId(unsigned char id[128]);
+    void commInit(int rank, int size, const unsigned char id[128]);
+    void distSolveMP(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh, const double* centroids,
+                     const double* diag, const double* upper, const double* lower, const double* b, const double* x0,
+                     double* x, int nRanks, const bcs_solver_config& cfg, bcs_report& rep);
     void distSolve(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh, const double* centroids,
                    const double* diag, const double* upper, const double* lower, const double* b, const double* x0,
                    double* x, int nRanks, int nEngines, const bcs_solver_config& cfg, bcs_report& rep);
@@ -172,6 +178,9 @@ private:
     void opAxpyDot(double* w, const double* h, const double* v, const double* nextv, double* out);
     void distSetupTopology(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh,
                            const double* centroids, int nRanks, int nEngines);
+    void mpSetupTopology(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh, const double* centroids,
+                         int nRanks);
+    void uploadEnginePart(DistPart& P, const Partition& p, int n, const std::vector<int>* hcolOverride);
     void solveKrylov(const double* d_b, double* d_x, const bcs_solver_config& cfg, bcs_report& rep);
     double dotHost(const double* a, const double* b, size_t N, bool sqrt_out);
     void sync();
@@ -218,6 +227,19 @@ private:
     void collectSpmvTimes();
     // Mode R state
     bool distActive_ = false;
+    // multi-process Mode R
+    void* comm_ = nullptr;  // ncclComm_t
+    int mpRank_ = 0, mpSize_ = 1;
+    bool mpActive_ = false;
+    int mpBps_ = 0, mpRows_ = 0, mpSendRows_ = 0, mpRecvRows_ = 0, mpMaxRows_ = 0;
+    std::vector<int> mpSendCnt_, mpRecvCnt_, mpEngStart_, mpEngRows_;
+    DArray<int> mpSendIdx_;
+    DArray<double> mpSend_, mpRecv_, mpPart_, mpGath_, mpXall_;
+    int mpRanks_ = 0, mpNc_ = 0, mpNf_ = 0, mpN_ = 0;
+    std::vector<int32_t> mpOwner_, mpNeigh_;
+    std::vector<double> mpCen_;
+    std::vector<int> mpNewToOld_;
+    void mpExchange(const double* x);
     std::vector<DistPart> dist_;
     std::vector<int32_t> distOwner_, distNeigh_;
     std::vector<double> distCen_;

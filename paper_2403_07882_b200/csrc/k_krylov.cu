@@ -86,9 +86,44 @@ static int seg_grid(int nseg) {
     return B * nseg;
 }
 
+int seg_blocks(int nseg) { return seg_grid(nseg) / nseg; }
+
 void dot(const double* a, const double* b, const long long* seg, int nseg, double* out, bool sqrt_out,
-         double* partials, int* ticket, cudaStream_t s) {
-    k_dot<<<seg_grid(nseg), kRedThreads, 0, s>>>(a, b, seg, nseg, out, sqrt_out ? 1 : 0, partials, ticket);
+         double* partials, int* ticket, cudaStream_t s, int bps) {
+    const int g = bps > 0 ? bps * nseg : seg_grid(nseg);
+    k_dot<<<g, kRedThreads, 0, s>>>(a, b, seg, nseg, out, sqrt_out ? 1 : 0, partials, ticket);
+    count_launch();
+}
+
+// per-engine partials (one per process, all-gathered) folded with the
+// reference's pairwise tree in engine order (partition.cpp:433-450)
+__global__ void k_fold_engines(const double* __restrict__ parts, int G, double* out, int sqrt_out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double t[64];
+    for (int i = 0; i < G; ++i) t[i] = parts[i];
+    int m = G;
+    while (m > 1) {
+        int w = 0;
+        for (int i = 0; i + 1 < m; i += 2) t[w++] = t[i] + t[i + 1];
+        if (m % 2) t[w++] = t[m - 1];
+        m = w;
+    }
+    out[0] = sqrt_out ? sqrt(t[0]) : t[0];
+}
+void fold_engines(const double* parts, int G, double* out, bool sqrt_out, cudaStream_t s) {
+    k_fold_engines<<<1, 32, 0, s>>>(parts, G, out, sqrt_out ? 1 : 0);
+    count_launch();
+}
+
+__global__ void k_pack_rows(int n, int cnt, const int* __restrict__ idx, const double* __restrict__ x, double* out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= cnt * n) return;
+    const int r = t / n, q = t - r * n;
+    out[t] = x[static_cast<size_t>(idx[r]) * n + q];
+}
+void pack_rows(int n, int cnt, const int* idx, const double* x, double* out, cudaStream_t s) {
+    if (cnt <= 0) return;
+    k_pack_rows<<<(cnt * n + 255) / 256, 256, 0, s>>>(n, cnt, idx, x, out);
     count_launch();
 }
 
@@ -97,7 +132,7 @@ __global__ void __launch_bounds__(kRedThreads) k_axpy_dot(double* __restrict__ w
                                                           const double* __restrict__ v,
                                                           const double* __restrict__ nextv,
                                                           const long long* __restrict__ seg, int nseg, double* out,
-                                                          double* partials, int* ticket) {
+                                                          double* partials, int* ticket, int sq) {
     const double hv = *h;
     const SegRange R = seg_range(seg, nseg);
     double s = 0.0;
@@ -106,12 +141,14 @@ __global__ void __launch_bounds__(kRedThreads) k_axpy_dot(double* __restrict__ w
         w[i] = wn;
         s += nextv ? wn * nextv[i] : wn * wn;
     }
-    finish_reduction(s, nseg, partials, ticket, out, nextv == nullptr);
+    finish_reduction(s, nseg, partials, ticket, out, sq != 0);
 }
 
 void axpy_dot(double* w, const double* h, const double* v, const double* nextv, const long long* seg, int nseg,
-              double* out, double* partials, int* ticket, cudaStream_t s) {
-    k_axpy_dot<<<seg_grid(nseg), kRedThreads, 0, s>>>(w, h, v, nextv, seg, nseg, out, partials, ticket);
+              double* out, double* partials, int* ticket, cudaStream_t s, int bps, int sqrt_mode) {
+    const int g = bps > 0 ? bps * nseg : seg_grid(nseg);
+    const int sq = sqrt_mode < 0 ? (nextv == nullptr ? 1 : 0) : sqrt_mode;
+    k_axpy_dot<<<g, kRedThreads, 0, s>>>(w, h, v, nextv, seg, nseg, out, partials, ticket, sq);
     count_launch();
 }
 

@@ -167,11 +167,16 @@ int reduce_blocks();
 // segment sums are folded with the reference's pairwise engine tree.
 // partials >= reduce_blocks() + 4*nseg doubles.
 void dot(const double* a, const double* b, const long long* seg, int nseg, double* out, bool sqrt_out,
-         double* partials, int* ticket, cudaStream_t s);
+         double* partials, int* ticket, cudaStream_t s, int bps = 0);
 // w -= (*h) * v ; out = dot(w, nextv) (nextv == nullptr: out = sqrt(dot(w,w)))
 void axpy_dot(double* w, const double* h, const double* v, const double* nextv, const long long* seg, int nseg,
-              double* out, double* partials, int* ticket, cudaStream_t s);
+              double* out, double* partials, int* ticket, cudaStream_t s, int bps = 0, int sqrt_mode = -1);
 // Mode-R halo adds after the local product (partition.cpp:335-350)
+// blocks per segment of the segmented reductions with nseg segments
+int seg_blocks(int nseg);
+// multi-process Mode R: engine partials folded in the reference's tree; rows packed for a halo send
+void fold_engines(const double* parts, int G, double* out, bool sqrt_out, cudaStream_t s);
+void pack_rows(int n, int cnt, const int* idx, const double* x, double* out, cudaStream_t s);
 void halo_spmv(int n, int nhr, const int* hrow, const int* hoff, const int* hcol, const double* hv, const double* x,
                double* y, int rowStart, cudaStream_t s);
 // y = x / (*den) if (*den > thr) ; else untouched

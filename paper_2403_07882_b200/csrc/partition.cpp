@@ -201,4 +201,37 @@ std::vector<Partition> consolidate(const std::vector<Partition>& parts, const Co
     return eng;
 }
 
+ExchangePlan makeExchangePlan(const std::vector<Partition>& engines, int me) {
+    const int G = static_cast<int>(engines.size());
+    if (me < 0 || me >= G) throw std::invalid_argument("makeExchangePlan: engine out of range");
+    ExchangePlan x;
+    x.sendCount.assign(G, 0);
+    x.recvCount.assign(G, 0);
+    for (const auto& [peer, row] : engines[me].sendPlan) {  // sorted (peer, row)
+        x.sendRows.push_back(row);
+        ++x.sendCount[peer];
+    }
+    std::vector<std::pair<int, int>> where;  // (global row, recv index)
+    for (int q = 0; q < G; ++q) {
+        if (q == me) continue;
+        for (const auto& [peer, row] : engines[q].sendPlan)
+            if (peer == me) {
+                const int g = engines[q].rowStart + row;
+                where.emplace_back(g, static_cast<int>(x.recvGlobalRow.size()));
+                x.recvGlobalRow.push_back(g);
+                ++x.recvCount[q];
+            }
+    }
+    std::sort(where.begin(), where.end());
+    const Partition& p = engines[me];
+    x.haloRecvIdx.resize(p.haloCol.size());
+    for (size_t h = 0; h < p.haloCol.size(); ++h) {
+        const auto it = std::lower_bound(where.begin(), where.end(), std::make_pair(p.haloCol[h], -1));
+        if (it == where.end() || it->first != p.haloCol[h])
+            throw std::logic_error("makeExchangePlan: halo column without a sender");
+        x.haloRecvIdx[h] = it->second;
+    }
+    return x;
+}
+
 }  // namespace bcs

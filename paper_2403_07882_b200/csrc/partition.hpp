@@ -50,4 +50,16 @@ ConsolidationPlan makeConsolidationPlan(const Decomposition& dec, int nEngines);
 std::vector<Partition> consolidate(const std::vector<Partition>& parts, const ConsolidationPlan& plan,
                                    const Decomposition& dec);
 
+// Multi-process Mode R: what engine `me` sends to and receives from every
+// peer per halo exchange, and where each of its halo entries finds its value.
+// Send: the engine's sendPlan grouped by peer (peers ascending, local rows
+// ascending) -> sendRows, sendCount[peer].  Receive: every other engine's
+// sendPlan entries addressed to `me`, in that engine's order -> recvGlobalRow
+// (renumbered global rows), recvCount[peer]; peers ascending.  haloRecvIdx[h]
+// = position of haloCol[h] in the concatenated receive buffer.
+struct ExchangePlan {
+    std::vector<int> sendRows, sendCount, recvGlobalRow, recvCount, haloRecvIdx;
+};
+ExchangePlan makeExchangePlan(const std::vector<Partition>& engines, int me);
+
 }  // namespace bcs

@@ -61,3 +61,18 @@ def test_dist_iterations_grow_with_engines(ctx):
                            amg=bcs.AmgConfig(maxLevels=30, minCoarseRows=8))
     its = [ctx.dist_solve(s.A, s.b, s.x0, s.centroids, g, g, cfg)[1].iterations for g in (1, 2, 4, 8)]
     assert its[0] < its[1] <= its[2] + 1 and its[1] <= its[3] + 1
+
+
+def test_dist_mp_single_process_equals_one_device(ctx):
+    """The multi-process Mode R path (NCCL communicator of one process): the
+    same arithmetic as the one-device Mode R with one engine, bit for bit."""
+    uid = bcs.comm_unique_id()
+    ctx.comm_init(0, 1, uid)
+    for ranks in (1, 3):
+        s = gen.hex_euler(9, scramble_seed=5)
+        cfg = bcs.SolverConfig(preconditioner=bcs.PrecondKind.AMG, relTol=1e-9, maxIters=500,
+                               amg=bcs.AmgConfig(maxLevels=30, minCoarseRows=8))
+        x1, r1 = ctx.dist_solve(s.A, s.b, s.x0, s.centroids, ranks, 1, cfg)
+        x2, r2 = ctx.dist_solve_mp(s.A, s.b, s.x0, s.centroids, ranks, cfg)
+        assert r1.iterations == r2.iterations and r2.converged
+        assert x1.values.tobytes() == x2.values.tobytes()

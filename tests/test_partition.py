@@ -113,3 +113,70 @@ def test_gloo_world2_send_plans_match_halos():
         p.join(timeout=60)
     assert all(ok for _, ok, _ in res), res
     assert all(n > 0 for _, _, n in res)
+
+
+def _gloo_exchange_worker(rank, world, port, ranks, q):
+    """One process per engine: pack the rows of the exchange plan from this
+    engine's slice of a known global vector, exchange them with point-to-point
+    gloo messages in the order the NCCL path uses (peers ascending), and check
+    every halo entry reads its column's value from the receive buffer."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        s = gen.hex_euler(7, 6, 5, scramble_seed=3)
+        n = 5
+        P = bcs.Partition(s.A.n_cells, s.A.owner, s.A.neighbour, s.centroids, ranks, world)  # engines = processes
+        mine = P.part(rank)
+        x = P.exchange(rank)
+        g = np.arange(s.A.n_cells * n, dtype=np.float64).reshape(-1, n) * 1.5 + 0.25  # global (renumbered) vector
+        local = g[mine["row_start"]:mine["row_end"]]
+        send = local[x["send_row"]]
+        recv = np.zeros((x["recv_global_row"].size, n))
+        reqs, so, ro = [], 0, 0
+        for peer in range(world):
+            c = int(x["send_count"][peer])
+            if c:
+                reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(send[so:so + c])), peer))
+            so += c
+        bufs = []
+        for peer in range(world):
+            c = int(x["recv_count"][peer])
+            if c:
+                t = torch.zeros((c, n), dtype=torch.float64)
+                reqs.append(dist.irecv(t, peer))
+                bufs.append((ro, t))
+            ro += c
+        for r in reqs:
+            r.wait()
+        for o, t in bufs:
+            recv[o:o + t.shape[0]] = t.numpy()
+        ok = np.array_equal(recv, g[x["recv_global_row"]])
+        ok = ok and np.array_equal(recv[x["halo_recv_idx"]], g[mine["halo_col"]])
+        ok = ok and int(x["send_count"].sum()) == x["send_row"].size and int(x["send_count"][rank]) == 0
+        q.put((rank, bool(ok), int(mine["halo_col"].size)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ranks", [2, 5])
+def test_gloo_world2_exchange_plan(ranks):
+    """The multi-process Mode R halo exchange (bcs_partition_exchange_*, used by
+    bcs_dist_solve_mp over NCCL) delivers exactly the halo columns, world size 2."""
+    import multiprocessing as mp
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_exchange_worker, args=(r, 2, port, ranks, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _ in res), res
+    assert all(n > 0 for _, _, n in res)
