@@ -82,6 +82,9 @@ print(f"  no-spin rows: start->first poll returned median {np.median(poll1[z]):.
       f"first poll -> ready {np.median((cy0-cys)[z]-poll1[z]):.0f} cycles")
 w9 = buf.cpu().numpy().reshape(rows, 10)[:, 9]
 plain = (w9 & 0xFFFFFFFF).astype(np.float64); ry = (w9 >> 32).astype(np.float64)
-print(f"  probe RTT (settled rin line): strong median {np.median(tr[:,8]):.0f} p90 {np.percentile(tr[:,8],90):.0f}; "
+w8 = buf.cpu().numpy().reshape(rows, 10)[:, 8]
+probe = (w8 & 0xFFFFFFFF).astype(np.float64); swait = (w8 >> 32).astype(np.float64)
+print(f"  stage wait cycles: median {np.median(swait):.0f} p90 {np.percentile(swait,90):.0f} mean {swait.mean():.0f}")
+print(f"  probe RTT (settled rin line): strong median {np.median(probe):.0f} p90 {np.percentile(probe,90):.0f}; "
       f"ld.cg median {np.median(plain):.0f} p90 {np.percentile(plain,90):.0f} cycles")
 print(f"  first dependency poll RTT (no-spin rows): median {np.median(ry[z]):.0f} p90 {np.percentile(ry[z],90):.0f}; all rows median {np.median(ry):.0f}")
