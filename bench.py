@@ -62,6 +62,8 @@ def parse():
     p.add_argument("--method", default="gmres", choices=["gmres", "bicgstab"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--mode-r", action="store_true",
+                   help="strong scaling: one 128^3 system in the reference's Mode R over the N processes (NCCL)")
     p.add_argument("--scramble", type=int, default=-1,
                    help="randomly permuted cell order with this seed (SURVEY C4-style input); default natural order")
     return p.parse_args()
@@ -397,10 +399,68 @@ def sweep_traffic(n):
         return None
 
 
+def run_mode_r(args):
+    """Mode R over N processes (bcs_dist_solve_mp): one system, ranks = engines = N, strong scaling.  The
+    timed call is the drop-in multi-rank entry (host buffers in, whole solution out on every rank)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_07882_b200 import bcs, gen
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo")  # broadcast of the NCCL id only
+    uid = [bcs.comm_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0)
+    ctx = bcs.Context(local)
+    ctx.comm_init(rank, world, uid[0])
+
+    def pinned(size, dt):
+        t = torch.empty(size, dtype=torch.float64 if dt == np.float64 else torch.int32, pin_memory=True)
+        return t.numpy()
+
+    s = gen.hex_euler(args.size, scramble_seed=args.scramble, alloc=pinned)
+    cfg = solver_config(args.method)
+    for _ in range(max(args.warmup, 3)):
+        x, r = ctx.dist_solve_mp(s.A, s.b, s.x0, s.centroids, world, cfg)
+    times = []
+    for _ in range(args.steps):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        x, r = ctx.dist_solve_mp(s.A, s.b, s.x0, s.centroids, world, cfg)
+        times.append(time.perf_counter() - t0)
+    t = statistics.mean(times)
+    if world > 1:
+        tt = [None] * world
+        dist.all_gather_object(tt, t)
+        t = max(tt)
+    if rank == 0:
+        h2d = s.A.diag.nbytes + s.A.upper.nbytes + s.A.lower.nbytes + s.b.values.nbytes + s.x0.values.nbytes
+        print(json.dumps({
+            "metric": METRIC, "value": t, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args), "method": args.method,
+                       "precond": "AMG(maxLevels 30, minCoarseRows 8, DILU 1/1) per engine (Mode R)",
+                       "rel_tol": 1e-8, "parallelism": f"Mode R, {world} engines = processes (NCCL)"},
+            "iterations": r.iterations, "converged": r.converged,
+            "e2e": {"value": t, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step":
+                    int(s.A.n_cells * s.A.n * 8)},
+        }), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.mode_r:
+        run_mode_r(args)
     else:
         run_ours(args)
 
