@@ -205,7 +205,7 @@ def run_reference(args):
               f"row ratio {scale:.2f} to {args.size}^3" +
               (" (scrambled: the dense coarsest LU grows ~m^3, so the row-ratio scaling is a lower bound)"
                if args.scramble >= 0 else ""))
-    print(json.dumps({
+    emit({
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic", "impl": "reference",
@@ -213,7 +213,7 @@ def run_reference(args):
                    "precond": "AMG(maxLevels 30, minCoarseRows 8, DILU 1/1)", "rel_tol": 1e-8},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "reference", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }), flush=True)
+    })
 
 
 # --------------------------------------------------------------------- ours
@@ -377,7 +377,7 @@ def run_ours(args):
                               "bytes_per_launch": bytes_per, "mean_launch_ms": spmv_ms, "peak_kind": peak_kind},
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk.summary(),
         }
-        print(json.dumps(out), flush=True)
+        emit(out)
     ctx.close()
     if world > 1:
         torch.distributed.destroy_process_group()
@@ -439,7 +439,7 @@ def run_mode_r(args):
         t = max(tt)
     if rank == 0:
         h2d = s.A.diag.nbytes + s.A.upper.nbytes + s.A.lower.nbytes + s.b.values.nbytes + s.x0.values.nbytes
-        print(json.dumps({
+        emit({
             "metric": METRIC, "value": t, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -449,13 +449,32 @@ def run_mode_r(args):
             "iterations": r.iterations, "converged": r.converged,
             "e2e": {"value": t, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step":
                     int(s.A.n_cells * s.A.n * 8)},
-        }), flush=True)
+        })
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
 
 
+_JSON_FD = None
+
+
+def emit(obj):
+    """The one JSON line, on the real stdout (everything else written to fd 1 goes to stderr)."""
+    line = (json.dumps(obj) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(line.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, line)
+
+
 def main():
+    global _JSON_FD
+    # stdout carries exactly one JSON line: libraries that print to fd 1 (NCCL's
+    # "NCCL version" banner, CUDA/NCCL warnings) are redirected to stderr
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     args = parse()
     if args.impl == "reference":
         run_reference(args)
