@@ -139,6 +139,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* m = std::getenv("BCS_AGG_MODE")) aggMode_ = std::atoi(m);    // 1: barrier rounds
     if (const char* m = std::getenv("BCS_DILU_MODE")) diluMode_ = std::atoi(m);  // 1: Kahn levels
     if (const char* m = std::getenv("BCS_DENSE_BLOCKED_MIN")) denseBlockedMin_ = std::atoi(m);
+    if (const char* m = std::getenv("BCS_TAIL_ROWS")) tailMaxRows_ = std::atoi(m);
     check(cudaSetDevice(device), "cudaSetDevice");
     check(cudaStreamCreateWithFlags(&own_, cudaStreamNonBlocking), "cudaStreamCreate");
     stream_ = own_;
@@ -172,7 +173,7 @@ Engine::~Engine() {
         rel(L.agg); rel(L.members); rel(L.r); rel(L.z); rel(L.res); rel(L.y); rel(L.zb);
     }
     rel(dOwner_); rel(dNeigh_); rel(ro_); rel(ci_); rel(dg_); rel(tpos_); rel(src_); rel(fill_); rel(vals_);
-    rel(ldu_diag_); rel(ldu_upper_); rel(ldu_lower_); rel(main_.dense); rel(main_.dpiv); rel(cnt_); rel(lvl_); rel(push_);
+    rel(ldu_diag_); rel(ldu_upper_); rel(ldu_lower_); rel(main_.dense); rel(main_.dpiv); rel(main_.tailDesc); rel(cnt_); rel(lvl_); rel(push_);
     rel(scanTmp_); rel(dkeys_); rel(dorder_); rel(ddesc_); rel(act2_); rel(flag_); rel(err_); rel(ctr_); rel(choice_); rel(segOff_); rel(cro_); rel(big_); rel(dn_); rel(tblk_);
     rel(str_); rel(keys_); rel(sorted_); rel(V_); rel(w_); rel(zk_); rel(rk_); rel(Hm_); rel(cs_); rel(sn_); rel(g_);
     rel(y_); rel(scal_); rel(partials_); rel(kb_); rel(kx_); rel(bp_); rel(bv_); rel(bs_); rel(bt_); rel(bph_);
@@ -606,6 +607,43 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
             L.zb.ensure(N, stream_);
         }
     }
+    setupTail();
+}
+
+// the one-CTA coarse tail: the first level from which every smoothed level
+// has at most tailMaxRows_ rows (the coarsest is solved densely in between)
+void Engine::setupTail() {
+    H_->tail = -1;
+    if (tailMaxRows_ <= 0 || H_->nlev < 2) return;
+    int t = H_->nlev - 1;
+    while (t > 0 && H_->levels[t - 1].rows <= tailMaxRows_) --t;
+    if (t >= H_->nlev - 1) return;  // no smoothed level small enough
+    const int nl = H_->nlev - t;
+    std::vector<TailLevelDev> d(nl);
+    for (int q = 0; q < nl; ++q) {
+        Level& L = H_->levels[t + q];
+        TailLevelDev& x = d[q];
+        x.rows = L.rows;
+        x.ncoarse = L.ncoarse;
+        x.ro = L.ro;
+        x.ci = L.ci;
+        x.dg = L.dg;
+        x.order = L.order.p;
+        x.agg = L.agg.p;
+        x.members = L.members.p;
+        x.v = L.v;
+        x.lu = L.lu.p;
+        x.rcp = L.rcp.p;
+        x.perm = L.perm.p;
+        x.r = L.r.p;
+        x.z = L.z.p;
+        x.res = L.res.p;
+    }
+    H_->tailDesc.ensure(sizeof(TailLevelDev) * nl, stream_);
+    check(cudaMemcpyAsync(H_->tailDesc.p, d.data(), sizeof(TailLevelDev) * nl, cudaMemcpyHostToDevice, stream_),
+          "H2D tail");
+    sync();  // d dies here
+    H_->tail = t;
 }
 
 FineMatrix Engine::serialFine() const {
@@ -682,6 +720,18 @@ void Engine::smootherApply(Level& L, const double* r, double* z, int accumulate)
 void Engine::vcycle(int l, const double* r, double* z) {
     Level& L = H_->levels[l];
     const size_t N = static_cast<size_t>(L.rows) * n_;
+    if (l == H_->tail) {  // the whole coarse tail: one CTA down, dense coarsest, one CTA up
+        const int nl = H_->nlev - l;
+        const auto* td = reinterpret_cast<const TailLevelDev*>(H_->tailDesc.p);
+        const int pre = H_->pcCfg.amg_pre_sweeps, post = H_->pcCfg.amg_post_sweeps;
+        vcycle_tail(n_, nl, td, L.rows, r, z, pre, post, 0, err_.p + 1, stream_);
+        const Level& Cl = H_->levels[H_->nlev - 1];
+        if (H_->m >= denseBlockedMin_) dense_solve_big(H_->m, H_->dense, H_->dpiv, Cl.r, Cl.z.p, stream_);
+        else dense_solve(H_->m, H_->dense, H_->dpiv, Cl.r, Cl.z.p, stream_);
+        vcycle_tail(n_, nl, td, L.rows, r, z, pre, post, 1, err_.p + 1, stream_);
+        profMark("vcycle:tail L" + std::to_string(l) + "+");
+        return;
+    }
     if (l == H_->nlev - 1) {
         if (H_->m >= denseBlockedMin_) dense_solve_big(H_->m, H_->dense, H_->dpiv, r, z, stream_);
         else dense_solve(H_->m, H_->dense, H_->dpiv, r, z, stream_);

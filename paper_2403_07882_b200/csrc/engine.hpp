@@ -78,6 +78,8 @@ struct Hier {
     DArray<int> dpiv;
     int m = 0;
     int pcKind = -1;  // 0 none, 1 LUSGS, 2 DILU, 3 AMG
+    int tail = -1;    // first level of the one-CTA coarse tail (-1: none)
+    DArray<unsigned char> tailDesc;  // TailLevelDev[nlev - tail]
     bcs_solver_config pcCfg{};
 };
 
@@ -253,6 +255,8 @@ private:
     int aggMode_ = 0;   // 0 sync-free aggregation, 1 cooperative rounds
     int diluMode_ = 0;  // 0 sync-free level-ordered DILU setup, 1 Kahn levels
     int denseBlockedMin_ = kDenseBlockedMin;  // coarsest m from which the blocked dense LU/solve run
+    int tailMaxRows_ = kTailMaxRows;          // levels at most this big run in the one-CTA tail (0: off)
+    void setupTail();
     std::vector<std::pair<std::string, double>> profRec_;
     std::chrono::steady_clock::time_point profT_;
     void profMark(const std::string& what);

@@ -154,6 +154,22 @@ void prolong_vec(int n, int rows, const int* agg, const double* zc, double* z, c
 void dense_build(int n, int rows, const int* ro, const int* ci, const double* v, double* dense, cudaStream_t s);
 void dense_factor(int m, double* a, int* piv, int* err, cudaStream_t s);
 void dense_solve(int m, const double* lu, const int* piv, const double* r, double* z, cudaStream_t s);
+// the coarse tail of the V-cycle in one CTA (k_tail.cu).  Levels of the
+// tail, top (largest) first, coarsest last; phase 0 = down path of all but the
+// coarsest (pre-smoothing, residual, restriction), phase 1 = up path
+// (prolongation, post-smoothing); the coarsest dense solve runs in between.
+// rtop/ztop replace lv[0].r / lv[0].z.
+struct TailLevelDev {
+    int rows, ncoarse;
+    const int *ro, *ci, *dg, *order, *agg, *members;
+    const double *v, *lu, *rcp;
+    const int* perm;
+    double *r, *z, *res;
+};
+constexpr int kTailMaxRows = 512;
+size_t tail_smem_bytes(int n, int rows);
+void vcycle_tail(int n, int nl, const TailLevelDev* lv, int top_rows, const double* rtop, double* ztop, int pre,
+                 int post, int phase, int* err, cudaStream_t s);
 // blocked variants for large coarsest levels (k_dense.cu); piv: 2m ints
 // (pivots, then the composed permutation the solve uses)
 constexpr int kDenseBlockedMin = 256;
