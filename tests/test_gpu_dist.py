@@ -76,3 +76,14 @@ def test_dist_mp_single_process_equals_one_device(ctx):
         x2, r2 = ctx.dist_solve_mp(s.A, s.b, s.x0, s.centroids, ranks, cfg)
         assert r1.iterations == r2.iterations and r2.converged
         assert x1.values.tobytes() == x2.values.tobytes()
+
+
+def test_dist_mp_requires_comm_init():
+    c = bcs.Context(0)
+    try:
+        s = gen.hex_euler(4)
+        cfg = bcs.SolverConfig(preconditioner=bcs.PrecondKind.AMG)
+        with pytest.raises(ValueError, match="bcs_comm_init"):
+            c.dist_solve_mp(s.A, s.b, s.x0, s.centroids, 2, cfg)
+    finally:
+        c.close()
