@@ -70,3 +70,22 @@ def test_sweep_variants_bit_exact(oracle):
             assert z.tobytes() == zo.tobytes(), s.name
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("env", [{"BCS_AGG_MODE": "1"}, {"BCS_DILU_MODE": "1"}, {"BCS_TAIL_ROWS": "0"},
+                                 {"BCS_TAIL_ROWS": "100000"}])
+def test_alternative_schedules_bit_exact(oracle, env, monkeypatch):
+    """The alternative schedules (cooperative-round aggregation, Kahn-level DILU
+    setup, no one-CTA tail, everything in the tail) give the same bits."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    ctx = bcs.Context(0)
+    try:
+        s = gen.hex_euler(12, scramble_seed=2)
+        cfg = make_cfg(precond=3, max_levels=30, min_coarse=8)
+        r = np.random.default_rng(9).uniform(-1, 1, s.A.n_cells * s.A.n)
+        z = _apply(ctx, s, cfg, r)
+        zo = oracle.precond_apply(s.A, cfg, r)
+        assert z.tobytes() == zo.tobytes()
+    finally:
+        ctx.close()
