@@ -465,7 +465,7 @@ void Engine::packSweeps(Level& L) {
     for (int d = 0; d < 2; ++d) {
         DArray<int>& off = d == 0 ? L.offf : L.offb;
         off.ensure(n1, stream_);
-        sweep_slot_sizes(n_, L.rows, d == 0 ? L.recf : L.recb, off.p, stream_);
+        sweep_slot_sizes(n_, d == 0, L.rows, L.depth, d == 0 ? L.recf : L.recb, off.p, stream_);
         exclusive_scan(off.p, L.rows, off.p + L.rows, scanTmp_.p, stream_);
         check(cudaMemcpyAsync(&tot[d], off.p + L.rows, sizeof(int), cudaMemcpyDeviceToHost, stream_), "slot total");
     }

@@ -99,7 +99,7 @@ void sweep_records(int rows, const int* order, const int* ro, const int* dg, int
 // per-ticket slots (the sweep program): slot sizes in 16-byte units into
 // off16 (rows entries; the caller scans them, off16[rows] = total), then the
 // packed slots of one direction (rec4 = that direction's records).
-void sweep_slot_sizes(int n, int rows, const int* rec4, int* off16, cudaStream_t s);
+void sweep_slot_sizes(int n, bool fwd, int rows, int depth, const int* rec4, int* off16, cudaStream_t s);
 void sweep_pack(int n, bool fwd, int rows, int depth, const int* rec4, const int* ci, const double* v,
                 const double* lu, const int* perm, const double* rcp, const int* off16, unsigned char* pk,
                 cudaStream_t s);
