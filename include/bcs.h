@@ -47,7 +47,12 @@ typedef enum {
 } bcs_status;
 
 /* KrylovMethod / PrecondKind (krylov.hpp:15-16) */
-enum { BCS_GMRES = 0, BCS_BICGSTAB = 1 };
+enum { BCS_GMRES = 0, BCS_BICGSTAB = 1,
+       /* Flexible GMRES (north_star "FGMRES"): the reference's Arnoldi process with
+        * z_j = M^-1 v_j kept, x += Z y at restart/exit instead of x += M^-1(V y).
+        * Identical Arnoldi scalars (residual history), one V-cycle fewer per
+        * restart cycle; the update differs from GMRES only by rounding. */
+       BCS_FGMRES = 2 };
 enum { BCS_PRECOND_NONE = 0, BCS_PRECOND_LUSGS = 1, BCS_PRECOND_DILU = 2, BCS_PRECOND_AMG = 3 };
 /* Backend (engine.hpp:17).  HOST_LDU keeps the reference's contract (only
  * none/LUSGS allowed, zero convert/setup/retrieve timings) but executes on the
@@ -57,7 +62,7 @@ enum { BCS_BACKEND_HOST_LDU = 0, BCS_BACKEND_ENGINE_CSR = 1 };
 /* SolverConfig + AmgConfig (krylov.hpp:18-37).  The leading fields are
  * layout-identical to the oracle's or_cfg. */
 typedef struct {
-    int method;              /* BCS_GMRES | BCS_BICGSTAB            (default GMRES) */
+    int method;              /* BCS_GMRES | BCS_BICGSTAB | BCS_FGMRES (default GMRES) */
     int precond;             /* BCS_PRECOND_*                        (default LUSGS) */
     double rel_tol;          /* (default 1e-6)  */
     double abs_tol;          /* (default 1e-300) */
@@ -103,6 +108,14 @@ const char* bcs_last_error(const bcs_ctx* ctx);
  * restores the context's own stream. */
 bcs_status bcs_set_stream(bcs_ctx* ctx, void* stream);
 bcs_status bcs_set_kernel_timing(bcs_ctx* ctx, int enable);
+
+/* Page-locked host buffers from a process-wide cache (cudaHostAlloc'd blocks
+ * are kept on free and reused by the next request of the same size class), so
+ * a caller that allocates its result vectors here gets full-rate DMA and no
+ * page faults on every call.  The Python mirror allocates the BlockVector
+ * returned by SolvePipeline::solve this way. */
+bcs_status bcs_host_alloc(size_t bytes, void** out);
+void bcs_host_free(void* p);
 
 /* topologySignature (block_csr.cpp:146-160), exact; host only. */
 uint64_t bcs_topology_signature(int n_cells, int n_faces, const int32_t* owner, const int32_t* neighbour);

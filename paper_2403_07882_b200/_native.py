@@ -9,6 +9,8 @@ from __future__ import annotations
 import ctypes
 import os
 
+import numpy as np
+
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(_HERE, "lib")
 LIB_PATH = os.path.join(LIB_DIR, "libbcs.so")
@@ -84,6 +86,8 @@ SIGNATURES = {
     "bcs_last_error": (ctypes.c_char_p, [c_void_p]),
     "bcs_set_stream": (c_int, [c_void_p, c_void_p]),
     "bcs_set_kernel_timing": (c_int, [c_void_p, c_int]),
+    "bcs_host_alloc": (c_int, [c_size_t, P(c_void_p)]),
+    "bcs_host_free": (None, [c_void_p]),
     "bcs_topology_signature": (c_uint64, [c_int, c_int, c_void_p, c_void_p]),
     "bcs_pipeline_solve": (
         c_int,
@@ -129,6 +133,22 @@ GEN_SIGNATURES = {
 
 _lib = None
 _gen = None
+
+
+def pinned_empty(count: int, dtype=np.float64) -> np.ndarray:
+    """Uninitialised array in page-locked host memory from the library's
+    pinned-buffer cache (bcs_host_alloc); the block returns to the cache when
+    the array is garbage-collected."""
+    import weakref
+    dt = np.dtype(dtype)
+    nbytes = max(1, int(count) * dt.itemsize)
+    p = c_void_p()
+    L = lib()
+    if L.bcs_host_alloc(nbytes, ctypes.byref(p)) != 0 or not p.value:
+        raise MemoryError(f"bcs_host_alloc({nbytes}) failed")
+    raw = (ctypes.c_ubyte * nbytes).from_address(p.value)
+    weakref.finalize(raw, L.bcs_host_free, p.value)
+    return np.frombuffer(raw, dtype=dt, count=int(count))
 
 
 def _bind(lib, sigs):

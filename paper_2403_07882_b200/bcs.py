@@ -26,6 +26,7 @@ from . import _native as N
 class KrylovMethod(enum.IntEnum):
     GMRES = 0
     PBiCGStab = 1
+    FGMRES = 2  # flexible GMRES (x += Z y); same Arnoldi scalars as GMRES
 
 
 class PrecondKind(enum.IntEnum):
@@ -269,7 +270,8 @@ class Context:
 
     def pipeline_solve(self, A: BlockLduMatrix, b: BlockVector, x0: BlockVector, backend: Backend,
                        cfg: SolverConfig) -> Tuple[BlockVector, SolveReport]:
-        x = BlockVector(A.n_cells, A.n)
+        # the result lives in cached page-locked memory: full-rate D2H, no page faults
+        x = BlockVector(A.n_cells, A.n, values=N.pinned_empty(A.n_cells * A.n))
         rep = N.ReportC()
         c = cfg.to_c()
         st = self._lib.bcs_pipeline_solve(

@@ -7,6 +7,8 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cstring>
 #include <new>
 #include <string>
@@ -81,6 +83,52 @@ void bcs_default_config(bcs_solver_config* c) {
 }
 
 const char* bcs_version(void) { return "bcs 0.1 (sm_100a)"; }
+
+// pinned host-buffer cache: size class -> free blocks; live block -> class
+namespace {
+std::mutex g_host_mu;
+std::multimap<size_t, void*> g_host_free;
+std::map<void*, size_t> g_host_live;
+size_t host_class(size_t bytes) {
+    size_t c = 4096;
+    while (c < bytes) c <<= 1;
+    return c;
+}
+}  // namespace
+
+bcs_status bcs_host_alloc(size_t bytes, void** out) {
+    if (!out) return BCS_INVALID_ARGUMENT;
+    *out = nullptr;
+    const size_t cls = host_class(bytes ? bytes : 1);
+    {
+        std::lock_guard<std::mutex> g(g_host_mu);
+        auto it = g_host_free.find(cls);
+        if (it != g_host_free.end()) {
+            *out = it->second;
+            g_host_free.erase(it);
+            g_host_live[*out] = cls;
+            return BCS_OK;
+        }
+    }
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, cls, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        return BCS_OUT_OF_MEMORY;
+    }
+    std::lock_guard<std::mutex> g(g_host_mu);
+    g_host_live[p] = cls;
+    *out = p;
+    return BCS_OK;
+}
+
+void bcs_host_free(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(g_host_mu);
+    auto it = g_host_live.find(p);
+    if (it == g_host_live.end()) return;
+    g_host_free.emplace(it->second, p);
+    g_host_live.erase(it);
+}
 
 bcs_status bcs_create(bcs_ctx** out, int device) {
     if (!out) return BCS_INVALID_ARGUMENT;

@@ -348,7 +348,7 @@ void Engine::validateConfig(const bcs_solver_config& c) const {
     if (c.gmres_restart < 1) throw std::invalid_argument("SolverConfig: gmresRestart must be >= 1");
     if (c.amg_max_levels < 1) throw std::invalid_argument("SolverConfig: amg.maxLevels must be >= 1");
     if (c.amg_pre_sweeps < 0 || c.amg_post_sweeps < 0) throw std::invalid_argument("SolverConfig: amg sweeps must be >= 0");
-    if (c.method != BCS_GMRES && c.method != BCS_BICGSTAB) throw std::invalid_argument("unknown Krylov method");
+    if (c.method != BCS_GMRES && c.method != BCS_BICGSTAB && c.method != BCS_FGMRES) throw std::invalid_argument("unknown Krylov method");
     if (c.precond < 0 || c.precond > 3) throw std::invalid_argument("unknown preconditioner kind");
 }
 
@@ -807,6 +807,8 @@ void Engine::gmres(const double* b, double* x, const bcs_solver_config& cfg, bcs
         return;
     }
     V_.ensure(static_cast<size_t>(m + 1) * N, stream_);
+    const bool flexible = cfg.method == BCS_FGMRES;
+    if (flexible) Z_.ensure(static_cast<size_t>(m) * N, stream_);
     Hm_.ensure(static_cast<size_t>(m + 1) * m, stream_);
     cs_.ensure(m, stream_);
     sn_.ensure(m, stream_);
@@ -823,8 +825,9 @@ void Engine::gmres(const double* b, double* x, const bcs_solver_config& cfg, bcs
         bool happy = false;
         for (; j < m && total < cfg.max_iters; ++j, ++total) {
             double* vj = V_.p + static_cast<size_t>(j) * N;
-            opPrecond(vj, zk_.p);
-            opSpmv(zk_, w_.p);
+            double* zj = flexible ? Z_.p + static_cast<size_t>(j) * N : zk_.p;
+            opPrecond(vj, zj);
+            opSpmv(zj, w_.p);
             opDot(w_, V_.p, Hm_.p + j, false);
             for (int i = 0; i < j; ++i)
                 opAxpyDot(w_.p, Hm_.p + static_cast<size_t>(i) * m + j, V_.p + static_cast<size_t>(i) * N,
@@ -846,11 +849,16 @@ void Engine::gmres(const double* b, double* x, const bcs_solver_config& cfg, bcs
                 break;
             }
         }
-        // back substitution, x += M^{-1}(V y)
+        // back substitution, x += M^{-1}(V y)   (FGMRES: x += Z y)
         back_subst(Hm_, m, j, g_, y_.p, stream_);
-        lincomb(V_, N, y_, j, w_.p, N, stream_);
-        opPrecond(w_, zk_.p);
-        add_to(x, zk_, N, stream_);
+        if (flexible) {
+            lincomb(Z_, N, y_, j, w_.p, N, stream_);
+            add_to(x, w_, N, stream_);
+        } else {
+            lincomb(V_, N, y_, j, w_.p, N, stream_);
+            opPrecond(w_, zk_.p);
+            add_to(x, zk_, N, stream_);
+        }
         opResidual(x, b, rk_.p);
         beta = dotHost(rk_, rk_, N, true);
         if (!hist_.empty()) hist_.back() = beta / beta0;
@@ -978,7 +986,7 @@ void Engine::solveDevice(const double* d_b, double* d_x, const bcs_solver_config
 }
 
 void Engine::solveKrylov(const double* d_b, double* d_x, const bcs_solver_config& cfg, bcs_report& rep) {
-    if (cfg.method == BCS_GMRES) gmres(d_b, d_x, cfg, rep);
+    if (cfg.method == BCS_GMRES || cfg.method == BCS_FGMRES) gmres(d_b, d_x, cfg, rep);
     else bicgstab(d_b, d_x, cfg, rep);
     sync();
     collectSpmvTimes();

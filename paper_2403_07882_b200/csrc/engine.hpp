@@ -218,7 +218,7 @@ private:
     DArray<unsigned long long> keys_, sorted_;
 
     // Krylov workspace
-    DArray<double> V_, w_, zk_, rk_, Hm_, cs_, sn_, g_, y_, scal_, partials_;
+    DArray<double> V_, Z_, w_, zk_, rk_, Hm_, cs_, sn_, g_, y_, scal_, partials_;
     DArray<double> kb_, kx_;  // staging for host-array entry points
     DArray<double> bp_, bv_, bs_, bt_, bph_, bsh_, brh_;
     DArray<int> ticket_;
