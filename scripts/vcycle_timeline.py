@@ -27,6 +27,13 @@ ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUD
 iv = sorted((e.time_range.start, e.time_range.end, e.name.split("(")[0].replace("void ", "")) for e in ev)
 # the V-cycles: from a k_sweep2 fwd launch following a k_scale_by/k_spmv to the next
 starts = [i for i, (_, _, nm) in enumerate(iv) if "k_scale_by" in nm]
+for l in range(ctx.amg_depth() - 1):
+    import ctypes
+    rr, nz = ctypes.c_int(), ctypes.c_int()
+    ctx._lib.bcs_amg_level_sizes(ctx.h, l, ctypes.byref(rr), ctypes.byref(nz))
+    rows_l, nnz_l = rr.value, nz.value
+    d = ctx.schedule_depth(l)
+    print(f"level {l}: rows {rows_l} nnz {nnz_l} depth {d} width {rows_l / max(d, 1):.1f}")
 print(f"solve: {r.iterations} its, {len(iv)} GPU records, span {(iv[-1][1]-iv[0][0])/1e3:.1f} ms")
 if len(starts) >= 3:
     a, b = starts[1], starts[2]
