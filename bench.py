@@ -141,6 +141,9 @@ def solver_config(method):
                             gmresRestart=30, amg=bcs.AmgConfig(maxLevels=30, minCoarseRows=8))
 
 
+TAIL_ROWS = 512  # Engine::tailMaxRows_ default (levels handled by k_vcycle_tail)
+
+
 def chain_hop_ns(bcs, L=20000, reps=3):
     """Measured latency floor of the sweep kernel: a DILU application on a 1-D
     chain of L 5x5 rows (every row depends on the previous one) costs 2L hops."""
@@ -298,15 +301,18 @@ def run_ours(args):
     latency = None
     try:
         nlev = ctx.amg_depth()
-        depth_sum = sum(ctx.schedule_depth(l) for l in range(max(0, nlev - 1)))
-        vcycles = sw_n / args.steps / (4 * max(1, nlev - 1))
+        # levels smoothed by k_sweep launches: the coarse tail (levels of at
+        # most TAIL_ROWS rows, one-CTA kernel) and the dense coarsest are not
+        swept = [l for l in range(max(0, nlev - 1)) if ctx.amg_level_rows(l) > TAIL_ROWS]
+        depth_sum = sum(ctx.schedule_depth(l) for l in swept)
+        vcycles = sw_n / args.steps / (4 * max(1, len(swept)))
         hops = vcycles * 4 * depth_sum
         hop = chain_hop_ns(bcs)
         floor_ms = hops * hop * 1e-6
         latency = {"hops_per_step": hops, "chain_hop_ns": hop, "floor_ms_per_step": floor_ms,
                    "measured_ms_per_step": sw_ms / args.steps,
                    "frac": floor_ms / (sw_ms / args.steps) if sw_ms else None,
-                   "note": "sum over levels of 4 sweeps x dependency depth x V-cycles, times the sweep kernel's "
+                   "note": "sum over the swept levels of 4 sweeps x dependency depth x V-cycles, times the fastest sweep variant's "
                            "own hop on a 1-D 5x5 chain (DILU apply, 2L hops)"}
     except Exception as e:  # diagnostic only
         latency = {"unavailable": str(e)}

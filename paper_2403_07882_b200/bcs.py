@@ -263,6 +263,11 @@ class Context:
         self._ck(self._lib.bcs_amg_level_get(self.h, level, N.ptr(ro), N.ptr(ci), N.ptr(v), N.ptr(agg)))
         return ro, ci, v, agg
 
+    def amg_level_rows(self, level: int) -> int:
+        rows, nnz = ctypes.c_int(), ctypes.c_int()
+        self._ck(self._lib.bcs_amg_level_sizes(self.h, level, ctypes.byref(rows), ctypes.byref(nnz)))
+        return rows.value
+
     def schedule_depth(self, level: int) -> int:
         d = ctypes.c_int()
         self._ck(self._lib.bcs_level_schedule_depth(self.h, level, ctypes.byref(d)))
