@@ -86,8 +86,10 @@ __device__ void tail_sweep(const TailLevelDev& L, const double* rin, double* ys,
 #pragma unroll
             for (int e = 0; e < DPP; ++e) sg[e] = __shfl_sync(kAll, sblk, e * N + (lane < N ? lane : 0));
 #pragma unroll
-            for (int e = 0; e < DPP; ++e)
-                if (e < ne) acc = FWD ? __dsub_rn(acc, sg[e]) : __dadd_rn(acc, sg[e]);
+            for (int e = 0; e < DPP; ++e) {
+                if (e >= ne) break;  // a branch, not a select chain: ne FP steps on the critical path, not DPP
+                acc = FWD ? __dsub_rn(acc, sg[e]) : __dadd_rn(acc, sg[e]);
+            }
         }
         double x[N];
 #pragma unroll
