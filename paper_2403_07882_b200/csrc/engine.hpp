@@ -260,6 +260,7 @@ private:
     std::vector<std::pair<std::string, double>> profRec_;
     std::chrono::steady_clock::time_point profT_;
     void profMark(const std::string& what);
+    bool sameFaces(const int32_t* owner, const int32_t* neigh, int nf) const;
     void profDump();
     cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evPool_;

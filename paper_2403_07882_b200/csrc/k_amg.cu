@@ -43,28 +43,60 @@ __global__ void k_diag_norm(int rows, const int* __restrict__ dg, const double* 
     dn[r] = d >= 0 ? frob<N>(v + static_cast<size_t>(d) * N * N) : 0.0;
 }
 
-// str[k] = ||A_k||_F / sqrt(max(dn_r dn_j, 1e-300))   (amg.cpp:27-28)
+// str[k] = ||A_k||_F / sqrt(max(dn_r dn_j, 1e-300))   (amg.cpp:27-28).
+// Same values, block-parallel: a CTA stages 256 consecutive blocks through
+// shared memory with coalesced 16-byte loads (a thread per row would read
+// 200-byte blocks 8 bytes at a time from 32 rows at once), then thread t
+// takes block k0 + t: row by binary search, sequential Frobenius sum.
+constexpr int kStrChunk = 256;
 template <int N>
-__global__ void k_strength(int rows, const int* __restrict__ ro, const int* __restrict__ ci,
-                           const double* __restrict__ v, const double* __restrict__ dn, double* str) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= rows) return;
-    const double dr = dn[r];
-    for (int k = ro[r]; k < ro[r + 1]; ++k) {
-        const int j = ci[k];
-        const double prod = __dmul_rn(dr, dn[j]);
-        const double den = __dsqrt_rn(prod < 1e-300 ? 1e-300 : prod);  // std::max(prod, 1e-300)
-        str[k] = __ddiv_rn(frob<N>(v + static_cast<size_t>(k) * N * N), den);
+__global__ void __launch_bounds__(kStrChunk) k_strength_blk(int rows, int nnz, const int* __restrict__ ro,
+                                                            const int* __restrict__ ci,
+                                                            const double* __restrict__ v,
+                                                            const double* __restrict__ dn, double* str) {
+    constexpr int NN = N * N;
+    extern __shared__ __align__(16) double sblk[];
+    const int k0 = blockIdx.x * kStrChunk;
+    const int cnt = nnz - k0 < kStrChunk ? nnz - k0 : kStrChunk;
+    const double* src = v + static_cast<size_t>(k0) * NN;
+    const int tot = cnt * NN;
+    if ((NN & 1) == 0 || (k0 & 1) == 0) {  // 16-byte aligned source (k0 is a multiple of 256)
+        const int t2 = tot >> 1;
+        for (int e = threadIdx.x; e < t2; e += blockDim.x)
+            reinterpret_cast<double2*>(sblk)[e] = __ldcs(reinterpret_cast<const double2*>(src) + e);
+        if ((tot & 1) && threadIdx.x == 0) sblk[tot - 1] = __ldcs(src + tot - 1);
+    } else {
+        for (int e = threadIdx.x; e < tot; e += blockDim.x) sblk[e] = __ldcs(src + e);
     }
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t >= cnt) return;
+    const int k = k0 + t;
+    int lo = 0, hi = rows - 1;  // last row with ro[row] <= k
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(&ro[mid]) <= k) lo = mid;
+        else hi = mid - 1;
+    }
+    const double prod = __dmul_rn(__ldg(&dn[lo]), __ldg(&dn[__ldg(&ci[k])]));
+    const double den = __dsqrt_rn(prod < 1e-300 ? 1e-300 : prod);  // std::max(prod, 1e-300)
+    str[k] = __ddiv_rn(frob<N>(sblk + t * NN), den);
 }
 
 void strengths(int n, int rows, const int* ro, const int* ci, const int* dg, const double* v, double* dn,
-               double* str, cudaStream_t s) {
+               double* str, int nnz, cudaStream_t s) {
     const unsigned g = (rows + 255) / 256;
     if (!g) return;
+    const unsigned gb = (nnz + kStrChunk - 1) / kStrChunk;
     BCS_DISPATCH_N(n, {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_strength_blk<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(sizeof(double) * kStrChunk * N * N));
+            attr = true;
+        }
         k_diag_norm<N><<<g, 256, 0, s>>>(rows, dg, v, dn);
-        k_strength<N><<<g, 256, 0, s>>>(rows, ro, ci, v, dn, str);
+        k_strength_blk<N><<<gb, kStrChunk, sizeof(double) * kStrChunk * N * N, s>>>(rows, nnz, ro, ci, v, dn, str);
     });
     count_launch(2);
 }
@@ -682,13 +714,17 @@ void galerkin_count(int nCoarse, const int* seg_off, const unsigned long long* s
     count_launch();
 }
 
-// one warp per coarse row; lane e accumulates block element e of each slot
+// one warp per coarse row; lane e accumulates block element e of each slot.
+// Keys are read 8 at a time and their fine blocks loaded before the
+// (sequential, reference-order) accumulation, so a warp keeps 8 block loads
+// in flight instead of one dependent key -> block round trip per term.
 template <int N>
 __global__ void __launch_bounds__(256) k_fill(int nC, const int* __restrict__ ro, const int* __restrict__ members,
                                               const int* __restrict__ seg, const unsigned long long* __restrict__ sorted,
                                               const double* __restrict__ v, const int* __restrict__ cro, int* cci,
                                               double* cv) {
     constexpr int NN = N * N;
+    constexpr int KB = 8;
     const int lane = threadIdx.x & 31;
     const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (c >= nC) return;
@@ -699,20 +735,35 @@ __global__ void __launch_bounds__(256) k_fill(int nC, const int* __restrict__ ro
     int slot = cro[c] - 1;
     unsigned prev = 0;
     double acc = 0.0;
-    for (int i = sb; i < se; ++i) {
-        const unsigned long long key = sorted[i];
-        const unsigned J = static_cast<unsigned>(key >> 32);
-        const unsigned pos = static_cast<unsigned>(key & 0xFFFFFFFFull);
-        if (i == sb || J != prev) {
-            if (i != sb && lane < NN) cv[static_cast<size_t>(slot) * NN + lane] = acc;
-            ++slot;
-            if (lane == 0) cci[slot] = static_cast<int>(J);
-            acc = 0.0;
-            prev = J;
+    for (int i0 = sb; i0 < se; i0 += KB) {
+        const int nk = se - i0 < KB ? se - i0 : KB;  // warp-uniform
+        const unsigned long long mine = lane < nk ? __ldg(&sorted[i0 + lane]) : 0ull;
+        unsigned Js[KB], ps[KB];
+        double vals[KB];
+#pragma unroll
+        for (int e = 0; e < KB; ++e) {
+            const unsigned long long key = __shfl_sync(0xffffffffu, mine, e);
+            Js[e] = static_cast<unsigned>(key >> 32);
+            ps[e] = static_cast<unsigned>(key & 0xFFFFFFFFull);
+            vals[e] = 0.0;
+            if (e < nk && ps[e] != 0xFFFFFFFFu && lane < NN) {
+                const int k = ps[e] < static_cast<unsigned>(len1) ? b1 + static_cast<int>(ps[e])
+                                                                  : b2 + static_cast<int>(ps[e]) - len1;
+                vals[e] = __ldg(&v[static_cast<size_t>(k) * NN + lane]);
+            }
         }
-        if (pos != 0xFFFFFFFFu && lane < NN) {
-            const int k = pos < static_cast<unsigned>(len1) ? b1 + static_cast<int>(pos) : b2 + static_cast<int>(pos) - len1;
-            acc = __dadd_rn(acc, v[static_cast<size_t>(k) * NN + lane]);
+#pragma unroll
+        for (int e = 0; e < KB; ++e) {
+            if (e >= nk) break;
+            const int i = i0 + e;
+            if (i == sb || Js[e] != prev) {
+                if (i != sb && lane < NN) cv[static_cast<size_t>(slot) * NN + lane] = acc;
+                ++slot;
+                if (lane == 0) cci[slot] = static_cast<int>(Js[e]);
+                acc = 0.0;
+                prev = Js[e];
+            }
+            if (ps[e] != 0xFFFFFFFFu && lane < NN) acc = __dadd_rn(acc, vals[e]);
         }
     }
     if (lane < NN) cv[static_cast<size_t>(slot) * NN + lane] = acc;

@@ -118,7 +118,7 @@ unsigned long long selftest_chain(int variant, int L, int warps);  // total ns  
 
 // ------------------------------------------------------------ AMG (K9-K12)
 void strengths(int n, int rows, const int* ro, const int* ci, const int* dg, const double* v, double* dn,
-               double* str, cudaStream_t s);
+               double* str, int nnz, cudaStream_t s);
 // greedy pairwise matching (amg.cpp:10-37), exact; choice[r]: -2 taken, -1 singleton, >=0 partner
 void aggregate_kahn(int rows, const int* ro, const int* ci, const int* dg, const int* tpos, const double* str,
                     int* choice, KahnWork w, int* err, cudaStream_t s);
