@@ -66,6 +66,11 @@ def parse():
                    help="strong scaling: one 128^3 system in the reference's Mode R over the N processes (NCCL)")
     p.add_argument("--scramble", type=int, default=-1,
                    help="randomly permuted cell order with this seed (SURVEY C4-style input); default natural order")
+    p.add_argument("--system", default="euler", choices=["euler", "coupled"],
+                   help="5x5 density-based Jacobian (default, BASELINE configs[1]) or 4x4 pressure-based coupled p-U")
+    p.add_argument("--poly", type=int, default=-1,
+                   help="polyhedral augmentation seed: extra edge-diagonal faces on 30%% of the cells (C5 style)")
+    p.add_argument("--aspect", type=float, default=1.0, help="cell aspect ratio h_x/h_z (C4: 100)")
     return p.parse_args()
 
 
@@ -173,16 +178,23 @@ def chain_hop_ns(bcs, L=20000, reps=3):
         c.close()
 
 
+def make_system(args, n, alloc=None):
+    """The bench workload at n^3 cells (generator restating the reference producers)."""
+    from paper_2403_07882_b200 import gen
+    mk = gen.hex_coupled if args.system == "coupled" else gen.hex_euler
+    return mk(n, aspect=args.aspect, scramble_seed=args.scramble, alloc=alloc, poly_seed=args.poly)
+
+
 # ---------------------------------------------------------------- reference
-def reference_step_seconds(n_sample, method, calls, scramble=-1):
+def reference_step_seconds(args, n_sample, calls):
     """Replace-branch SolvePipeline::solve of the reference on the n_sample^3
     instance; returns per-call seconds (after one setup call)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle_lib import Reference, make_cfg
-    from paper_2403_07882_b200 import gen
 
+    method = args.method
     R = Reference()
-    s = gen.hex_euler(n_sample, scramble_seed=scramble)
+    s = make_system(args, n_sample)
     # the reference has no FGMRES; its GMRES runs the same Arnoldi process
     cfg = make_cfg(method=1 if method == "bicgstab" else 0, precond=3, max_iters=1000)
     R.solve(s.A, s.b.values, s.x0.values, cfg, calls=1, hist=False)  # setup branch
@@ -203,7 +215,7 @@ def run_reference(args):
     nc_full, _ = gen.hex_sizes(args.size, args.size, args.size)
     nc_s, _ = gen.hex_sizes(CPU_SAMPLE_N, CPU_SAMPLE_N, CPU_SAMPLE_N)
     scale = nc_full / nc_s
-    times, iters = reference_step_seconds(CPU_SAMPLE_N, args.method, args.warmup + args.steps, args.scramble)
+    times, iters = reference_step_seconds(args, CPU_SAMPLE_N, args.warmup + args.steps)
     timed = times[args.warmup:]
     v = statistics.mean(timed) * scale
     sample = (f"reference SolvePipeline::solve (EngineCsr, replace branch, GMRES+AMG to 1e-8, {iters} its) on the "
@@ -240,7 +252,7 @@ def run_ours(args):
         t = torch.empty(size, dtype=torch.float64 if dt == np.float64 else torch.int32, pin_memory=True)
         return t.numpy()
 
-    s = gen.hex_euler(n, scramble_seed=args.scramble, alloc=pinned)
+    s = make_system(args, n, alloc=pinned)
     A, b, x0 = s.A, s.b, s.x0
     nc, nf, nb = A.n_cells, A.nFaces(), A.n
     cfg = solver_config(args.method)
@@ -319,7 +331,7 @@ def run_ours(args):
     launches = sum(r.kernelLaunches for r in reps) + args.steps  # + one value-permutation kernel per step
     traffic = None
     tp = os.path.join(ROOT, "profiles", "spmv_traffic.json")
-    if os.path.exists(tp) and args.scramble < 0:  # the committed captures are of the natural-order workload
+    if os.path.exists(tp) and default_workload(args):  # the committed captures are of the default workload
         try:
             traffic = json.load(open(tp)).get(f"{n}")
         except Exception:
@@ -351,7 +363,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            times, its = reference_step_seconds(CPU_SAMPLE_N, args.method, 1, args.scramble)
+            times, its = reference_step_seconds(args, CPU_SAMPLE_N, 1)
             scale = nc / gen.hex_sizes(CPU_SAMPLE_N, CPU_SAMPLE_N, CPU_SAMPLE_N)[0]
             cpu = {"value": times[0] * scale, "unit": UNIT, "cores": 1, "kind": "reference",
                    "sample": f"one replace-branch reference SolvePipeline::solve on the {CPU_SAMPLE_N}^3 instance "
@@ -368,7 +380,8 @@ def run_ours(args):
             "config": {"workload": f"{workload_name(args)}, {nc} cells, {nc + 2 * nf} blocks per GPU",
                        "method": args.method, "precond": "AMG(maxLevels 30, minCoarseRows 8, DILU 1/1)",
                        "rel_tol": 1e-8, "x0": "zero",
-                       "l2": "inputs (2.9 GB BSR values) exceed the 126 MB L2; no flush needed",
+                       "l2": f"inputs ({(nc + 2 * nf) * nb * nb * 8 / 1e9:.1f} GB BSR values) exceed the 126 MB L2; "
+                             "no flush needed",
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
             "iterations": last.iterations, "amg_levels": last.amgLevels, "coarse_rows": last.coarseRows,
             "final_rel_residual": last.finalResidual / last.initialResidual,
@@ -376,14 +389,14 @@ def run_ours(args):
             "stage_s": {"amg_setup": last.timings.get("amgSetup"), "krylov": last.timings.get("krylov")},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": sw_achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (sw_achieved / peak) if sw_achieved else None, "traffic": sweep_traffic(n) if args.scramble < 0 else None,
-                         "kernel": "k_sweep<5,*> (DILU smoother sweeps, all AMG levels)",
+                         "frac": (sw_achieved / peak) if sw_achieved else None, "traffic": sweep_traffic(n) if default_workload(args) else None,
+                         "kernel": f"k_sweep*<{nb},*> (DILU smoother sweeps, all swept AMG levels)",
                          "bytes_per_launch": (sw_bytes / sw_n) if sw_n else None,
                          "mean_launch_ms": (sw_ms / sw_n) if sw_n else None, "launches_per_step": sw_n / args.steps,
                          "share_of_step": sw_share, "peak_kind": peak_kind,
                          "note": "dependency-latency bound (level depth x hop latency), see DESIGN.md", "latency": latency},
             "roofline_spmv": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                              "frac": achieved / peak, "traffic": traffic, "kernel": "k_spmv<5> (fine level)",
+                              "frac": achieved / peak, "traffic": traffic, "kernel": f"k_spmv<{nb}> (fine level)",
                               "bytes_per_launch": bytes_per, "mean_launch_ms": spmv_ms, "peak_kind": peak_kind},
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk.summary(),
         }
@@ -393,11 +406,23 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def default_workload(args):
+    return args.system == "euler" and args.scramble < 0 and args.poly < 0 and args.aspect == 1.0
+
+
 def workload_name(args):
-    base = f"5x5 density-based hex {args.size}^3"
+    base = (f"4x4 pressure-based coupled hex {args.size}^3" if args.system == "coupled"
+            else f"5x5 density-based hex {args.size}^3")
+    extra = []
+    if args.poly >= 0:
+        extra.append(f"edge-diagonal faces on a seeded 30% of the cells (seed {args.poly}, C5-style mixed connectivity)")
+    if args.aspect != 1.0:
+        extra.append(f"aspect ratio {args.aspect:g}")
     if args.scramble >= 0:
-        return base + f", randomly permuted cell order (seed {args.scramble})"
-    return base + " (BASELINE configs[1])"
+        extra.append(f"randomly permuted cell order (seed {args.scramble})")
+    if not extra and args.system == "euler":
+        return base + " (BASELINE configs[1])"
+    return base + ", " + ", ".join(extra)
 
 
 def sweep_traffic(n):
@@ -431,7 +456,7 @@ def run_mode_r(args):
         t = torch.empty(size, dtype=torch.float64 if dt == np.float64 else torch.int32, pin_memory=True)
         return t.numpy()
 
-    s = gen.hex_euler(args.size, scramble_seed=args.scramble, alloc=pinned)
+    s = make_system(args, args.size, alloc=pinned)
     cfg = solver_config(args.method)
     for _ in range(max(args.warmup, 3)):
         x, r = ctx.dist_solve_mp(s.A, s.b, s.x0, s.centroids, world, cfg)

@@ -118,7 +118,9 @@ void fillLdu(BlockLduMatrix& A, const double* diag, const double* upper, const d
 }
 
 // --- synthetic hex mesh built with the reference Mesh type ---
-Mesh hexMesh(int nx, int ny, int nz, double aspect, long long scrambleSeed, PatchKind kind) {
+// polySeed >= 0: the generator's polyhedral augmentation (csrc/gen/bcs_gen.cpp
+// buildHex): a seeded 30% of the cells get a face to (i+1, j+1, k).
+Mesh hexMesh(int nx, int ny, int nz, double aspect, long long scrambleSeed, PatchKind kind, long long polySeed = -1) {
     const double lx = 1.0, ly = 1.0 * ny / nx;
     const double hx = lx / nx, hy = ly / ny;
     const double hz = hx / aspect;
@@ -139,12 +141,17 @@ Mesh hexMesh(int nx, int ny, int nz, double aspect, long long scrambleSeed, Patc
         for (int j = 0; j < ny; ++j)
             for (int i = 0; i < nx; ++i) cen[id(i, j, k)] = {(i + 0.5) * hx, (j + 0.5) * hy, (k + 0.5) * hz};
     std::vector<InternalFace> faces;
+    std::mt19937_64 prng(static_cast<std::uint64_t>(polySeed >= 0 ? polySeed : 0));
+    const double dl = std::sqrt(hx * hx + hy * hy);
+    const double ds = 0.25 * hx * hz / dl;
     for (int k = 0; k < nz; ++k)
         for (int j = 0; j < ny; ++j)
             for (int i = 0; i < nx; ++i) {
                 if (i + 1 < nx) faces.push_back({id(i, j, k), id(i + 1, j, k), {hy * hz, 0.0, 0.0}, 0.5});
                 if (j + 1 < ny) faces.push_back({id(i, j, k), id(i, j + 1, k), {0.0, hx * hz, 0.0}, 0.5});
                 if (k + 1 < nz) faces.push_back({id(i, j, k), id(i, j, k + 1), {0.0, 0.0, hx * hy}, 0.5});
+                if (polySeed >= 0 && i + 1 < nx && j + 1 < ny && prng() % 10 < 3)
+                    faces.push_back({id(i, j, k), id(i + 1, j + 1, k), {hx * ds, hy * ds, 0.0}, 0.5});
             }
     std::vector<BoundaryPatch> patches;
     BoundaryPatch p;
@@ -287,10 +294,10 @@ void ref_hex_sizes(int nx, int ny, int nz, int* nCells, int* nFaces, int* nBound
 
 // 5x5 density-based system: assembleJacobian (euler.cpp:390-455) on the
 // synthetic hex mesh, first-order Roe, all-farfield, cfl 50.
-int ref_gen_euler(int nx, int ny, int nz, double aspect, long long scrambleSeed, int* owner, int* neigh,
-                  double* diag, double* upper, double* lower, double* rhs, double* centroids) {
+int ref_gen_euler_poly(int nx, int ny, int nz, double aspect, long long scrambleSeed, long long polySeed, int* owner,
+                       int* neigh, double* diag, double* upper, double* lower, double* rhs, double* centroids) {
     return guard([&] {
-        const Mesh mesh = hexMesh(nx, ny, nz, aspect, scrambleSeed, PatchKind::farfield);
+        const Mesh mesh = hexMesh(nx, ny, nz, aspect, scrambleSeed, PatchKind::farfield, polySeed);
         EulerCase ec;
         ec.flux = FluxScheme::Roe;
         ec.recon.firstOrder = true;
@@ -312,10 +319,11 @@ int ref_gen_euler(int nx, int ny, int nz, double aspect, long long scrambleSeed,
 
 // 4x4 pressure-based coupled system (incompressible.cpp:143-264): lid-driven
 // box, nu 0.01, zmax moving wall u=(1,0,0), pressure pinned in cell 0.
-int ref_gen_coupled(int nx, int ny, int nz, double aspect, long long scrambleSeed, int* owner, int* neigh,
-                    double* diag, double* upper, double* lower, double* rhs, double* x0, double* centroids) {
+int ref_gen_coupled_poly(int nx, int ny, int nz, double aspect, long long scrambleSeed, long long polySeed,
+                         int* owner, int* neigh, double* diag, double* upper, double* lower, double* rhs, double* x0,
+                         double* centroids) {
     return guard([&] {
-        const Mesh mesh = hexMesh(nx, ny, nz, aspect, scrambleSeed, PatchKind::wall);
+        const Mesh mesh = hexMesh(nx, ny, nz, aspect, scrambleSeed, PatchKind::wall, polySeed);
         BcMap bcs;
         for (const char* nm : {"xmin", "xmax", "ymin", "ymax", "zmin"}) bcs[nm] = {IncompressibleBc::Kind::wall, {}, 0.0};
         bcs["zmax"] = {IncompressibleBc::Kind::movingWall, {1.0, 0.0, 0.0}, 0.0};
@@ -333,6 +341,16 @@ int ref_gen_coupled(int nx, int ny, int nz, double aspect, long long scrambleSee
         exportLdu(A, b, owner, neigh, diag, upper, lower, rhs, centroids);
         std::memcpy(x0, state.values.data(), sizeof(double) * state.values.size());
     });
+}
+
+int ref_gen_euler(int nx, int ny, int nz, double aspect, long long scrambleSeed, int* owner, int* neigh,
+                  double* diag, double* upper, double* lower, double* rhs, double* centroids) {
+    return ref_gen_euler_poly(nx, ny, nz, aspect, scrambleSeed, -1, owner, neigh, diag, upper, lower, rhs, centroids);
+}
+int ref_gen_coupled(int nx, int ny, int nz, double aspect, long long scrambleSeed, int* owner, int* neigh,
+                    double* diag, double* upper, double* lower, double* rhs, double* x0, double* centroids) {
+    return ref_gen_coupled_poly(nx, ny, nz, aspect, scrambleSeed, -1, owner, neigh, diag, upper, lower, rhs, x0,
+                                centroids);
 }
 
 // testsup::randomize (tests/support/test_helpers.hpp:47-70) on caller topology.

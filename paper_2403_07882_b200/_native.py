@@ -129,6 +129,11 @@ GEN_SIGNATURES = {
     "bcsgen_hex_sizes": (None, [c_int, c_int, c_int, P(c_int), P(c_int)]),
     "bcsgen_hex_euler": (c_int, [c_int, c_int, c_int, c_double, ctypes.c_longlong] + [c_void_p] * 7),
     "bcsgen_hex_coupled": (c_int, [c_int, c_int, c_int, c_double, ctypes.c_longlong] + [c_void_p] * 8),
+    "bcsgen_hex_sizes_poly": (None, [c_int, c_int, c_int, ctypes.c_longlong, P(c_int), P(c_int)]),
+    "bcsgen_hex_euler_poly": (c_int, [c_int, c_int, c_int, c_double, ctypes.c_longlong, ctypes.c_longlong]
+                              + [c_void_p] * 7),
+    "bcsgen_hex_coupled_poly": (c_int, [c_int, c_int, c_int, c_double, ctypes.c_longlong, ctypes.c_longlong]
+                                + [c_void_p] * 8),
 }
 
 _lib = None

@@ -53,7 +53,13 @@ struct Hex {
     std::vector<std::vector<BFace>> patches;  // xmin xmax ymin ymax zmin zmax
 };
 
-Hex buildHex(int nx, int ny, int nz, double aspect, long long scrambleSeed) {
+// Polyhedral augmentation: with polySeed >= 0 a seeded 30%
+// of the cells (i, j, k) with i + 1 < nx, j + 1 < ny also get a face to their
+// edge-diagonal neighbour (i+1, j+1, k), area h_x h_z / 4 along the centroid
+// delta, emitted after the cell's +z face.  Draw: mt19937_64(polySeed)() % 10 < 3.
+inline bool polyPick(std::mt19937_64& prng) { return prng() % 10 < 3; }
+
+Hex buildHex(int nx, int ny, int nz, double aspect, long long scrambleSeed, long long polySeed = -1) {
     Hex h;
     const double lx = 1.0, ly = 1.0 * ny / nx;
     const double hx = lx / nx, hy = ly / ny, hz = hx / aspect;
@@ -85,12 +91,17 @@ Hex buildHex(int nx, int ny, int nz, double aspect, long long scrambleSeed) {
         h.neigh.push_back(b);
         h.area.push_back(s);
     };
+    std::mt19937_64 prng(static_cast<std::uint64_t>(polySeed >= 0 ? polySeed : 0));
+    const double dl = std::sqrt(hx * hx + hy * hy);
+    const double ds = 0.25 * hx * hz / dl;
     for (int k = 0; k < nz; ++k)
         for (int j = 0; j < ny; ++j)
             for (int i = 0; i < nx; ++i) {
                 if (i + 1 < nx) face(id(i, j, k), id(i + 1, j, k), {hy * hz, 0.0, 0.0});
                 if (j + 1 < ny) face(id(i, j, k), id(i, j + 1, k), {0.0, hx * hz, 0.0});
                 if (k + 1 < nz) face(id(i, j, k), id(i, j, k + 1), {0.0, 0.0, hx * hy});
+                if (polySeed >= 0 && i + 1 < nx && j + 1 < ny && polyPick(prng))
+                    face(id(i, j, k), id(i + 1, j + 1, k), {hx * ds, hy * ds, 0.0});
             }
     h.patches.resize(6);
     for (int k = 0; k < nz; ++k) for (int j = 0; j < ny; ++j) h.patches[0].push_back({id(0, j, k), {-hy * hz, 0.0, 0.0}});
@@ -494,24 +505,51 @@ void bcsgen_hex_sizes(int nx, int ny, int nz, int* nCells, int* nFaces) {
     *nFaces = (nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1);
 }
 
-// 5x5 density-based system. scrambleSeed < 0 keeps natural order.
-int bcsgen_hex_euler(int nx, int ny, int nz, double aspect, long long scrambleSeed, int* owner, int* neigh,
-                     double* diag, double* upper, double* lower, double* rhs, double* centroids) {
+// sizes with the polyhedral augmentation of polySeed (< 0: plain hex)
+void bcsgen_hex_sizes_poly(int nx, int ny, int nz, long long polySeed, int* nCells, int* nFaces) {
+    bcsgen_hex_sizes(nx, ny, nz, nCells, nFaces);
+    if (polySeed < 0) return;
+    std::mt19937_64 prng(static_cast<std::uint64_t>(polySeed));
+    int extra = 0;
+    for (int k = 0; k < nz; ++k)
+        for (int j = 0; j < ny; ++j)
+            for (int i = 0; i < nx; ++i)
+                if (i + 1 < nx && j + 1 < ny && polyPick(prng)) ++extra;
+    *nFaces += extra;
+}
+
+// 5x5 density-based system. scrambleSeed < 0 keeps natural order; polySeed < 0: plain hex.
+int bcsgen_hex_euler_poly(int nx, int ny, int nz, double aspect, long long scrambleSeed, long long polySeed,
+                          int* owner, int* neigh, double* diag, double* upper, double* lower, double* rhs,
+                          double* centroids) {
     if (nx < 1 || ny < 1 || nz < 1 || !(aspect > 0.0)) return 1;
-    const Hex h = buildHex(nx, ny, nz, aspect, scrambleSeed);
+    const Hex h = buildHex(nx, ny, nz, aspect, scrambleSeed, polySeed);
     exportTopo(h, owner, neigh, centroids);
     euler(h, diag, upper, lower, rhs);
     return 0;
 }
 
 // 4x4 pressure-based coupled system; x0 = the seeded state.
-int bcsgen_hex_coupled(int nx, int ny, int nz, double aspect, long long scrambleSeed, int* owner, int* neigh,
-                       double* diag, double* upper, double* lower, double* rhs, double* x0, double* centroids) {
+int bcsgen_hex_coupled_poly(int nx, int ny, int nz, double aspect, long long scrambleSeed, long long polySeed,
+                            int* owner, int* neigh, double* diag, double* upper, double* lower, double* rhs,
+                            double* x0, double* centroids) {
     if (nx < 1 || ny < 1 || nz < 1 || !(aspect > 0.0)) return 1;
-    const Hex h = buildHex(nx, ny, nz, aspect, scrambleSeed);
+    const Hex h = buildHex(nx, ny, nz, aspect, scrambleSeed, polySeed);
     exportTopo(h, owner, neigh, centroids);
     coupled(h, diag, upper, lower, rhs, x0);
     return 0;
+}
+
+int bcsgen_hex_euler(int nx, int ny, int nz, double aspect, long long scrambleSeed, int* owner, int* neigh,
+                     double* diag, double* upper, double* lower, double* rhs, double* centroids) {
+    return bcsgen_hex_euler_poly(nx, ny, nz, aspect, scrambleSeed, -1, owner, neigh, diag, upper, lower, rhs,
+                                 centroids);
+}
+
+int bcsgen_hex_coupled(int nx, int ny, int nz, double aspect, long long scrambleSeed, int* owner, int* neigh,
+                       double* diag, double* upper, double* lower, double* rhs, double* x0, double* centroids) {
+    return bcsgen_hex_coupled_poly(nx, ny, nz, aspect, scrambleSeed, -1, owner, neigh, diag, upper, lower, rhs, x0,
+                                   centroids);
 }
 
 } // extern "C"

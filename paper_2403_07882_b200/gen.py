@@ -3,6 +3,10 @@
 ``hex_euler``   — 5x5 density-based Jacobian (restates euler.cpp:390-455)
 ``hex_coupled`` — 4x4 pressure-based coupled p-U system (incompressible.cpp:143-264)
 
+``poly_seed >= 0`` adds the polyhedral augmentation of SURVEY §8(d) (C5): a
+seeded 30% of the cells get an extra face to their edge-diagonal neighbour
+(i+1, j+1, k), so rows have mixed 6/7/8... couplings.
+
 Both are bit-identical to the reference producers (tests/test_generator.py).
 """
 from __future__ import annotations
@@ -25,14 +29,14 @@ class System:
     name: str
 
 
-def hex_sizes(nx: int, ny: int, nz: int):
+def hex_sizes(nx: int, ny: int, nz: int, poly_seed: int = -1):
     nc, nf = ctypes.c_int(), ctypes.c_int()
-    N.gen().bcsgen_hex_sizes(nx, ny, nz, ctypes.byref(nc), ctypes.byref(nf))
+    N.gen().bcsgen_hex_sizes_poly(nx, ny, nz, int(poly_seed), ctypes.byref(nc), ctypes.byref(nf))
     return nc.value, nf.value
 
 
-def _alloc(nx, ny, nz, n, pinned_alloc=None):
-    nc, nf = hex_sizes(nx, ny, nz)
+def _alloc(nx, ny, nz, n, pinned_alloc=None, poly_seed=-1):
+    nc, nf = hex_sizes(nx, ny, nz, poly_seed)
     mk = pinned_alloc or (lambda size, dt: np.zeros(size, dt))
     owner = mk(nf, np.int32)
     neigh = mk(nf, np.int32)
@@ -44,32 +48,35 @@ def _alloc(nx, ny, nz, n, pinned_alloc=None):
     return nc, nf, owner, neigh, diag, upper, lower, rhs, cen
 
 
+def _tag(scramble_seed, poly_seed):
+    return ("scrambled" if scramble_seed >= 0 else "natural") + (f" poly{poly_seed}" if poly_seed >= 0 else "")
+
+
 def hex_euler(nx: int, ny: int = None, nz: int = None, aspect: float = 1.0, scramble_seed: int = -1,
-              alloc=None) -> System:
+              alloc=None, poly_seed: int = -1) -> System:
     ny = nx if ny is None else ny
     nz = nx if nz is None else nz
-    nc, nf, owner, neigh, diag, upper, lower, rhs, cen = _alloc(nx, ny, nz, 5, alloc)
-    rc = N.gen().bcsgen_hex_euler(nx, ny, nz, float(aspect), int(scramble_seed), N.ptr(owner), N.ptr(neigh),
-                                  N.ptr(diag), N.ptr(upper), N.ptr(lower), N.ptr(rhs), N.ptr(cen))
+    nc, nf, owner, neigh, diag, upper, lower, rhs, cen = _alloc(nx, ny, nz, 5, alloc, poly_seed)
+    rc = N.gen().bcsgen_hex_euler_poly(nx, ny, nz, float(aspect), int(scramble_seed), int(poly_seed), N.ptr(owner),
+                                       N.ptr(neigh), N.ptr(diag), N.ptr(upper), N.ptr(lower), N.ptr(rhs), N.ptr(cen))
     if rc:
         raise ValueError("bcsgen_hex_euler: bad arguments")
     A = BlockLduMatrix(nc, owner, neigh, 5, diag, upper, lower)
-    tag = "scrambled" if scramble_seed >= 0 else "natural"
     return System(A, BlockVector(nc, 5, rhs), BlockVector(nc, 5), cen.reshape(nc, 3),
-                  f"euler5 {nx}x{ny}x{nz} {tag} AR{aspect:g}")
+                  f"euler5 {nx}x{ny}x{nz} {_tag(scramble_seed, poly_seed)} AR{aspect:g}")
 
 
 def hex_coupled(nx: int, ny: int = None, nz: int = None, aspect: float = 1.0, scramble_seed: int = -1,
-                alloc=None) -> System:
+                alloc=None, poly_seed: int = -1) -> System:
     ny = nx if ny is None else ny
     nz = nx if nz is None else nz
-    nc, nf, owner, neigh, diag, upper, lower, rhs, cen = _alloc(nx, ny, nz, 4, alloc)
+    nc, nf, owner, neigh, diag, upper, lower, rhs, cen = _alloc(nx, ny, nz, 4, alloc, poly_seed)
     x0 = np.zeros(nc * 4)
-    rc = N.gen().bcsgen_hex_coupled(nx, ny, nz, float(aspect), int(scramble_seed), N.ptr(owner), N.ptr(neigh),
-                                    N.ptr(diag), N.ptr(upper), N.ptr(lower), N.ptr(rhs), N.ptr(x0), N.ptr(cen))
+    rc = N.gen().bcsgen_hex_coupled_poly(nx, ny, nz, float(aspect), int(scramble_seed), int(poly_seed), N.ptr(owner),
+                                         N.ptr(neigh), N.ptr(diag), N.ptr(upper), N.ptr(lower), N.ptr(rhs), N.ptr(x0),
+                                         N.ptr(cen))
     if rc:
         raise ValueError("bcsgen_hex_coupled: bad arguments")
     A = BlockLduMatrix(nc, owner, neigh, 4, diag, upper, lower)
-    tag = "scrambled" if scramble_seed >= 0 else "natural"
     return System(A, BlockVector(nc, 4, rhs), BlockVector(nc, 4, x0), cen.reshape(nc, 3),
-                  f"coupled4 {nx}x{ny}x{nz} {tag} AR{aspect:g}")
+                  f"coupled4 {nx}x{ny}x{nz} {_tag(scramble_seed, poly_seed)} AR{aspect:g}")

@@ -173,6 +173,8 @@ class Reference:
         L.ref_signature.restype = ctypes.c_ulonglong
         L.ref_gen_euler.argtypes = [c_int] * 3 + [c_double, ctypes.c_longlong] + [c_void_p] * 7
         L.ref_gen_coupled.argtypes = [c_int] * 3 + [c_double, ctypes.c_longlong] + [c_void_p] * 8
+        L.ref_gen_euler_poly.argtypes = [c_int] * 3 + [c_double, ctypes.c_longlong, ctypes.c_longlong] + [c_void_p] * 7
+        L.ref_gen_coupled_poly.argtypes = [c_int] * 3 + [c_double, ctypes.c_longlong, ctypes.c_longlong] + [c_void_p] * 8
         L.ref_amg_build.restype = c_void_p
         L.ref_amg_depth.argtypes = [c_void_p]
         L.ref_amg_level_sizes.argtypes = [c_void_p, c_int] + [ctypes.POINTER(c_int)] * 3
@@ -187,19 +189,27 @@ class Reference:
     def err(self):
         return self.L.ref_last_error().decode()
 
-    def gen_euler(self, nx, ny, nz, aspect=1.0, seed=-1):
-        nc, nf = nx * ny * nz, (nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1)
+    @staticmethod
+    def _faces(nx, ny, nz, poly):
+        nf = (nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1)
+        if poly >= 0:  # the augmented count (sizing only; contents are compared)
+            from paper_2403_07882_b200 import gen
+            nf = gen.hex_sizes(nx, ny, nz, poly)[1]
+        return nx * ny * nz, nf
+
+    def gen_euler(self, nx, ny, nz, aspect=1.0, seed=-1, poly=-1):
+        nc, nf = self._faces(nx, ny, nz, poly)
         a = [np.zeros(nf, np.int32), np.zeros(nf, np.int32), np.zeros(nc * 25), np.zeros(nf * 25),
              np.zeros(nf * 25), np.zeros(nc * 5), np.zeros(nc * 3)]
-        rc = self.L.ref_gen_euler(nx, ny, nz, aspect, seed, *[ptr(x) for x in a])
+        rc = self.L.ref_gen_euler_poly(nx, ny, nz, aspect, seed, poly, *[ptr(x) for x in a])
         assert rc == 0, self.err()
         return a
 
-    def gen_coupled(self, nx, ny, nz, aspect=1.0, seed=-1):
-        nc, nf = nx * ny * nz, (nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1)
+    def gen_coupled(self, nx, ny, nz, aspect=1.0, seed=-1, poly=-1):
+        nc, nf = self._faces(nx, ny, nz, poly)
         a = [np.zeros(nf, np.int32), np.zeros(nf, np.int32), np.zeros(nc * 16), np.zeros(nf * 16),
              np.zeros(nf * 16), np.zeros(nc * 4), np.zeros(nc * 4), np.zeros(nc * 3)]
-        rc = self.L.ref_gen_coupled(nx, ny, nz, aspect, seed, *[ptr(x) for x in a])
+        rc = self.L.ref_gen_coupled_poly(nx, ny, nz, aspect, seed, poly, *[ptr(x) for x in a])
         assert rc == 0, self.err()
         return a
 

@@ -25,6 +25,26 @@ def test_coupled_bit_exact(ref, dims, aspect, seed):
         assert x.tobytes() == y.tobytes()
 
 
+@pytest.mark.parametrize("maker,dims,aspect,seed,poly", [
+    ("euler", (6, 5, 4), 1.0, -1, 11), ("euler", (5, 6, 3), 1.0, 4, 2), ("coupled", (6, 6, 5), 1.0, -1, 11),
+    ("coupled", (5, 4, 6), 100.0, 9, 3)])
+def test_polyhedral_augmentation_bit_exact(ref, maker, dims, aspect, seed, poly):
+    """C5-style meshes: extra edge-diagonal faces on a seeded 30% of the cells
+    (mixed row degrees); generator == reference producer on the same mesh."""
+    if maker == "euler":
+        s = gen.hex_euler(*dims, aspect=aspect, scramble_seed=seed, poly_seed=poly)
+        o, ne, d, u, lo, b, cen = ref.gen_euler(*dims, aspect, seed, poly)
+        pairs = ((s.b.values, b),)
+    else:
+        s = gen.hex_coupled(*dims, aspect=aspect, scramble_seed=seed, poly_seed=poly)
+        o, ne, d, u, lo, b, x0, cen = ref.gen_coupled(*dims, aspect, seed, poly)
+        pairs = ((s.b.values, b), (s.x0.values, x0))
+    base = gen.hex_sizes(*dims)[1]
+    assert s.A.nFaces() > base  # augmented
+    for x, y in ((s.A.owner, o), (s.A.neighbour, ne), (s.A.diag, d), (s.A.upper, u), (s.A.lower, lo)) + pairs:
+        assert x.tobytes() == y.tobytes()
+
+
 def test_hex_sizes_and_ordering():
     nc, nf = gen.hex_sizes(4, 3, 2)
     assert nc == 24 and nf == 3 * 3 * 2 + 4 * 2 * 2 + 4 * 3 * 1
