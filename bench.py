@@ -274,7 +274,6 @@ def run_ours(args):
 
     for _ in range(max(args.warmup, 3)):
         rep = step()
-    ctx.set_kernel_timing(True)
     reps = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -287,6 +286,12 @@ def run_ours(args):
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
+    free_b, total_b = torch.cuda.mem_get_info(dev)  # device-wide: our pools + torch's input copies
+    # per-kernel CUDA-event timings (roofline) from extra, untimed steps: the
+    # events around every sweep / SpMV launch are not part of the measured step
+    ctx.set_kernel_timing(True)
+    preps = [step() for _ in range(max(1, min(args.steps, 2)))]
+    torch.cuda.synchronize()
     ctx.set_kernel_timing(False)
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -298,16 +303,16 @@ def run_ours(args):
     last = reps[-1]
 
     # SpMV roofline from the launches inside the timed region
-    spmv_ms = sum(r.spmvMs for r in reps) / max(1, sum(r.spmvLaunches for r in reps))
+    spmv_ms = sum(r.spmvMs for r in preps) / max(1, sum(r.spmvLaunches for r in preps))
     bytes_per = spmv_bytes(nc, nf, nb)
     peak, peak_kind = peaks()
     achieved = bytes_per / (spmv_ms * 1e-3) / 1e9
     # the dominant kernel: the smoother sweeps (every level), algorithmic
     # bytes per launch / mean event-timed launch duration
-    sw_n = sum(r.sweepLaunches for r in reps)
-    sw_ms = sum(r.sweepMs for r in reps)
-    sw_bytes = sum(r.sweepBytes for r in reps)
-    sw_share = sw_ms / (ms * args.steps) if ms > 0 else None
+    sw_n = sum(r.sweepLaunches for r in preps)
+    sw_ms = sum(r.sweepMs for r in preps)
+    sw_bytes = sum(r.sweepBytes for r in preps)
+    sw_share = sw_ms / (ms * len(preps)) if ms > 0 else None
     sw_achieved = (sw_bytes / sw_n) / ((sw_ms / sw_n) * 1e-3) / 1e9 if sw_n else None
     # the sweeps' own bound: dependency hops x the kernel's measured 1-D chain hop
     latency = None
@@ -317,13 +322,13 @@ def run_ours(args):
         # most TAIL_ROWS rows, one-CTA kernel) and the dense coarsest are not
         swept = [l for l in range(max(0, nlev - 1)) if ctx.amg_level_rows(l) > TAIL_ROWS]
         depth_sum = sum(ctx.schedule_depth(l) for l in swept)
-        vcycles = sw_n / args.steps / (4 * max(1, len(swept)))
+        vcycles = sw_n / len(preps) / (4 * max(1, len(swept)))
         hops = vcycles * 4 * depth_sum
         hop = chain_hop_ns(bcs)
         floor_ms = hops * hop * 1e-6
         latency = {"hops_per_step": hops, "chain_hop_ns": hop, "floor_ms_per_step": floor_ms,
-                   "measured_ms_per_step": sw_ms / args.steps,
-                   "frac": floor_ms / (sw_ms / args.steps) if sw_ms else None,
+                   "measured_ms_per_step": sw_ms / len(preps),
+                   "frac": floor_ms / (sw_ms / len(preps)) if sw_ms else None,
                    "note": "sum over the swept levels of 4 sweeps x dependency depth x V-cycles, times the fastest sweep variant's "
                            "own hop on a 1-D 5x5 chain (DILU apply, 2L hops)"}
     except Exception as e:  # diagnostic only
@@ -388,11 +393,14 @@ def run_ours(args):
             "true_rel_residual_check": true_res / last.initialResidual,
             "stage_s": {"amg_setup": last.timings.get("amgSetup"), "krylov": last.timings.get("krylov")},
             "gpu_launches": launches,
+            "device_memory_gb": {"used": round((total_b - free_b) / 1e9, 2), "total": round(total_b / 1e9, 2),
+                                 "note": "cudaMemGetInfo after the timed steps: solver pools (hierarchy, sweep programs, "
+                                         "DILU scratch, Krylov basis) + the bench's device-resident LDU inputs"},
             "roofline": {"bound": "hbm", "achieved": sw_achieved, "peak": peak, "unit": "GB/s",
                          "frac": (sw_achieved / peak) if sw_achieved else None, "traffic": sweep_traffic(n) if default_workload(args) else None,
                          "kernel": f"k_sweep*<{nb},*> (DILU smoother sweeps, all swept AMG levels)",
                          "bytes_per_launch": (sw_bytes / sw_n) if sw_n else None,
-                         "mean_launch_ms": (sw_ms / sw_n) if sw_n else None, "launches_per_step": sw_n / args.steps,
+                         "mean_launch_ms": (sw_ms / sw_n) if sw_n else None, "launches_per_step": sw_n / len(preps),
                          "share_of_step": sw_share, "peak_kind": peak_kind,
                          "note": "dependency-latency bound (level depth x hop latency), see DESIGN.md", "latency": latency},
             "roofline_spmv": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
