@@ -62,7 +62,9 @@ def hex_euler(nx: int, ny: int = None, nz: int = None, aspect: float = 1.0, scra
     if rc:
         raise ValueError("bcsgen_hex_euler: bad arguments")
     A = BlockLduMatrix(nc, owner, neigh, 5, diag, upper, lower)
-    return System(A, BlockVector(nc, 5, rhs), BlockVector(nc, 5), cen.reshape(nc, 3),
+    x0 = (alloc or (lambda size, dt: np.zeros(size, dt)))(nc * 5, np.float64)
+    x0[:] = 0.0
+    return System(A, BlockVector(nc, 5, rhs), BlockVector(nc, 5, x0), cen.reshape(nc, 3),
                   f"euler5 {nx}x{ny}x{nz} {_tag(scramble_seed, poly_seed)} AR{aspect:g}")
 
 
@@ -71,7 +73,7 @@ def hex_coupled(nx: int, ny: int = None, nz: int = None, aspect: float = 1.0, sc
     ny = nx if ny is None else ny
     nz = nx if nz is None else nz
     nc, nf, owner, neigh, diag, upper, lower, rhs, cen = _alloc(nx, ny, nz, 4, alloc, poly_seed)
-    x0 = np.zeros(nc * 4)
+    x0 = (alloc or (lambda size, dt: np.zeros(size, dt)))(nc * 4, np.float64)
     rc = N.gen().bcsgen_hex_coupled_poly(nx, ny, nz, float(aspect), int(scramble_seed), int(poly_seed), N.ptr(owner),
                                          N.ptr(neigh), N.ptr(diag), N.ptr(upper), N.ptr(lower), N.ptr(rhs), N.ptr(x0),
                                          N.ptr(cen))
