@@ -196,6 +196,20 @@ bcs_status bcs_upload_ldu(bcs_ctx* ctx, const double* diag, const double* upper,
 bcs_status bcs_upload_ldu_device(bcs_ctx* ctx, const double* d_diag, const double* d_upper,
                                  const double* d_lower);
 /* Preconditioner build + Krylov on the current matrix; x holds x0 on entry. */
+/* Device assembly of the 5x5 density-based system:
+ * replaces assembleJacobian + computeResidual (euler.cpp:361-455) for
+ * first-order reconstruction, the Roe flux and farfield patches (ghost state
+ * = freestream).  Mesh: owner/neighbour per internal face (sets the topology
+ * when it differs), face_area 3 per internal face (owner -> neighbour), the
+ * boundary faces in patch order (cell, outward area vector), q the primitive
+ * state (rho, u, v, w, p) per cell, q_inf the freestream, cfl the pseudo-time
+ * CFL (<= 0: none).  The matrix goes straight into the context's block-CSR
+ * (as bcs_upload_ldu would put it, bit-identical); rhs (host, 5 per cell)
+ * receives the permuted residual. */
+bcs_status bcs_assemble_euler(bcs_ctx* ctx, int n_cells, int n_faces, const int32_t* owner, const int32_t* neighbour,
+                              const double* face_area, int n_bfaces, const int32_t* bface_cell,
+                              const double* bface_area, const double* q, const double* q_inf, double cfl,
+                              double* rhs);
 bcs_status bcs_solve(bcs_ctx* ctx, const double* b, double* x, const bcs_solver_config* cfg, bcs_report* report);
 bcs_status bcs_solve_device(bcs_ctx* ctx, const double* d_b, double* d_x, const bcs_solver_config* cfg,
                             bcs_report* report);

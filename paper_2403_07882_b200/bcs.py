@@ -200,6 +200,23 @@ class Context:
     def upload_ldu_device(self, d_diag: int, d_upper: int, d_lower: int):
         self._ck(self._lib.bcs_upload_ldu_device(self.h, c_ptr(d_diag), c_ptr(d_upper), c_ptr(d_lower)))
 
+    def assemble_euler(self, owner, neighbour, face_area, bface_cell, bface_area, q, q_inf, cfl: float) -> np.ndarray:
+        """Device assembleJacobian + computeResidual (first order, Roe, farfield):
+        the matrix goes into this context; returns the right-hand side."""
+        owner = np.ascontiguousarray(owner, np.int32)
+        neighbour = np.ascontiguousarray(neighbour, np.int32)
+        face_area = np.ascontiguousarray(face_area, np.float64)
+        bface_cell = np.ascontiguousarray(bface_cell, np.int32)
+        bface_area = np.ascontiguousarray(bface_area, np.float64)
+        q = np.ascontiguousarray(q, np.float64)
+        q_inf = np.ascontiguousarray(q_inf, np.float64)
+        nc = q.size // 5
+        rhs = np.zeros(nc * 5)
+        self._ck(self._lib.bcs_assemble_euler(self.h, nc, owner.size, N.ptr(owner), N.ptr(neighbour), N.ptr(face_area),
+                                              bface_cell.size, N.ptr(bface_cell), N.ptr(bface_area), N.ptr(q),
+                                              N.ptr(q_inf), float(cfl), N.ptr(rhs)))
+        return rhs
+
     def solve(self, b: np.ndarray, x: np.ndarray, cfg: SolverConfig) -> SolveReport:
         rep = N.ReportC()
         c = cfg.to_c()

@@ -112,6 +112,10 @@ public:
     // topology / values
     void setTopology(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh);
     void uploadLdu(const double* diag, const double* upper, const double* lower, bool device_ptrs);
+    // device assembly of the 5x5 density-based system (k_assemble.cu); rhs: host, 5 per cell
+    void assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* neigh, const double* faceArea, int nb,
+                       const int32_t* bcell, const double* barea, const double* q, const double* qinf, double cfl,
+                       double* rhs);
 
     // drop-in pipeline (engine.cpp:47-120)
     void pipelineSolve(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh, const double* diag,
@@ -201,6 +205,10 @@ private:
     DArray<int> dOwner_, dNeigh_, ro_, ci_, dg_, tpos_, src_, fill_;
     DArray<double> vals_;
     DArray<double> ldu_diag_, ldu_upper_, ldu_lower_;
+    // device assembly: slot of every LDU block, cell -> faces (face order), cell -> boundary faces
+    bool asmTopo_ = false;
+    DArray<int> asmInv_, asmCfo_, asmCf_, asmBco_;
+    DArray<double> asmArea_, asmBarea_, asmQ_, asmRhs_;
     // SolvePipeline state (engine.hpp:35-37): only the EngineCsr branch updates it
     bool pipeHasSetup_ = false;
     uint64_t pipeSig_ = 0;

@@ -24,18 +24,11 @@
 #include <random>
 #include <vector>
 
+#include "../euler_jac.cuh"
+
 namespace {
 
-struct V3 {
-    double x, y, z;
-};
-inline V3 add(V3 a, V3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
-inline V3 sub(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
-inline V3 scl(V3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
-inline V3 dvd(V3 a, double s) { return {a.x / s, a.y / s, a.z / s}; }
-inline double dot3(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
-inline double len3(V3 a) { return std::sqrt(dot3(a, a)); }
-inline double comp(V3 a, int i) { return i == 0 ? a.x : (i == 1 ? a.y : a.z); }
+using namespace bcs_euler;
 
 struct BFace {
     int cell;
@@ -113,121 +106,14 @@ Hex buildHex(int nx, int ny, int nz, double aspect, long long scrambleSeed, long
     return h;
 }
 
-// ---------------------------------------------------------------- Euler 5x5
-constexpr double kGamma = 1.4;
-// natural component [rho, m, E] -> block slot in the vector-first layout
-constexpr int kSlot[5] = {3, 0, 1, 2, 4};
-
-struct Prim {
-    double v[5];  // rho, ux, uy, uz, p
-};
-inline V3 vel(const Prim& q) { return {q.v[1], q.v[2], q.v[3]}; }
-
-struct RoeAvg {
-    double rho;
-    V3 u;
-    double H, c;
-};
-
-RoeAvg roeAvg(const Prim& L, const Prim& R) {
-    const double sL = std::sqrt(L.v[0]), sR = std::sqrt(R.v[0]);
-    const double w = 1.0 / (sL + sR);
-    RoeAvg a;
-    a.rho = sL * sR;
-    a.u = scl(add(scl(vel(L), sL), scl(vel(R), sR)), w);
-    const double HL = kGamma / (kGamma - 1.0) * L.v[4] / L.v[0] + 0.5 * dot3(vel(L), vel(L));
-    const double HR = kGamma / (kGamma - 1.0) * R.v[4] / R.v[0] + 0.5 * dot3(vel(R), vel(R));
-    a.H = (sL * HL + sR * HR) * w;
-    a.c = std::sqrt((kGamma - 1.0) * (a.H - 0.5 * dot3(a.u, a.u)));
-    return a;
-}
-
-void physFlux(const Prim& q, V3 n, double* f) {
-    const V3 u = vel(q);
-    const double un = dot3(u, n);
-    const double rhoE = q.v[4] / (kGamma - 1.0) + 0.5 * q.v[0] * dot3(u, u);
-    f[0] = q.v[0] * un;
-    f[1] = q.v[0] * u.x * un + q.v[4] * n.x;
-    f[2] = q.v[0] * u.y * un + q.v[4] * n.y;
-    f[3] = q.v[0] * u.z * un + q.v[4] * n.z;
-    f[4] = (rhoE + q.v[4]) * un;
-}
-
-// convective Jacobian d(F.n)/dQ in [rho, m, E] order
-void convJac(const Prim& q, V3 n, double* J) {
-    const V3 u = vel(q);
-    const double un = dot3(u, n);
-    const double g1 = kGamma - 1.0;
-    const double ek = 0.5 * dot3(u, u);
-    const double c = std::sqrt(kGamma * q.v[4] / q.v[0]);
-    const double H = c * c / g1 + ek;
-    const double nv[3] = {n.x, n.y, n.z};
-    const double uv[3] = {u.x, u.y, u.z};
-    J[0] = 0.0;
-    J[1] = nv[0];
-    J[2] = nv[1];
-    J[3] = nv[2];
-    J[4] = 0.0;
-    for (int i = 0; i < 3; ++i) {
-        double* row = J + 5 * (i + 1);
-        row[0] = g1 * ek * nv[i] - uv[i] * un;
-        for (int j = 0; j < 3; ++j) row[1 + j] = uv[i] * nv[j] - g1 * uv[j] * nv[i] + (i == j ? un : 0.0);
-        row[4] = g1 * nv[i];
-    }
-    double* e = J + 20;
-    e[0] = (g1 * ek - H) * un;
-    for (int j = 0; j < 3; ++j) e[1 + j] = H * nv[j] - g1 * uv[j] * un;
-    e[4] = kGamma * un;
-}
-
-void roe(const Prim& L, const Prim& R, V3 n, double* flux) {
-    double fL[5], fR[5];
-    physFlux(L, n, fL);
-    physFlux(R, n, fR);
-    const RoeAvg a = roeAvg(L, R);
-    const double un = dot3(a.u, n);
-    const double c = a.c;
-    const double dRho = R.v[0] - L.v[0];
-    const V3 dU = sub(vel(R), vel(L));
-    const double dUn = dot3(dU, n);
-    const double dP = R.v[4] - L.v[4];
-    const double a1 = (dP - a.rho * c * dUn) / (2.0 * c * c);
-    const double a5 = (dP + a.rho * c * dUn) / (2.0 * c * c);
-    const double a2 = dRho - dP / (c * c);
-    const double delta = 0.1 * (std::fabs(un) + c);
-    auto entropyFix = [delta](double lam) {
-        const double m = std::fabs(lam);
-        return m < delta ? (lam * lam + delta * delta) / (2.0 * delta) : m;
-    };
-    const double l1 = entropyFix(un - c);
-    const double l2 = std::fabs(un);
-    const double l5 = entropyFix(un + c);
-    double diss[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    auto wave = [&](double strength, double lam, double k0, V3 kU, double kE) {
-        const double w = strength * lam;
-        diss[0] += w * k0;
-        diss[1] += w * kU.x;
-        diss[2] += w * kU.y;
-        diss[3] += w * kU.z;
-        diss[4] += w * kE;
-    };
-    wave(a1, l1, 1.0, sub(a.u, scl(n, c)), a.H - c * un);
-    wave(a2, l2, 1.0, a.u, 0.5 * dot3(a.u, a.u));
-    wave(a5, l5, 1.0, add(a.u, scl(n, c)), a.H + c * un);
-    const V3 dUt = sub(dU, scl(n, dUn));
-    wave(a.rho, l2, 0.0, dUt, dot3(a.u, dU) - un * dUn);
-    for (int i = 0; i < 5; ++i) flux[i] = 0.5 * (fL[i] + fR[i]) - 0.5 * diss[i];
-}
-
 // dst(block order) += scale * J + lamScale * I
 void accumulate(double* dst, double scale, const double* J, double lamScale) {
     for (int r = 0; r < 5; ++r)
         for (int c = 0; c < 5; ++c) dst[kSlot[r] * 5 + kSlot[c]] += scale * J[r * 5 + c] + (r == c ? lamScale : 0.0);
 }
 
-void euler(const Hex& h, double* diag, double* upper, double* lower, double* rhs) {
-    const int nc = h.nc;
-    const int nf = static_cast<int>(h.owner.size());
+// the seeded primitive state of the 5x5 workload
+std::vector<Prim> eulerState(int nc) {
     std::mt19937 gen(2);
     std::uniform_real_distribution<double> U(-0.05, 0.05);
     std::vector<Prim> q(nc);
@@ -238,6 +124,13 @@ void euler(const Hex& h, double* diag, double* upper, double* lower, double* rhs
         const double d4 = U(gen);
         q[c] = {{1.0 * (1.0 + d0), 0.5 + d1, 0.1 + d2, 0.0, (1.0 / 1.4) * (1.0 + d4)}};
     }
+    return q;
+}
+
+void euler(const Hex& h, double* diag, double* upper, double* lower, double* rhs) {
+    const int nc = h.nc;
+    const int nf = static_cast<int>(h.owner.size());
+    const std::vector<Prim> q = eulerState(nc);
     const Prim farfield{{1.0, 0.5, 0.1, 0.0, 1.0 / 1.4}};
     std::memset(diag, 0, sizeof(double) * 25 * nc);
     std::memset(upper, 0, sizeof(double) * 25 * nf);
@@ -537,6 +430,34 @@ int bcsgen_hex_coupled_poly(int nx, int ny, int nz, double aspect, long long scr
     const Hex h = buildHex(nx, ny, nz, aspect, scrambleSeed, polySeed);
     exportTopo(h, owner, neigh, centroids);
     coupled(h, diag, upper, lower, rhs, x0);
+    return 0;
+}
+
+// inputs of the 5x5 assembly on the same mesh: face area vectors (3 per
+// internal face), boundary faces in patch order (cell, area vector; all
+// farfield), the seeded primitive state q (5 per cell: rho, u, v, w, p)
+void bcsgen_hex_boundary_count(int nx, int ny, int nz, int* nb) { *nb = 2 * (ny * nz + nx * nz + nx * ny); }
+int bcsgen_hex_euler_inputs(int nx, int ny, int nz, double aspect, long long scrambleSeed, long long polySeed,
+                            double* faceArea, int* bcell, double* barea, double* q) {
+    if (nx < 1 || ny < 1 || nz < 1 || !(aspect > 0.0)) return 1;
+    const Hex h = buildHex(nx, ny, nz, aspect, scrambleSeed, polySeed);
+    for (std::size_t f = 0; f < h.area.size(); ++f) {
+        faceArea[3 * f] = h.area[f].x;
+        faceArea[3 * f + 1] = h.area[f].y;
+        faceArea[3 * f + 2] = h.area[f].z;
+    }
+    std::size_t b = 0;
+    for (const auto& patch : h.patches)
+        for (const BFace& bf : patch) {
+            bcell[b] = bf.cell;
+            barea[3 * b] = bf.area.x;
+            barea[3 * b + 1] = bf.area.y;
+            barea[3 * b + 2] = bf.area.z;
+            ++b;
+        }
+    const std::vector<Prim> st = eulerState(h.nc);
+    for (int c = 0; c < h.nc; ++c)
+        for (int k = 0; k < 5; ++k) q[5 * static_cast<std::size_t>(c) + k] = st[c].v[k];
     return 0;
 }
 

@@ -1,0 +1,176 @@
+// Device-side assembly of the 5x5 density-based system:
+// assembleJacobian (euler.cpp:390-455: first-order approximate Jacobian,
+// Roe-averaged spectral radius, pseudo-time diagonal) and its right-hand side,
+// the steady residual (computeResidual, euler.cpp:361-389, Roe flux :103-150)
+// for first-order reconstruction and farfield boundary patches, written
+// straight into the engine's block-CSR slots.  A caller then uploads the
+// primitive state (5 doubles per cell) instead of the LDU values (50 doubles
+// per face + 25 per cell).
+//
+// Same arithmetic as the reference: the face kernel writes the two
+// off-diagonal blocks of a face (each is one contribution onto 0.0); the cell
+// kernel accumulates a cell's diagonal block, spectral-radius sum and residual
+// over its faces in face-index order, then its boundary faces in patch order,
+// then V/dtau -- the order of the reference's loops.  The flux, Jacobian and
+// Roe-average routines are the ones the host generator uses (euler_jac.cuh),
+// compiled without FMA contraction, so the values are bit-identical.
+#include "device.cuh"
+#include "euler_jac.cuh"
+#include "kernels.hpp"
+
+namespace bcs {
+
+namespace {
+
+using bcs_euler::Prim;
+using bcs_euler::RoeAvg;
+using bcs_euler::V3;
+
+// natural component [rho, m, E] -> block slot in the vector-first layout (euler.cpp:15)
+__device__ __forceinline__ int kslot(int r) { return r == 0 ? 3 : (r == 4 ? 4 : r - 1); }
+
+__device__ __forceinline__ Prim load_prim(const double* q, int c) {
+    const double* p = q + 5 * static_cast<size_t>(c);
+    return Prim{{p[0], p[1], p[2], p[3], p[4]}};
+}
+__device__ __forceinline__ V3 load_v3(const double* a, int i) {
+    const double* p = a + 3 * static_cast<size_t>(i);
+    return V3{p[0], p[1], p[2]};
+}
+
+__global__ void k_inverse_src(int nnzb, const int* __restrict__ src, int* inv) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < nnzb) inv[src[k]] = k;
+}
+
+// off-diagonal blocks of face f: lower (neighbour row, owner column) =
+// -0.5 S J(q_o) - 0.5 S lam I, upper (owner row, neighbour column) =
+// 0.5 S J(q_n) - 0.5 S lam I (euler.cpp:418-423)
+__global__ void k_asm_faces(int nc, int nf, const int* __restrict__ owner, const int* __restrict__ neigh,
+                            const double* __restrict__ area, const double* __restrict__ q,
+                            const int* __restrict__ inv, double* vals) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= nf) return;
+    const int o = owner[f], nb = neigh[f];
+    const V3 A = load_v3(area, f);
+    const double S = bcs_euler::len3(A);
+    const V3 n = bcs_euler::dvd(A, S);
+    const Prim qo = load_prim(q, o), qn = load_prim(q, nb);
+    const RoeAvg a = bcs_euler::roeAvg(qo, qn);
+    const double lam = fabs(bcs_euler::dot3(a.u, n)) + a.c;
+    double J[25];
+    {
+        bcs_euler::convJac(qo, n, J);
+        const double scale = -0.5 * S, lamScale = -0.5 * S * lam;
+        double* lo = vals + 25 * static_cast<size_t>(inv[nc + nf + f]);
+#pragma unroll
+        for (int r = 0; r < 5; ++r)
+#pragma unroll
+            for (int c = 0; c < 5; ++c)
+                lo[kslot(r) * 5 + kslot(c)] = __dadd_rn(0.0, __dadd_rn(__dmul_rn(scale, J[r * 5 + c]), r == c ? lamScale : 0.0));
+    }
+    {
+        bcs_euler::convJac(qn, n, J);
+        const double scale = 0.5 * S, lamScale = -0.5 * S * lam;
+        double* up = vals + 25 * static_cast<size_t>(inv[nc + f]);
+#pragma unroll
+        for (int r = 0; r < 5; ++r)
+#pragma unroll
+            for (int c = 0; c < 5; ++c)
+                up[kslot(r) * 5 + kslot(c)] = __dadd_rn(0.0, __dadd_rn(__dmul_rn(scale, J[r * 5 + c]), r == c ? lamScale : 0.0));
+    }
+}
+
+// diagonal block, spectral-radius sum and residual of cell c
+__global__ void __launch_bounds__(128) k_asm_cells(int nc, int nf, const int* __restrict__ owner,
+                                                   const int* __restrict__ neigh, const double* __restrict__ area,
+                                                   const int* __restrict__ cfo, const int* __restrict__ cfl,
+                                                   const int* __restrict__ bco, const double* __restrict__ barea,
+                                                   const double* __restrict__ q, const double* __restrict__ qinf,
+                                                   double cfl_num, const int* __restrict__ inv, double* vals,
+                                                   double* rhs) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    const Prim qc = load_prim(q, c);
+    const Prim far = load_prim(qinf, 0);
+    double D[25], res[5], J[25], fl[5];
+#pragma unroll
+    for (int e = 0; e < 25; ++e) D[e] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) res[k] = 0.0;
+    double lamSum = 0.0;
+    for (int e = cfo[c]; e < cfo[c + 1]; ++e) {
+        const int f = cfl[e];
+        const int o = owner[f], nb = neigh[f];
+        const bool own = o == c;
+        const V3 A = load_v3(area, f);
+        const double S = bcs_euler::len3(A);
+        const V3 n = bcs_euler::dvd(A, S);
+        const Prim qo = own ? qc : load_prim(q, o);
+        const Prim qn = own ? load_prim(q, nb) : qc;
+        const RoeAvg a = bcs_euler::roeAvg(qo, qn);
+        const double lam = fabs(bcs_euler::dot3(a.u, n)) + a.c;
+        // owner side: += 0.5 S J(q_o) + 0.5 S lam I; neighbour side: += -0.5 S J(q_n) + 0.5 S lam I
+        bcs_euler::convJac(own ? qo : qn, n, J);
+        const double scale = own ? 0.5 * S : -0.5 * S, lamScale = 0.5 * S * lam;
+#pragma unroll
+        for (int r = 0; r < 5; ++r)
+#pragma unroll
+            for (int cc = 0; cc < 5; ++cc)
+                D[r * 5 + cc] = __dadd_rn(D[r * 5 + cc], __dadd_rn(__dmul_rn(scale, J[r * 5 + cc]), r == cc ? lamScale : 0.0));
+        lamSum = __dadd_rn(lamSum, __dmul_rn(lam, S));
+        bcs_euler::roe(qo, qn, n, fl);
+#pragma unroll
+        for (int k = 0; k < 5; ++k) res[k] = own ? __dsub_rn(res[k], __dmul_rn(S, fl[k])) : __dadd_rn(res[k], __dmul_rn(S, fl[k]));
+    }
+    // farfield boundary faces: ghost state frozen, only the interior half enters (euler.cpp:426-441)
+    for (int b = bco[c]; b < bco[c + 1]; ++b) {
+        const V3 A = load_v3(barea, b);
+        const double S = bcs_euler::len3(A);
+        const V3 n = bcs_euler::dvd(A, S);
+        const RoeAvg a = bcs_euler::roeAvg(qc, far);
+        const double lam = fabs(bcs_euler::dot3(a.u, n)) + a.c;
+        bcs_euler::convJac(qc, n, J);
+        const double scale = 0.5 * S, lamScale = 0.5 * S * lam;
+#pragma unroll
+        for (int r = 0; r < 5; ++r)
+#pragma unroll
+            for (int cc = 0; cc < 5; ++cc)
+                D[r * 5 + cc] = __dadd_rn(D[r * 5 + cc], __dadd_rn(__dmul_rn(scale, J[r * 5 + cc]), r == cc ? lamScale : 0.0));
+        lamSum = __dadd_rn(lamSum, __dmul_rn(lam, S));
+        bcs_euler::roe(qc, far, n, fl);
+#pragma unroll
+        for (int k = 0; k < 5; ++k) res[k] = __dsub_rn(res[k], __dmul_rn(S, fl[k]));
+    }
+    if (cfl_num > 0.0) {
+        const double vOverDtau = __ddiv_rn(lamSum, cfl_num);  // V/dtau with dtau = cfl V / sum (euler.cpp:444-448)
+#pragma unroll
+        for (int r = 0; r < 5; ++r) D[r * 5 + r] = __dadd_rn(D[r * 5 + r], vOverDtau);
+    }
+    double* dst = vals + 25 * static_cast<size_t>(inv[c]);
+#pragma unroll
+    for (int r = 0; r < 5; ++r)
+#pragma unroll
+        for (int cc = 0; cc < 5; ++cc) dst[kslot(r) * 5 + kslot(cc)] = D[r * 5 + cc];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) rhs[5 * static_cast<size_t>(c) + kslot(k)] = res[k];
+}
+
+}  // namespace
+
+void assemble_inverse_src(int nnzb, const int* src, int* inv, cudaStream_t s) {
+    if (nnzb <= 0) return;
+    k_inverse_src<<<(nnzb + 255) / 256, 256, 0, s>>>(nnzb, src, inv);
+    count_launch();
+}
+
+void assemble_euler(int nc, int nf, const int* owner, const int* neigh, const double* area, const int* cfo,
+                    const int* cfl, const int* bco, const double* barea, const double* q, const double* qinf,
+                    double cfl_num, const int* inv, double* vals, double* rhs, cudaStream_t s) {
+    if (nf > 0) k_asm_faces<<<(nf + 255) / 256, 256, 0, s>>>(nc, nf, owner, neigh, area, q, inv, vals);
+    k_asm_cells<<<(nc + 127) / 128, 128, 0, s>>>(nc, nf, owner, neigh, area, cfo, cfl, bco, barea, q, qinf, cfl_num,
+                                                 inv, vals, rhs);
+    count_launch(nf > 0 ? 2 : 1);
+}
+
+}  // namespace bcs

@@ -116,6 +116,12 @@ unsigned long long selftest_pingpong(int mode, int n);
 void set_sweep_trace(unsigned long long* d, long long filter);  // filter: 0 any, else rows*2+fwd
 unsigned long long selftest_chain(int variant, int L, int warps);  // total ns  // diagnostics: per-ticket timing trace
 
+// ------------------------------------------------- device assembly (§8(f))
+void assemble_inverse_src(int nnzb, const int* src, int* inv, cudaStream_t s);
+void assemble_euler(int nc, int nf, const int* owner, const int* neigh, const double* area, const int* cfo,
+                    const int* cfl, const int* bco, const double* barea, const double* q, const double* qinf,
+                    double cfl_num, const int* inv, double* vals, double* rhs, cudaStream_t s);
+
 // ------------------------------------------------------------ AMG (K9-K12)
 void strengths(int n, int rows, const int* ro, const int* ci, const int* dg, const double* v, double* dn,
                double* str, int nnz, cudaStream_t s);

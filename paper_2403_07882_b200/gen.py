@@ -82,3 +82,25 @@ def hex_coupled(nx: int, ny: int = None, nz: int = None, aspect: float = 1.0, sc
     A = BlockLduMatrix(nc, owner, neigh, 4, diag, upper, lower)
     return System(A, BlockVector(nc, 4, rhs), BlockVector(nc, 4, x0), cen.reshape(nc, 3),
                   f"coupled4 {nx}x{ny}x{nz} {_tag(scramble_seed, poly_seed)} AR{aspect:g}")
+
+
+def hex_euler_inputs(nx: int, ny: int = None, nz: int = None, aspect: float = 1.0, scramble_seed: int = -1,
+                     poly_seed: int = -1):
+    """Inputs of the 5x5 assembly on the hex mesh of ``hex_euler`` (same
+    arguments): face area vectors, boundary faces (cell, area) in patch order,
+    the seeded primitive state q and the freestream -- for the device assembly."""
+    ny = nx if ny is None else ny
+    nz = nx if nz is None else nz
+    nc, nf = hex_sizes(nx, ny, nz, poly_seed)
+    nb = ctypes.c_int()
+    N.gen().bcsgen_hex_boundary_count(nx, ny, nz, ctypes.byref(nb))
+    area = np.zeros(3 * nf)
+    bcell = np.zeros(nb.value, np.int32)
+    barea = np.zeros(3 * nb.value)
+    q = np.zeros(5 * nc)
+    rc = N.gen().bcsgen_hex_euler_inputs(nx, ny, nz, float(aspect), int(scramble_seed), int(poly_seed), N.ptr(area),
+                                         N.ptr(bcell), N.ptr(barea), N.ptr(q))
+    if rc:
+        raise ValueError("bcsgen_hex_euler_inputs: bad arguments")
+    q_inf = np.array([1.0, 0.5, 0.1, 0.0, 1.0 / 1.4])
+    return area, bcell, barea, q, q_inf
