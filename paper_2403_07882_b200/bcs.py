@@ -200,7 +200,8 @@ class Context:
     def upload_ldu_device(self, d_diag: int, d_upper: int, d_lower: int):
         self._ck(self._lib.bcs_upload_ldu_device(self.h, c_ptr(d_diag), c_ptr(d_upper), c_ptr(d_lower)))
 
-    def assemble_euler(self, owner, neighbour, face_area, bface_cell, bface_area, q, q_inf, cfl: float) -> np.ndarray:
+    def assemble_euler(self, owner, neighbour, face_area, bface_cell, bface_area, q, q_inf, cfl: float,
+                       out: Optional[np.ndarray] = None) -> np.ndarray:
         """Device assembleJacobian + computeResidual (first order, Roe, farfield):
         the matrix goes into this context; returns the right-hand side."""
         owner = np.ascontiguousarray(owner, np.int32)
@@ -211,7 +212,7 @@ class Context:
         q = np.ascontiguousarray(q, np.float64)
         q_inf = np.ascontiguousarray(q_inf, np.float64)
         nc = q.size // 5
-        rhs = np.zeros(nc * 5)
+        rhs = np.zeros(nc * 5) if out is None else out
         self._ck(self._lib.bcs_assemble_euler(self.h, nc, owner.size, N.ptr(owner), N.ptr(neighbour), N.ptr(face_area),
                                               bface_cell.size, N.ptr(bface_cell), N.ptr(bface_area), N.ptr(q),
                                               N.ptr(q_inf), float(cfl), N.ptr(rhs)))
