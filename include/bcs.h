@@ -117,6 +117,24 @@ bcs_status bcs_set_kernel_timing(bcs_ctx* ctx, int enable);
 bcs_status bcs_host_alloc(size_t bytes, void** out);
 void bcs_host_free(void* p);
 
+/* Binary LDU dump (the reference only has a text mesh
+ * format, mesh.cpp:214-283): one file per system, host only.
+ *   header 64 bytes: "BCSLDU01", int32 version (1), n_cells, n_faces,
+ *   block_size, flags (bit 0: b present, bit 1: x0 present), uint64 FNV-1a of
+ *   the payload, zero padding;
+ *   payload, little endian: owner[n_faces], neighbour[n_faces] (int32),
+ *   diag[n_cells n^2], upper[n_faces n^2], lower[n_faces n^2] (float64,
+ *   row-major blocks), then b[n_cells n] and x0[n_cells n] when flagged.
+ * b / x0 may be NULL on save (not stored) and on load (skipped).  A file that
+ * is truncated, has another magic or fails the checksum -> BCS_RUNTIME_ERROR. */
+bcs_status bcs_ldu_save(const char* path, int n_cells, int n_faces, int block_size, const int32_t* owner,
+                        const int32_t* neighbour, const double* diag, const double* upper, const double* lower,
+                        const double* b, const double* x0);
+bcs_status bcs_ldu_load_sizes(const char* path, int* n_cells, int* n_faces, int* block_size, int* has_b,
+                              int* has_x0);
+bcs_status bcs_ldu_load(const char* path, int32_t* owner, int32_t* neighbour, double* diag, double* upper,
+                        double* lower, double* b, double* x0);
+
 /* topologySignature (block_csr.cpp:146-160), exact; host only. */
 uint64_t bcs_topology_signature(int n_cells, int n_faces, const int32_t* owner, const int32_t* neighbour);
 

@@ -88,6 +88,9 @@ SIGNATURES = {
     "bcs_set_kernel_timing": (c_int, [c_void_p, c_int]),
     "bcs_host_alloc": (c_int, [c_size_t, P(c_void_p)]),
     "bcs_host_free": (None, [c_void_p]),
+    "bcs_ldu_save": (c_int, [ctypes.c_char_p, c_int, c_int, c_int] + [c_void_p] * 7),
+    "bcs_ldu_load_sizes": (c_int, [ctypes.c_char_p] + [P(c_int)] * 5),
+    "bcs_ldu_load": (c_int, [ctypes.c_char_p] + [c_void_p] * 7),
     "bcs_topology_signature": (c_uint64, [c_int, c_int, c_void_p, c_void_p]),
     "bcs_pipeline_solve": (
         c_int,

@@ -458,3 +458,34 @@ def backend_solve(A: BlockLduMatrix, b: BlockVector, x0: BlockVector, backend: B
         return p.solve(A, b, x0, backend, cfg)
     finally:
         p.ctx.close()
+
+
+def _ck_global(st: int):
+    if st != 0:
+        _raise(st, N.lib().bcs_last_error(None).decode())
+
+
+def save_ldu(path: str, A: BlockLduMatrix, b: Optional[BlockVector] = None, x0: Optional[BlockVector] = None):
+    """Binary LDU dump (bcs_ldu_save): topology, blocks and optionally b / x0."""
+    n = A.n
+    _ck_global(N.lib().bcs_ldu_save(
+        str(path).encode(), A.n_cells, A.nFaces(), n, N.ptr(A.owner), N.ptr(A.neighbour), N.ptr(A.diag),
+        N.ptr(A.upper), N.ptr(A.lower), N.ptr(b.values) if b is not None else None,
+        N.ptr(x0.values) if x0 is not None else None))
+
+
+def load_ldu(path: str) -> Tuple[BlockLduMatrix, Optional[BlockVector], Optional[BlockVector]]:
+    """Read a bcs_ldu_save file; raises RuntimeError on a bad magic, truncation or checksum mismatch."""
+    nc, nf, n, hb, hx = (ctypes.c_int() for _ in range(5))
+    L = N.lib()
+    _ck_global(L.bcs_ldu_load_sizes(str(path).encode(), ctypes.byref(nc), ctypes.byref(nf), ctypes.byref(n),
+                                    ctypes.byref(hb), ctypes.byref(hx)))
+    nc, nf, n = nc.value, nf.value, n.value
+    owner, neigh = np.zeros(nf, np.int32), np.zeros(nf, np.int32)
+    diag, upper, lower = np.zeros(nc * n * n), np.zeros(nf * n * n), np.zeros(nf * n * n)
+    b = np.zeros(nc * n) if hb.value else None
+    x0 = np.zeros(nc * n) if hx.value else None
+    _ck_global(L.bcs_ldu_load(str(path).encode(), N.ptr(owner), N.ptr(neigh), N.ptr(diag), N.ptr(upper), N.ptr(lower),
+                              N.ptr(b) if b is not None else None, N.ptr(x0) if x0 is not None else None))
+    A = BlockLduMatrix(nc, owner, neigh, n, diag, upper, lower)
+    return A, (BlockVector(nc, n, b) if b is not None else None), (BlockVector(nc, n, x0) if x0 is not None else None)

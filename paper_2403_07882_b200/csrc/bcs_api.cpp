@@ -9,7 +9,9 @@
 #include <algorithm>
 #include <map>
 #include <mutex>
+#include <cstdio>
 #include <cstring>
+#include <vector>
 #include <new>
 #include <string>
 
@@ -159,6 +161,123 @@ bcs_status bcs_set_stream(bcs_ctx* ctx, void* stream) {
 
 bcs_status bcs_set_kernel_timing(bcs_ctx* ctx, int enable) {
     return guarded(ctx, [&] { eng(ctx).setKernelTiming(enable != 0); });
+}
+
+// ---- binary LDU dump (bcs.h) ----------------------------------------------
+namespace {
+constexpr char kLduMagic[8] = {'B', 'C', 'S', 'L', 'D', 'U', '0', '1'};
+struct LduHeader {
+    char magic[8];
+    int32_t version, n_cells, n_faces, block_size, flags;
+    uint64_t checksum;
+    char pad[24];
+};
+static_assert(sizeof(LduHeader) == 64, "LDU header is 64 bytes");
+uint64_t fnv1a(uint64_t h, const void* p, size_t n) {
+    const unsigned char* c = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) {
+        h ^= c[i];
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+struct Section {
+    void* p;
+    size_t bytes;
+};
+std::vector<Section> lduSections(const LduHeader& h, const void* owner, const void* neigh, const void* diag,
+                                 const void* upper, const void* lower, const void* b, const void* x0) {
+    const size_t nn = static_cast<size_t>(h.block_size) * h.block_size, nf = h.n_faces, nc = h.n_cells;
+    std::vector<Section> v = {{const_cast<void*>(owner), 4 * nf},          {const_cast<void*>(neigh), 4 * nf},
+                              {const_cast<void*>(diag), 8 * nc * nn},     {const_cast<void*>(upper), 8 * nf * nn},
+                              {const_cast<void*>(lower), 8 * nf * nn}};
+    if (h.flags & 1) v.push_back({const_cast<void*>(b), 8 * nc * h.block_size});
+    if (h.flags & 2) v.push_back({const_cast<void*>(x0), 8 * nc * h.block_size});
+    return v;
+}
+LduHeader readHeader(std::FILE* f, const char* path) {
+    LduHeader h{};
+    if (std::fread(&h, sizeof h, 1, f) != 1 || std::memcmp(h.magic, kLduMagic, 8) != 0 || h.version != 1 ||
+        h.n_cells < 1 || h.n_faces < 0 || h.block_size < 1 || h.block_size > 16)
+        throw std::runtime_error(std::string("bcs_ldu_load: not a BCSLDU01 file: ") + path);
+    return h;
+}
+}  // namespace
+
+bcs_status bcs_ldu_save(const char* path, int n_cells, int n_faces, int block_size, const int32_t* owner,
+                        const int32_t* neighbour, const double* diag, const double* upper, const double* lower,
+                        const double* b, const double* x0) {
+    return guarded(nullptr, [&] {
+        if (!path || n_cells < 1 || n_faces < 0 || block_size < 1 || block_size > 16 || !diag ||
+            (n_faces && (!owner || !neighbour || !upper || !lower)))
+            throw std::invalid_argument("bcs_ldu_save: bad arguments");
+        LduHeader h{};
+        std::memcpy(h.magic, kLduMagic, 8);
+        h.version = 1;
+        h.n_cells = n_cells;
+        h.n_faces = n_faces;
+        h.block_size = block_size;
+        h.flags = (b ? 1 : 0) | (x0 ? 2 : 0);
+        const auto sec = lduSections(h, owner, neighbour, diag, upper, lower, b, x0);
+        uint64_t sum = 1469598103934665603ull;
+        for (const auto& x : sec) sum = fnv1a(sum, x.p, x.bytes);
+        h.checksum = sum;
+        std::FILE* f = std::fopen(path, "wb");
+        if (!f) throw std::runtime_error(std::string("bcs_ldu_save: cannot open ") + path);
+        bool ok = std::fwrite(&h, sizeof h, 1, f) == 1;
+        for (const auto& x : sec) ok = ok && (x.bytes == 0 || std::fwrite(x.p, 1, x.bytes, f) == x.bytes);
+        ok = (std::fclose(f) == 0) && ok;
+        if (!ok) throw std::runtime_error(std::string("bcs_ldu_save: write failed: ") + path);
+    });
+}
+
+bcs_status bcs_ldu_load_sizes(const char* path, int* n_cells, int* n_faces, int* block_size, int* has_b,
+                              int* has_x0) {
+    return guarded(nullptr, [&] {
+        std::FILE* f = path ? std::fopen(path, "rb") : nullptr;
+        if (!f) throw std::runtime_error(std::string("bcs_ldu_load: cannot open ") + (path ? path : "(null)"));
+        LduHeader h{};
+        try {
+            h = readHeader(f, path);
+        } catch (...) {
+            std::fclose(f);
+            throw;
+        }
+        std::fclose(f);
+        if (n_cells) *n_cells = h.n_cells;
+        if (n_faces) *n_faces = h.n_faces;
+        if (block_size) *block_size = h.block_size;
+        if (has_b) *has_b = h.flags & 1;
+        if (has_x0) *has_x0 = (h.flags >> 1) & 1;
+    });
+}
+
+bcs_status bcs_ldu_load(const char* path, int32_t* owner, int32_t* neighbour, double* diag, double* upper,
+                        double* lower, double* b, double* x0) {
+    return guarded(nullptr, [&] {
+        std::FILE* f = path ? std::fopen(path, "rb") : nullptr;
+        if (!f) throw std::runtime_error(std::string("bcs_ldu_load: cannot open ") + (path ? path : "(null)"));
+        std::vector<unsigned char> skip;
+        try {
+            const LduHeader h = readHeader(f, path);
+            auto sec = lduSections(h, owner, neighbour, diag, upper, lower, b, x0);
+            uint64_t sum = 1469598103934665603ull;
+            for (auto& x : sec) {
+                if (!x.p) {  // caller skips this section: read into scratch for the checksum
+                    skip.resize(x.bytes);
+                    x.p = skip.data();
+                }
+                if (x.bytes && std::fread(x.p, 1, x.bytes, f) != x.bytes)
+                    throw std::runtime_error(std::string("bcs_ldu_load: truncated file: ") + path);
+                sum = fnv1a(sum, x.p, x.bytes);
+            }
+            if (sum != h.checksum) throw std::runtime_error(std::string("bcs_ldu_load: checksum mismatch: ") + path);
+        } catch (...) {
+            std::fclose(f);
+            throw;
+        }
+        std::fclose(f);
+    });
 }
 
 uint64_t bcs_topology_signature(int n_cells, int n_faces, const int32_t* owner, const int32_t* neighbour) {

@@ -66,3 +66,32 @@ def test_struct_layouts_match_header():
     body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
     names = re.findall(r"\b([a-z_]+)\s*[;,]", body)
     assert [f for f, _ in _native.ReportC._fields_] == names
+
+
+def test_ldu_dump_round_trip_and_corruption(tmp_path):
+    """Binary LDU dump (bcs_ldu_save/load, host only): exact round trip of a
+    generator system, optional vectors, and the error paths."""
+    from paper_2403_07882_b200 import bcs, gen
+    s = gen.hex_coupled(5, 4, 3, poly_seed=2)
+    p = tmp_path / "sys.bcsldu"
+    bcs.save_ldu(p, s.A, s.b, s.x0)
+    A, b, x0 = bcs.load_ldu(p)
+    for x, y in ((A.owner, s.A.owner), (A.neighbour, s.A.neighbour), (A.diag, s.A.diag), (A.upper, s.A.upper),
+                 (A.lower, s.A.lower), (b.values, s.b.values), (x0.values, s.x0.values)):
+        assert x.tobytes() == y.tobytes()
+    assert A.n == 4 and A.n_cells == s.A.n_cells
+    q = tmp_path / "nob.bcsldu"
+    bcs.save_ldu(q, s.A)
+    A2, b2, x02 = bcs.load_ldu(q)
+    assert b2 is None and x02 is None and A2.upper.tobytes() == s.A.upper.tobytes()
+    raw = bytearray(p.read_bytes())
+    raw[100] ^= 0x40  # payload bit flip
+    (tmp_path / "bad.bcsldu").write_bytes(bytes(raw))
+    with pytest.raises(RuntimeError, match="checksum"):
+        bcs.load_ldu(tmp_path / "bad.bcsldu")
+    (tmp_path / "short.bcsldu").write_bytes(p.read_bytes()[:1000])
+    with pytest.raises(RuntimeError, match="truncated"):
+        bcs.load_ldu(tmp_path / "short.bcsldu")
+    (tmp_path / "junk.bcsldu").write_bytes(b"\0" * 128)
+    with pytest.raises(RuntimeError, match="not a BCSLDU01"):
+        bcs.load_ldu(tmp_path / "junk.bcsldu")
