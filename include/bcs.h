@@ -228,6 +228,23 @@ bcs_status bcs_assemble_euler(bcs_ctx* ctx, int n_cells, int n_faces, const int3
                               const double* face_area, int n_bfaces, const int32_t* bface_cell,
                               const double* bface_area, const double* q, const double* q_inf, double cfl,
                               double* rhs);
+/* Device assembly of the 4x4 pressure-based coupled p-U system: replaces
+ * assembleCoupled (incompressible.cpp:143-250: momentumDiagCoeff, least-
+ * squares pressure gradients, upwind + diffusion momentum, fx-interpolated
+ * pressure gradient, negated continuity with the Rhie-Chow compact Laplacian)
+ * followed by pinPressure(pin_cell, pin_value) (:252-264), for wall (kind 0)
+ * and moving-wall (kind 1, wall velocity bface_u) patches.  face_fx: the
+ * owner-side interpolation weight per internal face; cell_vol, cell_centroid
+ * (3 per cell); state (u, v, w, p per cell); phi the face fluxes; nu the
+ * viscosity; pin_cell < 0: no pinning.  Values go straight into the context's
+ * block-CSR, bit-identical to uploading the reference's LDU matrix; rhs (host,
+ * 4 per cell) receives the right-hand side. */
+bcs_status bcs_assemble_coupled(bcs_ctx* ctx, int n_cells, int n_faces, const int32_t* owner,
+                                const int32_t* neighbour, const double* face_area, const double* face_fx,
+                                const double* cell_vol, const double* cell_centroid, int n_bfaces,
+                                const int32_t* bface_cell, const double* bface_area, const int32_t* bface_kind,
+                                const double* bface_u, const double* state, const double* phi, double nu,
+                                int pin_cell, double pin_value, double* rhs);
 bcs_status bcs_solve(bcs_ctx* ctx, const double* b, double* x, const bcs_solver_config* cfg, bcs_report* report);
 bcs_status bcs_solve_device(bcs_ctx* ctx, const double* d_b, double* d_x, const bcs_solver_config* cfg,
                             bcs_report* report);

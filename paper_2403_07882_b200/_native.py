@@ -102,6 +102,8 @@ SIGNATURES = {
     "bcs_upload_ldu_device": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "bcs_assemble_euler": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
                                    c_void_p, c_void_p, c_double, c_void_p]),
+    "bcs_assemble_coupled": (c_int, [c_void_p, c_int, c_int] + [c_void_p] * 6 + [c_int] + [c_void_p] * 6
+                             + [c_double, c_int, c_double, c_void_p]),
     "bcs_solve": (c_int, [c_void_p, c_void_p, c_void_p, P(SolverConfigC), P(ReportC)]),
     "bcs_solve_device": (c_int, [c_void_p, c_void_p, c_void_p, P(SolverConfigC), P(ReportC)]),
     "bcs_residual": (c_int, [c_void_p, c_void_p, c_void_p, P(c_double)]),
@@ -137,6 +139,8 @@ GEN_SIGNATURES = {
     "bcsgen_hex_boundary_count": (None, [c_int, c_int, c_int, P(c_int)]),
     "bcsgen_hex_euler_inputs": (c_int, [c_int, c_int, c_int, c_double, ctypes.c_longlong, ctypes.c_longlong]
                                 + [c_void_p] * 4),
+    "bcsgen_hex_coupled_inputs": (c_int, [c_int, c_int, c_int, c_double, ctypes.c_longlong, ctypes.c_longlong]
+                                  + [c_void_p] * 10),
     "bcsgen_hex_sizes_poly": (None, [c_int, c_int, c_int, ctypes.c_longlong, P(c_int), P(c_int)]),
     "bcsgen_hex_euler_poly": (c_int, [c_int, c_int, c_int, c_double, ctypes.c_longlong, ctypes.c_longlong]
                               + [c_void_p] * 7),

@@ -218,6 +218,24 @@ class Context:
                                               N.ptr(q_inf), float(cfl), N.ptr(rhs)))
         return rhs
 
+    def assemble_coupled(self, owner, neighbour, face_area, face_fx, cell_vol, cell_centroid, bface_cell, bface_area,
+                         bface_kind, bface_u, state, phi, nu: float, pin_cell: int = 0, pin_value: float = 0.0,
+                         out: Optional[np.ndarray] = None) -> np.ndarray:
+        """Device assembleCoupled + pinPressure (wall / moving-wall patches): the
+        matrix goes into this context; returns the right-hand side."""
+        i32 = lambda a: np.ascontiguousarray(a, np.int32)  # noqa: E731
+        f64 = lambda a: np.ascontiguousarray(a, np.float64)  # noqa: E731
+        owner, neighbour, bface_cell, bface_kind = i32(owner), i32(neighbour), i32(bface_cell), i32(bface_kind)
+        face_area, face_fx, cell_vol, cell_centroid = f64(face_area), f64(face_fx), f64(cell_vol), f64(cell_centroid)
+        bface_area, bface_u, state, phi = f64(bface_area), f64(bface_u), f64(state), f64(phi)
+        nc = cell_vol.size
+        rhs = np.zeros(nc * 4) if out is None else out
+        self._ck(self._lib.bcs_assemble_coupled(
+            self.h, nc, owner.size, N.ptr(owner), N.ptr(neighbour), N.ptr(face_area), N.ptr(face_fx), N.ptr(cell_vol),
+            N.ptr(cell_centroid), bface_cell.size, N.ptr(bface_cell), N.ptr(bface_area), N.ptr(bface_kind),
+            N.ptr(bface_u), N.ptr(state), N.ptr(phi), float(nu), int(pin_cell), float(pin_value), N.ptr(rhs)))
+        return rhs
+
     def solve(self, b: np.ndarray, x: np.ndarray, cfg: SolverConfig) -> SolveReport:
         rep = N.ReportC()
         c = cfg.to_c()

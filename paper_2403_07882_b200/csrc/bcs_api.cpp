@@ -434,6 +434,23 @@ bcs_status bcs_assemble_euler(bcs_ctx* ctx, int n_cells, int n_faces, const int3
     });
 }
 
+bcs_status bcs_assemble_coupled(bcs_ctx* ctx, int n_cells, int n_faces, const int32_t* owner,
+                                const int32_t* neighbour, const double* face_area, const double* face_fx,
+                                const double* cell_vol, const double* cell_centroid, int n_bfaces,
+                                const int32_t* bface_cell, const double* bface_area, const int32_t* bface_kind,
+                                const double* bface_u, const double* state, const double* phi, double nu,
+                                int pin_cell, double pin_value, double* rhs) {
+    return guarded(ctx, [&] {
+        if (n_cells < 1 || n_faces < 0 || !cell_vol || !cell_centroid || !state || !rhs ||
+            (n_faces && (!owner || !neighbour || !face_area || !face_fx || !phi)) ||
+            (n_bfaces && (!bface_cell || !bface_area || !bface_kind || !bface_u)))
+            throw std::invalid_argument("bcs_assemble_coupled: bad arguments");
+        eng(ctx).assembleCoupled(n_cells, n_faces, owner, neighbour, face_area, face_fx, cell_vol, cell_centroid,
+                                 n_bfaces, bface_cell, bface_area, bface_kind, bface_u, state, phi, nu, pin_cell,
+                                 pin_value, rhs);
+    });
+}
+
 bcs_status bcs_solve(bcs_ctx* ctx, const double* b, double* x, const bcs_solver_config* cfg, bcs_report* report) {
     return guarded(ctx, [&] {
         bcs_report rep{};

@@ -268,58 +268,66 @@ void Engine::setTopology(int nc, int nf, int n, const int32_t* owner, const int3
 
 // assembleJacobian + computeResidual (euler.cpp:361-455; first order, Roe,
 // farfield patches) on the device, straight into the BSR slots
+void Engine::assemblyTopology(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh) {
+    if (!(hasTopo_ && nc == nc_ && nf == nf_ && n_ == n && sameFaces(owner, neigh, nf)))
+        setTopology(nc, nf, n, owner, neigh);
+    if (asmTopo_) return;
+    // cell -> its faces in face order (the reference's accumulation order)
+    std::vector<int> cfo(static_cast<size_t>(nc) + 1, 0), cf(2 * static_cast<size_t>(nf));
+    for (int f = 0; f < nf; ++f) {
+        ++cfo[owner[f] + 1];
+        ++cfo[neigh[f] + 1];
+    }
+    for (int c = 0; c < nc; ++c) cfo[c + 1] += cfo[c];
+    std::vector<int> pos(cfo.begin(), cfo.end() - 1);
+    for (int f = 0; f < nf; ++f) {
+        cf[pos[owner[f]]++] = f;
+        cf[pos[neigh[f]]++] = f;
+    }
+    asmCfo_.ensure(cfo.size(), stream_);
+    asmCf_.ensure(cf.size() + 1, stream_);
+    check(cudaMemcpyAsync(asmCfo_.p, cfo.data(), sizeof(int) * cfo.size(), cudaMemcpyHostToDevice, stream_), "H2D cfo");
+    if (nf) check(cudaMemcpyAsync(asmCf_.p, cf.data(), sizeof(int) * cf.size(), cudaMemcpyHostToDevice, stream_), "H2D cf");
+    const size_t nnz = static_cast<size_t>(nc) + 2 * static_cast<size_t>(nf);
+    asmInv_.ensure(nnz, stream_);
+    assemble_inverse_src(static_cast<int>(nnz), src_, asmInv_.p, stream_);
+    sync();  // the host tables are released on return
+    asmTopo_ = true;
+}
+
+void Engine::assemblyBoundary(int nc, int nb, const int32_t* bcell, std::vector<int>& order) {
+    std::vector<int> bco(static_cast<size_t>(nc) + 1, 0);
+    order.assign(static_cast<size_t>(nb), 0);
+    for (int b = 0; b < nb; ++b) {
+        if (bcell[b] < 0 || bcell[b] >= nc) throw std::invalid_argument("bcs_assemble: boundary face cell out of range");
+        ++bco[bcell[b] + 1];
+    }
+    for (int c = 0; c < nc; ++c) bco[c + 1] += bco[c];
+    std::vector<int> pos(bco.begin(), bco.end() - 1);
+    for (int b = 0; b < nb; ++b) order[pos[bcell[b]]++] = b;
+    asmBco_.ensure(bco.size(), stream_);
+    check(cudaMemcpyAsync(asmBco_.p, bco.data(), sizeof(int) * bco.size(), cudaMemcpyHostToDevice, stream_), "H2D bco");
+    sync();  // bco is a stack temporary
+}
+
+// assembleJacobian + computeResidual (euler.cpp:361-455; first order, Roe,
+// farfield patches) on the device, straight into the BSR slots
 void Engine::assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* neigh, const double* faceArea,
                            int nb, const int32_t* bcell, const double* barea, const double* q, const double* qinf,
                            double cfl, double* rhs) {
     LaunchScope ls(&launches_);
     if (nb < 0) throw std::invalid_argument("bcs_assemble_euler: n_bfaces < 0");
-    if (!(hasTopo_ && nc == nc_ && nf == nf_ && n_ == 5 && sameFaces(owner, neigh, nf)))
-        setTopology(nc, nf, 5, owner, neigh);
-    if (!asmTopo_) {
-        // cell -> its faces in face order (the reference's accumulation order)
-        std::vector<int> cfo(static_cast<size_t>(nc) + 1, 0), cf(2 * static_cast<size_t>(nf));
-        for (int f = 0; f < nf; ++f) {
-            ++cfo[owner[f] + 1];
-            ++cfo[neigh[f] + 1];
-        }
-        for (int c = 0; c < nc; ++c) cfo[c + 1] += cfo[c];
-        std::vector<int> pos(cfo.begin(), cfo.end() - 1);
-        for (int f = 0; f < nf; ++f) {
-            cf[pos[owner[f]]++] = f;
-            cf[pos[neigh[f]]++] = f;
-        }
-        asmCfo_.ensure(cfo.size(), stream_);
-        asmCf_.ensure(cf.size() + 1, stream_);
-        check(cudaMemcpyAsync(asmCfo_.p, cfo.data(), sizeof(int) * cfo.size(), cudaMemcpyHostToDevice, stream_), "H2D cfo");
-        if (nf)
-            check(cudaMemcpyAsync(asmCf_.p, cf.data(), sizeof(int) * cf.size(), cudaMemcpyHostToDevice, stream_), "H2D cf");
-        const size_t nnz = static_cast<size_t>(nc) + 2 * static_cast<size_t>(nf);
-        asmInv_.ensure(nnz, stream_);
-        assemble_inverse_src(static_cast<int>(nnz), src_, asmInv_.p, stream_);
-        sync();  // the host tables are released on return
-        asmTopo_ = true;
-    }
-    // boundary faces per cell, patch order kept
-    std::vector<int> bco(static_cast<size_t>(nc) + 1, 0), border(static_cast<size_t>(nb));
-    for (int b = 0; b < nb; ++b) {
-        if (bcell[b] < 0 || bcell[b] >= nc) throw std::invalid_argument("bcs_assemble_euler: boundary face cell out of range");
-        ++bco[bcell[b] + 1];
-    }
-    for (int c = 0; c < nc; ++c) bco[c + 1] += bco[c];
-    {
-        std::vector<int> pos(bco.begin(), bco.end() - 1);
-        for (int b = 0; b < nb; ++b) border[pos[bcell[b]]++] = b;
-    }
+    assemblyTopology(nc, nf, 5, owner, neigh);
+    std::vector<int> border;
+    assemblyBoundary(nc, nb, bcell, border);
     std::vector<double> bsorted(3 * static_cast<size_t>(nb));
     for (int k = 0; k < nb; ++k)
         for (int d = 0; d < 3; ++d) bsorted[3 * static_cast<size_t>(k) + d] = barea[3 * static_cast<size_t>(border[k]) + d];
     const size_t N = static_cast<size_t>(nc) * 5;
-    asmBco_.ensure(bco.size(), stream_);
     asmArea_.ensure(3 * static_cast<size_t>(nf) + 3, stream_);
     asmBarea_.ensure(bsorted.size() + 3, stream_);
     asmQ_.ensure(N + 5, stream_);
     asmRhs_.ensure(N, stream_);
-    check(cudaMemcpyAsync(asmBco_.p, bco.data(), sizeof(int) * bco.size(), cudaMemcpyHostToDevice, stream_), "H2D bco");
     if (nf)
         check(cudaMemcpyAsync(asmArea_.p, faceArea, sizeof(double) * 3 * nf, cudaMemcpyHostToDevice, stream_), "H2D area");
     if (nb)
@@ -334,6 +342,62 @@ void Engine::assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* 
     checkErr("assembleEuler");
     hasValues_ = true;
     H_->pcKind = -1;  // any preconditioner built on old values is stale
+}
+
+// assembleCoupled + pinPressure (incompressible.cpp:143-264) on the device,
+// wall / moving-wall patches (bkind 0 / 1, wall velocity bu)
+void Engine::assembleCoupled(int nc, int nf, const int32_t* owner, const int32_t* neigh, const double* faceArea,
+                             const double* fx, const double* vol, const double* cen, int nb, const int32_t* bcell,
+                             const double* barea, const int32_t* bkind, const double* bu, const double* state,
+                             const double* phi, double nu, int pinCell, double pinValue, double* rhs) {
+    LaunchScope ls(&launches_);
+    if (nb < 0) throw std::invalid_argument("bcs_assemble_coupled: n_bfaces < 0");
+    for (int b = 0; b < nb; ++b)
+        if (bkind[b] != 0 && bkind[b] != 1)
+            throw std::invalid_argument("bcs_assemble_coupled: only wall (0) and moving-wall (1) patches");
+    if (pinCell >= nc) throw std::invalid_argument("bcs_assemble_coupled: pin cell out of range");
+    assemblyTopology(nc, nf, 4, owner, neigh);
+    std::vector<int> border;
+    assemblyBoundary(nc, nb, bcell, border);
+    std::vector<double> ba(3 * static_cast<size_t>(nb)), bv(3 * static_cast<size_t>(nb));
+    for (int k = 0; k < nb; ++k)
+        for (int d = 0; d < 3; ++d) {
+            ba[3 * static_cast<size_t>(k) + d] = barea[3 * static_cast<size_t>(border[k]) + d];
+            bv[3 * static_cast<size_t>(k) + d] = bu[3 * static_cast<size_t>(border[k]) + d];
+        }
+    const size_t N = static_cast<size_t>(nc) * 4;
+    asmArea_.ensure(3 * static_cast<size_t>(nf) + 3, stream_);
+    asmFx_.ensure(static_cast<size_t>(nf) + 1, stream_);
+    asmPhi_.ensure(static_cast<size_t>(nf) + 1, stream_);
+    asmVol_.ensure(nc, stream_);
+    asmCen_.ensure(3 * static_cast<size_t>(nc), stream_);
+    asmBarea_.ensure(ba.size() + 3, stream_);
+    asmBu_.ensure(bv.size() + 3, stream_);
+    asmQ_.ensure(N, stream_);
+    asmD_.ensure(nc, stream_);
+    asmGrad_.ensure(3 * static_cast<size_t>(nc), stream_);
+    asmRhs_.ensure(N, stream_);
+    if (nf) {
+        check(cudaMemcpyAsync(asmArea_.p, faceArea, sizeof(double) * 3 * nf, cudaMemcpyHostToDevice, stream_), "H2D area");
+        check(cudaMemcpyAsync(asmFx_.p, fx, sizeof(double) * nf, cudaMemcpyHostToDevice, stream_), "H2D fx");
+        check(cudaMemcpyAsync(asmPhi_.p, phi, sizeof(double) * nf, cudaMemcpyHostToDevice, stream_), "H2D phi");
+    }
+    check(cudaMemcpyAsync(asmVol_.p, vol, sizeof(double) * nc, cudaMemcpyHostToDevice, stream_), "H2D vol");
+    check(cudaMemcpyAsync(asmCen_.p, cen, sizeof(double) * 3 * nc, cudaMemcpyHostToDevice, stream_), "H2D cen");
+    if (nb) {
+        check(cudaMemcpyAsync(asmBarea_.p, ba.data(), sizeof(double) * ba.size(), cudaMemcpyHostToDevice, stream_),
+              "H2D barea");
+        check(cudaMemcpyAsync(asmBu_.p, bv.data(), sizeof(double) * bv.size(), cudaMemcpyHostToDevice, stream_), "H2D bu");
+    }
+    check(cudaMemcpyAsync(asmQ_.p, state, sizeof(double) * N, cudaMemcpyHostToDevice, stream_), "H2D state");
+    assemble_coupled(nc, nf, dOwner_, dNeigh_, asmArea_, asmFx_, asmVol_, asmCen_, asmCfo_, asmCf_, asmBco_, asmBarea_,
+                     asmBu_, asmQ_, asmPhi_, nu, pinCell, pinValue, asmInv_, asmD_.p, asmGrad_.p, vals_.p, asmRhs_.p,
+                     stream_);
+    check(cudaMemcpyAsync(rhs, asmRhs_.p, sizeof(double) * N, cudaMemcpyDeviceToHost, stream_), "D2H rhs");
+    sync();
+    checkErr("assembleCoupled");
+    hasValues_ = true;
+    H_->pcKind = -1;
 }
 
 void Engine::uploadLdu(const double* diag, const double* upper, const double* lower, bool device_ptrs) {

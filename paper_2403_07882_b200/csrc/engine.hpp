@@ -116,6 +116,14 @@ public:
     void assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* neigh, const double* faceArea, int nb,
                        const int32_t* bcell, const double* barea, const double* q, const double* qinf, double cfl,
                        double* rhs);
+    // device assembleCoupled + pinPressure (wall / moving-wall patches); rhs: host, 4 per cell
+    void assembleCoupled(int nc, int nf, const int32_t* owner, const int32_t* neigh, const double* faceArea,
+                         const double* fx, const double* vol, const double* cen, int nb, const int32_t* bcell,
+                         const double* barea, const int32_t* bkind, const double* bu, const double* state,
+                         const double* phi, double nu, int pinCell, double pinValue, double* rhs);
+    void assemblyTopology(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh);
+    // boundary faces grouped per cell (patch order kept): offsets and the permutation
+    void assemblyBoundary(int nc, int nb, const int32_t* bcell, std::vector<int>& order);
 
     // drop-in pipeline (engine.cpp:47-120)
     void pipelineSolve(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh, const double* diag,
@@ -208,7 +216,7 @@ private:
     // device assembly: slot of every LDU block, cell -> faces (face order), cell -> boundary faces
     bool asmTopo_ = false;
     DArray<int> asmInv_, asmCfo_, asmCf_, asmBco_;
-    DArray<double> asmArea_, asmBarea_, asmQ_, asmRhs_;
+    DArray<double> asmArea_, asmBarea_, asmQ_, asmRhs_, asmFx_, asmVol_, asmCen_, asmBu_, asmPhi_, asmD_, asmGrad_;
     // SolvePipeline state (engine.hpp:35-37): only the EngineCsr branch updates it
     bool pipeHasSetup_ = false;
     uint64_t pipeSig_ = 0;

@@ -133,4 +133,69 @@ BCS_HD void roe(const Prim& L, const Prim& R, V3 n, double* flux) {
 }
 
 
+// ---- coupled p-U building blocks (incompressible.cpp:91-126) --------------
+// smallmat::luFactor + luSolve for a 3x3 (first max by strict >, no singular
+// check: the caller regularises), in place
+BCS_HD void lu3Solve(double* a, double* x) {
+    int piv[3];
+    for (int k = 0; k < 3; ++k) {
+        int p = k;
+        double best = fabs(a[k * 3 + k]);
+        for (int i = k + 1; i < 3; ++i)
+            if (fabs(a[i * 3 + k]) > best) {
+                best = fabs(a[i * 3 + k]);
+                p = i;
+            }
+        piv[k] = p;
+        if (p != k)
+            for (int j = 0; j < 3; ++j) {
+                const double t = a[k * 3 + j];
+                a[k * 3 + j] = a[p * 3 + j];
+                a[p * 3 + j] = t;
+            }
+        const double d = a[k * 3 + k];
+        for (int i = k + 1; i < 3; ++i) {
+            a[i * 3 + k] /= d;
+            for (int j = k + 1; j < 3; ++j) a[i * 3 + j] -= a[i * 3 + k] * a[k * 3 + j];
+        }
+    }
+    for (int k = 0; k < 3; ++k)
+        if (piv[k] != k) {
+            const double t = x[k];
+            x[k] = x[piv[k]];
+            x[piv[k]] = t;
+        }
+    for (int i = 1; i < 3; ++i)
+        for (int j = 0; j < i; ++j) x[i] -= a[i * 3 + j] * x[j];
+    for (int i = 2; i >= 0; --i) {
+        for (int j = i + 1; j < 3; ++j) x[i] -= a[i * 3 + j] * x[j];
+        x[i] /= a[i * 3 + i];
+    }
+}
+
+// least-squares gradient term of neighbour j seen from cell i
+// (pressureGradients' accumulate: G += w d d^T, b += d (w (p_j - p_i)))
+BCS_HD void lsqAccumulate(V3 d, double pj_minus_pi, double* G, V3& b) {
+    const double w = 1.0 / dot3(d, d);
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) G[r * 3 + c] += w * comp(d, r) * comp(d, c);
+    const double t = w * pj_minus_pi;
+    b = add(b, scl(d, t));
+}
+
+// regularise degenerate directions and solve G g = b (pressureGradients' tail)
+BCS_HD V3 lsqFinish(double* G, V3 b) {
+    double rv[3] = {b.x, b.y, b.z};
+    double scale = 0.0;
+    for (int r = 0; r < 3; ++r) scale = scale < G[r * 3 + r] ? G[r * 3 + r] : scale;  // std::max
+    for (int r = 0; r < 3; ++r)
+        if (G[r * 3 + r] <= 1e-12 * scale) {
+            for (int c = 0; c < 3; ++c) G[r * 3 + c] = G[c * 3 + r] = 0.0;
+            G[r * 3 + r] = 1.0;
+            rv[r] = 0.0;
+        }
+    lu3Solve(G, rv);
+    return V3{rv[0], rv[1], rv[2]};
+}
+
 }  // namespace bcs_euler

@@ -192,90 +192,50 @@ void euler(const Hex& h, double* diag, double* upper, double* lower, double* rhs
 }
 
 // -------------------------------------------------------- coupled p-U 4x4
-// in-place partial-pivot LU + solve of a 3x3 (smallmat.hpp:67-108 semantics)
-void lu3Solve(double* a, double* x) {
-    int piv[3];
-    for (int k = 0; k < 3; ++k) {
-        int p = k;
-        double best = std::fabs(a[k * 3 + k]);
-        for (int i = k + 1; i < 3; ++i)
-            if (std::fabs(a[i * 3 + k]) > best) {
-                best = std::fabs(a[i * 3 + k]);
-                p = i;
-            }
-        piv[k] = p;
-        if (p != k)
-            for (int j = 0; j < 3; ++j) std::swap(a[k * 3 + j], a[p * 3 + j]);
-        const double d = a[k * 3 + k];
-        for (int i = k + 1; i < 3; ++i) {
-            a[i * 3 + k] /= d;
-            for (int j = k + 1; j < 3; ++j) a[i * 3 + j] -= a[i * 3 + k] * a[k * 3 + j];
-        }
-    }
-    for (int k = 0; k < 3; ++k)
-        if (piv[k] != k) std::swap(x[k], x[piv[k]]);
-    for (int i = 1; i < 3; ++i)
-        for (int j = 0; j < i; ++j) x[i] -= a[i * 3 + j] * x[j];
-    for (int i = 2; i >= 0; --i) {
-        for (int j = i + 1; j < 3; ++j) x[i] -= a[i * 3 + j] * x[j];
-        x[i] /= a[i * 3 + i];
-    }
-}
-
 std::vector<V3> lsqPressureGrad(const Hex& h, const std::vector<double>& s) {
     const int nc = h.nc;
     std::vector<double> G(9 * static_cast<std::size_t>(nc), 0.0);
     std::vector<V3> b(nc, V3{0.0, 0.0, 0.0});
     auto acc = [&](int i, int j) {
-        const V3 d = sub(h.cen[j], h.cen[i]);
-        const double w = 1.0 / dot3(d, d);
-        for (int r = 0; r < 3; ++r)
-            for (int c = 0; c < 3; ++c) G[9 * static_cast<std::size_t>(i) + r * 3 + c] += w * comp(d, r) * comp(d, c);
-        const double t = w * (s[4 * static_cast<std::size_t>(j) + 3] - s[4 * static_cast<std::size_t>(i) + 3]);
-        b[i] = add(b[i], scl(d, t));
+        lsqAccumulate(sub(h.cen[j], h.cen[i]), s[4 * static_cast<std::size_t>(j) + 3] - s[4 * static_cast<std::size_t>(i) + 3],
+                      &G[9 * static_cast<std::size_t>(i)], b[i]);
     };
     for (std::size_t f = 0; f < h.owner.size(); ++f) {
         acc(h.owner[f], h.neigh[f]);
         acc(h.neigh[f], h.owner[f]);
     }
     std::vector<V3> g(nc);
-    for (int i = 0; i < nc; ++i) {
-        double* Gi = &G[9 * static_cast<std::size_t>(i)];
-        double rv[3] = {b[i].x, b[i].y, b[i].z};
-        double scale = 0.0;
-        for (int r = 0; r < 3; ++r) scale = std::max(scale, Gi[r * 3 + r]);
-        for (int r = 0; r < 3; ++r)
-            if (Gi[r * 3 + r] <= 1e-12 * scale) {
-                for (int c = 0; c < 3; ++c) Gi[r * 3 + c] = Gi[c * 3 + r] = 0.0;
-                Gi[r * 3 + r] = 1.0;
-                rv[r] = 0.0;
-            }
-        lu3Solve(Gi, rv);
-        g[i] = {rv[0], rv[1], rv[2]};
-    }
+    for (int i = 0; i < nc; ++i) g[i] = lsqFinish(&G[9 * static_cast<std::size_t>(i)], b[i]);
     return g;
 }
 
-void coupled(const Hex& h, double* diag, double* upper, double* lower, double* rhs, double* x0) {
-    const int nc = h.nc;
-    const int nf = static_cast<int>(h.owner.size());
-    const double nu = 0.01;
+// seeded coupled state (u, v, w, p per cell) and the Rhie-Chow face fluxes the
+// workload assembles with: rhieChowFlux(state, D(momentumDiagCoeff(phi = 0)))
+std::vector<double> coupledState(int nc) {
     std::vector<double> s(4 * static_cast<std::size_t>(nc));
-    {
-        std::mt19937 gen(1);
-        std::uniform_real_distribution<double> U(-0.1, 0.1);
-        for (double& v : s) v = U(gen);
-    }
-    std::memcpy(x0, s.data(), sizeof(double) * s.size());
-    struct Geo {
-        double S, nd;
-    };
-    std::vector<Geo> geo(nf);
-    for (int f = 0; f < nf; ++f) {
+    std::mt19937 gen(1);
+    std::uniform_real_distribution<double> U(-0.1, 0.1);
+    for (double& v : s) v = U(gen);
+    return s;
+}
+
+struct Geo {
+    double S, nd;
+};
+std::vector<Geo> faceGeo(const Hex& h) {
+    std::vector<Geo> geo(h.owner.size());
+    for (std::size_t f = 0; f < h.owner.size(); ++f) {
         const double S = len3(h.area[f]);
         const V3 n = dvd(h.area[f], S);
         geo[f] = {S, dot3(n, sub(h.cen[h.neigh[f]], h.cen[h.owner[f]]))};
     }
+    return geo;
+}
+
+std::vector<double> coupledPhi(const Hex& h, const std::vector<double>& s, double nu) {
+    const int nc = h.nc;
+    const int nf = static_cast<int>(h.owner.size());
+    const std::vector<Geo> geo = faceGeo(h);
     auto wallDist = [&](const BFace& bf) { return h.vol[bf.cell] / (2.0 * len3(bf.area)); };
     // momentum diagonal with phi = 0 (moving/static walls only contribute diffusion)
     std::vector<double> aP(nc, 0.0);
@@ -300,6 +260,20 @@ void coupled(const Hex& h, double* diag, double* upper, double* lower, double* r
         const V3 gpBar = add(scl(gp[o], fx), scl(gp[nb], 1.0 - fx));
         phi[f] = dot3(h.area[f], uBar) - dBar * (geo[f].S * dpc - dot3(h.area[f], gpBar));
     }
+    return phi;
+}
+
+void coupled(const Hex& h, double* diag, double* upper, double* lower, double* rhs, double* x0) {
+    const int nc = h.nc;
+    const int nf = static_cast<int>(h.owner.size());
+    const double nu = 0.01;
+    const std::vector<double> s = coupledState(nc);
+    std::memcpy(x0, s.data(), sizeof(double) * s.size());
+    const std::vector<Geo> geo = faceGeo(h);
+    auto wallDist = [&](const BFace& bf) { return h.vol[bf.cell] / (2.0 * len3(bf.area)); };
+    const std::vector<double> phi = coupledPhi(h, s, nu);
+    const std::vector<V3> gp = lsqPressureGrad(h, s);
+    std::vector<double> D(nc);
     // assembleCoupled recomputes aP from the new fluxes
     std::vector<double> aP2(nc, 0.0);
     for (int f = 0; f < nf; ++f) {
@@ -458,6 +432,47 @@ int bcsgen_hex_euler_inputs(int nx, int ny, int nz, double aspect, long long scr
     const std::vector<Prim> st = eulerState(h.nc);
     for (int c = 0; c < h.nc; ++c)
         for (int k = 0; k < 5; ++k) q[5 * static_cast<std::size_t>(c) + k] = st[c].v[k];
+    return 0;
+}
+
+// inputs of the 4x4 assembleCoupled on the same mesh: face area vectors and
+// interpolation weights, cell volumes and centroids, boundary faces in patch
+// order (cell, area, kind 0 wall / 1 moving wall, wall velocity), the seeded
+// state (u, v, w, p per cell) and the Rhie-Chow face fluxes phi
+int bcsgen_hex_coupled_inputs(int nx, int ny, int nz, double aspect, long long scrambleSeed, long long polySeed,
+                              double* faceArea, double* fx, double* vol, double* cen, int* bcell, double* barea,
+                              int* bkind, double* bu, double* state, double* phi) {
+    if (nx < 1 || ny < 1 || nz < 1 || !(aspect > 0.0)) return 1;
+    const Hex h = buildHex(nx, ny, nz, aspect, scrambleSeed, polySeed);
+    for (std::size_t f = 0; f < h.area.size(); ++f) {
+        faceArea[3 * f] = h.area[f].x;
+        faceArea[3 * f + 1] = h.area[f].y;
+        faceArea[3 * f + 2] = h.area[f].z;
+        fx[f] = h.fx[f];
+    }
+    for (int c = 0; c < h.nc; ++c) {
+        vol[c] = h.vol[c];
+        cen[3 * c] = h.cen[c].x;
+        cen[3 * c + 1] = h.cen[c].y;
+        cen[3 * c + 2] = h.cen[c].z;
+    }
+    std::size_t b = 0;
+    for (int p = 0; p < 6; ++p)
+        for (const BFace& bf : h.patches[p]) {
+            bcell[b] = bf.cell;
+            barea[3 * b] = bf.area.x;
+            barea[3 * b + 1] = bf.area.y;
+            barea[3 * b + 2] = bf.area.z;
+            bkind[b] = p == 5 ? 1 : 0;  // zmax: the moving lid
+            bu[3 * b] = p == 5 ? 1.0 : 0.0;
+            bu[3 * b + 1] = 0.0;
+            bu[3 * b + 2] = 0.0;
+            ++b;
+        }
+    const std::vector<double> s = coupledState(h.nc);
+    std::memcpy(state, s.data(), sizeof(double) * s.size());
+    const std::vector<double> ph = coupledPhi(h, s, 0.01);
+    std::memcpy(phi, ph.data(), sizeof(double) * ph.size());
     return 0;
 }
 

@@ -156,6 +156,166 @@ __global__ void __launch_bounds__(128) k_asm_cells(int nc, int nf, const int* __
     for (int k = 0; k < 5; ++k) rhs[5 * static_cast<size_t>(c) + kslot(k)] = res[k];
 }
 
+
+// ---- 4x4 pressure-based coupled p-U system (assembleCoupled,
+// incompressible.cpp:143-250, + pinPressure :252-264) for wall / moving-wall
+// patches: D = V / momentumDiagCoeff(state, phi) and the least-squares
+// pressure gradient per cell, then the face blocks and the cell blocks.
+constexpr int kP = 3;
+__device__ __forceinline__ double maxd(double a, double b) { return a < b ? b : a; }  // std::max
+__device__ __forceinline__ double mind(double a, double b) { return b < a ? b : a; }  // std::min
+
+struct CoupledGeom {
+    const int *owner, *neigh, *cfo, *cf, *bco;
+    const double *area, *fx, *vol, *cen, *barea, *bu;
+};
+
+__global__ void k_cp_cellpre(int nc, CoupledGeom g, const double* __restrict__ phi, const double* __restrict__ state,
+                             double nu, double* D, double* grad) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    double aP = 0.0, G[9];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) G[e] = 0.0;
+    V3 b{0.0, 0.0, 0.0};
+    const V3 cc = load_v3(g.cen, c);
+    const double pc = state[4 * static_cast<size_t>(c) + kP];
+    for (int e = g.cfo[c]; e < g.cfo[c + 1]; ++e) {
+        const int f = g.cf[e];
+        const int o = g.owner[f], nb = g.neigh[f];
+        const bool own = o == c;
+        const V3 A = load_v3(g.area, f);
+        const double S = bcs_euler::len3(A);
+        const V3 n = bcs_euler::dvd(A, S);
+        const double nd = bcs_euler::dot3(n, bcs_euler::sub(load_v3(g.cen, nb), load_v3(g.cen, o)));
+        const double gDiff = nu * S / nd;
+        aP = __dadd_rn(aP, own ? __dadd_rn(maxd(phi[f], 0.0), gDiff) : __dadd_rn(-mind(phi[f], 0.0), gDiff));
+        const int j = own ? nb : o;
+        bcs_euler::lsqAccumulate(bcs_euler::sub(load_v3(g.cen, j), cc), state[4 * static_cast<size_t>(j) + kP] - pc, G, b);
+    }
+    for (int k = g.bco[c]; k < g.bco[c + 1]; ++k) {  // walls: nu S / wallDistance
+        const V3 A = load_v3(g.barea, k);
+        const double S = bcs_euler::len3(A);
+        const double db = g.vol[c] / (2.0 * bcs_euler::len3(A));
+        aP = __dadd_rn(aP, nu * S / db);
+    }
+    D[c] = g.vol[c] / aP;
+    const V3 gr = bcs_euler::lsqFinish(G, b);
+    grad[3 * static_cast<size_t>(c)] = gr.x;
+    grad[3 * static_cast<size_t>(c) + 1] = gr.y;
+    grad[3 * static_cast<size_t>(c) + 2] = gr.z;
+}
+
+__global__ void k_cp_faces(int nc, int nf, CoupledGeom g, const double* __restrict__ phi, const double* __restrict__ D,
+                           double nu, int pin, const int* __restrict__ inv, double* vals) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= nf) return;
+    const int o = g.owner[f], nb = g.neigh[f];
+    const V3 A = load_v3(g.area, f);
+    const double S = bcs_euler::len3(A);
+    const V3 n = bcs_euler::dvd(A, S);
+    const double nd = bcs_euler::dot3(n, bcs_euler::sub(load_v3(g.cen, nb), load_v3(g.cen, o)));
+    const double gDiff = nu * S / nd;
+    const double fx = g.fx[f];
+    const double dBar = fx * D[o] + (1.0 - fx) * D[nb];
+    const double c = dBar * S / nd;
+    double up[16], lo[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) up[e] = lo[e] = 0.0;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const double sr = bcs_euler::comp(A, r);
+        up[r * 4 + r] += mind(phi[f], 0.0) - gDiff;
+        lo[r * 4 + r] += -maxd(phi[f], 0.0) - gDiff;
+        up[r * 4 + kP] += (1.0 - fx) * sr;
+        lo[r * 4 + kP] -= fx * sr;
+        up[kP * 4 + r] -= (1.0 - fx) * sr;
+        lo[kP * 4 + r] += fx * sr;
+    }
+    up[kP * 4 + kP] += c;
+    lo[kP * 4 + kP] += c;
+    if (o == pin)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) up[kP * 4 + q] = 0.0;
+    if (nb == pin)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) lo[kP * 4 + q] = 0.0;
+    double* du = vals + 16 * static_cast<size_t>(inv[nc + f]);
+    double* dl = vals + 16 * static_cast<size_t>(inv[nc + nf + f]);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        du[e] = up[e];
+        dl[e] = lo[e];
+    }
+}
+
+__global__ void k_cp_cells(int nc, CoupledGeom g, const double* __restrict__ phi, const double* __restrict__ D,
+                           const double* __restrict__ grad, double nu, int pin, double pinValue,
+                           const int* __restrict__ inv, double* vals, double* rhs) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    double Dm[16], rr[4];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) Dm[e] = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rr[q] = 0.0;
+    for (int e = g.cfo[c]; e < g.cfo[c + 1]; ++e) {
+        const int f = g.cf[e];
+        const int o = g.owner[f], nb = g.neigh[f];
+        const bool own = o == c;
+        const V3 A = load_v3(g.area, f);
+        const double S = bcs_euler::len3(A);
+        const V3 n = bcs_euler::dvd(A, S);
+        const double nd = bcs_euler::dot3(n, bcs_euler::sub(load_v3(g.cen, nb), load_v3(g.cen, o)));
+        const double gDiff = nu * S / nd;
+        const double fx = g.fx[f];
+        const double dBar = fx * D[o] + (1.0 - fx) * D[nb];
+        const double cc = dBar * S / nd;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            const double sr = bcs_euler::comp(A, r);
+            if (own) {
+                Dm[r * 4 + r] += maxd(phi[f], 0.0) + gDiff;
+                Dm[r * 4 + kP] += fx * sr;
+                Dm[kP * 4 + r] -= fx * sr;
+            } else {
+                Dm[r * 4 + r] += -mind(phi[f], 0.0) + gDiff;
+                Dm[r * 4 + kP] -= (1.0 - fx) * sr;
+                Dm[kP * 4 + r] += (1.0 - fx) * sr;
+            }
+        }
+        Dm[kP * 4 + kP] -= cc;
+        const V3 gpBar = bcs_euler::add(bcs_euler::scl(load_v3(grad, o), fx), bcs_euler::scl(load_v3(grad, nb), 1.0 - fx));
+        const double ev = dBar * bcs_euler::dot3(A, gpBar);
+        if (own) rr[kP] += ev;
+        else rr[kP] -= ev;
+    }
+    for (int k = g.bco[c]; k < g.bco[c + 1]; ++k) {  // wall / moving wall
+        const V3 A = load_v3(g.barea, k);
+        const double S = bcs_euler::len3(A);
+        const double db = g.vol[c] / (2.0 * bcs_euler::len3(A));
+        const double gb = nu * S / db;
+        const V3 u = load_v3(g.bu, k);
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            Dm[r * 4 + r] += gb;
+            rr[r] += gb * bcs_euler::comp(u, r);
+            Dm[r * 4 + kP] += bcs_euler::comp(A, r);  // zero-gradient p
+        }
+    }
+    if (c == pin) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Dm[kP * 4 + q] = 0.0;
+        Dm[kP * 4 + kP] = 1.0;
+        rr[kP] = pinValue;
+    }
+    double* dst = vals + 16 * static_cast<size_t>(inv[c]);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) dst[e] = Dm[e];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rhs[4 * static_cast<size_t>(c) + q] = rr[q];
+}
+
 }  // namespace
 
 void assemble_inverse_src(int nnzb, const int* src, int* inv, cudaStream_t s) {
@@ -171,6 +331,18 @@ void assemble_euler(int nc, int nf, const int* owner, const int* neigh, const do
     k_asm_cells<<<(nc + 127) / 128, 128, 0, s>>>(nc, nf, owner, neigh, area, cfo, cfl, bco, barea, q, qinf, cfl_num,
                                                  inv, vals, rhs);
     count_launch(nf > 0 ? 2 : 1);
+}
+
+void assemble_coupled(int nc, int nf, const int* owner, const int* neigh, const double* area, const double* fx,
+                      const double* vol, const double* cen, const int* cfo, const int* cf, const int* bco,
+                      const double* barea, const double* bu, const double* state, const double* phi, double nu,
+                      int pin, double pinValue, const int* inv, double* D, double* grad, double* vals, double* rhs,
+                      cudaStream_t s) {
+    const CoupledGeom g{owner, neigh, cfo, cf, bco, area, fx, vol, cen, barea, bu};
+    k_cp_cellpre<<<(nc + 127) / 128, 128, 0, s>>>(nc, g, phi, state, nu, D, grad);
+    if (nf > 0) k_cp_faces<<<(nf + 255) / 256, 256, 0, s>>>(nc, nf, g, phi, D, nu, pin, inv, vals);
+    k_cp_cells<<<(nc + 127) / 128, 128, 0, s>>>(nc, g, phi, D, grad, nu, pin, pinValue, inv, vals, rhs);
+    count_launch(nf > 0 ? 3 : 2);
 }
 
 }  // namespace bcs

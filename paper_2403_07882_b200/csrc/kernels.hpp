@@ -122,6 +122,12 @@ void assemble_euler(int nc, int nf, const int* owner, const int* neigh, const do
                     const int* cfl, const int* bco, const double* barea, const double* q, const double* qinf,
                     double cfl_num, const int* inv, double* vals, double* rhs, cudaStream_t s);
 
+void assemble_coupled(int nc, int nf, const int* owner, const int* neigh, const double* area, const double* fx,
+                      const double* vol, const double* cen, const int* cfo, const int* cf, const int* bco,
+                      const double* barea, const double* bu, const double* state, const double* phi, double nu,
+                      int pin, double pinValue, const int* inv, double* D, double* grad, double* vals, double* rhs,
+                      cudaStream_t s);
+
 // ------------------------------------------------------------ AMG (K9-K12)
 void strengths(int n, int rows, const int* ro, const int* ci, const int* dg, const double* v, double* dn,
                double* str, int nnz, cudaStream_t s);

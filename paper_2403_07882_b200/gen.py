@@ -104,3 +104,26 @@ def hex_euler_inputs(nx: int, ny: int = None, nz: int = None, aspect: float = 1.
         raise ValueError("bcsgen_hex_euler_inputs: bad arguments")
     q_inf = np.array([1.0, 0.5, 0.1, 0.0, 1.0 / 1.4])
     return area, bcell, barea, q, q_inf
+
+
+def hex_coupled_inputs(nx: int, ny: int = None, nz: int = None, aspect: float = 1.0, scramble_seed: int = -1,
+                       poly_seed: int = -1) -> dict:
+    """Inputs of assembleCoupled on the mesh of ``hex_coupled`` (same
+    arguments): geometry, wall / moving-lid boundary faces, the seeded state and
+    the Rhie-Chow face fluxes -- for the device assembly."""
+    ny = nx if ny is None else ny
+    nz = nx if nz is None else nz
+    nc, nf = hex_sizes(nx, ny, nz, poly_seed)
+    nb = ctypes.c_int()
+    N.gen().bcsgen_hex_boundary_count(nx, ny, nz, ctypes.byref(nb))
+    nb = nb.value
+    d = dict(face_area=np.zeros(3 * nf), face_fx=np.zeros(nf), cell_vol=np.zeros(nc), cell_centroid=np.zeros(3 * nc),
+             bface_cell=np.zeros(nb, np.int32), bface_area=np.zeros(3 * nb), bface_kind=np.zeros(nb, np.int32),
+             bface_u=np.zeros(3 * nb), state=np.zeros(4 * nc), phi=np.zeros(nf))
+    rc = N.gen().bcsgen_hex_coupled_inputs(nx, ny, nz, float(aspect), int(scramble_seed), int(poly_seed),
+                                           *[N.ptr(d[k]) for k in ("face_area", "face_fx", "cell_vol", "cell_centroid",
+                                                                   "bface_cell", "bface_area", "bface_kind", "bface_u",
+                                                                   "state", "phi")])
+    if rc:
+        raise ValueError("bcsgen_hex_coupled_inputs: bad arguments")
+    return d
