@@ -87,3 +87,18 @@ def test_dist_mp_requires_comm_init():
             c.dist_solve_mp(s.A, s.b, s.x0, s.centroids, 2, cfg)
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("ranks,engines", [(2, 2), (4, 2), (8, 8)])
+def test_dist_fgmres_matches_reference_gmres(ctx, ref, ranks, engines):
+    """FGMRES in Mode R runs the reference's Arnoldi process: the iteration
+    count of the reference's distributedSolve with GMRES, the same solution."""
+    s = gen.hex_euler(10)
+    cfg_t = make_cfg(method=0, precond=3, max_iters=400)
+    cfg = bcs.SolverConfig(method=bcs.KrylovMethod.FGMRES, preconditioner=bcs.PrecondKind.AMG, relTol=1e-8,
+                           maxIters=400, amg=bcs.AmgConfig(maxLevels=30, minCoarseRows=8))
+    rc, xr, rr = ref_distributed_solve(ref, s.A, s.b.values, s.x0.values, s.centroids, ranks, engines, cfg_t)
+    assert rc == 0, ref.err()
+    x, r = ctx.dist_solve(s.A, s.b, s.x0, s.centroids, ranks, engines, cfg)
+    assert r.converged and rr.converged and r.iterations == rr.iterations
+    np.testing.assert_allclose(x.values, xr, rtol=0, atol=1e-6 * np.abs(xr).max())
