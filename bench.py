@@ -149,7 +149,7 @@ def solver_config(method):
 TAIL_ROWS = 512  # Engine::tailMaxRows_ default (levels handled by k_vcycle_tail)
 
 
-def chain_hop_ns(bcs, L=20000, reps=3):
+def chain_hop_ns(bcs, L=20000, reps=3, device=0):
     """Measured latency floor of the sweep kernel: a DILU application on a 1-D
     chain of L 5x5 rows (every row depends on the previous one) costs 2L hops."""
     owner = np.arange(L - 1, dtype=np.int32)
@@ -160,7 +160,7 @@ def chain_hop_ns(bcs, L=20000, reps=3):
         dg[:, i, i] += 4.0
     A = bcs.BlockLduMatrix(L, owner, neigh, 5, dg.reshape(-1), rng.uniform(-.1, .1, (L - 1) * 25),
                            rng.uniform(-.1, .1, (L - 1) * 25))
-    c = bcs.Context(0)
+    c = bcs.Context(device)
     try:
         c.set_topology(A)
         c.upload_ldu(A)
@@ -325,7 +325,7 @@ def run_ours(args):
         depth_sum = sum(ctx.schedule_depth(l) for l in swept)
         vcycles = sw_n / len(preps) / (4 * max(1, len(swept)))
         hops = vcycles * 4 * depth_sum
-        hop = chain_hop_ns(bcs)
+        hop = chain_hop_ns(bcs, device=local)
         floor_ms = hops * hop * 1e-6
         latency = {"hops_per_step": hops, "chain_hop_ns": hop, "floor_ms_per_step": floor_ms,
                    "measured_ms_per_step": sw_ms / len(preps),
