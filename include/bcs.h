@@ -228,6 +228,17 @@ bcs_status bcs_assemble_euler(bcs_ctx* ctx, int n_cells, int n_faces, const int3
                               const double* face_area, int n_bfaces, const int32_t* bface_cell,
                               const double* bface_area, const double* q, const double* q_inf, double cfl,
                               double* rhs);
+/* bcs_assemble_euler with a patch kind per boundary face (ghostState,
+ * euler.cpp:320-341; EulerCase::patchOverride resolved by the caller):
+ * bface_kind = the reference's PatchKind order, 0 wall, 1 inlet, 2 outlet,
+ * 3 farfield, 4 slip, 5 symmetry.  Wall/slip/symmetry reflect the interior
+ * velocity, inlet/farfield take q_inf, outlet the interior state.  Any other
+ * value: BCS_INVALID_ARGUMENT "unknown patch kind" (euler.cpp:340).
+ * bface_kind == NULL is bcs_assemble_euler (all farfield). */
+bcs_status bcs_assemble_euler_patches(bcs_ctx* ctx, int n_cells, int n_faces, const int32_t* owner,
+                                      const int32_t* neighbour, const double* face_area, int n_bfaces,
+                                      const int32_t* bface_cell, const double* bface_area, const int32_t* bface_kind,
+                                      const double* q, const double* q_inf, double cfl, double* rhs);
 /* Device assembly of the 4x4 pressure-based coupled p-U system: replaces
  * assembleCoupled (incompressible.cpp:143-250: momentumDiagCoeff, least-
  * squares pressure gradients, upwind + diffusion momentum, fx-interpolated

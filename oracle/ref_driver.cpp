@@ -293,12 +293,19 @@ void ref_hex_sizes(int nx, int ny, int nz, int* nCells, int* nFaces, int* nBound
 }
 
 // 5x5 density-based system: assembleJacobian (euler.cpp:390-455) on the
-// synthetic hex mesh, first-order Roe, all-farfield, cfl 50.
-int ref_gen_euler_poly(int nx, int ny, int nz, double aspect, long long scrambleSeed, long long polySeed, int* owner,
-                       int* neigh, double* diag, double* upper, double* lower, double* rhs, double* centroids) {
+// synthetic hex mesh, first-order Roe, cfl 50; patchKinds (6 ints in the
+// PatchKind order, for xmin xmax ymin ymax zmin zmax) go through
+// EulerCase::patchOverride, nullptr = all farfield.
+int ref_gen_euler_kinds(int nx, int ny, int nz, double aspect, long long scrambleSeed, long long polySeed,
+                        const int* patchKinds, int* owner, int* neigh, double* diag, double* upper, double* lower,
+                        double* rhs, double* centroids) {
     return guard([&] {
         const Mesh mesh = hexMesh(nx, ny, nz, aspect, scrambleSeed, PatchKind::farfield, polySeed);
         EulerCase ec;
+        if (patchKinds) {
+            const char* names[6] = {"xmin", "xmax", "ymin", "ymax", "zmin", "zmax"};
+            for (int p = 0; p < 6; ++p) ec.patchOverride[names[p]] = static_cast<PatchKind>(patchKinds[p]);
+        }
         ec.flux = FluxScheme::Roe;
         ec.recon.firstOrder = true;
         ec.freestream = {1.0, 0.5, 0.1, 0.0, 1.0 / 1.4};
@@ -315,6 +322,12 @@ int ref_gen_euler_poly(int nx, int ny, int nz, double aspect, long long scramble
         auto [A, b] = assembleJacobian(q, mesh, ec, 50.0);
         exportLdu(A, b, owner, neigh, diag, upper, lower, rhs, centroids);
     });
+}
+
+int ref_gen_euler_poly(int nx, int ny, int nz, double aspect, long long scrambleSeed, long long polySeed, int* owner,
+                       int* neigh, double* diag, double* upper, double* lower, double* rhs, double* centroids) {
+    return ref_gen_euler_kinds(nx, ny, nz, aspect, scrambleSeed, polySeed, nullptr, owner, neigh, diag, upper, lower,
+                               rhs, centroids);
 }
 
 // 4x4 pressure-based coupled system (incompressible.cpp:143-264): lid-driven

@@ -201,9 +201,11 @@ class Context:
         self._ck(self._lib.bcs_upload_ldu_device(self.h, c_ptr(d_diag), c_ptr(d_upper), c_ptr(d_lower)))
 
     def assemble_euler(self, owner, neighbour, face_area, bface_cell, bface_area, q, q_inf, cfl: float,
-                       out: Optional[np.ndarray] = None) -> np.ndarray:
-        """Device assembleJacobian + computeResidual (first order, Roe, farfield):
-        the matrix goes into this context; returns the right-hand side."""
+                       out: Optional[np.ndarray] = None, bface_kind=None) -> np.ndarray:
+        """Device assembleJacobian + computeResidual (first order, Roe): the
+        matrix goes into this context; returns the right-hand side.
+        ``bface_kind``: the reference's PatchKind per boundary face (0 wall,
+        1 inlet, 2 outlet, 3 farfield, 4 slip, 5 symmetry); None = all farfield."""
         owner = np.ascontiguousarray(owner, np.int32)
         neighbour = np.ascontiguousarray(neighbour, np.int32)
         face_area = np.ascontiguousarray(face_area, np.float64)
@@ -213,9 +215,18 @@ class Context:
         q_inf = np.ascontiguousarray(q_inf, np.float64)
         nc = q.size // 5
         rhs = np.zeros(nc * 5) if out is None else out
-        self._ck(self._lib.bcs_assemble_euler(self.h, nc, owner.size, N.ptr(owner), N.ptr(neighbour), N.ptr(face_area),
-                                              bface_cell.size, N.ptr(bface_cell), N.ptr(bface_area), N.ptr(q),
-                                              N.ptr(q_inf), float(cfl), N.ptr(rhs)))
+        if bface_kind is None:
+            self._ck(self._lib.bcs_assemble_euler(self.h, nc, owner.size, N.ptr(owner), N.ptr(neighbour),
+                                                  N.ptr(face_area), bface_cell.size, N.ptr(bface_cell),
+                                                  N.ptr(bface_area), N.ptr(q), N.ptr(q_inf), float(cfl), N.ptr(rhs)))
+        else:
+            bface_kind = np.ascontiguousarray(bface_kind, np.int32)
+            if bface_kind.size != bface_cell.size:
+                raise ValueError("assemble_euler: bface_kind needs one entry per boundary face")
+            self._ck(self._lib.bcs_assemble_euler_patches(self.h, nc, owner.size, N.ptr(owner), N.ptr(neighbour),
+                                                          N.ptr(face_area), bface_cell.size, N.ptr(bface_cell),
+                                                          N.ptr(bface_area), N.ptr(bface_kind), N.ptr(q), N.ptr(q_inf),
+                                                          float(cfl), N.ptr(rhs)))
         return rhs
 
     def assemble_coupled(self, owner, neighbour, face_area, face_fx, cell_vol, cell_centroid, bface_cell, bface_area,

@@ -421,17 +421,25 @@ bcs_status bcs_upload_ldu_device(bcs_ctx* ctx, const double* d_diag, const doubl
     return guarded(ctx, [&] { eng(ctx).uploadLdu(d_diag, d_upper, d_lower, true); });
 }
 
-bcs_status bcs_assemble_euler(bcs_ctx* ctx, int n_cells, int n_faces, const int32_t* owner, const int32_t* neighbour,
-                              const double* face_area, int n_bfaces, const int32_t* bface_cell,
-                              const double* bface_area, const double* q, const double* q_inf, double cfl,
-                              double* rhs) {
+bcs_status bcs_assemble_euler_patches(bcs_ctx* ctx, int n_cells, int n_faces, const int32_t* owner,
+                                      const int32_t* neighbour, const double* face_area, int n_bfaces,
+                                      const int32_t* bface_cell, const double* bface_area, const int32_t* bface_kind,
+                                      const double* q, const double* q_inf, double cfl, double* rhs) {
     return guarded(ctx, [&] {
         if (n_cells < 1 || n_faces < 0 || !q || !q_inf || !rhs || (n_faces && (!owner || !neighbour || !face_area)) ||
             (n_bfaces && (!bface_cell || !bface_area)))
             throw std::invalid_argument("bcs_assemble_euler: bad arguments");
-        eng(ctx).assembleEuler(n_cells, n_faces, owner, neighbour, face_area, n_bfaces, bface_cell, bface_area, q,
-                               q_inf, cfl, rhs);
+        eng(ctx).assembleEuler(n_cells, n_faces, owner, neighbour, face_area, n_bfaces, bface_cell, bface_area,
+                               bface_kind, q, q_inf, cfl, rhs);
     });
+}
+
+bcs_status bcs_assemble_euler(bcs_ctx* ctx, int n_cells, int n_faces, const int32_t* owner, const int32_t* neighbour,
+                              const double* face_area, int n_bfaces, const int32_t* bface_cell,
+                              const double* bface_area, const double* q, const double* q_inf, double cfl,
+                              double* rhs) {
+    return bcs_assemble_euler_patches(ctx, n_cells, n_faces, owner, neighbour, face_area, n_bfaces, bface_cell,
+                                      bface_area, nullptr, q, q_inf, cfl, rhs);
 }
 
 bcs_status bcs_assemble_coupled(bcs_ctx* ctx, int n_cells, int n_faces, const int32_t* owner,

@@ -311,18 +311,31 @@ void Engine::assemblyBoundary(int nc, int nb, const int32_t* bcell, std::vector<
 }
 
 // assembleJacobian + computeResidual (euler.cpp:361-455; first order, Roe,
-// farfield patches) on the device, straight into the BSR slots
+// any patch kinds, ghostState :320-341) on the device, straight into the BSR slots
 void Engine::assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* neigh, const double* faceArea,
-                           int nb, const int32_t* bcell, const double* barea, const double* q, const double* qinf,
-                           double cfl, double* rhs) {
+                           int nb, const int32_t* bcell, const double* barea, const int32_t* bkind, const double* q,
+                           const double* qinf, double cfl, double* rhs) {
     LaunchScope ls(&launches_);
     if (nb < 0) throw std::invalid_argument("bcs_assemble_euler: n_bfaces < 0");
+    if (bkind)
+        for (int b = 0; b < nb; ++b)
+            if (bkind[b] < 0 || bkind[b] > 5) throw std::invalid_argument("unknown patch kind");  // euler.cpp:340
     assemblyTopology(nc, nf, 5, owner, neigh);
     std::vector<int> border;
     assemblyBoundary(nc, nb, bcell, border);
     std::vector<double> bsorted(3 * static_cast<size_t>(nb));
-    for (int k = 0; k < nb; ++k)
+    std::vector<int> ksorted(bkind ? static_cast<size_t>(nb) : 0);
+    for (int k = 0; k < nb; ++k) {
         for (int d = 0; d < 3; ++d) bsorted[3 * static_cast<size_t>(k) + d] = barea[3 * static_cast<size_t>(border[k]) + d];
+        if (bkind) ksorted[k] = bkind[border[k]];
+    }
+    if (bkind) {
+        asmBkind_.ensure(ksorted.size() + 1, stream_);
+        if (nb)
+            check(cudaMemcpyAsync(asmBkind_.p, ksorted.data(), sizeof(int) * ksorted.size(), cudaMemcpyHostToDevice,
+                                  stream_),
+                  "H2D bkind");
+    }
     const size_t N = static_cast<size_t>(nc) * 5;
     asmArea_.ensure(3 * static_cast<size_t>(nf) + 3, stream_);
     asmBarea_.ensure(bsorted.size() + 3, stream_);
@@ -335,8 +348,8 @@ void Engine::assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* 
               "H2D barea");
     check(cudaMemcpyAsync(asmQ_.p, q, sizeof(double) * N, cudaMemcpyHostToDevice, stream_), "H2D q");
     check(cudaMemcpyAsync(asmQ_.p + N, qinf, sizeof(double) * 5, cudaMemcpyHostToDevice, stream_), "H2D qinf");
-    assemble_euler(nc, nf, dOwner_, dNeigh_, asmArea_, asmCfo_, asmCf_, asmBco_, asmBarea_, asmQ_, asmQ_.p + N, cfl,
-                   asmInv_, vals_.p, asmRhs_.p, stream_);
+    assemble_euler(nc, nf, dOwner_, dNeigh_, asmArea_, asmCfo_, asmCf_, asmBco_, asmBarea_,
+                   bkind ? asmBkind_.p : nullptr, asmQ_, asmQ_.p + N, cfl, asmInv_, vals_.p, asmRhs_.p, stream_);
     check(cudaMemcpyAsync(rhs, asmRhs_.p, sizeof(double) * N, cudaMemcpyDeviceToHost, stream_), "D2H rhs");
     sync();
     checkErr("assembleEuler");

@@ -2,7 +2,9 @@
 // assembleJacobian (euler.cpp:390-455: first-order approximate Jacobian,
 // Roe-averaged spectral radius, pseudo-time diagonal) and its right-hand side,
 // the steady residual (computeResidual, euler.cpp:361-389, Roe flux :103-150)
-// for first-order reconstruction and farfield boundary patches, written
+// for first-order reconstruction and every boundary patch kind of the
+// reference (ghostState, euler.cpp:320-341: wall/slip/symmetry reflect the
+// velocity, inlet/farfield take the freestream, outlet the interior), written
 // straight into the engine's block-CSR slots.  A caller then uploads the
 // primitive state (5 doubles per cell) instead of the LDU values (50 doubles
 // per face + 25 per cell).
@@ -36,6 +38,21 @@ __device__ __forceinline__ Prim load_prim(const double* q, int c) {
 __device__ __forceinline__ V3 load_v3(const double* a, int i) {
     const double* p = a + 3 * static_cast<size_t>(i);
     return V3{p[0], p[1], p[2]};
+}
+
+// ghost state across a boundary face (ghostState, euler.cpp:320-341); kind =
+// the reference's PatchKind (0 wall, 1 inlet, 2 outlet, 3 farfield, 4 slip,
+// 5 symmetry), validated on the host
+__device__ __forceinline__ Prim ghost_state(const Prim& in, V3 n, int kind, const Prim& far) {
+    if (kind == 1 || kind == 3) return far;
+    if (kind == 2) return in;
+    const V3 u{in.v[1], in.v[2], in.v[3]};
+    const double s = 2.0 * bcs_euler::dot3(u, n);  // u - n * (2 dot(u, n))
+    Prim g = in;
+    g.v[1] = u.x - n.x * s;
+    g.v[2] = u.y - n.y * s;
+    g.v[3] = u.z - n.z * s;
+    return g;
 }
 
 __global__ void k_inverse_src(int nnzb, const int* __restrict__ src, int* inv) {
@@ -86,6 +103,7 @@ __global__ void __launch_bounds__(128) k_asm_cells(int nc, int nf, const int* __
                                                    const int* __restrict__ neigh, const double* __restrict__ area,
                                                    const int* __restrict__ cfo, const int* __restrict__ cfl,
                                                    const int* __restrict__ bco, const double* __restrict__ barea,
+                                                   const int* __restrict__ bkind,
                                                    const double* __restrict__ q, const double* __restrict__ qinf,
                                                    double cfl_num, const int* __restrict__ inv, double* vals,
                                                    double* rhs) {
@@ -123,12 +141,13 @@ __global__ void __launch_bounds__(128) k_asm_cells(int nc, int nf, const int* __
 #pragma unroll
         for (int k = 0; k < 5; ++k) res[k] = own ? __dsub_rn(res[k], __dmul_rn(S, fl[k])) : __dadd_rn(res[k], __dmul_rn(S, fl[k]));
     }
-    // farfield boundary faces: ghost state frozen, only the interior half enters (euler.cpp:426-441)
+    // boundary faces: ghost state frozen, only the interior half enters (euler.cpp:426-441)
     for (int b = bco[c]; b < bco[c + 1]; ++b) {
         const V3 A = load_v3(barea, b);
         const double S = bcs_euler::len3(A);
         const V3 n = bcs_euler::dvd(A, S);
-        const RoeAvg a = bcs_euler::roeAvg(qc, far);
+        const Prim g = ghost_state(qc, n, bkind ? bkind[b] : 3, far);
+        const RoeAvg a = bcs_euler::roeAvg(qc, g);
         const double lam = fabs(bcs_euler::dot3(a.u, n)) + a.c;
         bcs_euler::convJac(qc, n, J);
         const double scale = 0.5 * S, lamScale = 0.5 * S * lam;
@@ -138,7 +157,7 @@ __global__ void __launch_bounds__(128) k_asm_cells(int nc, int nf, const int* __
             for (int cc = 0; cc < 5; ++cc)
                 D[r * 5 + cc] = __dadd_rn(D[r * 5 + cc], __dadd_rn(__dmul_rn(scale, J[r * 5 + cc]), r == cc ? lamScale : 0.0));
         lamSum = __dadd_rn(lamSum, __dmul_rn(lam, S));
-        bcs_euler::roe(qc, far, n, fl);
+        bcs_euler::roe(qc, g, n, fl);
 #pragma unroll
         for (int k = 0; k < 5; ++k) res[k] = __dsub_rn(res[k], __dmul_rn(S, fl[k]));
     }
@@ -325,11 +344,11 @@ void assemble_inverse_src(int nnzb, const int* src, int* inv, cudaStream_t s) {
 }
 
 void assemble_euler(int nc, int nf, const int* owner, const int* neigh, const double* area, const int* cfo,
-                    const int* cfl, const int* bco, const double* barea, const double* q, const double* qinf,
-                    double cfl_num, const int* inv, double* vals, double* rhs, cudaStream_t s) {
+                    const int* cfl, const int* bco, const double* barea, const int* bkind, const double* q,
+                    const double* qinf, double cfl_num, const int* inv, double* vals, double* rhs, cudaStream_t s) {
     if (nf > 0) k_asm_faces<<<(nf + 255) / 256, 256, 0, s>>>(nc, nf, owner, neigh, area, q, inv, vals);
-    k_asm_cells<<<(nc + 127) / 128, 128, 0, s>>>(nc, nf, owner, neigh, area, cfo, cfl, bco, barea, q, qinf, cfl_num,
-                                                 inv, vals, rhs);
+    k_asm_cells<<<(nc + 127) / 128, 128, 0, s>>>(nc, nf, owner, neigh, area, cfo, cfl, bco, barea, bkind, q, qinf,
+                                                 cfl_num, inv, vals, rhs);
     count_launch(nf > 0 ? 2 : 1);
 }
 

@@ -118,9 +118,10 @@ unsigned long long selftest_chain(int variant, int L, int warps);  // total ns  
 
 // ------------------------------------------------- device assembly (§8(f))
 void assemble_inverse_src(int nnzb, const int* src, int* inv, cudaStream_t s);
+// bkind: PatchKind per boundary face in bco order, or nullptr (all farfield)
 void assemble_euler(int nc, int nf, const int* owner, const int* neigh, const double* area, const int* cfo,
-                    const int* cfl, const int* bco, const double* barea, const double* q, const double* qinf,
-                    double cfl_num, const int* inv, double* vals, double* rhs, cudaStream_t s);
+                    const int* cfl, const int* bco, const double* barea, const int* bkind, const double* q,
+                    const double* qinf, double cfl_num, const int* inv, double* vals, double* rhs, cudaStream_t s);
 
 void assemble_coupled(int nc, int nf, const int* owner, const int* neigh, const double* area, const double* fx,
                       const double* vol, const double* cen, const int* cfo, const int* cf, const int* bco,

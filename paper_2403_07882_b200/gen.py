@@ -106,6 +106,22 @@ def hex_euler_inputs(nx: int, ny: int = None, nz: int = None, aspect: float = 1.
     return area, bcell, barea, q, q_inf
 
 
+PATCH_KINDS = {"wall": 0, "inlet": 1, "outlet": 2, "farfield": 3, "slip": 4, "symmetry": 5}
+
+
+def hex_patch_kinds(nx: int, ny: int = None, nz: int = None, kinds=(3, 3, 3, 3, 3, 3)) -> np.ndarray:
+    """Per-boundary-face PatchKind (the reference's enum order, PATCH_KINDS)
+    for the hex mesh's six patches xmin xmax ymin ymax zmin zmax, in the patch
+    order of ``hex_euler_inputs``' boundary faces."""
+    ny = nx if ny is None else ny
+    nz = nx if nz is None else nz
+    k = [PATCH_KINDS[x] if isinstance(x, str) else int(x) for x in kinds]
+    if len(k) != 6:
+        raise ValueError("hex_patch_kinds: six patch kinds (xmin xmax ymin ymax zmin zmax)")
+    sizes = [ny * nz, ny * nz, nx * nz, nx * nz, nx * ny, nx * ny]
+    return np.concatenate([np.full(n, v, np.int32) for n, v in zip(sizes, k)])
+
+
 def hex_coupled_inputs(nx: int, ny: int = None, nz: int = None, aspect: float = 1.0, scramble_seed: int = -1,
                        poly_seed: int = -1) -> dict:
     """Inputs of assembleCoupled on the mesh of ``hex_coupled`` (same

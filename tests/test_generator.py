@@ -51,3 +51,22 @@ def test_hex_sizes_and_ordering():
     s = gen.hex_euler(4, 3, 2, scramble_seed=5)
     assert np.all(s.A.owner < s.A.neighbour)
     assert sorted(set(np.concatenate([s.A.owner, s.A.neighbour]).tolist())) == list(range(nc))
+
+
+def test_euler_patch_override_reference(ref):
+    """The reference's patchOverride hook (euler.cpp:345-348) that the device
+    patch-kind assembly is checked against: all-farfield overrides reproduce the
+    plain generator bit for bit, other kinds change the system."""
+    base = ref.gen_euler(5, 4, 3)
+    same = ref.gen_euler_kinds(5, 4, 3, [3] * 6)
+    assert all(a.tobytes() == b.tobytes() for a, b in zip(base, same))
+    mixed = ref.gen_euler_kinds(5, 4, 3, [0, 1, 2, 3, 4, 5])
+    assert mixed[5].tobytes() != base[5].tobytes() and mixed[2].tobytes() != base[2].tobytes()
+    assert mixed[3].tobytes() == base[3].tobytes()  # internal-face blocks do not see the patches
+
+
+def test_hex_patch_kinds_layout():
+    k = gen.hex_patch_kinds(5, 4, 3, ["wall", "inlet", "outlet", "farfield", "slip", "symmetry"])
+    _, bcell, _, _, _ = gen.hex_euler_inputs(5, 4, 3)
+    assert k.size == bcell.size
+    assert np.array_equal(np.bincount(k), [12, 12, 15, 15, 20, 20])
