@@ -239,6 +239,18 @@ bcs_status bcs_assemble_euler_patches(bcs_ctx* ctx, int n_cells, int n_faces, co
                                       const int32_t* neighbour, const double* face_area, int n_bfaces,
                                       const int32_t* bface_cell, const double* bface_area, const int32_t* bface_kind,
                                       const double* q, const double* q_inf, double cfl, double* rhs);
+/* bcs_assemble_euler_patches with second-order MUSCL face states in the
+ * residual (musclReconstruct, euler.cpp:236-312: least-squares primitive
+ * gradients :205-234, limiter 0 none / 1 Barth-Jespersen, first order where a
+ * reconstructed state is non-physical); the Jacobian stays first order as in
+ * assembleJacobian.  face_fx: owner-side weight per internal face (face
+ * centre = fx c_owner + (1 - fx) c_neighbour, mesh.hpp:55-59);
+ * cell_centroid: 3 per cell. */
+bcs_status bcs_assemble_euler_muscl(bcs_ctx* ctx, int n_cells, int n_faces, const int32_t* owner,
+                                    const int32_t* neighbour, const double* face_area, const double* face_fx,
+                                    const double* cell_centroid, int n_bfaces, const int32_t* bface_cell,
+                                    const double* bface_area, const int32_t* bface_kind, const double* q,
+                                    const double* q_inf, int limiter, double cfl, double* rhs);
 /* Device assembly of the 4x4 pressure-based coupled p-U system: replaces
  * assembleCoupled (incompressible.cpp:143-250: momentumDiagCoeff, least-
  * squares pressure gradients, upwind + diffusion momentum, fx-interpolated

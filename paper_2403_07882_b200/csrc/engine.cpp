@@ -314,9 +314,13 @@ void Engine::assemblyBoundary(int nc, int nb, const int32_t* bcell, std::vector<
 // any patch kinds, ghostState :320-341) on the device, straight into the BSR slots
 void Engine::assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* neigh, const double* faceArea,
                            int nb, const int32_t* bcell, const double* barea, const int32_t* bkind, const double* q,
-                           const double* qinf, double cfl, double* rhs) {
+                           const double* qinf, double cfl, double* rhs, int recon, const double* faceFx,
+                           const double* cellCen) {
     LaunchScope ls(&launches_);
     if (nb < 0) throw std::invalid_argument("bcs_assemble_euler: n_bfaces < 0");
+    if (recon < 0 || recon > 2) throw std::invalid_argument("bcs_assemble_euler: unknown reconstruction");
+    if (recon && (!cellCen || (nf && !faceFx)))
+        throw std::invalid_argument("bcs_assemble_euler: MUSCL needs face_fx and cell_centroid");
     if (bkind)
         for (int b = 0; b < nb; ++b)
             if (bkind[b] < 0 || bkind[b] > 5) throw std::invalid_argument("unknown patch kind");  // euler.cpp:340
@@ -348,8 +352,24 @@ void Engine::assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* 
               "H2D barea");
     check(cudaMemcpyAsync(asmQ_.p, q, sizeof(double) * N, cudaMemcpyHostToDevice, stream_), "H2D q");
     check(cudaMemcpyAsync(asmQ_.p + N, qinf, sizeof(double) * 5, cudaMemcpyHostToDevice, stream_), "H2D qinf");
+    const double *fsL = nullptr, *fsR = nullptr;
+    if (recon) {  // musclReconstruct on the device (euler.cpp:236-312)
+        asmFx_.ensure(static_cast<size_t>(nf) + 1, stream_);
+        asmCen_.ensure(3 * static_cast<size_t>(nc), stream_);
+        asmMuGrad_.ensure(15 * static_cast<size_t>(nc), stream_);
+        asmPsi_.ensure(5 * static_cast<size_t>(nc), stream_);
+        asmFs_.ensure(10 * static_cast<size_t>(nf) + 1, stream_);
+        if (nf)
+            check(cudaMemcpyAsync(asmFx_.p, faceFx, sizeof(double) * nf, cudaMemcpyHostToDevice, stream_), "H2D fx");
+        check(cudaMemcpyAsync(asmCen_.p, cellCen, sizeof(double) * 3 * nc, cudaMemcpyHostToDevice, stream_), "H2D cen");
+        fsL = asmFs_.p;
+        fsR = asmFs_.p + 5 * static_cast<size_t>(nf);
+        assemble_euler_muscl(nc, nf, dOwner_, dNeigh_, asmCfo_, asmCf_, asmCen_, asmFx_, asmQ_, recon == 2 ? 1 : 0,
+                             asmMuGrad_, asmPsi_, asmFs_.p, asmFs_.p + 5 * static_cast<size_t>(nf), stream_);
+    }
     assemble_euler(nc, nf, dOwner_, dNeigh_, asmArea_, asmCfo_, asmCf_, asmBco_, asmBarea_,
-                   bkind ? asmBkind_.p : nullptr, asmQ_, asmQ_.p + N, cfl, asmInv_, vals_.p, asmRhs_.p, stream_);
+                   bkind ? asmBkind_.p : nullptr, fsL, fsR, asmQ_, asmQ_.p + N, cfl, asmInv_, vals_.p, asmRhs_.p,
+                   stream_);
     check(cudaMemcpyAsync(rhs, asmRhs_.p, sizeof(double) * N, cudaMemcpyDeviceToHost, stream_), "D2H rhs");
     sync();
     checkErr("assembleEuler");

@@ -113,10 +113,12 @@ public:
     void setTopology(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh);
     void uploadLdu(const double* diag, const double* upper, const double* lower, bool device_ptrs);
     // device assembly of the 5x5 density-based system (k_assemble.cu); rhs: host, 5 per cell
-    // bkind: PatchKind per boundary face (0 wall .. 5 symmetry) or nullptr (all farfield)
+    // bkind: PatchKind per boundary face (0 wall .. 5 symmetry) or nullptr (all farfield);
+    // recon 0 first order, 1 MUSCL without limiter, 2 MUSCL + Barth-Jespersen (needs faceFx, cellCen)
     void assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* neigh, const double* faceArea, int nb,
                        const int32_t* bcell, const double* barea, const int32_t* bkind, const double* q,
-                       const double* qinf, double cfl, double* rhs);
+                       const double* qinf, double cfl, double* rhs, int recon = 0, const double* faceFx = nullptr,
+                       const double* cellCen = nullptr);
     // device assembleCoupled + pinPressure (wall / moving-wall patches); rhs: host, 4 per cell
     void assembleCoupled(int nc, int nf, const int32_t* owner, const int32_t* neigh, const double* faceArea,
                          const double* fx, const double* vol, const double* cen, int nb, const int32_t* bcell,
@@ -217,6 +219,7 @@ private:
     // device assembly: slot of every LDU block, cell -> faces (face order), cell -> boundary faces
     bool asmTopo_ = false;
     DArray<int> asmInv_, asmCfo_, asmCf_, asmBco_, asmBkind_;
+    DArray<double> asmMuGrad_, asmPsi_, asmFs_;
     DArray<double> asmArea_, asmBarea_, asmQ_, asmRhs_, asmFx_, asmVol_, asmCen_, asmBu_, asmPhi_, asmD_, asmGrad_;
     // SolvePipeline state (engine.hpp:35-37): only the EngineCsr branch updates it
     bool pipeHasSetup_ = false;

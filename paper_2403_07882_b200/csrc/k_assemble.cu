@@ -40,6 +40,9 @@ __device__ __forceinline__ V3 load_v3(const double* a, int i) {
     return V3{p[0], p[1], p[2]};
 }
 
+__device__ __forceinline__ double maxd(double a, double b) { return a < b ? b : a; }  // std::max
+__device__ __forceinline__ double mind(double a, double b) { return b < a ? b : a; }  // std::min
+
 // ghost state across a boundary face (ghostState, euler.cpp:320-341); kind =
 // the reference's PatchKind (0 wall, 1 inlet, 2 outlet, 3 farfield, 4 slip,
 // 5 symmetry), validated on the host
@@ -98,12 +101,115 @@ __global__ void k_asm_faces(int nc, int nf, const int* __restrict__ owner, const
     }
 }
 
+// ---- MUSCL reconstruction of the residual's face states (musclReconstruct,
+// euler.cpp:236-312; primitiveGradients :205-234).  Per cell: least-squares
+// gradients of the five primitives (G and the five right-hand sides summed
+// over the cell's faces in face order, the order of the reference's
+// accumulate loop), then the Barth-Jespersen factor (min/max are
+// order-free).  Per face: the limited linear extrapolation from both sides,
+// first order where the result is non-physical.  The Jacobian stays first
+// order (assembleJacobian uses q itself); only computeResidual sees these.
+__device__ __forceinline__ V3 face_centre(const double* cen, const double* fx, int f, int o, int nb) {
+    const V3 co = load_v3(cen, o), cn = load_v3(cen, nb);  // Mesh::faceCentre (mesh.hpp:55-59)
+    const double w = fx[f];
+    return bcs_euler::add(bcs_euler::scl(co, w), bcs_euler::scl(cn, 1.0 - w));
+}
+
+__global__ void __launch_bounds__(128) k_mu_cells(int nc, const int* __restrict__ owner, const int* __restrict__ neigh,
+                                                  const int* __restrict__ cfo, const int* __restrict__ cfl,
+                                                  const double* __restrict__ cen, const double* __restrict__ fx,
+                                                  const double* __restrict__ q, int limiter, double* grad,
+                                                  double* psi) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    const Prim qc = load_prim(q, c);
+    const V3 cc = load_v3(cen, c);
+    double G[9];
+    V3 b[5];
+    Prim qmin = qc, qmax = qc;
+#pragma unroll
+    for (int e = 0; e < 9; ++e) G[e] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) b[k] = V3{0.0, 0.0, 0.0};
+    for (int e = cfo[c]; e < cfo[c + 1]; ++e) {
+        const int f = cfl[e];
+        const int j = owner[f] == c ? neigh[f] : owner[f];
+        const Prim qj = load_prim(q, j);
+        const V3 d = bcs_euler::sub(load_v3(cen, j), cc);
+        const double w = 1.0 / bcs_euler::dot3(d, d);
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int cl = 0; cl < 3; ++cl) G[r * 3 + cl] += w * bcs_euler::comp(d, r) * bcs_euler::comp(d, cl);
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            b[k] = bcs_euler::add(b[k], bcs_euler::scl(d, w * (qj.v[k] - qc.v[k])));
+            qmin.v[k] = mind(qmin.v[k], qj.v[k]);
+            qmax.v[k] = maxd(qmax.v[k], qj.v[k]);
+        }
+    }
+    V3 g[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        double Gk[9];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) Gk[e] = G[e];
+        g[k] = bcs_euler::lsqFinish(Gk, b[k]);  // same regularisation and LU for every component
+        grad[15 * static_cast<size_t>(c) + 3 * k] = g[k].x;
+        grad[15 * static_cast<size_t>(c) + 3 * k + 1] = g[k].y;
+        grad[15 * static_cast<size_t>(c) + 3 * k + 2] = g[k].z;
+    }
+    double ps[5] = {1.0, 1.0, 1.0, 1.0, 1.0};
+    if (limiter == 1) {  // Barth-Jespersen (euler.cpp:262-283)
+        for (int e = cfo[c]; e < cfo[c + 1]; ++e) {
+            const int f = cfl[e];
+            const V3 dx = bcs_euler::sub(face_centre(cen, fx, f, owner[f], neigh[f]), cc);
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                const double d = bcs_euler::dot3(g[k], dx);
+                double r = 1.0;
+                if (d > 1e-300) r = (qmax.v[k] - qc.v[k]) / d;
+                else if (d < -1e-300) r = (qmin.v[k] - qc.v[k]) / d;
+                ps[k] = mind(ps[k], mind(1.0, r));
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 5; ++k) psi[5 * static_cast<size_t>(c) + k] = ps[k];
+}
+
+__global__ void k_mu_faces(int nf, const int* __restrict__ owner, const int* __restrict__ neigh,
+                           const double* __restrict__ cen, const double* __restrict__ fx, const double* __restrict__ q,
+                           const double* __restrict__ grad, const double* __restrict__ psi, double* fsL, double* fsR) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= nf) return;
+    const int o = owner[f], nb = neigh[f];
+    const V3 xf = face_centre(cen, fx, f, o, nb);
+    const V3 dL = bcs_euler::sub(xf, load_v3(cen, o)), dR = bcs_euler::sub(xf, load_v3(cen, nb));
+    Prim L = load_prim(q, o), R = load_prim(q, nb);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        L.v[k] += psi[5 * static_cast<size_t>(o) + k] * bcs_euler::dot3(load_v3(grad, 5 * o + k), dL);
+        R.v[k] += psi[5 * static_cast<size_t>(nb) + k] * bcs_euler::dot3(load_v3(grad, 5 * nb + k), dR);
+    }
+    if (!(L.v[0] > 0.0 && L.v[4] > 0.0) || !(R.v[0] > 0.0 && R.v[4] > 0.0)) {  // physical() (euler.hpp:29)
+        L = load_prim(q, o);
+        R = load_prim(q, nb);
+    }
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        fsL[5 * static_cast<size_t>(f) + k] = L.v[k];
+        fsR[5 * static_cast<size_t>(f) + k] = R.v[k];
+    }
+}
+
 // diagonal block, spectral-radius sum and residual of cell c
 __global__ void __launch_bounds__(128) k_asm_cells(int nc, int nf, const int* __restrict__ owner,
                                                    const int* __restrict__ neigh, const double* __restrict__ area,
                                                    const int* __restrict__ cfo, const int* __restrict__ cfl,
                                                    const int* __restrict__ bco, const double* __restrict__ barea,
-                                                   const int* __restrict__ bkind,
+                                                   const int* __restrict__ bkind, const double* __restrict__ fsL,
+                                                   const double* __restrict__ fsR,
                                                    const double* __restrict__ q, const double* __restrict__ qinf,
                                                    double cfl_num, const int* __restrict__ inv, double* vals,
                                                    double* rhs) {
@@ -137,7 +243,10 @@ __global__ void __launch_bounds__(128) k_asm_cells(int nc, int nf, const int* __
             for (int cc = 0; cc < 5; ++cc)
                 D[r * 5 + cc] = __dadd_rn(D[r * 5 + cc], __dadd_rn(__dmul_rn(scale, J[r * 5 + cc]), r == cc ? lamScale : 0.0));
         lamSum = __dadd_rn(lamSum, __dmul_rn(lam, S));
-        bcs_euler::roe(qo, qn, n, fl);
+        if (fsL)  // second order: the reconstructed face states (computeResidual, euler.cpp:364-374)
+            bcs_euler::roe(load_prim(fsL, f), load_prim(fsR, f), n, fl);
+        else
+            bcs_euler::roe(qo, qn, n, fl);
 #pragma unroll
         for (int k = 0; k < 5; ++k) res[k] = own ? __dsub_rn(res[k], __dmul_rn(S, fl[k])) : __dadd_rn(res[k], __dmul_rn(S, fl[k]));
     }
@@ -181,8 +290,6 @@ __global__ void __launch_bounds__(128) k_asm_cells(int nc, int nf, const int* __
 // patches: D = V / momentumDiagCoeff(state, phi) and the least-squares
 // pressure gradient per cell, then the face blocks and the cell blocks.
 constexpr int kP = 3;
-__device__ __forceinline__ double maxd(double a, double b) { return a < b ? b : a; }  // std::max
-__device__ __forceinline__ double mind(double a, double b) { return b < a ? b : a; }  // std::min
 
 struct CoupledGeom {
     const int *owner, *neigh, *cfo, *cf, *bco;
@@ -343,12 +450,21 @@ void assemble_inverse_src(int nnzb, const int* src, int* inv, cudaStream_t s) {
     count_launch();
 }
 
+void assemble_euler_muscl(int nc, int nf, const int* owner, const int* neigh, const int* cfo, const int* cfl,
+                          const double* cen, const double* fx, const double* q, int limiter, double* grad, double* psi,
+                          double* fsL, double* fsR, cudaStream_t s) {
+    k_mu_cells<<<(nc + 127) / 128, 128, 0, s>>>(nc, owner, neigh, cfo, cfl, cen, fx, q, limiter, grad, psi);
+    if (nf > 0) k_mu_faces<<<(nf + 255) / 256, 256, 0, s>>>(nf, owner, neigh, cen, fx, q, grad, psi, fsL, fsR);
+    count_launch(nf > 0 ? 2 : 1);
+}
+
 void assemble_euler(int nc, int nf, const int* owner, const int* neigh, const double* area, const int* cfo,
-                    const int* cfl, const int* bco, const double* barea, const int* bkind, const double* q,
-                    const double* qinf, double cfl_num, const int* inv, double* vals, double* rhs, cudaStream_t s) {
+                    const int* cfl, const int* bco, const double* barea, const int* bkind, const double* fsL,
+                    const double* fsR, const double* q, const double* qinf, double cfl_num, const int* inv,
+                    double* vals, double* rhs, cudaStream_t s) {
     if (nf > 0) k_asm_faces<<<(nf + 255) / 256, 256, 0, s>>>(nc, nf, owner, neigh, area, q, inv, vals);
-    k_asm_cells<<<(nc + 127) / 128, 128, 0, s>>>(nc, nf, owner, neigh, area, cfo, cfl, bco, barea, bkind, q, qinf,
-                                                 cfl_num, inv, vals, rhs);
+    k_asm_cells<<<(nc + 127) / 128, 128, 0, s>>>(nc, nf, owner, neigh, area, cfo, cfl, bco, barea, bkind, fsL, fsR,
+                                                 q, qinf, cfl_num, inv, vals, rhs);
     count_launch(nf > 0 ? 2 : 1);
 }
 

@@ -70,3 +70,25 @@ def test_hex_patch_kinds_layout():
     _, bcell, _, _, _ = gen.hex_euler_inputs(5, 4, 3)
     assert k.size == bcell.size
     assert np.array_equal(np.bincount(k), [12, 12, 15, 15, 20, 20])
+
+
+def test_euler_muscl_reference_changes_only_rhs(ref):
+    """musclReconstruct feeds only computeResidual (euler.cpp:361-389): with
+    MUSCL the reference's matrix is the first-order one, the right-hand side
+    differs, and the limiter matters."""
+    k = [0, 1, 2, 3, 4, 5]
+    first = ref.gen_euler_kinds(6, 5, 4, k)
+    plain = ref.gen_euler_kinds(6, 5, 4, k, recon=1)
+    bj = ref.gen_euler_kinds(6, 5, 4, k, recon=2)
+    for i in (2, 3, 4):
+        assert first[i].tobytes() == plain[i].tobytes() == bj[i].tobytes()
+    assert first[5].tobytes() != plain[5].tobytes() and plain[5].tobytes() != bj[5].tobytes()
+
+
+def test_hex_geometry_shared_by_both_generators():
+    """The MUSCL device test takes face_fx / cell_centroid from the coupled
+    inputs: both generators build the same mesh."""
+    area, bcell, barea, q, q_inf = gen.hex_euler_inputs(5, 4, 3, scramble_seed=2, poly_seed=1)
+    d = gen.hex_coupled_inputs(5, 4, 3, scramble_seed=2, poly_seed=1)
+    assert area.tobytes() == d["face_area"].tobytes()
+    assert bcell.tobytes() == d["bface_cell"].tobytes() and barea.tobytes() == d["bface_area"].tobytes()
