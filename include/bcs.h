@@ -239,18 +239,23 @@ bcs_status bcs_assemble_euler_patches(bcs_ctx* ctx, int n_cells, int n_faces, co
                                       const int32_t* neighbour, const double* face_area, int n_bfaces,
                                       const int32_t* bface_cell, const double* bface_area, const int32_t* bface_kind,
                                       const double* q, const double* q_inf, double cfl, double* rhs);
-/* bcs_assemble_euler_patches with second-order MUSCL face states in the
- * residual (musclReconstruct, euler.cpp:236-312: least-squares primitive
- * gradients :205-234, limiter 0 none / 1 Barth-Jespersen, first order where a
- * reconstructed state is non-physical); the Jacobian stays first order as in
- * assembleJacobian.  face_fx: owner-side weight per internal face (face
- * centre = fx c_owner + (1 - fx) c_neighbour, mesh.hpp:55-59);
- * cell_centroid: 3 per cell. */
-bcs_status bcs_assemble_euler_muscl(bcs_ctx* ctx, int n_cells, int n_faces, const int32_t* owner,
-                                    const int32_t* neighbour, const double* face_area, const double* face_fx,
-                                    const double* cell_centroid, int n_bfaces, const int32_t* bface_cell,
-                                    const double* bface_area, const int32_t* bface_kind, const double* q,
-                                    const double* q_inf, int limiter, double cfl, double* rhs);
+/* The general Euler assembly: bcs_assemble_euler_patches plus the
+ * EulerCase choices that shape the residual.  recon (ReconstructionConfig,
+ * euler.hpp:62-65): 0 first order, 1 MUSCL without limiter, 2 MUSCL +
+ * Barth-Jespersen (musclReconstruct, euler.cpp:236-312: least-squares
+ * primitive gradients :205-234, first order where a reconstructed state is
+ * non-physical); flux (FluxScheme order, euler.hpp:51): 0 Roe, 1 HLLC,
+ * 2 Rusanov (riemannFlux :195-203, used on internal and boundary faces).
+ * The Jacobian stays the first-order Roe-dissipation one, as in
+ * assembleJacobian.  face_fx (owner-side weight per internal face; face
+ * centre = fx c_owner + (1 - fx) c_neighbour, mesh.hpp:55-59) and
+ * cell_centroid (3 per cell) are read only when recon > 0; bface_kind may
+ * be NULL (all farfield).  Unknown flux: "unknown flux scheme". */
+bcs_status bcs_assemble_euler_ex(bcs_ctx* ctx, int n_cells, int n_faces, const int32_t* owner,
+                                 const int32_t* neighbour, const double* face_area, const double* face_fx,
+                                 const double* cell_centroid, int n_bfaces, const int32_t* bface_cell,
+                                 const double* bface_area, const int32_t* bface_kind, const double* q,
+                                 const double* q_inf, int recon, int flux, double cfl, double* rhs);
 /* Device assembly of the 4x4 pressure-based coupled p-U system: replaces
  * assembleCoupled (incompressible.cpp:143-250: momentumDiagCoeff, least-
  * squares pressure gradients, upwind + diffusion momentum, fx-interpolated

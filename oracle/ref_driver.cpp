@@ -296,9 +296,9 @@ void ref_hex_sizes(int nx, int ny, int nz, int* nCells, int* nFaces, int* nBound
 // synthetic hex mesh, Roe, cfl 50; patchKinds (6 ints in the PatchKind
 // order, for xmin xmax ymin ymax zmin zmax) go through
 // EulerCase::patchOverride, nullptr = all farfield; recon 0 first order,
-// 1 MUSCL without limiter, 2 MUSCL + Barth-Jespersen.
+// 1 MUSCL without limiter, 2 MUSCL + Barth-Jespersen; flux in FluxScheme order.
 int ref_gen_euler_kinds(int nx, int ny, int nz, double aspect, long long scrambleSeed, long long polySeed,
-                        const int* patchKinds, int recon, int* owner, int* neigh, double* diag, double* upper, double* lower,
+                        const int* patchKinds, int recon, int flux, int* owner, int* neigh, double* diag, double* upper, double* lower,
                         double* rhs, double* centroids) {
     return guard([&] {
         const Mesh mesh = hexMesh(nx, ny, nz, aspect, scrambleSeed, PatchKind::farfield, polySeed);
@@ -307,7 +307,7 @@ int ref_gen_euler_kinds(int nx, int ny, int nz, double aspect, long long scrambl
             const char* names[6] = {"xmin", "xmax", "ymin", "ymax", "zmin", "zmax"};
             for (int p = 0; p < 6; ++p) ec.patchOverride[names[p]] = static_cast<PatchKind>(patchKinds[p]);
         }
-        ec.flux = FluxScheme::Roe;
+        ec.flux = static_cast<FluxScheme>(flux);
         ec.recon.firstOrder = recon == 0;
         ec.recon.limiter = recon == 1 ? Limiter::none : Limiter::BarthJespersen;
         ec.freestream = {1.0, 0.5, 0.1, 0.0, 1.0 / 1.4};
@@ -328,7 +328,7 @@ int ref_gen_euler_kinds(int nx, int ny, int nz, double aspect, long long scrambl
 
 int ref_gen_euler_poly(int nx, int ny, int nz, double aspect, long long scrambleSeed, long long polySeed, int* owner,
                        int* neigh, double* diag, double* upper, double* lower, double* rhs, double* centroids) {
-    return ref_gen_euler_kinds(nx, ny, nz, aspect, scrambleSeed, polySeed, nullptr, 0, owner, neigh, diag, upper, lower,
+    return ref_gen_euler_kinds(nx, ny, nz, aspect, scrambleSeed, polySeed, nullptr, 0, 0, owner, neigh, diag, upper, lower,
                                rhs, centroids);
 }
 

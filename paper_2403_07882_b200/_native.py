@@ -104,8 +104,8 @@ SIGNATURES = {
                                    c_void_p, c_void_p, c_double, c_void_p]),
     "bcs_assemble_euler_patches": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p,
                                            c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_void_p]),
-    "bcs_assemble_euler_muscl": (c_int, [c_void_p, c_int, c_int] + [c_void_p] * 5 + [c_int] + [c_void_p] * 5
-                                 + [c_int, c_double, c_void_p]),
+    "bcs_assemble_euler_ex": (c_int, [c_void_p, c_int, c_int] + [c_void_p] * 5 + [c_int] + [c_void_p] * 5
+                              + [c_int, c_int, c_double, c_void_p]),
     "bcs_assemble_coupled": (c_int, [c_void_p, c_int, c_int] + [c_void_p] * 6 + [c_int] + [c_void_p] * 6
                              + [c_double, c_int, c_double, c_void_p]),
     "bcs_solve": (c_int, [c_void_p, c_void_p, c_void_p, P(SolverConfigC), P(ReportC)]),

@@ -202,13 +202,14 @@ class Context:
 
     def assemble_euler(self, owner, neighbour, face_area, bface_cell, bface_area, q, q_inf, cfl: float,
                        out: Optional[np.ndarray] = None, bface_kind=None, muscl: Optional[str] = None,
-                       face_fx=None, cell_centroid=None) -> np.ndarray:
+                       face_fx=None, cell_centroid=None, flux: str = "roe") -> np.ndarray:
         """Device assembleJacobian + computeResidual (Roe): the matrix goes into
         this context; returns the right-hand side.  ``bface_kind``: the
         reference's PatchKind per boundary face (0 wall, 1 inlet, 2 outlet,
         3 farfield, 4 slip, 5 symmetry); None = all farfield.  ``muscl``: None
         (first order), "none" or "BarthJespersen" (ReconstructionConfig::limiter;
-        needs ``face_fx`` and ``cell_centroid``)."""
+        needs ``face_fx`` and ``cell_centroid``).  ``flux``: "roe", "hllc" or
+        "rusanov" (fluxSchemeFromString names) for the residual."""
         owner = np.ascontiguousarray(owner, np.int32)
         neighbour = np.ascontiguousarray(neighbour, np.int32)
         face_area = np.ascontiguousarray(face_area, np.float64)
@@ -218,22 +219,24 @@ class Context:
         q_inf = np.ascontiguousarray(q_inf, np.float64)
         nc = q.size // 5
         rhs = np.zeros(nc * 5) if out is None else out
-        if muscl is not None:
-            limiter = {"none": 0, "BarthJespersen": 1}.get(muscl)
-            if limiter is None:
+        if muscl is not None or flux != "roe":
+            recon = {None: 0, "none": 1, "BarthJespersen": 2}.get(muscl, -1)
+            if recon < 0:
                 raise ValueError(f"assemble_euler: unknown limiter {muscl!r}")
-            if face_fx is None or cell_centroid is None:
+            scheme = {"roe": 0, "hllc": 1, "rusanov": 2}.get(flux)
+            if scheme is None:
+                raise ValueError(f"unknown flux scheme: {flux}")
+            if recon and (face_fx is None or cell_centroid is None):
                 raise ValueError("assemble_euler: MUSCL needs face_fx and cell_centroid")
-            face_fx = np.ascontiguousarray(face_fx, np.float64)
-            cell_centroid = np.ascontiguousarray(cell_centroid, np.float64)
+            fx = None if face_fx is None else np.ascontiguousarray(face_fx, np.float64)
+            cen = None if cell_centroid is None else np.ascontiguousarray(cell_centroid, np.float64)
             bk = None if bface_kind is None else np.ascontiguousarray(bface_kind, np.int32)
             if bk is not None and bk.size != bface_cell.size:
                 raise ValueError("assemble_euler: bface_kind needs one entry per boundary face")
-            self._ck(self._lib.bcs_assemble_euler_muscl(self.h, nc, owner.size, N.ptr(owner), N.ptr(neighbour),
-                                                        N.ptr(face_area), N.ptr(face_fx), N.ptr(cell_centroid),
-                                                        bface_cell.size, N.ptr(bface_cell), N.ptr(bface_area),
-                                                        N.ptr(bk), N.ptr(q), N.ptr(q_inf), limiter, float(cfl),
-                                                        N.ptr(rhs)))
+            self._ck(self._lib.bcs_assemble_euler_ex(self.h, nc, owner.size, N.ptr(owner), N.ptr(neighbour),
+                                                     N.ptr(face_area), N.ptr(fx), N.ptr(cen), bface_cell.size,
+                                                     N.ptr(bface_cell), N.ptr(bface_area), N.ptr(bk), N.ptr(q),
+                                                     N.ptr(q_inf), recon, scheme, float(cfl), N.ptr(rhs)))
         elif bface_kind is None:
             self._ck(self._lib.bcs_assemble_euler(self.h, nc, owner.size, N.ptr(owner), N.ptr(neighbour),
                                                   N.ptr(face_area), bface_cell.size, N.ptr(bface_cell),

@@ -434,18 +434,18 @@ bcs_status bcs_assemble_euler_patches(bcs_ctx* ctx, int n_cells, int n_faces, co
     });
 }
 
-bcs_status bcs_assemble_euler_muscl(bcs_ctx* ctx, int n_cells, int n_faces, const int32_t* owner,
-                                    const int32_t* neighbour, const double* face_area, const double* face_fx,
-                                    const double* cell_centroid, int n_bfaces, const int32_t* bface_cell,
-                                    const double* bface_area, const int32_t* bface_kind, const double* q,
-                                    const double* q_inf, int limiter, double cfl, double* rhs) {
+bcs_status bcs_assemble_euler_ex(bcs_ctx* ctx, int n_cells, int n_faces, const int32_t* owner,
+                                 const int32_t* neighbour, const double* face_area, const double* face_fx,
+                                 const double* cell_centroid, int n_bfaces, const int32_t* bface_cell,
+                                 const double* bface_area, const int32_t* bface_kind, const double* q,
+                                 const double* q_inf, int recon, int flux, double cfl, double* rhs) {
     return guarded(ctx, [&] {
-        if (n_cells < 1 || n_faces < 0 || !q || !q_inf || !rhs || !cell_centroid ||
-            (n_faces && (!owner || !neighbour || !face_area || !face_fx)) || (n_bfaces && (!bface_cell || !bface_area)) ||
-            limiter < 0 || limiter > 1)
-            throw std::invalid_argument("bcs_assemble_euler_muscl: bad arguments");
+        if (n_cells < 1 || n_faces < 0 || !q || !q_inf || !rhs || (n_faces && (!owner || !neighbour || !face_area)) ||
+            (n_bfaces && (!bface_cell || !bface_area)) || recon < 0 || recon > 2 ||
+            (recon && (!cell_centroid || (n_faces && !face_fx))))
+            throw std::invalid_argument("bcs_assemble_euler_ex: bad arguments");
         eng(ctx).assembleEuler(n_cells, n_faces, owner, neighbour, face_area, n_bfaces, bface_cell, bface_area,
-                               bface_kind, q, q_inf, cfl, rhs, 1 + limiter, face_fx, cell_centroid);
+                               bface_kind, q, q_inf, cfl, rhs, recon, face_fx, cell_centroid, flux);
     });
 }
 

@@ -315,10 +315,11 @@ void Engine::assemblyBoundary(int nc, int nb, const int32_t* bcell, std::vector<
 void Engine::assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* neigh, const double* faceArea,
                            int nb, const int32_t* bcell, const double* barea, const int32_t* bkind, const double* q,
                            const double* qinf, double cfl, double* rhs, int recon, const double* faceFx,
-                           const double* cellCen) {
+                           const double* cellCen, int flux) {
     LaunchScope ls(&launches_);
     if (nb < 0) throw std::invalid_argument("bcs_assemble_euler: n_bfaces < 0");
     if (recon < 0 || recon > 2) throw std::invalid_argument("bcs_assemble_euler: unknown reconstruction");
+    if (flux < 0 || flux > 2) throw std::invalid_argument("unknown flux scheme");  // euler.cpp:202
     if (recon && (!cellCen || (nf && !faceFx)))
         throw std::invalid_argument("bcs_assemble_euler: MUSCL needs face_fx and cell_centroid");
     if (bkind)
@@ -368,7 +369,7 @@ void Engine::assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* 
                              asmMuGrad_, asmPsi_, asmFs_.p, asmFs_.p + 5 * static_cast<size_t>(nf), stream_);
     }
     assemble_euler(nc, nf, dOwner_, dNeigh_, asmArea_, asmCfo_, asmCf_, asmBco_, asmBarea_,
-                   bkind ? asmBkind_.p : nullptr, fsL, fsR, asmQ_, asmQ_.p + N, cfl, asmInv_, vals_.p, asmRhs_.p,
+                   bkind ? asmBkind_.p : nullptr, fsL, fsR, flux, asmQ_, asmQ_.p + N, cfl, asmInv_, vals_.p, asmRhs_.p,
                    stream_);
     check(cudaMemcpyAsync(rhs, asmRhs_.p, sizeof(double) * N, cudaMemcpyDeviceToHost, stream_), "D2H rhs");
     sync();

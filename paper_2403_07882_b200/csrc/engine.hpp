@@ -114,11 +114,12 @@ public:
     void uploadLdu(const double* diag, const double* upper, const double* lower, bool device_ptrs);
     // device assembly of the 5x5 density-based system (k_assemble.cu); rhs: host, 5 per cell
     // bkind: PatchKind per boundary face (0 wall .. 5 symmetry) or nullptr (all farfield);
-    // recon 0 first order, 1 MUSCL without limiter, 2 MUSCL + Barth-Jespersen (needs faceFx, cellCen)
+    // recon 0 first order, 1 MUSCL without limiter, 2 MUSCL + Barth-Jespersen (needs faceFx, cellCen);
+    // flux: the residual's riemannFlux, 0 Roe, 1 HLLC, 2 Rusanov
     void assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* neigh, const double* faceArea, int nb,
                        const int32_t* bcell, const double* barea, const int32_t* bkind, const double* q,
                        const double* qinf, double cfl, double* rhs, int recon = 0, const double* faceFx = nullptr,
-                       const double* cellCen = nullptr);
+                       const double* cellCen = nullptr, int flux = 0);
     // device assembleCoupled + pinPressure (wall / moving-wall patches); rhs: host, 4 per cell
     void assembleCoupled(int nc, int nf, const int32_t* owner, const int32_t* neigh, const double* faceArea,
                          const double* fx, const double* vol, const double* cen, int nb, const int32_t* bcell,

@@ -133,6 +133,67 @@ BCS_HD void roe(const Prim& L, const Prim& R, V3 n, double* flux) {
 }
 
 
+// ---- HLLC and Rusanov fluxes (euler.cpp:150-193), for FluxScheme::HLLC / Rusanov
+BCS_HD double soundSpeed(const Prim& q) { return sqrt(kGamma * q.v[4] / q.v[0]); }
+
+BCS_HD void primToCons(const Prim& q, double* Q) {
+    const V3 u = vel(q);
+    Q[0] = q.v[0];
+    Q[1] = q.v[0] * u.x;
+    Q[2] = q.v[0] * u.y;
+    Q[3] = q.v[0] * u.z;
+    Q[4] = q.v[4] / (kGamma - 1.0) + 0.5 * q.v[0] * dot3(u, u);
+}
+
+BCS_HD void hllc(const Prim& L, const Prim& R, V3 n, double* flux) {
+    const double unL = dot3(vel(L), n), unR = dot3(vel(R), n);
+    const double cL = soundSpeed(L), cR = soundSpeed(R);
+    const RoeAvg a = roeAvg(L, R);
+    const double unTilde = dot3(a.u, n);
+    const double x1 = unL - cL, y1 = unTilde - a.c;
+    const double sL = y1 < x1 ? y1 : x1;  // std::min
+    const double x2 = unR + cR, y2 = unTilde + a.c;
+    const double sR = x2 < y2 ? y2 : x2;  // std::max
+    if (sL >= 0.0) { physFlux(L, n, flux); return; }
+    if (sR <= 0.0) { physFlux(R, n, flux); return; }
+    const double sStar = (R.v[4] - L.v[4] + L.v[0] * unL * (sL - unL) - R.v[0] * unR * (sR - unR)) /
+                         (L.v[0] * (sL - unL) - R.v[0] * (sR - unR));
+    const Prim& K = sStar >= 0.0 ? L : R;
+    const double sK = sStar >= 0.0 ? sL : sR;
+    const double unK = sStar >= 0.0 ? unL : unR;
+    double QK[5], FK[5];
+    primToCons(K, QK);
+    physFlux(K, n, FK);
+    const double fac = K.v[0] * (sK - unK) / (sK - sStar);
+    double Qs[5];
+    Qs[0] = fac;
+    const V3 uStar = add(vel(K), scl(n, sStar - unK));
+    Qs[1] = fac * uStar.x;
+    Qs[2] = fac * uStar.y;
+    Qs[3] = fac * uStar.z;
+    Qs[4] = fac * (QK[4] / K.v[0] + (sStar - unK) * (sStar + K.v[4] / (K.v[0] * (sK - unK))));
+    for (int i = 0; i < 5; ++i) flux[i] = FK[i] + sK * (Qs[i] - QK[i]);
+}
+
+BCS_HD void rusanov(const Prim& L, const Prim& R, V3 n, double* flux) {
+    double fL[5], fR[5], QL[5], QR[5];
+    physFlux(L, n, fL);
+    physFlux(R, n, fR);
+    primToCons(L, QL);
+    primToCons(R, QR);
+    const RoeAvg a = roeAvg(L, R);
+    const double lam = fabs(dot3(a.u, n)) + a.c;
+    for (int i = 0; i < 5; ++i) flux[i] = 0.5 * (fL[i] + fR[i]) - 0.5 * lam * (QR[i] - QL[i]);
+}
+
+// riemannFlux (euler.cpp:195-203): scheme 0 Roe, 1 HLLC, 2 Rusanov (FluxScheme order)
+BCS_HD void riemann(int scheme, const Prim& L, const Prim& R, V3 n, double* flux) {
+    if (scheme == 1) hllc(L, R, n, flux);
+    else if (scheme == 2) rusanov(L, R, n, flux);
+    else roe(L, R, n, flux);
+}
+
+
 // ---- coupled p-U building blocks (incompressible.cpp:91-126) --------------
 // smallmat::luFactor + luSolve for a 3x3 (first max by strict >, no singular
 // check: the caller regularises), in place

@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(128) k_asm_cells(int nc, int nf, const int* __
                                                    const int* __restrict__ cfo, const int* __restrict__ cfl,
                                                    const int* __restrict__ bco, const double* __restrict__ barea,
                                                    const int* __restrict__ bkind, const double* __restrict__ fsL,
-                                                   const double* __restrict__ fsR,
+                                                   const double* __restrict__ fsR, int scheme,
                                                    const double* __restrict__ q, const double* __restrict__ qinf,
                                                    double cfl_num, const int* __restrict__ inv, double* vals,
                                                    double* rhs) {
@@ -244,9 +244,9 @@ __global__ void __launch_bounds__(128) k_asm_cells(int nc, int nf, const int* __
                 D[r * 5 + cc] = __dadd_rn(D[r * 5 + cc], __dadd_rn(__dmul_rn(scale, J[r * 5 + cc]), r == cc ? lamScale : 0.0));
         lamSum = __dadd_rn(lamSum, __dmul_rn(lam, S));
         if (fsL)  // second order: the reconstructed face states (computeResidual, euler.cpp:364-374)
-            bcs_euler::roe(load_prim(fsL, f), load_prim(fsR, f), n, fl);
+            bcs_euler::riemann(scheme, load_prim(fsL, f), load_prim(fsR, f), n, fl);
         else
-            bcs_euler::roe(qo, qn, n, fl);
+            bcs_euler::riemann(scheme, qo, qn, n, fl);
 #pragma unroll
         for (int k = 0; k < 5; ++k) res[k] = own ? __dsub_rn(res[k], __dmul_rn(S, fl[k])) : __dadd_rn(res[k], __dmul_rn(S, fl[k]));
     }
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(128) k_asm_cells(int nc, int nf, const int* __
             for (int cc = 0; cc < 5; ++cc)
                 D[r * 5 + cc] = __dadd_rn(D[r * 5 + cc], __dadd_rn(__dmul_rn(scale, J[r * 5 + cc]), r == cc ? lamScale : 0.0));
         lamSum = __dadd_rn(lamSum, __dmul_rn(lam, S));
-        bcs_euler::roe(qc, g, n, fl);
+        bcs_euler::riemann(scheme, qc, g, n, fl);
 #pragma unroll
         for (int k = 0; k < 5; ++k) res[k] = __dsub_rn(res[k], __dmul_rn(S, fl[k]));
     }
@@ -460,11 +460,11 @@ void assemble_euler_muscl(int nc, int nf, const int* owner, const int* neigh, co
 
 void assemble_euler(int nc, int nf, const int* owner, const int* neigh, const double* area, const int* cfo,
                     const int* cfl, const int* bco, const double* barea, const int* bkind, const double* fsL,
-                    const double* fsR, const double* q, const double* qinf, double cfl_num, const int* inv,
-                    double* vals, double* rhs, cudaStream_t s) {
+                    const double* fsR, int scheme, const double* q, const double* qinf, double cfl_num,
+                    const int* inv, double* vals, double* rhs, cudaStream_t s) {
     if (nf > 0) k_asm_faces<<<(nf + 255) / 256, 256, 0, s>>>(nc, nf, owner, neigh, area, q, inv, vals);
     k_asm_cells<<<(nc + 127) / 128, 128, 0, s>>>(nc, nf, owner, neigh, area, cfo, cfl, bco, barea, bkind, fsL, fsR,
-                                                 q, qinf, cfl_num, inv, vals, rhs);
+                                                 scheme, q, qinf, cfl_num, inv, vals, rhs);
     count_launch(nf > 0 ? 2 : 1);
 }
 

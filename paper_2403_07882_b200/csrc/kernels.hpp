@@ -119,11 +119,12 @@ unsigned long long selftest_chain(int variant, int L, int warps);  // total ns  
 // ------------------------------------------------- device assembly (§8(f))
 void assemble_inverse_src(int nnzb, const int* src, int* inv, cudaStream_t s);
 // bkind: PatchKind per boundary face in bco order, or nullptr (all farfield)
-// fsL/fsR: reconstructed face states (5 per internal face) or nullptr (first order)
+// fsL/fsR: reconstructed face states (5 per internal face) or nullptr (first order);
+// scheme: riemannFlux of the residual, 0 Roe, 1 HLLC, 2 Rusanov
 void assemble_euler(int nc, int nf, const int* owner, const int* neigh, const double* area, const int* cfo,
                     const int* cfl, const int* bco, const double* barea, const int* bkind, const double* fsL,
-                    const double* fsR, const double* q, const double* qinf, double cfl_num, const int* inv,
-                    double* vals, double* rhs, cudaStream_t s);
+                    const double* fsR, int scheme, const double* q, const double* qinf, double cfl_num,
+                    const int* inv, double* vals, double* rhs, cudaStream_t s);
 // musclReconstruct (euler.cpp:236-312): grad 15 per cell, psi 5 per cell, fsL/fsR 5 per face;
 // limiter 0 none, 1 Barth-Jespersen
 void assemble_euler_muscl(int nc, int nf, const int* owner, const int* neigh, const int* cfo, const int* cfl,

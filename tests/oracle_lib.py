@@ -174,8 +174,8 @@ class Reference:
         L.ref_gen_euler.argtypes = [c_int] * 3 + [c_double, ctypes.c_longlong] + [c_void_p] * 7
         L.ref_gen_coupled.argtypes = [c_int] * 3 + [c_double, ctypes.c_longlong] + [c_void_p] * 8
         L.ref_gen_euler_poly.argtypes = [c_int] * 3 + [c_double, ctypes.c_longlong, ctypes.c_longlong] + [c_void_p] * 7
-        L.ref_gen_euler_kinds.argtypes = ([c_int] * 3 + [c_double, ctypes.c_longlong, ctypes.c_longlong, c_void_p, c_int]
-                                          + [c_void_p] * 7)
+        L.ref_gen_euler_kinds.argtypes = ([c_int] * 3 + [c_double, ctypes.c_longlong, ctypes.c_longlong, c_void_p, c_int,
+                                           c_int] + [c_void_p] * 7)
         L.ref_gen_coupled_poly.argtypes = [c_int] * 3 + [c_double, ctypes.c_longlong, ctypes.c_longlong] + [c_void_p] * 8
         L.ref_amg_build.restype = c_void_p
         L.ref_amg_depth.argtypes = [c_void_p]
@@ -207,16 +207,17 @@ class Reference:
         assert rc == 0, self.err()
         return a
 
-    def gen_euler_kinds(self, nx, ny, nz, kinds, aspect=1.0, seed=-1, poly=-1, recon=0):
+    def gen_euler_kinds(self, nx, ny, nz, kinds, aspect=1.0, seed=-1, poly=-1, recon=0, flux=0):
         """gen_euler with EulerCase::patchOverride: kinds = 6 PatchKind values
         for the xmin xmax ymin ymax zmin zmax patches (euler.cpp:345-348);
-        recon 0 first order, 1 MUSCL (no limiter), 2 MUSCL + Barth-Jespersen."""
+        recon 0 first order, 1 MUSCL (no limiter), 2 MUSCL + Barth-Jespersen;
+        flux 0 Roe, 1 HLLC, 2 Rusanov."""
         nc, nf = self._faces(nx, ny, nz, poly)
         k = np.ascontiguousarray(kinds, np.int32)
         assert k.size == 6
         a = [np.zeros(nf, np.int32), np.zeros(nf, np.int32), np.zeros(nc * 25), np.zeros(nf * 25),
              np.zeros(nf * 25), np.zeros(nc * 5), np.zeros(nc * 3)]
-        rc = self.L.ref_gen_euler_kinds(nx, ny, nz, aspect, seed, poly, ptr(k), recon, *[ptr(x) for x in a])
+        rc = self.L.ref_gen_euler_kinds(nx, ny, nz, aspect, seed, poly, ptr(k), recon, flux, *[ptr(x) for x in a])
         assert rc == 0, self.err()
         return a
 

@@ -92,3 +92,12 @@ def test_hex_geometry_shared_by_both_generators():
     d = gen.hex_coupled_inputs(5, 4, 3, scramble_seed=2, poly_seed=1)
     assert area.tobytes() == d["face_area"].tobytes()
     assert bcell.tobytes() == d["bface_cell"].tobytes() and barea.tobytes() == d["bface_area"].tobytes()
+
+
+def test_euler_flux_schemes_reference(ref):
+    """HLLC and Rusanov change only the residual of the reference assembly."""
+    k = [0, 1, 2, 3, 4, 5]
+    sys = [ref.gen_euler_kinds(5, 4, 3, k, flux=f) for f in (0, 1, 2)]
+    for i in (2, 3, 4):
+        assert sys[0][i].tobytes() == sys[1][i].tobytes() == sys[2][i].tobytes()
+    assert len({x[5].tobytes() for x in sys}) == 3
