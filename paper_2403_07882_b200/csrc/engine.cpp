@@ -353,6 +353,8 @@ void Engine::assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* 
               "H2D barea");
     check(cudaMemcpyAsync(asmQ_.p, q, sizeof(double) * N, cudaMemcpyHostToDevice, stream_), "H2D q");
     check(cudaMemcpyAsync(asmQ_.p + N, qinf, sizeof(double) * 5, cudaMemcpyHostToDevice, stream_), "H2D qinf");
+    asmBad_.ensure(1, stream_);
+    check(cudaMemsetAsync(asmBad_.p, 0x7f, sizeof(int), stream_), "memset bad");  // 0x7f7f7f7f > any cell index
     const double *fsL = nullptr, *fsR = nullptr;
     if (recon) {  // musclReconstruct on the device (euler.cpp:236-312)
         asmFx_.ensure(static_cast<size_t>(nf) + 1, stream_);
@@ -370,10 +372,17 @@ void Engine::assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* 
     }
     assemble_euler(nc, nf, dOwner_, dNeigh_, asmArea_, asmCfo_, asmCf_, asmBco_, asmBarea_,
                    bkind ? asmBkind_.p : nullptr, fsL, fsR, flux, asmQ_, asmQ_.p + N, cfl, asmInv_, vals_.p, asmRhs_.p,
-                   stream_);
+                   asmBad_.p, stream_);
+    int firstBad = 0;
+    check(cudaMemcpyAsync(&firstBad, asmBad_.p, sizeof(int), cudaMemcpyDeviceToHost, stream_), "D2H bad");
     check(cudaMemcpyAsync(rhs, asmRhs_.p, sizeof(double) * N, cudaMemcpyDeviceToHost, stream_), "D2H rhs");
     sync();
     checkErr("assembleEuler");
+    if (firstBad < nc) {  // the values written are not a valid system
+        hasValues_ = false;
+        H_->pcKind = -1;
+        throw std::runtime_error("non-physical state in cell " + std::to_string(firstBad));
+    }
     hasValues_ = true;
     H_->pcKind = -1;  // any preconditioner built on old values is stale
 }

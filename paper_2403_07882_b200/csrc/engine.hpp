@@ -219,7 +219,7 @@ private:
     DArray<double> ldu_diag_, ldu_upper_, ldu_lower_;
     // device assembly: slot of every LDU block, cell -> faces (face order), cell -> boundary faces
     bool asmTopo_ = false;
-    DArray<int> asmInv_, asmCfo_, asmCf_, asmBco_, asmBkind_;
+    DArray<int> asmInv_, asmCfo_, asmCf_, asmBco_, asmBkind_, asmBad_;
     DArray<double> asmMuGrad_, asmPsi_, asmFs_;
     DArray<double> asmArea_, asmBarea_, asmQ_, asmRhs_, asmFx_, asmVol_, asmCen_, asmBu_, asmPhi_, asmD_, asmGrad_;
     // SolvePipeline state (engine.hpp:35-37): only the EngineCsr branch updates it

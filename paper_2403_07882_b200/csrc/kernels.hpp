@@ -120,11 +120,12 @@ unsigned long long selftest_chain(int variant, int L, int warps);  // total ns  
 void assemble_inverse_src(int nnzb, const int* src, int* inv, cudaStream_t s);
 // bkind: PatchKind per boundary face in bco order, or nullptr (all farfield)
 // fsL/fsR: reconstructed face states (5 per internal face) or nullptr (first order);
-// scheme: riemannFlux of the residual, 0 Roe, 1 HLLC, 2 Rusanov
+// scheme: riemannFlux of the residual, 0 Roe, 1 HLLC, 2 Rusanov; *firstBad = min(*firstBad, first
+// cell whose state is non-physical)
 void assemble_euler(int nc, int nf, const int* owner, const int* neigh, const double* area, const int* cfo,
                     const int* cfl, const int* bco, const double* barea, const int* bkind, const double* fsL,
                     const double* fsR, int scheme, const double* q, const double* qinf, double cfl_num,
-                    const int* inv, double* vals, double* rhs, cudaStream_t s);
+                    const int* inv, double* vals, double* rhs, int* firstBad, cudaStream_t s);
 // musclReconstruct (euler.cpp:236-312): grad 15 per cell, psi 5 per cell, fsL/fsR 5 per face;
 // limiter 0 none, 1 Barth-Jespersen
 void assemble_euler_muscl(int nc, int nf, const int* owner, const int* neigh, const int* cfo, const int* cfl,
