@@ -72,10 +72,11 @@ constexpr int kAsmT = 128;  // threads (faces / cells) per assembly CTA
 // go out one 200-byte block per 25 consecutive lanes: coalesced stores of
 // whole sectors instead of 32 scattered 8-byte stores per instruction
 // (which cost ~30% extra DRAM write and read-for-ownership traffic).
+template <int NN = 25>
 __device__ __forceinline__ void flush_blocks(const double* st, const int* slot, int count, double* vals) {
-    for (int e = threadIdx.x; e < 25 * count; e += kAsmT) {
-        const int b = e / 25;
-        vals[25 * static_cast<size_t>(slot[b]) + (e - 25 * b)] = st[e];
+    for (int e = threadIdx.x; e < NN * count; e += kAsmT) {
+        const int b = e / NN;
+        vals[NN * static_cast<size_t>(slot[b]) + (e - NN * b)] = st[e];
     }
 }
 
@@ -384,10 +385,8 @@ __global__ void k_cp_cellpre(int nc, CoupledGeom g, const double* __restrict__ p
     grad[3 * static_cast<size_t>(c) + 2] = gr.z;
 }
 
-__global__ void k_cp_faces(int nc, int nf, CoupledGeom g, const double* __restrict__ phi, const double* __restrict__ D,
-                           double nu, int pin, const int* __restrict__ inv, double* vals) {
-    const int f = blockIdx.x * blockDim.x + threadIdx.x;
-    if (f >= nf) return;
+__device__ __forceinline__ void cp_face(int f, CoupledGeom g, const double* __restrict__ phi,
+                                        const double* __restrict__ D, double nu, int pin, double* up, double* lo) {
     const int o = g.owner[f], nb = g.neigh[f];
     const V3 A = load_v3(g.area, f);
     const double S = bcs_euler::len3(A);
@@ -397,7 +396,6 @@ __global__ void k_cp_faces(int nc, int nf, CoupledGeom g, const double* __restri
     const double fx = g.fx[f];
     const double dBar = fx * D[o] + (1.0 - fx) * D[nb];
     const double c = dBar * S / nd;
-    double up[16], lo[16];
 #pragma unroll
     for (int e = 0; e < 16; ++e) up[e] = lo[e] = 0.0;
 #pragma unroll
@@ -418,20 +416,36 @@ __global__ void k_cp_faces(int nc, int nf, CoupledGeom g, const double* __restri
     if (nb == pin)
 #pragma unroll
         for (int q = 0; q < 4; ++q) lo[kP * 4 + q] = 0.0;
-    double* du = vals + 16 * static_cast<size_t>(inv[nc + f]);
-    double* dl = vals + 16 * static_cast<size_t>(inv[nc + nf + f]);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-        du[e] = up[e];
-        dl[e] = lo[e];
-    }
 }
 
-__global__ void k_cp_cells(int nc, CoupledGeom g, const double* __restrict__ phi, const double* __restrict__ D,
-                           const double* __restrict__ grad, double nu, int pin, double pinValue,
-                           const int* __restrict__ inv, double* vals, double* rhs) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= nc) return;
+// the two off-diagonal 4x4 blocks of kAsmT faces, staged and stored coalesced (flush_blocks)
+__global__ void __launch_bounds__(kAsmT) k_cp_faces(int nc, int nf, CoupledGeom g, const double* __restrict__ phi,
+                                                    const double* __restrict__ D, double nu, int pin,
+                                                    const int* __restrict__ inv, double* vals) {
+    __shared__ double su[16 * kAsmT], sl[16 * kAsmT];
+    __shared__ int slotU[kAsmT], slotL[kAsmT];
+    const int f0 = blockIdx.x * kAsmT;
+    const int f = f0 + threadIdx.x;
+    const int count = min(kAsmT, nf - f0);
+    if (f < nf) {
+        double up[16], lo[16];
+        cp_face(f, g, phi, D, nu, pin, up, lo);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            su[16 * threadIdx.x + e] = up[e];
+            sl[16 * threadIdx.x + e] = lo[e];
+        }
+        slotU[threadIdx.x] = inv[nc + f];
+        slotL[threadIdx.x] = inv[nc + nf + f];
+    }
+    __syncthreads();
+    flush_blocks<16>(su, slotU, count, vals);
+    flush_blocks<16>(sl, slotL, count, vals);
+}
+
+__device__ __forceinline__ void cp_cell(int c, CoupledGeom g, const double* __restrict__ phi,
+                                        const double* __restrict__ D, const double* __restrict__ grad, double nu,
+                                        int pin, double pinValue, double* dst, double* rdst) {
     double Dm[16], rr[4];
 #pragma unroll
     for (int e = 0; e < 16; ++e) Dm[e] = 0.0;
@@ -487,11 +501,29 @@ __global__ void k_cp_cells(int nc, CoupledGeom g, const double* __restrict__ phi
         Dm[kP * 4 + kP] = 1.0;
         rr[kP] = pinValue;
     }
-    double* dst = vals + 16 * static_cast<size_t>(inv[c]);
 #pragma unroll
     for (int e = 0; e < 16; ++e) dst[e] = Dm[e];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) rhs[4 * static_cast<size_t>(c) + q] = rr[q];
+    for (int q = 0; q < 4; ++q) rdst[q] = rr[q];
+}
+
+// diagonal 4x4 blocks and right-hand side of kAsmT cells, staged and stored coalesced
+__global__ void __launch_bounds__(kAsmT) k_cp_cells(int nc, CoupledGeom g, const double* __restrict__ phi,
+                                                    const double* __restrict__ D, const double* __restrict__ grad,
+                                                    double nu, int pin, double pinValue, const int* __restrict__ inv,
+                                                    double* vals, double* rhs) {
+    __shared__ double st[16 * kAsmT], rst[4 * kAsmT];
+    __shared__ int slot[kAsmT];
+    const int c0 = blockIdx.x * kAsmT;
+    const int c = c0 + threadIdx.x;
+    const int count = min(kAsmT, nc - c0);
+    if (c < nc) {
+        cp_cell(c, g, phi, D, grad, nu, pin, pinValue, st + 16 * threadIdx.x, rst + 4 * threadIdx.x);
+        slot[threadIdx.x] = inv[c];
+    }
+    __syncthreads();
+    flush_blocks<16>(st, slot, count, vals);
+    for (int e = threadIdx.x; e < 4 * count; e += kAsmT) rhs[4 * static_cast<size_t>(c0) + e] = rst[e];
 }
 
 }  // namespace
@@ -527,8 +559,8 @@ void assemble_coupled(int nc, int nf, const int* owner, const int* neigh, const 
                       cudaStream_t s) {
     const CoupledGeom g{owner, neigh, cfo, cf, bco, area, fx, vol, cen, barea, bu};
     k_cp_cellpre<<<(nc + 127) / 128, 128, 0, s>>>(nc, g, phi, state, nu, D, grad);
-    if (nf > 0) k_cp_faces<<<(nf + 255) / 256, 256, 0, s>>>(nc, nf, g, phi, D, nu, pin, inv, vals);
-    k_cp_cells<<<(nc + 127) / 128, 128, 0, s>>>(nc, g, phi, D, grad, nu, pin, pinValue, inv, vals, rhs);
+    if (nf > 0) k_cp_faces<<<(nf + kAsmT - 1) / kAsmT, kAsmT, 0, s>>>(nc, nf, g, phi, D, nu, pin, inv, vals);
+    k_cp_cells<<<(nc + kAsmT - 1) / kAsmT, kAsmT, 0, s>>>(nc, g, phi, D, grad, nu, pin, pinValue, inv, vals, rhs);
     count_launch(nf > 0 ? 3 : 2);
 }
 
