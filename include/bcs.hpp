@@ -146,6 +146,73 @@ public:
         return {std::move(x), std::move(out)};
     }
 
+    // Device assembleJacobian + computeResidual (euler.cpp:361-455) over the
+    // reference's own Mesh / EulerCase / PrimState types: patchOverride is
+    // resolved per patch (:345-348), the flux scheme and the reconstruction
+    // are passed through (bcs_assemble_euler_ex).  The matrix stays in this
+    // pipeline's context for solveAssembled; the right-hand side (vector-first
+    // order, like the reference's) is returned.  The device kernels carry the
+    // reference's default gas (gamma 1.4).
+    template <class Vector, class States, class Mesh, class Case>
+    Vector assembleJacobian(const States& q, const Mesh& mesh, const Case& ec, double cfl) {
+        if (ec.gas.gamma != 1.4) throw std::invalid_argument("device assembly: only gamma = 1.4 is compiled in");
+        const auto& faces = mesh.faces();
+        const int nf = static_cast<int>(faces.size()), nc = mesh.nCells();
+        if (static_cast<int>(q.size()) != nc) throw std::invalid_argument("assembleJacobian: state size mismatch");
+        std::vector<int32_t> own(nf), nei(nf), bcell, bkind;
+        std::vector<double> area(3 * static_cast<size_t>(nf)), fx(nf), cen(3 * static_cast<size_t>(nc)), barea, qv;
+        for (int f = 0; f < nf; ++f) {
+            own[f] = faces[f].owner;
+            nei[f] = faces[f].neighbour;
+            area[3 * f] = faces[f].areaVector.x;
+            area[3 * f + 1] = faces[f].areaVector.y;
+            area[3 * f + 2] = faces[f].areaVector.z;
+            fx[f] = faces[f].fx;
+        }
+        const auto& cc = mesh.cellCentroids();
+        for (int i = 0; i < nc; ++i) {
+            cen[3 * i] = cc[i].x;
+            cen[3 * i + 1] = cc[i].y;
+            cen[3 * i + 2] = cc[i].z;
+        }
+        for (const auto& patch : mesh.patches()) {
+            const auto it = ec.patchOverride.find(patch.name);
+            const int kind = static_cast<int>(it == ec.patchOverride.end() ? patch.kind : it->second);
+            for (const auto& bf : patch.faces) {
+                bcell.push_back(bf.cell);
+                bkind.push_back(kind);
+                barea.push_back(bf.areaVector.x);
+                barea.push_back(bf.areaVector.y);
+                barea.push_back(bf.areaVector.z);
+            }
+        }
+        qv.resize(5 * static_cast<size_t>(nc));
+        for (int i = 0; i < nc; ++i)
+            for (int k = 0; k < 5; ++k) qv[5 * static_cast<size_t>(i) + k] = q[i][k];
+        double qinf[5];
+        for (int k = 0; k < 5; ++k) qinf[k] = ec.freestream[k];
+        const int recon = ec.recon.firstOrder ? 0 : (static_cast<int>(ec.recon.limiter) == 0 ? 1 : 2);
+        Vector rhs(nc, 5);
+        const bcs_status st = bcs_assemble_euler_ex(
+            ctx_, nc, nf, own.data(), nei.data(), area.data(), fx.data(), cen.data(), static_cast<int>(bcell.size()),
+            bcell.data(), barea.data(), bkind.data(), qv.data(), qinf, recon, static_cast<int>(ec.flux), cfl,
+            rhs.values.data());
+        if (st != BCS_OK) throwStatus(st, bcs_last_error(ctx_));
+        return rhs;
+    }
+
+    // Krylov + preconditioner on the matrix assembled in this context
+    // (bcs_solve: the reference's solveCsr, engine.cpp:31-45).
+    template <class Report, class Vector, class Config>
+    std::pair<Vector, Report> solveAssembled(const Vector& b, const Vector& x0, const Config& cfg) {
+        Vector x = x0;
+        const bcs_solver_config c = toC(cfg);
+        bcs_report r{};
+        const bcs_status st = bcs_solve(ctx_, b.values.data(), x.values.data(), &c, &r);
+        if (st != BCS_OK) throwStatus(st, bcs_last_error(ctx_));
+        return {std::move(x), fromC<Report>(r, false)};
+    }
+
     bcs_ctx* handle() const { return ctx_; }
 
 private:
