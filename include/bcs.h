@@ -273,6 +273,17 @@ bcs_status bcs_assemble_coupled(bcs_ctx* ctx, int n_cells, int n_faces, const in
                                 const int32_t* bface_cell, const double* bface_area, const int32_t* bface_kind,
                                 const double* bface_u, const double* state, const double* phi, double nu,
                                 int pin_cell, double pin_value, double* rhs);
+/* bcs_assemble_coupled for every IncompressibleBc kind (incompressible.hpp:24-29;
+ * momentumDiagCoeff's and assembleCoupled's patch terms, incompressible.cpp:70-86,
+ * 203-247): bface_kind 0 wall, 1 moving wall, 2 inlet (velocity bface_u,
+ * known flux), 3 outlet (zero-gradient velocity, fixed pressure bface_p, one
+ * per boundary face; may be NULL when there is no outlet). */
+bcs_status bcs_assemble_coupled_ex(bcs_ctx* ctx, int n_cells, int n_faces, const int32_t* owner,
+                                   const int32_t* neighbour, const double* face_area, const double* face_fx,
+                                   const double* cell_vol, const double* cell_centroid, int n_bfaces,
+                                   const int32_t* bface_cell, const double* bface_area, const int32_t* bface_kind,
+                                   const double* bface_u, const double* bface_p, const double* state,
+                                   const double* phi, double nu, int pin_cell, double pin_value, double* rhs);
 bcs_status bcs_solve(bcs_ctx* ctx, const double* b, double* x, const bcs_solver_config* cfg, bcs_report* report);
 bcs_status bcs_solve_device(bcs_ctx* ctx, const double* d_b, double* d_x, const bcs_solver_config* cfg,
                             bcs_report* report);

@@ -358,6 +358,36 @@ int ref_gen_coupled_poly(int nx, int ny, int nz, double aspect, long long scramb
     });
 }
 
+// the same coupled system with one IncompressibleBc per hex patch (xmin xmax
+// ymin ymax zmin zmax): kinds (Kind order), u (3 per patch), p (per patch);
+// pinCell < 0: no pinPressure; phiOut: the Rhie-Chow face fluxes assembled with.
+int ref_gen_coupled_bcs(int nx, int ny, int nz, double aspect, long long scrambleSeed, long long polySeed,
+                        const int* kinds, const double* u, const double* p, int pinCell, int* owner, int* neigh,
+                        double* diag, double* upper, double* lower, double* rhs, double* x0, double* centroids,
+                        double* phiOut) {
+    return guard([&] {
+        const Mesh mesh = hexMesh(nx, ny, nz, aspect, scrambleSeed, PatchKind::wall, polySeed);
+        BcMap bcs;
+        const char* names[6] = {"xmin", "xmax", "ymin", "ymax", "zmin", "zmax"};
+        for (int q = 0; q < 6; ++q)
+            bcs[names[q]] = {static_cast<IncompressibleBc::Kind>(kinds[q]), {u[3 * q], u[3 * q + 1], u[3 * q + 2]}, p[q]};
+        BlockVector state(mesh.nCells(), 4);
+        std::mt19937 gen(1);
+        std::uniform_real_distribution<double> U(-0.1, 0.1);
+        for (double& v : state.values) v = U(gen);
+        const FaceFluxField phi0(mesh.nInternalFaces(), 0.0);
+        const std::vector<double> a = momentumDiagCoeff(state, phi0, mesh, 0.01, bcs);
+        std::vector<double> D(mesh.nCells());
+        for (int i = 0; i < mesh.nCells(); ++i) D[i] = mesh.cellVolumes()[i] / a[i];
+        const FaceFluxField phi = rhieChowFlux(state, mesh, D);
+        auto [A, b] = assembleCoupled(state, phi, mesh, 0.01, bcs);
+        if (pinCell >= 0) pinPressure(A, b, pinCell, 0.0);
+        exportLdu(A, b, owner, neigh, diag, upper, lower, rhs, centroids);
+        std::memcpy(x0, state.values.data(), sizeof(double) * state.values.size());
+        std::memcpy(phiOut, phi.data(), sizeof(double) * phi.size());
+    });
+}
+
 int ref_gen_euler(int nx, int ny, int nz, double aspect, long long scrambleSeed, int* owner, int* neigh,
                   double* diag, double* upper, double* lower, double* rhs, double* centroids) {
     return ref_gen_euler_poly(nx, ny, nz, aspect, scrambleSeed, -1, owner, neigh, diag, upper, lower, rhs, centroids);

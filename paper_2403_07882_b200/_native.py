@@ -108,6 +108,8 @@ SIGNATURES = {
                               + [c_int, c_int, c_double, c_void_p]),
     "bcs_assemble_coupled": (c_int, [c_void_p, c_int, c_int] + [c_void_p] * 6 + [c_int] + [c_void_p] * 6
                              + [c_double, c_int, c_double, c_void_p]),
+    "bcs_assemble_coupled_ex": (c_int, [c_void_p, c_int, c_int] + [c_void_p] * 6 + [c_int] + [c_void_p] * 7
+                                + [c_double, c_int, c_double, c_void_p]),
     "bcs_solve": (c_int, [c_void_p, c_void_p, c_void_p, P(SolverConfigC), P(ReportC)]),
     "bcs_solve_device": (c_int, [c_void_p, c_void_p, c_void_p, P(SolverConfigC), P(ReportC)]),
     "bcs_residual": (c_int, [c_void_p, c_void_p, c_void_p, P(c_double)]),

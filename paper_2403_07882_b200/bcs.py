@@ -253,9 +253,12 @@ class Context:
 
     def assemble_coupled(self, owner, neighbour, face_area, face_fx, cell_vol, cell_centroid, bface_cell, bface_area,
                          bface_kind, bface_u, state, phi, nu: float, pin_cell: int = 0, pin_value: float = 0.0,
-                         out: Optional[np.ndarray] = None) -> np.ndarray:
-        """Device assembleCoupled + pinPressure (wall / moving-wall patches): the
-        matrix goes into this context; returns the right-hand side."""
+                         out: Optional[np.ndarray] = None, bface_p=None) -> np.ndarray:
+        """Device assembleCoupled + pinPressure: the matrix goes into this
+        context; returns the right-hand side.  ``bface_kind``: the
+        IncompressibleBc kind per boundary face (0 wall, 1 moving wall, 2 inlet,
+        3 outlet); ``bface_u`` the wall / inlet velocity, ``bface_p`` the outlet
+        pressure (needed when there is an outlet)."""
         i32 = lambda a: np.ascontiguousarray(a, np.int32)  # noqa: E731
         f64 = lambda a: np.ascontiguousarray(a, np.float64)  # noqa: E731
         owner, neighbour, bface_cell, bface_kind = i32(owner), i32(neighbour), i32(bface_cell), i32(bface_kind)
@@ -263,10 +266,12 @@ class Context:
         bface_area, bface_u, state, phi = f64(bface_area), f64(bface_u), f64(state), f64(phi)
         nc = cell_vol.size
         rhs = np.zeros(nc * 4) if out is None else out
-        self._ck(self._lib.bcs_assemble_coupled(
+        bp = None if bface_p is None else f64(bface_p)
+        self._ck(self._lib.bcs_assemble_coupled_ex(
             self.h, nc, owner.size, N.ptr(owner), N.ptr(neighbour), N.ptr(face_area), N.ptr(face_fx), N.ptr(cell_vol),
             N.ptr(cell_centroid), bface_cell.size, N.ptr(bface_cell), N.ptr(bface_area), N.ptr(bface_kind),
-            N.ptr(bface_u), N.ptr(state), N.ptr(phi), float(nu), int(pin_cell), float(pin_value), N.ptr(rhs)))
+            N.ptr(bface_u), N.ptr(bp), N.ptr(state), N.ptr(phi), float(nu), int(pin_cell), float(pin_value),
+            N.ptr(rhs)))
         return rhs
 
     def solve(self, b: np.ndarray, x: np.ndarray, cfg: SolverConfig) -> SolveReport:

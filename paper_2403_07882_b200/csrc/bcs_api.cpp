@@ -457,21 +457,32 @@ bcs_status bcs_assemble_euler(bcs_ctx* ctx, int n_cells, int n_faces, const int3
                                       bface_area, nullptr, q, q_inf, cfl, rhs);
 }
 
-bcs_status bcs_assemble_coupled(bcs_ctx* ctx, int n_cells, int n_faces, const int32_t* owner,
-                                const int32_t* neighbour, const double* face_area, const double* face_fx,
-                                const double* cell_vol, const double* cell_centroid, int n_bfaces,
-                                const int32_t* bface_cell, const double* bface_area, const int32_t* bface_kind,
-                                const double* bface_u, const double* state, const double* phi, double nu,
-                                int pin_cell, double pin_value, double* rhs) {
+bcs_status bcs_assemble_coupled_ex(bcs_ctx* ctx, int n_cells, int n_faces, const int32_t* owner,
+                                   const int32_t* neighbour, const double* face_area, const double* face_fx,
+                                   const double* cell_vol, const double* cell_centroid, int n_bfaces,
+                                   const int32_t* bface_cell, const double* bface_area, const int32_t* bface_kind,
+                                   const double* bface_u, const double* bface_p, const double* state,
+                                   const double* phi, double nu, int pin_cell, double pin_value, double* rhs) {
     return guarded(ctx, [&] {
         if (n_cells < 1 || n_faces < 0 || !cell_vol || !cell_centroid || !state || !rhs ||
             (n_faces && (!owner || !neighbour || !face_area || !face_fx || !phi)) ||
             (n_bfaces && (!bface_cell || !bface_area || !bface_kind || !bface_u)))
             throw std::invalid_argument("bcs_assemble_coupled: bad arguments");
         eng(ctx).assembleCoupled(n_cells, n_faces, owner, neighbour, face_area, face_fx, cell_vol, cell_centroid,
-                                 n_bfaces, bface_cell, bface_area, bface_kind, bface_u, state, phi, nu, pin_cell,
-                                 pin_value, rhs);
+                                 n_bfaces, bface_cell, bface_area, bface_kind, bface_u, bface_p, state, phi, nu,
+                                 pin_cell, pin_value, rhs);
     });
+}
+
+bcs_status bcs_assemble_coupled(bcs_ctx* ctx, int n_cells, int n_faces, const int32_t* owner,
+                                const int32_t* neighbour, const double* face_area, const double* face_fx,
+                                const double* cell_vol, const double* cell_centroid, int n_bfaces,
+                                const int32_t* bface_cell, const double* bface_area, const int32_t* bface_kind,
+                                const double* bface_u, const double* state, const double* phi, double nu,
+                                int pin_cell, double pin_value, double* rhs) {
+    return bcs_assemble_coupled_ex(ctx, n_cells, n_faces, owner, neighbour, face_area, face_fx, cell_vol,
+                                   cell_centroid, n_bfaces, bface_cell, bface_area, bface_kind, bface_u, nullptr,
+                                   state, phi, nu, pin_cell, pin_value, rhs);
 }
 
 bcs_status bcs_solve(bcs_ctx* ctx, const double* b, double* x, const bcs_solver_config* cfg, bcs_report* report) {

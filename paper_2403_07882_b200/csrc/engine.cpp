@@ -387,27 +387,35 @@ void Engine::assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* 
     H_->pcKind = -1;  // any preconditioner built on old values is stale
 }
 
-// assembleCoupled + pinPressure (incompressible.cpp:143-264) on the device,
-// wall / moving-wall patches (bkind 0 / 1, wall velocity bu)
+// assembleCoupled + pinPressure (incompressible.cpp:143-264) on the device:
+// IncompressibleBc kinds per boundary face (0 wall, 1 moving wall, 2 inlet,
+// 3 outlet), velocity bu (moving wall / inlet), pressure bp (outlet)
 void Engine::assembleCoupled(int nc, int nf, const int32_t* owner, const int32_t* neigh, const double* faceArea,
                              const double* fx, const double* vol, const double* cen, int nb, const int32_t* bcell,
-                             const double* barea, const int32_t* bkind, const double* bu, const double* state,
-                             const double* phi, double nu, int pinCell, double pinValue, double* rhs) {
+                             const double* barea, const int32_t* bkind, const double* bu, const double* bp,
+                             const double* state, const double* phi, double nu, int pinCell, double pinValue,
+                             double* rhs) {
     LaunchScope ls(&launches_);
     if (nb < 0) throw std::invalid_argument("bcs_assemble_coupled: n_bfaces < 0");
-    for (int b = 0; b < nb; ++b)
-        if (bkind[b] != 0 && bkind[b] != 1)
-            throw std::invalid_argument("bcs_assemble_coupled: only wall (0) and moving-wall (1) patches");
+    for (int b = 0; b < nb; ++b) {
+        if (bkind[b] < 0 || bkind[b] > 3)
+            throw std::invalid_argument("bcs_assemble_coupled: unknown boundary kind " + std::to_string(bkind[b]));
+        if (bkind[b] == 3 && !bp) throw std::invalid_argument("bcs_assemble_coupled: outlet patches need bface_p");
+    }
     if (pinCell >= nc) throw std::invalid_argument("bcs_assemble_coupled: pin cell out of range");
     assemblyTopology(nc, nf, 4, owner, neigh);
     std::vector<int> border;
     assemblyBoundary(nc, nb, bcell, border);
-    std::vector<double> ba(3 * static_cast<size_t>(nb)), bv(3 * static_cast<size_t>(nb));
-    for (int k = 0; k < nb; ++k)
+    std::vector<double> ba(3 * static_cast<size_t>(nb)), bv(3 * static_cast<size_t>(nb)), bps(nb, 0.0);
+    std::vector<int> bks(nb);
+    for (int k = 0; k < nb; ++k) {
         for (int d = 0; d < 3; ++d) {
             ba[3 * static_cast<size_t>(k) + d] = barea[3 * static_cast<size_t>(border[k]) + d];
             bv[3 * static_cast<size_t>(k) + d] = bu[3 * static_cast<size_t>(border[k]) + d];
         }
+        bks[k] = bkind[border[k]];
+        if (bp) bps[k] = bp[border[k]];
+    }
     const size_t N = static_cast<size_t>(nc) * 4;
     asmArea_.ensure(3 * static_cast<size_t>(nf) + 3, stream_);
     asmFx_.ensure(static_cast<size_t>(nf) + 1, stream_);
@@ -416,6 +424,8 @@ void Engine::assembleCoupled(int nc, int nf, const int32_t* owner, const int32_t
     asmCen_.ensure(3 * static_cast<size_t>(nc), stream_);
     asmBarea_.ensure(ba.size() + 3, stream_);
     asmBu_.ensure(bv.size() + 3, stream_);
+    asmBkind_.ensure(bks.size() + 1, stream_);
+    asmBp_.ensure(bps.size() + 1, stream_);
     asmQ_.ensure(N, stream_);
     asmD_.ensure(nc, stream_);
     asmGrad_.ensure(3 * static_cast<size_t>(nc), stream_);
@@ -431,10 +441,14 @@ void Engine::assembleCoupled(int nc, int nf, const int32_t* owner, const int32_t
         check(cudaMemcpyAsync(asmBarea_.p, ba.data(), sizeof(double) * ba.size(), cudaMemcpyHostToDevice, stream_),
               "H2D barea");
         check(cudaMemcpyAsync(asmBu_.p, bv.data(), sizeof(double) * bv.size(), cudaMemcpyHostToDevice, stream_), "H2D bu");
+        check(cudaMemcpyAsync(asmBkind_.p, bks.data(), sizeof(int) * bks.size(), cudaMemcpyHostToDevice, stream_),
+              "H2D bkind");
+        check(cudaMemcpyAsync(asmBp_.p, bps.data(), sizeof(double) * bps.size(), cudaMemcpyHostToDevice, stream_),
+              "H2D bp");
     }
     check(cudaMemcpyAsync(asmQ_.p, state, sizeof(double) * N, cudaMemcpyHostToDevice, stream_), "H2D state");
     assemble_coupled(nc, nf, dOwner_, dNeigh_, asmArea_, asmFx_, asmVol_, asmCen_, asmCfo_, asmCf_, asmBco_, asmBarea_,
-                     asmBu_, asmQ_, asmPhi_, nu, pinCell, pinValue, asmInv_, asmD_.p, asmGrad_.p, vals_.p, asmRhs_.p,
+                     asmBu_, asmBkind_, asmBp_, asmQ_, asmPhi_, nu, pinCell, pinValue, asmInv_, asmD_.p, asmGrad_.p, vals_.p, asmRhs_.p,
                      stream_);
     check(cudaMemcpyAsync(rhs, asmRhs_.p, sizeof(double) * N, cudaMemcpyDeviceToHost, stream_), "D2H rhs");
     sync();

@@ -123,8 +123,9 @@ public:
     // device assembleCoupled + pinPressure (wall / moving-wall patches); rhs: host, 4 per cell
     void assembleCoupled(int nc, int nf, const int32_t* owner, const int32_t* neigh, const double* faceArea,
                          const double* fx, const double* vol, const double* cen, int nb, const int32_t* bcell,
-                         const double* barea, const int32_t* bkind, const double* bu, const double* state,
-                         const double* phi, double nu, int pinCell, double pinValue, double* rhs);
+                         const double* barea, const int32_t* bkind, const double* bu, const double* bp,
+                         const double* state, const double* phi, double nu, int pinCell, double pinValue,
+                         double* rhs);
     void assemblyTopology(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh);
     // boundary faces grouped per cell (patch order kept): offsets and the permutation
     void assemblyBoundary(int nc, int nb, const int32_t* bcell, std::vector<int>& order);
@@ -220,7 +221,7 @@ private:
     // device assembly: slot of every LDU block, cell -> faces (face order), cell -> boundary faces
     bool asmTopo_ = false;
     DArray<int> asmInv_, asmCfo_, asmCf_, asmBco_, asmBkind_, asmBad_;
-    DArray<double> asmMuGrad_, asmPsi_, asmFs_;
+    DArray<double> asmMuGrad_, asmPsi_, asmFs_, asmBp_;
     DArray<double> asmArea_, asmBarea_, asmQ_, asmRhs_, asmFx_, asmVol_, asmCen_, asmBu_, asmPhi_, asmD_, asmGrad_;
     // SolvePipeline state (engine.hpp:35-37): only the EngineCsr branch updates it
     bool pipeHasSetup_ = false;

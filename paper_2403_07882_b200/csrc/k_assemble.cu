@@ -347,6 +347,8 @@ constexpr int kP = 3;
 struct CoupledGeom {
     const int *owner, *neigh, *cfo, *cf, *bco;
     const double *area, *fx, *vol, *cen, *barea, *bu;
+    const int* bkind;   // IncompressibleBc::Kind per boundary face: 0 wall, 1 moving wall, 2 inlet, 3 outlet
+    const double* bp;   // outlet pressure per boundary face
 };
 
 __global__ void k_cp_cellpre(int nc, CoupledGeom g, const double* __restrict__ phi, const double* __restrict__ state,
@@ -372,11 +374,20 @@ __global__ void k_cp_cellpre(int nc, CoupledGeom g, const double* __restrict__ p
         const int j = own ? nb : o;
         bcs_euler::lsqAccumulate(bcs_euler::sub(load_v3(g.cen, j), cc), state[4 * static_cast<size_t>(j) + kP] - pc, G, b);
     }
-    for (int k = g.bco[c]; k < g.bco[c + 1]; ++k) {  // walls: nu S / wallDistance
+    for (int k = g.bco[c]; k < g.bco[c + 1]; ++k) {  // momentumDiagCoeff's patch terms (incompressible.cpp:70-86)
         const V3 A = load_v3(g.barea, k);
         const double S = bcs_euler::len3(A);
         const double db = g.vol[c] / (2.0 * bcs_euler::len3(A));
-        aP = __dadd_rn(aP, nu * S / db);
+        const int kind = g.bkind[k];
+        if (kind == 3) {  // outlet: outflow through the face
+            const V3 uc{state[4 * static_cast<size_t>(c)], state[4 * static_cast<size_t>(c) + 1],
+                        state[4 * static_cast<size_t>(c) + 2]};
+            aP = __dadd_rn(aP, maxd(bcs_euler::dot3(A, uc), 0.0));
+        } else if (kind == 2) {  // inlet: diffusion + inflow
+            aP = __dadd_rn(aP, nu * S / db + maxd(bcs_euler::dot3(A, load_v3(g.bu, k)), 0.0));
+        } else {  // walls: nu S / wallDistance
+            aP = __dadd_rn(aP, nu * S / db);
+        }
     }
     D[c] = g.vol[c] / aP;
     const V3 gr = bcs_euler::lsqFinish(G, b);
@@ -444,8 +455,9 @@ __global__ void __launch_bounds__(kAsmT) k_cp_faces(int nc, int nf, CoupledGeom 
 }
 
 __device__ __forceinline__ void cp_cell(int c, CoupledGeom g, const double* __restrict__ phi,
-                                        const double* __restrict__ D, const double* __restrict__ grad, double nu,
-                                        int pin, double pinValue, double* dst, double* rdst) {
+                                        const double* __restrict__ D, const double* __restrict__ grad,
+                                        const double* __restrict__ state, double nu, int pin, double pinValue,
+                                        double* dst, double* rdst) {
     double Dm[16], rr[4];
 #pragma unroll
     for (int e = 0; e < 16; ++e) Dm[e] = 0.0;
@@ -482,17 +494,45 @@ __device__ __forceinline__ void cp_cell(int c, CoupledGeom g, const double* __re
         if (own) rr[kP] += ev;
         else rr[kP] -= ev;
     }
-    for (int k = g.bco[c]; k < g.bco[c + 1]; ++k) {  // wall / moving wall
+    for (int k = g.bco[c]; k < g.bco[c + 1]; ++k) {  // boundary patches (incompressible.cpp:203-247)
         const V3 A = load_v3(g.barea, k);
         const double S = bcs_euler::len3(A);
         const double db = g.vol[c] / (2.0 * bcs_euler::len3(A));
-        const double gb = nu * S / db;
-        const V3 u = load_v3(g.bu, k);
+        const int kind = g.bkind[k];
+        if (kind <= 1) {  // wall / moving wall
+            const double gb = nu * S / db;
+            const V3 u = load_v3(g.bu, k);
 #pragma unroll
-        for (int r = 0; r < 3; ++r) {
-            Dm[r * 4 + r] += gb;
-            rr[r] += gb * bcs_euler::comp(u, r);
-            Dm[r * 4 + kP] += bcs_euler::comp(A, r);  // zero-gradient p
+            for (int r = 0; r < 3; ++r) {
+                Dm[r * 4 + r] += gb;
+                rr[r] += gb * bcs_euler::comp(u, r);
+                Dm[r * 4 + kP] += bcs_euler::comp(A, r);  // zero-gradient p
+            }
+        } else if (kind == 2) {  // inlet: fixed velocity, known flux
+            const double gb = nu * S / db;
+            const V3 u = load_v3(g.bu, k);
+            const double phiB = bcs_euler::dot3(A, u);
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                Dm[r * 4 + r] += gb + maxd(phiB, 0.0);
+                rr[r] += gb * bcs_euler::comp(u, r) - mind(phiB, 0.0) * bcs_euler::comp(u, r);
+                Dm[r * 4 + kP] += bcs_euler::comp(A, r);
+            }
+            rr[kP] += phiB;  // known flux, negated row
+        } else {  // outlet: zero-gradient u, fixed pressure
+            const V3 uc{state[4 * static_cast<size_t>(c)], state[4 * static_cast<size_t>(c) + 1],
+                        state[4 * static_cast<size_t>(c) + 2]};
+            const double phiB = bcs_euler::dot3(A, uc);
+            const double cb = D[c] * S / db;
+            const double pb = g.bp[k];
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                Dm[r * 4 + r] += maxd(phiB, 0.0);
+                rr[r] -= bcs_euler::comp(A, r) * pb;
+                Dm[kP * 4 + r] -= bcs_euler::comp(A, r);
+            }
+            Dm[kP * 4 + kP] -= cb;
+            rr[kP] -= cb * pb;
         }
     }
     if (c == pin) {
@@ -510,7 +550,7 @@ __device__ __forceinline__ void cp_cell(int c, CoupledGeom g, const double* __re
 // diagonal 4x4 blocks and right-hand side of kAsmT cells, staged and stored coalesced
 __global__ void __launch_bounds__(kAsmT) k_cp_cells(int nc, CoupledGeom g, const double* __restrict__ phi,
                                                     const double* __restrict__ D, const double* __restrict__ grad,
-                                                    double nu, int pin, double pinValue, const int* __restrict__ inv,
+                                                    const double* __restrict__ state, double nu, int pin, double pinValue, const int* __restrict__ inv,
                                                     double* vals, double* rhs) {
     __shared__ double st[16 * kAsmT], rst[4 * kAsmT];
     __shared__ int slot[kAsmT];
@@ -518,7 +558,7 @@ __global__ void __launch_bounds__(kAsmT) k_cp_cells(int nc, CoupledGeom g, const
     const int c = c0 + threadIdx.x;
     const int count = min(kAsmT, nc - c0);
     if (c < nc) {
-        cp_cell(c, g, phi, D, grad, nu, pin, pinValue, st + 16 * threadIdx.x, rst + 4 * threadIdx.x);
+        cp_cell(c, g, phi, D, grad, state, nu, pin, pinValue, st + 16 * threadIdx.x, rst + 4 * threadIdx.x);
         slot[threadIdx.x] = inv[c];
     }
     __syncthreads();
@@ -554,13 +594,14 @@ void assemble_euler(int nc, int nf, const int* owner, const int* neigh, const do
 
 void assemble_coupled(int nc, int nf, const int* owner, const int* neigh, const double* area, const double* fx,
                       const double* vol, const double* cen, const int* cfo, const int* cf, const int* bco,
-                      const double* barea, const double* bu, const double* state, const double* phi, double nu,
-                      int pin, double pinValue, const int* inv, double* D, double* grad, double* vals, double* rhs,
-                      cudaStream_t s) {
-    const CoupledGeom g{owner, neigh, cfo, cf, bco, area, fx, vol, cen, barea, bu};
+                      const double* barea, const double* bu, const int* bkind, const double* bp,
+                      const double* state, const double* phi, double nu, int pin, double pinValue, const int* inv,
+                      double* D, double* grad, double* vals, double* rhs, cudaStream_t s) {
+    const CoupledGeom g{owner, neigh, cfo, cf, bco, area, fx, vol, cen, barea, bu, bkind, bp};
     k_cp_cellpre<<<(nc + 127) / 128, 128, 0, s>>>(nc, g, phi, state, nu, D, grad);
     if (nf > 0) k_cp_faces<<<(nf + kAsmT - 1) / kAsmT, kAsmT, 0, s>>>(nc, nf, g, phi, D, nu, pin, inv, vals);
-    k_cp_cells<<<(nc + kAsmT - 1) / kAsmT, kAsmT, 0, s>>>(nc, g, phi, D, grad, nu, pin, pinValue, inv, vals, rhs);
+    k_cp_cells<<<(nc + kAsmT - 1) / kAsmT, kAsmT, 0, s>>>(nc, g, phi, D, grad, state, nu, pin, pinValue, inv, vals,
+                                                        rhs);
     count_launch(nf > 0 ? 3 : 2);
 }
 

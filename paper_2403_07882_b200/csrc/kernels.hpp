@@ -134,9 +134,9 @@ void assemble_euler_muscl(int nc, int nf, const int* owner, const int* neigh, co
 
 void assemble_coupled(int nc, int nf, const int* owner, const int* neigh, const double* area, const double* fx,
                       const double* vol, const double* cen, const int* cfo, const int* cf, const int* bco,
-                      const double* barea, const double* bu, const double* state, const double* phi, double nu,
-                      int pin, double pinValue, const int* inv, double* D, double* grad, double* vals, double* rhs,
-                      cudaStream_t s);
+                      const double* barea, const double* bu, const int* bkind, const double* bp,
+                      const double* state, const double* phi, double nu, int pin, double pinValue, const int* inv,
+                      double* D, double* grad, double* vals, double* rhs, cudaStream_t s);
 
 // ------------------------------------------------------------ AMG (K9-K12)
 void strengths(int n, int rows, const int* ro, const int* ci, const int* dg, const double* v, double* dn,

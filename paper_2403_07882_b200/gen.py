@@ -122,6 +122,16 @@ def hex_patch_kinds(nx: int, ny: int = None, nz: int = None, kinds=(3, 3, 3, 3, 
     return np.concatenate([np.full(n, v, np.int32) for n, v in zip(sizes, k)])
 
 
+def hex_patch_values(nx: int, ny: int = None, nz: int = None, values=None, width: int = 1) -> np.ndarray:
+    """Per-boundary-face copy of one value (width doubles) per hex patch, in
+    the patch order of the boundary faces (see hex_patch_kinds)."""
+    ny = nx if ny is None else ny
+    nz = nx if nz is None else nz
+    v = np.asarray(values, np.float64).reshape(6, width)
+    sizes = [ny * nz, ny * nz, nx * nz, nx * nz, nx * ny, nx * ny]
+    return np.concatenate([np.tile(v[i], n) for i, n in enumerate(sizes)])
+
+
 def hex_coupled_inputs(nx: int, ny: int = None, nz: int = None, aspect: float = 1.0, scramble_seed: int = -1,
                        poly_seed: int = -1) -> dict:
     """Inputs of assembleCoupled on the mesh of ``hex_coupled`` (same

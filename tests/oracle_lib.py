@@ -177,6 +177,8 @@ class Reference:
         L.ref_gen_euler_kinds.argtypes = ([c_int] * 3 + [c_double, ctypes.c_longlong, ctypes.c_longlong, c_void_p, c_int,
                                            c_int] + [c_void_p] * 7)
         L.ref_gen_coupled_poly.argtypes = [c_int] * 3 + [c_double, ctypes.c_longlong, ctypes.c_longlong] + [c_void_p] * 8
+        L.ref_gen_coupled_bcs.argtypes = ([c_int] * 3 + [c_double, ctypes.c_longlong, ctypes.c_longlong]
+                                          + [c_void_p] * 3 + [c_int] + [c_void_p] * 9)
         L.ref_amg_build.restype = c_void_p
         L.ref_amg_depth.argtypes = [c_void_p]
         L.ref_amg_level_sizes.argtypes = [c_void_p, c_int] + [ctypes.POINTER(c_int)] * 3
@@ -218,6 +220,21 @@ class Reference:
         a = [np.zeros(nf, np.int32), np.zeros(nf, np.int32), np.zeros(nc * 25), np.zeros(nf * 25),
              np.zeros(nf * 25), np.zeros(nc * 5), np.zeros(nc * 3)]
         rc = self.L.ref_gen_euler_kinds(nx, ny, nz, aspect, seed, poly, ptr(k), recon, flux, *[ptr(x) for x in a])
+        assert rc == 0, self.err()
+        return a
+
+    def gen_coupled_bcs(self, nx, ny, nz, kinds, u, p, aspect=1.0, seed=-1, poly=-1, pin=0):
+        """gen_coupled with one IncompressibleBc per hex patch (kinds: Kind
+        order wall, movingWall, inlet, outlet; u: 6x3; p: 6).  Returns owner,
+        neighbour, diag, upper, lower, rhs, state, centroids, phi."""
+        nc, nf = self._faces(nx, ny, nz, poly)
+        k = np.ascontiguousarray(kinds, np.int32)
+        uu = np.ascontiguousarray(u, np.float64).reshape(-1)
+        pp = np.ascontiguousarray(p, np.float64)
+        a = [np.zeros(nf, np.int32), np.zeros(nf, np.int32), np.zeros(nc * 16), np.zeros(nf * 16),
+             np.zeros(nf * 16), np.zeros(nc * 4), np.zeros(nc * 4), np.zeros(nc * 3), np.zeros(nf)]
+        rc = self.L.ref_gen_coupled_bcs(nx, ny, nz, aspect, seed, poly, ptr(k), ptr(uu), ptr(pp), pin,
+                                        *[ptr(x) for x in a])
         assert rc == 0, self.err()
         return a
 

@@ -101,3 +101,20 @@ def test_euler_flux_schemes_reference(ref):
     for i in (2, 3, 4):
         assert sys[0][i].tobytes() == sys[1][i].tobytes() == sys[2][i].tobytes()
     assert len({x[5].tobytes() for x in sys}) == 3
+
+
+def test_coupled_bcs_reference_hook(ref):
+    """ref_gen_coupled_bcs with the plain generator's boundary conditions (walls,
+    moving zmax lid, pin 0) reproduces ref_gen_coupled bit for bit."""
+    u = [(0, 0, 0)] * 5 + [(1.0, 0.0, 0.0)]
+    base = ref.gen_coupled(5, 4, 3)
+    same = ref.gen_coupled_bcs(5, 4, 3, [0, 0, 0, 0, 0, 1], u, [0.0] * 6)
+    assert all(a.tobytes() == b.tobytes() for a, b in zip(base, same[:8]))
+    chan = ref.gen_coupled_bcs(5, 4, 3, [2, 3, 0, 0, 0, 1], [(1, 0, 0)] + u[1:], [0, 0.5, 0, 0, 0, 0])
+    assert chan[5].tobytes() != base[5].tobytes()
+
+
+def test_hex_patch_values_layout():
+    v = gen.hex_patch_values(5, 4, 3, [(i, 10 * i, 100 * i) for i in range(6)], 3).reshape(-1, 3)
+    k = gen.hex_patch_kinds(5, 4, 3, range(6))
+    assert np.array_equal(v[:, 0], k) and np.array_equal(v[:, 2], 100 * k)
