@@ -201,6 +201,60 @@ public:
         return rhs;
     }
 
+    // Device assembleCoupled (incompressible.cpp:143-250) followed by
+    // pinPressure(pinCell, pinValue) (:252-264; pinCell < 0: none) over the
+    // reference's own state / face fluxes / Mesh / BcMap (every
+    // IncompressibleBc kind).  The matrix stays in this context for
+    // solveAssembled; the right-hand side is returned.
+    template <class Vector, class Flux, class Mesh, class Bcs>
+    Vector assembleCoupled(const Vector& state, const Flux& phi, const Mesh& mesh, double nu, const Bcs& bcs,
+                           int pinCell, double pinValue = 0.0) {
+        const auto& faces = mesh.faces();
+        const int nf = static_cast<int>(faces.size()), nc = mesh.nCells();
+        if (state.nCells() != nc || state.blockSize != 4 || static_cast<int>(phi.size()) != nf)
+            throw std::invalid_argument("assembleCoupled: size mismatch");
+        std::vector<int32_t> own(nf), nei(nf), bcell, bkind;
+        std::vector<double> area(3 * static_cast<size_t>(nf)), fx(nf), cen(3 * static_cast<size_t>(nc)), barea, bu, bp;
+        for (int f = 0; f < nf; ++f) {
+            own[f] = faces[f].owner;
+            nei[f] = faces[f].neighbour;
+            area[3 * f] = faces[f].areaVector.x;
+            area[3 * f + 1] = faces[f].areaVector.y;
+            area[3 * f + 2] = faces[f].areaVector.z;
+            fx[f] = faces[f].fx;
+        }
+        const auto& cc = mesh.cellCentroids();
+        for (int i = 0; i < nc; ++i) {
+            cen[3 * i] = cc[i].x;
+            cen[3 * i + 1] = cc[i].y;
+            cen[3 * i + 2] = cc[i].z;
+        }
+        for (const auto& patch : mesh.patches()) {
+            const auto it = bcs.find(patch.name);
+            if (it == bcs.end())  // bcFor (incompressible.cpp:43-48)
+                throw std::invalid_argument("no boundary condition for patch '" + patch.name + "'");
+            const auto& bc = it->second;
+            for (const auto& bf : patch.faces) {
+                bcell.push_back(bf.cell);
+                bkind.push_back(static_cast<int32_t>(bc.kind));
+                barea.push_back(bf.areaVector.x);
+                barea.push_back(bf.areaVector.y);
+                barea.push_back(bf.areaVector.z);
+                bu.push_back(bc.u.x);
+                bu.push_back(bc.u.y);
+                bu.push_back(bc.u.z);
+                bp.push_back(bc.p);
+            }
+        }
+        Vector rhs(nc, 4);
+        const bcs_status st = bcs_assemble_coupled_ex(
+            ctx_, nc, nf, own.data(), nei.data(), area.data(), fx.data(), mesh.cellVolumes().data(), cen.data(),
+            static_cast<int>(bcell.size()), bcell.data(), barea.data(), bkind.data(), bu.data(), bp.data(),
+            state.values.data(), phi.data(), nu, pinCell, pinValue, rhs.values.data());
+        if (st != BCS_OK) throwStatus(st, bcs_last_error(ctx_));
+        return rhs;
+    }
+
     // Krylov + preconditioner on the matrix assembled in this context
     // (bcs_solve: the reference's solveCsr, engine.cpp:31-45).
     template <class Report, class Vector, class Config>
