@@ -190,6 +190,8 @@ Engine::~Engine() {
         rel(P.H.dense); rel(P.H.dpiv);
     }
     cudaStreamSynchronize(stream_);
+    for (void* p : stage_) cudaFreeHost(p);
+    for (cudaEvent_t e : stageEv_) cudaEventDestroy(e);
     if (hStatus_) cudaFreeHost(hStatus_);
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
@@ -347,11 +349,11 @@ void Engine::assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* 
     asmQ_.ensure(N + 5, stream_);
     asmRhs_.ensure(N, stream_);
     if (nf)
-        check(cudaMemcpyAsync(asmArea_.p, faceArea, sizeof(double) * 3 * nf, cudaMemcpyHostToDevice, stream_), "H2D area");
+        h2d(asmArea_.p, faceArea, sizeof(double) * 3 * nf, "H2D area");
     if (nb)
         check(cudaMemcpyAsync(asmBarea_.p, bsorted.data(), sizeof(double) * bsorted.size(), cudaMemcpyHostToDevice, stream_),
               "H2D barea");
-    check(cudaMemcpyAsync(asmQ_.p, q, sizeof(double) * N, cudaMemcpyHostToDevice, stream_), "H2D q");
+    h2d(asmQ_.p, q, sizeof(double) * N, "H2D q");
     check(cudaMemcpyAsync(asmQ_.p + N, qinf, sizeof(double) * 5, cudaMemcpyHostToDevice, stream_), "H2D qinf");
     asmBad_.ensure(1, stream_);
     check(cudaMemsetAsync(asmBad_.p, 0x7f, sizeof(int), stream_), "memset bad");  // 0x7f7f7f7f > any cell index
@@ -363,8 +365,8 @@ void Engine::assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* 
         asmPsi_.ensure(5 * static_cast<size_t>(nc), stream_);
         asmFs_.ensure(10 * static_cast<size_t>(nf) + 1, stream_);
         if (nf)
-            check(cudaMemcpyAsync(asmFx_.p, faceFx, sizeof(double) * nf, cudaMemcpyHostToDevice, stream_), "H2D fx");
-        check(cudaMemcpyAsync(asmCen_.p, cellCen, sizeof(double) * 3 * nc, cudaMemcpyHostToDevice, stream_), "H2D cen");
+            h2d(asmFx_.p, faceFx, sizeof(double) * nf, "H2D fx");
+        h2d(asmCen_.p, cellCen, sizeof(double) * 3 * nc, "H2D cen");
         fsL = asmFs_.p;
         fsR = asmFs_.p + 5 * static_cast<size_t>(nf);
         assemble_euler_muscl(nc, nf, dOwner_, dNeigh_, asmCfo_, asmCf_, asmCen_, asmFx_, asmQ_, recon == 2 ? 1 : 0,
@@ -375,8 +377,7 @@ void Engine::assembleEuler(int nc, int nf, const int32_t* owner, const int32_t* 
                    asmBad_.p, stream_);
     int firstBad = 0;
     check(cudaMemcpyAsync(&firstBad, asmBad_.p, sizeof(int), cudaMemcpyDeviceToHost, stream_), "D2H bad");
-    check(cudaMemcpyAsync(rhs, asmRhs_.p, sizeof(double) * N, cudaMemcpyDeviceToHost, stream_), "D2H rhs");
-    sync();
+    d2h(rhs, asmRhs_.p, sizeof(double) * N, "D2H rhs");  // synchronous
     checkErr("assembleEuler");
     if (firstBad < nc) {  // the values written are not a valid system
         hasValues_ = false;
@@ -431,12 +432,12 @@ void Engine::assembleCoupled(int nc, int nf, const int32_t* owner, const int32_t
     asmGrad_.ensure(3 * static_cast<size_t>(nc), stream_);
     asmRhs_.ensure(N, stream_);
     if (nf) {
-        check(cudaMemcpyAsync(asmArea_.p, faceArea, sizeof(double) * 3 * nf, cudaMemcpyHostToDevice, stream_), "H2D area");
-        check(cudaMemcpyAsync(asmFx_.p, fx, sizeof(double) * nf, cudaMemcpyHostToDevice, stream_), "H2D fx");
-        check(cudaMemcpyAsync(asmPhi_.p, phi, sizeof(double) * nf, cudaMemcpyHostToDevice, stream_), "H2D phi");
+        h2d(asmArea_.p, faceArea, sizeof(double) * 3 * nf, "H2D area");
+        h2d(asmFx_.p, fx, sizeof(double) * nf, "H2D fx");
+        h2d(asmPhi_.p, phi, sizeof(double) * nf, "H2D phi");
     }
     check(cudaMemcpyAsync(asmVol_.p, vol, sizeof(double) * nc, cudaMemcpyHostToDevice, stream_), "H2D vol");
-    check(cudaMemcpyAsync(asmCen_.p, cen, sizeof(double) * 3 * nc, cudaMemcpyHostToDevice, stream_), "H2D cen");
+    h2d(asmCen_.p, cen, sizeof(double) * 3 * nc, "H2D cen");
     if (nb) {
         check(cudaMemcpyAsync(asmBarea_.p, ba.data(), sizeof(double) * ba.size(), cudaMemcpyHostToDevice, stream_),
               "H2D barea");
@@ -446,15 +447,116 @@ void Engine::assembleCoupled(int nc, int nf, const int32_t* owner, const int32_t
         check(cudaMemcpyAsync(asmBp_.p, bps.data(), sizeof(double) * bps.size(), cudaMemcpyHostToDevice, stream_),
               "H2D bp");
     }
-    check(cudaMemcpyAsync(asmQ_.p, state, sizeof(double) * N, cudaMemcpyHostToDevice, stream_), "H2D state");
+    h2d(asmQ_.p, state, sizeof(double) * N, "H2D state");
     assemble_coupled(nc, nf, dOwner_, dNeigh_, asmArea_, asmFx_, asmVol_, asmCen_, asmCfo_, asmCf_, asmBco_, asmBarea_,
                      asmBu_, asmBkind_, asmBp_, asmQ_, asmPhi_, nu, pinCell, pinValue, asmInv_, asmD_.p, asmGrad_.p, vals_.p, asmRhs_.p,
                      stream_);
-    check(cudaMemcpyAsync(rhs, asmRhs_.p, sizeof(double) * N, cudaMemcpyDeviceToHost, stream_), "D2H rhs");
-    sync();
+    d2h(rhs, asmRhs_.p, sizeof(double) * N, "D2H rhs");  // synchronous
     checkErr("assembleCoupled");
     hasValues_ = true;
     H_->pcKind = -1;
+}
+
+// Staged H2D (pinned streaming upload): kWorkers host
+// threads each own two pinned kChunk slots; worker w copies chunks w, w + W,
+// w + 2W, ... of the source into its next free slot (waiting for that slot's
+// previous DMA through its event) and enqueues the DMA on the engine stream.
+// Chunks land at disjoint offsets, so their order on the stream is free; work
+// enqueued after h2d returns sees every chunk.
+namespace {
+constexpr size_t kStageChunk = size_t(8) << 20;
+constexpr int kStageWorkers = 8, kStageSlots = 2;
+}  // namespace
+
+bool Engine::hostPinned(const void* p) const {
+    cudaPointerAttributes at{};
+    const bool pinned = cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    cudaGetLastError();  // a pageable pointer is not an error worth keeping
+    return pinned;
+}
+
+void Engine::ensureStaging() {
+    if (!stage_.empty()) return;
+    for (int k = 0; k < kStageWorkers * kStageSlots; ++k) {
+        void* p = nullptr;
+        check(cudaHostAlloc(&p, kStageChunk, cudaHostAllocPortable), "cudaHostAlloc staging");
+        stage_.push_back(p);
+        cudaEvent_t e;
+        check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate staging");
+        stageEv_.push_back(e);
+    }
+}
+
+void Engine::h2d(void* dst, const void* src, size_t bytes, const char* what) {
+    if (!bytes) return;
+    constexpr size_t kChunk = kStageChunk;
+    constexpr int kWorkers = kStageWorkers, kSlots = kStageSlots;
+    if (bytes <= kChunk || hostPinned(src)) {
+        check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_), what);
+        return;
+    }
+    ensureStaging();
+    const size_t nChunks = (bytes + kChunk - 1) / kChunk;
+    const int workers = static_cast<int>(std::min<size_t>(kWorkers, nChunks));
+    std::vector<cudaError_t> errs(workers, cudaSuccess);
+    auto work = [&](int w) {
+        cudaSetDevice(device_);
+        int j = 0;
+        for (size_t i = w; i < nChunks; i += workers, ++j) {
+            const int k = w * kSlots + (j % kSlots);
+            if (j >= kSlots) {
+                const cudaError_t e = cudaEventSynchronize(stageEv_[k]);
+                if (e != cudaSuccess) { errs[w] = e; return; }
+            }
+            const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+            std::memcpy(stage_[k], static_cast<const char*>(src) + off, len);
+            cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + off, stage_[k], len, cudaMemcpyHostToDevice,
+                                            stream_);
+            if (e == cudaSuccess) e = cudaEventRecord(stageEv_[k], stream_);
+            if (e != cudaSuccess) { errs[w] = e; return; }
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int w = 1; w < workers; ++w) pool.emplace_back(work, w);
+    work(0);
+    for (auto& t : pool) t.join();
+    for (cudaError_t e : errs) check(e, what);
+    // the staging slots are reused by the next call: drain this call's DMAs first
+    for (int k = 0; k < workers * kSlots; ++k) check(cudaEventSynchronize(stageEv_[k]), what);
+}
+
+// D2H into a pageable buffer: each worker DMAs its chunks into its pinned
+// slots (in stream order after the work that produced src) and copies them
+// out as they land.
+void Engine::d2h(void* dst, const void* src, size_t bytes, const char* what) {
+    if (!bytes) return;
+    if (bytes <= kStageChunk || hostPinned(dst)) {
+        check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream_), what);
+        sync();
+        return;
+    }
+    ensureStaging();
+    const size_t nChunks = (bytes + kStageChunk - 1) / kStageChunk;
+    const int workers = static_cast<int>(std::min<size_t>(kStageWorkers, nChunks));
+    std::vector<cudaError_t> errs(workers, cudaSuccess);
+    auto work = [&](int w) {
+        cudaSetDevice(device_);
+        for (size_t i = w; i < nChunks; i += workers) {
+            const int k = w * kStageSlots;
+            const size_t off = i * kStageChunk, len = std::min(kStageChunk, bytes - off);
+            cudaError_t e = cudaMemcpyAsync(stage_[k], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost,
+                                            stream_);
+            if (e == cudaSuccess) e = cudaEventRecord(stageEv_[k], stream_);
+            if (e == cudaSuccess) e = cudaEventSynchronize(stageEv_[k]);
+            if (e != cudaSuccess) { errs[w] = e; return; }
+            std::memcpy(static_cast<char*>(dst) + off, stage_[k], len);
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int w = 1; w < workers; ++w) pool.emplace_back(work, w);
+    work(0);
+    for (auto& t : pool) t.join();
+    for (cudaError_t e : errs) check(e, what);
 }
 
 void Engine::uploadLdu(const double* diag, const double* upper, const double* lower, bool device_ptrs) {
@@ -466,12 +568,10 @@ void Engine::uploadLdu(const double* diag, const double* upper, const double* lo
         ldu_diag_.ensure(nc_ * nn, stream_);
         ldu_upper_.ensure(nf_ * nn, stream_);
         ldu_lower_.ensure(nf_ * nn, stream_);
-        check(cudaMemcpyAsync(ldu_diag_.p, diag, sizeof(double) * nc_ * nn, cudaMemcpyHostToDevice, stream_), "H2D diag");
+        h2d(ldu_diag_.p, diag, sizeof(double) * nc_ * nn, "H2D diag");
         if (nf_) {
-            check(cudaMemcpyAsync(ldu_upper_.p, upper, sizeof(double) * nf_ * nn, cudaMemcpyHostToDevice, stream_),
-                  "H2D upper");
-            check(cudaMemcpyAsync(ldu_lower_.p, lower, sizeof(double) * nf_ * nn, cudaMemcpyHostToDevice, stream_),
-                  "H2D lower");
+            h2d(ldu_upper_.p, upper, sizeof(double) * nf_ * nn, "H2D upper");
+            h2d(ldu_lower_.p, lower, sizeof(double) * nf_ * nn, "H2D lower");
         }
         dd = ldu_diag_;
         du = ldu_upper_;
@@ -1375,10 +1475,10 @@ void Engine::distSolve(int nc, int nf, int n, const int32_t* owner, const int32_
     ldu_diag_.ensure(nc * nn, stream_);
     ldu_upper_.ensure(nf * nn, stream_);
     ldu_lower_.ensure(nf * nn, stream_);
-    check(cudaMemcpyAsync(ldu_diag_.p, diag, sizeof(double) * nc * nn, cudaMemcpyHostToDevice, stream_), "H2D");
+    h2d(ldu_diag_.p, diag, sizeof(double) * nc * nn, "H2D");
     if (nf) {
-        check(cudaMemcpyAsync(ldu_upper_.p, upper, sizeof(double) * nf * nn, cudaMemcpyHostToDevice, stream_), "H2D");
-        check(cudaMemcpyAsync(ldu_lower_.p, lower, sizeof(double) * nf * nn, cudaMemcpyHostToDevice, stream_), "H2D");
+        h2d(ldu_upper_.p, upper, sizeof(double) * nf * nn, "H2D");
+        h2d(ldu_lower_.p, lower, sizeof(double) * nf * nn, "H2D");
     }
     for (auto& P : dist_) {
         gather_values(n, P.nnz, nc, nf, P.src, ldu_diag_, ldu_upper_, ldu_lower_, P.vals.p, stream_);
@@ -1544,10 +1644,10 @@ void Engine::distSolveMP(int nc, int nf, int n, const int32_t* owner, const int3
     ldu_diag_.ensure(nc * nn, stream_);
     ldu_upper_.ensure(nf * nn, stream_);
     ldu_lower_.ensure(nf * nn, stream_);
-    check(cudaMemcpyAsync(ldu_diag_.p, diag, sizeof(double) * nc * nn, cudaMemcpyHostToDevice, stream_), "H2D");
+    h2d(ldu_diag_.p, diag, sizeof(double) * nc * nn, "H2D");
     if (nf) {
-        check(cudaMemcpyAsync(ldu_upper_.p, upper, sizeof(double) * nf * nn, cudaMemcpyHostToDevice, stream_), "H2D");
-        check(cudaMemcpyAsync(ldu_lower_.p, lower, sizeof(double) * nf * nn, cudaMemcpyHostToDevice, stream_), "H2D");
+        h2d(ldu_upper_.p, upper, sizeof(double) * nf * nn, "H2D");
+        h2d(ldu_lower_.p, lower, sizeof(double) * nf * nn, "H2D");
     }
     gather_values(n, P.nnz, nc, nf, P.src, ldu_diag_, ldu_upper_, ldu_lower_, P.vals.p, stream_);
     if (P.nh) gather_values(n, P.nh, nc, nf, P.hsrc, ldu_diag_, ldu_upper_, ldu_lower_, P.hvals.p, stream_);
@@ -1640,11 +1740,10 @@ void Engine::solveHost(const double* b, double* x, const bcs_solver_config& cfg,
     const size_t N = static_cast<size_t>(nc_) * n_;
     kb_.ensure(N, stream_);
     kx_.ensure(N, stream_);
-    check(cudaMemcpyAsync(kb_.p, b, N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D b");
-    check(cudaMemcpyAsync(kx_.p, x, N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D x");
+    h2d(kb_.p, b, N * sizeof(double), "H2D b");
+    h2d(kx_.p, x, N * sizeof(double), "H2D x");
     solveDevice(kb_, kx_, cfg, rep);
-    check(cudaMemcpyAsync(x, kx_.p, N * sizeof(double), cudaMemcpyDeviceToHost, stream_), "D2H x");
-    sync();
+    d2h(x, kx_.p, N * sizeof(double), "D2H x");  // synchronous
 }
 
 // SolvePipeline::solve (engine.cpp:47-120)
@@ -1695,8 +1794,8 @@ void Engine::pipelineSolve(int nc, int nf, int n, const int32_t* owner, const in
     auto t = clk::now();
     kb_.ensure(N, stream_);
     kx_.ensure(N, stream_);
-    check(cudaMemcpyAsync(kb_.p, b, N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D b");
-    check(cudaMemcpyAsync(kx_.p, x0, N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D x0");
+    h2d(kb_.p, b, N * sizeof(double), "H2D b");
+    h2d(kx_.p, x0, N * sizeof(double), "H2D x0");
     sync();
     rep.t_convert = secs(t, clk::now());
     // setup-or-replace by topology signature (engine.cpp:85-98)
@@ -1731,8 +1830,7 @@ void Engine::pipelineSolve(int nc, int nf, int n, const int32_t* owner, const in
     rep.t_solve = secs(t, clk::now());
     // "retrieve"
     t = clk::now();
-    check(cudaMemcpyAsync(x, kx_.p, N * sizeof(double), cudaMemcpyDeviceToHost, stream_), "D2H x");
-    sync();
+    d2h(x, kx_.p, N * sizeof(double), "D2H x");  // synchronous
     rep.t_retrieve = secs(t, clk::now());
 }
 
@@ -1747,8 +1845,8 @@ double Engine::residualNorm(const double* b, const double* x) {
     kb_.ensure(N, stream_);
     kx_.ensure(N, stream_);
     rk_.ensure(N, stream_);
-    check(cudaMemcpyAsync(kb_.p, b, N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D b");
-    check(cudaMemcpyAsync(kx_.p, x, N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D x");
+    h2d(kb_.p, b, N * sizeof(double), "H2D b");
+    h2d(kx_.p, x, N * sizeof(double), "H2D x");
     spmv(n_, nc_, ro_, ci_, vals_, kx_, kb_, rk_.p, stream_);
     return dotHost(rk_, rk_, N, true);
 }

@@ -218,6 +218,16 @@ private:
     DArray<int> dOwner_, dNeigh_, ro_, ci_, dg_, tpos_, src_, fill_;
     DArray<double> vals_;
     DArray<double> ldu_diag_, ldu_upper_, ldu_lower_;
+    // host->device copy of a caller's buffer: straight DMA when it is
+    // page-locked, else streamed through a ring of pinned staging chunks filled
+    // by several host threads (pageable cudaMemcpyAsync runs at ~11 GB/s)
+    void h2d(void* dst, const void* src, size_t bytes, const char* what);
+    // device->host counterpart (synchronous: dst is complete on return)
+    void d2h(void* dst, const void* src, size_t bytes, const char* what);
+    bool hostPinned(const void* p) const;
+    void ensureStaging();
+    std::vector<void*> stage_;
+    std::vector<cudaEvent_t> stageEv_;
     // device assembly: slot of every LDU block, cell -> faces (face order), cell -> boundary faces
     bool asmTopo_ = false;
     DArray<int> asmInv_, asmCfo_, asmCf_, asmBco_, asmBkind_, asmBad_;
