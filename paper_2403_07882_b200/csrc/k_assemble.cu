@@ -144,13 +144,10 @@ __device__ __forceinline__ V3 face_centre(const double* cen, const double* fx, i
     return bcs_euler::add(bcs_euler::scl(co, w), bcs_euler::scl(cn, 1.0 - w));
 }
 
-__global__ void __launch_bounds__(128) k_mu_cells(int nc, const int* __restrict__ owner, const int* __restrict__ neigh,
-                                                  const int* __restrict__ cfo, const int* __restrict__ cfl,
-                                                  const double* __restrict__ cen, const double* __restrict__ fx,
-                                                  const double* __restrict__ q, int limiter, double* grad,
-                                                  double* psi) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= nc) return;
+__device__ __forceinline__ void mu_cell(int c, const int* __restrict__ owner, const int* __restrict__ neigh,
+                                        const int* __restrict__ cfo, const int* __restrict__ cfl,
+                                        const double* __restrict__ cen, const double* __restrict__ fx,
+                                        const double* __restrict__ q, int limiter, double* grad, double* psi) {
     const Prim qc = load_prim(q, c);
     const V3 cc = load_v3(cen, c);
     double G[9];
@@ -184,9 +181,9 @@ __global__ void __launch_bounds__(128) k_mu_cells(int nc, const int* __restrict_
 #pragma unroll
         for (int e = 0; e < 9; ++e) Gk[e] = G[e];
         g[k] = bcs_euler::lsqFinish(Gk, b[k]);  // same regularisation and LU for every component
-        grad[15 * static_cast<size_t>(c) + 3 * k] = g[k].x;
-        grad[15 * static_cast<size_t>(c) + 3 * k + 1] = g[k].y;
-        grad[15 * static_cast<size_t>(c) + 3 * k + 2] = g[k].z;
+        grad[3 * k] = g[k].x;
+        grad[3 * k + 1] = g[k].y;
+        grad[3 * k + 2] = g[k].z;
     }
     double ps[5] = {1.0, 1.0, 1.0, 1.0, 1.0};
     if (limiter == 1) {  // Barth-Jespersen (euler.cpp:262-283)
@@ -204,7 +201,24 @@ __global__ void __launch_bounds__(128) k_mu_cells(int nc, const int* __restrict_
         }
     }
 #pragma unroll
-    for (int k = 0; k < 5; ++k) psi[5 * static_cast<size_t>(c) + k] = ps[k];
+    for (int k = 0; k < 5; ++k) psi[k] = ps[k];
+}
+
+// gradients (15 per cell) and limiter factors (5 per cell) of kAsmT cells,
+// staged in shared memory and stored as two contiguous runs
+__global__ void __launch_bounds__(kAsmT) k_mu_cells(int nc, const int* __restrict__ owner,
+                                                    const int* __restrict__ neigh, const int* __restrict__ cfo,
+                                                    const int* __restrict__ cfl, const double* __restrict__ cen,
+                                                    const double* __restrict__ fx, const double* __restrict__ q,
+                                                    int limiter, double* grad, double* psi) {
+    __shared__ double sg[15 * kAsmT], sp[5 * kAsmT];
+    const int c0 = blockIdx.x * kAsmT;
+    const int c = c0 + threadIdx.x;
+    const int count = min(kAsmT, nc - c0);
+    if (c < nc) mu_cell(c, owner, neigh, cfo, cfl, cen, fx, q, limiter, sg + 15 * threadIdx.x, sp + 5 * threadIdx.x);
+    __syncthreads();
+    for (int e = threadIdx.x; e < 15 * count; e += kAsmT) grad[15 * static_cast<size_t>(c0) + e] = sg[e];
+    for (int e = threadIdx.x; e < 5 * count; e += kAsmT) psi[5 * static_cast<size_t>(c0) + e] = sp[e];
 }
 
 __global__ void k_mu_faces(int nf, const int* __restrict__ owner, const int* __restrict__ neigh,
@@ -577,7 +591,7 @@ void assemble_inverse_src(int nnzb, const int* src, int* inv, cudaStream_t s) {
 void assemble_euler_muscl(int nc, int nf, const int* owner, const int* neigh, const int* cfo, const int* cfl,
                           const double* cen, const double* fx, const double* q, int limiter, double* grad, double* psi,
                           double* fsL, double* fsR, cudaStream_t s) {
-    k_mu_cells<<<(nc + 127) / 128, 128, 0, s>>>(nc, owner, neigh, cfo, cfl, cen, fx, q, limiter, grad, psi);
+    k_mu_cells<<<(nc + kAsmT - 1) / kAsmT, kAsmT, 0, s>>>(nc, owner, neigh, cfo, cfl, cen, fx, q, limiter, grad, psi);
     if (nf > 0) k_mu_faces<<<(nf + 255) / 256, 256, 0, s>>>(nf, owner, neigh, cen, fx, q, grad, psi, fsL, fsR);
     count_launch(nf > 0 ? 2 : 1);
 }
