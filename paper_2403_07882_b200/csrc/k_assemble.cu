@@ -206,7 +206,7 @@ __device__ __forceinline__ void mu_cell(int c, const int* __restrict__ owner, co
 
 // gradients (15 per cell) and limiter factors (5 per cell) of kAsmT cells,
 // staged in shared memory and stored as two contiguous runs
-__global__ void __launch_bounds__(kAsmT) k_mu_cells(int nc, const int* __restrict__ owner,
+__global__ void __launch_bounds__(kAsmT, 4) k_mu_cells(int nc, const int* __restrict__ owner,
                                                     const int* __restrict__ neigh, const int* __restrict__ cfo,
                                                     const int* __restrict__ cfl, const double* __restrict__ cen,
                                                     const double* __restrict__ fx, const double* __restrict__ q,
@@ -326,7 +326,7 @@ __device__ __forceinline__ void asm_cell(int c, int nf, const int* __restrict__ 
 
 // diagonal blocks and right-hand side of kAsmT consecutive cells, staged in
 // shared memory and stored coalesced (the rhs of the CTA is one contiguous run)
-__global__ void __launch_bounds__(kAsmT) k_asm_cells(int nc, int nf, const int* __restrict__ owner,
+__global__ void __launch_bounds__(kAsmT, 3) k_asm_cells(int nc, int nf, const int* __restrict__ owner,
                                                      const int* __restrict__ neigh, const double* __restrict__ area,
                                                      const int* __restrict__ cfo, const int* __restrict__ cfl,
                                                      const int* __restrict__ bco, const double* __restrict__ barea,
