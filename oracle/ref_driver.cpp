@@ -282,6 +282,34 @@ struct AmgDump {
 
 } // namespace
 
+void fillReport(const SolveReport& r, RefReport* rep) {
+    auto t = [&](const char* k) {
+        const auto it = r.timings.find(k);
+        return it == r.timings.end() ? 0.0 : it->second;
+    };
+    rep->iterations = r.iterations;
+    rep->converged = r.converged;
+    rep->breakdown = r.breakdown;
+    rep->initialResidual = r.initialResidual;
+    rep->finalResidual = r.finalResidual;
+    rep->tConvert = t("convert");
+    rep->tSetup = t("setup");
+    rep->tReplace = t("replace");
+    rep->tSolve = t("solve");
+    rep->tRetrieve = t("retrieve");
+    rep->setupBranch = (r.timings.count("setup") && r.timings.at("setup") > 0.0) ? 1 : 0;
+}
+
+// A persistent SolvePipeline over one system (bench: per-call wall times of
+// the setup branch, then of replace-branch calls, engine.cpp:85-98)
+struct PipeHandle {
+    std::unique_ptr<Mesh> mesh;
+    std::unique_ptr<BlockLduMatrix> A;
+    BlockVector b, x0;
+    SolvePipeline pipe;
+    PipeHandle(int nc, int n) : b(nc, n), x0(nc, n) {}
+};
+
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
@@ -523,27 +551,19 @@ int ref_solve(int nc, int nf, int n, const int* owner, const int* neigh, const d
         std::memcpy(bv.values.data(), b, sizeof(double) * bv.values.size());
         std::memcpy(xv.values.data(), x0, sizeof(double) * xv.values.size());
         const SolverConfig scfg = toCfg(cfg);
-        SolvePipeline pipe;
-        std::pair<BlockVector, SolveReport> out;
-        for (int c = 0; c < calls; ++c)
-            out = pipe.solve(A, bv, xv, backend == 0 ? Backend::HostLdu : Backend::EngineCsr, scfg);
-        std::memcpy(x, out.first.values.data(), sizeof(double) * out.first.values.size());
-        const SolveReport& r = out.second;
-        auto t = [&](const char* k) {
-            const auto it = r.timings.find(k);
-            return it == r.timings.end() ? 0.0 : it->second;
-        };
-        rep->iterations = r.iterations;
-        rep->converged = r.converged;
-        rep->breakdown = r.breakdown;
-        rep->initialResidual = r.initialResidual;
-        rep->finalResidual = r.finalResidual;
-        rep->tConvert = t("convert");
-        rep->tSetup = t("setup");
-        rep->tReplace = t("replace");
-        rep->tSolve = t("solve");
-        rep->tRetrieve = t("retrieve");
-        rep->setupBranch = (r.timings.count("setup") && r.timings.at("setup") > 0.0) ? 1 : 0;
+        // calls == 0 (with a history buffer): only the instrumented run below,
+        // which is solveCsr (engine.cpp:31-45) with a recording dot; its
+        // report and solution are returned (halves the cost at 128^3)
+        if (calls > 0) {
+            SolvePipeline pipe;
+            std::pair<BlockVector, SolveReport> out;
+            for (int c = 0; c < calls; ++c)
+                out = pipe.solve(A, bv, xv, backend == 0 ? Backend::HostLdu : Backend::EngineCsr, scfg);
+            std::memcpy(x, out.first.values.data(), sizeof(double) * out.first.values.size());
+            fillReport(out.second, rep);
+        } else if (!(hist && histN)) {
+            throw std::invalid_argument("ref_solve: calls == 0 needs a history buffer");
+        }
         if (hist && histN) {
             const BlockCsrMatrix csr = lduToBlockCsr(A);
             const auto M = makeCsrPreconditioner(csr, scfg);
@@ -560,8 +580,13 @@ int ref_solve(int nc, int nf, int n, const int* owner, const int* neigh, const d
             };
             std::vector<double> xx(x0, x0 + ops.size);
             try {
-                krylovSolve(ops, b, xx.data(), scfg);
+                const SolveReport r = krylovSolve(ops, b, xx.data(), scfg);
+                if (calls == 0) {
+                    fillReport(r, rep);
+                    std::memcpy(x, xx.data(), sizeof(double) * xx.size());
+                }
             } catch (const std::runtime_error&) {
+                if (calls == 0) throw;
             }
             std::vector<double> h;
             if (scfg.method == KrylovMethod::GMRES) replayGmres(tape.v, scfg, h);
@@ -571,6 +596,37 @@ int ref_solve(int nc, int nf, int n, const int* owner, const int* neigh, const d
         }
     });
 }
+
+void* ref_pipe_new(int nc, int nf, int n, const int* owner, const int* neigh, const double* diag,
+                   const double* upper, const double* lower, const double* b, const double* x0) {
+    try {
+        auto h = std::make_unique<PipeHandle>(nc, n);
+        h->mesh = topoMesh(nc, nf, owner, neigh, nullptr);
+        h->A = std::make_unique<BlockLduMatrix>(*h->mesh, varsFor(n));
+        fillLdu(*h->A, diag, upper, lower);
+        std::memcpy(h->b.values.data(), b, sizeof(double) * h->b.values.size());
+        std::memcpy(h->x0.values.data(), x0, sizeof(double) * h->x0.values.size());
+        return h.release();
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+// one SolvePipeline::solve call; *wall = its wall time (seconds)
+int ref_pipe_solve(void* hp, int backend, const RefCfg* cfg, double* x, RefReport* rep, double* wall) {
+    return guard([&] {
+        auto* h = static_cast<PipeHandle*>(hp);
+        const SolverConfig scfg = toCfg(cfg);
+        const auto t0 = std::chrono::steady_clock::now();
+        auto out = h->pipe.solve(*h->A, h->b, h->x0, backend == 0 ? Backend::HostLdu : Backend::EngineCsr, scfg);
+        *wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (x) std::memcpy(x, out.first.values.data(), sizeof(double) * out.first.values.size());
+        fillReport(out.second, rep);
+    });
+}
+
+void ref_pipe_free(void* h) { delete static_cast<PipeHandle*>(h); }
 
 // AMG hierarchy dump (amg.cpp:73-105): handle API.
 void* ref_amg_build(int nc, int nf, int n, const int* owner, const int* neigh, const double* diag,
@@ -604,9 +660,9 @@ void ref_amg_level_sizes(void* h, int l, int* rows, int* nnz, int* aggLen) {
 void ref_amg_level_get(void* h, int l, int* rowOffsets, int* cols, double* vals, int* agg) {
     auto* d = static_cast<AmgDump*>(h);
     const BlockCsrMatrix& A = d->A[l];
-    std::memcpy(rowOffsets, A.rowOffsets.data(), sizeof(int) * (A.nRows + 1));
-    std::memcpy(cols, A.colIndices.data(), sizeof(int) * A.nnz());
-    std::memcpy(vals, A.values.data(), sizeof(double) * A.values.size());
+    if (rowOffsets) std::memcpy(rowOffsets, A.rowOffsets.data(), sizeof(int) * (A.nRows + 1));
+    if (cols) std::memcpy(cols, A.colIndices.data(), sizeof(int) * A.nnz());
+    if (vals) std::memcpy(vals, A.values.data(), sizeof(double) * A.values.size());
     if (agg && !d->agg[l].empty()) std::memcpy(agg, d->agg[l].data(), sizeof(int) * d->agg[l].size());
 }
 void ref_amg_free(void* h) { delete static_cast<AmgDump*>(h); }

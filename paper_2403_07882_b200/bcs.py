@@ -337,6 +337,16 @@ class Context:
         self._ck(self._lib.bcs_amg_level_get(self.h, level, N.ptr(ro), N.ptr(ci), N.ptr(v), N.ptr(agg)))
         return ro, ci, v, agg
 
+    def amg_level_shape(self, level: int, want_agg: bool = True):
+        """(rows, nnz, aggregate or None) of one level without copying its values."""
+        rows, nnz = ctypes.c_int(), ctypes.c_int()
+        self._ck(self._lib.bcs_amg_level_sizes(self.h, level, ctypes.byref(rows), ctypes.byref(nnz)))
+        agg = None
+        if want_agg:
+            agg = np.full(rows.value, -1, np.int32)
+            self._ck(self._lib.bcs_amg_level_get(self.h, level, None, None, None, N.ptr(agg)))
+        return rows.value, nnz.value, agg
+
     def amg_level_rows(self, level: int) -> int:
         rows, nnz = ctypes.c_int(), ctypes.c_int()
         self._ck(self._lib.bcs_amg_level_sizes(self.h, level, ctypes.byref(rows), ctypes.byref(nnz)))

@@ -229,11 +229,12 @@ void Engine::setTopology(int nc, int nf, int n, const int32_t* owner, const int3
         if (owner[f] < 0 || neigh[f] >= nc || owner[f] >= neigh[f])
             throw std::invalid_argument("bcs: face " + std::to_string(f) +
                                         " violates 0 <= owner < neighbour < n_cells");
-    nc_ = nc;
-    nf_ = nf;
-    n_ = n;
-    hOwner_.assign(owner, owner + nf);
-    hNeigh_.assign(neigh, neigh + nf);
+    // nothing of the previous topology stays usable if this call throws (e.g.
+    // out of memory): sizes and host face copies are committed at the end
+    hasTopo_ = false;
+    hasValues_ = false;
+    asmTopo_ = false;
+    H_->pcKind = -1;
     const size_t nnz = static_cast<size_t>(nc) + 2 * static_cast<size_t>(nf);
     if (nnz > static_cast<size_t>(std::numeric_limits<int>::max()))
         throw std::invalid_argument("bcs: more than 2^31-1 blocks");
@@ -263,9 +264,12 @@ void Engine::setTopology(int nc, int nf, int n, const int32_t* owner, const int3
     vals_.ensure(nnz * n * n, stream_);
     checkErr("setTopology");
     if (readErrCell()) throw std::runtime_error("bcs: structurally asymmetric block pattern");
+    nc_ = nc;
+    nf_ = nf;
+    n_ = n;
+    hOwner_.assign(owner, owner + nf);
+    hNeigh_.assign(neigh, neigh + nf);
     hasTopo_ = true;
-    hasValues_ = false;
-    asmTopo_ = false;
 }
 
 // assembleJacobian + computeResidual (euler.cpp:361-455; first order, Roe,
@@ -1446,9 +1450,7 @@ void Engine::distSetupTopology(int nc, int nf, int n, const int32_t* owner, cons
         segh[e + 1] = static_cast<long long>(p.rowEnd) * n;
         segh[e] = static_cast<long long>(p.rowStart) * n;
     }
-    nseg_ = static_cast<int>(eng.size());
-    seg_.ensure(eng.size() + 1, stream_);
-    check(cudaMemcpyAsync(seg_.p, segh.data(), sizeof(long long) * segh.size(), cudaMemcpyHostToDevice, stream_), "H2D");
+    distSegh_ = segh;
     distNewToOld_ = dec.newToOld;
     distOwner_.assign(owner, owner + nf);
     distNeigh_.assign(neigh, neigh + nf);
@@ -1504,6 +1506,11 @@ void Engine::distSolve(int nc, int nf, int n, const int32_t* owner, const int32_
     check(cudaMemcpyAsync(kx_.p, hx.data(), N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D x0");
     sync();
     const auto t1 = clk::now();
+    // dot-product segments of the engines (a serial call in between rewrites seg_)
+    nseg_ = static_cast<int>(dist_.size());
+    seg_.ensure(distSegh_.size(), stream_);
+    check(cudaMemcpyAsync(seg_.p, distSegh_.data(), sizeof(long long) * distSegh_.size(), cudaMemcpyHostToDevice,
+                          stream_), "H2D seg");
     // per-engine preconditioners (partition.cpp:411-412)
     hist_.clear();
     spmvMs_ = 0.0;
@@ -1615,9 +1622,7 @@ void Engine::mpSetupTopology(int nc, int nf, int n, const int32_t* owner, const 
     mpXall_.ensure(static_cast<size_t>(mpMaxRows_) * n * (mpSize_ + 1), stream_);
     // reductions: the block layout of an engine segment in the one-device Mode R
     mpBps_ = seg_blocks(mpSize_);
-    const long long segh[2] = {0, static_cast<long long>(mpRows_) * n};
-    seg_.ensure(2, stream_);
-    check(cudaMemcpyAsync(seg_.p, segh, sizeof segh, cudaMemcpyHostToDevice, stream_), "H2D");
+
     mpNewToOld_ = dec.newToOld;
     mpOwner_.assign(owner, owner + nf);
     mpNeigh_.assign(neigh, neigh + nf);
@@ -1704,6 +1709,10 @@ void Engine::distSolveMP(int nc, int nf, int n, const int32_t* owner, const int3
     distActive_ = true;
     mpActive_ = true;
     nseg_ = 1;
+    {
+        const long long segh[2] = {0, static_cast<long long>(mpRows_) * n};
+        check(cudaMemcpyAsync(seg_.p, segh, sizeof segh, cudaMemcpyHostToDevice, stream_), "H2D seg");
+    }
     try {
         solveKrylov(kb_, kx_.p, cfg, rep);
     } catch (...) {

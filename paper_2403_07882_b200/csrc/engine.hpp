@@ -280,6 +280,7 @@ private:
     int distRanks_ = 0, distEngines_ = 0, distNc_ = 0, distNf_ = 0, distN_ = 0;
     std::vector<int> distNewToOld_;
     DArray<long long> seg_;  // segment offsets for reductions (1 segment serial, E for Mode R)
+    std::vector<long long> distSegh_;  // the one-device Mode R engines' segments
     int nseg_ = 1;
     DArray<double> distTmp_;
     // BCS_PROFILE=1: per-phase / per-level wall times (with syncs) to stderr

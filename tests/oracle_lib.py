@@ -184,6 +184,10 @@ class Reference:
         L.ref_amg_level_sizes.argtypes = [c_void_p, c_int] + [ctypes.POINTER(c_int)] * 3
         L.ref_amg_level_get.argtypes = [c_void_p, c_int] + [c_void_p] * 4
         L.ref_amg_free.argtypes = [c_void_p]
+        L.ref_pipe_new.restype = c_void_p
+        L.ref_pipe_new.argtypes = [c_int, c_int, c_int] + [c_void_p] * 7
+        L.ref_pipe_solve.argtypes = [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]
+        L.ref_pipe_free.argtypes = [c_void_p]
         L.ref_partition.restype = c_void_p
         L.ref_part_count.argtypes = [c_void_p]
         L.ref_part_sizes.argtypes = [c_void_p, c_int] + [ctypes.POINTER(c_int)] * 5
@@ -283,6 +287,28 @@ class Reference:
                               ctypes.byref(rep), ptr(h), hist_cap, ctypes.byref(hn) if hist else None)
         return rc, x, rep, (h[: min(hn.value, hist_cap)] if hist else None)
 
+    def amg_shape(self, A, max_levels=30, min_coarse=8):
+        """[(rows, nnz, aggregate or None)] per level of the reference's AmgHierarchy (amg.cpp:73-105),
+        without copying level values (cheap enough at 128^3)."""
+        h = self.L.ref_amg_build(*_sys_args(A), max_levels, min_coarse)
+        if not h:
+            raise RuntimeError(self.err())
+        out = []
+        try:
+            for lvl in range(self.L.ref_amg_depth(h)):
+                rows, nnz, alen = c_int(), c_int(), c_int()
+                self.L.ref_amg_level_sizes(h, lvl, ctypes.byref(rows), ctypes.byref(nnz), ctypes.byref(alen))
+                agg = np.full(rows.value, -1, np.int32) if alen.value else None
+                if agg is not None:
+                    self.L.ref_amg_level_get(h, lvl, None, None, None, ptr(agg))
+                out.append((rows.value, nnz.value, agg))
+        finally:
+            self.L.ref_amg_free(h)
+        return out
+
+    def pipeline(self, A, b, x0):
+        return RefPipeline(self, A, b, x0)
+
     def amg_levels(self, A, max_levels=30, min_coarse=8):
         h = self.L.ref_amg_build(*_sys_args(A), max_levels, min_coarse)
         if not h:
@@ -312,6 +338,38 @@ class Reference:
         if rc:
             raise ValueError(self.err())
         return c2r, rro, o2n
+
+
+class RefPipeline:
+    """One persistent reference SolvePipeline (engine.hpp:28-38) over a fixed
+    system: the first solve takes the setup branch, later ones the replace
+    branch (engine.cpp:85-98).  solve() returns (wall seconds, report, x)."""
+
+    def __init__(self, R, A, b, x0):
+        self.R = R
+        self._keep = (A, b, x0)
+        self.h = R.L.ref_pipe_new(*_sys_args(A), ptr(b), ptr(x0))
+        if not self.h:
+            raise RuntimeError(R.err())
+        self.size = b.size
+
+    def solve(self, cfg, backend=1, want_x=False):
+        c = OrCfg(*cfg)
+        rep = RefReport()
+        wall = c_double()
+        x = np.zeros(self.size) if want_x else None
+        rc = self.R.L.ref_pipe_solve(self.h, backend, ctypes.byref(c), ptr(x), ctypes.byref(rep), ctypes.byref(wall))
+        if rc:
+            raise RuntimeError(self.R.err())
+        return wall.value, rep, x
+
+    def close(self):
+        if self.h:
+            self.R.L.ref_pipe_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
 
 
 # --- reference test-suite fixtures (tests/support/test_helpers.hpp via ref_driver)
