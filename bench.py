@@ -314,6 +314,7 @@ def run_ours(args):
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
     free_b, total_b = torch.cuda.mem_get_info(dev)  # device-wide: our pools + torch's input copies
+    mem_ctx = {k: round(v / 1e9, 3) for k, v in ctx.memory_report().items()}
     # per-kernel CUDA-event timings (roofline) from extra, untimed steps: the
     # events around every sweep / SpMV launch are not part of the measured step
     ctx.set_kernel_timing(True)
@@ -496,6 +497,7 @@ def run_ours(args):
             "stage_s": {"amg_setup": last.timings.get("amgSetup"), "krylov": last.timings.get("krylov")},
             "gpu_launches": launches,
             "device_memory_gb": {"used": round((total_b - free_b) / 1e9, 2), "total": round(total_b / 1e9, 2),
+                                 "solver_context": mem_ctx,
                                  "note": "cudaMemGetInfo after the timed steps: solver pools (hierarchy, sweep programs, "
                                          "DILU scratch, Krylov basis) + the bench's device-resident LDU inputs"},
             "roofline": {"bound": "hbm", "achieved": sw_achieved, "peak": peak, "unit": "GB/s",

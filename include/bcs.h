@@ -72,8 +72,25 @@ typedef struct {
     int amg_min_coarse_rows; /* (default 8)     */
     int amg_pre_sweeps;      /* (default 1)     */
     int amg_post_sweeps;     /* (default 1)     */
-    int mode;                /* 0 = parity (reference operation order). Reserved. */
+    int mode;                /* BCS_MODE_* (default BCS_MODE_PARITY) */
 } bcs_solver_config;
+
+/* Execution modes.
+ * PARITY (default): every element-wise, block and per-row operation in the
+ *   reference's order (bit-identical BSR, SpMV, LU, LUSGS/DILU, Galerkin,
+ *   V-cycle, vector updates; the reference libm's hypot in the Givens
+ *   rotation); global dot products are deterministic two-level trees, the
+ *   only association that differs from the reference.
+ * PERF: the north_star performance smoothers -- multicolour block DILU on
+ *   every AMG level (deterministic colouring, colour-parallel sweeps) instead
+ *   of the natural-order sweeps; iteration counts differ from the reference
+ *   and are reported, never silently substituted.
+ * EXACT: PARITY plus the reference's own dot order (defaultDot,
+ *   krylov.cpp:38-42: one sequential chain per engine, engine partials
+ *   folded by the pairwise tree of partition.cpp:433-450): residual
+ *   histories and solutions are bit-identical to the reference.  A dot is
+ *   then a serial chain of N dependent adds (~4.3 ns each): a proof mode. */
+enum { BCS_MODE_PARITY = 0, BCS_MODE_PERF = 1, BCS_MODE_EXACT = 2 };
 
 /* SolveReport (krylov.hpp:39-50) + per-stage timings (seconds) with the
  * reference keys (engine.cpp:80-112) and device sub-stages. */
@@ -305,6 +322,15 @@ bcs_status bcs_amg_level_get(bcs_ctx* ctx, int level, int32_t* row_offsets, int3
 /* Level schedule of the last DILU/LUSGS setup of `level`: number of
  * dependency levels of its lower-triangular DAG (critical path). */
 bcs_status bcs_level_schedule_depth(bcs_ctx* ctx, int level, int* depth);
+
+/* Diagnostics: the device restatement of the reference libm's hypot (used by
+ * the Givens rotation) on n host pairs -- the test pins it against libm. */
+bcs_status bcs_selftest_hypot(const double* x, const double* y, double* out, int n);
+
+/* Device memory held by the context, per category (bytes), as a JSON object
+ * {"bsr_fine": .., "bsr_coarse": .., "sweep_programs": .., ..., "total": ..}.
+ * *needed = length + 1; buf may be NULL (size query). */
+bcs_status bcs_memory_report(bcs_ctx* ctx, char* buf, size_t cap, size_t* needed);
 
 /* Device self-tests (diagnostics).  what = 0: the sweeps' reciprocal-based
  * exact division against IEEE __ddiv_rn on n random operand pairs; *result =

@@ -50,6 +50,15 @@ class AmgConfig:
     aggregationSize: int = 2
 
 
+class Mode(enum.IntEnum):
+    """bcs_solver_config.mode (include/bcs.h): PARITY (default: reference order
+    except the global dot association), PERF (multicolour smoothers), EXACT
+    (the reference's sequential dot order too: bit-identical histories)."""
+    PARITY = 0
+    PERF = 1
+    EXACT = 2
+
+
 @dataclass
 class SolverConfig:
     method: KrylovMethod = KrylovMethod.GMRES
@@ -59,12 +68,13 @@ class SolverConfig:
     maxIters: int = 500
     gmresRestart: int = 30
     amg: AmgConfig = field(default_factory=AmgConfig)
+    mode: Mode = Mode.PARITY
 
     def to_c(self) -> N.SolverConfigC:
         return N.SolverConfigC(
             int(self.method), int(self.preconditioner), float(self.relTol), float(self.absTol),
             int(self.maxIters), int(self.gmresRestart), int(self.amg.maxLevels), int(self.amg.minCoarseRows),
-            int(self.amg.preSweeps), int(self.amg.postSweeps), 0,
+            int(self.amg.preSweeps), int(self.amg.postSweeps), int(self.mode),
         )
 
 
@@ -351,6 +361,15 @@ class Context:
         rows, nnz = ctypes.c_int(), ctypes.c_int()
         self._ck(self._lib.bcs_amg_level_sizes(self.h, level, ctypes.byref(rows), ctypes.byref(nnz)))
         return rows.value
+
+    def memory_report(self) -> dict:
+        """Device bytes held by this context per category (bcs_memory_report)."""
+        import json
+        need = ctypes.c_size_t()
+        self._ck(self._lib.bcs_memory_report(self.h, None, 0, ctypes.byref(need)))
+        buf = ctypes.create_string_buffer(need.value + 16)
+        self._ck(self._lib.bcs_memory_report(self.h, buf, need.value + 16, ctypes.byref(need)))
+        return json.loads(buf.value.decode())
 
     def schedule_depth(self, level: int) -> int:
         d = ctypes.c_int()

@@ -554,6 +554,37 @@ bcs_status bcs_amg_level_get(bcs_ctx* ctx, int level, int32_t* row_offsets, int3
     return guarded(ctx, [&] { eng(ctx).amgLevelGet(level, row_offsets, cols, values, aggregate); });
 }
 
+bcs_status bcs_selftest_hypot(const double* x, const double* y, double* out, int n) {
+    return guarded(nullptr, [&] {
+        if (n <= 0) return;
+        double *dx = nullptr, *dy = nullptr, *dz = nullptr;
+        const size_t b = sizeof(double) * static_cast<size_t>(n);
+        bcs::check(cudaMalloc(&dx, b), "cudaMalloc");
+        bcs::check(cudaMalloc(&dy, b), "cudaMalloc");
+        bcs::check(cudaMalloc(&dz, b), "cudaMalloc");
+        cudaMemcpy(dx, x, b, cudaMemcpyHostToDevice);
+        cudaMemcpy(dy, y, b, cudaMemcpyHostToDevice);
+        bcs::hypot_eval(dx, dy, dz, n, nullptr);
+        const cudaError_t e = cudaMemcpy(out, dz, b, cudaMemcpyDeviceToHost);
+        cudaFree(dx);
+        cudaFree(dy);
+        cudaFree(dz);
+        bcs::check(e, "hypot selftest");
+    });
+}
+
+bcs_status bcs_memory_report(bcs_ctx* ctx, char* buf, size_t cap, size_t* needed) {
+    return guarded(ctx, [&] {
+        const std::string r = eng(ctx).memoryReport();
+        if (needed) *needed = r.size() + 1;
+        if (buf && cap) {
+            const size_t k = std::min(cap - 1, r.size());
+            std::memcpy(buf, r.data(), k);
+            buf[k] = 0;
+        }
+    });
+}
+
 bcs_status bcs_level_schedule_depth(bcs_ctx* ctx, int level, int* depth) {
     return guarded(ctx, [&] {
         if (depth) *depth = eng(ctx).scheduleDepth(level);

@@ -652,6 +652,8 @@ void Engine::validateConfig(const bcs_solver_config& c) const {
     if (c.amg_pre_sweeps < 0 || c.amg_post_sweeps < 0) throw std::invalid_argument("SolverConfig: amg sweeps must be >= 0");
     if (c.method != BCS_GMRES && c.method != BCS_BICGSTAB && c.method != BCS_FGMRES) throw std::invalid_argument("unknown Krylov method");
     if (c.precond < 0 || c.precond > 3) throw std::invalid_argument("unknown preconditioner kind");
+    if (c.mode != BCS_MODE_PARITY && c.mode != BCS_MODE_PERF && c.mode != BCS_MODE_EXACT)
+        throw std::invalid_argument("bcs: unknown mode");
 }
 
 void Engine::setupLevelPattern(Level& L) {
@@ -706,7 +708,6 @@ void Engine::diluSetupAll(int nl) {
         L.dlev.ensure(L.rows, stream_);
         lh[l] = {L.rows, L.ro, L.ci, L.dg, L.dlev.p, L.order.p};
         totalRows += L.rows;
-        totalT += static_cast<size_t>(L.nnz) * nn;
         maxRows = std::max(maxRows, static_cast<size_t>(L.rows));
     }
     cnt_.ensure(maxRows + 2, stream_);
@@ -719,13 +720,21 @@ void Engine::diluSetupAll(int nl) {
         maxdepth = std::max(maxdepth, depth[l]);
     }
     profMark("dilu:levels");
+    // T (D~_j^-1 A_ji per lower slot) is setup-phase memory: compact (lower
+    // slots only) and released when the factorisation is done
     std::vector<DiluLevelHost> desc(nl);
     size_t toff = 0;
     for (int l = 0; l < nl; ++l) {
         Level& L = H_->levels[l];
-        desc[l] = {L.rows, L.ro, L.dg, L.tpos, L.dlev.p, L.v, L.lu.p, L.piv.p, toff};
-        toff += static_cast<size_t>(L.nnz) * nn;
+        L.lpre.ensure(static_cast<size_t>(L.rows) + 1, stream_);
+        L.tc.ensure(L.nnz, stream_);
+        scanTmp_.ensure(scan_tmp_ints(static_cast<size_t>(L.rows) + 1) + 16, stream_);
+        const size_t lower = dilu_compact_index(L.rows, L.ro, L.dg, L.ci, L.tpos, L.lpre.p, L.tc.p, push_.p + 9,
+                                                scanTmp_.p, stream_);
+        desc[l] = {L.rows, L.ro, L.dg, L.tpos, L.tc.p, L.lpre.p, L.dlev.p, L.v, L.lu.p, L.piv.p, toff};
+        toff += lower * nn;
     }
+    totalT = toff;
     const size_t buckets = static_cast<size_t>(maxdepth) * nl + 1;
     dkeys_.ensure(totalRows, stream_);
     dorder_.ensure(totalRows, stream_);
@@ -743,6 +752,11 @@ void Engine::diluSetupAll(int nl) {
     if (cell != big)
         throw std::runtime_error("DILU setup: singular modified diagonal in cell " + std::to_string(cell & ((1 << 26) - 1)));
     profMark("dilu:factor");
+    tblk_.release(stream_);
+    for (int l = 0; l < nl; ++l) {
+        H_->levels[l].tc.release(stream_);
+        H_->levels[l].lpre.release(stream_);
+    }
     for (int l = 0; l < nl; ++l) finishSmoother(H_->levels[l]);
 }
 
@@ -882,6 +896,9 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
         profMark("setup:pattern");
     }
     H_->levels[H_->nlev - 1].ncoarse = 0;
+    keys_.release(stream_);  // setup-phase scratch of the coarsening
+    sorted_.release(stream_);
+    str_.release(stream_);
     // DILU smoother on all but the coarsest level (amg.cpp:86-88)
     diluSetupAll(H_->nlev - 1);
     // dense factorisation of the coarsest level (amg.cpp:90-104)
@@ -968,6 +985,16 @@ void Engine::buildPrecond(const bcs_solver_config& cfg) {
 
 void Engine::buildPrecondOn(const FineMatrix& F, const bcs_solver_config& cfg) {
     H_->pcKind = -1;
+    // phase-local memory: the previous call's solve-phase arrays (sweep
+    // programs, Krylov basis) go back to the stream-ordered pool before the
+    // setup phase allocates its scratch (Galerkin keys, DILU T), so the peak is
+    // max(setup, solve) rather than their sum (what lets 256^3 fit one B200)
+    for (auto& L : H_->levels) {
+        L.pkf.release(stream_);
+        L.pkb.release(stream_);
+    }
+    V_.release(stream_);
+    Z_.release(stream_);
     if (H_->levels.empty()) H_->levels.emplace_back();
     H_->nlev = 1;
     Level& L0 = H_->levels[0];
@@ -1288,6 +1315,11 @@ void Engine::solveDevice(const double* d_b, double* d_x, const bcs_solver_config
 }
 
 void Engine::solveKrylov(const double* d_b, double* d_x, const bcs_solver_config& cfg, bcs_report& rep) {
+    exactDots_ = cfg.mode == BCS_MODE_EXACT;
+    struct Reset {
+        bool& f;
+        ~Reset() { f = false; }
+    } reset{exactDots_};
     if (cfg.method == BCS_GMRES || cfg.method == BCS_FGMRES) gmres(d_b, d_x, cfg, rep);
     else bicgstab(d_b, d_x, cfg, rep);
     sync();
@@ -1368,6 +1400,17 @@ void Engine::opPrecond(const double* r, double* z) {
 // multi-process: this engine's partial with the block layout the one-device
 // Mode R uses for an engine segment, all-gathered, folded in engine order
 void Engine::opDot(const double* a, const double* b, double* out, bool sqrt_out) {
+    if (exactDots_) {  // BCS_MODE_EXACT: the reference's sequential order (krylov.cpp:38-42)
+        if (mpActive_) {
+            dot_seq(a, b, seg_, 1, mpPart_.p, false, partials_.p, stream_);
+            nccl::ck(nccl::api().allGather(mpPart_.p, mpGath_.p, 1, ncclDouble, static_cast<ncclComm_t>(comm_), stream_),
+                     "allgather");
+            fold_engines(mpGath_, mpSize_, out, sqrt_out, stream_);
+            return;
+        }
+        dot_seq(a, b, seg_, nseg_, out, sqrt_out, partials_.p, stream_);
+        return;
+    }
     if (mpActive_) {
         dot(a, b, seg_, 1, mpPart_.p, false, partials_.p, ticket_.p, stream_, mpBps_);
         nccl::ck(nccl::api().allGather(mpPart_.p, mpGath_.p, 1, ncclDouble, static_cast<ncclComm_t>(comm_), stream_),
@@ -1379,6 +1422,18 @@ void Engine::opDot(const double* a, const double* b, double* out, bool sqrt_out)
 }
 
 void Engine::opAxpyDot(double* w, const double* h, const double* v, const double* nextv, double* out) {
+    if (exactDots_) {
+        const size_t N = static_cast<size_t>(nc_) * n_;
+        if (mpActive_) {
+            axpy_dot_seq(w, h, v, nextv, N, seg_, 1, mpPart_.p, partials_.p, stream_);
+            nccl::ck(nccl::api().allGather(mpPart_.p, mpGath_.p, 1, ncclDouble, static_cast<ncclComm_t>(comm_), stream_),
+                     "allgather");
+            fold_engines(mpGath_, mpSize_, out, nextv == nullptr, stream_);
+            return;
+        }
+        axpy_dot_seq(w, h, v, nextv, N, seg_, nseg_, out, partials_.p, stream_);
+        return;
+    }
     if (mpActive_) {
         axpy_dot(w, h, v, nextv, seg_, 1, mpPart_.p, partials_.p, ticket_.p, stream_, mpBps_, 0);
         nccl::ck(nccl::api().allGather(mpPart_.p, mpGath_.p, 1, ncclDouble, static_cast<ncclComm_t>(comm_), stream_),
@@ -1932,6 +1987,60 @@ void Engine::amgLevelGet(int l, int32_t* ro, int32_t* ci, double* v, int32_t* ag
     if (agg && l + 1 < H_->nlev)
         check(cudaMemcpyAsync(agg, L.agg.p, sizeof(int) * L.rows, cudaMemcpyDeviceToHost, stream_), "D2H");
     sync();
+}
+
+std::string Engine::memoryReport() const {
+    std::map<std::string, double> m;
+    auto add = [&](const char* k, const auto& a) { m[k] += static_cast<double>(a.cap) * sizeof(*a.p); };
+    auto hier = [&](const Hier& H, bool fine) {
+        for (size_t l = 0; l < H.levels.size(); ++l) {
+            const Level& L = H.levels[l];
+            add("bsr_coarse", L.o_v);
+            add("pattern", L.o_ro); add("pattern", L.o_ci); add("pattern", L.o_dg); add("pattern", L.o_tpos);
+            add("smoother_factors", L.lu); add("smoother_factors", L.rcp); add("smoother_factors", L.piv);
+            add("smoother_factors", L.perm);
+            add("schedule", L.order); add("schedule", L.recf); add("schedule", L.recb); add("schedule", L.offf);
+            add("schedule", L.offb); add("schedule", L.dlev);
+            add("sweep_programs", L.pkf); add("sweep_programs", L.pkb);
+            add("aggregates", L.agg); add("aggregates", L.members);
+            add("vcycle_vectors", L.r); add("vcycle_vectors", L.z); add("vcycle_vectors", L.res);
+            add("vcycle_vectors", L.y); add("vcycle_vectors", L.zb);
+        }
+        add("dense_coarsest", H.dense); add("dense_coarsest", H.dpiv); add("schedule", H.tailDesc);
+        (void)fine;
+    };
+    hier(main_, true);
+    for (const auto& P : dist_) {
+        add("mode_r_engines", P.vals); add("mode_r_engines", P.hvals); add("mode_r_engines", P.ro);
+        add("mode_r_engines", P.ci); add("mode_r_engines", P.src); add("mode_r_engines", P.dg);
+        add("mode_r_engines", P.tpos); add("mode_r_engines", P.hrow); add("mode_r_engines", P.hoff);
+        add("mode_r_engines", P.hcol); add("mode_r_engines", P.hsrc);
+        hier(P.H, false);
+    }
+    add("bsr_fine", vals_);
+    add("pattern", ro_); add("pattern", ci_); add("pattern", dg_); add("pattern", tpos_); add("pattern", src_);
+    add("pattern", fill_); add("pattern", dOwner_); add("pattern", dNeigh_);
+    add("ldu_staging", ldu_diag_); add("ldu_staging", ldu_upper_); add("ldu_staging", ldu_lower_);
+    add("dilu_setup_scratch", tblk_);
+    for (const auto* a : {&V_, &Z_, &w_, &zk_, &rk_, &kb_, &kx_, &bp_, &bv_, &bs_, &bt_, &bph_, &bsh_, &brh_, &distTmp_})
+        add("krylov", *a);
+    for (const auto* a : {&asmMuGrad_, &asmPsi_, &asmFs_, &asmBp_, &asmArea_, &asmBarea_, &asmQ_, &asmRhs_, &asmFx_,
+                          &asmVol_, &asmCen_, &asmBu_, &asmPhi_, &asmD_, &asmGrad_})
+        add("assembly", *a);
+    for (const auto* a : {&asmInv_, &asmCfo_, &asmCf_, &asmBco_, &asmBkind_, &asmBad_}) add("assembly", *a);
+    for (const auto* a : {&cnt_, &lvl_, &act2_, &push_, &scanTmp_, &flag_, &err_, &ctr_, &choice_, &segOff_, &cro_,
+                          &big_, &dkeys_, &dorder_, &ticket_})
+        add("setup_scratch", *a);
+    add("setup_scratch", dn_); add("setup_scratch", str_); add("setup_scratch", keys_); add("setup_scratch", sorted_);
+    add("setup_scratch", ddesc_);
+    double total = 0.0;
+    std::string out = "{";
+    for (const auto& [k, v] : m) {
+        total += v;
+        out += "\"" + k + "\": " + std::to_string(static_cast<long long>(v)) + ", ";
+    }
+    out += "\"total\": " + std::to_string(static_cast<long long>(total)) + "}";
+    return out;
 }
 
 int Engine::scheduleDepth(int l) const {

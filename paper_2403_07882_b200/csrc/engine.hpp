@@ -61,6 +61,7 @@ struct Level {
     DArray<int> piv, perm, order, recf, recb;  // perm: composed pivot permutation; recf/recb: int4 records
     DArray<int> offf, offb;                    // per-ticket slot offsets (16-byte units), rows + 1
     DArray<int> dlev;                          // dependency level of every row
+    DArray<int> tc, lpre;                      // DILU setup only: compact T indices (released after)
     DArray<unsigned char> pkf, pkb;            // packed per-ticket slots of the two sweeps
     int depth = 0;
     // aggregation to level+1
@@ -166,6 +167,9 @@ public:
     void amgLevelGet(int l, int32_t* ro, int32_t* ci, double* v, int32_t* agg);
     int scheduleDepth(int l) const;
 
+    // device bytes held by this context, per category (JSON object)
+    std::string memoryReport() const;
+
     cudaStream_t stream() const { return stream_; }
     long long totalLaunches() const { return launches_.launches; }
     int blockSize() const { return n_; }
@@ -209,6 +213,7 @@ private:
     int device_ = 0;
     cudaStream_t own_ = nullptr, stream_ = nullptr;
     bool kernelTiming_ = false;
+    bool exactDots_ = false;  // BCS_MODE_EXACT for the current Krylov run
     LaunchCounter launches_;
 
     // topology

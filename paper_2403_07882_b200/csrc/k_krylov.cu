@@ -80,6 +80,63 @@ __global__ void __launch_bounds__(kRedThreads) k_dot(const double* __restrict__ 
     finish_reduction(s, nseg, partials, ticket, out, sqrt_out != 0);
 }
 
+// Exact mode (BCS_MODE_EXACT): the reference's own association order.
+// defaultDot (krylov.cpp:38-42) is `s += a[i] * b[i]` from s = 0 in index
+// order, i.e. a serial chain of rounded additions; one CTA per segment
+// (engine) runs it: threads 32.. stage the rounded products of the next chunk
+// in shared memory while thread 0 adds the current chunk in order.  The
+// engine partials are then folded with the pairwise tree (partition.cpp:433-450).
+// Throughput is one dependent FP64 add per element (~4.3 ns): diagnostic /
+// proof speed, not the default.
+constexpr int kSeqChunk = 2048;
+__global__ void __launch_bounds__(256) k_dot_seq(const double* __restrict__ a, const double* __restrict__ b,
+                                                 const long long* __restrict__ seg, double* part) {
+    __shared__ double buf[2][kSeqChunk];
+    const size_t s0 = static_cast<size_t>(seg[blockIdx.x]);
+    const size_t n = static_cast<size_t>(seg[blockIdx.x + 1]) - s0;
+    const int nch = static_cast<int>((n + kSeqChunk - 1) / kSeqChunk);
+    const double* pa = a + s0;
+    const double* pb = b + s0;
+    auto fill = [&](int c, int t0, int nt) {
+        const size_t base = static_cast<size_t>(c) * kSeqChunk;
+        const int len = static_cast<int>(n - base < static_cast<size_t>(kSeqChunk) ? n - base : kSeqChunk);
+        for (int k = threadIdx.x - t0; k < len; k += nt) buf[c & 1][k] = __dmul_rn(pa[base + k], pb[base + k]);
+    };
+    if (nch > 0) fill(0, 0, blockDim.x);
+    __syncthreads();
+    double s = 0.0;
+    for (int c = 0; c < nch; ++c) {
+        if (threadIdx.x >= 32 && c + 1 < nch) fill(c + 1, 32, blockDim.x - 32);
+        if (threadIdx.x == 0) {
+            const size_t base = static_cast<size_t>(c) * kSeqChunk;
+            const int len = static_cast<int>(n - base < static_cast<size_t>(kSeqChunk) ? n - base : kSeqChunk);
+            const double* bc = buf[c & 1];
+#pragma unroll 16
+            for (int k = 0; k < len; ++k) s = __dadd_rn(s, bc[k]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+__global__ void k_axpy(double* __restrict__ w, const double* __restrict__ h, const double* __restrict__ v, size_t N) {
+    const double hv = *h;
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < N; i += stride) w[i] = w[i] - hv * v[i];
+}
+
+void dot_seq(const double* a, const double* b, const long long* seg, int nseg, double* out, bool sqrt_out,
+             double* partials, cudaStream_t s) {
+    k_dot_seq<<<nseg, 256, 0, s>>>(a, b, seg, partials);
+    count_launch();
+    fold_engines(partials, nseg, out, sqrt_out, s);
+}
+void axpy_dot_seq(double* w, const double* h, const double* v, const double* nextv, size_t N, const long long* seg,
+                  int nseg, double* out, double* partials, cudaStream_t s) {
+    k_axpy<<<4 * num_sms(), 256, 0, s>>>(w, h, v, N);
+    count_launch();
+    dot_seq(w, nextv ? nextv : w, seg, nseg, out, nextv == nullptr, partials, s);
+}
+
 static int seg_grid(int nseg) {
     int B = reduce_blocks() / nseg;
     if (B < 4) B = 4;
@@ -226,6 +283,56 @@ void lincomb(const double* V, size_t ld, const double* y, int j, double* w, size
     count_launch();
 }
 
+// std::hypot of the reference's libm (glibc 2.35+ e_hypot.c: Borges' "An
+// Improved Algorithm for hypot(a,b)", the non-FMA kernel with its scaling
+// thresholds 2^511 / 2^-459 / 2^-54 and scale 2^-600), restated operation by
+// operation so the Givens rotation of krylov.cpp:106-117 rounds as the
+// reference's does.  Pinned against the host libm bit for bit
+// (tests/test_oracle.py::test_glibc_hypot_restatement, bcs_selftest_hypot).
+__device__ __forceinline__ double glibc_hypot_kernel(double ax, double ay) {
+    double h = __dsqrt_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)));
+    double t1, t2;
+    if (h <= __dmul_rn(2.0, ay)) {
+        const double delta = __dsub_rn(h, ay);
+        t1 = __dmul_rn(ax, __dsub_rn(__dmul_rn(2.0, delta), ax));
+        t2 = __dmul_rn(__dsub_rn(delta, __dmul_rn(2.0, __dsub_rn(ax, ay))), delta);
+    } else {
+        const double delta = __dsub_rn(h, ax);
+        t1 = __dmul_rn(__dmul_rn(2.0, delta), __dsub_rn(ax, __dmul_rn(2.0, ay)));
+        t2 = __dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(4.0, delta), ay), ay), __dmul_rn(delta, delta));
+    }
+    return __dsub_rn(h, __ddiv_rn(__dadd_rn(t1, t2), __dmul_rn(2.0, h)));
+}
+__device__ double glibc_hypot(double x, double y) {
+    if (!isfinite(x) || !isfinite(y)) {
+        if (isinf(x) || isinf(y)) return __longlong_as_double(0x7ff0000000000000ll);
+        return __dadd_rn(x, y);
+    }
+    x = fabs(x);
+    y = fabs(y);
+    const double ax = x < y ? y : x, ay = x < y ? x : y;
+    constexpr double kScale = 0x1p-600, kLarge = 0x1p+511, kTiny = 0x1p-459, kEps = 0x1p-54;
+    if (ax > kLarge) {
+        if (ay <= __dmul_rn(ax, kEps)) return __dadd_rn(ax, ay);
+        return __ddiv_rn(glibc_hypot_kernel(__dmul_rn(ax, kScale), __dmul_rn(ay, kScale)), kScale);
+    }
+    if (ay < kTiny) {
+        if (ax >= __ddiv_rn(ay, kEps)) return __dadd_rn(ax, ay);
+        return __dmul_rn(glibc_hypot_kernel(__ddiv_rn(ax, kScale), __ddiv_rn(ay, kScale)), kScale);
+    }
+    if (ay <= __dmul_rn(ax, kEps)) return __dadd_rn(ax, ay);
+    return glibc_hypot_kernel(ax, ay);
+}
+__global__ void k_hypot_eval(const double* x, const double* y, double* out, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = glibc_hypot(x[i], y[i]);
+}
+void hypot_eval(const double* x, const double* y, double* out, int n, cudaStream_t s) {
+    if (n <= 0) return;
+    k_hypot_eval<<<(n + 255) / 256, 256, 0, s>>>(x, y, out, n);
+    count_launch();
+}
+
 // Givens update of column j (krylov.cpp:104-117); H is (m+1) x m row-major
 __global__ void k_givens(double* H, int m, int j, double* cs, double* sn, double* g, double* status) {
     if (threadIdx.x != 0) return;
@@ -235,7 +342,7 @@ __global__ void k_givens(double* H, int m, int j, double* cs, double* sn, double
         H[(i + 1) * m + j] = -sn[i] * H[i * m + j] + cs[i] * H[(i + 1) * m + j];
         H[i * m + j] = t;
     }
-    const double den = hypot(H[j * m + j], H[(j + 1) * m + j]);
+    const double den = glibc_hypot(H[j * m + j], H[(j + 1) * m + j]);
     cs[j] = den > 0.0 ? H[j * m + j] / den : 1.0;
     sn[j] = den > 0.0 ? H[(j + 1) * m + j] / den : 0.0;
     H[j * m + j] = den;

@@ -70,7 +70,7 @@ int level_schedule(int rows, const int* ro, const int* ci, const int* dg, int* o
 // *err_cell = min over singular rows of (matrix << 26 | row).
 struct DiluLevelHost {
     int rows;
-    const int *ro, *dg, *tpos, *dlev;
+    const int *ro, *dg, *tpos, *tc, *lpre, *dlev;
     const double* v;
     double* lu;
     int* piv;
@@ -80,6 +80,10 @@ void dilu_setup_multi(int n, int nl, const DiluLevelHost* levels, int maxdepth, 
                       int* scan_tmp, int* small, void* desc_dev, double* Tbase, size_t tcount, int* err_cell,
                       int* err, cudaStream_t s);
 size_t dilu_desc_bytes();
+// lower-slot prefix lpre[rows+1] and compact transposed index tc[nnz] of the
+// DILU setup's T (lower slots only); returns the number of lower slots (syncs)
+size_t dilu_compact_index(int rows, const int* ro, const int* dg, const int* ci, const int* tpos, int* lpre, int* tc,
+                          int* d_total, int* scan_tmp, cudaStream_t s);
 // dependency levels + level-ordered schedules of several matrices in one
 // sync-free pass; depth[l] out; small >= 2 + nl ints; cnt >= max depth + 2.
 struct LevelsHost {
@@ -214,6 +218,13 @@ void axpy_dot(double* w, const double* h, const double* v, const double* nextv, 
 int seg_blocks(int nseg);
 // multi-process Mode R: engine partials folded in the reference's tree; rows packed for a halo send
 void fold_engines(const double* parts, int G, double* out, bool sqrt_out, cudaStream_t s);
+// exact mode: the reference's sequential dot order per segment + engine tree
+void dot_seq(const double* a, const double* b, const long long* seg, int nseg, double* out, bool sqrt_out,
+             double* partials, cudaStream_t s);
+void axpy_dot_seq(double* w, const double* h, const double* v, const double* nextv, size_t N, const long long* seg,
+                  int nseg, double* out, double* partials, cudaStream_t s);
+// the reference libm's hypot (glibc algorithm) on n device pairs
+void hypot_eval(const double* x, const double* y, double* out, int n, cudaStream_t s);
 void pack_rows(int n, int cnt, const int* idx, const double* x, double* out, cudaStream_t s);
 void halo_spmv(int n, int nhr, const int* hrow, const int* hoff, const int* hcol, const double* hv, const double* x,
                double* y, int rowStart, cudaStream_t s);
