@@ -370,6 +370,12 @@ def run_ours(args):
         except Exception:
             traffic = None
 
+    # phase 1 done: its context and the device-resident inputs are released
+    # before the e2e phases build theirs (256^3 does not fit twice)
+    ctx.close()
+    del d_diag, d_up, d_lo, d_b, d_x0, d_x
+    torch.cuda.empty_cache()
+
     # e2e through the drop-in ABI call with pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -513,7 +519,6 @@ def run_ours(args):
             "e2e": e2e, "e2e_device_assembly": e2e_asm, "cpu_baseline": cpu, "clocks": clk.summary(),
         }
         emit(out)
-    ctx.close()
     if world > 1:
         torch.distributed.destroy_process_group()
 

@@ -206,6 +206,15 @@ bcs_status bcs_partition_exchange_sizes(const bcs_partition* p, int part, int* n
 bcs_status bcs_partition_exchange_get(const bcs_partition* p, int part, int32_t* send_row, int32_t* send_count,
                                       int32_t* recv_global_row, int32_t* recv_count, int32_t* halo_recv_idx);
 
+/* The reference's per-rank upload (partition.cpp:384-407) of engine `part`:
+ * the LDU blocks of its local slots (slot order, nnz * n^2 doubles) and of
+ * its halo entries (entry order, n_halo * n^2 doubles) gathered on the host
+ * from the face-addressed arrays; bcs_dist_solve_mp ships exactly these to
+ * the engine's GPU.  Either output may be NULL. */
+bcs_status bcs_partition_gather_values(const bcs_partition* p, int part, int n_cells, int n_faces, int block_size,
+                                       const double* diag, const double* upper, const double* lower,
+                                       double* local_values, double* halo_values);
+
 /* ---- Mode R with one process per GPU (NCCL) -------------------------------
  * bcs_comm_unique_id fills 128 bytes on one rank; every rank passes them to
  * bcs_comm_init (collective).  bcs_dist_solve_mp is then called collectively

@@ -476,6 +476,19 @@ class Partition:
                                                                         "send_row")))
         return d
 
+    def gather_values(self, i: int, A: "BlockLduMatrix"):
+        """The per-rank upload of engine i (bcs_partition_gather_values): its local
+        slots' and halo entries' LDU blocks, gathered on the host in slot order."""
+        d = self.part(i)
+        nn = A.n * A.n
+        loc = np.zeros(d["ci"].size * nn)
+        halo = np.zeros(d["halo_col"].size * nn)
+        st = self._lib.bcs_partition_gather_values(self.h, i, A.n_cells, A.nFaces(), A.n, N.ptr(A.diag),
+                                                   N.ptr(A.upper), N.ptr(A.lower), N.ptr(loc), N.ptr(halo))
+        if st != N.BCS_OK:
+            _raise(st, self._lib.bcs_last_error(None).decode())
+        return loc, halo
+
     def exchange(self, i: int) -> dict:
         """Per-process halo exchange plan of engine i (see bcs_partition_exchange_get)."""
         ns, nr = ctypes.c_int(), ctypes.c_int()

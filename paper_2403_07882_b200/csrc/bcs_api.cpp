@@ -387,6 +387,17 @@ bcs_status bcs_partition_exchange_get(const bcs_partition* p, int part, int32_t*
     });
 }
 
+bcs_status bcs_partition_gather_values(const bcs_partition* p, int part, int n_cells, int n_faces, int block_size,
+                                       const double* diag, const double* upper, const double* lower,
+                                       double* local_values, double* halo_values) {
+    return guarded(nullptr, [&] {
+        if (!p || part < 0 || part >= static_cast<int>(p->parts.size())) throw std::invalid_argument("bad partition index");
+        if (block_size < 1 || block_size > 5) throw std::invalid_argument("bcs: block size must be 1..5");
+        bcs::gatherPartValues(p->parts[part], n_cells, n_faces, block_size, diag, upper, lower, local_values,
+                              halo_values, 8);
+    });
+}
+
 bcs_status bcs_comm_unique_id(unsigned char id[128]) {
     return guarded(nullptr, [&] { bcs::Engine::commUniqueId(id); });
 }

@@ -67,9 +67,15 @@ const Api& api() {
         throw std::runtime_error("bcs: NCCL (libnccl.so.2) not found; set BCS_NCCL_LIB");
     return a;
 }
-void ck(ncclResult_t r, const char* what) {
+// NCCL failures surface as the reference's distributed-failure runtime_error
+// (MailboxNetwork::receive / partitionedMatvec, partition.cpp:254-267, 345-347),
+// naming this rank (and the peer for point-to-point operations)
+int g_rank = 0;
+void ck(ncclResult_t r, const char* what, int peer = -1) {
     if (r != ncclSuccess)
-        throw std::runtime_error(std::string("bcs: NCCL ") + what + ": " + (api().errorString ? api().errorString(r) : "error"));
+        throw std::runtime_error("distributed failure: rank " + std::to_string(g_rank) + " NCCL " + what +
+                                 (peer >= 0 ? " with rank " + std::to_string(peer) : std::string()) + ": " +
+                                 (api().errorString ? api().errorString(r) : "error"));
 }
 }  // namespace nccl
 
@@ -149,6 +155,7 @@ Engine::Engine(int device) : device_(device) {
     uint64_t thr = std::numeric_limits<uint64_t>::max();
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     check(cudaMallocHost(reinterpret_cast<void**>(&hStatus_), 8 * sizeof(double)), "cudaMallocHost");
+    check(cudaMallocHost(reinterpret_cast<void**>(&hTot_), 2 * 64 * sizeof(int)), "cudaMallocHost");
     check(cudaEventCreate(&ev0_), "cudaEventCreate");
     check(cudaEventCreate(&ev1_), "cudaEventCreate");
     err_.ensure(4, stream_);
@@ -188,11 +195,18 @@ Engine::~Engine() {
             rel(L.y); rel(L.zb);
         }
         rel(P.H.dense); rel(P.H.dpiv);
+        P.H.arena.release(stream_);
     }
+    main_.arena.release(stream_);
     cudaStreamSynchronize(stream_);
     for (void* p : stage_) cudaFreeHost(p);
+    if (mpStage_) cudaFreeHost(mpStage_);
+    if (mpEvPack_) cudaEventDestroy(mpEvPack_);
+    if (mpEvComm_) cudaEventDestroy(mpEvComm_);
+    if (commStream_) cudaStreamDestroy(commStream_);
     for (cudaEvent_t e : stageEv_) cudaEventDestroy(e);
     if (hStatus_) cudaFreeHost(hStatus_);
+    if (hTot_) cudaFreeHost(hTot_);
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
     for (auto& e : evPool_) {
@@ -674,7 +688,7 @@ static KahnWork kahnWork(DArray<int>& cnt, DArray<int>& push, DArray<int>& lvl, 
 // DILU smoothers of levels [0, nl) (preconditioner.cpp:101-126): dependency
 // levels per matrix, then ONE sync-free factorisation over all of them
 // (tickets ordered by dependency level, then matrix), then the sweeps' data.
-void Engine::diluSetupAll(int nl) {
+void Engine::diluSetupAll(int nl, const bcs_solver_config* cfg) {
     const size_t nn = static_cast<size_t>(n_) * n_;
     const int big = std::numeric_limits<int>::max();
     if (diluMode_ != 0) {  // Kahn-rounds variant (BCS_DILU_MODE=1), level by level
@@ -692,8 +706,8 @@ void Engine::diluSetupAll(int nl) {
             const int cell = readErrCell();
             if (cell != big)
                 throw std::runtime_error("DILU setup: singular modified diagonal in cell " + std::to_string(cell));
-            finishSmoother(L);
         }
+        finishSmoothers(nl, nullptr);
         return;
     }
     size_t totalRows = 0, totalT = 0, maxRows = 0;
@@ -724,23 +738,39 @@ void Engine::diluSetupAll(int nl) {
     // slots only) and released when the factorisation is done
     std::vector<DiluLevelHost> desc(nl);
     size_t toff = 0;
+    {
+        // setup phase of the arena: tc + lpre per level and T (lower slots:
+        // (nnz - rows) / 2 blocks, the patterns being structurally symmetric)
+        size_t bytes = 0;
+        for (int l = 0; l < nl; ++l) {
+            const Level& L = H_->levels[l];
+            bytes += PhaseArena::al(sizeof(int) * (static_cast<size_t>(L.rows) + 1)) +
+                     PhaseArena::al(sizeof(int) * static_cast<size_t>(L.nnz));
+            totalT += (static_cast<size_t>(L.nnz) - L.rows) / 2 * nn;
+        }
+        H_->arena.reserve(bytes + PhaseArena::al(sizeof(double) * (totalT + 1)), stream_);
+        for (int l = 0; l < nl; ++l) {
+            Level& L = H_->levels[l];
+            L.lpre.borrow(H_->arena.take<int>(static_cast<size_t>(L.rows) + 1), static_cast<size_t>(L.rows) + 1, stream_);
+            L.tc.borrow(H_->arena.take<int>(L.nnz), L.nnz, stream_);
+        }
+        tblk_.borrow(H_->arena.take<double>(totalT + 1), totalT + 1, stream_);
+    }
     for (int l = 0; l < nl; ++l) {
         Level& L = H_->levels[l];
-        L.lpre.ensure(static_cast<size_t>(L.rows) + 1, stream_);
-        L.tc.ensure(L.nnz, stream_);
         scanTmp_.ensure(scan_tmp_ints(static_cast<size_t>(L.rows) + 1) + 16, stream_);
         const size_t lower = dilu_compact_index(L.rows, L.ro, L.dg, L.ci, L.tpos, L.lpre.p, L.tc.p, push_.p + 9,
                                                 scanTmp_.p, stream_);
         desc[l] = {L.rows, L.ro, L.dg, L.tpos, L.tc.p, L.lpre.p, L.dlev.p, L.v, L.lu.p, L.piv.p, toff};
         toff += lower * nn;
     }
+    if (toff > totalT) throw std::logic_error("bcs: DILU scratch larger than its lower-slot bound");
     totalT = toff;
     const size_t buckets = static_cast<size_t>(maxdepth) * nl + 1;
     dkeys_.ensure(totalRows, stream_);
     dorder_.ensure(totalRows, stream_);
     cnt_.ensure(buckets + 1, stream_);
     scanTmp_.ensure(scan_tmp_ints(buckets + 1) + 16, stream_);
-    tblk_.ensure(totalT, stream_);
     ddesc_.ensure(dilu_desc_bytes(), stream_);
     check(cudaMemcpyAsync(err_.p, &big, sizeof(int), cudaMemcpyHostToDevice, stream_), "err init");
     dilu_setup_multi(n_, nl, desc.data(), maxdepth, dkeys_.p, dorder_.p, cnt_.p, scanTmp_.p, push_.p + 8, ddesc_.p,
@@ -752,46 +782,61 @@ void Engine::diluSetupAll(int nl) {
     if (cell != big)
         throw std::runtime_error("DILU setup: singular modified diagonal in cell " + std::to_string(cell & ((1 << 26) - 1)));
     profMark("dilu:factor");
-    tblk_.release(stream_);
+    finishSmoothers(nl, cfg);
+}
+
+// reciprocals, composed permutations, ticket records and packed slots of
+// levels [0, nl); the sweep programs (and, for a serial GMRES solve, the
+// Krylov basis) are the solve phase of the hierarchy's arena.  cfg == nullptr:
+// no Krylov basis reserved (preconditioner-only setups).
+void Engine::finishSmoothers(int nl, const bcs_solver_config* cfg) {
+    if (nl > 64) throw std::logic_error("bcs: more than 64 smoothed levels");
     for (int l = 0; l < nl; ++l) {
-        H_->levels[l].tc.release(stream_);
-        H_->levels[l].lpre.release(stream_);
-    }
-    for (int l = 0; l < nl; ++l) finishSmoother(H_->levels[l]);
-}
-
-// reciprocals, composed permutations, ticket records and packed slots
-void Engine::finishSmoother(Level& L) {
-    L.rcp.ensure(static_cast<size_t>(L.rows) * n_, stream_);
-    L.perm.ensure(static_cast<size_t>(L.rows) * n_, stream_);
-    make_reciprocals(n_, L.rows, L.lu, L.piv, L.rcp.p, L.perm.p, stream_);
-    L.recf.ensure(4 * static_cast<size_t>(L.rows), stream_);
-    L.recb.ensure(4 * static_cast<size_t>(L.rows), stream_);
-    sweep_records(L.rows, L.order, L.ro, L.dg, L.recf.p, L.recb.p, stream_);
-    profMark("dilu:rcp+records");
-    packSweeps(L);
-    profMark("dilu:pack");
-}
-
-// the two sweeps' per-ticket slots (k_sweep.cu: slot layout)
-void Engine::packSweeps(Level& L) {
-    const size_t n1 = static_cast<size_t>(L.rows) + 1;
-    scanTmp_.ensure(scan_tmp_ints(n1) + 16, stream_);
-    int tot[2] = {0, 0};
-    for (int d = 0; d < 2; ++d) {
-        DArray<int>& off = d == 0 ? L.offf : L.offb;
-        off.ensure(n1, stream_);
-        sweep_slot_sizes(n_, d == 0, L.rows, L.depth, d == 0 ? L.recf : L.recb, off.p, stream_);
-        exclusive_scan(off.p, L.rows, off.p + L.rows, scanTmp_.p, stream_);
-        check(cudaMemcpyAsync(&tot[d], off.p + L.rows, sizeof(int), cudaMemcpyDeviceToHost, stream_), "slot total");
+        Level& L = H_->levels[l];
+        L.rcp.ensure(static_cast<size_t>(L.rows) * n_, stream_);
+        L.perm.ensure(static_cast<size_t>(L.rows) * n_, stream_);
+        make_reciprocals(n_, L.rows, L.lu, L.piv, L.rcp.p, L.perm.p, stream_);
+        L.recf.ensure(4 * static_cast<size_t>(L.rows), stream_);
+        L.recb.ensure(4 * static_cast<size_t>(L.rows), stream_);
+        sweep_records(L.rows, L.order, L.ro, L.dg, L.recf.p, L.recb.p, stream_);
+        const size_t n1 = static_cast<size_t>(L.rows) + 1;
+        scanTmp_.ensure(scan_tmp_ints(n1) + 16, stream_);
+        for (int d = 0; d < 2; ++d) {
+            DArray<int>& off = d == 0 ? L.offf : L.offb;
+            off.ensure(n1, stream_);
+            sweep_slot_sizes(n_, d == 0, L.rows, L.depth, d == 0 ? L.recf : L.recb, off.p, stream_);
+            exclusive_scan(off.p, L.rows, off.p + L.rows, scanTmp_.p, stream_);
+            check(cudaMemcpyAsync(hTot_ + 2 * l + d, off.p + L.rows, sizeof(int), cudaMemcpyDeviceToHost, stream_),
+                  "slot total");
+        }
     }
     sync();
-    for (int d = 0; d < 2; ++d) {
-        DArray<unsigned char>& pk = d == 0 ? L.pkf : L.pkb;
-        pk.ensure(16 * static_cast<size_t>(tot[d]), stream_);
-        sweep_pack(n_, d == 0, L.rows, L.depth, d == 0 ? L.recf : L.recb, L.ci, L.v, L.lu, L.perm, L.rcp,
-                   d == 0 ? L.offf : L.offb, pk.p, stream_);
+    profMark("dilu:rcp+records");
+    size_t bytes = 0;
+    for (int l = 0; l < 2 * nl; ++l) bytes += PhaseArena::al(16 * static_cast<size_t>(hTot_[l]) + 16);
+    // a serial GMRES solve's basis V (and FGMRES's Z) share the phase
+    const bool basis = cfg && H_ == &main_ && !distActive_ &&
+                       (cfg->method == BCS_GMRES || cfg->method == BCS_FGMRES);
+    const size_t N = static_cast<size_t>(H_->levels[0].rows) * n_;
+    const size_t nV = basis ? static_cast<size_t>(cfg->gmres_restart + 1) * N : 0;
+    const size_t nZ = basis && cfg->method == BCS_FGMRES ? static_cast<size_t>(cfg->gmres_restart) * N : 0;
+    if (basis) bytes += PhaseArena::al(nV * sizeof(double)) + (nZ ? PhaseArena::al(nZ * sizeof(double)) : 0);
+    H_->arena.reserve(bytes, stream_);
+    if (basis) {
+        V_.borrow(H_->arena.take<double>(nV), nV, stream_);
+        if (nZ) Z_.borrow(H_->arena.take<double>(nZ), nZ, stream_);
     }
+    for (int l = 0; l < nl; ++l) {
+        Level& L = H_->levels[l];
+        for (int d = 0; d < 2; ++d) {
+            DArray<unsigned char>& pk = d == 0 ? L.pkf : L.pkb;
+            const size_t b = 16 * static_cast<size_t>(hTot_[2 * l + d]) + 16;
+            pk.borrow(H_->arena.take<unsigned char>(b), b, stream_);
+            sweep_pack(n_, d == 0, L.rows, L.depth, d == 0 ? L.recf : L.recb, L.ci, L.v, L.lu, L.perm, L.rcp,
+                       d == 0 ? L.offf : L.offb, pk.p, stream_);
+        }
+    }
+    profMark("dilu:pack");
 }
 
 void Engine::lusgsSetup(Level& L) {
@@ -812,7 +857,7 @@ void Engine::lusgsSetup(Level& L) {
     cudaMemsetAsync(err_.p + 2, 0, sizeof(int), stream_);
     L.depth = level_schedule(L.rows, L.ro, L.ci, L.dg, L.order.p, lvl_.p, cnt_.p, scanTmp_.p, push_.p, err_.p + 2,
                              stream_);
-    finishSmoother(L);
+    finishSmoothers(1, nullptr);
 }
 
 void Engine::buildHierarchy(const bcs_solver_config& cfg) {
@@ -896,11 +941,9 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
         profMark("setup:pattern");
     }
     H_->levels[H_->nlev - 1].ncoarse = 0;
-    keys_.release(stream_);  // setup-phase scratch of the coarsening
-    sorted_.release(stream_);
-    str_.release(stream_);
+
     // DILU smoother on all but the coarsest level (amg.cpp:86-88)
-    diluSetupAll(H_->nlev - 1);
+    diluSetupAll(H_->nlev - 1, &cfg);
     // dense factorisation of the coarsest level (amg.cpp:90-104)
     const Level& Cl = H_->levels[H_->nlev - 1];
     H_->m = Cl.rows * n_;
@@ -985,16 +1028,7 @@ void Engine::buildPrecond(const bcs_solver_config& cfg) {
 
 void Engine::buildPrecondOn(const FineMatrix& F, const bcs_solver_config& cfg) {
     H_->pcKind = -1;
-    // phase-local memory: the previous call's solve-phase arrays (sweep
-    // programs, Krylov basis) go back to the stream-ordered pool before the
-    // setup phase allocates its scratch (Galerkin keys, DILU T), so the peak is
-    // max(setup, solve) rather than their sum (what lets 256^3 fit one B200)
-    for (auto& L : H_->levels) {
-        L.pkf.release(stream_);
-        L.pkb.release(stream_);
-    }
-    V_.release(stream_);
-    Z_.release(stream_);
+
     if (H_->levels.empty()) H_->levels.emplace_back();
     H_->nlev = 1;
     Level& L0 = H_->levels[0];
@@ -1013,7 +1047,7 @@ void Engine::buildPrecondOn(const FineMatrix& F, const bcs_solver_config& cfg) {
             L0.y.ensure(N, stream_);
             break;
         case BCS_PRECOND_DILU:
-            diluSetupAll(1);
+            diluSetupAll(1, &cfg);
             L0.y.ensure(N, stream_);
             break;
         case BCS_PRECOND_AMG: buildHierarchy(cfg); break;
@@ -1343,22 +1377,30 @@ void Engine::opResidual(const double* x, const double* b, double* r) {
 
 // halo exchange of the multi-process Mode R: pack the rows peers need, one
 // grouped NCCL send/recv per peer (peers ascending), values land in mpRecv_
+// The exchange runs on its own stream: pack (engine stream) -> event ->
+// grouped send/recv (comm stream) -> event; the caller's local product runs
+// meanwhile and waits for the event only before the halo couplings, which the
+// reference adds after the local product anyway (partition.cpp:335-350).
 void Engine::mpExchange(const double* x) {
     const auto& A = nccl::api();
+    nccl::g_rank = mpRank_;
     pack_rows(n_, mpSendRows_, mpSendIdx_, x, mpSend_.p, stream_);
+    check(cudaEventRecord(mpEvPack_, stream_), "record pack");
+    check(cudaStreamWaitEvent(commStream_, mpEvPack_, 0), "wait pack");
     nccl::ck(A.groupStart(), "group start");
     size_t so = 0, ro = 0;
     for (int q = 0; q < mpSize_; ++q) {
         if (mpSendCnt_[q])
             nccl::ck(A.send(mpSend_.p + so * n_, static_cast<size_t>(mpSendCnt_[q]) * n_, ncclDouble, q,
-                            static_cast<ncclComm_t>(comm_), stream_), "send");
+                            static_cast<ncclComm_t>(comm_), commStream_), "send", q);
         if (mpRecvCnt_[q])
             nccl::ck(A.recv(mpRecv_.p + ro * n_, static_cast<size_t>(mpRecvCnt_[q]) * n_, ncclDouble, q,
-                            static_cast<ncclComm_t>(comm_), stream_), "recv");
+                            static_cast<ncclComm_t>(comm_), commStream_), "recv", q);
         so += mpSendCnt_[q];
         ro += mpRecvCnt_[q];
     }
     nccl::ck(A.groupEnd(), "group end");
+    check(cudaEventRecord(mpEvComm_, commStream_), "record comm");
 }
 
 // partitionedMatvec (partition.cpp:298-352): every engine's local product on
@@ -1372,7 +1414,8 @@ void Engine::opSpmv(const double* x, double* y) {
     if (mpActive_) {  // this process's engine; halo columns index the receive buffer
         DistPart& P = dist_[0];
         mpExchange(x);
-        spmv(n_, P.rows, P.ro, P.ci, P.vals, x, nullptr, y, stream_);
+        spmv(n_, P.rows, P.ro, P.ci, P.vals, x, nullptr, y, stream_);  // overlaps the exchange
+        check(cudaStreamWaitEvent(stream_, mpEvComm_, 0), "wait comm");
         halo_spmv(n_, P.nhr, P.hrow, P.hoff, P.hcol, P.hvals, mpRecv_, y, 0, stream_);
         return;
     }
@@ -1636,8 +1679,14 @@ void Engine::commInit(int rank, int size, const unsigned char id[128]) {
     ncclUniqueId u;
     std::memcpy(&u, id, sizeof u);
     ncclComm_t c = nullptr;
+    nccl::g_rank = rank;
     nccl::ck(A.commInitRank(&c, size, u, rank), "comm init");
     comm_ = c;
+    if (!commStream_) {
+        check(cudaStreamCreateWithFlags(&commStream_, cudaStreamNonBlocking), "cudaStreamCreate comm");
+        check(cudaEventCreateWithFlags(&mpEvPack_, cudaEventDisableTiming), "cudaEventCreate");
+        check(cudaEventCreateWithFlags(&mpEvComm_, cudaEventDisableTiming), "cudaEventCreate");
+    }
     mpRank_ = rank;
     mpSize_ = size;
     mpNc_ = -1;  // topology cache belongs to the previous communicator
@@ -1651,6 +1700,7 @@ void Engine::mpSetupTopology(int nc, int nf, int n, const int32_t* owner, const 
     const ConsolidationPlan plan = makeConsolidationPlan(dec, mpSize_);
     const std::vector<Partition> eng = consolidate(parts, plan, dec);
     const ExchangePlan xp = makeExchangePlan(eng, mpRank_);
+    mpPart = eng[mpRank_];  // host slot sources for the per-rank upload
     dist_.resize(1);
     uploadEnginePart(dist_[0], eng[mpRank_], n, &xp.haloRecvIdx);
     mpRows_ = dist_[0].rows;
@@ -1706,16 +1756,26 @@ void Engine::distSolveMP(int nc, int nf, int n, const int32_t* owner, const int3
     n_ = n;
     DistPart& P = dist_[0];
     const size_t nn = static_cast<size_t>(n) * n;
-    ldu_diag_.ensure(nc * nn, stream_);
-    ldu_upper_.ensure(nf * nn, stream_);
-    ldu_lower_.ensure(nf * nn, stream_);
-    h2d(ldu_diag_.p, diag, sizeof(double) * nc * nn, "H2D");
-    if (nf) {
-        h2d(ldu_upper_.p, upper, sizeof(double) * nf * nn, "H2D");
-        h2d(ldu_lower_.p, lower, sizeof(double) * nf * nn, "H2D");
+    // upload (partition.cpp:384-407): only this engine's local and halo blocks
+    // cross PCIe, gathered on the host into page-locked staging in slot order
+    {
+        const size_t cnt = (static_cast<size_t>(P.nnz) + P.nh) * nn;
+        if (mpStageCap_ < cnt) {
+            if (mpStage_) cudaFreeHost(mpStage_);
+            mpStage_ = nullptr;
+            mpStageCap_ = 0;
+            check(cudaHostAlloc(reinterpret_cast<void**>(&mpStage_), cnt * sizeof(double), cudaHostAllocPortable),
+                  "cudaHostAlloc upload staging");
+            mpStageCap_ = cnt;
+        }
+        sync();  // the previous call's copies out of the staging buffer are done
+        gatherPartValues(mpPart, nc, nf, n, diag, upper, lower, mpStage_, mpStage_ + static_cast<size_t>(P.nnz) * nn,
+                         8);
+        check(cudaMemcpyAsync(P.vals.p, mpStage_, sizeof(double) * P.nnz * nn, cudaMemcpyHostToDevice, stream_), "H2D");
+        if (P.nh)
+            check(cudaMemcpyAsync(P.hvals.p, mpStage_ + static_cast<size_t>(P.nnz) * nn, sizeof(double) * P.nh * nn,
+                                  cudaMemcpyHostToDevice, stream_), "H2D halo");
     }
-    gather_values(n, P.nnz, nc, nf, P.src, ldu_diag_, ldu_upper_, ldu_lower_, P.vals.p, stream_);
-    if (P.nh) gather_values(n, P.nh, nc, nf, P.hsrc, ldu_diag_, ldu_upper_, ldu_lower_, P.hvals.p, stream_);
     // this engine's slice of scatterVector (partition.cpp:269-280)
     const size_t Nl = static_cast<size_t>(mpRows_) * n;
     std::vector<double> hb(Nl), hx(Nl);
@@ -1991,7 +2051,10 @@ void Engine::amgLevelGet(int l, int32_t* ro, int32_t* ci, double* v, int32_t* ag
 
 std::string Engine::memoryReport() const {
     std::map<std::string, double> m;
-    auto add = [&](const char* k, const auto& a) { m[k] += static_cast<double>(a.cap) * sizeof(*a.p); };
+    // owned arrays only; arena views are counted once, as the arena
+    auto add = [&](const char* k, const auto& a) {
+        if (a.owned) m[k] += static_cast<double>(a.cap) * sizeof(*a.p);
+    };
     auto hier = [&](const Hier& H, bool fine) {
         for (size_t l = 0; l < H.levels.size(); ++l) {
             const Level& L = H.levels[l];
@@ -2007,6 +2070,7 @@ std::string Engine::memoryReport() const {
             add("vcycle_vectors", L.y); add("vcycle_vectors", L.zb);
         }
         add("dense_coarsest", H.dense); add("dense_coarsest", H.dpiv); add("schedule", H.tailDesc);
+        m["phase_arena (DILU scratch | sweep programs + Krylov basis)"] += static_cast<double>(H.arena.cap);
         (void)fine;
     };
     hier(main_, true);

@@ -29,21 +29,65 @@ template <class T>
 struct DArray {
     T* p = nullptr;
     size_t cap = 0;
+    bool owned = true;  // false: a view into a PhaseArena (never freed here)
     void ensure(size_t n, cudaStream_t s) {
         if (n <= cap && p) return;
-        if (p) check(cudaFreeAsync(p, s), "cudaFreeAsync");
+        if (p && owned) check(cudaFreeAsync(p, s), "cudaFreeAsync");
         p = nullptr;
         cap = 0;
+        owned = true;
         const size_t bytes = (n ? n : 1) * sizeof(T);
         check(cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, s), "cudaMallocAsync");
         cap = n ? n : 1;
     }
+    // point at n elements of arena memory (valid until the arena's next phase)
+    void borrow(T* q, size_t n, cudaStream_t s) {
+        if (p && owned) cudaFreeAsync(p, s);
+        p = q;
+        cap = n;
+        owned = false;
+    }
     void release(cudaStream_t s) {
-        if (p) cudaFreeAsync(p, s);
+        if (p && owned) cudaFreeAsync(p, s);
         p = nullptr;
         cap = 0;
+        owned = true;
     }
     operator T*() const { return p; }
+};
+
+// Memory whose lifetime is one phase of a solve: the DILU factorisation's
+// scratch (T, setup phase) and the sweep programs + Krylov basis (solve
+// phase) never coexist, so they share one buffer (peak = max of the phases,
+// not their sum).  reserve() starts a phase: it re-allocates only when the
+// phase needs more than the buffer holds (first solve / bigger system); in
+// steady state no allocator call happens.
+struct PhaseArena {
+    char* base = nullptr;
+    size_t cap = 0, off = 0;
+    static size_t al(size_t b) { return (b + 255) & ~static_cast<size_t>(255); }
+    void reserve(size_t bytes, cudaStream_t s) {
+        off = 0;
+        if (bytes <= cap) return;
+        if (base) check(cudaFreeAsync(base, s), "cudaFreeAsync arena");
+        base = nullptr;
+        cap = 0;
+        check(cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, s), "cudaMallocAsync arena");
+        cap = bytes;
+    }
+    template <class T>
+    T* take(size_t n) {
+        const size_t b = al(n * sizeof(T));
+        if (off + b > cap) throw std::logic_error("bcs: phase arena overflow");
+        T* q = reinterpret_cast<T*>(base + off);
+        off += b;
+        return q;
+    }
+    void release(cudaStream_t s) {
+        if (base) cudaFreeAsync(base, s);
+        base = nullptr;
+        cap = off = 0;
+    }
 };
 
 struct Level {
@@ -82,6 +126,7 @@ struct Hier {
     int tail = -1;    // first level of the one-CTA coarse tail (-1: none)
     DArray<unsigned char> tailDesc;  // TailLevelDev[nlev - tail]
     bcs_solver_config pcCfg{};
+    PhaseArena arena;  // DILU scratch (setup phase) / sweep programs + Krylov basis (solve phase)
 };
 
 // One Mode-R engine on the device: its consolidated local BSR (local
@@ -183,10 +228,10 @@ private:
     FineMatrix serialFine() const;
     void buildHierarchy(const bcs_solver_config& cfg);
     void setupLevelPattern(Level& L);
-    void diluSetupAll(int nl);
-    void finishSmoother(Level& L);
+    void diluSetupAll(int nl, const bcs_solver_config* cfg);
+    void finishSmoothers(int nl, const bcs_solver_config* cfg);
     void lusgsSetup(Level& L);
-    void packSweeps(Level& L);
+
     void applyPrecond(const double* r, double* z);
     void smootherApply(Level& L, const double* r, double* z, int accumulate);
     void vcycle(int l, const double* r, double* z);
@@ -279,6 +324,11 @@ private:
     std::vector<double> mpCen_;
     std::vector<int> mpNewToOld_;
     void mpExchange(const double* x);
+    Partition mpPart;                  // this process's engine (host slot sources)
+    double* mpStage_ = nullptr;        // pinned per-rank upload staging
+    size_t mpStageCap_ = 0;
+    cudaStream_t commStream_ = nullptr;
+    cudaEvent_t mpEvPack_ = nullptr, mpEvComm_ = nullptr;
     std::vector<DistPart> dist_;
     std::vector<int32_t> distOwner_, distNeigh_;
     std::vector<double> distCen_;
@@ -294,6 +344,7 @@ private:
     int diluMode_ = 0;  // 0 sync-free level-ordered DILU setup, 1 Kahn levels
     int denseBlockedMin_ = kDenseBlockedMin;  // coarsest m from which the blocked dense LU/solve run
     int tailMaxRows_ = kTailMaxRows;          // levels at most this big run in the one-CTA tail (0: off)
+    int* hTot_ = nullptr;                     // pinned: per-level sweep program sizes
     void setupTail();
     std::vector<std::pair<std::string, double>> profRec_;
     std::chrono::steady_clock::time_point profT_;

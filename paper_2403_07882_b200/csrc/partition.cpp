@@ -3,6 +3,10 @@
 #include "partition.hpp"
 
 #include <algorithm>
+#include <cstring>
+#include <thread>
+
+#include <algorithm>
 #include <cstdint>
 #include <numeric>
 #include <stdexcept>
@@ -232,6 +236,35 @@ ExchangePlan makeExchangePlan(const std::vector<Partition>& engines, int me) {
         x.haloRecvIdx[h] = it->second;
     }
     return x;
+}
+
+namespace {
+void gatherBlocks(const std::vector<int>& src, int nCells, int nFaces, size_t nn, const double* diag,
+                  const double* upper, const double* lower, double* out, int threads) {
+    const size_t cnt = src.size();
+    if (!cnt) return;
+    auto work = [&](size_t b, size_t e) {
+        for (size_t k = b; k < e; ++k) {
+            const int id = src[k];
+            const double* from = id < nCells ? diag + static_cast<size_t>(id) * nn
+                                 : id < nCells + nFaces ? upper + static_cast<size_t>(id - nCells) * nn
+                                                        : lower + static_cast<size_t>(id - nCells - nFaces) * nn;
+            std::memcpy(out + k * nn, from, nn * sizeof(double));
+        }
+    };
+    const int T = std::max(1, std::min<int>(threads, static_cast<int>(cnt / 4096 + 1)));
+    std::vector<std::thread> pool;
+    for (int t = 1; t < T; ++t) pool.emplace_back(work, cnt * t / T, cnt * (t + 1) / T);
+    work(0, cnt / T);
+    for (auto& th : pool) th.join();
+}
+}  // namespace
+
+void gatherPartValues(const Partition& p, int nCells, int nFaces, int n, const double* diag, const double* upper,
+                      const double* lower, double* localVals, double* haloVals, int threads) {
+    const size_t nn = static_cast<size_t>(n) * n;
+    if (localVals) gatherBlocks(p.src, nCells, nFaces, nn, diag, upper, lower, localVals, threads);
+    if (haloVals) gatherBlocks(p.haloSrc, nCells, nFaces, nn, diag, upper, lower, haloVals, threads);
 }
 
 }  // namespace bcs

@@ -62,4 +62,13 @@ struct ExchangePlan {
 };
 ExchangePlan makeExchangePlan(const std::vector<Partition>& engines, int me);
 
+// The reference's per-rank "upload" (partition.cpp:384-407, the paper's
+// per-partition NExternalNZ arrays) on the host: the LDU
+// blocks of one engine's local slots (slot order) and halo entries (entry
+// order), n*n doubles each, gathered from the caller's face-addressed arrays
+// by `threads` host threads over contiguous slot ranges.  Only these bytes
+// cross PCIe to that engine's GPU (about 1/G of the system).
+void gatherPartValues(const Partition& p, int nCells, int nFaces, int n, const double* diag, const double* upper,
+                      const double* lower, double* localVals, double* haloVals, int threads);
+
 }  // namespace bcs

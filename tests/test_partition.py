@@ -180,3 +180,57 @@ def test_gloo_world2_exchange_plan(ranks):
         p.join(timeout=60)
     assert all(ok for _, ok, _ in res), res
     assert all(n > 0 for _, _, n in res)
+
+
+def _gloo_upload_worker(rank, world, port, ranks, q):
+    """One process per engine: the per-rank upload (bcs_partition_gather_values,
+    what bcs_dist_solve_mp ships to its GPU) equals the reference's consolidated
+    partition of that engine (local BSR values and halo blocks, bit for bit), and
+    the engines' uploads together hold every LDU block exactly once as a local
+    slot or once per coupling as a halo entry."""
+    import torch
+    import torch.distributed as dist
+    from oracle_lib import Reference, ref_partition
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        s = gen.hex_euler(7, 6, 5, scramble_seed=3)
+        A = s.A
+        P = bcs.Partition(A.n_cells, A.owner, A.neighbour, s.centroids, ranks, world)
+        loc, halo = P.gather_values(rank, A)
+        refp = ref_partition(Reference(), A, s.centroids, ranks, world)[rank]
+        ok = loc.tobytes() == refp["vals"].tobytes() and halo.tobytes() == refp["halo_vals"].tobytes()
+        # every LDU block is uploaded exactly once: a local slot or a halo entry of one engine
+        d = P.part(rank)
+        mine = np.concatenate([d["src"], d["halo_src"]]).astype(np.int64)
+        counts = torch.zeros(A.n_cells + 2 * A.nFaces(), dtype=torch.int64)
+        counts.index_add_(0, torch.from_numpy(mine), torch.ones(mine.size, dtype=torch.int64))
+        dist.all_reduce(counts)
+        ok = ok and bool((counts == 1).all())
+        q.put((rank, bool(ok), int(loc.size + halo.size)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                                    "oracle", "_ref", "libbcs_ref.so")), reason="oracle/_ref not built")
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_gloo_world2_per_rank_upload(ranks):
+    import multiprocessing as mp
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_upload_worker, args=(r, 2, port, ranks, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _ in res), res
+    s = gen.hex_euler(7, 6, 5, scramble_seed=3)
+    # each engine uploads about half of the system, not all of it
+    assert all(n < 0.75 * (s.A.diag.size + s.A.upper.size + s.A.lower.size) for _, _, n in res)
