@@ -341,6 +341,14 @@ bcs_status bcs_selftest_hypot(const double* x, const double* y, double* out, int
  * *needed = length + 1; buf may be NULL (size query). */
 bcs_status bcs_memory_report(bcs_ctx* ctx, char* buf, size_t cap, size_t* needed);
 
+/* Performance mode: the multicolouring of level `level`'s smoother after a
+ * BCS_MODE_PERF setup: *n_colors (0 when the level is smoothed in natural
+ * order), if perm != NULL its row order perm[new] = row (rows sorted by
+ * (colour, row)) and if color_offsets != NULL the n_colors + 1 boundaries of
+ * the colours in that order; the smoother is the natural-order DILU of the
+ * symmetrically permuted level matrix. */
+bcs_status bcs_level_coloring(bcs_ctx* ctx, int level, int* n_colors, int32_t* perm, int32_t* color_offsets);
+
 /* Device self-tests (diagnostics).  what = 0: the sweeps' reciprocal-based
  * exact division against IEEE __ddiv_rn on n random operand pairs; *result =
  * number of bit mismatches (must be 0).  what = 10..14: total ns of n cross-SM

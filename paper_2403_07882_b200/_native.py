@@ -125,6 +125,7 @@ SIGNATURES = {
     "bcs_level_schedule_depth": (c_int, [c_void_p, c_int, P(c_int)]),
     "bcs_memory_report": (c_int, [c_void_p, ctypes.c_char_p, ctypes.c_size_t, P(ctypes.c_size_t)]),
     "bcs_selftest_hypot": (c_int, [c_void_p, c_void_p, c_void_p, c_int]),
+    "bcs_level_coloring": (c_int, [c_void_p, c_int, P(c_int), c_void_p, c_void_p]),
     "bcs_partition_gather_values": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,
                                             c_void_p, c_void_p]),
     "bcs_dist_solve": (c_int, [c_void_p, c_int, c_int, c_int] + [c_void_p] * 9 + [c_int, c_int, P(SolverConfigC), P(ReportC)]),

@@ -371,6 +371,18 @@ class Context:
         self._ck(self._lib.bcs_memory_report(self.h, buf, need.value + 16, ctypes.byref(need)))
         return json.loads(buf.value.decode())
 
+    def level_coloring(self, level: int):
+        """(n_colors, perm, color_offsets) of a level's performance-mode smoother
+        (n_colors 0: natural order; perm[new] = row; colour c = perm[off[c]:off[c+1]])."""
+        nc = ctypes.c_int()
+        self._ck(self._lib.bcs_level_coloring(self.h, level, ctypes.byref(nc), None, None))
+        if nc.value == 0:
+            return 0, None, None
+        perm = np.zeros(self.amg_level_rows(level), np.int32)
+        off = np.zeros(nc.value + 1, np.int32)
+        self._ck(self._lib.bcs_level_coloring(self.h, level, ctypes.byref(nc), N.ptr(perm), N.ptr(off)))
+        return nc.value, perm, off
+
     def schedule_depth(self, level: int) -> int:
         d = ctypes.c_int()
         self._ck(self._lib.bcs_level_schedule_depth(self.h, level, ctypes.byref(d)))

@@ -596,6 +596,13 @@ bcs_status bcs_memory_report(bcs_ctx* ctx, char* buf, size_t cap, size_t* needed
     });
 }
 
+bcs_status bcs_level_coloring(bcs_ctx* ctx, int level, int* n_colors, int32_t* perm, int32_t* color_offsets) {
+    return guarded(ctx, [&] {
+        const int c = eng(ctx).levelColoring(level, perm, color_offsets);
+        if (n_colors) *n_colors = c;
+    });
+}
+
 bcs_status bcs_level_schedule_depth(bcs_ctx* ctx, int level, int* depth) {
     return guarded(ctx, [&] {
         if (depth) *depth = eng(ctx).scheduleDepth(level);

@@ -177,6 +177,13 @@ Engine::~Engine() {
     // free explicitly to keep long-lived processes lean
     auto rel = [&](auto& a) { a.release(stream_); };
     for (auto& L : main_.levels) {
+        if (L.mc) {
+            Level& M = *L.mc;
+            rel(M.o_ro); rel(M.o_ci); rel(M.o_dg); rel(M.o_tpos); rel(M.o_v); rel(M.lu); rel(M.rcp); rel(M.perm);
+            rel(M.recf); rel(M.recb); rel(M.dlev); rel(M.offf); rel(M.offb); rel(M.piv); rel(M.order);
+            rel(M.r); rel(M.y); rel(M.zb);
+        }
+        rel(L.mcPerm);
         rel(L.o_ro); rel(L.o_ci); rel(L.o_dg); rel(L.o_tpos); rel(L.o_v); rel(L.lu); rel(L.rcp); rel(L.perm); rel(L.recf); rel(L.recb); rel(L.dlev); rel(L.offf); rel(L.offb); rel(L.pkf); rel(L.pkb); rel(L.piv); rel(L.order);
         rel(L.agg); rel(L.members); rel(L.r); rel(L.z); rel(L.res); rel(L.y); rel(L.zb);
     }
@@ -185,7 +192,7 @@ Engine::~Engine() {
     rel(scanTmp_); rel(dkeys_); rel(dorder_); rel(ddesc_); rel(act2_); rel(flag_); rel(err_); rel(ctr_); rel(choice_); rel(segOff_); rel(cro_); rel(big_); rel(dn_); rel(tblk_);
     rel(str_); rel(keys_); rel(sorted_); rel(V_); rel(w_); rel(zk_); rel(rk_); rel(Hm_); rel(cs_); rel(sn_); rel(g_);
     rel(y_); rel(scal_); rel(partials_); rel(kb_); rel(kx_); rel(bp_); rel(bv_); rel(bs_); rel(bt_); rel(bph_);
-    rel(bsh_); rel(brh_); rel(ticket_); rel(seg_); rel(distTmp_);
+    rel(bsh_); rel(brh_); rel(ticket_); rel(seg_); rel(distTmp_); rel(mcSv_);
     for (auto& P : dist_) {
         rel(P.ro); rel(P.ci); rel(P.src); rel(P.dg); rel(P.tpos); rel(P.vals); rel(P.hrow); rel(P.hoff);
         rel(P.hcol); rel(P.hsrc); rel(P.hvals);
@@ -685,15 +692,16 @@ static KahnWork kahnWork(DArray<int>& cnt, DArray<int>& push, DArray<int>& lvl, 
     return KahnWork{cnt.p, push.p, lvl.p, lvl2};
 }
 
-// DILU smoothers of levels [0, nl) (preconditioner.cpp:101-126): dependency
+// DILU smoothers of the levels lv (preconditioner.cpp:101-126): dependency
 // levels per matrix, then ONE sync-free factorisation over all of them
 // (tickets ordered by dependency level, then matrix), then the sweeps' data.
-void Engine::diluSetupAll(int nl, const bcs_solver_config* cfg) {
+void Engine::diluSetupAll(const std::vector<Level*>& lv, const bcs_solver_config* cfg) {
+    const int nl = static_cast<int>(lv.size());
     const size_t nn = static_cast<size_t>(n_) * n_;
     const int big = std::numeric_limits<int>::max();
     if (diluMode_ != 0) {  // Kahn-rounds variant (BCS_DILU_MODE=1), level by level
         for (int l = 0; l < nl; ++l) {
-            Level& L = H_->levels[l];
+            Level& L = *lv[l];
             L.lu.ensure(L.rows * nn, stream_);
             L.piv.ensure(static_cast<size_t>(L.rows) * n_, stream_);
             L.order.ensure(L.rows, stream_);
@@ -707,7 +715,7 @@ void Engine::diluSetupAll(int nl, const bcs_solver_config* cfg) {
             if (cell != big)
                 throw std::runtime_error("DILU setup: singular modified diagonal in cell " + std::to_string(cell));
         }
-        finishSmoothers(nl, nullptr);
+        finishSmoothers(lv, nullptr);
         return;
     }
     size_t totalRows = 0, totalT = 0, maxRows = 0;
@@ -715,7 +723,7 @@ void Engine::diluSetupAll(int nl, const bcs_solver_config* cfg) {
     cudaMemsetAsync(err_.p + 2, 0, sizeof(int), stream_);
     std::vector<LevelsHost> lh(nl);
     for (int l = 0; l < nl; ++l) {
-        Level& L = H_->levels[l];
+        Level& L = *lv[l];
         L.lu.ensure(L.rows * nn, stream_);
         L.piv.ensure(static_cast<size_t>(L.rows) * n_, stream_);
         L.order.ensure(L.rows, stream_);
@@ -730,7 +738,7 @@ void Engine::diluSetupAll(int nl, const bcs_solver_config* cfg) {
     std::vector<int> depth(nl, 0);
     level_schedule_multi(nl, lh.data(), depth.data(), cnt_.p, scanTmp_.p, push_.p, ddesc_.p, err_.p + 2, stream_);
     for (int l = 0; l < nl; ++l) {
-        H_->levels[l].depth = depth[l];
+        lv[l]->depth = depth[l];
         maxdepth = std::max(maxdepth, depth[l]);
     }
     profMark("dilu:levels");
@@ -743,21 +751,21 @@ void Engine::diluSetupAll(int nl, const bcs_solver_config* cfg) {
         // (nnz - rows) / 2 blocks, the patterns being structurally symmetric)
         size_t bytes = 0;
         for (int l = 0; l < nl; ++l) {
-            const Level& L = H_->levels[l];
+            const Level& L = *lv[l];
             bytes += PhaseArena::al(sizeof(int) * (static_cast<size_t>(L.rows) + 1)) +
                      PhaseArena::al(sizeof(int) * static_cast<size_t>(L.nnz));
             totalT += (static_cast<size_t>(L.nnz) - L.rows) / 2 * nn;
         }
         H_->arena.reserve(bytes + PhaseArena::al(sizeof(double) * (totalT + 1)), stream_);
         for (int l = 0; l < nl; ++l) {
-            Level& L = H_->levels[l];
+            Level& L = *lv[l];
             L.lpre.borrow(H_->arena.take<int>(static_cast<size_t>(L.rows) + 1), static_cast<size_t>(L.rows) + 1, stream_);
             L.tc.borrow(H_->arena.take<int>(L.nnz), L.nnz, stream_);
         }
         tblk_.borrow(H_->arena.take<double>(totalT + 1), totalT + 1, stream_);
     }
     for (int l = 0; l < nl; ++l) {
-        Level& L = H_->levels[l];
+        Level& L = *lv[l];
         scanTmp_.ensure(scan_tmp_ints(static_cast<size_t>(L.rows) + 1) + 16, stream_);
         const size_t lower = dilu_compact_index(L.rows, L.ro, L.dg, L.ci, L.tpos, L.lpre.p, L.tc.p, push_.p + 9,
                                                 scanTmp_.p, stream_);
@@ -782,17 +790,18 @@ void Engine::diluSetupAll(int nl, const bcs_solver_config* cfg) {
     if (cell != big)
         throw std::runtime_error("DILU setup: singular modified diagonal in cell " + std::to_string(cell & ((1 << 26) - 1)));
     profMark("dilu:factor");
-    finishSmoothers(nl, cfg);
+    finishSmoothers(lv, cfg);
 }
 
 // reciprocals, composed permutations, ticket records and packed slots of
-// levels [0, nl); the sweep programs (and, for a serial GMRES solve, the
+// the levels lv; the sweep programs (and, for a serial GMRES solve, the
 // Krylov basis) are the solve phase of the hierarchy's arena.  cfg == nullptr:
 // no Krylov basis reserved (preconditioner-only setups).
-void Engine::finishSmoothers(int nl, const bcs_solver_config* cfg) {
+void Engine::finishSmoothers(const std::vector<Level*>& lv, const bcs_solver_config* cfg) {
+    const int nl = static_cast<int>(lv.size());
     if (nl > 64) throw std::logic_error("bcs: more than 64 smoothed levels");
     for (int l = 0; l < nl; ++l) {
-        Level& L = H_->levels[l];
+        Level& L = *lv[l];
         L.rcp.ensure(static_cast<size_t>(L.rows) * n_, stream_);
         L.perm.ensure(static_cast<size_t>(L.rows) * n_, stream_);
         make_reciprocals(n_, L.rows, L.lu, L.piv, L.rcp.p, L.perm.p, stream_);
@@ -827,7 +836,7 @@ void Engine::finishSmoothers(int nl, const bcs_solver_config* cfg) {
         if (nZ) Z_.borrow(H_->arena.take<double>(nZ), nZ, stream_);
     }
     for (int l = 0; l < nl; ++l) {
-        Level& L = H_->levels[l];
+        Level& L = *lv[l];
         for (int d = 0; d < 2; ++d) {
             DArray<unsigned char>& pk = d == 0 ? L.pkf : L.pkb;
             const size_t b = 16 * static_cast<size_t>(hTot_[2 * l + d]) + 16;
@@ -857,7 +866,7 @@ void Engine::lusgsSetup(Level& L) {
     cudaMemsetAsync(err_.p + 2, 0, sizeof(int), stream_);
     L.depth = level_schedule(L.rows, L.ro, L.ci, L.dg, L.order.p, lvl_.p, cnt_.p, scanTmp_.p, push_.p, err_.p + 2,
                              stream_);
-    finishSmoothers(1, nullptr);
+    finishSmoothers({&L}, nullptr);
 }
 
 void Engine::buildHierarchy(const bcs_solver_config& cfg) {
@@ -943,7 +952,7 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
     H_->levels[H_->nlev - 1].ncoarse = 0;
 
     // DILU smoother on all but the coarsest level (amg.cpp:86-88)
-    diluSetupAll(H_->nlev - 1, &cfg);
+    diluSetupAll(smoothedLevels(cfg), &cfg);
     // dense factorisation of the coarsest level (amg.cpp:90-104)
     const Level& Cl = H_->levels[H_->nlev - 1];
     H_->m = Cl.rows * n_;
@@ -972,13 +981,77 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
     setupTail();
 }
 
+// the first level of the one-CTA coarse tail (nlev - 1: none)
+int Engine::tailStart() const {
+    if (tailMaxRows_ <= 0 || H_->nlev < 2) return H_->nlev - 1;
+    int t = H_->nlev - 1;
+    while (t > 0 && H_->levels[t - 1].rows <= tailMaxRows_) --t;
+    return t;
+}
+
+std::vector<Level*> Engine::smoothedLevels(const bcs_solver_config& cfg) {
+    std::vector<Level*> lv;
+    const int t = cfg.mode == BCS_MODE_PERF ? tailStart() : 0;
+    for (int l = 0; l + 1 < H_->nlev; ++l) lv.push_back(l < t ? perfLevel(H_->levels[l], cfg) : &H_->levels[l]);
+    for (int l = t; l + 1 < H_->nlev; ++l) H_->levels[l].mcValid = false;
+    return lv;
+}
+
+Level* Engine::perfLevel(Level& L, const bcs_solver_config& cfg) {
+    L.mcValid = false;
+    if (cfg.mode != BCS_MODE_PERF) return &L;
+    if (!buildColoured(L)) return &L;  // more than 64 colours: natural-order smoother on this level
+    L.mcValid = true;
+    return L.mc.get();
+}
+
+// the colour-permuted copy of L (k_color.cu): rows ordered by (colour, row),
+// columns renumbered and sorted, blocks gathered; the smoother's DILU is then
+// built on it by the natural-order machinery (a DAG #colours deep)
+bool Engine::buildColoured(Level& L) {
+    const size_t nn = static_cast<size_t>(n_) * n_;
+    if (!L.mc) L.mc = std::make_unique<Level>();
+    Level& M = *L.mc;
+    const int R = L.rows;
+    cnt_.ensure(static_cast<size_t>(R) + 2, stream_);
+    lvl_.ensure(static_cast<size_t>(R) + 1, stream_);
+    const int rounds = mc_color(R, L.ro, L.ci, cnt_.p, lvl_.p, ctr_.p, hTot_, stream_);
+    if (rounds < 0) return false;
+    L.mcPerm.ensure(R, stream_);
+    act2_.ensure(static_cast<size_t>(R) + 1, stream_);  // inverse permutation
+    const size_t scratch = static_cast<size_t>((R + 1023) / 1024) * 64 + 256;
+    flag_.ensure(std::max<size_t>(scratch, R), stream_);
+    L.ncolors = mc_permutation(R, cnt_.p, L.mcPerm.p, act2_.p, flag_.p, flag_.cap, hTot_, stream_);
+    L.mcColorOff.assign(1, 0);  // hTot_[c] = rows of colour c (mc_permutation)
+    for (int c = 0; c < L.ncolors; ++c) L.mcColorOff.push_back(L.mcColorOff.back() + hTot_[c]);
+    M.rows = R;
+    M.nnz = L.nnz;
+    M.o_ro.ensure(static_cast<size_t>(R) + 1, stream_);
+    M.o_ci.ensure(L.nnz, stream_);
+    mcSv_.ensure(L.nnz, stream_);
+    scanTmp_.ensure(scan_tmp_ints(static_cast<size_t>(R) + 1) + 16, stream_);
+    mc_permute_pattern(R, L.ro, L.ci, L.mcPerm.p, act2_.p, M.o_ro.p, M.o_ci.p, mcSv_.p, scanTmp_.p, push_.p + 10,
+                       stream_);
+    M.o_v.ensure(static_cast<size_t>(L.nnz) * nn, stream_);
+    mc_permute_values(n_, static_cast<size_t>(L.nnz), mcSv_.p, L.v, M.o_v.p, stream_);
+    M.ro = M.o_ro;
+    M.ci = M.o_ci;
+    M.v = M.o_v;
+    setupLevelPattern(M);
+    const size_t N = static_cast<size_t>(R) * n_;
+    M.r.ensure(N, stream_);
+    M.y.ensure(N, stream_);
+    M.zb.ensure(N, stream_);
+    profMark("perf:colour");
+    return true;
+}
+
 // the one-CTA coarse tail: the first level from which every smoothed level
 // has at most tailMaxRows_ rows (the coarsest is solved densely in between)
 void Engine::setupTail() {
     H_->tail = -1;
     if (tailMaxRows_ <= 0 || H_->nlev < 2) return;
-    int t = H_->nlev - 1;
-    while (t > 0 && H_->levels[t - 1].rows <= tailMaxRows_) --t;
+    const int t = tailStart();
     if (t >= H_->nlev - 1) return;  // no smoothed level small enough
     const int nl = H_->nlev - t;
     std::vector<TailLevelDev> d(nl);
@@ -1028,6 +1101,7 @@ void Engine::buildPrecond(const bcs_solver_config& cfg) {
 
 void Engine::buildPrecondOn(const FineMatrix& F, const bcs_solver_config& cfg) {
     H_->pcKind = -1;
+    for (auto& L : H_->levels) L.mcValid = false;
 
     if (H_->levels.empty()) H_->levels.emplace_back();
     H_->nlev = 1;
@@ -1047,7 +1121,7 @@ void Engine::buildPrecondOn(const FineMatrix& F, const bcs_solver_config& cfg) {
             L0.y.ensure(N, stream_);
             break;
         case BCS_PRECOND_DILU:
-            diluSetupAll(1, &cfg);
+            diluSetupAll({perfLevel(L0, cfg)}, &cfg);
             L0.y.ensure(N, stream_);
             break;
         case BCS_PRECOND_AMG: buildHierarchy(cfg); break;
@@ -1060,6 +1134,15 @@ void Engine::buildPrecondOn(const FineMatrix& F, const bcs_solver_config& cfg) {
 
 // DILU/LUSGS sweep pair: z = (D+U)^{-1} D (D+L)^{-1} r  (accumulate: see sweep_backward)
 void Engine::smootherApply(Level& L, const double* r, double* z, int accumulate) {
+    if (L.mcValid && H_->pcCfg.mode == BCS_MODE_PERF) {
+        // performance mode: the multicolour DILU on the colour-permuted copy;
+        // r in, result scattered back (and accumulated) in the level's numbering
+        Level& M = *L.mc;
+        mc_vec_gather(n_, L.rows, L.mcPerm, r, M.r.p, stream_);
+        smootherApply(M, M.r, M.zb.p, 0);
+        mc_vec_scatter(n_, L.rows, L.mcPerm, M.zb, z, accumulate, stream_);
+        return;
+    }
     const size_t N = static_cast<size_t>(L.rows) * n_;
     double* zb = accumulate ? L.zb.p : z;
     cudaMemsetAsync(L.y.p, 0xFF, N * sizeof(double), stream_);
@@ -2105,6 +2188,18 @@ std::string Engine::memoryReport() const {
     }
     out += "\"total\": " + std::to_string(static_cast<long long>(total)) + "}";
     return out;
+}
+
+int Engine::levelColoring(int l, int32_t* perm, int32_t* colorOff) {
+    if (l < 0 || l >= H_->nlev) throw std::invalid_argument("bcs: level out of range");
+    Level& L = H_->levels[l];
+    if (!L.mcValid) return 0;
+    if (colorOff) std::copy(L.mcColorOff.begin(), L.mcColorOff.end(), colorOff);
+    if (perm) {
+        check(cudaMemcpyAsync(perm, L.mcPerm.p, sizeof(int) * L.rows, cudaMemcpyDeviceToHost, stream_), "D2H perm");
+        sync();
+    }
+    return L.ncolors;
 }
 
 int Engine::scheduleDepth(int l) const {

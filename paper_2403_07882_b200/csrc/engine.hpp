@@ -8,6 +8,7 @@
 #include "partition.hpp"
 
 #include <chrono>
+#include <memory>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -113,6 +114,12 @@ struct Level {
     int ncoarse = 0;
     // V-cycle vectors
     DArray<double> r, z, res, y, zb;
+    // performance mode (BCS_MODE_PERF): colour-permuted copy for the smoother
+    std::unique_ptr<Level> mc;
+    DArray<int> mcPerm;  // new (colour-ordered) row -> row
+    int ncolors = 0;
+    std::vector<int> mcColorOff;  // colour c = new rows [off[c], off[c+1])
+    bool mcValid = false;  // mc built for the current values
 };
 
 // Preconditioner state of one matrix (the serial system or one Mode-R engine)
@@ -211,6 +218,9 @@ public:
     void amgLevelSizes(int l, int* rows, int* nnz) const;
     void amgLevelGet(int l, int32_t* ro, int32_t* ci, double* v, int32_t* agg);
     int scheduleDepth(int l) const;
+    // performance mode: colours of level l's smoother and its row order
+    // (perm[new] = row), 0 when the level is smoothed in natural order
+    int levelColoring(int l, int32_t* perm, int32_t* colorOff);
 
     // device bytes held by this context, per category (JSON object)
     std::string memoryReport() const;
@@ -228,8 +238,16 @@ private:
     FineMatrix serialFine() const;
     void buildHierarchy(const bcs_solver_config& cfg);
     void setupLevelPattern(Level& L);
-    void diluSetupAll(int nl, const bcs_solver_config* cfg);
-    void finishSmoothers(int nl, const bcs_solver_config* cfg);
+    void diluSetupAll(const std::vector<Level*>& lv, const bcs_solver_config* cfg);
+    void finishSmoothers(const std::vector<Level*>& lv, const bcs_solver_config* cfg);
+    // performance mode: the colour-permuted copy of L the smoother runs on
+    // (k_color.cu), or L itself when the colouring is not possible
+    Level* perfLevel(Level& L, const bcs_solver_config& cfg);
+    bool buildColoured(Level& L);
+    // the levels whose DILU is built: every level but the coarsest, coloured
+    // copies in performance mode above the one-CTA tail
+    std::vector<Level*> smoothedLevels(const bcs_solver_config& cfg);
+    int tailStart() const;
     void lusgsSetup(Level& L);
 
     void applyPrecond(const double* r, double* z);
@@ -296,6 +314,7 @@ private:
     DArray<int> cnt_, lvl_, act2_, push_, scanTmp_, flag_, err_, ctr_, choice_, segOff_, cro_, big_;
     DArray<double> dn_, str_, tblk_;
     DArray<int> dkeys_, dorder_;       // combined DILU tickets
+    DArray<int> mcSv_;                 // performance mode: source slot of every permuted slot
     DArray<unsigned char> ddesc_;      // device level descriptors of the combined DILU setup
     DArray<unsigned long long> keys_, sorted_;
 

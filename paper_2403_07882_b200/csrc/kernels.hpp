@@ -36,6 +36,21 @@ void transpose_pos(int rows, const int* ro, const int* ci, int* tpos, int* asym_
 void gather_values(int n, int nnz, int nc, int nf, const int* src, const double* diag, const double* upper,
                    const double* lower, double* vals, cudaStream_t s);
 
+// -------------------------------- performance mode: multicolouring (k_color.cu)
+// Jones-Plassmann colouring (deterministic); colA receives the colours.
+// Returns the number of rounds, -1 when a row would need more than 64 colours.
+int mc_color(int rows, const int* ro, const int* ci, int* colA, int* colB, int* counters, int* hostCounters,
+             cudaStream_t s);
+// perm[new] = old, inv[old] = new, rows ordered by (colour, index); returns #colours (syncs)
+int mc_permutation(int rows, const int* color, int* perm, int* inv, int* scratch, size_t scratchInts, int* hostBuf,
+                   cudaStream_t s);
+// permuted BSR pattern (nro: rows+1, nci/sv: nnz; sv = source slot of each new slot)
+void mc_permute_pattern(int rows, const int* ro, const int* ci, const int* perm, const int* inv, int* nro, int* nci,
+                        int* sv, int* scanTmp, int* dTotal, cudaStream_t s);
+void mc_permute_values(int n, size_t nnz, const int* sv, const double* v, double* nv, cudaStream_t s);
+void mc_vec_gather(int n, int rows, const int* perm, const double* x, double* xp, cudaStream_t s);
+void mc_vec_scatter(int n, int rows, const int* perm, const double* sp, double* z, int acc, cudaStream_t s);
+
 // ------------------------------------------------------------- SpMV (K3)
 // y = A x  (sub == nullptr)   or   y = sub - A x
 void spmv(int n, int rows, const int* ro, const int* ci, const double* v, const double* x, const double* sub,
