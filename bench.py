@@ -60,6 +60,9 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--size", type=int, default=128)
     p.add_argument("--method", default="gmres", choices=["gmres", "bicgstab", "fgmres"])
+    p.add_argument("--mode", default="parity", choices=["parity", "perf", "exact"],
+                   help="parity (default, the headline): reference operation order; perf: multicolour DILU "
+                        "smoothing (iterations differ, reported); exact: + the reference's sequential dot order")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--ref-budget", type=float, default=150.0,
                    help="--impl reference: seconds of replace-branch calls to time after the setup-branch call")
@@ -139,13 +142,14 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": reasons, "samples": len(sm)}
 
 
-def solver_config(method):
+def solver_config(method, mode="parity"):
     from paper_2403_07882_b200 import bcs
     kind = {"gmres": bcs.KrylovMethod.GMRES, "bicgstab": bcs.KrylovMethod.PBiCGStab,
             "fgmres": bcs.KrylovMethod.FGMRES}[method]
     return bcs.SolverConfig(method=kind,
                             preconditioner=bcs.PrecondKind.AMG, relTol=1e-8, absTol=1e-300, maxIters=1000,
-                            gmresRestart=30, amg=bcs.AmgConfig(maxLevels=30, minCoarseRows=8))
+                            gmresRestart=30, amg=bcs.AmgConfig(maxLevels=30, minCoarseRows=8),
+                            mode={"parity": bcs.Mode.PARITY, "perf": bcs.Mode.PERF, "exact": bcs.Mode.EXACT}[mode])
 
 
 TAIL_ROWS = 512  # Engine::tailMaxRows_ default (levels handled by k_vcycle_tail)
@@ -281,7 +285,7 @@ def run_ours(args):
     s = make_system(args, n, alloc=pinned)
     A, b, x0 = s.A, s.b, s.x0
     nc, nf, nb = A.n_cells, A.nFaces(), A.n
-    cfg = solver_config(args.method)
+    cfg = solver_config(args.method, args.mode)
 
     ctx = bcs.Context(local)
     stream = torch.cuda.current_stream(dev)
@@ -491,7 +495,9 @@ def run_ours(args):
             "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{workload_name(args)}, {nc} cells, {nc + 2 * nf} blocks per GPU",
-                       "method": args.method, "precond": "AMG(maxLevels 30, minCoarseRows 8, DILU 1/1)",
+                       "method": args.method, "mode": args.mode,
+                       "precond": "AMG(maxLevels 30, minCoarseRows 8, " +
+                                  ("multicolour DILU 1/1)" if args.mode == "perf" else "DILU 1/1)"),
                        "rel_tol": 1e-8,
                        "x0": "zero" if args.system == "euler" else "the seeded state (reference assembleCoupled input)",
                        "l2": f"inputs ({(nc + 2 * nf) * nb * nb * 8 / 1e9:.1f} GB BSR values) exceed the 126 MB L2; "
@@ -537,6 +543,9 @@ def workload_name(args):
         extra.append(f"aspect ratio {args.aspect:g}")
     if args.scramble >= 0:
         extra.append(f"randomly permuted cell order (seed {args.scramble})")
+    if args.mode != "parity":
+        extra.append({"perf": "PERFORMANCE MODE (multicolour DILU smoothing; iterations differ from the reference)",
+                      "exact": "EXACT mode (the reference's sequential dot order)"}[args.mode])
     if not extra and args.system == "euler" and args.size == 128:
         return base + " (BASELINE configs[1])"
     return base + ", " + ", ".join(extra)
@@ -574,7 +583,7 @@ def run_mode_r(args):
         return t.numpy()
 
     s = make_system(args, args.size, alloc=pinned)
-    cfg = solver_config(args.method)
+    cfg = solver_config(args.method, args.mode)
     for _ in range(max(args.warmup, 3)):
         x, r = ctx.dist_solve_mp(s.A, s.b, s.x0, s.centroids, world, cfg)
     times = []
