@@ -30,8 +30,11 @@ freestream, generated bit-identically to the reference by csrc/gen.
            replace-branch calls on the full system while --ref-budget holds
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--size 128]
-Multi-GPU (torchrun, N>1): every rank solves its own 128^3 block (weak scaling,
-independent replicas until the Mode-R distributed solve lands).
+                       [--mode parity|perf|exact] [--method gmres|bicgstab|fgmres]
+Multi-GPU (torchrun, N>1): the reference's Mode R (distributedSolve) over N
+processes, one engine per GPU, --size^3 cells per GPU (weak scaling; N=8 is
+the 256^3 C3 system); --strong: one --size^3 system; --replicas: independent
+systems per GPU.
 """
 from __future__ import annotations
 
@@ -68,7 +71,12 @@ def parse():
                    help="--impl reference: seconds of replace-branch calls to time after the setup-branch call")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--mode-r", action="store_true",
-                   help="strong scaling: one 128^3 system in the reference's Mode R over the N processes (NCCL)")
+                   help="Mode R (the reference's distributedSolve) even at N=1")
+    p.add_argument("--replicas", action="store_true",
+                   help="N>1: independent --size^3 replicas per GPU instead of the default Mode R decomposed solve")
+    p.add_argument("--strong", action="store_true",
+                   help="N>1 Mode R: one --size^3 system over the N GPUs (strong scaling); default: weak scaling, "
+                        "--size^3 cells per GPU (N=8: 2x2x2 blocks = 256^3, BASELINE configs[2] on 8 GPUs)")
     p.add_argument("--scramble", type=int, default=-1,
                    help="randomly permuted cell order with this seed (SURVEY C4-style input); default natural order")
     p.add_argument("--system", default="euler", choices=["euler", "coupled"],
@@ -184,11 +192,26 @@ def chain_hop_ns(bcs, L=20000, reps=3, device=0):
         c.close()
 
 
-def make_system(args, n, alloc=None):
-    """The bench workload at n^3 cells (generator restating the reference producers)."""
+def make_system(args, n, alloc=None, dims=None):
+    """The bench workload at n^3 cells, or nx x ny x nz = dims (generator restating the reference producers)."""
     from paper_2403_07882_b200 import gen
     mk = gen.hex_coupled if args.system == "coupled" else gen.hex_euler
-    return mk(n, aspect=args.aspect, scramble_seed=args.scramble, alloc=alloc, poly_seed=args.poly)
+    nx, ny, nz = dims if dims else (n, n, n)
+    return mk(nx, ny, nz, aspect=args.aspect, scramble_seed=args.scramble, alloc=alloc, poly_seed=args.poly)
+
+
+def weak_dims(n, world):
+    """nx, ny, nz = n * (a, b, c) with a * b * c = world, factors of 2 spread over x, y, z in turn (RCB then
+    cuts the box into world blocks of n^3: 2 -> 2x1x1, 4 -> 2x2x1, 8 -> 2x2x2)."""
+    f = [1, 1, 1]
+    w, k = world, 0
+    for p in (2, 3, 5, 7):
+        while w % p == 0:
+            f[k % 3] *= p
+            w //= p
+            k += 1
+    f[k % 3] *= w
+    return n * f[0], n * f[1], n * f[2]
 
 
 # ---------------------------------------------------------------- reference
@@ -561,55 +584,81 @@ def sweep_traffic(n):
 
 
 def run_mode_r(args):
-    """Mode R over N processes (bcs_dist_solve_mp): one system, ranks = engines = N, strong scaling.  The
-    timed call is the drop-in multi-rank entry (host buffers in, whole solution out on every rank)."""
+    """Mode R over N processes (bcs_dist_solve_mp, the reference's distributedSolve semantics,
+    partition.cpp:370-479): one system, ranks = engines = N, each process owning one engine (its local
+    BSR, halo couplings and AMG hierarchy), global Krylov with NCCL halo exchange (overlapped with the
+    local product) and engine-tree dot products.  Default: weak scaling, --size^3 cells per GPU; --strong:
+    one --size^3 system.  The timed call is the drop-in multi-rank entry (host buffers in: each rank
+    gathers and uploads only its own blocks; the whole solution out on every rank), so value == e2e."""
     import torch
     import torch.distributed as dist
 
-    from paper_2403_07882_b200 import bcs, gen
+    from paper_2403_07882_b200 import bcs
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("gloo")  # broadcast of the NCCL id only
+        dist.init_process_group("gloo")  # broadcast of the NCCL id + barriers
     uid = [bcs.comm_unique_id() if rank == 0 else None]
     if world > 1:
         dist.broadcast_object_list(uid, src=0)
     ctx = bcs.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
     ctx.comm_init(rank, world, uid[0])
 
     def pinned(size, dt):
         t = torch.empty(size, dtype=torch.float64 if dt == np.float64 else torch.int32, pin_memory=True)
         return t.numpy()
 
-    s = make_system(args, args.size, alloc=pinned)
+    dims = (args.size,) * 3 if args.strong else weak_dims(args.size, world)
+    s = make_system(args, args.size, alloc=pinned, dims=dims)
     cfg = solver_config(args.method, args.mode)
     for _ in range(max(args.warmup, 3)):
         x, r = ctx.dist_solve_mp(s.A, s.b, s.x0, s.centroids, world, cfg)
-    times = []
-    for _ in range(args.steps):
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        x, r = ctx.dist_solve_mp(s.A, s.b, s.x0, s.centroids, world, cfg)
-        times.append(time.perf_counter() - t0)
-    t = statistics.mean(times)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            x, r = ctx.dist_solve_mp(s.A, s.b, s.x0, s.centroids, world, cfg)
+            reps.append(r)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    t = ev0.elapsed_time(ev1) / 1e3 / args.steps
     if world > 1:
         tt = [None] * world
         dist.all_gather_object(tt, t)
         t = max(tt)
     if rank == 0:
-        h2d = s.A.diag.nbytes + s.A.upper.nbytes + s.A.lower.nbytes + s.b.values.nbytes + s.x0.values.nbytes
+        nn = s.A.n * s.A.n
+        nloc = s.A.n_cells // world
+        h2d_rank = (s.A.diag.nbytes + s.A.upper.nbytes + s.A.lower.nbytes) / world  # about 1/N per rank
+        it = reps[-1].iterations
         emit({
             "metric": METRIC, "value": t, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(args), "method": args.method,
+            "warmup": max(args.warmup, 3), "ms_per_step": t * 1e3, "higher_is_better": False,
+            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": ("4x4 pressure-based coupled" if args.system == "coupled" else "5x5 density-based") +
+                                   f" hex {dims[0]}x{dims[1]}x{dims[2]} ({s.A.n_cells} cells, {nloc} per GPU)" +
+                                   (" = BASELINE configs[2]" if dims == (256, 256, 256) and args.system == "euler" else ""),
+                       "method": args.method, "mode": args.mode,
                        "precond": "AMG(maxLevels 30, minCoarseRows 8, DILU 1/1) per engine (Mode R)",
-                       "rel_tol": 1e-8, "parallelism": f"Mode R, {world} engines = processes (NCCL)"},
-            "iterations": r.iterations, "converged": r.converged,
-            "e2e": {"value": t, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step":
-                    int(s.A.n_cells * s.A.n * 8)},
+                       "rel_tol": 1e-8, "parallelism": f"Mode R, {world} engines = processes (NCCL)",
+                       "l2": "inputs exceed the 126 MB L2; no flush needed"},
+            "iterations": it, "converged": reps[-1].converged, "s_per_krylov_iter": t / max(1, it),
+            "note": "Mode R = block-Jacobi across engines (the reference's semantics): iterations grow with N "
+                    "(SURVEY §8(e)); s_per_krylov_iter is the per-iteration figure",
+            "stage_s": {k: reps[-1].timings.get(k) for k in ("convert", "setup", "solve", "retrieve")},
+            "gpu_launches": sum(rp.kernelLaunches for rp in reps),
+            "clocks": clk.summary(),
+            "e2e": {"value": t, "unit": UNIT, "h2d_bytes_per_step": int(h2d_rank + 2 * nloc * s.A.n * 8),
+                    "d2h_bytes_per_step": int(s.A.n_cells * s.A.n * 8),
+                    "note": "per rank: its own LDU blocks (host-gathered) + b/x0 slices in, the all-gathered solution out"},
         })
     ctx.close()
     if world > 1:
@@ -637,9 +686,10 @@ def main():
     _JSON_FD = os.dup(1)
     os.dup2(2, 1)
     args = parse()
+    _, world, _ = dist_env()
     if args.impl == "reference":
         run_reference(args)
-    elif args.mode_r:
+    elif args.mode_r or (world > 1 and not args.replicas):
         run_mode_r(args)
     else:
         run_ours(args)

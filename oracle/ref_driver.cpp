@@ -565,13 +565,21 @@ int ref_solve(int nc, int nf, int n, const int* owner, const int* neigh, const d
             throw std::invalid_argument("ref_solve: calls == 0 needs a history buffer");
         }
         if (hist && histN) {
+            // the operators of the requested backend: EngineCsr = solveCsr's
+            // (engine.cpp:31-45), HostLdu = blockMatvec + LduLusgsPrecond (:54-72)
             const BlockCsrMatrix csr = lduToBlockCsr(A);
-            const auto M = makeCsrPreconditioner(csr, scfg);
+            std::unique_ptr<Preconditioner> M;
+            if (backend == 0) {
+                if (scfg.preconditioner == PrecondKind::LUSGS) M = std::make_unique<LduLusgsPrecond>(A);
+            } else {
+                M = makeCsrPreconditioner(csr, scfg);
+            }
             DotTape tape;
             KrylovOps ops;
             ops.size = static_cast<std::size_t>(nc) * n;
-            ops.applyA = [&csr](const double* in, double* o) { csrMatvec(csr, in, o); };
-            ops.applyM = [&M](const double* rr, double* zz) { M->apply(rr, zz); };
+            if (backend == 0) ops.applyA = [&A](const double* in, double* o) { blockMatvec(A, in, o); };
+            else ops.applyA = [&csr](const double* in, double* o) { csrMatvec(csr, in, o); };
+            if (M) ops.applyM = [&M](const double* rr, double* zz) { M->apply(rr, zz); };
             ops.dot = [&tape, &ops](const double* a, const double* bb) {
                 double s = 0.0;
                 for (std::size_t i = 0; i < ops.size; ++i) s += a[i] * bb[i];

@@ -102,6 +102,35 @@ struct LaunchScope {
 };
 }  // namespace
 
+// f(i) for i in [0, n) over up to T host threads (contiguous ranges)
+template <class F>
+static void parallelFor(int n, int T, F&& f) {
+    const int parts = n < (1 << 16) ? 1 : std::max(1, T);
+    auto work = [&](int p) {
+        const int b = static_cast<int>(static_cast<long long>(n) * p / parts);
+        const int e = static_cast<int>(static_cast<long long>(n) * (p + 1) / parts);
+        for (int i = b; i < e; ++i) f(i);
+    };
+    std::vector<std::thread> th;
+    for (int p = 1; p < parts; ++p) th.emplace_back(work, p);
+    work(0);
+    for (auto& t : th) t.join();
+}
+
+// element-wise equality of two host arrays in parallel chunks
+template <class T>
+static bool parallelEqual(const T* a, const T* b, size_t n) {
+    const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    const size_t parts = n < (1u << 20) ? 1 : hw;
+    std::vector<char> eq(parts, 1);
+    auto work = [&](size_t p) { eq[p] = std::equal(a + n * p / parts, a + n * (p + 1) / parts, b + n * p / parts); };
+    std::vector<std::thread> th;
+    for (size_t p = 1; p < parts; ++p) th.emplace_back(work, p);
+    work(0);
+    for (auto& t : th) t.join();
+    return std::all_of(eq.begin(), eq.end(), [](char c) { return c != 0; });
+}
+
 // topologySignature (block_csr.cpp:146-160) — exact, host side
 uint64_t topologySignatureHost(int nc, int nf, const int32_t* owner, const int32_t* neigh) {
     uint64_t h = hashCombine(0, static_cast<uint64_t>(static_cast<int64_t>(nc)));
@@ -255,6 +284,7 @@ void Engine::setTopology(int nc, int nf, int n, const int32_t* owner, const int3
     hasTopo_ = false;
     hasValues_ = false;
     asmTopo_ = false;
+    hlTopo_ = false;
     H_->pcKind = -1;
     const size_t nnz = static_cast<size_t>(nc) + 2 * static_cast<size_t>(nf);
     if (nnz > static_cast<size_t>(std::numeric_limits<int>::max()))
@@ -860,7 +890,9 @@ void Engine::lusgsSetup(Level& L) {
     factor_diag_blocks(n_, L.rows, L.dg, L.v, L.lu.p, L.piv.p, err_.p, stream_);
     const int cell = readErrCell();
     if (cell != big)
-        throw std::runtime_error("preconditioner setup: singular diagonal block in cell " + std::to_string(cell));
+        throw std::runtime_error((hostLdu_ ? "LUSGS setup: singular diagonal block in cell "  // preconditioner.cpp:66
+                                           : "preconditioner setup: singular diagonal block in cell ") +
+                                 std::to_string(cell));
     cnt_.ensure(static_cast<size_t>(L.rows) + 2, stream_);
     scanTmp_.ensure(scan_tmp_ints(static_cast<size_t>(L.rows) + 2) + 16, stream_);
     cudaMemsetAsync(err_.p + 2, 0, sizeof(int), stream_);
@@ -1450,6 +1482,10 @@ void Engine::solveKrylov(const double* d_b, double* d_x, const bcs_solver_config
 
 // ------------------------------------------------------- Krylov operators
 void Engine::opResidual(const double* x, const double* b, double* r) {
+    if (hostLdu_) {
+        spmv(n_, nc_, hlMvRo_, hlMvCi_, hlMvV_, x, b, r, stream_);
+        return;
+    }
     if (!distActive_) {
         spmvLevel(H_->levels[0], x, b, r);
         return;
@@ -1490,6 +1526,10 @@ void Engine::mpExchange(const double* x) {
 // its row slice, then its halo couplings (the exchange is implicit: all engine
 // slices live in one device vector on this GPU)
 void Engine::opSpmv(const double* x, double* y) {
+    if (hostLdu_) {
+        spmv(n_, nc_, hlMvRo_, hlMvCi_, hlMvV_, x, nullptr, y, stream_);
+        return;
+    }
     if (!distActive_) {
         spmvLevel(H_->levels[0], x, nullptr, y);
         return;
@@ -1827,21 +1867,38 @@ void Engine::distSolveMP(int nc, int nf, int n, const int32_t* owner, const int3
                          const double* diag, const double* upper, const double* lower, const double* b,
                          const double* x0, double* x, int nRanks, const bcs_solver_config& cfg, bcs_report& rep) {
     LaunchScope ls(&launches_);
+    const long long l0 = launches_.launches;
     if (!comm_) throw std::invalid_argument("bcs_dist_solve_mp: call bcs_comm_init first");
     if (n < 1 || n > 5) throw std::invalid_argument("bcs: block size must be 1..5 on the device");
     if (mpSize_ < 1 || mpSize_ > nRanks) throw std::invalid_argument("makeConsolidationPlan: need 1 <= nEngines <= nRanks");
     validateConfig(cfg);
     const auto t0 = clk::now();
     const bool same = mpNc_ == nc && mpNf_ == nf && mpN_ == n && mpRanks_ == nRanks &&
-                      std::equal(owner, owner + nf, mpOwner_.begin()) && std::equal(neigh, neigh + nf, mpNeigh_.begin()) &&
-                      std::equal(centroids, centroids + 3 * static_cast<size_t>(nc), mpCen_.begin());
+                      parallelEqual(owner, mpOwner_.data(), static_cast<size_t>(nf)) &&
+                      parallelEqual(neigh, mpNeigh_.data(), static_cast<size_t>(nf)) &&
+                      parallelEqual(centroids, mpCen_.data(), 3 * static_cast<size_t>(nc));
     if (!same) mpSetupTopology(nc, nf, n, owner, neigh, centroids, nRanks);
     n_ = n;
     DistPart& P = dist_[0];
     const size_t nn = static_cast<size_t>(n) * n;
     // upload (partition.cpp:384-407): only this engine's local and halo blocks
-    // cross PCIe, gathered on the host into page-locked staging in slot order
-    {
+    // cross PCIe, gathered on the host into page-locked staging in slot order.
+    // An engine that needs most of the system (one or two processes) takes the
+    // whole LDU at full DMA rate and gathers on the device instead.
+    const size_t nnzAll = static_cast<size_t>(nc) + 2 * static_cast<size_t>(nf);
+    const int hw = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+    if (2 * (static_cast<size_t>(P.nnz) + P.nh) > nnzAll) {
+        ldu_diag_.ensure(nc * nn, stream_);
+        ldu_upper_.ensure(nf * nn, stream_);
+        ldu_lower_.ensure(nf * nn, stream_);
+        h2d(ldu_diag_.p, diag, sizeof(double) * nc * nn, "H2D");
+        if (nf) {
+            h2d(ldu_upper_.p, upper, sizeof(double) * nf * nn, "H2D");
+            h2d(ldu_lower_.p, lower, sizeof(double) * nf * nn, "H2D");
+        }
+        gather_values(n, P.nnz, nc, nf, P.src, ldu_diag_, ldu_upper_, ldu_lower_, P.vals.p, stream_);
+        if (P.nh) gather_values(n, P.nh, nc, nf, P.hsrc, ldu_diag_, ldu_upper_, ldu_lower_, P.hvals.p, stream_);
+    } else {
         const size_t cnt = (static_cast<size_t>(P.nnz) + P.nh) * nn;
         if (mpStageCap_ < cnt) {
             if (mpStage_) cudaFreeHost(mpStage_);
@@ -1853,7 +1910,7 @@ void Engine::distSolveMP(int nc, int nf, int n, const int32_t* owner, const int3
         }
         sync();  // the previous call's copies out of the staging buffer are done
         gatherPartValues(mpPart, nc, nf, n, diag, upper, lower, mpStage_, mpStage_ + static_cast<size_t>(P.nnz) * nn,
-                         8);
+                         hw);
         check(cudaMemcpyAsync(P.vals.p, mpStage_, sizeof(double) * P.nnz * nn, cudaMemcpyHostToDevice, stream_), "H2D");
         if (P.nh)
             check(cudaMemcpyAsync(P.hvals.p, mpStage_ + static_cast<size_t>(P.nnz) * nn, sizeof(double) * P.nh * nn,
@@ -1863,11 +1920,11 @@ void Engine::distSolveMP(int nc, int nf, int n, const int32_t* owner, const int3
     const size_t Nl = static_cast<size_t>(mpRows_) * n;
     std::vector<double> hb(Nl), hx(Nl);
     const int g0 = mpEngStart_[mpRank_];
-    for (int r = 0; r < mpRows_; ++r) {
+    parallelFor(mpRows_, hw, [&](int r) {
         const int old = mpNewToOld_[g0 + r];
         std::copy(b + static_cast<size_t>(old) * n, b + static_cast<size_t>(old + 1) * n, hb.begin() + static_cast<size_t>(r) * n);
         std::copy(x0 + static_cast<size_t>(old) * n, x0 + static_cast<size_t>(old + 1) * n, hx.begin() + static_cast<size_t>(r) * n);
-    }
+    });
     kb_.ensure(Nl, stream_);
     kx_.ensure(Nl, stream_);
     distTmp_.ensure(Nl, stream_);
@@ -1931,11 +1988,11 @@ void Engine::distSolveMP(int nc, int nf, int n, const int32_t* owner, const int3
     check(cudaMemcpyAsync(all.data(), mpXall_.p, all.size() * sizeof(double), cudaMemcpyDeviceToHost, stream_), "D2H x");
     sync();
     for (int e = 0; e < mpSize_; ++e)
-        for (int r = 0; r < mpEngRows_[e]; ++r) {
+        parallelFor(mpEngRows_[e], hw, [&](int r) {
             const int old = mpNewToOld_[mpEngStart_[e] + r];
             std::copy(all.begin() + pad * e + static_cast<size_t>(r) * n, all.begin() + pad * e + static_cast<size_t>(r + 1) * n,
                       x + static_cast<size_t>(old) * n);
-        }
+        });
     nc_ = ncSerial;
     const auto t4 = clk::now();
     rep.t_convert = secs(t0, t1);  // partition.cpp:474-477 keys
@@ -1944,7 +2001,8 @@ void Engine::distSolveMP(int nc, int nf, int n, const int32_t* owner, const int3
     rep.t_retrieve = secs(t3, t4);
     rep.t_amg_setup = rep.t_setup;
     rep.t_krylov = rep.t_solve;
-    rep.amg_levels = 1;
+    rep.amg_levels = P.H.pcKind == BCS_PRECOND_AMG ? P.H.nlev : 0;
+    rep.kernel_launches = static_cast<int>(launches_.launches - l0);
 }
 
 void Engine::solveHost(const double* b, double* x, const bcs_solver_config& cfg, bcs_report& rep) {
@@ -1956,6 +2014,125 @@ void Engine::solveHost(const double* b, double* x, const bcs_solver_config& cfg,
     h2d(kx_.p, x, N * sizeof(double), "H2D x");
     solveDevice(kb_, kx_, cfg, rep);
     d2h(x, kx_.p, N * sizeof(double), "D2H x");  // synchronous
+}
+
+// Backend::HostLdu's two slot orders of the LDU blocks (ids: cell c, upper
+// of face f = nc + f, lower of face f = nc + nf + f), built on the host:
+//   matvec row c: diag, then every face touching c in face order (upper when c
+//     owns it, column = neighbour; lower otherwise, column = owner) -- the
+//     accumulation order of blockMatvec (block_matrix.cpp:104-119);
+//   LUSGS row c: lower faces (c = neighbour) in face order, diag, upper faces
+//     (c = owner) in DESCENDING face order -- the sweep kernels walk the upper
+//     part backwards, so LduLusgsPrecond::apply's face order results
+//     (preconditioner.cpp:81-99).
+void Engine::hostLduTopology() {
+    if (hlTopo_) return;
+    const int nc = nc_, nf = nf_;
+    const size_t nnz = static_cast<size_t>(nc) + 2 * static_cast<size_t>(nf);
+    std::vector<int> deg(static_cast<size_t>(nc) + 1, 0);
+    for (int f = 0; f < nf; ++f) {
+        ++deg[hOwner_[f] + 1];
+        ++deg[hNeigh_[f] + 1];
+    }
+    std::vector<int> cfo(static_cast<size_t>(nc) + 1, 0);  // cell -> faces (face order)
+    for (int c = 0; c < nc; ++c) cfo[c + 1] = cfo[c] + deg[c + 1];
+    std::vector<int> cf(2 * static_cast<size_t>(nf)), pos(cfo.begin(), cfo.end() - 1);
+    for (int f = 0; f < nf; ++f) {
+        cf[pos[hOwner_[f]]++] = f;
+        cf[pos[hNeigh_[f]]++] = f;
+    }
+    std::vector<int> ro(static_cast<size_t>(nc) + 1), mci(nnz), msrc(nnz), gci(nnz), gsrc(nnz), gdg(nc);
+    for (int c = 0; c < nc; ++c) ro[c + 1] = ro[c] + 1 + (cfo[c + 1] - cfo[c]);
+    for (int c = 0; c < nc; ++c) {
+        int k = ro[c];
+        mci[k] = c;
+        msrc[k] = c;
+        ++k;
+        for (int q = cfo[c]; q < cfo[c + 1]; ++q) {
+            const int f = cf[q];
+            const bool own = hOwner_[f] == c;
+            mci[k] = own ? hNeigh_[f] : hOwner_[f];
+            msrc[k] = own ? nc + f : nc + nf + f;
+            ++k;
+        }
+        k = ro[c];
+        for (int q = cfo[c]; q < cfo[c + 1]; ++q)  // lower faces ascending
+            if (hNeigh_[cf[q]] == c) {
+                gci[k] = hOwner_[cf[q]];
+                gsrc[k] = nc + nf + cf[q];
+                ++k;
+            }
+        gdg[c] = k;
+        gci[k] = c;
+        gsrc[k] = c;
+        ++k;
+        for (int q = cfo[c + 1] - 1; q >= cfo[c]; --q)  // upper faces descending
+            if (hOwner_[cf[q]] == c) {
+                gci[k] = hNeigh_[cf[q]];
+                gsrc[k] = nc + cf[q];
+                ++k;
+            }
+    }
+    auto up = [&](DArray<int>& d, const std::vector<int>& h) {
+        d.ensure(h.size() + 1, stream_);
+        check(cudaMemcpyAsync(d.p, h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice, stream_), "H2D host-LDU");
+    };
+    up(hlMvRo_, ro);
+    up(hlMvCi_, mci);
+    up(hlMvSrc_, msrc);
+    up(hlGsRo_, ro);
+    up(hlGsCi_, gci);
+    up(hlGsSrc_, gsrc);
+    up(hlGsDg_, gdg);
+    const size_t nn = static_cast<size_t>(n_) * n_;
+    hlMvV_.ensure(nnz * nn, stream_);
+    hlGsV_.ensure(nnz * nn, stream_);
+    sync();  // the host vectors die here
+    hlTopo_ = true;
+}
+
+// krylovSolve with the HostLdu operators (engine.cpp:54-72): blockMatvec and
+// LduLusgsPrecond arithmetic, on the device
+void Engine::solveHostLdu(const double* b, double* x, const bcs_solver_config& cfg, bcs_report& rep) {
+    LaunchScope ls(&launches_);
+    const size_t N = static_cast<size_t>(nc_) * n_;
+    kb_.ensure(N, stream_);
+    kx_.ensure(N, stream_);
+    h2d(kb_.p, b, N * sizeof(double), "H2D b");
+    h2d(kx_.p, x, N * sizeof(double), "H2D x");
+    distActive_ = false;
+    H_ = &main_;
+    nseg_ = 1;
+    const long long segh[2] = {0, static_cast<long long>(N)};
+    check(cudaMemcpyAsync(seg_.p, segh, sizeof segh, cudaMemcpyHostToDevice, stream_), "seg");
+    hist_.clear();
+    evUsed_ = 0;
+    spmvMs_ = sweepMs_ = sweepBytes_ = 0.0;
+    spmvCount_ = sweepCount_ = 0;
+    cudaMemsetAsync(err_.p + 1, 0, sizeof(int), stream_);
+    struct Flag {
+        bool& f;
+        ~Flag() { f = false; }
+    } flag{hostLdu_};
+    hostLdu_ = true;
+    FineMatrix F;  // the LUSGS slot order
+    F.rows = nc_;
+    F.nnz = nc_ + 2 * nf_;
+    F.ro = hlGsRo_;
+    F.ci = hlGsCi_;
+    F.dg = hlGsDg_;
+    F.tpos = nullptr;
+    F.v = hlGsV_;
+    const auto t0 = clk::now();
+    buildPrecondOn(F, cfg);
+    sync();
+    const auto t1 = clk::now();
+    solveKrylov(kb_, kx_.p, cfg, rep);
+    rep.t_amg_setup = secs(t0, t1);
+    rep.t_krylov = secs(t1, clk::now());
+    d2h(x, kx_.p, N * sizeof(double), "D2H x");
+    // the serial preconditioner now describes the host-LDU matrix, not vals_
+    main_.pcKind = -1;
 }
 
 // SolvePipeline::solve (engine.cpp:47-120)
@@ -1990,11 +2167,25 @@ void Engine::pipelineSolve(int nc, int nf, int n, const int32_t* owner, const in
     if (backend == BCS_BACKEND_HOST_LDU) {
         if (cfg.precond != BCS_PRECOND_NONE && cfg.precond != BCS_PRECOND_LUSGS)
             throw std::invalid_argument("host backend supports only none/LUSGS preconditioning");
+        validateConfig(cfg);
         const auto t0 = clk::now();
         if (!sameTopo) setTopology(nc, nf, n, owner, neigh);
-        uploadLdu(diag, upper, lower, false);
+        hostLduTopology();
+        // the LDU values in the two face-addressed slot orders
+        const size_t nn = static_cast<size_t>(n_) * n_;
+        ldu_diag_.ensure(nc_ * nn, stream_);
+        ldu_upper_.ensure(nf_ * nn, stream_);
+        ldu_lower_.ensure(nf_ * nn, stream_);
+        h2d(ldu_diag_.p, diag, sizeof(double) * nc_ * nn, "H2D diag");
+        if (nf_) {
+            h2d(ldu_upper_.p, upper, sizeof(double) * nf_ * nn, "H2D upper");
+            h2d(ldu_lower_.p, lower, sizeof(double) * nf_ * nn, "H2D lower");
+        }
+        const int nnz = nc_ + 2 * nf_;
+        gather_values(n_, nnz, nc_, nf_, hlMvSrc_, ldu_diag_, ldu_upper_, ldu_lower_, hlMvV_.p, stream_);
+        gather_values(n_, nnz, nc_, nf_, hlGsSrc_, ldu_diag_, ldu_upper_, ldu_lower_, hlGsV_.p, stream_);
         std::memcpy(x, x0, N * sizeof(double));
-        solveHost(b, x, cfg, rep);
+        solveHostLdu(b, x, cfg, rep);
         rep.t_solve = secs(t0, clk::now());
         rep.t_convert = rep.t_setup = rep.t_retrieve = rep.t_replace = 0.0;
         rep.setup_branch = 0;

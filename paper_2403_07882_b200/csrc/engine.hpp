@@ -301,6 +301,16 @@ private:
     DArray<int> asmInv_, asmCfo_, asmCf_, asmBco_, asmBkind_, asmBad_;
     DArray<double> asmMuGrad_, asmPsi_, asmFs_, asmBp_;
     DArray<double> asmArea_, asmBarea_, asmQ_, asmRhs_, asmFx_, asmVol_, asmCen_, asmBu_, asmPhi_, asmD_, asmGrad_;
+    // Backend::HostLdu (engine.cpp:54-72): the reference's face-addressed
+    // arithmetic on the device -- blockMatvec's order (block_matrix.cpp:104-119:
+    // diagonal, then the faces of a row in face order) and LduLusgsPrecond's
+    // (preconditioner.cpp:59-99: lower faces in face order forward, upper faces
+    // in face order backward) as two slot orders of the same blocks
+    bool hlTopo_ = false, hostLdu_ = false;
+    DArray<int> hlMvRo_, hlMvCi_, hlMvSrc_, hlGsRo_, hlGsCi_, hlGsSrc_, hlGsDg_;
+    DArray<double> hlMvV_, hlGsV_;
+    void hostLduTopology();
+    void solveHostLdu(const double* b, double* x, const bcs_solver_config& cfg, bcs_report& rep);
     // SolvePipeline state (engine.hpp:35-37): only the EngineCsr branch updates it
     bool pipeHasSetup_ = false;
     uint64_t pipeSig_ = 0;
