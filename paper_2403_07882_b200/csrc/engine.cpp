@@ -176,6 +176,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* m = std::getenv("BCS_DILU_MODE")) diluMode_ = std::atoi(m);  // 1: Kahn levels
     if (const char* m = std::getenv("BCS_DENSE_BLOCKED_MIN")) denseBlockedMin_ = std::atoi(m);
     if (const char* m = std::getenv("BCS_TAIL_ROWS")) tailMaxRows_ = std::atoi(m);
+    if (const char* m = std::getenv("BCS_DENSE_TILED_MIN")) denseTiledMin_ = std::atoi(m);
     check(cudaSetDevice(device), "cudaSetDevice");
     check(cudaStreamCreateWithFlags(&own_, cudaStreamNonBlocking), "cudaStreamCreate");
     stream_ = own_;
@@ -1194,6 +1195,17 @@ void Engine::smootherApply(Level& L, const double* r, double* z, int accumulate)
     if (timed) timerEnd(1, per + (accumulate == 2 ? 2.0 : accumulate == 1 ? 1.0 : 0.0) * R * 8.0 * nb);
 }
 
+// coarsest level: denseSolve (smallmat.hpp:163-174) in the reference's order;
+// from m >= denseTiledMin_ (scrambled inputs' stalled aggregation) the
+// backward substitution runs tiled (tolerance-level) unless the
+// EXACT mode asks for the reference's order throughout
+void Engine::denseSolve(const double* r, double* z) {
+    const int m = H_->m;
+    if (m >= denseTiledMin_ && !exactDots_) dense_solve_tiled(m, H_->dense, H_->dpiv, r, z, stream_);
+    else if (m >= denseBlockedMin_) dense_solve_big(m, H_->dense, H_->dpiv, r, z, stream_);
+    else dense_solve(m, H_->dense, H_->dpiv, r, z, stream_);
+}
+
 // AmgHierarchy::vcycle (amg.cpp:111-158)
 void Engine::vcycle(int l, const double* r, double* z) {
     Level& L = H_->levels[l];
@@ -1204,15 +1216,13 @@ void Engine::vcycle(int l, const double* r, double* z) {
         const int pre = H_->pcCfg.amg_pre_sweeps, post = H_->pcCfg.amg_post_sweeps;
         vcycle_tail(n_, nl, td, L.rows, r, z, pre, post, 0, err_.p + 1, stream_);
         const Level& Cl = H_->levels[H_->nlev - 1];
-        if (H_->m >= denseBlockedMin_) dense_solve_big(H_->m, H_->dense, H_->dpiv, Cl.r, Cl.z.p, stream_);
-        else dense_solve(H_->m, H_->dense, H_->dpiv, Cl.r, Cl.z.p, stream_);
+        denseSolve(Cl.r, Cl.z.p);
         vcycle_tail(n_, nl, td, L.rows, r, z, pre, post, 1, err_.p + 1, stream_);
         profMark("vcycle:tail L" + std::to_string(l) + "+");
         return;
     }
     if (l == H_->nlev - 1) {
-        if (H_->m >= denseBlockedMin_) dense_solve_big(H_->m, H_->dense, H_->dpiv, r, z, stream_);
-        else dense_solve(H_->m, H_->dense, H_->dpiv, r, z, stream_);
+        denseSolve(r, z);
         profMark("vcycle:dense_solve");
         return;
     }

@@ -373,6 +373,8 @@ private:
     int diluMode_ = 0;  // 0 sync-free level-ordered DILU setup, 1 Kahn levels
     int denseBlockedMin_ = kDenseBlockedMin;  // coarsest m from which the blocked dense LU/solve run
     int tailMaxRows_ = kTailMaxRows;          // levels at most this big run in the one-CTA tail (0: off)
+    int denseTiledMin_ = 2048;                // coarsest m from which the backward solve is tiled (non-EXACT)
+    void denseSolve(const double* r, double* z);
     int* hTot_ = nullptr;                     // pinned: per-level sweep program sizes
     void setupTail();
     std::vector<std::pair<std::string, double>> profRec_;

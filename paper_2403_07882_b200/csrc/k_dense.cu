@@ -475,7 +475,94 @@ __global__ void __launch_bounds__(1024) k_dense_solve_big(int m, const double* _
         for (int i = tid; i < m; i += nt) z[i] = x[i];
 }
 
+// Tolerance-level solve for large coarsest levels (the
+// scrambled inputs' aggregation stall leaves m in the thousands): the forward
+// substitution is k_dense_solve_big's (reference order, bit-exact); the
+// backward one runs by column tiles of 32 from the right -- warp 0 finishes a
+// tile's x (in-tile chain), then every thread folds the tile into the rows
+// above -- so the critical path is m/32 tiles, not the reference's m^2/2
+// dependent subtractions (whose order it does not keep: rounding differs).
+__global__ void __launch_bounds__(1024) k_dense_solve_tiled(int m, const double* __restrict__ lu,
+                                                            const int* __restrict__ perm, const double* r, double* z,
+                                                            int sx) {
+    extern __shared__ double sm[];
+    double* tile = sm;                     // 32 x 33
+    double* x = sx ? sm + 32 * 33 : z;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+    for (int i = tid; i < m; i += nt) x[i] = r[perm[i]];
+    __syncthreads();
+    for (int j0 = 0; j0 < m; j0 += 32) {  // forward (unit lower), reference order per row
+        const int j1 = j0 + 32 < m ? j0 + 32 : m;
+        for (int t = tid; t < 32 * 32; t += nt) {
+            const int i = j0 + t / 32, j = j0 + t % 32;
+            tile[(t / 32) * 33 + t % 32] = (i < j1 && j < i) ? lu[static_cast<size_t>(i) * m + j] : 0.0;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            const int i = j0 + lane;
+            double xi = i < j1 ? x[i] : 0.0;
+            for (int j = j0; j < j1 - 1; ++j) {
+                const double xj = __shfl_sync(0xffffffffu, xi, j - j0);
+                if (i > j && i < j1) xi = __dsub_rn(xi, __dmul_rn(tile[lane * 33 + (j - j0)], xj));
+            }
+            if (i < j1) x[i] = xi;
+        }
+        __syncthreads();
+        for (int i = j1 + tid; i < m; i += nt) {
+            double xi = x[i];
+            const double* row = lu + static_cast<size_t>(i) * m;
+#pragma unroll 8
+            for (int j = j0; j < j1; ++j) xi = __dsub_rn(xi, __dmul_rn(row[j], x[j]));
+            x[i] = xi;
+        }
+        __syncthreads();
+    }
+    for (int j1 = m; j1 > 0; j1 -= 32) {  // backward (upper), tiles from the right
+        const int j0 = j1 - 32 > 0 ? j1 - 32 : 0;
+        for (int t = tid; t < 32 * 32; t += nt) {
+            const int i = j0 + t / 32, j = j0 + t % 32;
+            tile[(t / 32) * 33 + t % 32] = (i < j1 && j < j1 && j >= i) ? lu[static_cast<size_t>(i) * m + j] : 0.0;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            const int i = j0 + lane;
+            double xi = i < j1 ? x[i] : 0.0;
+            for (int j = j1 - 1; j >= j0; --j) {
+                if (i == j) xi = __ddiv_rn(xi, tile[lane * 33 + (j - j0)]);
+                const double xj = __shfl_sync(0xffffffffu, xi, j - j0);
+                if (i < j && i >= j0) xi = __dsub_rn(xi, __dmul_rn(tile[lane * 33 + (j - j0)], xj));
+            }
+            if (i < j1) x[i] = xi;
+        }
+        __syncthreads();
+        for (int i = tid; i < j0; i += nt) {
+            double xi = x[i];
+            const double* row = lu + static_cast<size_t>(i) * m;
+#pragma unroll 8
+            for (int j = j0; j < j1; ++j) xi = __dsub_rn(xi, __dmul_rn(row[j], x[j]));
+            x[i] = xi;
+        }
+        __syncthreads();
+    }
+    if (sx)
+        for (int i = tid; i < m; i += nt) z[i] = x[i];
+}
+
 constexpr size_t kDenseSmemMax = 200 * 1024;
+
+void dense_solve_tiled(int m, const double* lu, const int* piv, const double* r, double* z, cudaStream_t s) {
+    const size_t full = (static_cast<size_t>(32) * 33 + static_cast<size_t>(m)) * sizeof(double);
+    const int sx = full <= kDenseSmemMax ? 1 : 0;
+    const size_t smem = sx ? full : static_cast<size_t>(32) * 33 * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_dense_solve_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kDenseSmemMax));
+        attr = true;
+    }
+    k_dense_solve_tiled<<<1, 1024, smem, s>>>(m, lu, piv + m, r, z, sx);
+    count_launch();
+}
 
 void dense_solve_big(int m, const double* lu, const int* piv, const double* r, double* z, cudaStream_t s) {
     const size_t full = (static_cast<size_t>(32) * 33 + 3 * static_cast<size_t>(m) + 128) * sizeof(double);

@@ -215,6 +215,8 @@ void vcycle_tail(int n, int nl, const TailLevelDev* lv, int top_rows, const doub
 // (pivots, then the composed permutation the solve uses)
 constexpr int kDenseBlockedMin = 256;
 void dense_factor_blocked(int m, double* a, int* piv, int* err, cudaStream_t s);
+// tolerance-level (tiled backward substitution) for large m; forward in reference order
+void dense_solve_tiled(int m, const double* lu, const int* piv, const double* r, double* z, cudaStream_t s);
 void dense_solve_big(int m, const double* lu, const int* piv, const double* r, double* z, cudaStream_t s);
 
 // ------------------------------------------------------ Krylov (K13-K15)

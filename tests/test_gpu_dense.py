@@ -89,3 +89,34 @@ def test_alternative_schedules_bit_exact(oracle, env, monkeypatch):
         assert z.tobytes() == zo.tobytes()
     finally:
         ctx.close()
+
+
+def test_tiled_dense_solve_tolerance_level(oracle, monkeypatch):
+    """Large coarsest levels (m >= 2048 by default; forced here from 64): the
+    backward substitution runs by tiles (tolerance-level): the
+    V-cycle application agrees with the reference-order one to rounding."""
+    monkeypatch.setenv("BCS_DENSE_TILED_MIN", "64")
+    monkeypatch.setenv("BCS_DENSE_BLOCKED_MIN", "64")
+    ctx = bcs.Context(0)
+    try:
+        s = gen.hex_euler(32, scramble_seed=7)
+        cfg = make_cfg(precond=3, max_levels=30, min_coarse=8)
+        r = np.random.default_rng(5).uniform(-1, 1, s.A.n_cells * s.A.n)
+        z = _apply(ctx, s, cfg, r)
+        m = (ctx.amg_level(ctx.amg_depth() - 1, s.A.n)[0].size - 1) * s.A.n
+        assert m >= 64
+        zo = oracle.precond_apply(s.A, cfg, r)
+        np.testing.assert_allclose(z, zo, rtol=0, atol=1e-10 * np.abs(zo).max())
+        # EXACT mode keeps the reference order (bit-identical solve)
+        rexact = ctx.solve(s.b.values, xe := s.x0.values.copy(),
+                           bcs.SolverConfig(preconditioner=bcs.PrecondKind.AMG, relTol=1e-8, maxIters=200,
+                                            amg=bcs.AmgConfig(maxLevels=30, minCoarseRows=8), mode=bcs.Mode.EXACT))
+        rc, xo, rep, ho = oracle.solve(s.A, s.b.values, s.x0.values, cfg)
+        assert rexact.iterations == rep.iterations and xe.tobytes() == xo.tobytes()
+        # default mode: tiled, iterations within +-1
+        rd = ctx.solve(s.b.values, s.x0.values.copy(),
+                       bcs.SolverConfig(preconditioner=bcs.PrecondKind.AMG, relTol=1e-8, maxIters=200,
+                                        amg=bcs.AmgConfig(maxLevels=30, minCoarseRows=8)))
+        assert rd.converged and abs(rd.iterations - rep.iterations) <= 1
+    finally:
+        ctx.close()
