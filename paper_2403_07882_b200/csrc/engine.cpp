@@ -177,6 +177,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* m = std::getenv("BCS_DENSE_BLOCKED_MIN")) denseBlockedMin_ = std::atoi(m);
     if (const char* m = std::getenv("BCS_TAIL_ROWS")) tailMaxRows_ = std::atoi(m);
     if (const char* m = std::getenv("BCS_DENSE_TILED_MIN")) denseTiledMin_ = std::atoi(m);
+    if (const char* m = std::getenv("BCS_MC_SWEEP")) mcSweep_ = std::atoi(m) != 0;
     check(cudaSetDevice(device), "cudaSetDevice");
     check(cudaStreamCreateWithFlags(&own_, cudaStreamNonBlocking), "cudaStreamCreate");
     stream_ = own_;
@@ -214,6 +215,7 @@ Engine::~Engine() {
             rel(M.r); rel(M.y); rel(M.zb);
         }
         rel(L.mcPerm);
+        rel(L.mcColorOffD);
         rel(L.o_ro); rel(L.o_ci); rel(L.o_dg); rel(L.o_tpos); rel(L.o_v); rel(L.lu); rel(L.rcp); rel(L.perm); rel(L.recf); rel(L.recb); rel(L.dlev); rel(L.offf); rel(L.offb); rel(L.pkf); rel(L.pkb); rel(L.piv); rel(L.order);
         rel(L.agg); rel(L.members); rel(L.r); rel(L.z); rel(L.res); rel(L.y); rel(L.zb);
     }
@@ -836,6 +838,10 @@ void Engine::finishSmoothers(const std::vector<Level*>& lv, const bcs_solver_con
         L.rcp.ensure(static_cast<size_t>(L.rows) * n_, stream_);
         L.perm.ensure(static_cast<size_t>(L.rows) * n_, stream_);
         make_reciprocals(n_, L.rows, L.lu, L.piv, L.rcp.p, L.perm.p, stream_);
+        if (L.colourSweep) {  // no sweep programs
+            hTot_[2 * l] = hTot_[2 * l + 1] = 0;
+            continue;
+        }
         L.recf.ensure(4 * static_cast<size_t>(L.rows), stream_);
         L.recb.ensure(4 * static_cast<size_t>(L.rows), stream_);
         sweep_records(L.rows, L.order, L.ro, L.dg, L.recf.p, L.recb.p, stream_);
@@ -868,6 +874,7 @@ void Engine::finishSmoothers(const std::vector<Level*>& lv, const bcs_solver_con
     }
     for (int l = 0; l < nl; ++l) {
         Level& L = *lv[l];
+        if (L.colourSweep) continue;
         for (int d = 0; d < 2; ++d) {
             DArray<unsigned char>& pk = d == 0 ? L.pkf : L.pkb;
             const size_t b = 16 * static_cast<size_t>(hTot_[2 * l + d]) + 16;
@@ -1057,6 +1064,10 @@ bool Engine::buildColoured(Level& L) {
     L.ncolors = mc_permutation(R, cnt_.p, L.mcPerm.p, act2_.p, flag_.p, flag_.cap, hTot_, stream_);
     L.mcColorOff.assign(1, 0);  // hTot_[c] = rows of colour c (mc_permutation)
     for (int c = 0; c < L.ncolors; ++c) L.mcColorOff.push_back(L.mcColorOff.back() + hTot_[c]);
+    L.mcColorOffD.ensure(L.mcColorOff.size(), stream_);
+    check(cudaMemcpyAsync(L.mcColorOffD.p, L.mcColorOff.data(), sizeof(int) * L.mcColorOff.size(),
+                          cudaMemcpyHostToDevice, stream_), "H2D colour offsets");
+    M.colourSweep = mcSweep_;
     M.rows = R;
     M.nnz = L.nnz;
     M.o_ro.ensure(static_cast<size_t>(R) + 1, stream_);
@@ -1172,7 +1183,23 @@ void Engine::smootherApply(Level& L, const double* r, double* z, int accumulate)
         // r in, result scattered back (and accumulated) in the level's numbering
         Level& M = *L.mc;
         mc_vec_gather(n_, L.rows, L.mcPerm, r, M.r.p, stream_);
-        smootherApply(M, M.r, M.zb.p, 0);
+        if (M.colourSweep) {
+            // colour-synchronous sweeps: the forward reads the lower triangle,
+            // the backward the upper one, each with the row's LU, input, output
+            const double nb = static_cast<double>(n_), R = static_cast<double>(M.rows);
+            const double per = 0.5 * (static_cast<double>(M.nnz) - R) * (8.0 * nb * nb + 4.0) +
+                               R * (8.0 * nb * nb + 8.0 * nb + 4.0 * nb + 12.0) + 2.0 * R * 8.0 * nb;
+            if (kernelTiming_) timerBegin();
+            mc_sweep(n_, true, M.rows, L.ncolors, L.mcColorOffD, M.ro, M.dg, M.ci, M.v, M.lu, M.rcp, M.perm, M.r,
+                     M.y.p, stream_);
+            if (kernelTiming_) timerEnd(1, per);
+            if (kernelTiming_) timerBegin();
+            mc_sweep(n_, false, M.rows, L.ncolors, L.mcColorOffD, M.ro, M.dg, M.ci, M.v, M.lu, M.rcp, M.perm, M.y,
+                     M.zb.p, stream_);
+            if (kernelTiming_) timerEnd(1, per);
+        } else {
+            smootherApply(M, M.r, M.zb.p, 0);
+        }
         mc_vec_scatter(n_, L.rows, L.mcPerm, M.zb, z, accumulate, stream_);
         return;
     }

@@ -117,6 +117,8 @@ struct Level {
     // performance mode (BCS_MODE_PERF): colour-permuted copy for the smoother
     std::unique_ptr<Level> mc;
     DArray<int> mcPerm;  // new (colour-ordered) row -> row
+    DArray<int> mcColorOffD;  // device copy of mcColorOff
+    bool colourSweep = false; // this is a coloured copy: colour-synchronous sweeps, no sweep programs
     int ncolors = 0;
     std::vector<int> mcColorOff;  // colour c = new rows [off[c], off[c+1])
     bool mcValid = false;  // mc built for the current values
@@ -374,6 +376,7 @@ private:
     int denseBlockedMin_ = kDenseBlockedMin;  // coarsest m from which the blocked dense LU/solve run
     int tailMaxRows_ = kTailMaxRows;          // levels at most this big run in the one-CTA tail (0: off)
     int denseTiledMin_ = 2048;                // coarsest m from which the backward solve is tiled (non-EXACT)
+    bool mcSweep_ = true;                     // perf mode: colour-synchronous sweeps (0: sync-free on the copy)
     void denseSolve(const double* r, double* z);
     int* hTot_ = nullptr;                     // pinned: per-level sweep program sizes
     void setupTail();

@@ -17,7 +17,10 @@
 #include "device.cuh"
 #include "kernels.hpp"
 
+#include <cooperative_groups.h>
+
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 namespace bcs {
@@ -40,32 +43,44 @@ constexpr int kMaxColors = 64;
 __global__ void k_jp_round(int rows, const int* __restrict__ ro, const int* __restrict__ ci, const int* __restrict__ cin,
                            int* cout, int* left, int* overflow) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= rows) return;
-    const int ci0 = cin[i];
-    cout[i] = ci0;
-    if (ci0 >= 0) return;
-    const unsigned hi = mc_hash(static_cast<unsigned>(i));
-    unsigned long long used = 0ull;
-    for (int k = ro[i]; k < ro[i + 1]; ++k) {
-        const int j = ci[k];
-        if (j == i) continue;
-        const int cj = cin[j];
-        if (cj < 0) {
-            if (mc_above(mc_hash(static_cast<unsigned>(j)), j, hi, i)) {  // an uncoloured neighbour goes first
-                atomicAdd(left, 1);
-                return;
+    bool wait = false, over = false;
+    if (i < rows) {
+        const int ci0 = cin[i];
+        int out = ci0;
+        if (ci0 < 0) {
+            const unsigned hi = mc_hash(static_cast<unsigned>(i));
+            unsigned long long used = 0ull;
+            for (int k = ro[i]; k < ro[i + 1]; ++k) {
+                const int j = ci[k];
+                if (j == i) continue;
+                const int cj = cin[j];
+                if (cj < 0) {
+                    if (mc_above(mc_hash(static_cast<unsigned>(j)), j, hi, i)) {  // an uncoloured neighbour goes first
+                        wait = true;
+                        break;
+                    }
+                } else if (cj < kMaxColors) {
+                    used |= 1ull << cj;
+                }
             }
-        } else if (cj < kMaxColors) {
-            used |= 1ull << cj;
+            if (!wait) {
+                const unsigned long long freeMask = ~used;
+                if (!freeMask) {
+                    over = true;
+                    out = kMaxColors;  // colour count overflow: reported, level falls back
+                } else {
+                    out = __ffsll(static_cast<long long>(freeMask)) - 1;
+                }
+            }
         }
+        cout[i] = out;
     }
-    const unsigned long long freeMask = ~used;
-    if (!freeMask) {
-        atomicExch(overflow, 1);
-        cout[i] = kMaxColors;  // colour count overflow: reported, level falls back
-        return;
+    // one atomic per warp (a single counter would serialise millions of rows)
+    const unsigned wm = __ballot_sync(0xffffffffu, wait), om = __ballot_sync(0xffffffffu, over);
+    if ((threadIdx.x & 31) == 0) {
+        if (wm) atomicAdd(left, __popc(wm));
+        if (om) atomicExch(overflow, 1);
     }
-    cout[i] = __ffsll(static_cast<long long>(freeMask)) - 1;
 }
 
 __global__ void k_color_hist(int rows, const int* __restrict__ color, int* cnt) {
@@ -245,6 +260,133 @@ void mc_vec_gather(int n, int rows, const int* perm, const double* x, double* xp
 void mc_vec_scatter(int n, int rows, const int* perm, const double* sp, double* z, int acc, cudaStream_t s) {
     k_vec_scatter<<<(rows * n + 255) / 256, 256, 0, s>>>(n, rows, perm, sp, z, acc);
     count_launch();
+}
+
+
+// ---- colour-synchronous sweeps of a coloured level --------------------------
+// On the colour-permuted matrix every dependency of a row of colour c has a
+// smaller colour (forward) / larger colour (backward), so the sweep is c
+// rounds of independent rows: one cooperative kernel, grid barrier between
+// colours, no per-row dependency polling and no staging -- an HBM stream over
+// the level's triangle like an SpMV.  N lanes per row (lane q = component q),
+// 32/N rows per warp; the arithmetic is k_sweep's (k_sweep.cu) operation for
+// operation: acc = r_i - sum_k (A_ik y_k) per block in slot order (backward:
+// 0 + sum over the upper slots from the last one down), the composed pivot
+// permutation, the reciprocal-based LU solve with the exact IEEE fallback --
+// so the result is bit-identical to the sync-free sweeps on the same matrix.
+template <int N, bool FWD>
+__global__ void __launch_bounds__(256) k_mc_sweep(int ncol, const int* __restrict__ coff, const int* __restrict__ ro,
+                                                  const int* __restrict__ dg, const int* __restrict__ ci,
+                                                  const double* __restrict__ v, const double* __restrict__ lu,
+                                                  const double* __restrict__ rcp, const int* __restrict__ perm,
+                                                  const double* __restrict__ rin, double* out) {
+    namespace cg = cooperative_groups;
+    constexpr int NN = N * N, G = 32 / N;
+    cg::grid_group grid = cg::this_grid();
+    const int lane = threadIdx.x & 31, g = lane / N, q = lane - (lane / N) * N;
+    const int warp = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int W = static_cast<int>((gridDim.x * blockDim.x) >> 5);
+    for (int cc = 0; cc < ncol; ++cc) {
+        const int c = FWD ? cc : ncol - 1 - cc;
+        const int b = __ldg(&coff[c]), e = __ldg(&coff[c + 1]);
+        for (int i0 = b + warp * G; i0 < e; i0 += W * G) {
+            const int i = i0 + g;
+            const bool row = g < G && i < e;
+            double ri = 0.0, acc = 0.0;
+            if (row) {
+                ri = __ldg(&rin[static_cast<size_t>(i) * N + q]);
+                acc = FWD ? ri : 0.0;
+                const int k0 = __ldg(&ro[i]), kd = __ldg(&dg[i]), k1 = __ldg(&ro[i + 1]);
+                if (FWD) {
+                    for (int k = k0; k < kd; ++k) {
+                        const double* a = v + static_cast<size_t>(k) * NN + q * N;
+                        const double* y = out + static_cast<size_t>(__ldg(&ci[k])) * N;
+                        double s = 0.0;
+#pragma unroll
+                        for (int p = 0; p < N; ++p) s = __dadd_rn(s, __dmul_rn(__ldg(&a[p]), __ldcg(&y[p])));
+                        acc = __dsub_rn(acc, s);
+                    }
+                } else {
+                    for (int k = k1 - 1; k > kd; --k) {
+                        const double* a = v + static_cast<size_t>(k) * NN + q * N;
+                        const double* y = out + static_cast<size_t>(__ldg(&ci[k])) * N;
+                        double s = 0.0;
+#pragma unroll
+                        for (int p = 0; p < N; ++p) s = __dadd_rn(s, __dmul_rn(__ldg(&a[p]), __ldcg(&y[p])));
+                        acc = __dadd_rn(acc, s);
+                    }
+                }
+            }
+            // composed pivot permutation: x[p] = acc of component perm[p] of this row
+            const size_t ib = static_cast<size_t>(row ? i : 0);
+            double x[N];
+#pragma unroll
+            for (int p = 0; p < N; ++p) {
+                const int src = row ? g * N + __ldg(&perm[ib * N + p]) : lane;
+                x[p] = __shfl_sync(0xffffffffu, acc, src);
+            }
+            if (row) {
+                double lf[NN], rc[N];
+#pragma unroll
+                for (int t = 0; t < NN; ++t) lf[t] = __ldg(&lu[ib * NN + t]);
+#pragma unroll
+                for (int p = 0; p < N; ++p) rc[p] = __ldg(&rcp[ib * N + p]);
+                DVec<N> xin;
+#pragma unroll
+                for (int p = 0; p < N; ++p) xin.v[p] = x[p];
+                if (__builtin_expect(!lu_solve_perm_fast<N>(lf, rc, x), 0)) {
+                    const DVec<N> xe = lu_solve_perm_exact<N>(lu + ib * NN, xin);
+#pragma unroll
+                    for (int p = 0; p < N; ++p) x[p] = xe.v[p];
+                }
+                double mine = x[0];
+#pragma unroll
+                for (int p = 1; p < N; ++p) mine = (q == p) ? x[p] : mine;
+                out[ib * N + q] = FWD ? mine : __dsub_rn(ri, mine);
+            }
+        }
+        if (cc + 1 < ncol) grid.sync();
+    }
+}
+
+template <int N, bool FWD>
+static void launch_mc_sweep(int rows, int ncol, const int* coff, const int* ro, const int* dg, const int* ci,
+                            const double* v, const double* lu, const double* rcp, const int* perm, const double* rin,
+                            double* out, cudaStream_t s) {
+    static int cap = 0;
+    if (!cap) {
+        int bps = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_mc_sweep<N, FWD>, 256, 0);
+        cap = num_sms() * (bps < 1 ? 1 : bps);
+    }
+    constexpr int G = 32 / N;
+    long long want = (static_cast<long long>(rows) / G + 63) / 64;  // ~8 row groups per warp per pass over the level
+    int g = static_cast<int>(want < 1 ? 1 : (want > cap ? cap : want));
+    void* args[] = {(void*)&ncol, (void*)&coff, (void*)&ro, (void*)&dg, (void*)&ci, (void*)&v,
+                    (void*)&lu, (void*)&rcp, (void*)&perm, (void*)&rin, (void*)&out};
+    const cudaError_t e = cudaLaunchCooperativeKernel((void*)k_mc_sweep<N, FWD>, dim3(g), dim3(256), args, 0, s);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("colour sweep launch failed: ") + cudaGetErrorString(e));
+    count_launch();
+}
+
+void mc_sweep(int n, bool fwd, int rows, int ncol, const int* coff, const int* ro, const int* dg, const int* ci,
+              const double* v, const double* lu, const double* rcp, const int* perm, const double* rin, double* out,
+              cudaStream_t s) {
+    if (rows <= 0) return;
+    switch (n) {
+#define BCS_MC_CASE(NV)                                                                                            \
+    case NV:                                                                                                       \
+        if (fwd) launch_mc_sweep<NV, true>(rows, ncol, coff, ro, dg, ci, v, lu, rcp, perm, rin, out, s);           \
+        else launch_mc_sweep<NV, false>(rows, ncol, coff, ro, dg, ci, v, lu, rcp, perm, rin, out, s);              \
+        break;
+        BCS_MC_CASE(1)
+        BCS_MC_CASE(2)
+        BCS_MC_CASE(3)
+        BCS_MC_CASE(4)
+        BCS_MC_CASE(5)
+#undef BCS_MC_CASE
+        default: throw std::invalid_argument("block size must be 1..5 on the device");
+    }
 }
 
 }  // namespace bcs
