@@ -376,7 +376,7 @@ private:
     int denseBlockedMin_ = kDenseBlockedMin;  // coarsest m from which the blocked dense LU/solve run
     int tailMaxRows_ = kTailMaxRows;          // levels at most this big run in the one-CTA tail (0: off)
     int denseTiledMin_ = 2048;                // coarsest m from which the backward solve is tiled (non-EXACT)
-    bool mcSweep_ = true;                     // perf mode: colour-synchronous sweeps (0: sync-free on the copy)
+    bool mcSweep_ = false;                    // perf mode: colour-synchronous sweeps (BCS_MC_SWEEP=1; measured slower)
     void denseSolve(const double* r, double* z);
     int* hTot_ = nullptr;                     // pinned: per-level sweep program sizes
     void setupTail();
