@@ -19,6 +19,7 @@
 
 #include <cooperative_groups.h>
 
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
