@@ -1628,13 +1628,13 @@ void Engine::opAxpyDot(double* w, const double* h, const double* v, const double
     if (exactDots_) {
         const size_t N = static_cast<size_t>(nc_) * n_;
         if (mpActive_) {
-            axpy_dot_seq(w, h, v, nextv, N, seg_, 1, mpPart_.p, partials_.p, stream_);
+            axpy_dot_seq(w, h, v, nextv, N, seg_, 1, mpPart_.p, partials_.p, false, stream_);  // sqrt after the fold
             nccl::ck(nccl::api().allGather(mpPart_.p, mpGath_.p, 1, ncclDouble, static_cast<ncclComm_t>(comm_), stream_),
                      "allgather");
             fold_engines(mpGath_, mpSize_, out, nextv == nullptr, stream_);
             return;
         }
-        axpy_dot_seq(w, h, v, nextv, N, seg_, nseg_, out, partials_.p, stream_);
+        axpy_dot_seq(w, h, v, nextv, N, seg_, nseg_, out, partials_.p, nextv == nullptr, stream_);
         return;
     }
     if (mpActive_) {

@@ -25,6 +25,7 @@
 #include "kernels.hpp"
 
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -222,6 +223,168 @@ __global__ void __launch_bounds__(256) k_dense_panel_coop(int m, int k0, int nb,
     }
 }
 
+// The same panel on ONE thread-block cluster of kPanelCl CTAs: the panel's
+// rows live in the cluster's distributed shared memory (CTA c owns rows
+// [k0 + c*per, ...)), a step's candidates and the pivot / swapped rows are
+// read from peer CTAs' shared memory, and the two grid barriers per step
+// become cluster barriers (~0.5 us instead of a few us over the whole grid).
+// Same pivot rule and per-element operation sequence as k_dense_panel_coop.
+constexpr int kPanelCl = 16;
+__device__ __forceinline__ unsigned dsm_map(const void* p, unsigned cta) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))), "r"(cta));
+    return r;
+}
+__device__ __forceinline__ double dsm_ld(unsigned addr) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ int dsm_ld_int(unsigned addr) {
+    int v;
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void cl_barrier() {
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(512, 1) k_dense_panel_cl(int m, int k0, int nb, int per, double* a, int* piv,
+                                                           int* err) {
+    extern __shared__ double sp[];  // per x kDB rows of the panel
+    __shared__ double cand_v, rb[kDB], rk[kDB];
+    __shared__ int cand_i;
+    __shared__ double sv[16];
+    __shared__ int si[16];
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+    unsigned c;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(c));
+    const int r0 = k0 + static_cast<int>(c) * per;
+    const int r1 = min(m, r0 + per);
+    const int k1 = k0 + nb;
+    for (int t = tid; t < per * nb; t += nt) {
+        const int rr = t / nb, j = t % nb;
+        sp[rr * kDB + j] = r0 + rr < r1 ? a[static_cast<size_t>(r0 + rr) * m + k0 + j] : 0.0;
+    }
+    __syncthreads();
+    cl_barrier();  // every CTA's rows are loaded before any peer reads them
+    for (int k = k0; k < k1; ++k) {
+        const int kc = k - k0;
+        double best = -1.0;
+        int bi = 0x7fffffff;
+        for (int i = max(r0, k) + tid; i < r1; i += nt) {
+            const double v = fabs(sp[(i - r0) * kDB + kc]);
+            if (v > best || (v == best && i < bi)) {
+                best = v;
+                bi = i;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_down_sync(0xffffffffu, best, o);
+            const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+            if (ov > best || (ov == best && oi < bi)) {
+                best = ov;
+                bi = oi;
+            }
+        }
+        if (lane == 0) {
+            sv[wid] = best;
+            si[wid] = bi;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 1; w < (nt >> 5); ++w)
+                if (sv[w] > sv[0] || (sv[w] == sv[0] && si[w] < si[0])) {
+                    sv[0] = sv[w];
+                    si[0] = si[w];
+                }
+            cand_v = sv[0];
+            cand_i = si[0];
+        }
+        cl_barrier();  // A: candidates visible cluster-wide
+        // every CTA reduces the kPanelCl candidates in CTA order (same result everywhere)
+        __shared__ int s_p;
+        __shared__ double s_pv;
+        if (wid == 0) {
+            double b2 = -1.0;
+            int i2 = 0x7fffffff;
+            if (lane < kPanelCl) {
+                b2 = dsm_ld(dsm_map(&cand_v, lane));
+                i2 = dsm_ld_int(dsm_map(&cand_i, lane));
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_down_sync(0xffffffffu, b2, o);
+                const int oi = __shfl_down_sync(0xffffffffu, i2, o);
+                if (ov > b2 || (ov == b2 && oi < i2)) {
+                    b2 = ov;
+                    i2 = oi;
+                }
+            }
+            if (lane == 0) {
+                s_p = i2;
+                s_pv = b2;
+            }
+        }
+        __syncthreads();
+        const int p = s_p;
+        if (c == 0 && tid == 0) {
+            piv[k] = p;
+            if (s_pv < 1e-300) atomicExch(err, 1);
+        }
+        // the pivot row (old row p) into every CTA; its owner also takes old row k
+        const unsigned op = static_cast<unsigned>((p - k0) / per), ok = static_cast<unsigned>((k - k0) / per);
+        for (int j = tid; j < nb; j += nt) {
+            rb[j] = dsm_ld(dsm_map(&sp[(p - (k0 + static_cast<int>(op) * per)) * kDB + j], op));
+            if (c == op && p != k) rk[j] = dsm_ld(dsm_map(&sp[(k - (k0 + static_cast<int>(ok) * per)) * kDB + j], ok));
+        }
+        cl_barrier();  // B: every read of rows p and k done before they are overwritten
+        if (k >= r0 && k < r1)
+            for (int j = tid; j < nb; j += nt) sp[(k - r0) * kDB + j] = rb[j];
+        if (p != k && p >= r0 && p < r1)
+            for (int j = tid; j < nb; j += nt) sp[(p - r0) * kDB + j] = rk[j];
+        __syncthreads();
+        const double d = rb[kc];
+        for (int i = max(r0, k + 1) + tid; i < r1; i += nt) {
+            double* row = sp + (i - r0) * kDB;
+            const double l = __ddiv_rn(row[kc], d);
+            row[kc] = l;
+            for (int j = kc + 1; j < nb; ++j) row[j] = __dsub_rn(row[j], __dmul_rn(l, rb[j]));
+        }
+        __syncthreads();
+    }
+    for (int t = tid; t < per * nb; t += nt) {
+        const int rr = t / nb, j = t % nb;
+        if (r0 + rr < r1) a[static_cast<size_t>(r0 + rr) * m + k0 + j] = sp[rr * kDB + j];
+    }
+    cl_barrier();  // no CTA exits while a peer may still read its shared memory
+}
+
+static bool panel_cl_ok(size_t smem) {
+    static int ok = -1;
+    if (ok < 0) {
+        ok = 0;
+        if (cudaFuncSetAttribute(k_dense_panel_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ==
+                cudaSuccess &&
+            cudaFuncSetAttribute(k_dense_panel_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = kPanelCl;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3(kPanelCl);
+            cfg.blockDim = dim3(512);
+            cfg.dynamicSmemBytes = 200 * 1024;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int nc = 0;
+            if (cudaOccupancyMaxActiveClusters(&nc, k_dense_panel_cl, &cfg) == cudaSuccess && nc >= 1) ok = 1;
+        }
+        cudaGetLastError();
+    }
+    return ok == 1 && smem <= 200 * 1024;
+}
+
 // the panel's row swaps, in order, on every column outside the panel
 __global__ void k_dense_laswp(int m, int k0, int nb, double* a, const int* piv) {
     const int j0 = blockIdx.x * blockDim.x + threadIdx.x;
@@ -323,6 +486,12 @@ __global__ void k_dense_perm(int m, const int* piv, int* perm) {
     }
 }
 
+// BCS_DENSE_PANEL_CL=0: the grid-cooperative panel only
+static int g_panel_cl = [] {
+    const char* e = std::getenv("BCS_DENSE_PANEL_CL");
+    return e ? std::atoi(e) : 1;
+}();
+
 void dense_factor_blocked(int m, double* a, int* piv, int* err, cudaStream_t s) {
     static bool attr = false;
     const int smem = 2 * kDB * 64 * static_cast<int>(sizeof(double));
@@ -348,7 +517,24 @@ void dense_factor_blocked(int m, double* a, int* piv, int* err, cudaStream_t s) 
         int per = (rows + g - 1) / g;
         g = (rows + per - 1) / per;
         const size_t psmem = sizeof(double) * static_cast<size_t>(per) * kDB;
-        if (psmem <= 200 * 1024) {
+        const int pcl = (rows + kPanelCl - 1) / kPanelCl;
+        const size_t clsmem = sizeof(double) * static_cast<size_t>(pcl) * kDB;
+        if (g_panel_cl && rows >= 4 * kPanelCl && panel_cl_ok(clsmem)) {
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = kPanelCl;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3(kPanelCl);
+            cfg.blockDim = dim3(512);
+            cfg.dynamicSmemBytes = clsmem;
+            cfg.stream = s;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            const cudaError_t e = cudaLaunchKernelEx(&cfg, k_dense_panel_cl, m, k0, nb, pcl, a, piv, err);
+            if (e != cudaSuccess) throw std::runtime_error(std::string("dense cluster panel: ") + cudaGetErrorString(e));
+        } else if (psmem <= 200 * 1024) {
             static size_t attr_p = 0;
             if (psmem > attr_p) {
                 cudaFuncSetAttribute(k_dense_panel_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

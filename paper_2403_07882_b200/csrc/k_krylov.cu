@@ -131,10 +131,10 @@ void dot_seq(const double* a, const double* b, const long long* seg, int nseg, d
     fold_engines(partials, nseg, out, sqrt_out, s);
 }
 void axpy_dot_seq(double* w, const double* h, const double* v, const double* nextv, size_t N, const long long* seg,
-                  int nseg, double* out, double* partials, cudaStream_t s) {
+                  int nseg, double* out, double* partials, bool sqrt_out, cudaStream_t s) {
     k_axpy<<<4 * num_sms(), 256, 0, s>>>(w, h, v, N);
     count_launch();
-    dot_seq(w, nextv ? nextv : w, seg, nseg, out, nextv == nullptr, partials, s);
+    dot_seq(w, nextv ? nextv : w, seg, nseg, out, sqrt_out, partials, s);
 }
 
 static int seg_grid(int nseg) {

@@ -243,7 +243,7 @@ void fold_engines(const double* parts, int G, double* out, bool sqrt_out, cudaSt
 void dot_seq(const double* a, const double* b, const long long* seg, int nseg, double* out, bool sqrt_out,
              double* partials, cudaStream_t s);
 void axpy_dot_seq(double* w, const double* h, const double* v, const double* nextv, size_t N, const long long* seg,
-                  int nseg, double* out, double* partials, cudaStream_t s);
+                  int nseg, double* out, double* partials, bool sqrt_out, cudaStream_t s);
 // the reference libm's hypot (glibc algorithm) on n device pairs
 void hypot_eval(const double* x, const double* y, double* out, int n, cudaStream_t s);
 void pack_rows(int n, int cnt, const int* idx, const double* x, double* out, cudaStream_t s);

@@ -102,3 +102,35 @@ def test_dist_fgmres_matches_reference_gmres(ctx, ref, ranks, engines):
     x, r = ctx.dist_solve(s.A, s.b, s.x0, s.centroids, ranks, engines, cfg)
     assert r.converged and rr.converged and r.iterations == rr.iterations
     np.testing.assert_allclose(x.values, xr, rtol=0, atol=1e-6 * np.abs(xr).max())
+
+
+@pytest.mark.parametrize("maker", [lambda: gen.hex_euler(10), lambda: gen.hex_coupled(8, scramble_seed=3)])
+@pytest.mark.parametrize("ranks,engines", [(2, 2), (4, 2), (3, 2), (8, 3)])
+@pytest.mark.parametrize("method", [0, 1])
+def test_dist_exact_mode_bit_identical_to_reference(ctx, ref, maker, ranks, engines, method):
+    """EXACT mode in Mode R: per-engine sequential dot partials folded by the
+    reference's pairwise engine tree (partition.cpp:433-450) -- the reference's
+    distributedSolve bit for bit: iterations, final residual and solution."""
+    s = maker()
+    cfg_t = make_cfg(method=method, precond=3, max_iters=400)
+    cfg = bcs.SolverConfig(method=bcs.KrylovMethod(method), preconditioner=bcs.PrecondKind.AMG, relTol=1e-8,
+                           maxIters=400, amg=bcs.AmgConfig(maxLevels=30, minCoarseRows=8), mode=bcs.Mode.EXACT)
+    rc, xr, rr = ref_distributed_solve(ref, s.A, s.b.values, s.x0.values, s.centroids, ranks, engines, cfg_t)
+    assert rc == 0, ref.err()
+    x, r = ctx.dist_solve(s.A, s.b, s.x0, s.centroids, ranks, engines, cfg)
+    assert r.iterations == rr.iterations and r.converged == bool(rr.converged)
+    assert r.finalResidual == rr.final_residual
+    assert x.values.tobytes() == xr.tobytes()
+
+
+def test_dist_mp_exact_mode_equals_one_device(ctx):
+    """EXACT mode through the NCCL path (one process) equals the one-device engines bit for bit."""
+    uid = bcs.comm_unique_id()
+    ctx.comm_init(0, 1, uid)
+    s = gen.hex_euler(9, scramble_seed=5)
+    cfg = bcs.SolverConfig(preconditioner=bcs.PrecondKind.AMG, relTol=1e-9, maxIters=500,
+                           amg=bcs.AmgConfig(maxLevels=30, minCoarseRows=8), mode=bcs.Mode.EXACT)
+    x1, r1 = ctx.dist_solve(s.A, s.b, s.x0, s.centroids, 3, 1, cfg)
+    x2, r2 = ctx.dist_solve_mp(s.A, s.b, s.x0, s.centroids, 3, cfg)
+    assert r1.iterations == r2.iterations and r2.converged
+    assert x1.values.tobytes() == x2.values.tobytes()
