@@ -223,168 +223,6 @@ __global__ void __launch_bounds__(256) k_dense_panel_coop(int m, int k0, int nb,
     }
 }
 
-// The same panel on ONE thread-block cluster of kPanelCl CTAs: the panel's
-// rows live in the cluster's distributed shared memory (CTA c owns rows
-// [k0 + c*per, ...)), a step's candidates and the pivot / swapped rows are
-// read from peer CTAs' shared memory, and the two grid barriers per step
-// become cluster barriers (~0.5 us instead of a few us over the whole grid).
-// Same pivot rule and per-element operation sequence as k_dense_panel_coop.
-constexpr int kPanelCl = 16;
-__device__ __forceinline__ unsigned dsm_map(const void* p, unsigned cta) {
-    unsigned r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))), "r"(cta));
-    return r;
-}
-__device__ __forceinline__ double dsm_ld(unsigned addr) {
-    double v;
-    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
-    return v;
-}
-__device__ __forceinline__ int dsm_ld_int(unsigned addr) {
-    int v;
-    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
-    return v;
-}
-__device__ __forceinline__ void cl_barrier() {
-    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
-}
-
-__global__ void __launch_bounds__(512, 1) k_dense_panel_cl(int m, int k0, int nb, int per, double* a, int* piv,
-                                                           int* err) {
-    extern __shared__ double sp[];  // per x kDB rows of the panel
-    __shared__ double cand_v, rb[kDB], rk[kDB];
-    __shared__ int cand_i;
-    __shared__ double sv[16];
-    __shared__ int si[16];
-    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
-    unsigned c;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(c));
-    const int r0 = k0 + static_cast<int>(c) * per;
-    const int r1 = min(m, r0 + per);
-    const int k1 = k0 + nb;
-    for (int t = tid; t < per * nb; t += nt) {
-        const int rr = t / nb, j = t % nb;
-        sp[rr * kDB + j] = r0 + rr < r1 ? a[static_cast<size_t>(r0 + rr) * m + k0 + j] : 0.0;
-    }
-    __syncthreads();
-    cl_barrier();  // every CTA's rows are loaded before any peer reads them
-    for (int k = k0; k < k1; ++k) {
-        const int kc = k - k0;
-        double best = -1.0;
-        int bi = 0x7fffffff;
-        for (int i = max(r0, k) + tid; i < r1; i += nt) {
-            const double v = fabs(sp[(i - r0) * kDB + kc]);
-            if (v > best || (v == best && i < bi)) {
-                best = v;
-                bi = i;
-            }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_down_sync(0xffffffffu, best, o);
-            const int oi = __shfl_down_sync(0xffffffffu, bi, o);
-            if (ov > best || (ov == best && oi < bi)) {
-                best = ov;
-                bi = oi;
-            }
-        }
-        if (lane == 0) {
-            sv[wid] = best;
-            si[wid] = bi;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            for (int w = 1; w < (nt >> 5); ++w)
-                if (sv[w] > sv[0] || (sv[w] == sv[0] && si[w] < si[0])) {
-                    sv[0] = sv[w];
-                    si[0] = si[w];
-                }
-            cand_v = sv[0];
-            cand_i = si[0];
-        }
-        cl_barrier();  // A: candidates visible cluster-wide
-        // every CTA reduces the kPanelCl candidates in CTA order (same result everywhere)
-        __shared__ int s_p;
-        __shared__ double s_pv;
-        if (wid == 0) {
-            double b2 = -1.0;
-            int i2 = 0x7fffffff;
-            if (lane < kPanelCl) {
-                b2 = dsm_ld(dsm_map(&cand_v, lane));
-                i2 = dsm_ld_int(dsm_map(&cand_i, lane));
-            }
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_down_sync(0xffffffffu, b2, o);
-                const int oi = __shfl_down_sync(0xffffffffu, i2, o);
-                if (ov > b2 || (ov == b2 && oi < i2)) {
-                    b2 = ov;
-                    i2 = oi;
-                }
-            }
-            if (lane == 0) {
-                s_p = i2;
-                s_pv = b2;
-            }
-        }
-        __syncthreads();
-        const int p = s_p;
-        if (c == 0 && tid == 0) {
-            piv[k] = p;
-            if (s_pv < 1e-300) atomicExch(err, 1);
-        }
-        // the pivot row (old row p) into every CTA; its owner also takes old row k
-        const unsigned op = static_cast<unsigned>((p - k0) / per), ok = static_cast<unsigned>((k - k0) / per);
-        for (int j = tid; j < nb; j += nt) {
-            rb[j] = dsm_ld(dsm_map(&sp[(p - (k0 + static_cast<int>(op) * per)) * kDB + j], op));
-            if (c == op && p != k) rk[j] = dsm_ld(dsm_map(&sp[(k - (k0 + static_cast<int>(ok) * per)) * kDB + j], ok));
-        }
-        cl_barrier();  // B: every read of rows p and k done before they are overwritten
-        if (k >= r0 && k < r1)
-            for (int j = tid; j < nb; j += nt) sp[(k - r0) * kDB + j] = rb[j];
-        if (p != k && p >= r0 && p < r1)
-            for (int j = tid; j < nb; j += nt) sp[(p - r0) * kDB + j] = rk[j];
-        __syncthreads();
-        const double d = rb[kc];
-        for (int i = max(r0, k + 1) + tid; i < r1; i += nt) {
-            double* row = sp + (i - r0) * kDB;
-            const double l = __ddiv_rn(row[kc], d);
-            row[kc] = l;
-            for (int j = kc + 1; j < nb; ++j) row[j] = __dsub_rn(row[j], __dmul_rn(l, rb[j]));
-        }
-        __syncthreads();
-    }
-    for (int t = tid; t < per * nb; t += nt) {
-        const int rr = t / nb, j = t % nb;
-        if (r0 + rr < r1) a[static_cast<size_t>(r0 + rr) * m + k0 + j] = sp[rr * kDB + j];
-    }
-    cl_barrier();  // no CTA exits while a peer may still read its shared memory
-}
-
-static bool panel_cl_ok(size_t smem) {
-    static int ok = -1;
-    if (ok < 0) {
-        ok = 0;
-        if (cudaFuncSetAttribute(k_dense_panel_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ==
-                cudaSuccess &&
-            cudaFuncSetAttribute(k_dense_panel_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
-            cudaLaunchConfig_t cfg = {};
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = kPanelCl;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            cfg.gridDim = dim3(kPanelCl);
-            cfg.blockDim = dim3(512);
-            cfg.dynamicSmemBytes = 200 * 1024;
-            cfg.attrs = at;
-            cfg.numAttrs = 1;
-            int nc = 0;
-            if (cudaOccupancyMaxActiveClusters(&nc, k_dense_panel_cl, &cfg) == cudaSuccess && nc >= 1) ok = 1;
-        }
-        cudaGetLastError();
-    }
-    return ok == 1 && smem <= 200 * 1024;
-}
-
 // the panel's row swaps, in order, on every column outside the panel
 __global__ void k_dense_laswp(int m, int k0, int nb, double* a, const int* piv) {
     const int j0 = blockIdx.x * blockDim.x + threadIdx.x;
@@ -486,12 +324,6 @@ __global__ void k_dense_perm(int m, const int* piv, int* perm) {
     }
 }
 
-// BCS_DENSE_PANEL_CL=0: the grid-cooperative panel only
-static int g_panel_cl = [] {
-    const char* e = std::getenv("BCS_DENSE_PANEL_CL");
-    return e ? std::atoi(e) : 1;
-}();
-
 void dense_factor_blocked(int m, double* a, int* piv, int* err, cudaStream_t s) {
     static bool attr = false;
     const int smem = 2 * kDB * 64 * static_cast<int>(sizeof(double));
@@ -517,24 +349,7 @@ void dense_factor_blocked(int m, double* a, int* piv, int* err, cudaStream_t s) 
         int per = (rows + g - 1) / g;
         g = (rows + per - 1) / per;
         const size_t psmem = sizeof(double) * static_cast<size_t>(per) * kDB;
-        const int pcl = (rows + kPanelCl - 1) / kPanelCl;
-        const size_t clsmem = sizeof(double) * static_cast<size_t>(pcl) * kDB;
-        if (g_panel_cl && rows >= 4 * kPanelCl && panel_cl_ok(clsmem)) {
-            cudaLaunchConfig_t cfg = {};
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = kPanelCl;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            cfg.gridDim = dim3(kPanelCl);
-            cfg.blockDim = dim3(512);
-            cfg.dynamicSmemBytes = clsmem;
-            cfg.stream = s;
-            cfg.attrs = at;
-            cfg.numAttrs = 1;
-            const cudaError_t e = cudaLaunchKernelEx(&cfg, k_dense_panel_cl, m, k0, nb, pcl, a, piv, err);
-            if (e != cudaSuccess) throw std::runtime_error(std::string("dense cluster panel: ") + cudaGetErrorString(e));
-        } else if (psmem <= 200 * 1024) {
+        if (psmem <= 200 * 1024) {
             static size_t attr_p = 0;
             if (psmem > attr_p) {
                 cudaFuncSetAttribute(k_dense_panel_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -662,91 +477,121 @@ __global__ void __launch_bounds__(1024) k_dense_solve_big(int m, const double* _
 }
 
 // Tolerance-level solve for large coarsest levels (the
-// scrambled inputs' aggregation stall leaves m in the thousands): the forward
-// substitution is k_dense_solve_big's (reference order, bit-exact); the
-// backward one runs by column tiles of 32 from the right -- warp 0 finishes a
-// tile's x (in-tile chain), then every thread folds the tile into the rows
-// above -- so the critical path is m/32 tiles, not the reference's m^2/2
-// dependent subtractions (whose order it does not keep: rounding differs).
-__global__ void __launch_bounds__(1024) k_dense_solve_tiled(int m, const double* __restrict__ lu,
-                                                            const int* __restrict__ perm, const double* r, double* z,
-                                                            int sx) {
-    extern __shared__ double sm[];
-    double* tile = sm;                     // 32 x 33
-    double* x = sx ? sm + 32 * 33 : z;
-    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
-    for (int i = tid; i < m; i += nt) x[i] = r[perm[i]];
-    __syncthreads();
-    for (int j0 = 0; j0 < m; j0 += 32) {  // forward (unit lower), reference order per row
-        const int j1 = j0 + 32 < m ? j0 + 32 : m;
-        for (int t = tid; t < 32 * 32; t += nt) {
-            const int i = j0 + t / 32, j = j0 + t % 32;
-            tile[(t / 32) * 33 + t % 32] = (i < j1 && j < i) ? lu[static_cast<size_t>(i) * m + j] : 0.0;
+// scrambled inputs' aggregation stall leaves m in the thousands): forward and
+// backward substitution by 64-column tiles over the whole GPU (cooperative
+// grid, one grid barrier per tile).  CTA 0 folds the current tile into the
+// next tile's rows and finishes that tile (in-tile triangular solve, one
+// warp), while every other warp folds the current tile into the remaining
+// rows (a warp per row, lanes over the tile's 64 columns: coalesced 512-byte
+// row segments, warp-tree sums) -- the reference's per-row subtraction order
+// is not kept (rounding differs; EXACT mode keeps k_dense_solve_big), the
+// critical path is m/64 tiles and the factor streams at HBM rate.
+constexpr int kTS = 64;
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+// x_i -= sum_{k in [j0, j1)} a_ik x_k  for one row i, by one warp
+__device__ __forceinline__ void fold_row(int m, const double* __restrict__ lu, double* x, int i, int j0, int j1,
+                                         const double* xt, int lane) {
+    const double* row = lu + static_cast<size_t>(i) * m;
+    double s = 0.0;
+    for (int k = j0 + lane; k < j1; k += 32) s = __dadd_rn(s, __dmul_rn(row[k], xt[k - j0]));
+    s = warp_sum(s);
+    if (lane == 0) x[i] = __dsub_rn(x[i], s);
+}
+__global__ void __launch_bounds__(256) k_dense_solve_coop(int m, const double* __restrict__ lu,
+                                                          const int* __restrict__ perm, const double* r, double* x) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double xt[kTS];             // the current tile's final x
+    __shared__ double tile[kTS][kTS + 1];  // CTA 0: the next tile's diagonal block
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int T = (m + kTS - 1) / kTS;
+    const int gw = static_cast<int>(blockIdx.x) * (blockDim.x >> 5) + wid;  // global warp
+    const int W = static_cast<int>(gridDim.x * (blockDim.x >> 5));
+    for (int i = static_cast<int>(blockIdx.x * blockDim.x) + tid; i < m; i += static_cast<int>(gridDim.x * blockDim.x))
+        x[i] = r[perm[i]];
+    grid.sync();
+    // finish tile t in CTA 0 (unit lower forward / upper backward with division)
+    auto finish = [&](int t, bool fwd) {
+        const int j0 = t * kTS, j1 = min(m, j0 + kTS), nb = j1 - j0;
+        for (int e = tid; e < kTS * kTS; e += blockDim.x) {
+            const int a = e / kTS, b = e % kTS;
+            tile[a][b] = (a < nb && b < nb) ? lu[static_cast<size_t>(j0 + a) * m + j0 + b] : 0.0;
         }
         __syncthreads();
         if (wid == 0) {
-            const int i = j0 + lane;
-            double xi = i < j1 ? x[i] : 0.0;
-            for (int j = j0; j < j1 - 1; ++j) {
-                const double xj = __shfl_sync(0xffffffffu, xi, j - j0);
-                if (i > j && i < j1) xi = __dsub_rn(xi, __dmul_rn(tile[lane * 33 + (j - j0)], xj));
+            double v0 = lane < nb ? x[j0 + lane] : 0.0, v1 = lane + 32 < nb ? x[j0 + 32 + lane] : 0.0;
+            if (fwd) {
+                for (int k = 0; k < nb - 1; ++k) {
+                    const double xk = __shfl_sync(0xffffffffu, k < 32 ? v0 : v1, k & 31);
+                    if (lane > k) v0 = __dsub_rn(v0, __dmul_rn(tile[lane][k], xk));
+                    if (lane + 32 > k) v1 = __dsub_rn(v1, __dmul_rn(tile[lane + 32][k], xk));
+                }
+            } else {
+                for (int k = nb - 1; k >= 0; --k) {
+                    if (k < 32 && lane == k) v0 = __ddiv_rn(v0, tile[k][k]);
+                    if (k >= 32 && lane + 32 == k) v1 = __ddiv_rn(v1, tile[k][k]);
+                    const double xk = __shfl_sync(0xffffffffu, k < 32 ? v0 : v1, k & 31);
+                    if (lane < k) v0 = __dsub_rn(v0, __dmul_rn(tile[lane][k], xk));
+                    if (lane + 32 < k) v1 = __dsub_rn(v1, __dmul_rn(tile[lane + 32][k], xk));
+                }
             }
-            if (i < j1) x[i] = xi;
+            if (lane < nb) x[j0 + lane] = v0;
+            if (lane + 32 < nb) x[j0 + 32 + lane] = v1;
         }
+    };
+    // forward (unit lower): tiles ascending
+    if (blockIdx.x == 0) finish(0, true);
+    grid.sync();
+    for (int t = 0; t + 1 < T; ++t) {
+        const int j0 = t * kTS, j1 = j0 + kTS;
+        for (int e = tid; e < kTS; e += blockDim.x) xt[e] = x[j0 + e];
         __syncthreads();
-        for (int i = j1 + tid; i < m; i += nt) {
-            double xi = x[i];
-            const double* row = lu + static_cast<size_t>(i) * m;
-#pragma unroll 8
-            for (int j = j0; j < j1; ++j) xi = __dsub_rn(xi, __dmul_rn(row[j], x[j]));
-            x[i] = xi;
+        const int n0 = j1, n1 = min(m, j1 + kTS);  // the next tile's rows: CTA 0
+        if (blockIdx.x == 0) {
+            for (int i = n0 + wid; i < n1; i += blockDim.x >> 5) fold_row(m, lu, x, i, j0, j1, xt, lane);
+            __syncthreads();
+            finish(t + 1, true);
+        } else {
+            for (int i = n1 + (gw - (blockDim.x >> 5)); i < m; i += W - (blockDim.x >> 5)) fold_row(m, lu, x, i, j0, j1, xt, lane);
         }
-        __syncthreads();
+        grid.sync();
     }
-    for (int j1 = m; j1 > 0; j1 -= 32) {  // backward (upper), tiles from the right
-        const int j0 = j1 - 32 > 0 ? j1 - 32 : 0;
-        for (int t = tid; t < 32 * 32; t += nt) {
-            const int i = j0 + t / 32, j = j0 + t % 32;
-            tile[(t / 32) * 33 + t % 32] = (i < j1 && j < j1 && j >= i) ? lu[static_cast<size_t>(i) * m + j] : 0.0;
-        }
+    // backward (upper, diagonal division): tiles descending
+    if (blockIdx.x == 0) finish(T - 1, false);
+    grid.sync();
+    for (int t = T - 1; t > 0; --t) {
+        const int j0 = t * kTS, j1 = min(m, j0 + kTS);
+        for (int e = tid; e < j1 - j0; e += blockDim.x) xt[e] = x[j0 + e];
         __syncthreads();
-        if (wid == 0) {
-            const int i = j0 + lane;
-            double xi = i < j1 ? x[i] : 0.0;
-            for (int j = j1 - 1; j >= j0; --j) {
-                if (i == j) xi = __ddiv_rn(xi, tile[lane * 33 + (j - j0)]);
-                const double xj = __shfl_sync(0xffffffffu, xi, j - j0);
-                if (i < j && i >= j0) xi = __dsub_rn(xi, __dmul_rn(tile[lane * 33 + (j - j0)], xj));
-            }
-            if (i < j1) x[i] = xi;
+        const int p1 = j0, p0 = j0 - kTS;  // the previous tile's rows [p0, p1): CTA 0
+        if (blockIdx.x == 0) {
+            for (int i = p0 + wid; i < p1; i += blockDim.x >> 5) fold_row(m, lu, x, i, j0, j1, xt, lane);
+            __syncthreads();
+            finish(t - 1, false);
+        } else {
+            for (int i = gw - (blockDim.x >> 5); i < p0; i += W - (blockDim.x >> 5)) fold_row(m, lu, x, i, j0, j1, xt, lane);
         }
-        __syncthreads();
-        for (int i = tid; i < j0; i += nt) {
-            double xi = x[i];
-            const double* row = lu + static_cast<size_t>(i) * m;
-#pragma unroll 8
-            for (int j = j0; j < j1; ++j) xi = __dsub_rn(xi, __dmul_rn(row[j], x[j]));
-            x[i] = xi;
-        }
-        __syncthreads();
+        grid.sync();
     }
-    if (sx)
-        for (int i = tid; i < m; i += nt) z[i] = x[i];
 }
 
 constexpr size_t kDenseSmemMax = 200 * 1024;
 
 void dense_solve_tiled(int m, const double* lu, const int* piv, const double* r, double* z, cudaStream_t s) {
-    const size_t full = (static_cast<size_t>(32) * 33 + static_cast<size_t>(m)) * sizeof(double);
-    const int sx = full <= kDenseSmemMax ? 1 : 0;
-    const size_t smem = sx ? full : static_cast<size_t>(32) * 33 * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_dense_solve_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kDenseSmemMax));
-        attr = true;
+    static int G = 0;
+    if (!G) {
+        int bps = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dense_solve_coop, 256, 0);
+        G = num_sms() * (bps < 1 ? 1 : bps);
     }
-    k_dense_solve_tiled<<<1, 1024, smem, s>>>(m, lu, piv + m, r, z, sx);
+    const int* perm = piv + m;
+    void* args[] = {(void*)&m, (void*)&lu, (void*)&perm, (void*)&r, (void*)&z};
+    const cudaError_t e = cudaLaunchCooperativeKernel((void*)k_dense_solve_coop, dim3(G), dim3(256), args, 0, s);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("dense solve launch failed: ") + cudaGetErrorString(e));
     count_launch();
 }
 
