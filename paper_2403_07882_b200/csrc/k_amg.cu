@@ -895,28 +895,47 @@ void dense_factor(int m, double* a, int* piv, int* err, cudaStream_t s) {
 }
 
 // denseSolve (smallmat.hpp:163-174), sequential reference order
+// denseSolve (smallmat.hpp:163-174) for small m: the factor and the vector
+// are staged in shared memory by the whole warp, then lane 0 runs the
+// reference's chains (swaps, forward, backward) on shared-memory operands
+// (a chain of global loads cost ~90 us at m = 35)
+constexpr int kDenseSmallMax = 72;  // m <= kDenseSmallMax: staged (m^2 doubles, <= 41 KB of shared memory)
 __global__ void k_dense_solve(int m, const double* lu, const int* piv, const double* r, double* z) {
+    __shared__ double sl[kDenseSmallMax * kDenseSmallMax];
+    __shared__ double sz[kDenseSmallMax];
+    const bool staged = m <= kDenseSmallMax;
+    if (staged) {
+        for (int e = threadIdx.x; e < m * m; e += blockDim.x) sl[e] = lu[e];
+        for (int e = threadIdx.x; e < m; e += blockDim.x) sz[e] = r[e];
+        __syncwarp();
+    }
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    for (int i = 0; i < m; ++i) z[i] = r[i];
+    const double* L = staged ? sl : lu;
+    double* x = staged ? sz : z;
+    if (!staged)
+        for (int i = 0; i < m; ++i) x[i] = r[i];
     for (int k = 0; k < m; ++k) {
         const int p = piv[k];
         if (p != k) {
-            const double t = z[k];
-            z[k] = z[p];
-            z[p] = t;
+            const double t = x[k];
+            x[k] = x[p];
+            x[p] = t;
         }
     }
     for (int i = 1; i < m; ++i) {
-        double x = z[i];
-        for (int j = 0; j < i; ++j) x = __dsub_rn(x, __dmul_rn(lu[static_cast<size_t>(i) * m + j], z[j]));
-        z[i] = x;
+        double v = x[i];
+        for (int j = 0; j < i; ++j) v = __dsub_rn(v, __dmul_rn(L[static_cast<size_t>(i) * m + j], x[j]));
+        x[i] = v;
     }
     for (int i = m - 1; i >= 0; --i) {
-        double x = z[i];
-        for (int j = i + 1; j < m; ++j) x = __dsub_rn(x, __dmul_rn(lu[static_cast<size_t>(i) * m + j], z[j]));
-        z[i] = __ddiv_rn(x, lu[static_cast<size_t>(i) * m + i]);
+        double v = x[i];
+        for (int j = i + 1; j < m; ++j) v = __dsub_rn(v, __dmul_rn(L[static_cast<size_t>(i) * m + j], x[j]));
+        x[i] = __ddiv_rn(v, L[static_cast<size_t>(i) * m + i]);
     }
+    if (staged)
+        for (int i = 0; i < m; ++i) z[i] = x[i];
 }
+
 void dense_solve(int m, const double* lu, const int* piv, const double* r, double* z, cudaStream_t s) {
     k_dense_solve<<<1, 32, 0, s>>>(m, lu, piv, r, z);
     count_launch();
