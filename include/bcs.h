@@ -90,7 +90,11 @@ typedef struct {
  *   folded by the pairwise tree of partition.cpp:433-450): residual
  *   histories and solutions are bit-identical to the reference.  A dot is
  *   then a serial chain of N dependent adds (~4.3 ns each): a proof mode. */
-enum { BCS_MODE_PARITY = 0, BCS_MODE_PERF = 1, BCS_MODE_EXACT = 2 };
+enum { BCS_MODE_PARITY = 0, BCS_MODE_PERF = 1, BCS_MODE_EXACT = 2,
+       /* PERF with block-Jacobi smoothing (z += 0.9 D^-1 r per block row, AmgX's
+        * relaxation-factor default) on every level above the one-CTA tail:
+        * dependency-free, HBM-streaming, weaker than DILU (more iterations). */
+       BCS_MODE_PERF_JACOBI = 3 };
 
 /* SolveReport (krylov.hpp:39-50) + per-stage timings (seconds) with the
  * reference keys (engine.cpp:80-112) and device sub-stages. */

@@ -57,6 +57,7 @@ class Mode(enum.IntEnum):
     PARITY = 0
     PERF = 1
     EXACT = 2
+    PERF_JACOBI = 3
 
 
 @dataclass

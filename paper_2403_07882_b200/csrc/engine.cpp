@@ -178,6 +178,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* m = std::getenv("BCS_TAIL_ROWS")) tailMaxRows_ = std::atoi(m);
     if (const char* m = std::getenv("BCS_DENSE_TILED_MIN")) denseTiledMin_ = std::atoi(m);
     if (const char* m = std::getenv("BCS_MC_SWEEP")) mcSweep_ = std::atoi(m) != 0;
+    if (const char* m = std::getenv("BCS_JACOBI_OMEGA")) jacobiOmega_ = std::atof(m);
     check(cudaSetDevice(device), "cudaSetDevice");
     check(cudaStreamCreateWithFlags(&own_, cudaStreamNonBlocking), "cudaStreamCreate");
     stream_ = own_;
@@ -706,7 +707,8 @@ void Engine::validateConfig(const bcs_solver_config& c) const {
     if (c.amg_pre_sweeps < 0 || c.amg_post_sweeps < 0) throw std::invalid_argument("SolverConfig: amg sweeps must be >= 0");
     if (c.method != BCS_GMRES && c.method != BCS_BICGSTAB && c.method != BCS_FGMRES) throw std::invalid_argument("unknown Krylov method");
     if (c.precond < 0 || c.precond > 3) throw std::invalid_argument("unknown preconditioner kind");
-    if (c.mode != BCS_MODE_PARITY && c.mode != BCS_MODE_PERF && c.mode != BCS_MODE_EXACT)
+    if (c.mode != BCS_MODE_PARITY && c.mode != BCS_MODE_PERF && c.mode != BCS_MODE_EXACT &&
+        c.mode != BCS_MODE_PERF_JACOBI)
         throw std::invalid_argument("bcs: unknown mode");
 }
 
@@ -886,6 +888,24 @@ void Engine::finishSmoothers(const std::vector<Level*>& lv, const bcs_solver_con
     profMark("dilu:pack");
 }
 
+// performance mode, block Jacobi: the diagonal blocks' LU (luFactor order,
+// smallmat.hpp:67-94), reciprocals and composed permutations
+void Engine::jacobiSetup(Level& L) {
+    const size_t nn = static_cast<size_t>(n_) * n_;
+    L.lu.ensure(L.rows * nn, stream_);
+    L.piv.ensure(static_cast<size_t>(L.rows) * n_, stream_);
+    L.rcp.ensure(static_cast<size_t>(L.rows) * n_, stream_);
+    L.perm.ensure(static_cast<size_t>(L.rows) * n_, stream_);
+    const int big = std::numeric_limits<int>::max();
+    check(cudaMemcpyAsync(err_.p, &big, sizeof(int), cudaMemcpyHostToDevice, stream_), "err init");
+    factor_diag_blocks(n_, L.rows, L.dg, L.v, L.lu.p, L.piv.p, err_.p, stream_);
+    make_reciprocals(n_, L.rows, L.lu, L.piv, L.rcp.p, L.perm.p, stream_);
+    const int cell = readErrCell();
+    if (cell != big)
+        throw std::runtime_error("preconditioner setup: singular diagonal block in cell " + std::to_string(cell));
+    L.jacobi = true;
+}
+
 void Engine::lusgsSetup(Level& L) {
     const size_t nn = static_cast<size_t>(n_) * n_;
     L.lu.ensure(L.rows * nn, stream_);
@@ -991,8 +1011,20 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
     }
     H_->levels[H_->nlev - 1].ncoarse = 0;
 
-    // DILU smoother on all but the coarsest level (amg.cpp:86-88)
-    diluSetupAll(smoothedLevels(cfg), &cfg);
+    // DILU smoother on all but the coarsest level (amg.cpp:86-88); the block-Jacobi
+    // performance mode smooths the levels above the one-CTA tail with omega D^-1
+    if (cfg.mode == BCS_MODE_PERF_JACOBI) {
+        const int t = tailStart();
+        std::vector<Level*> tail;
+        for (int l = 0; l + 1 < H_->nlev; ++l) {
+            if (l < t) jacobiSetup(H_->levels[l]);
+            else tail.push_back(&H_->levels[l]);
+        }
+        if (!tail.empty()) diluSetupAll(tail, &cfg);
+        profMark("perf:jacobi");
+    } else {
+        diluSetupAll(smoothedLevels(cfg), &cfg);
+    }
     // dense factorisation of the coarsest level (amg.cpp:90-104)
     const Level& Cl = H_->levels[H_->nlev - 1];
     H_->m = Cl.rows * n_;
@@ -1145,7 +1177,7 @@ void Engine::buildPrecond(const bcs_solver_config& cfg) {
 
 void Engine::buildPrecondOn(const FineMatrix& F, const bcs_solver_config& cfg) {
     H_->pcKind = -1;
-    for (auto& L : H_->levels) L.mcValid = false;
+    for (auto& L : H_->levels) L.mcValid = L.jacobi = false;
 
     if (H_->levels.empty()) H_->levels.emplace_back();
     H_->nlev = 1;
@@ -1178,6 +1210,14 @@ void Engine::buildPrecondOn(const FineMatrix& F, const bcs_solver_config& cfg) {
 
 // DILU/LUSGS sweep pair: z = (D+U)^{-1} D (D+L)^{-1} r  (accumulate: see sweep_backward)
 void Engine::smootherApply(Level& L, const double* r, double* z, int accumulate) {
+    if (L.jacobi && H_->pcCfg.mode == BCS_MODE_PERF_JACOBI) {
+        const double nb = static_cast<double>(n_), R = static_cast<double>(L.rows);
+        const double per = R * (8.0 * nb * nb + 8.0 * nb + 4.0 * nb + 16.0 * nb) + (accumulate == 2 ? R * 8.0 * nb : 0.0);
+        if (kernelTiming_) timerBegin();
+        block_jacobi(n_, L.rows, L.lu, L.rcp, L.perm, r, z, accumulate, jacobiOmega_, stream_);
+        if (kernelTiming_) timerEnd(1, per);
+        return;
+    }
     if (L.mcValid && H_->pcCfg.mode == BCS_MODE_PERF) {
         // performance mode: the multicolour DILU on the colour-permuted copy;
         // r in, result scattered back (and accumulated) in the level's numbering

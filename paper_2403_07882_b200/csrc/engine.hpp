@@ -119,6 +119,7 @@ struct Level {
     DArray<int> mcPerm;  // new (colour-ordered) row -> row
     DArray<int> mcColorOffD;  // device copy of mcColorOff
     bool colourSweep = false; // this is a coloured copy: colour-synchronous sweeps, no sweep programs
+    bool jacobi = false;      // performance mode, block Jacobi: smoothed by omega * D^-1 (no DILU)
     int ncolors = 0;
     std::vector<int> mcColorOff;  // colour c = new rows [off[c], off[c+1])
     bool mcValid = false;  // mc built for the current values
@@ -250,6 +251,7 @@ private:
     // copies in performance mode above the one-CTA tail
     std::vector<Level*> smoothedLevels(const bcs_solver_config& cfg);
     int tailStart() const;
+    void jacobiSetup(Level& L);
     void lusgsSetup(Level& L);
 
     void applyPrecond(const double* r, double* z);
@@ -377,6 +379,7 @@ private:
     int tailMaxRows_ = kTailMaxRows;          // levels at most this big run in the one-CTA tail (0: off)
     int denseTiledMin_ = 2048;                // coarsest m from which the backward solve is tiled (non-EXACT)
     bool mcSweep_ = false;                    // perf mode: colour-synchronous sweeps (BCS_MC_SWEEP=1; measured slower)
+    double jacobiOmega_ = 0.9;                // block-Jacobi damping (AmgX's relaxation_factor default); BCS_JACOBI_OMEGA
     void denseSolve(const double* r, double* z);
     int* hTot_ = nullptr;                     // pinned: per-level sweep program sizes
     void setupTail();

@@ -350,6 +350,73 @@ __global__ void __launch_bounds__(256) k_mc_sweep(int ncol, const int* __restric
     }
 }
 
+// ---- performance mode, block-Jacobi smoothing ------------------------------
+// out_i = omega * D_i^-1 r_i per block row (the diagonal block's LU with the
+// composed pivot permutation and reciprocal-based division, as the sweeps),
+// z = out | 0 + out | z + out by `acc` (the V-cycle's pre/post-smoothing
+// forms).  No dependencies: one pass over the factors, HBM-bound.  The rows'
+// factors are staged through shared memory with coalesced loads.
+constexpr int kJacRows = 128;
+template <int N>
+__global__ void __launch_bounds__(kJacRows) k_block_jacobi(int rows, const double* __restrict__ lu,
+                                                          const double* __restrict__ rcp, const int* __restrict__ perm,
+                                                          const double* __restrict__ r, double* z, int acc,
+                                                          double omega) {
+    constexpr int NN = N * N;
+    __shared__ double sl[kJacRows * NN];
+    const int r0 = blockIdx.x * kJacRows;
+    const int nrow = rows - r0 < kJacRows ? rows - r0 : kJacRows;
+    const double* src = lu + static_cast<size_t>(r0) * NN;
+    for (int e = threadIdx.x; e < nrow * NN; e += blockDim.x) sl[e] = __ldcs(&src[e]);
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t >= nrow) return;
+    const size_t i = static_cast<size_t>(r0 + t);
+    double rv[N], x[N], rc[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+        rv[q] = __ldcs(&r[i * N + q]);
+        rc[q] = __ldcs(&rcp[i * N + q]);
+    }
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+        const int sp = __ldcs(&perm[i * N + p]);
+        double v = rv[0];
+#pragma unroll
+        for (int q = 1; q < N; ++q) v = (sp == q) ? rv[q] : v;
+        x[p] = v;
+    }
+    DVec<N> xin;
+#pragma unroll
+    for (int p = 0; p < N; ++p) xin.v[p] = x[p];
+    const double* L = sl + t * NN;
+    if (__builtin_expect(!lu_solve_perm_fast<N>(L, rc, x), 0)) {
+        const DVec<N> xe = lu_solve_perm_exact<N>(L, xin);
+#pragma unroll
+        for (int p = 0; p < N; ++p) x[p] = xe.v[p];
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+        const double o = __dmul_rn(omega, x[q]);
+        double* zq = z + i * N + q;
+        *zq = acc == 2 ? __dadd_rn(*zq, o) : acc == 1 ? __dadd_rn(0.0, o) : o;
+    }
+}
+
+void block_jacobi(int n, int rows, const double* lu, const double* rcp, const int* perm, const double* r, double* z,
+                  int acc, double omega, cudaStream_t s) {
+    if (rows <= 0) return;
+    const unsigned g = static_cast<unsigned>((rows + kJacRows - 1) / kJacRows);
+    switch (n) {
+        case 1: k_block_jacobi<1><<<g, kJacRows, 0, s>>>(rows, lu, rcp, perm, r, z, acc, omega); break;
+        case 2: k_block_jacobi<2><<<g, kJacRows, 0, s>>>(rows, lu, rcp, perm, r, z, acc, omega); break;
+        case 3: k_block_jacobi<3><<<g, kJacRows, 0, s>>>(rows, lu, rcp, perm, r, z, acc, omega); break;
+        case 4: k_block_jacobi<4><<<g, kJacRows, 0, s>>>(rows, lu, rcp, perm, r, z, acc, omega); break;
+        default: k_block_jacobi<5><<<g, kJacRows, 0, s>>>(rows, lu, rcp, perm, r, z, acc, omega); break;
+    }
+    count_launch();
+}
+
 template <int N, bool FWD>
 static void launch_mc_sweep(int rows, int ncol, const int* coff, const int* ro, const int* dg, const int* ci,
                             const double* v, const double* lu, const double* rcp, const int* perm, const double* rin,

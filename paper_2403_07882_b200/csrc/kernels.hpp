@@ -50,6 +50,9 @@ void mc_permute_pattern(int rows, const int* ro, const int* ci, const int* perm,
 void mc_permute_values(int n, size_t nnz, const int* sv, const double* v, double* nv, cudaStream_t s);
 void mc_vec_gather(int n, int rows, const int* perm, const double* x, double* xp, cudaStream_t s);
 void mc_vec_scatter(int n, int rows, const int* perm, const double* sp, double* z, int acc, cudaStream_t s);
+// performance mode, block-Jacobi smoothing: z (=|+=) omega * D^-1 r per block row
+void block_jacobi(int n, int rows, const double* lu, const double* rcp, const int* perm, const double* r, double* z,
+                  int acc, double omega, cudaStream_t s);
 // colour-synchronous DILU sweep of a coloured level (coff: device, ncol + 1 colour boundaries)
 void mc_sweep(int n, bool fwd, int rows, int ncol, const int* coff, const int* ro, const int* dg, const int* ci,
               const double* v, const double* lu, const double* rcp, const int* perm, const double* rin, double* out,

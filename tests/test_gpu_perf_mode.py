@@ -115,3 +115,22 @@ def test_perf_amg_solve(ctx, maker, method):
     # reported, not claimed equal: the colour-ordered smoother costs some iterations
     assert rp.iterations <= 3 * r.iterations + 2, (rp.iterations, r.iterations)
     np.testing.assert_allclose(xp, x, rtol=0, atol=1e-6 * np.abs(x).max())
+
+
+@pytest.mark.parametrize("maker", [lambda: gen.hex_euler(24), lambda: gen.hex_coupled(16, poly_seed=1),
+                                   lambda: gen.hex_euler(16, 16, 12, aspect=100.0, scramble_seed=4)])
+def test_perf_block_jacobi_amg_solve(ctx, maker):
+    """Mode.PERF_JACOBI: block-Jacobi smoothing (0.9 D^-1 per block row) on the
+    levels above the one-CTA tail: converges to the requested tolerance (true
+    residual), iterations reported next to the parity mode's."""
+    s = maker()
+    A = s.A
+    ctx.set_topology(A)
+    ctx.upload_ldu(A)
+    base = dict(preconditioner=bcs.PrecondKind.AMG, relTol=1e-8, maxIters=1000, amg=AMG)
+    xj = s.x0.values.copy()
+    rj = ctx.solve(s.b.values, xj, bcs.SolverConfig(mode=bcs.Mode.PERF_JACOBI, **base))
+    assert rj.converged
+    assert ctx.residual(s.b.values, xj) <= 1e-8 * rj.initialResidual * 1.0000001
+    r = ctx.solve(s.b.values, s.x0.values.copy(), bcs.SolverConfig(**base))
+    assert rj.iterations <= 6 * r.iterations + 5, (rj.iterations, r.iterations)
