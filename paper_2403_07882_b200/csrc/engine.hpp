@@ -379,7 +379,7 @@ private:
     int tailMaxRows_ = kTailMaxRows;          // levels at most this big run in the one-CTA tail (0: off)
     int denseTiledMin_ = 2048;                // coarsest m from which the backward solve is tiled (non-EXACT)
     bool mcSweep_ = false;                    // perf mode: colour-synchronous sweeps (BCS_MC_SWEEP=1; measured slower)
-    double jacobiOmega_ = 0.9;                // block-Jacobi damping (AmgX's relaxation_factor default); BCS_JACOBI_OMEGA
+XX
     void denseSolve(const double* r, double* z);
     int* hTot_ = nullptr;                     // pinned: per-level sweep program sizes
     void setupTail();
