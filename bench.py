@@ -569,7 +569,7 @@ def workload_name(args):
         extra.append(f"randomly permuted cell order (seed {args.scramble})")
     if args.mode != "parity":
         extra.append({"perf": "PERFORMANCE MODE (multicolour DILU smoothing; iterations differ from the reference)",
-                      "jacobi": "PERFORMANCE MODE (block-Jacobi smoothing, omega 0.9; iterations differ from the reference)",
+                      "jacobi": "PERFORMANCE MODE (block-Jacobi smoothing, omega 0.8; iterations differ from the reference)",
                       "exact": "EXACT mode (the reference's sequential dot order)"}[args.mode])
     if not extra and args.system == "euler" and args.size == 128:
         return base + " (BASELINE configs[1])"

@@ -120,7 +120,7 @@ def test_perf_amg_solve(ctx, maker, method):
 @pytest.mark.parametrize("maker", [lambda: gen.hex_euler(24), lambda: gen.hex_coupled(16, poly_seed=1),
                                    lambda: gen.hex_euler(16, 16, 12, aspect=100.0, scramble_seed=4)])
 def test_perf_block_jacobi_amg_solve(ctx, maker):
-    """Mode.PERF_JACOBI: block-Jacobi smoothing (0.9 D^-1 per block row) on the
+    """Mode.PERF_JACOBI: block-Jacobi smoothing (0.8 D^-1 per block row) on the
     levels above the one-CTA tail: converges to the requested tolerance (true
     residual), iterations reported next to the parity mode's."""
     s = maker()
