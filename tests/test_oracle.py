@@ -153,3 +153,51 @@ def test_restatement_decompose_live(oracle, ref, ranks):
     b = ref.decompose(s.centroids, ranks)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def _glibc_hypot(x, y):
+    """The reference libm's hypot (glibc >= 2.35 sysdeps/ieee754/dbl-64/e_hypot.c,
+    non-FMA kernel), restated in Python double arithmetic -- the algorithm the
+    device Givens rotation runs (k_krylov.cu glibc_hypot)."""
+    import math
+    if not math.isfinite(x) or not math.isfinite(y):
+        return math.inf if (math.isinf(x) or math.isinf(y)) else x + y
+    x, y = abs(x), abs(y)
+    ax, ay = max(x, y), min(x, y)
+
+    def kernel(ax, ay):
+        h = math.sqrt(ax * ax + ay * ay)
+        if h <= 2.0 * ay:
+            delta = h - ay
+            t1 = ax * (2.0 * delta - ax)
+            t2 = (delta - 2.0 * (ax - ay)) * delta
+        else:
+            delta = h - ax
+            t1 = 2.0 * delta * (ax - 2.0 * ay)
+            t2 = (4.0 * delta - ay) * ay + delta * delta
+        return h - (t1 + t2) / (2.0 * h)
+
+    scale, large, tiny, eps = 2.0 ** -600, 2.0 ** 511, 2.0 ** -459, 2.0 ** -54
+    if ax > large:
+        return ax + ay if ay <= ax * eps else kernel(ax * scale, ay * scale) / scale
+    if ay < tiny:
+        return ax + ay if ax >= ay / eps else kernel(ax / scale, ay / scale) * scale
+    return ax + ay if ay <= ax * eps else kernel(ax, ay)
+
+
+def test_glibc_hypot_restatement_matches_libm():
+    """The restated hypot equals this host's libm bit for bit (the reference
+    links the same libm); the device copy is pinned on the GPU
+    (test_device_hypot_is_the_reference_libm_hypot)."""
+    import ctypes
+    import random
+    libm = ctypes.CDLL("libm.so.6")
+    libm.hypot.restype = ctypes.c_double
+    libm.hypot.argtypes = [ctypes.c_double, ctypes.c_double]
+    rnd = random.Random(11)
+    for _ in range(50000):
+        e1 = rnd.randint(-1070, 1020)
+        e2 = max(-1070, min(1020, e1 + rnd.randint(-70, 70))) if rnd.random() < 0.7 else rnd.randint(-1070, 1020)
+        x = rnd.uniform(-1, 1) * 2.0 ** e1
+        y = 0.0 if rnd.random() < 0.03 else rnd.uniform(-1, 1) * 2.0 ** e2
+        assert _glibc_hypot(x, y) == libm.hypot(x, y), (x.hex(), y.hex())
