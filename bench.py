@@ -273,6 +273,10 @@ def run_reference(args):
     sample = (f"the full {workload_name(args)} system: reference SolvePipeline::solve (EngineCsr, GMRES+AMG to 1e-8, "
               f"{rep.iterations} its), 1 setup-branch call ({t_setup:.1f} s, untimed warm-up) then {len(timed)} "
               f"replace-branch call(s) timed (budget {args.ref_budget:.0f} s of the requested {args.steps})")
+    if world > 1:
+        sample += (f"; N = {world}: our line solves {world} x this system (Mode R, weak scaling), whose serial "
+                   f"reference solve would take ~{world} x as long on one core (not timed: the run would exceed the "
+                   f"driver's few-minute budget), so this is the per-GPU share")
     emit({
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": len(timed), "warmup": 1,
         "requested": {"steps": args.steps, "warmup": args.warmup},
