@@ -179,7 +179,6 @@ Engine::Engine(int device) : device_(device) {
     if (const char* m = std::getenv("BCS_DENSE_TILED_MIN")) denseTiledMin_ = std::atoi(m);
     if (const char* m = std::getenv("BCS_MC_SWEEP")) mcSweep_ = std::atoi(m) != 0;
     if (const char* m = std::getenv("BCS_JACOBI_OMEGA")) jacobiOmega_ = std::atof(m);
-    if (const char* m = std::getenv("BCS_DILU_OVERLAP")) overlapDilu_ = std::atoi(m) != 0;
     check(cudaSetDevice(device), "cudaSetDevice");
     check(cudaStreamCreateWithFlags(&own_, cudaStreamNonBlocking), "cudaStreamCreate");
     stream_ = own_;
@@ -227,7 +226,6 @@ Engine::~Engine() {
     rel(str_); rel(keys_); rel(sorted_); rel(V_); rel(w_); rel(zk_); rel(rk_); rel(Hm_); rel(cs_); rel(sn_); rel(g_);
     rel(y_); rel(scal_); rel(partials_); rel(kb_); rel(kx_); rel(bp_); rel(bv_); rel(bs_); rel(bt_); rel(bph_);
     rel(bsh_); rel(brh_); rel(ticket_); rel(seg_); rel(distTmp_); rel(mcSv_);
-    rel(sCnt_); rel(sScan_); rel(sSmall_); rel(sDepth_); rel(sErr_); rel(sDesc_);
     for (auto& P : dist_) {
         rel(P.ro); rel(P.ci); rel(P.src); rel(P.dg); rel(P.tpos); rel(P.vals); rel(P.hrow); rel(P.hoff);
         rel(P.hcol); rel(P.hsrc); rel(P.hvals);
@@ -249,13 +247,6 @@ Engine::~Engine() {
     for (cudaEvent_t e : stageEv_) cudaEventDestroy(e);
     if (hStatus_) cudaFreeHost(hStatus_);
     if (hTot_) cudaFreeHost(hTot_);
-    if (sDescHost_) cudaFreeHost(sDescHost_);
-    if (evMainReady_) cudaEventDestroy(evMainReady_);
-    if (evSideDone_) cudaEventDestroy(evSideDone_);
-    if (side_) {
-        cudaStreamSynchronize(side_);
-        cudaStreamDestroy(side_);
-    }
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
     for (auto& e : evPool_) {
@@ -739,9 +730,8 @@ static KahnWork kahnWork(DArray<int>& cnt, DArray<int>& push, DArray<int>& lvl, 
 // DILU smoothers of the levels lv (preconditioner.cpp:101-126): dependency
 // levels per matrix, then ONE sync-free factorisation over all of them
 // (tickets ordered by dependency level, then matrix), then the sweeps' data.
-void Engine::diluFactor(const std::vector<Level*>& lv) {
+void Engine::diluSetupAll(const std::vector<Level*>& lv, const bcs_solver_config* cfg) {
     const int nl = static_cast<int>(lv.size());
-    if (nl == 0) return;
     const size_t nn = static_cast<size_t>(n_) * n_;
     const int big = std::numeric_limits<int>::max();
     if (diluMode_ != 0) {  // Kahn-rounds variant (BCS_DILU_MODE=1), level by level
@@ -760,6 +750,7 @@ void Engine::diluFactor(const std::vector<Level*>& lv) {
             if (cell != big)
                 throw std::runtime_error("DILU setup: singular modified diagonal in cell " + std::to_string(cell));
         }
+        finishSmoothers(lv, nullptr);
         return;
     }
     size_t totalRows = 0, totalT = 0, maxRows = 0;
@@ -834,110 +825,6 @@ void Engine::diluFactor(const std::vector<Level*>& lv) {
     if (cell != big)
         throw std::runtime_error("DILU setup: singular modified diagonal in cell " + std::to_string(cell & ((1 << 26) - 1)));
     profMark("dilu:factor");
-}
-
-// ---- overlapped hierarchy setup --------------------------------------------
-// The DILU smoother of a level (dependency levels + factorisation, the
-// latency-bound half of the setup) depends only on that level's matrix, so it
-// runs on a side stream, on at most half of the SMs, while the main stream
-// coarsens further (strengths, aggregation, Galerkin: the other, host-sync
-// bound half).  Same kernels, same per-element arithmetic: the factors are
-// bit-identical to the one-pass setup (diluSetupAll).  T, tc and lpre of the
-// side levels come from the setup phase of the hierarchy's arena, reserved
-// up front at 4x the fine level's need (the coarse levels' sum is ~1.7x);
-// a level that does not fit is factored after the join instead.
-void Engine::sideBegin(const bcs_solver_config& cfg) {
-    (void)cfg;
-    if (!side_) {
-        check(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "cudaStreamCreate side");
-        check(cudaEventCreateWithFlags(&evMainReady_, cudaEventDisableTiming), "cudaEventCreate");
-        check(cudaEventCreateWithFlags(&evSideDone_, cudaEventDisableTiming), "cudaEventCreate");
-        check(cudaMallocHost(reinterpret_cast<void**>(&sDescHost_), 64 * side_desc_bytes()), "cudaMallocHost");
-        sSmall_.ensure(16, stream_);
-        sDepth_.ensure(64, stream_);
-        sErr_.ensure(3 * 64, stream_);
-        sDesc_.ensure(side_desc_bytes(), stream_);
-        int bps = 0;
-        sideGridCap_ = std::max(1, num_sms() / 2);  // one CTA per SM on half of the GPU
-        (void)bps;
-    }
-    sideLevels_.clear();
-    lateLevels_.clear();
-    const Level& L0 = H_->levels[0];
-    const size_t nn = static_cast<size_t>(n_) * n_;
-    const size_t t0 = (static_cast<size_t>(L0.nnz) - L0.rows) / 2 * nn;
-    const size_t i0 = static_cast<size_t>(L0.nnz) + L0.rows + 1;
-    H_->arena.reserve(4 * (PhaseArena::al(sizeof(double) * (t0 + 1)) + 2 * PhaseArena::al(sizeof(int) * i0)), stream_);
-    // error cells: INT_MAX = no singular row; wait-timeout flags 0
-    std::vector<int> init(3 * 64, 0);
-    for (int l = 0; l < 64; ++l) init[2 * l] = std::numeric_limits<int>::max();
-    check(cudaMemcpyAsync(sErr_.p, init.data(), sizeof(int) * init.size(), cudaMemcpyHostToDevice, stream_), "err init");
-    sync();  // init dies here; the side stream waits on the main stream's events anyway
-}
-
-void Engine::sideDilu(int l) {
-    if (l >= 64) {
-        lateLevels_.push_back(l);
-        return;
-    }
-    Level& L = H_->levels[l];
-    const size_t nn = static_cast<size_t>(n_) * n_;
-    const size_t lower = (static_cast<size_t>(L.nnz) - L.rows) / 2;  // structurally symmetric (checked)
-    const size_t need = PhaseArena::al(sizeof(int) * (static_cast<size_t>(L.rows) + 1)) +
-                        PhaseArena::al(sizeof(int) * static_cast<size_t>(L.nnz)) +
-                        PhaseArena::al(sizeof(double) * (lower * nn + 1));
-    if (H_->arena.off + need > H_->arena.cap) {
-        lateLevels_.push_back(l);
-        return;
-    }
-    L.lpre.borrow(H_->arena.take<int>(static_cast<size_t>(L.rows) + 1), static_cast<size_t>(L.rows) + 1, stream_);
-    L.tc.borrow(H_->arena.take<int>(L.nnz), L.nnz, stream_);
-    double* T = H_->arena.take<double>(lower * nn + 1);
-    L.lu.ensure(L.rows * nn, stream_);
-    L.piv.ensure(static_cast<size_t>(L.rows) * n_, stream_);
-    L.order.ensure(L.rows, stream_);
-    L.dlev.ensure(L.rows, stream_);
-    // side scratch, sized for the largest level (level 0 comes first)
-    sCnt_.ensure(static_cast<size_t>(L.rows) + 2, stream_);
-    sScan_.ensure(scan_tmp_ints(static_cast<size_t>(L.rows) + 2) + 16, stream_);
-    // the level's matrix and these buffers are ready in main-stream order
-    check(cudaEventRecord(evMainReady_, stream_), "record");
-    check(cudaStreamWaitEvent(side_, evMainReady_, 0), "wait");
-    void* dh = sDescHost_ + static_cast<size_t>(l) * side_desc_bytes();
-    level_schedule_async(L.rows, L.ro, L.ci, L.dg, L.dlev.p, L.order.p, sDepth_.p + l, sCnt_.p, sScan_.p, sSmall_.p,
-                         sDesc_.p, dh, sErr_.p + 128 + l, sideGridCap_, side_);
-    dilu_compact_index_async(L.rows, L.ro, L.dg, L.ci, L.tpos, L.lpre.p, L.tc.p, sSmall_.p + 8, sScan_.p, side_);
-    const DiluLevelHost h{L.rows, L.ro, L.dg, L.tpos, L.tc.p, L.lpre.p, L.dlev.p, L.v, L.lu.p, L.piv.p, 0};
-    dilu_setup_level(n_, h, L.order, sDesc_.p, dh, T, lower * nn + 1, sErr_.p + 2 * l, sErr_.p + 2 * l + 1,
-                     sideGridCap_, side_);
-    sideLevels_.push_back(l);
-}
-
-void Engine::sideJoin(const bcs_solver_config& cfg) {
-    check(cudaEventRecord(evSideDone_, side_), "record");
-    check(cudaStreamWaitEvent(stream_, evSideDone_, 0), "wait");
-    std::vector<int> err(3 * 64), depth(64);
-    check(cudaMemcpyAsync(err.data(), sErr_.p, sizeof(int) * err.size(), cudaMemcpyDeviceToHost, stream_), "D2H err");
-    check(cudaMemcpyAsync(depth.data(), sDepth_.p, sizeof(int) * depth.size(), cudaMemcpyDeviceToHost, stream_),
-          "D2H depth");
-    sync();
-    profMark("dilu:side");
-    for (int l : sideLevels_) {  // levels ascending: the first singular level reports, as the one-pass setup
-        if (err[2 * l + 1] || err[128 + l]) throw std::runtime_error("bcs: DILU setup dependency wait timed out");
-        if (err[2 * l] != std::numeric_limits<int>::max())
-            throw std::runtime_error("DILU setup: singular modified diagonal in cell " +
-                                     std::to_string(err[2 * l] & ((1 << 26) - 1)));
-        H_->levels[l].depth = depth[l];
-    }
-    std::vector<Level*> late, all;
-    for (int l : lateLevels_) late.push_back(&H_->levels[l]);
-    diluFactor(late);  // levels the setup arena could not hold
-    for (int l = 0; l + 1 < H_->nlev; ++l) all.push_back(&H_->levels[l]);
-    finishSmoothers(all, &cfg);
-}
-
-void Engine::diluSetupAll(const std::vector<Level*>& lv, const bcs_solver_config* cfg) {
-    diluFactor(lv);
     finishSmoothers(lv, cfg);
 }
 
@@ -1045,15 +932,6 @@ void Engine::lusgsSetup(Level& L) {
 void Engine::buildHierarchy(const bcs_solver_config& cfg) {
     const size_t nn = static_cast<size_t>(n_) * n_;
     H_->nlev = 1;
-    const bool overlap = overlapDilu_ && diluMode_ == 0 && (cfg.mode == BCS_MODE_PARITY || cfg.mode == BCS_MODE_EXACT);
-    if (overlap) sideBegin(cfg);
-    struct SideGuard {  // a throw in the coarsening must not leave side-stream work behind
-        cudaStream_t s;
-        bool armed;
-        ~SideGuard() {
-            if (armed && s) cudaStreamSynchronize(s);
-        }
-    } sideGuard{side_, overlap};
     // coarsening loop (amg.cpp:75-84)
     while (H_->nlev < cfg.amg_max_levels && H_->levels[H_->nlev - 1].rows > cfg.amg_min_coarse_rows) {
         const int l = H_->nlev - 1;
@@ -1087,7 +965,6 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
             profMark("setup:aggregate_number");
             if (nC == L.rows) break;  // no coarsening possible (amg.cpp:80)
             L.ncoarse = nC;
-            if (overlap) sideDilu(l);  // level l is smoothed: its DILU starts now, beside the coarsening
         }
         if (static_cast<int>(H_->levels.size()) < H_->nlev + 1) H_->levels.emplace_back();
         ++H_->nlev;
@@ -1136,9 +1013,7 @@ void Engine::buildHierarchy(const bcs_solver_config& cfg) {
 
     // DILU smoother on all but the coarsest level (amg.cpp:86-88); the block-Jacobi
     // performance mode smooths the levels above the one-CTA tail with omega D^-1
-    if (overlap) {
-        sideJoin(cfg);
-    } else if (cfg.mode == BCS_MODE_PERF_JACOBI) {
+    if (cfg.mode == BCS_MODE_PERF_JACOBI) {
         const int t = tailStart();
         std::vector<Level*> tail;
         for (int l = 0; l + 1 < H_->nlev; ++l) {

@@ -382,21 +382,6 @@ private:
     double jacobiOmega_ = 0.8;                // block-Jacobi damping (of 0.8 / 0.9 / 1.0: 18 / 22 / 94 its at 128^3); BCS_JACOBI_OMEGA
     void denseSolve(const double* r, double* z);
     int* hTot_ = nullptr;                     // pinned: per-level sweep program sizes
-    // Overlapped hierarchy setup (PARITY / EXACT modes): level l's dependency
-    // levels and DILU factorisation run on a side stream while the coarsening
-    // builds the next levels (BCS_DILU_OVERLAP=0: after the hierarchy instead)
-    bool overlapDilu_ = true;
-    cudaStream_t side_ = nullptr;
-    cudaEvent_t evMainReady_ = nullptr, evSideDone_ = nullptr;
-    std::vector<int> sideLevels_, lateLevels_;
-    DArray<int> sCnt_, sScan_, sSmall_, sDepth_, sErr_;
-    DArray<unsigned char> sDesc_;
-    unsigned char* sDescHost_ = nullptr;  // pinned descriptor slots, one per level
-    int sideGridCap_ = 0;
-    void sideBegin(const bcs_solver_config& cfg);
-    void sideDilu(int l);
-    void sideJoin(const bcs_solver_config& cfg);
-    void diluFactor(const std::vector<Level*>& lv);
     void setupTail();
     std::vector<std::pair<std::string, double>> profRec_;
     std::chrono::steady_clock::time_point profT_;

@@ -98,21 +98,10 @@ struct DiluLevelHost {
     int* piv;
     size_t tOff;
 };
-void dilu_setup_level(int n, const DiluLevelHost& h, const int* order, void* desc_dev, void* desc_host, double* T,
-                      size_t tcount, int* err_cell, int* err, int grid_cap, cudaStream_t s);
 void dilu_setup_multi(int n, int nl, const DiluLevelHost* levels, int maxdepth, int* keys, int* order, int* cnt,
                       int* scan_tmp, int* small, void* desc_dev, double* Tbase, size_t tcount, int* err_cell,
                       int* err, cudaStream_t s);
 size_t dilu_desc_bytes();
-// one level's smoother setup without host synchronisation (overlapped setup):
-// descriptors go through desc_host (pinned, side_desc_bytes()) -> desc_dev;
-// d_depth receives the DAG depth, err/err_cell the wait and singularity flags
-size_t side_desc_bytes();
-void level_schedule_async(int rows, const int* ro, const int* ci, const int* dg, int* level, int* order, int* d_depth,
-                          int* cnt, int* scan_tmp, int* small, void* desc_dev, void* desc_host, int* err,
-                          int grid_cap, cudaStream_t s);
-void dilu_compact_index_async(int rows, const int* ro, const int* dg, const int* ci, const int* tpos, int* lpre, int* tc,
-                              int* d_total, int* scan_tmp, cudaStream_t s);
 // lower-slot prefix lpre[rows+1] and compact transposed index tc[nnz] of the
 // DILU setup's T (lower slots only); returns the number of lower slots (syncs)
 size_t dilu_compact_index(int rows, const int* ro, const int* dg, const int* ci, const int* tpos, int* lpre, int* tc,
