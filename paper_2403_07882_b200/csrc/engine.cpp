@@ -2419,6 +2419,16 @@ std::string Engine::memoryReport() const {
             add("aggregates", L.agg); add("aggregates", L.members);
             add("vcycle_vectors", L.r); add("vcycle_vectors", L.z); add("vcycle_vectors", L.res);
             add("vcycle_vectors", L.y); add("vcycle_vectors", L.zb);
+            if (L.mc) {  // performance mode: the colour-permuted copy and its smoother
+                const Level& M = *L.mc;
+                add("perf_coloured_copies", M.o_v); add("perf_coloured_copies", M.o_ro); add("perf_coloured_copies", M.o_ci);
+                add("perf_coloured_copies", M.o_dg); add("perf_coloured_copies", M.o_tpos); add("perf_coloured_copies", M.lu);
+                add("perf_coloured_copies", M.rcp); add("perf_coloured_copies", M.piv); add("perf_coloured_copies", M.perm);
+                add("perf_coloured_copies", M.order); add("perf_coloured_copies", M.recf); add("perf_coloured_copies", M.recb);
+                add("perf_coloured_copies", M.offf); add("perf_coloured_copies", M.offb); add("perf_coloured_copies", M.dlev);
+                add("perf_coloured_copies", M.r); add("perf_coloured_copies", M.y); add("perf_coloured_copies", M.zb);
+                add("perf_coloured_copies", L.mcPerm); add("perf_coloured_copies", L.mcColorOffD);
+            }
         }
         add("dense_coarsest", H.dense); add("dense_coarsest", H.dpiv); add("schedule", H.tailDesc);
         m["phase_arena (DILU scratch | sweep programs + Krylov basis)"] += static_cast<double>(H.arena.cap);
