@@ -243,23 +243,40 @@ void transpose_pos(int rows, const int* ro, const int* ci, int* tpos, int* asym_
 }
 
 // value permutation: one thread per double, coalesced writes
-__global__ void k_gather(int nn, size_t total, int nc, int nf, const int* src, const double* diag,
-                         const double* upper, const double* lower, double* vals) {
-    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total; i += stride) {
-        const size_t k = i / nn;
-        const int e = static_cast<int>(i - k * nn);
+// 4 doubles per thread (a CTA covers 1024 consecutive ones, coalesced per
+// instruction); NN compile-time so the slot index is a constant division;
+// the grid covers the array once (no grid-stride loop)
+template <int NN>
+__global__ void __launch_bounds__(256) k_gather(size_t total, int nc, int nf, const int* __restrict__ src,
+                                                const double* __restrict__ diag, const double* __restrict__ upper,
+                                                const double* __restrict__ lower, double* __restrict__ vals) {
+    const size_t i0 = 4 * blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const size_t i = i0 + static_cast<size_t>(u) * blockDim.x;  // coalesced per instruction
+        if (i >= total) return;
+        const size_t k = i / NN;
+        const int e = static_cast<int>(i - k * NN);
         const int sidx = __ldg(&src[k]);
-        const double* from = sidx < nc ? diag + static_cast<size_t>(sidx) * nn
-                             : sidx < nc + nf ? upper + static_cast<size_t>(sidx - nc) * nn
-                                              : lower + static_cast<size_t>(sidx - nc - nf) * nn;
-        vals[i] = __ldg(&from[e]);
+        const double* from = sidx < nc ? diag + static_cast<size_t>(sidx) * NN
+                             : sidx < nc + nf ? upper + static_cast<size_t>(sidx - nc) * NN
+                                              : lower + static_cast<size_t>(sidx - nc - nf) * NN;
+        __stcs(&vals[i], __ldcs(&from[e]));
     }
 }
+
 void gather_values(int n, int nnz, int nc, int nf, const int* src, const double* diag, const double* upper,
                    const double* lower, double* vals, cudaStream_t s) {
     const size_t total = static_cast<size_t>(nnz) * n * n;
-    k_gather<<<grid_for(total, 256, 148 * 16), 256, 0, s>>>(n * n, total, nc, nf, src, diag, upper, lower, vals);
+    if (!total) return;
+    const unsigned g = static_cast<unsigned>((total + 1023) / 1024);
+    switch (n) {
+        case 1: k_gather<1><<<g, 256, 0, s>>>(total, nc, nf, src, diag, upper, lower, vals); break;
+        case 2: k_gather<4><<<g, 256, 0, s>>>(total, nc, nf, src, diag, upper, lower, vals); break;
+        case 3: k_gather<9><<<g, 256, 0, s>>>(total, nc, nf, src, diag, upper, lower, vals); break;
+        case 4: k_gather<16><<<g, 256, 0, s>>>(total, nc, nf, src, diag, upper, lower, vals); break;
+        default: k_gather<25><<<g, 256, 0, s>>>(total, nc, nf, src, diag, upper, lower, vals); break;
+    }
     count_launch();
 }
 
