@@ -76,7 +76,8 @@ __global__ void __launch_bounds__(kRedThreads) k_dot(const double* __restrict__ 
                                                      int sqrt_out, double* partials, int* ticket) {
     const SegRange R = seg_range(seg, nseg);
     double s = 0.0;
-    for (size_t i = R.i0; i < R.e; i += R.stride) s += a[i] * b[i];
+#pragma unroll 4
+    for (size_t i = R.i0; i < R.e; i += R.stride) s += a[i] * b[i];  // (unrolled: loads in flight, same order)
     finish_reduction(s, nseg, partials, ticket, out, sqrt_out != 0);
 }
 
@@ -193,6 +194,7 @@ __global__ void __launch_bounds__(kRedThreads) k_axpy_dot(double* __restrict__ w
     const double hv = *h;
     const SegRange R = seg_range(seg, nseg);
     double s = 0.0;
+#pragma unroll 4
     for (size_t i = R.i0; i < R.e; i += R.stride) {
         const double wn = w[i] - hv * v[i];
         w[i] = wn;
