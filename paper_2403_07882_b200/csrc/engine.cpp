@@ -1773,6 +1773,9 @@ void Engine::distSolve(int nc, int nf, int n, const int32_t* owner, const int32_
     const bool same = distNc_ == nc && distNf_ == nf && distN_ == n && distRanks_ == nRanks && distEngines_ == nEngines &&
                       std::equal(owner, owner + nf, distOwner_.begin()) && std::equal(neigh, neigh + nf, distNeigh_.begin()) &&
                       std::equal(centroids, centroids + 3 * static_cast<size_t>(nc), distCen_.begin());
+    // the serial system's sizes (n_, nc_) are borrowed for the Krylov operators of
+    // this call and restored on every exit, with H_ and the operator switches
+    SerialStateGuard guard(*this);
     if (!same) distSetupTopology(nc, nf, n, owner, neigh, centroids, nRanks, nEngines);
     n_ = n;
     // upload: LDU values -> engine slots and halo blocks (replace semantics)
@@ -1835,13 +1838,7 @@ void Engine::distSolve(int nc, int nf, int n, const int32_t* owner, const int32_
     sync();
     const auto t2 = clk::now();
     distActive_ = true;
-    try {
-        solveKrylov(kb_, kx_.p, cfg, rep);
-    } catch (...) {
-        distActive_ = false;
-        nseg_ = 1;
-        throw;
-    }
+    solveKrylov(kb_, kx_.p, cfg, rep);
     distActive_ = false;
     const auto t3 = clk::now();
     check(cudaMemcpyAsync(hx.data(), kx_.p, N * sizeof(double), cudaMemcpyDeviceToHost, stream_), "D2H x");
@@ -1954,6 +1951,7 @@ void Engine::distSolveMP(int nc, int nf, int n, const int32_t* owner, const int3
                       parallelEqual(owner, mpOwner_.data(), static_cast<size_t>(nf)) &&
                       parallelEqual(neigh, mpNeigh_.data(), static_cast<size_t>(nf)) &&
                       parallelEqual(centroids, mpCen_.data(), 3 * static_cast<size_t>(nc));
+    SerialStateGuard guard(*this);
     if (!same) mpSetupTopology(nc, nf, n, owner, neigh, centroids, nRanks);
     n_ = n;
     DistPart& P = dist_[0];
@@ -2017,7 +2015,6 @@ void Engine::distSolveMP(int nc, int nf, int n, const int32_t* owner, const int3
     sweepCount_ = 0;
     evUsed_ = 0;
     cudaMemsetAsync(err_.p + 1, 0, sizeof(int), stream_);
-    const int ncSerial = nc_;
     nc_ = mpRows_;
     H_ = &P.H;
     FineMatrix F;
@@ -2028,13 +2025,7 @@ void Engine::distSolveMP(int nc, int nf, int n, const int32_t* owner, const int3
     F.dg = P.dg;
     F.tpos = P.tpos;
     F.v = P.vals;
-    try {
-        buildPrecondOn(F, cfg);
-    } catch (...) {
-        H_ = &main_;
-        nc_ = ncSerial;
-        throw;
-    }
+    buildPrecondOn(F, cfg);
     H_ = &main_;
     sync();
     const auto t2 = clk::now();
@@ -2045,13 +2036,7 @@ void Engine::distSolveMP(int nc, int nf, int n, const int32_t* owner, const int3
         const long long segh[2] = {0, static_cast<long long>(mpRows_) * n};
         check(cudaMemcpyAsync(seg_.p, segh, sizeof segh, cudaMemcpyHostToDevice, stream_), "H2D seg");
     }
-    try {
-        solveKrylov(kb_, kx_.p, cfg, rep);
-    } catch (...) {
-        distActive_ = mpActive_ = false;
-        nc_ = ncSerial;
-        throw;
-    }
+    solveKrylov(kb_, kx_.p, cfg, rep);
     distActive_ = mpActive_ = false;
     const auto t3 = clk::now();
     // gatherVector (partition.cpp:282-296): padded all-gather of the slices
@@ -2070,7 +2055,6 @@ void Engine::distSolveMP(int nc, int nf, int n, const int32_t* owner, const int3
             std::copy(all.begin() + pad * e + static_cast<size_t>(r) * n, all.begin() + pad * e + static_cast<size_t>(r + 1) * n,
                       x + static_cast<size_t>(old) * n);
         });
-    nc_ = ncSerial;
     const auto t4 = clk::now();
     rep.t_convert = secs(t0, t1);  // partition.cpp:474-477 keys
     rep.t_setup = secs(t1, t2);
@@ -2289,7 +2273,15 @@ void Engine::pipelineSolve(int nc, int nf, int n, const int32_t* owner, const in
         takeSetup = sig != pipeSig_;
     }
     t = clk::now();
-    if (takeSetup || !sameTopo) setTopology(nc, nf, n, owner, neigh);
+    if (takeSetup || !sameTopo) {
+        try {
+            setTopology(nc, nf, n, owner, neigh);
+        } catch (...) {
+            pipeHasSetup_ = false;  // the next call takes the setup branch again
+            pipeSigValid_ = false;
+            throw;
+        }
+    }
     uploadLdu(diag, upper, lower, false);
     sync();
     const double tsr = secs(t, clk::now());

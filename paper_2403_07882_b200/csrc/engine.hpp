@@ -158,6 +158,10 @@ struct FineMatrix {
 };
 
 class Engine {
+    // Mode R calls borrow n_/nc_/H_ and the operator switches for their Krylov
+    // run; this restores the serial system's view on every exit (incl. throws)
+    friend struct SerialStateGuard;
+
 public:
     explicit Engine(int device);
     ~Engine();
@@ -400,6 +404,20 @@ private:
     int sweepCount_ = 0;
     void timerBegin();
     void timerEnd(int kind, double bytes);
+};
+
+struct SerialStateGuard {
+    Engine& e;
+    int nc, n, nseg;
+    explicit SerialStateGuard(Engine& en) : e(en), nc(en.nc_), n(en.n_), nseg(en.nseg_) {}
+    ~SerialStateGuard() {
+        e.nc_ = nc;
+        e.n_ = n;
+        e.nseg_ = nseg;
+        e.H_ = &e.main_;
+        e.distActive_ = false;
+        e.mpActive_ = false;
+    }
 };
 
 }  // namespace bcs

@@ -134,3 +134,27 @@ def test_dist_mp_exact_mode_equals_one_device(ctx):
     x2, r2 = ctx.dist_solve_mp(s.A, s.b, s.x0, s.centroids, 3, cfg)
     assert r1.iterations == r2.iterations and r2.converged
     assert x1.values.tobytes() == x2.values.tobytes()
+
+
+def test_serial_system_survives_a_dist_solve():
+    """A Mode R call on another system (other block size and cell count) borrows
+    the context's sizes for its Krylov run and restores them: the serial matrix
+    uploaded before solves bit-identically afterwards."""
+    c = bcs.Context(0)
+    try:
+        s = gen.hex_euler(6)
+        cfg = bcs.SolverConfig(preconditioner=bcs.PrecondKind.AMG, relTol=1e-8, maxIters=400,
+                               amg=bcs.AmgConfig(maxLevels=30, minCoarseRows=8))
+        c.set_topology(s.A)
+        c.upload_ldu(s.A)
+        x1 = s.x0.values.copy()
+        r1 = c.solve(s.b.values, x1, cfg)
+        t = gen.hex_coupled(8)
+        xd, rd = c.dist_solve(t.A, t.b, t.x0, t.centroids, 4, 2, cfg)
+        assert rd.converged
+        x2 = s.x0.values.copy()
+        r2 = c.solve(s.b.values, x2, cfg)
+        assert r2.iterations == r1.iterations and x2.tobytes() == x1.tobytes()
+        assert c.residual(s.b.values, x2) == pytest.approx(r2.finalResidual, rel=1e-9)
+    finally:
+        c.close()
