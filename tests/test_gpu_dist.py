@@ -158,3 +158,17 @@ def test_serial_system_survives_a_dist_solve():
         assert c.residual(s.b.values, x2) == pytest.approx(r2.finalResidual, rel=1e-9)
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("mode", [bcs.Mode.PERF, bcs.Mode.PERF_JACOBI])
+def test_dist_perf_modes_converge(ctx, mode):
+    """The performance smoothers inside Mode R engines: every engine's hierarchy
+    is coloured (or Jacobi-smoothed) on its own; the solve reaches the tolerance."""
+    s = gen.hex_euler(12)
+    cfg = bcs.SolverConfig(preconditioner=bcs.PrecondKind.AMG, relTol=1e-8, maxIters=400,
+                           amg=bcs.AmgConfig(maxLevels=30, minCoarseRows=8), mode=mode)
+    x, r = ctx.dist_solve(s.A, s.b, s.x0, s.centroids, 4, 2, cfg)
+    assert r.converged
+    ctx.set_topology(s.A)
+    ctx.upload_ldu(s.A)
+    assert ctx.residual(s.b.values, x.values) <= 1e-8 * r.initialResidual * 1.01
