@@ -218,6 +218,7 @@ Engine::~Engine() {
         rel(L.mcPerm);
         rel(L.mcColorOffD);
         rel(L.o_ro); rel(L.o_ci); rel(L.o_dg); rel(L.o_tpos); rel(L.o_v); rel(L.lu); rel(L.rcp); rel(L.perm); rel(L.recf); rel(L.recb); rel(L.dlev); rel(L.offf); rel(L.offb); rel(L.pkf); rel(L.pkb); rel(L.piv); rel(L.order);
+        rel(L.woff); rel(L.woffb);
         rel(L.agg); rel(L.members); rel(L.r); rel(L.z); rel(L.res); rel(L.y); rel(L.zb);
     }
     rel(dOwner_); rel(dNeigh_); rel(ro_); rel(ci_); rel(dg_); rel(tpos_); rel(src_); rel(fill_); rel(vals_);
@@ -225,14 +226,14 @@ Engine::~Engine() {
     rel(scanTmp_); rel(dkeys_); rel(dorder_); rel(ddesc_); rel(act2_); rel(flag_); rel(err_); rel(ctr_); rel(choice_); rel(segOff_); rel(cro_); rel(big_); rel(dn_); rel(tblk_);
     rel(str_); rel(keys_); rel(sorted_); rel(V_); rel(w_); rel(zk_); rel(rk_); rel(Hm_); rel(cs_); rel(sn_); rel(g_);
     rel(y_); rel(scal_); rel(partials_); rel(kb_); rel(kx_); rel(bp_); rel(bv_); rel(bs_); rel(bt_); rel(bph_);
-    rel(bsh_); rel(brh_); rel(ticket_); rel(seg_); rel(distTmp_); rel(mcSv_);
+    rel(bsh_); rel(brh_); rel(ticket_); rel(seg_); rel(distTmp_); rel(mcSv_); rel(chunkOrd_); rel(chainCnt_);
     for (auto& P : dist_) {
         rel(P.ro); rel(P.ci); rel(P.src); rel(P.dg); rel(P.tpos); rel(P.vals); rel(P.hrow); rel(P.hoff);
         rel(P.hcol); rel(P.hsrc); rel(P.hvals);
         for (auto& L : P.H.levels) {
             rel(L.o_ro); rel(L.o_ci); rel(L.o_dg); rel(L.o_tpos); rel(L.o_v); rel(L.lu); rel(L.rcp); rel(L.perm); rel(L.recf);
             rel(L.recb); rel(L.dlev); rel(L.offf); rel(L.offb); rel(L.pkf); rel(L.pkb); rel(L.piv); rel(L.order); rel(L.agg); rel(L.members); rel(L.r); rel(L.z); rel(L.res);
-            rel(L.y); rel(L.zb);
+            rel(L.y); rel(L.zb); rel(L.woff); rel(L.woffb);
         }
         rel(P.H.dense); rel(P.H.dpiv);
         P.H.arena.release(stream_);
@@ -749,6 +750,7 @@ void Engine::diluSetupAll(const std::vector<Level*>& lv, const bcs_solver_config
             const int cell = readErrCell();
             if (cell != big)
                 throw std::runtime_error("DILU setup: singular modified diagonal in cell " + std::to_string(cell));
+            L.dlevOk = false;
         }
         finishSmoothers(lv, nullptr);
         return;
@@ -763,6 +765,7 @@ void Engine::diluSetupAll(const std::vector<Level*>& lv, const bcs_solver_config
         L.piv.ensure(static_cast<size_t>(L.rows) * n_, stream_);
         L.order.ensure(L.rows, stream_);
         L.dlev.ensure(L.rows, stream_);
+        L.dlevOk = true;
         lh[l] = {L.rows, L.ro, L.ci, L.dg, L.dlev.p, L.order.p};
         totalRows += L.rows;
         maxRows = std::max(maxRows, static_cast<size_t>(L.rows));
@@ -835,6 +838,69 @@ void Engine::diluSetupAll(const std::vector<Level*>& lv, const bcs_solver_config
 void Engine::finishSmoothers(const std::vector<Level*>& lv, const bcs_solver_config* cfg) {
     const int nl = static_cast<int>(lv.size());
     if (nl > 64) throw std::logic_error("bcs: more than 64 smoothed levels");
+    // chain schedules (opt-in, BCS_CHAIN=1) for wide levels whose rows mostly
+    // chain to the previous row (natural-order meshes): see k_chain_starts.
+    // Measured at 128^3 it loses to the level order (0.310 vs 0.2935 s/step):
+    // every y/z coupling is a cross-warp hop between lines in flight at the
+    // same time, so the rows advance at the hop rate.
+    static const bool chainOn = [] {
+        const char* e = std::getenv("BCS_CHAIN");
+        return e && std::atoi(e) != 0;
+    }();
+    static const int chainMinWidth = [] {  // rows per dependency level
+        const char* e = std::getenv("BCS_CHAIN_MIN_WIDTH");
+        return e ? std::atoi(e) : 4096;
+    }();
+    auto candidate = [&](const Level& L) {
+        return chainOn && !L.colourSweep && L.dlevOk && L.depth > 0 && L.rows / L.depth >= chainMinWidth;
+    };
+    int chains[2 * 64];
+    bool anyCand = false;
+    chainCnt_.ensure(2 * 64, stream_);
+    cudaMemsetAsync(chainCnt_.p, 0, 2 * 64 * sizeof(int), stream_);
+    for (int l = 0; l < nl; ++l) {
+        Level& L = *lv[l];
+        L.chain = false;
+        if (candidate(L)) {
+            chain_count(L.rows, L.ro, L.dg, L.ci, chainCnt_.p + l, stream_);
+            anyCand = true;
+        }
+    }
+    if (anyCand) {
+        check(cudaMemcpyAsync(chains, chainCnt_.p, nl * sizeof(int), cudaMemcpyDeviceToHost, stream_), "chains");
+        sync();
+        size_t need = 0;
+        for (int l = 0; l < nl; ++l) {
+            Level& L = *lv[l];
+            L.chain = candidate(L) && 2LL * chains[l] >= L.rows;
+            if (L.chain) need += 2 * static_cast<size_t>(L.rows);
+        }
+        // the schedules (orders in chunkOrd_, checked before use)
+        chunkOrd_.ensure(need, stream_);
+        size_t at = 0;
+        for (int l = 0; l < nl; ++l) {
+            Level& L = *lv[l];
+            if (!L.chain) continue;
+            const int Wf = sweep_chunk_warps(n_, true), Wb = sweep_chunk_warps(n_, false);
+            L.woff.ensure(static_cast<size_t>(Wf) + 1, stream_);
+            L.woffb.ensure(static_cast<size_t>(Wb) + 1, stream_);
+            chain_schedule(L.rows, true, L.depth, L.ro, L.dg, L.ci, L.dlev, Wf, chunkOrd_.p + at, L.woff.p,
+                           chainCnt_.p + 64 + l, stream_);
+            chain_schedule(L.rows, false, L.depth, L.ro, L.dg, L.ci, L.dlev, Wb, chunkOrd_.p + at + L.rows,
+                           L.woffb.p, chainCnt_.p + 64 + l, stream_);
+            at += 2 * static_cast<size_t>(L.rows);
+        }
+        check(cudaMemcpyAsync(chains + 64, chainCnt_.p + 64, nl * sizeof(int), cudaMemcpyDeviceToHost, stream_),
+              "chain check");
+        sync();
+        static const bool verbose = std::getenv("BCS_CHAIN_VERBOSE") != nullptr;
+        for (int l = 0; l < nl; ++l) {
+            if (lv[l]->chain && chains[64 + l]) lv[l]->chain = false;  // progress check failed: level order
+            if (verbose && candidate(*lv[l]))
+                std::fprintf(stderr, "bcs chain: level rows %d depth %d chained %d -> %s\n", lv[l]->rows,
+                             lv[l]->depth, chains[l], lv[l]->chain ? "chain schedule" : "level order");
+        }
+    }
     for (int l = 0; l < nl; ++l) {
         Level& L = *lv[l];
         L.rcp.ensure(static_cast<size_t>(L.rows) * n_, stream_);
@@ -846,13 +912,21 @@ void Engine::finishSmoothers(const std::vector<Level*>& lv, const bcs_solver_con
         }
         L.recf.ensure(4 * static_cast<size_t>(L.rows), stream_);
         L.recb.ensure(4 * static_cast<size_t>(L.rows), stream_);
-        sweep_records(L.rows, L.order, L.ro, L.dg, L.recf.p, L.recb.p, stream_);
+        if (L.chain) {
+            size_t at = 0;  // this level's schedules in chunkOrd_
+            for (int k = 0; k < l; ++k)
+                if (lv[k]->chain) at += 2 * static_cast<size_t>(lv[k]->rows);
+            sweep_records(L.rows, chunkOrd_.p + at, chunkOrd_.p + at + L.rows, L.ro, L.dg, L.recf.p, L.recb.p,
+                          stream_);
+        } else {
+            sweep_records(L.rows, L.order, nullptr, L.ro, L.dg, L.recf.p, L.recb.p, stream_);
+        }
         const size_t n1 = static_cast<size_t>(L.rows) + 1;
         scanTmp_.ensure(scan_tmp_ints(n1) + 16, stream_);
         for (int d = 0; d < 2; ++d) {
             DArray<int>& off = d == 0 ? L.offf : L.offb;
             off.ensure(n1, stream_);
-            sweep_slot_sizes(n_, d == 0, L.rows, L.depth, d == 0 ? L.recf : L.recb, off.p, stream_);
+            sweep_slot_sizes(n_, d == 0, L.rows, L.sweepDepth(), d == 0 ? L.recf : L.recb, off.p, stream_);
             exclusive_scan(off.p, L.rows, off.p + L.rows, scanTmp_.p, stream_);
             check(cudaMemcpyAsync(hTot_ + 2 * l + d, off.p + L.rows, sizeof(int), cudaMemcpyDeviceToHost, stream_),
                   "slot total");
@@ -881,7 +955,7 @@ void Engine::finishSmoothers(const std::vector<Level*>& lv, const bcs_solver_con
             DArray<unsigned char>& pk = d == 0 ? L.pkf : L.pkb;
             const size_t b = 16 * static_cast<size_t>(hTot_[2 * l + d]) + 16;
             pk.borrow(H_->arena.take<unsigned char>(b), b, stream_);
-            sweep_pack(n_, d == 0, L.rows, L.depth, d == 0 ? L.recf : L.recb, L.ci, L.v, L.lu, L.perm, L.rcp,
+            sweep_pack(n_, d == 0, L.rows, L.sweepDepth(), d == 0 ? L.recf : L.recb, L.ci, L.v, L.lu, L.perm, L.rcp,
                        d == 0 ? L.offf : L.offb, pk.p, stream_);
         }
     }
@@ -924,8 +998,10 @@ void Engine::lusgsSetup(Level& L) {
     cnt_.ensure(static_cast<size_t>(L.rows) + 2, stream_);
     scanTmp_.ensure(scan_tmp_ints(static_cast<size_t>(L.rows) + 2) + 16, stream_);
     cudaMemsetAsync(err_.p + 2, 0, sizeof(int), stream_);
-    L.depth = level_schedule(L.rows, L.ro, L.ci, L.dg, L.order.p, lvl_.p, cnt_.p, scanTmp_.p, push_.p, err_.p + 2,
-                             stream_);
+    L.dlev.ensure(static_cast<size_t>(L.rows) + 1, stream_);
+    L.depth = level_schedule(L.rows, L.ro, L.ci, L.dg, L.order.p, L.dlev.p, cnt_.p, scanTmp_.p, push_.p,
+                             err_.p + 2, stream_);
+    L.dlevOk = true;
     finishSmoothers({&L}, nullptr);
 }
 
@@ -1255,10 +1331,10 @@ void Engine::smootherApply(Level& L, const double* r, double* z, int accumulate)
     const double per = tri + R * (8.0 * nb * nb + 8.0 * nb + 4.0 * nb + 16.0) + 2.0 * R * 8.0 * nb;
     const bool timed = kernelTiming_;
     if (timed) timerBegin();
-    sweep_forward(n_, L.rows, L.depth, L.offf, L.pkf, L.ci, L.v, r, L.y.p, err_.p + 1, stream_);
+    sweep_forward(n_, L.rows, L.sweepDepth(), L.offf, L.pkf, L.recf, L.woff, L.ci, L.v, r, L.y.p, err_.p + 1, stream_);
     if (timed) timerEnd(1, per);
     if (timed) timerBegin();
-    sweep_backward(n_, L.rows, L.depth, L.offb, L.pkb, L.ci, L.v, L.y, zb, z, accumulate, err_.p + 1, stream_);
+    sweep_backward(n_, L.rows, L.sweepDepth(), L.offb, L.pkb, L.recb, L.woffb, L.ci, L.v, L.y, zb, z, accumulate, err_.p + 1, stream_);
     if (timed) timerEnd(1, per + (accumulate == 2 ? 2.0 : accumulate == 1 ? 1.0 : 0.0) * R * 8.0 * nb);
 }
 
@@ -2406,7 +2482,7 @@ std::string Engine::memoryReport() const {
             add("smoother_factors", L.lu); add("smoother_factors", L.rcp); add("smoother_factors", L.piv);
             add("smoother_factors", L.perm);
             add("schedule", L.order); add("schedule", L.recf); add("schedule", L.recb); add("schedule", L.offf);
-            add("schedule", L.offb); add("schedule", L.dlev);
+            add("schedule", L.offb); add("schedule", L.dlev); add("schedule", L.woff); add("schedule", L.woffb);
             add("sweep_programs", L.pkf); add("sweep_programs", L.pkb);
             add("aggregates", L.agg); add("aggregates", L.members);
             add("vcycle_vectors", L.r); add("vcycle_vectors", L.z); add("vcycle_vectors", L.res);
@@ -2446,7 +2522,7 @@ std::string Engine::memoryReport() const {
         add("assembly", *a);
     for (const auto* a : {&asmInv_, &asmCfo_, &asmCf_, &asmBco_, &asmBkind_, &asmBad_}) add("assembly", *a);
     for (const auto* a : {&cnt_, &lvl_, &act2_, &push_, &scanTmp_, &flag_, &err_, &ctr_, &choice_, &segOff_, &cro_,
-                          &big_, &dkeys_, &dorder_, &ticket_})
+                          &big_, &dkeys_, &dorder_, &ticket_, &chunkOrd_, &chainCnt_})
         add("setup_scratch", *a);
     add("setup_scratch", dn_); add("setup_scratch", str_); add("setup_scratch", keys_); add("setup_scratch", sorted_);
     add("setup_scratch", ddesc_);

@@ -109,6 +109,10 @@ struct Level {
     DArray<int> tc, lpre;                      // DILU setup only: compact T indices (released after)
     DArray<unsigned char> pkf, pkb;            // packed per-ticket slots of the two sweeps
     int depth = 0;
+    bool dlevOk = false;     // dlev holds the dependency levels of the current factorisation
+    bool chain = false;      // chain schedule (k_sweep_chain), launched with depth -1
+    DArray<int> woff, woffb;  // chain schedule: warp ticket ranges of the two sweeps
+    int sweepDepth() const { return chain ? -1 : depth; }
     // aggregation to level+1
     DArray<int> agg, members;
     int ncoarse = 0;
@@ -329,6 +333,7 @@ private:
     Hier main_;
     Hier* H_ = &main_;
     // scratch
+    DArray<int> chunkOrd_, chainCnt_;  // chain schedules: orders, chain counts / check flags
     DArray<int> cnt_, lvl_, act2_, push_, scanTmp_, flag_, err_, ctr_, choice_, segOff_, cro_, big_;
     DArray<double> dn_, str_, tblk_;
     DArray<int> dkeys_, dorder_;       // combined DILU tickets

@@ -121,7 +121,18 @@ void level_schedule_multi(int nl, const LevelsHost* lv, int* depth, int* cnt, in
 // 2 z += zb.  rcp: per-row diagonal reciprocals (make_reciprocals).
 void make_reciprocals(int n, int rows, const double* lu, const int* piv, double* rcp, int* perm, cudaStream_t s);
 // ticket-order records (int4: row, first slot, #deps) for both sweeps
-void sweep_records(int rows, const int* order, const int* ro, const int* dg, int* fwd4, int* bwd4, cudaStream_t s);
+// order: forward tickets -> rows; border: backward tickets -> rows, or
+// nullptr for the forward order reversed (the level schedule)
+void sweep_records(int rows, const int* order, const int* border, const int* ro, const int* dg, int* fwd4,
+                   int* bwd4, cudaStream_t s);
+// chain schedule (k_sweep.cu): W = warps of the chain kernel's cooperative
+// grid; order (rows) = tickets -> rows, woff (W+1) = warp ticket ranges;
+// *bad |= 1 when the schedule's progress check fails on this pattern.
+// Launch the level's sweeps with depth = -1 and woff.
+int sweep_chunk_warps(int n, bool fwd);
+void chain_schedule(int rows, bool fwd, int depth, const int* ro, const int* dg, const int* ci, const int* dlev, int W,
+                    int* order, int* woff, int* bad, cudaStream_t s);
+void chain_count(int rows, const int* ro, const int* dg, const int* ci, int* cnt, cudaStream_t s);
 // per-ticket slots (the sweep program): slot sizes in 16-byte units into
 // off16 (rows entries; the caller scans them, off16[rows] = total), then the
 // packed slots of one direction (rec4 = that direction's records).
@@ -129,11 +140,14 @@ void sweep_slot_sizes(int n, bool fwd, int rows, int depth, const int* rec4, int
 void sweep_pack(int n, bool fwd, int rows, int depth, const int* rec4, const int* ci, const double* v,
                 const double* lu, const int* perm, const double* rcp, const int* off16, unsigned char* pk,
                 cudaStream_t s);
-void sweep_forward(int n, int rows, int depth, const int* off16, const unsigned char* pk, const int* ci,
-                   const double* v, const double* r, double* y, int* err, cudaStream_t s);
-void sweep_backward(int n, int rows, int depth, const int* off16, const unsigned char* pk, const int* ci,
-                    const double* v, const double* y, double* zb, double* z, int accumulate, int* err,
-                    cudaStream_t s);
+// rec4: the sweep's ticket records, woff: warp ticket ranges (both read by
+// the chain variant only, depth = -1)
+void sweep_forward(int n, int rows, int depth, const int* off16, const unsigned char* pk, const int* rec4,
+                   const int* woff, const int* ci, const double* v, const double* r, double* y, int* err,
+                   cudaStream_t s);
+void sweep_backward(int n, int rows, int depth, const int* off16, const unsigned char* pk, const int* rec4,
+                    const int* woff, const int* ci, const double* v, const double* y, double* zb, double* z,
+                    int accumulate, int* err, cudaStream_t s);
 // number of mismatches of the reciprocal-based division against __ddiv_rn
 unsigned long long selftest_division(unsigned long long n, unsigned long long seed);
 unsigned long long selftest_latency(int op, int n);  // cycles of n dependent ops (0 dadd 1 dmul 2 dfma 3 shfl.f64 4 shfl.b32)
