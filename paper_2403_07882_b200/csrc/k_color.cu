@@ -354,52 +354,119 @@ __global__ void __launch_bounds__(256) k_mc_sweep(int ncol, const int* __restric
 // out_i = omega * D_i^-1 r_i per block row (the diagonal block's LU with the
 // composed pivot permutation and reciprocal-based division, as the sweeps),
 // z = out | 0 + out | z + out by `acc` (the V-cycle's pre/post-smoothing
-// forms).  No dependencies: one pass over the factors, HBM-bound.  The rows'
-// factors are staged through shared memory with coalesced loads.
+// forms).  No dependencies: one pass over the factors, HBM-bound.  Every
+// per-row array (factors, reciprocals, permutation, r, z) moves between HBM
+// and shared memory with coalesced 16-byte streaming accesses; a thread then
+// solves one row out of shared memory.
 constexpr int kJacRows = 128;
+
+// fallback copy (unaligned tails): 4-byte words
+__device__ __forceinline__ void jac_load_words(void* dst, const void* src, int bytes) {
+    const int* s1 = reinterpret_cast<const int*>(src);
+    int* d1 = reinterpret_cast<int*>(dst);
+    for (int e = threadIdx.x; e < bytes / 4; e += blockDim.x) d1[e] = __ldcs(&s1[e]);
+}
+__device__ __forceinline__ unsigned jac_smem(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+// one TMA bulk copy global -> shared, completion counted on the mbarrier
+__device__ __forceinline__ void jac_bulk(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(jac_smem(dst)),
+        "l"(src), "r"(bytes), "r"(jac_smem(bar))
+        : "memory");
+}
+
 template <int N>
 __global__ void __launch_bounds__(kJacRows) k_block_jacobi(int rows, const double* __restrict__ lu,
                                                           const double* __restrict__ rcp, const int* __restrict__ perm,
                                                           const double* __restrict__ r, double* z, int acc,
                                                           double omega) {
     constexpr int NN = N * N;
-    __shared__ double sl[kJacRows * NN];
+    __shared__ alignas(16) double sl[kJacRows * NN];
+    __shared__ alignas(16) double sr[kJacRows * N];
+    __shared__ alignas(16) double sc[kJacRows * N];
+    __shared__ alignas(16) double sz[kJacRows * N];
+    __shared__ alignas(16) int sp[kJacRows * N];
+    __shared__ alignas(8) unsigned long long bar;
     const int r0 = blockIdx.x * kJacRows;
     const int nrow = rows - r0 < kJacRows ? rows - r0 : kJacRows;
-    const double* src = lu + static_cast<size_t>(r0) * NN;
-    for (int e = threadIdx.x; e < nrow * NN; e += blockDim.x) sl[e] = __ldcs(&src[e]);
+    const size_t b0 = static_cast<size_t>(r0) * N;
+    // the block's rows arrive by TMA bulk copies (one thread issues them, no
+    // register round trip); sizes and addresses are 16-byte multiples except
+    // possibly in the last block, which copies word by word
+    const unsigned bl = nrow * NN * 8, bv = nrow * N * 8, bp = nrow * N * 4;
+    const bool bulk = ((reinterpret_cast<unsigned long long>(lu + b0 * N) | reinterpret_cast<unsigned long long>(r + b0) |
+                        reinterpret_cast<unsigned long long>(rcp + b0) | reinterpret_cast<unsigned long long>(perm + b0) |
+                        reinterpret_cast<unsigned long long>(z + b0) | bl | bv | bp) & 15) == 0;
+    if (bulk) {
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(jac_smem(&bar)) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            const unsigned tx = bl + 2 * bv + bp + (acc == 2 ? bv : 0);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(jac_smem(&bar)), "r"(tx)
+                         : "memory");
+            jac_bulk(sl, lu + b0 * N, bl, &bar);
+            jac_bulk(sr, r + b0, bv, &bar);
+            jac_bulk(sc, rcp + b0, bv, &bar);
+            jac_bulk(sp, perm + b0, bp, &bar);
+            if (acc == 2) jac_bulk(sz, z + b0, bv, &bar);
+        }
+        __syncthreads();  // barrier initialised before anyone waits on it
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+            "@!p bra W;\n\t}" ::"r"(jac_smem(&bar))
+            : "memory");
+    } else {
+        jac_load_words(sl, lu + b0 * N, bl);
+        jac_load_words(sr, r + b0, bv);
+        jac_load_words(sc, rcp + b0, bv);
+        jac_load_words(sp, perm + b0, bp);
+        if (acc == 2) jac_load_words(sz, z + b0, bv);
+    }
     __syncthreads();
     const int t = threadIdx.x;
-    if (t >= nrow) return;
-    const size_t i = static_cast<size_t>(r0 + t);
-    double rv[N], x[N], rc[N];
+    if (t < nrow) {
+        double rv[N], x[N], rc[N];
 #pragma unroll
-    for (int q = 0; q < N; ++q) {
-        rv[q] = __ldcs(&r[i * N + q]);
-        rc[q] = __ldcs(&rcp[i * N + q]);
+        for (int q = 0; q < N; ++q) {
+            rv[q] = sr[t * N + q];
+            rc[q] = sc[t * N + q];
+        }
+#pragma unroll
+        for (int p = 0; p < N; ++p) {
+            const int spp = sp[t * N + p];
+            double v = rv[0];
+#pragma unroll
+            for (int q = 1; q < N; ++q) v = (spp == q) ? rv[q] : v;
+            x[p] = v;
+        }
+        DVec<N> xin;
+#pragma unroll
+        for (int p = 0; p < N; ++p) xin.v[p] = x[p];
+        const double* L = sl + t * NN;
+        if (__builtin_expect(!lu_solve_perm_fast<N>(L, rc, x), 0)) {
+            const DVec<N> xe = lu_solve_perm_exact<N>(L, xin);
+#pragma unroll
+            for (int p = 0; p < N; ++p) x[p] = xe.v[p];
+        }
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+            const double o = __dmul_rn(omega, x[q]);
+            sz[t * N + q] = acc == 2 ? __dadd_rn(sz[t * N + q], o) : acc == 1 ? __dadd_rn(0.0, o) : o;
+        }
     }
-#pragma unroll
-    for (int p = 0; p < N; ++p) {
-        const int sp = __ldcs(&perm[i * N + p]);
-        double v = rv[0];
-#pragma unroll
-        for (int q = 1; q < N; ++q) v = (sp == q) ? rv[q] : v;
-        x[p] = v;
-    }
-    DVec<N> xin;
-#pragma unroll
-    for (int p = 0; p < N; ++p) xin.v[p] = x[p];
-    const double* L = sl + t * NN;
-    if (__builtin_expect(!lu_solve_perm_fast<N>(L, rc, x), 0)) {
-        const DVec<N> xe = lu_solve_perm_exact<N>(L, xin);
-#pragma unroll
-        for (int p = 0; p < N; ++p) x[p] = xe.v[p];
-    }
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-        const double o = __dmul_rn(omega, x[q]);
-        double* zq = z + i * N + q;
-        *zq = acc == 2 ? __dadd_rn(*zq, o) : acc == 1 ? __dadd_rn(0.0, o) : o;
+    __syncthreads();
+    // coalesced store of the block's results
+    double* dz = z + b0;
+    const int nd = nrow * N;
+    if ((reinterpret_cast<unsigned long long>(dz) & 15) == 0 && (nd & 1) == 0) {
+        const double2* s2 = reinterpret_cast<const double2*>(sz);
+        double2* d2 = reinterpret_cast<double2*>(dz);
+        for (int e = threadIdx.x; e < nd / 2; e += blockDim.x) __stcs(&d2[e], s2[e]);
+    } else {
+        for (int e = threadIdx.x; e < nd; e += blockDim.x) __stcs(&dz[e], sz[e]);
     }
 }
 

@@ -134,3 +134,50 @@ def test_perf_block_jacobi_amg_solve(ctx, maker):
     assert ctx.residual(s.b.values, xj) <= 1e-8 * rj.initialResidual * 1.0000001
     r = ctx.solve(s.b.values, s.x0.values.copy(), bcs.SolverConfig(**base))
     assert rj.iterations <= 6 * r.iterations + 5, (rj.iterations, r.iterations)
+
+
+def _bsr_matvec(ro, ci, v, n, x):
+    blocks = v.reshape(-1, n, n)
+    xb = x.reshape(-1, n)
+    rows = np.repeat(np.arange(ro.size - 1), np.diff(ro))
+    y = np.zeros_like(xb)
+    np.add.at(y, rows, np.einsum("kab,kb->ka", blocks, xb[ci]))
+    return y.reshape(-1)
+
+
+@pytest.mark.parametrize("maker", [lambda: gen.hex_euler(12), lambda: gen.hex_coupled(12, poly_seed=2)])
+def test_block_jacobi_vcycle_against_numpy(ctx, maker):
+    """Two-level V-cycle of Mode.PERF_JACOBI against a numpy restatement:
+    z = w D^-1 r, res = r - A z, z += P A_c^-1 R res, z += w D^-1 (r - A z)
+    (w = 0.8; D the diagonal blocks; R/P the aggregate sum/injection)."""
+    s = maker()
+    A = s.A
+    n = A.n
+    ctx.set_topology(A)
+    ctx.upload_ldu(A)
+    ctx.precond_setup(bcs.SolverConfig(preconditioner=bcs.PrecondKind.AMG, mode=bcs.Mode.PERF_JACOBI,
+                                       amg=bcs.AmgConfig(maxLevels=2, minCoarseRows=8)))
+    assert ctx.amg_depth() == 2
+    ro, ci, v, agg = ctx.amg_level(0, n)
+    cro, cci, cv, _ = ctx.amg_level(1, n)
+    assert ro.size - 1 > 512  # above the one-CTA tail: smoothed by block Jacobi
+    r = np.random.default_rng(5).uniform(-1, 1, A.n_cells * n)
+    z = ctx.precond_apply(r)
+
+    rows = np.repeat(np.arange(ro.size - 1), np.diff(ro))
+    D = v.reshape(-1, n, n)[ci == rows]  # one diagonal block per row, in row order
+    def smooth(x):
+        return 0.8 * np.linalg.solve(D, x.reshape(-1, n, 1)).reshape(-1)
+    zn = smooth(r)
+    res = r - _bsr_matvec(ro, ci, v, n, zn)
+    nc = cro.size - 1
+    rc = np.zeros((nc, n))
+    np.add.at(rc, agg, res.reshape(-1, n))
+    Ac = np.zeros((nc * n, nc * n))
+    crows = np.repeat(np.arange(nc), np.diff(cro))
+    for k, (i, j) in enumerate(zip(crows, cci)):
+        Ac[i * n:(i + 1) * n, j * n:(j + 1) * n] = cv.reshape(-1, n, n)[k]
+    ec = np.linalg.solve(Ac, rc.reshape(-1)).reshape(-1, n)
+    zn = zn + ec[agg].reshape(-1)
+    zn = zn + smooth(r - _bsr_matvec(ro, ci, v, n, zn))
+    np.testing.assert_allclose(z, zn, rtol=0, atol=1e-10 * np.abs(zn).max())
