@@ -178,6 +178,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* m = std::getenv("BCS_TAIL_ROWS")) tailMaxRows_ = std::atoi(m);
     if (const char* m = std::getenv("BCS_DENSE_TILED_MIN")) denseTiledMin_ = std::atoi(m);
     if (const char* m = std::getenv("BCS_MC_SWEEP")) mcSweep_ = std::atoi(m) != 0;
+    if (const char* m = std::getenv("BCS_MC_LAUNCH_MIN")) mcLaunchMin_ = std::atoi(m);
     if (const char* m = std::getenv("BCS_JACOBI_OMEGA")) jacobiOmega_ = std::atof(m);
     check(cudaSetDevice(device), "cudaSetDevice");
     check(cudaStreamCreateWithFlags(&own_, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -1175,7 +1176,9 @@ bool Engine::buildColoured(Level& L) {
     L.mcColorOffD.ensure(L.mcColorOff.size(), stream_);
     check(cudaMemcpyAsync(L.mcColorOffD.p, L.mcColorOff.data(), sizeof(int) * L.mcColorOff.size(),
                           cudaMemcpyHostToDevice, stream_), "H2D colour offsets");
-    M.colourSweep = mcSweep_;
+    // big levels: one streaming launch per colour (k_mc_colour); small ones
+    // keep the sync-free sweeps (a DAG #colours deep) in one launch each way
+    M.colourSweep = mcSweep_ || (mcLaunchMin_ > 0 && R >= static_cast<long long>(mcLaunchMin_) * L.ncolors);
     M.rows = R;
     M.nnz = L.nnz;
     M.o_ro.ensure(static_cast<size_t>(R) + 1, stream_);
@@ -1305,14 +1308,28 @@ void Engine::smootherApply(Level& L, const double* r, double* z, int accumulate)
             const double nb = static_cast<double>(n_), R = static_cast<double>(M.rows);
             const double per = 0.5 * (static_cast<double>(M.nnz) - R) * (8.0 * nb * nb + 4.0) +
                                R * (8.0 * nb * nb + 8.0 * nb + 4.0 * nb + 12.0) + 2.0 * R * 8.0 * nb;
-            if (kernelTiming_) timerBegin();
-            mc_sweep(n_, true, M.rows, L.ncolors, L.mcColorOffD, M.ro, M.dg, M.ci, M.v, M.lu, M.rcp, M.perm, M.r,
-                     M.y.p, stream_);
-            if (kernelTiming_) timerEnd(1, per);
-            if (kernelTiming_) timerBegin();
-            mc_sweep(n_, false, M.rows, L.ncolors, L.mcColorOffD, M.ro, M.dg, M.ci, M.v, M.lu, M.rcp, M.perm, M.y,
-                     M.zb.p, stream_);
-            if (kernelTiming_) timerEnd(1, per);
+            if (mcSweep_) {  // opt-in: one cooperative kernel, a grid barrier per colour
+                if (kernelTiming_) timerBegin();
+                mc_sweep(n_, true, M.rows, L.ncolors, L.mcColorOffD, M.ro, M.dg, M.ci, M.v, M.lu, M.rcp, M.perm, M.r,
+                         M.y.p, stream_);
+                if (kernelTiming_) timerEnd(1, per);
+                if (kernelTiming_) timerBegin();
+                mc_sweep(n_, false, M.rows, L.ncolors, L.mcColorOffD, M.ro, M.dg, M.ci, M.v, M.lu, M.rcp, M.perm, M.y,
+                         M.zb.p, stream_);
+                if (kernelTiming_) timerEnd(1, per);
+            } else {  // one streaming launch per colour
+                const auto& co = L.mcColorOff;
+                if (kernelTiming_) timerBegin();
+                for (int c = 0; c < L.ncolors; ++c)
+                    mc_colour_sweep(n_, true, co[c], co[c + 1], M.ro, M.dg, M.ci, M.v, M.lu, M.rcp, M.perm, M.r,
+                                    M.y.p, stream_);
+                if (kernelTiming_) timerEnd(1, per);
+                if (kernelTiming_) timerBegin();
+                for (int c = L.ncolors - 1; c >= 0; --c)
+                    mc_colour_sweep(n_, false, co[c], co[c + 1], M.ro, M.dg, M.ci, M.v, M.lu, M.rcp, M.perm, M.y,
+                                    M.zb.p, stream_);
+                if (kernelTiming_) timerEnd(1, per);
+            }
         } else {
             smootherApply(M, M.r, M.zb.p, 0);
         }

@@ -388,6 +388,7 @@ private:
     int tailMaxRows_ = kTailMaxRows;          // levels at most this big run in the one-CTA tail (0: off)
     int denseTiledMin_ = 2048;                // coarsest m from which the backward solve is tiled (non-EXACT)
     bool mcSweep_ = false;                    // perf mode: colour-synchronous sweeps (BCS_MC_SWEEP=1; measured slower)
+    int mcLaunchMin_ = 16384;  // performance mode: rows per colour (mean) for one launch per colour
     double jacobiOmega_ = 0.8;                // block-Jacobi damping (of 0.8 / 0.9 / 1.0: 18 / 22 / 94 its at 128^3); BCS_JACOBI_OMEGA
     void denseSolve(const double* r, double* z);
     int* hTot_ = nullptr;                     // pinned: per-level sweep program sizes

@@ -350,6 +350,160 @@ __global__ void __launch_bounds__(256) k_mc_sweep(int ncol, const int* __restric
     }
 }
 
+// ---- performance mode: one colour per launch -------------------------------
+// Rows of one colour are independent, so a colour is a streaming pass: warps
+// take G = 32/N rows (N lanes each, lane q = component q), issue the loads of
+// up to kMcDeps dependency rows at once (block row q of A_ij from HBM, y_j[q]
+// from the earlier colours' results), then fold them in slot order and solve
+// with the row's LU -- the operation sequence of the sync-free sweeps, so the
+// result is bit-identical to them.  Kernel boundaries order the colours.
+constexpr int kMcDeps = 3;
+constexpr int kMcWarps = 8;  // warps per CTA
+
+__device__ __forceinline__ unsigned mc_smem(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+// TMA bulk copy of [src, src + bytes) widened to 16-byte bounds into dst;
+// returns the byte offset of src inside dst.  Caller counts the bytes.
+__device__ __forceinline__ unsigned mc_bulk(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                            unsigned* tx) {
+    const unsigned long long s0 = reinterpret_cast<unsigned long long>(src);
+    const unsigned long long lo = s0 & ~15ull, hi = (s0 + bytes + 15ull) & ~15ull;
+    const unsigned len = static_cast<unsigned>(hi - lo);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(mc_smem(dst)),
+        "l"(lo), "r"(len), "r"(mc_smem(bar))
+        : "memory");
+    *tx += len;
+    return static_cast<unsigned>(s0 - lo);
+}
+
+template <int N, bool FWD>
+__global__ void __launch_bounds__(256, 3) k_mc_colour(int i0, int i1, const int* __restrict__ ro,
+                                                   const int* __restrict__ dg, const int* __restrict__ ci,
+                                                   const double* __restrict__ v, const double* __restrict__ lu,
+                                                   const double* __restrict__ rcp, const int* __restrict__ perm,
+                                                   const double* __restrict__ rin, double* out) {
+    constexpr int NN = N * N, G = 32 / N, RB = kMcWarps * G;  // rows per CTA
+    // the CTA's rows' factors, reciprocals and permutations (contiguous in the
+    // colour-ordered level) arrive by TMA while the warps fold their dependencies
+    __shared__ alignas(16) double slu[RB * NN + 2];
+    __shared__ alignas(16) double src_[RB * N + 2];
+    __shared__ alignas(16) int spm[RB * N + 4];
+    __shared__ alignas(8) unsigned long long bar;
+    __shared__ unsigned offs[3];
+    const int lane = threadIdx.x & 31, g = lane / N, q = lane - (lane / N) * N;
+    const int wib = threadIdx.x >> 5;
+    const int c0row = i0 + blockIdx.x * RB;
+    const int nrow = i1 - c0row < RB ? i1 - c0row : RB;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mc_smem(&bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        unsigned tx = 0;
+        const size_t r0 = static_cast<size_t>(c0row);
+        // expect_tx after the byte count is known: arrive once with the total
+        offs[0] = mc_bulk(slu, lu + r0 * NN, nrow * NN * 8, &bar, &tx);
+        offs[1] = mc_bulk(src_, rcp + r0 * N, nrow * N * 8, &bar, &tx);
+        offs[2] = mc_bulk(spm, perm + r0 * N, nrow * N * 4, &bar, &tx);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mc_smem(&bar)), "r"(tx) : "memory");
+    }
+    const int li = wib * G + g;  // row within the CTA
+    const int i = c0row + li;
+    const bool row = g < G && li < nrow;
+    const size_t ib = static_cast<size_t>(row ? i : c0row);
+    double ri = 0.0;
+    int kb = 0, cnt = 0;
+    if (row) {
+        ri = __ldg(&rin[ib * N + q]);
+        const int k0 = __ldg(&ro[ib]), kd = __ldg(&dg[ib]), k1 = __ldg(&ro[ib + 1]);
+        kb = FWD ? k0 : k1 - 1;
+        cnt = FWD ? kd - k0 : k1 - 1 - kd;
+    }
+    double acc = FWD ? ri : 0.0;
+    const int cmax = __reduce_max_sync(0xffffffffu, cnt);
+    for (int cc = 0; cc < cmax; cc += kMcDeps) {
+        double aq[kMcDeps][N], yq[kMcDeps];
+#pragma unroll
+        for (int d = 0; d < kMcDeps; ++d) {
+            const int c = cc + d;
+            const int k = FWD ? kb + c : kb - c;
+            if (c < cnt) {
+                const double* a = v + static_cast<size_t>(k) * NN + q * N;
+#pragma unroll
+                for (int p = 0; p < N; ++p) aq[d][p] = __ldcs(&a[p]);
+                yq[d] = __ldcg(&out[static_cast<size_t>(__ldg(&ci[k])) * N + q]);
+            } else {
+#pragma unroll
+                for (int p = 0; p < N; ++p) aq[d][p] = 0.0;
+                yq[d] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int d = 0; d < kMcDeps; ++d) {
+            double sblk = 0.0;
+#pragma unroll
+            for (int p = 0; p < N; ++p)
+                sblk = __dadd_rn(sblk, __dmul_rn(aq[d][p], __shfl_sync(0xffffffffu, yq[d], g * N + p)));
+            if (cc + d < cnt) acc = FWD ? __dsub_rn(acc, sblk) : __dadd_rn(acc, sblk);
+        }
+    }
+    __syncthreads();  // barrier initialised and offsets published
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+        "@!p bra W;\n\t}" ::"r"(mc_smem(&bar))
+        : "memory");
+    const double* L = reinterpret_cast<const double*>(reinterpret_cast<const unsigned char*>(slu) + offs[0]) +
+                      (row ? li : 0) * NN;
+    const double* rc = reinterpret_cast<const double*>(reinterpret_cast<const unsigned char*>(src_) + offs[1]) +
+                       (row ? li : 0) * N;
+    const int* pm = reinterpret_cast<const int*>(reinterpret_cast<const unsigned char*>(spm) + offs[2]) +
+                    (row ? li : 0) * N;
+    // composed pivot permutation, then the row's LU solve (every lane of the row)
+    double x[N];
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+        const int sl = row ? g * N + pm[p] : lane;
+        x[p] = __shfl_sync(0xffffffffu, acc, sl);
+    }
+    if (!row) return;
+    DVec<N> xin;
+#pragma unroll
+    for (int p = 0; p < N; ++p) xin.v[p] = x[p];
+    if (__builtin_expect(!lu_solve_perm_fast<N>(L, rc, x), 0)) {
+        const DVec<N> xe = lu_solve_perm_exact<N>(lu + ib * NN, xin);
+#pragma unroll
+        for (int p = 0; p < N; ++p) x[p] = xe.v[p];
+    }
+    double mine = x[0];
+#pragma unroll
+    for (int p = 1; p < N; ++p) mine = (q == p) ? x[p] : mine;
+    out[ib * N + q] = FWD ? mine : __dsub_rn(ri, mine);
+}
+
+void mc_colour_sweep(int n, bool fwd, int i0, int i1, const int* ro, const int* dg, const int* ci, const double* v,
+                     const double* lu, const double* rcp, const int* perm, const double* rin, double* out,
+                     cudaStream_t s) {
+    if (i1 <= i0) return;
+    const long long rb = static_cast<long long>(kMcWarps) * (32 / n);  // rows per CTA
+    const unsigned g = static_cast<unsigned>((static_cast<long long>(i1 - i0) + rb - 1) / rb);
+    switch (n) {
+#define BCS_MCC_CASE(NV)                                                                                        \
+    case NV:                                                                                                    \
+        if (fwd) k_mc_colour<NV, true><<<g, 256, 0, s>>>(i0, i1, ro, dg, ci, v, lu, rcp, perm, rin, out);      \
+        else k_mc_colour<NV, false><<<g, 256, 0, s>>>(i0, i1, ro, dg, ci, v, lu, rcp, perm, rin, out);         \
+        break;
+        BCS_MCC_CASE(1)
+        BCS_MCC_CASE(2)
+        BCS_MCC_CASE(3)
+        BCS_MCC_CASE(4)
+        BCS_MCC_CASE(5)
+#undef BCS_MCC_CASE
+        default: throw std::invalid_argument("block size must be 1..5 on the device");
+    }
+    count_launch();
+}
+
 // ---- performance mode, block-Jacobi smoothing ------------------------------
 // out_i = omega * D_i^-1 r_i per block row (the diagonal block's LU with the
 // composed pivot permutation and reciprocal-based division, as the sweeps),

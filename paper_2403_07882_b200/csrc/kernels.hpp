@@ -54,6 +54,12 @@ void mc_vec_scatter(int n, int rows, const int* perm, const double* sp, double* 
 void block_jacobi(int n, int rows, const double* lu, const double* rcp, const int* perm, const double* r, double* z,
                   int acc, double omega, cudaStream_t s);
 // colour-synchronous DILU sweep of a coloured level (coff: device, ncol + 1 colour boundaries)
+// performance mode: one colour [i0, i1) of the colour-permuted level as a
+// streaming pass (rows of a colour are independent); forward colours in
+// increasing order, backward in decreasing order, one launch each
+void mc_colour_sweep(int n, bool fwd, int i0, int i1, const int* ro, const int* dg, const int* ci, const double* v,
+                     const double* lu, const double* rcp, const int* perm, const double* rin, double* out,
+                     cudaStream_t s);
 void mc_sweep(int n, bool fwd, int rows, int ncol, const int* coff, const int* ro, const int* dg, const int* ci,
               const double* v, const double* lu, const double* rcp, const int* perm, const double* rin, double* out,
               cudaStream_t s);

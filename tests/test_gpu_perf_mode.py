@@ -48,6 +48,9 @@ def permuted_ldu(A, perm):
 
 SYSTEMS = {
     "euler8": lambda: gen.hex_euler(8).A,
+    # >= 16384 rows per colour: one streaming launch per colour (k_mc_colour)
+    "euler56": lambda: gen.hex_euler(56).A,
+    "coupled56p": lambda: gen.hex_coupled(56, poly_seed=2).A,
     "euler7s": lambda: gen.hex_euler(7, scramble_seed=3).A,
     "coupled7p": lambda: gen.hex_coupled(7, poly_seed=2).A,
     "rand4": lambda: random_system(9, 7, 6, 4, 5)[0],
@@ -63,6 +66,8 @@ def test_perf_dilu_is_the_natural_dilu_of_the_colour_permuted_matrix(ctx, oracle
     ctx.precond_setup(bcs.SolverConfig(preconditioner=bcs.PrecondKind.DILU, mode=bcs.Mode.PERF))
     ncol, perm, off = ctx.level_coloring(0)
     assert 2 <= ncol <= 64
+    if name.endswith("56") or name.endswith("56p"):
+        assert A.n_cells >= 16384 * ncol  # one launch per colour (engine mcLaunchMin_)
     r = np.random.default_rng(7).uniform(-1, 1, A.n_cells * A.n)
     z = ctx.precond_apply(r)
     P = permuted_ldu(A, perm)
