@@ -541,12 +541,19 @@ def run_ours(args):
                                  "note": "cudaMemGetInfo after the timed steps: solver pools (hierarchy, sweep programs, "
                                          "DILU scratch, Krylov basis) + the bench's device-resident LDU inputs"},
             "roofline": {"bound": "hbm", "achieved": sw_achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (sw_achieved / peak) if sw_achieved else None, "traffic": sweep_traffic(n) if default_workload(args) else None,
-                         "kernel": f"k_sweep*<{nb},*> (DILU smoother sweeps, all swept AMG levels)",
+                         "frac": (sw_achieved / peak) if sw_achieved else None,
+                         "traffic": sweep_traffic(n) if default_workload(args) and args.mode in ("parity", "exact") else None,
+                         "kernel": {"perf": f"k_mc_colour<{nb},*> (one launch per colour) + k_sweep*<{nb},*> on the "
+                                            "colour-permuted levels (multicolour DILU smoother, all smoothed levels)",
+                                    "jacobi": f"k_block_jacobi<{nb}> (block-Jacobi smoother, levels above the one-CTA tail)"
+                                    }.get(args.mode, f"k_sweep*<{nb},*> (DILU smoother sweeps, all swept AMG levels)"),
                          "bytes_per_launch": (sw_bytes / sw_n) if sw_n else None,
                          "mean_launch_ms": (sw_ms / sw_n) if sw_n else None, "launches_per_step": sw_n / len(preps),
                          "share_of_step": sw_share, "peak_kind": peak_kind,
-                         "note": "dependency-latency bound (level depth x hop latency), see DESIGN.md", "latency": latency},
+                         "note": {"perf": "streaming per colour on the big levels; small levels launch-latency bound",
+                                  "jacobi": "HBM streaming (TMA-staged rows); small levels launch-latency bound"
+                                  }.get(args.mode, "dependency-latency bound (level depth x hop latency), see DESIGN.md"),
+                         "latency": latency},
             "roofline_spmv": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                               "frac": achieved / peak, "traffic": traffic, "kernel": f"k_spmv<{nb}> (fine level)",
                               "bytes_per_launch": bytes_per, "mean_launch_ms": spmv_ms, "peak_kind": peak_kind},
