@@ -227,7 +227,7 @@ Engine::~Engine() {
     rel(scanTmp_); rel(dkeys_); rel(dorder_); rel(ddesc_); rel(act2_); rel(flag_); rel(err_); rel(ctr_); rel(choice_); rel(segOff_); rel(cro_); rel(big_); rel(dn_); rel(tblk_);
     rel(str_); rel(keys_); rel(sorted_); rel(V_); rel(w_); rel(zk_); rel(rk_); rel(Hm_); rel(cs_); rel(sn_); rel(g_);
     rel(y_); rel(scal_); rel(partials_); rel(kb_); rel(kx_); rel(bp_); rel(bv_); rel(bs_); rel(bt_); rel(bph_);
-    rel(bsh_); rel(brh_); rel(ticket_); rel(seg_); rel(distTmp_); rel(mcSv_); rel(chunkOrd_); rel(chainCnt_);
+    rel(bsh_); rel(brh_); rel(ticket_); rel(seg_); rel(distTmp_); rel(mcSv_); rel(chunkOrd_); rel(chainCnt_); rel(partOrd_);
     for (auto& P : dist_) {
         rel(P.ro); rel(P.ci); rel(P.src); rel(P.dg); rel(P.tpos); rel(P.vals); rel(P.hrow); rel(P.hoff);
         rel(P.hcol); rel(P.hsrc); rel(P.hvals);
@@ -919,6 +919,11 @@ void Engine::finishSmoothers(const std::vector<Level*>& lv, const bcs_solver_con
                 if (lv[k]->chain) at += 2 * static_cast<size_t>(lv[k]->rows);
             sweep_records(L.rows, chunkOrd_.p + at, chunkOrd_.p + at + L.rows, L.ro, L.dg, L.recf.p, L.recb.p,
                           stream_);
+        } else if (const int G = sweep_cluster_parts(n_, L.rows, L.depth); G > 1) {
+            // several clusters: tickets range-major (each cluster's rows in level order)
+            partOrd_.ensure(static_cast<size_t>(L.rows), stream_);
+            cluster_part_order(L.rows, G, L.order, partOrd_.p, stream_);
+            sweep_records(L.rows, partOrd_.p, nullptr, L.ro, L.dg, L.recf.p, L.recb.p, stream_);
         } else {
             sweep_records(L.rows, L.order, nullptr, L.ro, L.dg, L.recf.p, L.recb.p, stream_);
         }
@@ -2539,7 +2544,7 @@ std::string Engine::memoryReport() const {
         add("assembly", *a);
     for (const auto* a : {&asmInv_, &asmCfo_, &asmCf_, &asmBco_, &asmBkind_, &asmBad_}) add("assembly", *a);
     for (const auto* a : {&cnt_, &lvl_, &act2_, &push_, &scanTmp_, &flag_, &err_, &ctr_, &choice_, &segOff_, &cro_,
-                          &big_, &dkeys_, &dorder_, &ticket_, &chunkOrd_, &chainCnt_})
+                          &big_, &dkeys_, &dorder_, &ticket_, &chunkOrd_, &chainCnt_, &partOrd_})
         add("setup_scratch", *a);
     add("setup_scratch", dn_); add("setup_scratch", str_); add("setup_scratch", keys_); add("setup_scratch", sorted_);
     add("setup_scratch", ddesc_);

@@ -334,6 +334,7 @@ private:
     Hier* H_ = &main_;
     // scratch
     DArray<int> chunkOrd_, chainCnt_;  // chain schedules: orders, chain counts / check flags
+    DArray<int> partOrd_;              // cluster variant over several clusters: range-major order
     DArray<int> cnt_, lvl_, act2_, push_, scanTmp_, flag_, err_, ctr_, choice_, segOff_, cro_, big_;
     DArray<double> dn_, str_, tblk_;
     DArray<int> dkeys_, dorder_;       // combined DILU tickets

@@ -136,6 +136,11 @@ void sweep_records(int rows, const int* order, const int* border, const int* ro,
 // *bad |= 1 when the schedule's progress check fails on this pattern.
 // Launch the level's sweeps with depth = -1 and woff.
 int sweep_chunk_warps(int n, bool fwd);
+// cluster variant spread over G > 1 clusters: the level's rows must be
+// ticketed range-major (rows/G contiguous row ranges, each in level order):
+// out = order stably sorted by range.  G = 0: not the cluster variant.
+int sweep_cluster_parts(int n, int rows, int depth);
+void cluster_part_order(int rows, int G, const int* order, int* out, cudaStream_t s);
 void chain_schedule(int rows, bool fwd, int depth, const int* ro, const int* dg, const int* ci, const int* dlev, int W,
                     int* order, int* woff, int* bad, cudaStream_t s);
 void chain_count(int rows, const int* ro, const int* dg, const int* ci, int* cnt, cudaStream_t s);
