@@ -79,6 +79,12 @@ public:
     SolvePipeline(const SolvePipeline&) = delete;
     SolvePipeline& operator=(const SolvePipeline&) = delete;
 
+    // execution mode of the following solves (bcs_solver_config.mode:
+    // BCS_MODE_PARITY default, BCS_MODE_EXACT, BCS_MODE_PERF, BCS_MODE_PERF_JACOBI);
+    // the reference's SolverConfig has no such field
+    void setMode(int mode) { mode_ = mode; }
+    int mode() const { return mode_; }
+
     template <class Report, class Matrix, class Vector, class Backend, class Config>
     std::pair<Vector, Report> solve(const Matrix& A, const Vector& b, const Vector& x0, Backend backend,
                                     const Config& cfg) {
@@ -99,7 +105,8 @@ public:
             mesh_ = mesh;
         }
         Vector x(A.nCells(), A.blockSize());
-        const bcs_solver_config c = toC(cfg);
+        bcs_solver_config c = toC(cfg);
+        c.mode = mode_;
         bcs_report r{};
         const int be = static_cast<int>(backend);
         const bcs_status st = bcs_pipeline_solve(
@@ -135,7 +142,8 @@ public:
             c[3 * i + 2] = cen[i].z;
         }
         Vector x(A.nCells(), A.blockSize());
-        const bcs_solver_config cc = toC(cfg);
+        bcs_solver_config cc = toC(cfg);
+        cc.mode = mode_;
         bcs_report r{};
         const bcs_status st = bcs_dist_solve(ctx_, A.nCells(), nf, A.blockSize(), own.data(), nei.data(), c.data(),
                                              A.diagValues().data(), A.upperValues().data(), A.lowerValues().data(),
@@ -260,7 +268,8 @@ public:
     template <class Report, class Vector, class Config>
     std::pair<Vector, Report> solveAssembled(const Vector& b, const Vector& x0, const Config& cfg) {
         Vector x = x0;
-        const bcs_solver_config c = toC(cfg);
+        bcs_solver_config c = toC(cfg);
+        c.mode = mode_;
         bcs_report r{};
         const bcs_status st = bcs_solve(ctx_, b.values.data(), x.values.data(), &c, &r);
         if (st != BCS_OK) throwStatus(st, bcs_last_error(ctx_));
@@ -271,6 +280,7 @@ public:
 
 private:
     bcs_ctx* ctx_ = nullptr;
+    int mode_ = BCS_MODE_PARITY;
     const void* mesh_ = nullptr;
     std::vector<int32_t> owner_, neigh_;
 };

@@ -16,3 +16,27 @@ def test_dropin_with_reference_types():
     print(p.stdout)
     assert p.returncode == 0, p.stdout + p.stderr
     assert "PASSED" in p.stdout
+
+
+RUNCASE = os.path.join(ROOT, "oracle", "_ref", "runcase_test")
+
+
+@pytest.mark.skipif(not os.path.exists(RUNCASE), reason="oracle/_ref/runcase_test not built (reference absent at build)")
+def test_runcase_with_b200_pipeline_interposed(parity_log):
+    """fvb::runCase unchanged, its LinearDispatch's SolvePipeline::solve routed
+    to the B200 pipeline at link time (tests/cpp/runcase_main.cpp): 200
+    nonlinear iterations of the coupled cavity and the implicit Sod tube,
+    EXACT mode bit-identical to the reference, PARITY mode within 1e-6."""
+    p = subprocess.run([RUNCASE], capture_output=True, text=True, timeout=1800)
+    print(p.stdout)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "PASSED" in p.stdout
+    import re
+    for line in p.stdout.splitlines():
+        m = re.match(r"summary (\S+): exact maxResidualDelta (\S+) \| parity maxResidualRelDelta (\S+) "
+                     r"maxResidualDelta (\S+) worst coefficient delta (\S+)", line)
+        if m:
+            parity_log("runCase " + m.group(1) + " 200 nonlinear its (EngineCsr/AMG)",
+                       dict(max_rel_dev=float(m.group(3)), exact_max_delta=float(m.group(2)),
+                            max_abs_dev=float(m.group(4)), worst_coef_rel_dev=float(m.group(5)),
+                            exact_bit_identical=float(m.group(2)) == 0.0))
