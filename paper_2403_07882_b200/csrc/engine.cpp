@@ -795,6 +795,7 @@ void Engine::diluSetupAll(const std::vector<Level*>& lv, const bcs_solver_config
                      PhaseArena::al(sizeof(int) * static_cast<size_t>(L.nnz));
             totalT += (static_cast<size_t>(L.nnz) - L.rows) / 2 * nn;
         }
+        dropArenaViews();
         H_->arena.reserve(bytes + PhaseArena::al(sizeof(double) * (totalT + 1)), stream_);
         for (int l = 0; l < nl; ++l) {
             Level& L = *lv[l];
@@ -830,6 +831,15 @@ void Engine::diluSetupAll(const std::vector<Level*>& lv, const bcs_solver_config
         throw std::runtime_error("DILU setup: singular modified diagonal in cell " + std::to_string(cell & ((1 << 26) - 1)));
     profMark("dilu:factor");
     finishSmoothers(lv, cfg);
+}
+
+// Engine-level arrays that borrow arena memory (the serial Krylov basis, the
+// DILU scratch T) are views of the phase they were taken in: a new reserve
+// recycles that memory, so the views are dropped first and the next ensure()
+// allocates (e.g. a LUSGS setup after an AMG solve on the same context).
+void Engine::dropArenaViews() {
+    for (auto* a : {&V_, &Z_, &tblk_})
+        if (!a->owned) a->release(stream_);
 }
 
 // reciprocals, composed permutations, ticket records and packed slots of
@@ -949,6 +959,7 @@ void Engine::finishSmoothers(const std::vector<Level*>& lv, const bcs_solver_con
     const size_t nV = basis ? static_cast<size_t>(cfg->gmres_restart + 1) * N : 0;
     const size_t nZ = basis && cfg->method == BCS_FGMRES ? static_cast<size_t>(cfg->gmres_restart) * N : 0;
     if (basis) bytes += PhaseArena::al(nV * sizeof(double)) + (nZ ? PhaseArena::al(nZ * sizeof(double)) : 0);
+    dropArenaViews();
     H_->arena.reserve(bytes, stream_);
     if (basis) {
         V_.borrow(H_->arena.take<double>(nV), nV, stream_);

@@ -250,6 +250,7 @@ private:
     void buildHierarchy(const bcs_solver_config& cfg);
     void setupLevelPattern(Level& L);
     void diluSetupAll(const std::vector<Level*>& lv, const bcs_solver_config* cfg);
+    void dropArenaViews();
     void finishSmoothers(const std::vector<Level*>& lv, const bcs_solver_config* cfg);
     // performance mode: the colour-permuted copy of L the smoother runs on
     // (k_color.cu), or L itself when the colouring is not possible

@@ -1,0 +1,55 @@
+// Link-time interposition of fvb::SolvePipeline::solve (TEST INFRASTRUCTURE
+// and the zero-source-change integration recipe of INTEGRATION.md).
+//
+// Linked with -Wl,--wrap=<mangled fvb::SolvePipeline::solve> next to the
+// reference's objects, every call another reference object makes to
+// SolvePipeline::solve (engine.cpp:47-120) -- LinearDispatch's serial branch
+// in runCase (case_runner.cpp:333) above all -- lands here and runs on the
+// B200 pipeline (include/bcs.hpp); one bcs::SolvePipeline per reference
+// pipeline object keeps its setup-vs-replace state.
+//   bcs_interpose_route: -1 the reference's own solve (__real_), else the
+//   BCS_MODE_* of the B200 solve; initialised from $BCS_INTERPOSE
+//   (off | parity | exact; default parity).
+#include "blockfv/engine.hpp"
+
+#include "../../include/bcs.hpp"
+
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+
+using SolveResult = std::pair<fvb::BlockVector, fvb::SolveReport>;
+
+extern "C" SolveResult
+__real__ZN3fvb13SolvePipeline5solveERKNS_14BlockLduMatrixERKNS_11BlockVectorES6_NS_7BackendERKNS_12SolverConfigE(
+    fvb::SolvePipeline* self, const fvb::BlockLduMatrix& A, const fvb::BlockVector& b, const fvb::BlockVector& x0,
+    fvb::Backend backend, const fvb::SolverConfig& cfg);
+
+static int route_from_env() {
+    const char* e = std::getenv("BCS_INTERPOSE");
+    if (!e || !std::strcmp(e, "parity")) return BCS_MODE_PARITY;
+    if (!std::strcmp(e, "exact")) return BCS_MODE_EXACT;
+    if (!std::strcmp(e, "off")) return -1;
+    return BCS_MODE_PARITY;
+}
+
+extern "C" {
+int bcs_interpose_route = route_from_env();
+long bcs_interpose_calls = 0;  // solves that ran on the B200
+}
+
+extern "C" SolveResult
+__wrap__ZN3fvb13SolvePipeline5solveERKNS_14BlockLduMatrixERKNS_11BlockVectorES6_NS_7BackendERKNS_12SolverConfigE(
+    fvb::SolvePipeline* self, const fvb::BlockLduMatrix& A, const fvb::BlockVector& b, const fvb::BlockVector& x0,
+    fvb::Backend backend, const fvb::SolverConfig& cfg) {
+    if (bcs_interpose_route < 0)
+        return __real__ZN3fvb13SolvePipeline5solveERKNS_14BlockLduMatrixERKNS_11BlockVectorES6_NS_7BackendERKNS_12SolverConfigE(
+            self, A, b, x0, backend, cfg);
+    static std::map<const fvb::SolvePipeline*, std::unique_ptr<bcs::SolvePipeline>> pipes;
+    auto& p = pipes[self];
+    if (!p) p = std::make_unique<bcs::SolvePipeline>(0);
+    p->setMode(bcs_interpose_route);
+    ++bcs_interpose_calls;
+    return p->solve<fvb::SolveReport>(A, b, x0, backend, cfg);
+}

@@ -4,7 +4,8 @@
 // with its LinearDispatch (case_runner.cpp:322-353) -- runs unchanged; only
 // the serial branch's call into fvb::SolvePipeline::solve (case_runner.cpp:333)
 // is routed to the B200 pipeline, by link-time interposition
-// (-Wl,--wrap=<that symbol>, oracle/Makefile): no reference source is touched,
+// (-Wl,--wrap=<that symbol> + tests/cpp/pipeline_interpose.cpp, oracle/Makefile):
+// no reference source is touched,
 // which is exactly the one-symbol swap INTEGRATION.md describes.
 //
 // Checks, in the style of the reference's acceptance criterion 2
@@ -24,38 +25,13 @@
 
 #include <cmath>
 #include <cstdio>
-#include <map>
-#include <memory>
 #include <string>
 
 using namespace fvb;
-using SolveResult = std::pair<BlockVector, SolveReport>;
 
-// the reference's definition (engine.cpp:47-120) and our replacement of it
-extern "C" SolveResult
-__real__ZN3fvb13SolvePipeline5solveERKNS_14BlockLduMatrixERKNS_11BlockVectorES6_NS_7BackendERKNS_12SolverConfigE(
-    SolvePipeline* self, const BlockLduMatrix& A, const BlockVector& b, const BlockVector& x0, Backend backend,
-    const SolverConfig& cfg);
-
-static int g_route = -1;  // -1: the reference's pipeline; else the B200 pipeline in this BCS_MODE_*
-static std::map<const SolvePipeline*, std::unique_ptr<bcs::SolvePipeline>> g_pipes;
-static long g_gpu_calls = 0;
-
-extern "C" SolveResult
-__wrap__ZN3fvb13SolvePipeline5solveERKNS_14BlockLduMatrixERKNS_11BlockVectorES6_NS_7BackendERKNS_12SolverConfigE(
-    SolvePipeline* self, const BlockLduMatrix& A, const BlockVector& b, const BlockVector& x0, Backend backend,
-    const SolverConfig& cfg) {
-    if (g_route < 0)
-        return __real__ZN3fvb13SolvePipeline5solveERKNS_14BlockLduMatrixERKNS_11BlockVectorES6_NS_7BackendERKNS_12SolverConfigE(
-            self, A, b, x0, backend, cfg);
-    // one B200 pipeline per reference pipeline object: the setup-vs-replace
-    // state of LinearDispatch's stateful pipeline carries over
-    auto& p = g_pipes[self];
-    if (!p) p = std::make_unique<bcs::SolvePipeline>(0);
-    p->setMode(g_route);
-    ++g_gpu_calls;
-    return p->solve<SolveReport>(A, b, x0, backend, cfg);
-}
+// tests/cpp/pipeline_interpose.cpp: the __wrap_ of fvb::SolvePipeline::solve
+extern "C" int bcs_interpose_route;
+extern "C" long bcs_interpose_calls;
 
 static int g_fail = 0;
 static void check(bool ok, const std::string& what) {
@@ -92,11 +68,12 @@ static CaseConfig engineAmg(CaseConfig c) {
 }
 
 static RunReport run(const CaseConfig& cfg, int route) {
-    g_route = route;
-    const long before = g_gpu_calls;
+    bcs_interpose_route = route;
+    const long before = bcs_interpose_calls;
     RunReport r = runCase(cfg);
-    if (route >= 0) check(g_gpu_calls - before >= 200, cfg.name + ": runCase's linear solves went through the B200 pipeline");
-    g_route = -1;
+    if (route >= 0)
+        check(bcs_interpose_calls - before >= 200, cfg.name + ": runCase's linear solves went through the B200 pipeline");
+    bcs_interpose_route = -1;
     return r;
 }
 
