@@ -11,3 +11,9 @@ for mode in parity exact off; do
     echo "$mode  ($(( (e - s) / 1000000 )) ms)  $out"
   done
 done
+# the reference's own unit tests (proj/tests/test_*.cpp) with the same interposition
+for mode in parity exact off; do
+  BCS_INTERPOSE=$mode timeout 1200 ./oracle/_ref/unit_tests_b200 > gpurun_out/unit_$mode.log 2>&1
+  echo "unit tests $mode rc=$?: $(tail -1 gpurun_out/unit_$mode.log)"
+  grep "^FAIL" gpurun_out/unit_$mode.log | head -20
+done

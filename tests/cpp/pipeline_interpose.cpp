@@ -6,7 +6,9 @@
 // SolvePipeline::solve (engine.cpp:47-120) -- LinearDispatch's serial branch
 // in runCase (case_runner.cpp:333) above all -- lands here and runs on the
 // B200 pipeline (include/bcs.hpp); one bcs::SolvePipeline per reference
-// pipeline object keeps its setup-vs-replace state.
+// pipeline object keeps its setup-vs-replace state.  fvb::backendSolve (the
+// one-shot wrapper, engine.cpp:123-129) is interposed the same way with a
+// fresh pipeline per call.
 //   bcs_interpose_route: -1 the reference's own solve (__real_), else the
 //   BCS_MODE_* of the B200 solve; initialised from $BCS_INTERPOSE
 //   (off | parity | exact; default parity).
@@ -14,6 +16,7 @@
 
 #include "../../include/bcs.hpp"
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -39,6 +42,11 @@ int bcs_interpose_route = route_from_env();
 long bcs_interpose_calls = 0;  // solves that ran on the B200
 }
 
+// the count goes to stderr at exit, so a caller can tell the B200 really ran
+static struct ReportAtExit {
+    ~ReportAtExit() { std::fprintf(stderr, "bcs interpose: %ld solves on the B200\n", bcs_interpose_calls); }
+} g_report_at_exit;
+
 extern "C" SolveResult
 __wrap__ZN3fvb13SolvePipeline5solveERKNS_14BlockLduMatrixERKNS_11BlockVectorES6_NS_7BackendERKNS_12SolverConfigE(
     fvb::SolvePipeline* self, const fvb::BlockLduMatrix& A, const fvb::BlockVector& b, const fvb::BlockVector& x0,
@@ -52,4 +60,22 @@ __wrap__ZN3fvb13SolvePipeline5solveERKNS_14BlockLduMatrixERKNS_11BlockVectorES6_
     p->setMode(bcs_interpose_route);
     ++bcs_interpose_calls;
     return p->solve<fvb::SolveReport>(A, b, x0, backend, cfg);
+}
+
+extern "C" SolveResult
+__real__ZN3fvb12backendSolveERKNS_14BlockLduMatrixERKNS_11BlockVectorES5_NS_7BackendERKNS_12SolverConfigE(
+    const fvb::BlockLduMatrix& A, const fvb::BlockVector& b, const fvb::BlockVector& x0, fvb::Backend backend,
+    const fvb::SolverConfig& cfg);
+
+extern "C" SolveResult
+__wrap__ZN3fvb12backendSolveERKNS_14BlockLduMatrixERKNS_11BlockVectorES5_NS_7BackendERKNS_12SolverConfigE(
+    const fvb::BlockLduMatrix& A, const fvb::BlockVector& b, const fvb::BlockVector& x0, fvb::Backend backend,
+    const fvb::SolverConfig& cfg) {
+    if (bcs_interpose_route < 0)
+        return __real__ZN3fvb12backendSolveERKNS_14BlockLduMatrixERKNS_11BlockVectorES5_NS_7BackendERKNS_12SolverConfigE(
+            A, b, x0, backend, cfg);
+    bcs::SolvePipeline p(0);
+    p.setMode(bcs_interpose_route);
+    ++bcs_interpose_calls;
+    return p.solve<fvb::SolveReport>(A, b, x0, backend, cfg);
 }
