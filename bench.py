@@ -512,7 +512,7 @@ def run_ours(args):
             t_setup, _, rr = reference_calls(args, 0.0, 0, want_timed=False)
             cpu = {"value": t_setup, "unit": UNIT, "cores": 1, "kind": "reference",
                    "sample": f"one reference SolvePipeline::solve call (setup branch, {rr.iterations} its) on the same "
-                             f"full {workload_name(args)} system, measured (not extrapolated)",
+                             f"full {workload_name(args, system_only=True)} system, measured (not extrapolated)",
                    "host": host_record()}
         except Exception as e:  # reference lib absent
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
@@ -568,7 +568,9 @@ def default_workload(args):
     return args.system == "euler" and args.scramble < 0 and args.poly < 0 and args.aspect == 1.0
 
 
-def workload_name(args):
+def workload_name(args, system_only=False):
+    """The workload; system_only: the system alone, without our execution mode
+    (the reference's CPU solve has none)."""
     base = (f"4x4 pressure-based coupled hex {args.size}^3" if args.system == "coupled"
             else f"5x5 density-based hex {args.size}^3")
     extra = []
@@ -578,7 +580,7 @@ def workload_name(args):
         extra.append(f"aspect ratio {args.aspect:g}")
     if args.scramble >= 0:
         extra.append(f"randomly permuted cell order (seed {args.scramble})")
-    if args.mode != "parity":
+    if args.mode != "parity" and not system_only:
         extra.append({"perf": "PERFORMANCE MODE (multicolour DILU smoothing; iterations differ from the reference)",
                       "jacobi": "PERFORMANCE MODE (block-Jacobi smoothing, omega 0.8; iterations differ from the reference)",
                       "exact": "EXACT mode (the reference's sequential dot order)"}[args.mode])
