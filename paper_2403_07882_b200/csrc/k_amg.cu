@@ -534,6 +534,7 @@ __global__ void k_agg_check(int rows, const int* choice, int* out) {
 
 void aggregate_kahn(int rows, const int* ro, const int* ci, const int* dg, const int* tpos, const double* str,
                     int* choice, KahnWork w, int* err, cudaStream_t s) {
+    (void)err;
     if (rows <= 0) return;
     int* push = w.tail;  // push[3] + out[2]
     cudaMemsetAsync(push, 0, 5 * sizeof(int), s);
