@@ -23,7 +23,8 @@
  * written) during the call only.  *_device entry points take device pointers
  * on the context's device and enqueue on the context stream.
  * Threading: a context is not thread-safe (the reference solve is not
- * reentrant either).  Calls return with results valid.
+ * reentrant either); distinct contexts may be used from distinct
+ * host threads at the same time.  Calls return with results valid.
  */
 #ifndef BCS_H
 #define BCS_H

@@ -90,10 +90,13 @@ void strengths(int n, int rows, const int* ro, const int* ci, const int* dg, con
     const unsigned gb = (nnz + kStrChunk - 1) / kStrChunk;
     BCS_DISPATCH_N(n, {
         static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_strength_blk<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(sizeof(double) * kStrChunk * N * N));
-            attr = true;
+        {
+            std::lock_guard<std::recursive_mutex> lazy_lk(lazy_init_mutex());
+            if (!attr) {
+                cudaFuncSetAttribute(k_strength_blk<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(sizeof(double) * kStrChunk * N * N));
+                attr = true;
+            }
         }
         k_diag_norm<N><<<g, 256, 0, s>>>(rows, dg, v, dn);
         k_strength_blk<N><<<gb, kStrChunk, sizeof(double) * kStrChunk * N * N, s>>>(rows, nnz, ro, ci, v, dn, str);
@@ -509,6 +512,7 @@ void aggregate_syncfree(int rows, const int* ro, const int* ci, const int* dg, c
     // coarse levels (higher degree): more columns kept per row
     const bool lean = rows >= (1 << 20);
     static int cap[2] = {0, 0};
+    std::unique_lock<std::recursive_mutex> lazy_lk(lazy_init_mutex());
     if (!cap[0]) {
         int bps = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_agg_syncfree<6>, 256, 0);
@@ -516,6 +520,7 @@ void aggregate_syncfree(int rows, const int* ro, const int* ci, const int* dg, c
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_agg_syncfree<10>, 256, 0);
         cap[1] = num_sms() * (bps < 1 ? 1 : bps);
     }
+    lazy_lk.unlock();
     int g = (rows + 255) / 256;
     const int c = cap[lean ? 0 : 1];
     if (g > c) g = c;
@@ -547,9 +552,12 @@ void aggregate_kahn(int rows, const int* ro, const int* ci, const int* dg, const
         k_agg_rounds<false><<<1, 256, 0, s>>>(rows, ro, ci, dg, tpos, str, choice, w.cnt, actA, actB, push, out);
     } else {
         static int bps = 0;
-        if (!bps) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_agg_rounds<true>, 256, 0);
-            if (bps < 1) bps = 1;
+        {
+            std::lock_guard<std::recursive_mutex> lazy_lk(lazy_init_mutex());
+            if (!bps) {
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_agg_rounds<true>, 256, 0);
+                if (bps < 1) bps = 1;
+            }
         }
         int grid = num_sms() * bps;
         const int need = (rows + 7) / 8;
@@ -687,10 +695,13 @@ void galerkin_sort(int nCoarse, const int* seg_off, const unsigned long long* ke
     cudaStreamSynchronize(s);
     if (nb > 0) {
         static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kBlockSeg * static_cast<int>(sizeof(unsigned long long)));
-            attr = true;
+        {
+            std::lock_guard<std::recursive_mutex> lazy_lk(lazy_init_mutex());
+            if (!attr) {
+                cudaFuncSetAttribute(k_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kBlockSeg * static_cast<int>(sizeof(unsigned long long)));
+                attr = true;
+            }
         }
         k_sort_big<<<nb, 1024, kBlockSeg * sizeof(unsigned long long), s>>>(seg_off, keys, sorted, big, err);
         count_launch();

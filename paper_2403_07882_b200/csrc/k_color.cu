@@ -643,10 +643,13 @@ static void launch_mc_sweep(int rows, int ncol, const int* coff, const int* ro, 
                             const double* v, const double* lu, const double* rcp, const int* perm, const double* rin,
                             double* out, cudaStream_t s) {
     static int cap = 0;
-    if (!cap) {
-        int bps = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_mc_sweep<N, FWD>, 256, 0);
-        cap = num_sms() * (bps < 1 ? 1 : bps);
+    {
+        std::lock_guard<std::recursive_mutex> lazy_lk(lazy_init_mutex());
+        if (!cap) {
+            int bps = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_mc_sweep<N, FWD>, 256, 0);
+            cap = num_sms() * (bps < 1 ? 1 : bps);
+        }
     }
     constexpr int G = 32 / N;
     long long want = (static_cast<long long>(rows) / G + 63) / 64;  // ~8 row groups per warp per pass over the level

@@ -14,15 +14,24 @@
 
 namespace bcs {
 
+std::recursive_mutex& lazy_init_mutex() {
+    static std::recursive_mutex m;
+    return m;
+}
+
+
 thread_local LaunchCounter* g_launches = nullptr;
 
 int num_sms() {
     static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
+    {
+        std::lock_guard<std::recursive_mutex> lazy_lk(lazy_init_mutex());
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            if (sms <= 0) sms = 148;
+        }
     }
     return sms;
 }

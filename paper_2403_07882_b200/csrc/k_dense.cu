@@ -327,9 +327,12 @@ __global__ void k_dense_perm(int m, const int* piv, int* perm) {
 void dense_factor_blocked(int m, double* a, int* piv, int* err, cudaStream_t s) {
     static bool attr = false;
     const int smem = 2 * kDB * 64 * static_cast<int>(sizeof(double));
-    if (!attr) {
-        cudaFuncSetAttribute(k_dense_update, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
+    {
+        std::lock_guard<std::recursive_mutex> lazy_lk(lazy_init_mutex());
+        if (!attr) {
+            cudaFuncSetAttribute(k_dense_update, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            attr = true;
+        }
     }
     // cooperative panel: one CTA per SM at most, rows split evenly
     static int G = 0;
@@ -351,9 +354,12 @@ void dense_factor_blocked(int m, double* a, int* piv, int* err, cudaStream_t s) 
         const size_t psmem = sizeof(double) * static_cast<size_t>(per) * kDB;
         if (psmem <= 200 * 1024) {
             static size_t attr_p = 0;
-            if (psmem > attr_p) {
-                cudaFuncSetAttribute(k_dense_panel_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-                attr_p = 200 * 1024;
+            {
+                std::lock_guard<std::recursive_mutex> lazy_lk(lazy_init_mutex());
+                if (psmem > attr_p) {
+                    cudaFuncSetAttribute(k_dense_panel_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                    attr_p = 200 * 1024;
+                }
             }
             void* args[] = {(void*)&m, (void*)&k0, (void*)&nb, (void*)&per, (void*)&a, (void*)&piv, (void*)&err,
                             (void*)&cand_v, (void*)&cand_i, (void*)&rowbuf};
@@ -600,10 +606,13 @@ void dense_solve_big(int m, const double* lu, const int* piv, const double* r, d
     const bool sx = full <= kDenseSmemMax;
     const size_t smem = sx ? full : static_cast<size_t>(32) * 33 * sizeof(double);
     static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_dense_solve_big<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kDenseSmemMax));
-        attr = true;
+    {
+        std::lock_guard<std::recursive_mutex> lazy_lk(lazy_init_mutex());
+        if (!attr) {
+            cudaFuncSetAttribute(k_dense_solve_big<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kDenseSmemMax));
+            attr = true;
+        }
     }
     if (sx) k_dense_solve_big<true><<<1, 1024, smem, s>>>(m, lu, piv + m, r, z);
     else k_dense_solve_big<false><<<1, 1024, smem, s>>>(m, lu, piv + m, r, z);

@@ -218,11 +218,14 @@ template <int N>
 static void launch_tail(int nl, const TailLevelDev* lv, size_t smem, const double* rtop, double* ztop, int pre,
                         int post, int phase, int* err, cudaStream_t s) {
     static size_t set = 0;  // per block size: the attribute belongs to the instantiation
-    if (smem > set) {
-        const cudaError_t e = cudaFuncSetAttribute(k_vcycle_tail<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   static_cast<int>(smem));
-        if (e != cudaSuccess) throw std::runtime_error(std::string("V-cycle tail: ") + cudaGetErrorString(e));
-        set = smem;
+    {
+        std::lock_guard<std::recursive_mutex> lazy_lk(lazy_init_mutex());
+        if (smem > set) {
+            const cudaError_t e = cudaFuncSetAttribute(k_vcycle_tail<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       static_cast<int>(smem));
+            if (e != cudaSuccess) throw std::runtime_error(std::string("V-cycle tail: ") + cudaGetErrorString(e));
+            set = smem;
+        }
     }
     k_vcycle_tail<N><<<1, 512, smem, s>>>(nl, lv, rtop, ztop, pre, post, phase, err);
 }

@@ -6,8 +6,15 @@
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <mutex>
 
 namespace bcs {
+
+// guards the lazily initialised per-process launch parameters (occupancy
+// capacities, function attributes): contexts on different host threads may
+// make their first launches at the same time
+std::recursive_mutex& lazy_init_mutex();
+
 
 struct LaunchCounter {
     long long launches = 0;
