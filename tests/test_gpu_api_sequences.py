@@ -13,16 +13,29 @@ import numpy as np
 import pytest
 
 from paper_2403_07882_b200 import bcs, gen
+from test_gpu_parity import random_system
 
 pytestmark = pytest.mark.gpu
 
 AMG = bcs.AmgConfig(maxLevels=30, minCoarseRows=8)
+
+def _rand(nx, ny, nz, n, seed):
+    """a random diagonally dominant n x n block system (n = 1..3) as a
+    gen.System-like record"""
+    A, b = random_system(nx, ny, nz, n, seed)
+    base = gen.hex_euler(nx, ny, nz)
+    return gen.System(A=A, b=bcs.BlockVector(A.n_cells, n, values=b), x0=bcs.BlockVector(A.n_cells, n),
+                      centroids=base.centroids, name=f"rand{n}_{nx}x{ny}x{nz}")
+
 
 SYSTEMS = [
     lambda: gen.hex_euler(9),
     lambda: gen.hex_euler(8, 7, 6, scramble_seed=3),
     lambda: gen.hex_coupled(8, poly_seed=2),
     lambda: gen.hex_coupled(7, scramble_seed=1),
+    lambda: _rand(9, 8, 7, 1, 11),
+    lambda: _rand(7, 7, 6, 2, 12),
+    lambda: _rand(6, 7, 5, 3, 13),
 ]
 
 
