@@ -186,6 +186,28 @@ bcs_status bcs_dist_solve(bcs_ctx* ctx, int n_cells, int n_faces, int block_size
                           const double* lower, const double* b, const double* x0, double* x, int n_ranks,
                           int n_engines, const bcs_solver_config* cfg, bcs_report* report);
 
+/* distributedSolve(rankParts, b, x0, cfg, plan, dec, net) itself
+ * (partition.hpp, partition.cpp:370-479) on partitions the caller already
+ * built (e.g. the reference's buildPartitioned): rank r owns the global rows
+ * [rank_row_offset[r], rank_row_offset[r+1]) (new, rank-major numbering),
+ * with its local BSR (local_row_offsets[r]: rows+1, local_cols[r] local
+ * column ids, local_values[r] n*n blocks row-major) and halo_counts[r]
+ * off-rank couplings (halo_rows[r] local row, halo_cols[r] global column,
+ * halo_peers[r] owning rank, halo_values[r] blocks).  The ranks are
+ * consolidated onto n_engines engines by the caller's ConsolidationPlan
+ * (rank_to_engine, engine_row_offset: partition.cpp:184-199) exactly as the
+ * reference's consolidate (partition.cpp:201-248).  b, x0 and x are global
+ * vectors in the new numbering (the rank slices of a DistributedVector
+ * concatenated in rank order).  Same engine semantics, timing keys and
+ * EXACT-mode bit-identity as bcs_dist_solve. */
+bcs_status bcs_dist_solve_parts(bcs_ctx* ctx, int n_ranks, int block_size, const int32_t* rank_row_offset,
+                                const int32_t* const* local_row_offsets, const int32_t* const* local_cols,
+                                const double* const* local_values, const int32_t* halo_counts,
+                                const int32_t* const* halo_rows, const int32_t* const* halo_cols,
+                                const int32_t* const* halo_peers, const double* const* halo_values, int n_engines,
+                                const int32_t* rank_to_engine, const int32_t* engine_row_offset, const double* b,
+                                const double* x0, double* x, const bcs_solver_config* cfg, bcs_report* report);
+
 /* Host-side partition layer (no device needed): decompose + buildPartitioned
  * (+ consolidate when n_engines > 0).  Local slots and halo entries carry the
  * id of their LDU source block: cell c -> c, upper of face f -> n_cells + f,

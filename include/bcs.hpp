@@ -13,6 +13,7 @@
 
 #include "bcs.h"
 
+#include <algorithm>
 #include <cstdint>
 #include <map>
 #include <new>
@@ -115,6 +116,88 @@ public:
             x0.values.size(), x.values.data(), be, &c, &r);
         if (st != BCS_OK) throwStatus(st, bcs_last_error(ctx_));
         return {std::move(x), fromC<Report>(r, be == BCS_BACKEND_HOST_LDU)};
+    }
+
+    // distributedSolve itself (partition.hpp, partition.cpp:370-479) over the
+    // reference's own partition types: rank partitions as buildPartitioned
+    // returns them (rowStart/rowEnd, BlockCsrMatrix `local`, HaloCoefficients
+    // `halo`), DistributedVector b/x0 (rank slices), its ConsolidationPlan and
+    // Decomposition.  The MailboxNetwork of the reference's simulated ranks is
+    // not needed (the engines share this device).  Returns x as rank slices.
+    template <class Report, class Parts, class DVec, class Config, class Plan, class Dec>
+    std::pair<DVec, Report> distributedSolve(const Parts& parts, const DVec& b, const DVec& x0, const Config& cfg,
+                                             const Plan& plan, const Dec& dec) {
+        const int R = static_cast<int>(parts.size());
+        if (R < 1 || static_cast<int>(b.size()) != R || static_cast<int>(x0.size()) != R)
+            throw std::invalid_argument("distributedSolve: dimension mismatch");
+        const int n = parts[0].local.blockSize;
+        const size_t nn = static_cast<size_t>(n) * n;
+        std::vector<int32_t> rro(R + 1, 0), hcnt(R);
+        std::vector<const int32_t*> lro(R), lci(R), hrow(R), hcol(R), hpeer(R);
+        std::vector<const double*> lv(R), hv(R);
+        std::vector<std::vector<int32_t>> hr(R), hc(R), hp(R);
+        std::vector<std::vector<double>> hb(R);
+        for (int r = 0; r < R; ++r) {
+            const auto& p = parts[r];
+            if (p.id != r || p.local.blockSize != n) throw std::invalid_argument("distributedSolve: bad partition list");
+            rro[r] = p.rowStart;
+            rro[r + 1] = p.rowEnd;
+            lro[r] = p.local.rowOffsets.data();
+            lci[r] = p.local.colIndices.data();
+            lv[r] = p.local.values.data();
+            const auto& E = p.halo.entries;
+            hcnt[r] = static_cast<int32_t>(E.size());
+            hr[r].resize(E.size());
+            hc[r].resize(E.size());
+            hp[r].resize(E.size());
+            hb[r].resize(E.size() * nn);
+            for (size_t h = 0; h < E.size(); ++h) {
+                hr[r][h] = E[h].localRow;
+                hc[r][h] = E[h].globalCol;
+                hp[r][h] = E[h].peerRank;
+                std::copy(E[h].block.begin(), E[h].block.end(), hb[r].begin() + h * nn);
+            }
+            hrow[r] = hr[r].data();
+            hcol[r] = hc[r].data();
+            hpeer[r] = hp[r].data();
+            hv[r] = hb[r].data();
+            if (b[r].size() != static_cast<size_t>(p.rowEnd - p.rowStart) * n || x0[r].size() != b[r].size())
+                throw std::invalid_argument("distributedSolve: dimension mismatch");
+        }
+        (void)dec;  // rank row ranges travel with the partitions
+        std::vector<double> gb, gx0;
+        for (int r = 0; r < R; ++r) {
+            gb.insert(gb.end(), b[r].begin(), b[r].end());
+            gx0.insert(gx0.end(), x0[r].begin(), x0[r].end());
+        }
+        std::vector<double> gx(gb.size());
+        std::vector<int32_t> r2e(plan.rankToEngine.begin(), plan.rankToEngine.end()),
+            ero(plan.engineRowOffset.begin(), plan.engineRowOffset.end());
+        bcs_solver_config c = toC(cfg);
+        c.mode = mode_;
+        bcs_report rep{};
+        const bcs_status st = bcs_dist_solve_parts(ctx_, R, n, rro.data(), lro.data(), lci.data(), lv.data(),
+                                                   hcnt.data(), hrow.data(), hcol.data(), hpeer.data(), hv.data(),
+                                                   plan.nEngines, r2e.data(), ero.data(), gb.data(), gx0.data(),
+                                                   gx.data(), &c, &rep);
+        if (st != BCS_OK) throwStatus(st, bcs_last_error(ctx_));
+        DVec x(R);
+        size_t off = 0;
+        for (int r = 0; r < R; ++r) {
+            x[r].assign(gx.begin() + off, gx.begin() + off + b[r].size());
+            off += b[r].size();
+        }
+        Report out;
+        out.iterations = rep.iterations;
+        out.initialResidual = rep.initial_residual;
+        out.finalResidual = rep.final_residual;
+        out.converged = rep.converged != 0;
+        out.breakdown = rep.breakdown != 0;
+        out.timings["convert"] = rep.t_convert;
+        out.timings["setup"] = rep.t_setup;
+        out.timings["solve"] = rep.t_solve;
+        out.timings["retrieve"] = rep.t_retrieve;
+        return {std::move(x), std::move(out)};
     }
 
     // Mode R: the multi-rank branch of LinearDispatch::solve

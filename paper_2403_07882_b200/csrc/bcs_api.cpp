@@ -309,6 +309,25 @@ bcs_status bcs_dist_solve(bcs_ctx* ctx, int n_cells, int n_faces, int block_size
     });
 }
 
+bcs_status bcs_dist_solve_parts(bcs_ctx* ctx, int n_ranks, int block_size, const int32_t* rank_row_offset,
+                                const int32_t* const* local_row_offsets, const int32_t* const* local_cols,
+                                const double* const* local_values, const int32_t* halo_counts,
+                                const int32_t* const* halo_rows, const int32_t* const* halo_cols,
+                                const int32_t* const* halo_peers, const double* const* halo_values, int n_engines,
+                                const int32_t* rank_to_engine, const int32_t* engine_row_offset, const double* b,
+                                const double* x0, double* x, const bcs_solver_config* cfg, bcs_report* report) {
+    return guarded(ctx, [&] {
+        if (!rank_row_offset || !local_row_offsets || !local_cols || !local_values || !halo_counts || !rank_to_engine ||
+            !engine_row_offset || !b || !x0 || !x)
+            throw std::invalid_argument("bcs_dist_solve_parts: null argument");
+        bcs_report rep{};
+        eng(ctx).distSolveParts(n_ranks, block_size, rank_row_offset, local_row_offsets, local_cols, local_values,
+                                halo_counts, halo_rows, halo_cols, halo_peers, halo_values, n_engines, rank_to_engine,
+                                engine_row_offset, b, x0, x, cfgOf(cfg), rep);
+        if (report) *report = rep;
+    });
+}
+
 bcs_status bcs_partition_create(bcs_partition** out, int n_cells, int n_faces, const int32_t* owner,
                                 const int32_t* neighbour, const double* centroids, int n_ranks, int n_engines) {
     return guarded(nullptr, [&] {

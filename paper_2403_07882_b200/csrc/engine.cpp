@@ -1677,7 +1677,7 @@ void Engine::opResidual(const double* x, const double* b, double* r) {
         return;
     }
     opSpmv(x, distTmp_.p);
-    sub_vec(b, distTmp_, r, static_cast<size_t>(mpActive_ ? mpRows_ : distNc_) * n_, stream_);
+    sub_vec(b, distTmp_, r, static_cast<size_t>(mpActive_ ? mpRows_ : nc_) * n_, stream_);  // nc_: the global rows of this Mode R call
 }
 
 // halo exchange of the multi-process Mode R: pack the rows peers need, one
@@ -1870,6 +1870,45 @@ void Engine::distSetupTopology(int nc, int nf, int n, const int32_t* owner, cons
     sync();
 }
 
+// Mode R on this device over dist_'s engines (partition.cpp:411-471): the
+// engines' dot segments, one local preconditioner per engine, global Krylov
+// on kb_/kx_ (new numbering); returns the time the preconditioners were ready
+std::chrono::steady_clock::time_point Engine::distSolveCore(const bcs_solver_config& cfg, bcs_report& rep) {
+    // dot-product segments of the engines (a serial call in between rewrites seg_)
+    nseg_ = static_cast<int>(dist_.size());
+    seg_.ensure(distSegh_.size(), stream_);
+    check(cudaMemcpyAsync(seg_.p, distSegh_.data(), sizeof(long long) * distSegh_.size(), cudaMemcpyHostToDevice,
+                          stream_), "H2D seg");
+    // per-engine preconditioners (partition.cpp:411-412)
+    hist_.clear();
+    spmvMs_ = 0.0;
+    spmvCount_ = 0;
+    sweepMs_ = 0.0;
+    sweepBytes_ = 0.0;
+    sweepCount_ = 0;
+    evUsed_ = 0;
+    cudaMemsetAsync(err_.p + 1, 0, sizeof(int), stream_);
+    for (auto& P : dist_) {
+        H_ = &P.H;
+        FineMatrix F;
+        F.rows = P.rows;
+        F.nnz = P.nnz;
+        F.ro = P.ro;
+        F.ci = P.ci;
+        F.dg = P.dg;
+        F.tpos = P.tpos;
+        F.v = P.vals;
+        buildPrecondOn(F, cfg);
+    }
+    H_ = &main_;
+    sync();
+    const auto t2 = clk::now();
+    distActive_ = true;
+    solveKrylov(kb_, kx_.p, cfg, rep);
+    distActive_ = false;
+    return t2;
+}
+
 void Engine::distSolve(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh, const double* centroids,
                        const double* diag, const double* upper, const double* lower, const double* b,
                        const double* x0, double* x, int nRanks, int nEngines, const bcs_solver_config& cfg,
@@ -1916,39 +1955,8 @@ void Engine::distSolve(int nc, int nf, int n, const int32_t* owner, const int32_
     check(cudaMemcpyAsync(kx_.p, hx.data(), N * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D x0");
     sync();
     const auto t1 = clk::now();
-    // dot-product segments of the engines (a serial call in between rewrites seg_)
-    nseg_ = static_cast<int>(dist_.size());
-    seg_.ensure(distSegh_.size(), stream_);
-    check(cudaMemcpyAsync(seg_.p, distSegh_.data(), sizeof(long long) * distSegh_.size(), cudaMemcpyHostToDevice,
-                          stream_), "H2D seg");
-    // per-engine preconditioners (partition.cpp:411-412)
-    hist_.clear();
-    spmvMs_ = 0.0;
-    spmvCount_ = 0;
-    sweepMs_ = 0.0;
-    sweepBytes_ = 0.0;
-    sweepCount_ = 0;
-    evUsed_ = 0;
-    cudaMemsetAsync(err_.p + 1, 0, sizeof(int), stream_);
     nc_ = nc;
-    for (auto& P : dist_) {
-        H_ = &P.H;
-        FineMatrix F;
-        F.rows = P.rows;
-        F.nnz = P.nnz;
-        F.ro = P.ro;
-        F.ci = P.ci;
-        F.dg = P.dg;
-        F.tpos = P.tpos;
-        F.v = P.vals;
-        buildPrecondOn(F, cfg);
-    }
-    H_ = &main_;
-    sync();
-    const auto t2 = clk::now();
-    distActive_ = true;
-    solveKrylov(kb_, kx_.p, cfg, rep);
-    distActive_ = false;
+    const auto t2 = distSolveCore(cfg, rep);
     const auto t3 = clk::now();
     check(cudaMemcpyAsync(hx.data(), kx_.p, N * sizeof(double), cudaMemcpyDeviceToHost, stream_), "D2H x");
     sync();
@@ -1957,6 +1965,121 @@ void Engine::distSolve(int nc, int nf, int n, const int32_t* owner, const int32_
         std::copy(hx.begin() + static_cast<size_t>(g) * n, hx.begin() + static_cast<size_t>(g + 1) * n,
                   x + static_cast<size_t>(old) * n);
     }
+    const auto t4 = clk::now();
+    rep.t_convert = secs(t0, t1);  // partition.cpp:474-477 keys
+    rep.t_setup = secs(t1, t2);
+    rep.t_solve = secs(t2, t3);
+    rep.t_retrieve = secs(t3, t4);
+    rep.t_amg_setup = rep.t_setup;
+    rep.t_krylov = rep.t_solve;
+    rep.amg_levels = static_cast<int>(dist_.size());
+}
+
+// distributedSolve (partition.cpp:370-479) on partitions the caller already
+// built (the reference's buildPartitioned output): rank r owns global rows
+// [rank_row_offset[r], rank_row_offset[r+1]) with a local BSR (local columns)
+// and halo entries (local row, global column, peer rank, block).  The ranks
+// are consolidated onto engines by the caller's plan (consolidate,
+// partition.cpp:201-248, restated bit-exact) with every block carried by the
+// id of its position in one concatenated value array [all local blocks in
+// rank order | all halo blocks in rank order], which is then gathered on the
+// device.  b, x0 and x are global vectors in the new (rank-major) numbering.
+void Engine::distSolveParts(int nRanks, int n, const int* rankRowOffset, const int* const* localRo,
+                            const int* const* localCi, const double* const* localVals, const int* haloCount,
+                            const int* const* haloRow, const int* const* haloCol, const int* const* haloPeer,
+                            const double* const* haloVals, int nEngines, const int* rankToEngine,
+                            const int* engineRowOffset, const double* b, const double* x0, double* x,
+                            const bcs_solver_config& cfg, bcs_report& rep) {
+    LaunchScope ls(&launches_);
+    if (n < 1 || n > 5) throw std::invalid_argument("bcs: block size must be 1..5 on the device");
+    if (nRanks < 1) throw std::invalid_argument("distributedSolve: no partitions");
+    if (nEngines < 1 || nEngines > nRanks) throw std::invalid_argument("makeConsolidationPlan: need 1 <= nEngines <= nRanks");
+    if (nEngines > 64) throw std::invalid_argument("bcs: at most 64 engines per device");
+    validateConfig(cfg);
+    const auto t0 = clk::now();
+    SerialStateGuard guard(*this);
+    const size_t nn = static_cast<size_t>(n) * n;
+    Decomposition dec;
+    dec.nRanks = nRanks;
+    dec.rankRowOffset.assign(rankRowOffset, rankRowOffset + nRanks + 1);
+    for (int r = 0; r < nRanks; ++r)
+        if (dec.rankRowOffset[r + 1] < dec.rankRowOffset[r]) throw std::invalid_argument("distributedSolve: bad row ranges");
+    const int nc = dec.rankRowOffset[nRanks];
+    // partitions with value ids into the concatenated array
+    std::vector<Partition> parts(nRanks);
+    size_t localTotal = 0, haloTotal = 0;
+    for (int r = 0; r < nRanks; ++r) localTotal += static_cast<size_t>(localRo[r][dec.nLocalRows(r)]);
+    for (int r = 0; r < nRanks; ++r) haloTotal += static_cast<size_t>(haloCount[r]);
+    if (localTotal + haloTotal > static_cast<size_t>(INT32_MAX)) throw std::invalid_argument("distributedSolve: too many blocks");
+    size_t lb = 0, hb = localTotal;
+    for (int r = 0; r < nRanks; ++r) {
+        Partition& p = parts[r];
+        const int rows = dec.nLocalRows(r);
+        p.id = r;
+        p.rowStart = dec.rankRowOffset[r];
+        p.rowEnd = dec.rankRowOffset[r + 1];
+        p.ro.assign(localRo[r], localRo[r] + rows + 1);
+        const int nnz = p.ro[rows];
+        p.ci.assign(localCi[r], localCi[r] + nnz);
+        p.src.resize(nnz);
+        for (int k = 0; k < nnz; ++k) p.src[k] = static_cast<int>(lb + k);
+        lb += nnz;
+        const int nh = haloCount[r];
+        p.haloRow.assign(haloRow[r], haloRow[r] + nh);
+        p.haloCol.assign(haloCol[r], haloCol[r] + nh);
+        p.haloPeer.assign(haloPeer[r], haloPeer[r] + nh);
+        p.haloSrc.resize(nh);
+        for (int h = 0; h < nh; ++h) p.haloSrc[h] = static_cast<int>(hb + h);
+        hb += nh;
+    }
+    ConsolidationPlan plan;
+    plan.nEngines = nEngines;
+    plan.rankToEngine.assign(rankToEngine, rankToEngine + nRanks);
+    plan.engineRowOffset.assign(engineRowOffset, engineRowOffset + nRanks);
+    for (int r = 0; r < nRanks; ++r)
+        if (plan.rankToEngine[r] < 0 || plan.rankToEngine[r] >= nEngines)
+            throw std::invalid_argument("distributedSolve: rank mapped to no engine");
+    const std::vector<Partition> engs = consolidate(parts, plan, dec);
+    // the concatenated values on the device (staged), then the engines' slots
+    const size_t total = localTotal + haloTotal;
+    ldu_diag_.ensure(std::max<size_t>(total, 1) * nn, stream_);
+    lb = 0;
+    for (int r = 0; r < nRanks; ++r) {
+        const size_t cnt = static_cast<size_t>(parts[r].ro.back());
+        if (cnt) h2d(ldu_diag_.p + lb * nn, localVals[r], cnt * nn * sizeof(double), "H2D local blocks");
+        lb += cnt;
+    }
+    for (int r = 0; r < nRanks; ++r) {
+        const size_t cnt = static_cast<size_t>(haloCount[r]);
+        if (cnt) h2d(ldu_diag_.p + lb * nn, haloVals[r], cnt * nn * sizeof(double), "H2D halo blocks");
+        lb += cnt;
+    }
+    dist_.resize(engs.size());
+    std::vector<long long> segh(engs.size() + 1, 0);
+    for (size_t e = 0; e < engs.size(); ++e) {
+        uploadEnginePart(dist_[e], engs[e], n, nullptr);
+        dist_[e].rowStart = engs[e].rowStart;
+        segh[e] = static_cast<long long>(engs[e].rowStart) * n;
+        segh[e + 1] = static_cast<long long>(engs[e].rowEnd) * n;
+        DistPart& P = dist_[e];
+        gather_values(n, P.nnz, static_cast<int>(total), 0, P.src, ldu_diag_, nullptr, nullptr, P.vals.p, stream_);
+        if (P.nh) gather_values(n, P.nh, static_cast<int>(total), 0, P.hsrc, ldu_diag_, nullptr, nullptr, P.hvals.p, stream_);
+    }
+    distSegh_ = segh;
+    distNc_ = -1;  // the LDU-based Mode R cache no longer describes dist_
+    n_ = n;
+    const size_t N = static_cast<size_t>(nc) * n;
+    kb_.ensure(N, stream_);
+    kx_.ensure(N, stream_);
+    distTmp_.ensure(N, stream_);
+    h2d(kb_.p, b, N * sizeof(double), "H2D b");
+    h2d(kx_.p, x0, N * sizeof(double), "H2D x0");
+    sync();
+    const auto t1 = clk::now();
+    nc_ = nc;
+    const auto t2 = distSolveCore(cfg, rep);
+    const auto t3 = clk::now();
+    d2h(x, kx_.p, N * sizeof(double), "D2H x");
     const auto t4 = clk::now();
     rep.t_convert = secs(t0, t1);  // partition.cpp:474-477 keys
     rep.t_setup = secs(t1, t2);

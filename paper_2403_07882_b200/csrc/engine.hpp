@@ -209,6 +209,13 @@ public:
     void distSolveMP(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh, const double* centroids,
                      const double* diag, const double* upper, const double* lower, const double* b, const double* x0,
                      double* x, int nRanks, const bcs_solver_config& cfg, bcs_report& rep);
+    // distributedSolve on caller-built rank partitions (bcs_dist_solve_parts)
+    void distSolveParts(int nRanks, int n, const int* rankRowOffset, const int* const* localRo,
+                        const int* const* localCi, const double* const* localVals, const int* haloCount,
+                        const int* const* haloRow, const int* const* haloCol, const int* const* haloPeer,
+                        const double* const* haloVals, int nEngines, const int* rankToEngine,
+                        const int* engineRowOffset, const double* b, const double* x0, double* x,
+                        const bcs_solver_config& cfg, bcs_report& rep);
     void distSolve(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh, const double* centroids,
                    const double* diag, const double* upper, const double* lower, const double* b, const double* x0,
                    double* x, int nRanks, int nEngines, const bcs_solver_config& cfg, bcs_report& rep);
@@ -275,6 +282,7 @@ private:
     void opPrecond(const double* r, double* z);
     void opDot(const double* a, const double* b, double* out, bool sqrt_out);
     void opAxpyDot(double* w, const double* h, const double* v, const double* nextv, double* out);
+    std::chrono::steady_clock::time_point distSolveCore(const bcs_solver_config& cfg, bcs_report& rep);
     void distSetupTopology(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh,
                            const double* centroids, int nRanks, int nEngines);
     void mpSetupTopology(int nc, int nf, int n, const int32_t* owner, const int32_t* neigh, const double* centroids,

@@ -8,11 +8,14 @@
 // B200 pipeline (include/bcs.hpp); one bcs::SolvePipeline per reference
 // pipeline object keeps its setup-vs-replace state.  fvb::backendSolve (the
 // one-shot wrapper, engine.cpp:123-129) is interposed the same way with a
-// fresh pipeline per call.
+// fresh pipeline per call, and fvb::distributedSolve (partition.cpp:370-479,
+// LinearDispatch's multi-rank branch) runs the one-device Mode R on the
+// caller's partitions (bcs_dist_solve_parts).
 //   bcs_interpose_route: -1 the reference's own solve (__real_), else the
 //   BCS_MODE_* of the B200 solve; initialised from $BCS_INTERPOSE
 //   (off | parity | exact; default parity).
 #include "blockfv/engine.hpp"
+#include "blockfv/partition.hpp"
 
 #include "../../include/bcs.hpp"
 
@@ -78,4 +81,27 @@ __wrap__ZN3fvb12backendSolveERKNS_14BlockLduMatrixERKNS_11BlockVectorES5_NS_7Bac
     p.setMode(bcs_interpose_route);
     ++bcs_interpose_calls;
     return p.solve<fvb::SolveReport>(A, b, x0, backend, cfg);
+}
+
+using DistResult = std::pair<fvb::DistributedVector, fvb::SolveReport>;
+#define BCS_DIST_SOLVE                                                                                              \
+    _ZN3fvb16distributedSolveERKSt6vectorINS_15MatrixPartitionESaIS1_EERKS0_IS0_IdSaIdEESaIS7_EESB_RKNS_12SolverConfigERKNS_17ConsolidationPlanERKNS_13DecompositionERNS_14MailboxNetworkE
+#define BCS_CAT2(a, b) a##b
+#define BCS_CAT(a, b) BCS_CAT2(a, b)
+
+extern "C" DistResult BCS_CAT(__real_, BCS_DIST_SOLVE)(const std::vector<fvb::MatrixPartition>& parts,
+                                                       const fvb::DistributedVector& b, const fvb::DistributedVector& x0,
+                                                       const fvb::SolverConfig& cfg, const fvb::ConsolidationPlan& plan,
+                                                       const fvb::Decomposition& dec, fvb::MailboxNetwork& net);
+
+extern "C" DistResult BCS_CAT(__wrap_, BCS_DIST_SOLVE)(const std::vector<fvb::MatrixPartition>& parts,
+                                                       const fvb::DistributedVector& b, const fvb::DistributedVector& x0,
+                                                       const fvb::SolverConfig& cfg, const fvb::ConsolidationPlan& plan,
+                                                       const fvb::Decomposition& dec, fvb::MailboxNetwork& net) {
+    if (bcs_interpose_route < 0) return BCS_CAT(__real_, BCS_DIST_SOLVE)(parts, b, x0, cfg, plan, dec, net);
+    static std::unique_ptr<bcs::SolvePipeline> p;
+    if (!p) p = std::make_unique<bcs::SolvePipeline>(0);
+    p->setMode(bcs_interpose_route);
+    ++bcs_interpose_calls;
+    return p->distributedSolve<fvb::SolveReport>(parts, b, x0, cfg, plan, dec);
 }

@@ -15,7 +15,10 @@
 //   * EXACT mode: every nonlinear residual of the history bit-identical
 //     (compareRuns' maxResidualDelta == 0), coefficients identical;
 //   * default (PARITY) mode: compareRuns' maxResidualRelDelta <= 1e-6 and the
-//     coefficients within 1e-6 (the criterion's bar).
+//     coefficients within 1e-6 (the criterion's bar);
+// and the same two cases through LinearDispatch's multi-rank branch (4 ranks
+// on 2 engines, 3 ranks on 3 engines), whose fvb::distributedSolve runs the
+// B200's one-device Mode R on the reference's own partitions.
 // Prints one "ok"/"FAIL" line per check and a summary line with the measured
 // deltas; exit code = number of failures.  Run by tests/test_gpu_dropin.py.
 #include "blockfv/case_runner.hpp"
@@ -72,29 +75,43 @@ static RunReport run(const CaseConfig& cfg, int route) {
     const long before = bcs_interpose_calls;
     RunReport r = runCase(cfg);
     if (route >= 0)
-        check(bcs_interpose_calls - before >= 200, cfg.name + ": runCase's linear solves went through the B200 pipeline");
+        check(bcs_interpose_calls - before >= cfg.run.maxIters,
+              cfg.name + ": runCase's linear solves went through the B200 pipeline");
     bcs_interpose_route = -1;
     return r;
 }
 
+// LinearDispatch's multi-rank branch (case_runner.cpp:329-343): buildPartitioned
+// + distributedSolve over simulated ranks consolidated onto engines
+static CaseConfig ranks(CaseConfig c, int nRanks, int nEngines, int iters) {
+    c.partitioning.ranks = nRanks;
+    c.partitioning.engines = nEngines;
+    c.run.maxIters = iters;
+    c.name += "/ranks" + std::to_string(nRanks) + "x" + std::to_string(nEngines);
+    return c;
+}
+
 int main() {
-    for (const CaseConfig& cfg : {engineAmg(cavity(32, 200)), engineAmg(sod(100, 200))}) {
+    for (const CaseConfig& cfg : {engineAmg(cavity(32, 200)), engineAmg(sod(100, 200)),
+                                  ranks(engineAmg(cavity(32, 200)), 4, 2, 200),
+                                  ranks(engineAmg(sod(100, 200)), 3, 3, 200)}) {
         const RunReport ref = run(cfg, -1);
-        check(ref.iterations == 200 && ref.history.size() == 200, cfg.name + ": reference run has 200 iterations");
+        check(ref.iterations == cfg.run.maxIters && static_cast<int>(ref.history.size()) == cfg.run.maxIters,
+              cfg.name + ": reference run has all its iterations");
         // EXACT: bit-identical nonlinear history
         const RunReport ex = run(cfg, BCS_MODE_EXACT);
         const ComparisonSummary se = compareRuns(ref, ex);
         bool same = ex.history.size() == ref.history.size();
         for (std::size_t k = 0; same && k < ref.history.size(); ++k)
             same = ex.history[k].residuals == ref.history[k].residuals;
-        check(se.overlapIters == 200 && same && se.maxResidualDelta == 0.0,
+        check(se.overlapIters == cfg.run.maxIters && same && se.maxResidualDelta == 0.0,
               cfg.name + ": EXACT mode, 200 nonlinear residuals bit-identical to the reference through runCase");
         bool coefSame = ex.coefficients == ref.coefficients;
         check(coefSame, cfg.name + ": EXACT mode, final coefficients identical");
         // default mode: the acceptance bar
         const RunReport pa = run(cfg, BCS_MODE_PARITY);
         const ComparisonSummary sp = compareRuns(ref, pa);
-        check(sp.overlapIters == 200 && sp.maxResidualRelDelta <= 1e-6,
+        check(sp.overlapIters == cfg.run.maxIters && sp.maxResidualRelDelta <= 1e-6,
               cfg.name + ": PARITY mode, residual histories within 1e-6 relative over 200 iterations");
         double worstCoef = 0.0;
         for (const auto& [k, d] : sp.coefficientDeltas) {

@@ -23,10 +23,11 @@ RUNCASE = os.path.join(ROOT, "oracle", "_ref", "runcase_test")
 
 @pytest.mark.skipif(not os.path.exists(RUNCASE), reason="oracle/_ref/runcase_test not built (reference absent at build)")
 def test_runcase_with_b200_pipeline_interposed(parity_log):
-    """fvb::runCase unchanged, its LinearDispatch's SolvePipeline::solve routed
-    to the B200 pipeline at link time (tests/cpp/runcase_main.cpp): 200
-    nonlinear iterations of the coupled cavity and the implicit Sod tube,
-    EXACT mode bit-identical to the reference, PARITY mode within 1e-6."""
+    """fvb::runCase unchanged, its LinearDispatch's SolvePipeline::solve and
+    distributedSolve routed to the B200 at link time (tests/cpp/runcase_main.cpp):
+    200 nonlinear iterations of the coupled cavity and the implicit Sod tube,
+    serial and over simulated ranks (4 on 2 engines, 3 on 3), EXACT mode
+    bit-identical to the reference, PARITY mode within 1e-6."""
     p = subprocess.run([RUNCASE], capture_output=True, text=True, timeout=1800)
     print(p.stdout)
     assert p.returncode == 0, p.stdout + p.stderr

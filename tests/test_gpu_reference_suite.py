@@ -3,10 +3,11 @@
 oracle/Makefile compiles the reference's unit tests (proj/tests/test_*.cpp,
 against tests/cpp/doctest_shim/doctest.h) and its acceptance program
 (proj/tests/acceptance_main.cpp) where they lie, linked with
--Wl,--wrap of fvb::SolvePipeline::solve and fvb::backendSolve
-(tests/cpp/pipeline_interpose.cpp): every linear solve they make through the
-pipeline -- runCase's LinearDispatch, the one-shot backendSolve, the SIMPLE
-path's backendSolve calls -- runs on the B200 ($BCS_INTERPOSE = parity |
+-Wl,--wrap of fvb::SolvePipeline::solve, fvb::backendSolve and
+fvb::distributedSolve (tests/cpp/pipeline_interpose.cpp): every linear solve
+they make through the pipeline -- runCase's LinearDispatch (serial and
+multi-rank branches), the one-shot backendSolve, the SIMPLE path's
+backendSolve calls, the distributed tests -- runs on the B200 ($BCS_INTERPOSE = parity |
 exact).  No reference source is modified."""
 import os
 import re
@@ -48,5 +49,5 @@ def test_reference_acceptance_with_b200_pipeline(criterion):
         p, n = _run([ACC, str(criterion)], "parity", 1200)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
     assert "PASS" in p.stdout
-    if criterion in (2, 6, 7, 9):  # the criteria whose solves go through runCase
+    if criterion in (2, 3, 6, 7, 9):  # the criteria whose solves go through runCase / distributedSolve
         assert n > 0, n
