@@ -129,6 +129,8 @@ SIGNATURES = {
     "bcs_partition_gather_values": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,
                                             c_void_p, c_void_p]),
     "bcs_dist_solve": (c_int, [c_void_p, c_int, c_int, c_int] + [c_void_p] * 9 + [c_int, c_int, P(SolverConfigC), P(ReportC)]),
+    "bcs_dist_solve_parts": (c_int, [c_void_p, c_int, c_int] + [c_void_p] * 9 + [c_int] + [c_void_p] * 5 +
+                             [P(SolverConfigC), P(ReportC)]),
     "bcs_partition_create": (c_int, [P(c_void_p), c_int, c_int, c_void_p, c_void_p, c_void_p, c_int, c_int]),
     "bcs_partition_destroy": (None, [c_void_p]),
     "bcs_partition_count": (c_int, [c_void_p]),

@@ -418,6 +418,39 @@ class Context:
         r.timings = {"convert": rep.t_convert, "setup": rep.t_setup, "solve": rep.t_solve, "retrieve": rep.t_retrieve}
         return x, r
 
+    def dist_solve_parts(self, parts, b: np.ndarray, x0: np.ndarray, n: int, n_engines: int,
+                         rank_to_engine, engine_row_offset, cfg: SolverConfig) -> Tuple[np.ndarray, SolveReport]:
+        """distributedSolve on caller-built rank partitions (bcs_dist_solve_parts).
+        parts: one dict per rank with row_start, row_end, ro, ci, values (nnz*n*n),
+        halo_row, halo_col, halo_peer, halo_values; b, x0 and the result are global
+        vectors in the new (rank-major) numbering."""
+        R = len(parts)
+        keep = []  # keep every array alive for the call
+
+        def arr(a, dt):
+            a = np.ascontiguousarray(a, dt)
+            keep.append(a)
+            return a
+
+        def ptrs(key, dt):
+            ps = (ctypes.c_void_p * R)(*[arr(p[key], dt).ctypes.data for p in parts])
+            keep.append(ps)
+            return ctypes.cast(ps, ctypes.c_void_p)
+        rro = arr([parts[0]["row_start"]] + [p["row_end"] for p in parts], np.int32)
+        hcnt = arr([len(p["halo_col"]) for p in parts], np.int32)
+        bb, xx = arr(b, np.float64), arr(x0, np.float64)
+        x = np.zeros_like(bb)
+        r2e, ero = arr(rank_to_engine, np.int32), arr(engine_row_offset, np.int32)
+        c = cfg.to_c()
+        rep = N.ReportC()
+        st = self._lib.bcs_dist_solve_parts(
+            self.h, R, int(n), N.ptr(rro), ptrs("ro", np.int32), ptrs("ci", np.int32), ptrs("values", np.float64),
+            N.ptr(hcnt), ptrs("halo_row", np.int32), ptrs("halo_col", np.int32), ptrs("halo_peer", np.int32),
+            ptrs("halo_values", np.float64), int(n_engines), N.ptr(r2e), N.ptr(ero), N.ptr(bb), N.ptr(xx),
+            N.ptr(x), ctypes.byref(c), ctypes.byref(rep))
+        self._ck(st)
+        return x, SolveReport.from_c(rep)
+
     def comm_init(self, rank: int, size: int, uid: bytes):
         """Collective: this context joins an NCCL communicator of `size` processes (one per GPU)."""
         buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)

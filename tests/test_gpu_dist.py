@@ -172,3 +172,40 @@ def test_dist_perf_modes_converge(ctx, mode):
     ctx.set_topology(s.A)
     ctx.upload_ldu(s.A)
     assert ctx.residual(s.b.values, x.values) <= 1e-8 * r.initialResidual * 1.01
+
+
+@pytest.mark.parametrize("maker,ranks,engines", [(lambda: gen.hex_euler(10), 4, 2),
+                                                 (lambda: gen.hex_coupled(9, scramble_seed=2, poly_seed=1), 5, 3),
+                                                 (lambda: gen.hex_euler(8, 7, 9, aspect=20.0), 3, 3)])
+@pytest.mark.parametrize("mode", [bcs.Mode.EXACT, bcs.Mode.PARITY])
+def test_dist_solve_parts_matches_dist_solve(ctx, maker, ranks, engines, mode):
+    """bcs_dist_solve_parts (distributedSolve on caller-built rank partitions,
+    here the host partition layer's buildPartitioned output with its values
+    gathered per rank) equals bcs_dist_solve on the same system bit for bit."""
+    s = maker()
+    A, n = s.A, s.A.n
+    cfg = bcs.SolverConfig(preconditioner=bcs.PrecondKind.AMG, relTol=1e-8, maxIters=300,
+                           amg=bcs.AmgConfig(maxLevels=30, minCoarseRows=8), mode=mode)
+    x_ref, r_ref = ctx.dist_solve(A, s.b, s.x0, s.centroids, ranks, engines, cfg)
+    P = bcs.Partition(A.n_cells, A.owner, A.neighbour, s.centroids, ranks)
+    _, rro, o2n = P.decomposition()
+    parts = []
+    for r in range(ranks):
+        d = P.part(r)
+        loc, halo = P.gather_values(r, A)
+        parts.append(dict(row_start=d["row_start"], row_end=d["row_end"], ro=d["ro"], ci=d["ci"], values=loc,
+                          halo_row=d["halo_row"], halo_col=d["halo_col"], halo_peer=d["halo_peer"], halo_values=halo))
+    # makeConsolidationPlan (partition.cpp:184-199): contiguous rank groups
+    r2e = [(r * engines) // ranks for r in range(ranks)]
+    ero, acc = [], {}
+    for r in range(ranks):
+        ero.append(acc.get(r2e[r], 0))
+        acc[r2e[r]] = acc.get(r2e[r], 0) + (rro[r + 1] - rro[r])
+    # scatterVector: new numbering
+    bnew = np.empty_like(s.b.values).reshape(-1, n)
+    xnew = np.empty_like(s.x0.values).reshape(-1, n)
+    bnew[o2n] = s.b.values.reshape(-1, n)
+    xnew[o2n] = s.x0.values.reshape(-1, n)
+    x, r = ctx.dist_solve_parts(parts, bnew.reshape(-1), xnew.reshape(-1), n, engines, r2e, ero, cfg)
+    assert r.iterations == r_ref.iterations
+    assert x.reshape(-1, n)[o2n].tobytes() == np.asarray(x_ref.values).tobytes()
