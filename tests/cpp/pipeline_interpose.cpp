@@ -7,8 +7,8 @@
 // in runCase (case_runner.cpp:333) above all -- lands here and runs on the
 // B200 pipeline (include/bcs.hpp); one bcs::SolvePipeline per reference
 // pipeline object keeps its setup-vs-replace state.  fvb::backendSolve (the
-// one-shot wrapper, engine.cpp:123-129) is interposed the same way with a
-// fresh pipeline per call, and fvb::distributedSolve (partition.cpp:370-479,
+// one-shot wrapper, engine.cpp:123-129) is interposed the same way on one
+// shared pipeline, and fvb::distributedSolve (partition.cpp:370-479,
 // LinearDispatch's multi-rank branch) runs the one-device Mode R on the
 // caller's partitions (bcs_dist_solve_parts).
 //   bcs_interpose_route: -1 the reference's own solve (__real_), else the
@@ -77,10 +77,14 @@ __wrap__ZN3fvb12backendSolveERKNS_14BlockLduMatrixERKNS_11BlockVectorES5_NS_7Bac
     if (bcs_interpose_route < 0)
         return __real__ZN3fvb12backendSolveERKNS_14BlockLduMatrixERKNS_11BlockVectorES5_NS_7BackendERKNS_12SolverConfigE(
             A, b, x0, backend, cfg);
-    bcs::SolvePipeline p(0);
-    p.setMode(bcs_interpose_route);
+    // one context for every one-shot call: the results do not depend on the
+    // setup-vs-replace branch (bit-identical either way), and a context per
+    // call would cost more than a small solve
+    static std::unique_ptr<bcs::SolvePipeline> p;
+    if (!p) p = std::make_unique<bcs::SolvePipeline>(0);
+    p->setMode(bcs_interpose_route);
     ++bcs_interpose_calls;
-    return p.solve<fvb::SolveReport>(A, b, x0, backend, cfg);
+    return p->solve<fvb::SolveReport>(A, b, x0, backend, cfg);
 }
 
 using DistResult = std::pair<fvb::DistributedVector, fvb::SolveReport>;
