@@ -37,7 +37,9 @@ struct DArray {
         p = nullptr;
         cap = 0;
         owned = true;
-        const size_t bytes = (n ? n : 1) * sizeof(T);
+        // + 64 bytes: the 16-byte-widened copies (cp.async / TMA bulk ranges
+        // rounded out to 16-byte bounds) may touch up to 15 bytes past the end
+        const size_t bytes = (n ? n : 1) * sizeof(T) + 64;
         check(cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, s), "cudaMallocAsync");
         cap = n ? n : 1;
     }
@@ -73,7 +75,7 @@ struct PhaseArena {
         if (base) check(cudaFreeAsync(base, s), "cudaFreeAsync arena");
         base = nullptr;
         cap = 0;
-        check(cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, s), "cudaMallocAsync arena");
+        check(cudaMallocAsync(reinterpret_cast<void**>(&base), bytes + 64, s), "cudaMallocAsync arena");  // widened-copy slack
         cap = bytes;
     }
     template <class T>
