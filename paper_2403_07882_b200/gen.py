@@ -44,7 +44,7 @@ def _alloc(nx, ny, nz, n, pinned_alloc=None, poly_seed=-1):
     upper = mk(nf * n * n, np.float64)
     lower = mk(nf * n * n, np.float64)
     rhs = mk(nc * n, np.float64)
-    cen = np.zeros(nc * 3)
+    cen = mk(nc * 3, np.float64) if pinned_alloc else np.zeros(nc * 3)
     return nc, nf, owner, neigh, diag, upper, lower, rhs, cen
 
 
@@ -53,32 +53,39 @@ def _tag(scramble_seed, poly_seed):
 
 
 def hex_euler(nx: int, ny: int = None, nz: int = None, aspect: float = 1.0, scramble_seed: int = -1,
-              alloc=None, poly_seed: int = -1) -> System:
+              alloc=None, poly_seed: int = -1, fill: bool = True) -> System:
+    """fill=False: the arrays `alloc` returns already hold this system (e.g.
+    mappings of a copy another process generated); nothing is written."""
     ny = nx if ny is None else ny
     nz = nx if nz is None else nz
     nc, nf, owner, neigh, diag, upper, lower, rhs, cen = _alloc(nx, ny, nz, 5, alloc, poly_seed)
-    rc = N.gen().bcsgen_hex_euler_poly(nx, ny, nz, float(aspect), int(scramble_seed), int(poly_seed), N.ptr(owner),
-                                       N.ptr(neigh), N.ptr(diag), N.ptr(upper), N.ptr(lower), N.ptr(rhs), N.ptr(cen))
-    if rc:
-        raise ValueError("bcsgen_hex_euler: bad arguments")
+    if fill:
+        rc = N.gen().bcsgen_hex_euler_poly(nx, ny, nz, float(aspect), int(scramble_seed), int(poly_seed),
+                                           N.ptr(owner), N.ptr(neigh), N.ptr(diag), N.ptr(upper), N.ptr(lower),
+                                           N.ptr(rhs), N.ptr(cen))
+        if rc:
+            raise ValueError("bcsgen_hex_euler: bad arguments")
     A = BlockLduMatrix(nc, owner, neigh, 5, diag, upper, lower)
     x0 = (alloc or (lambda size, dt: np.zeros(size, dt)))(nc * 5, np.float64)
-    x0[:] = 0.0
+    if fill:
+        x0[:] = 0.0
     return System(A, BlockVector(nc, 5, rhs), BlockVector(nc, 5, x0), cen.reshape(nc, 3),
                   f"euler5 {nx}x{ny}x{nz} {_tag(scramble_seed, poly_seed)} AR{aspect:g}")
 
 
 def hex_coupled(nx: int, ny: int = None, nz: int = None, aspect: float = 1.0, scramble_seed: int = -1,
-                alloc=None, poly_seed: int = -1) -> System:
+                alloc=None, poly_seed: int = -1, fill: bool = True) -> System:
+    """fill=False: as hex_euler."""
     ny = nx if ny is None else ny
     nz = nx if nz is None else nz
     nc, nf, owner, neigh, diag, upper, lower, rhs, cen = _alloc(nx, ny, nz, 4, alloc, poly_seed)
     x0 = (alloc or (lambda size, dt: np.zeros(size, dt)))(nc * 4, np.float64)
-    rc = N.gen().bcsgen_hex_coupled_poly(nx, ny, nz, float(aspect), int(scramble_seed), int(poly_seed), N.ptr(owner),
-                                         N.ptr(neigh), N.ptr(diag), N.ptr(upper), N.ptr(lower), N.ptr(rhs), N.ptr(x0),
-                                         N.ptr(cen))
-    if rc:
-        raise ValueError("bcsgen_hex_coupled: bad arguments")
+    if fill:
+        rc = N.gen().bcsgen_hex_coupled_poly(nx, ny, nz, float(aspect), int(scramble_seed), int(poly_seed),
+                                             N.ptr(owner), N.ptr(neigh), N.ptr(diag), N.ptr(upper), N.ptr(lower),
+                                             N.ptr(rhs), N.ptr(x0), N.ptr(cen))
+        if rc:
+            raise ValueError("bcsgen_hex_coupled: bad arguments")
     A = BlockLduMatrix(nc, owner, neigh, 4, diag, upper, lower)
     return System(A, BlockVector(nc, 4, rhs), BlockVector(nc, 4, x0), cen.reshape(nc, 3),
                   f"coupled4 {nx}x{ny}x{nz} {_tag(scramble_seed, poly_seed)} AR{aspect:g}")
