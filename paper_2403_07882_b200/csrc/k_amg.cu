@@ -6,10 +6,11 @@
 // Aggregation is a sequential greedy matching in row order.  Its exact
 // parallel form: row r's decision depends only on (a) its lower neighbours
 // (was r already taken?) and (b) the lower-than-r neighbours of each upper
-// neighbour j (is j still free?).  We run Kahn's algorithm over that
-// dependency DAG in a persistent cooperative kernel (one grid barrier per
-// round); when all dependencies of r are decided its decision equals the
-// sequential one.  Strengths are computed with the reference's operation
+// neighbour j (is j still free?).  k_agg_syncfree resolves that DAG
+// sync-free: rows are taken in index order by co-resident warps (cooperative
+// launch), each polls the decisions it depends on and decides as soon as they
+// are known, which equals the sequential decision (the round-synchronous Kahn
+// form, k_agg_rounds, is kept behind BCS_AGG_MODE=1).  Strengths are computed with the reference's operation
 // order (sequential Frobenius sums, IEEE sqrt/div, no FMA), so the integer
 // aggregates are bit-identical.  Galerkin sums are taken per coarse block in
 // (fine row ascending, slot ascending) order from +0.0 — also bit-identical.

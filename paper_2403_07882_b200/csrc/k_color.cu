@@ -6,8 +6,9 @@
 // coupled rows share a colour) and the smoother runs on the level's matrix
 // symmetrically permuted by colour.  On that matrix a row's lower neighbours
 // all carry smaller colours, so the natural-order machinery (sync-free DILU
-// setup, sync-free sweeps, k_sweep.cu) sees a DAG only #colours deep: the
-// sweeps become throughput (HBM) bound.  The hierarchy itself, the SpMVs and
+// setup, sync-free sweeps, k_sweep.cu) sees a DAG only #colours deep, and the
+// big levels run one streaming launch per colour (k_mc_colour): the sweeps
+// become throughput (HBM) bound.  The hierarchy itself, the SpMVs and
 // the Krylov method are unchanged; the smoother is a different operator, so
 // iteration counts differ from the reference and are reported as such.
 //
