@@ -8,10 +8,11 @@ from paper_2403_07882_b200 import bcs, gen
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 method = sys.argv[2] if len(sys.argv) > 2 else "gmres"
+mode = {"parity": bcs.Mode.PARITY, "perf": bcs.Mode.PERF, "jacobi": bcs.Mode.PERF_JACOBI}[sys.argv[3] if len(sys.argv) > 3 else "parity"]
 s = gen.hex_euler(n)
 cfg = bcs.SolverConfig(method=bcs.KrylovMethod.FGMRES if method == "fgmres" else bcs.KrylovMethod.GMRES,
                        preconditioner=bcs.PrecondKind.AMG, relTol=1e-8, maxIters=1000,
-                       amg=bcs.AmgConfig(maxLevels=30, minCoarseRows=8))
+                       amg=bcs.AmgConfig(maxLevels=30, minCoarseRows=8), mode=mode)
 ctx = bcs.Context(0)
 ctx.set_stream(torch.cuda.current_stream().cuda_stream)
 ctx.set_topology(s.A)
