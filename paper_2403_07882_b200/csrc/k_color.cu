@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(256) k_mc_sweep(int ncol, const int* __restric
 // from the earlier colours' results), then fold them in slot order and solve
 // with the row's LU -- the operation sequence of the sync-free sweeps, so the
 // result is bit-identical to them.  Kernel boundaries order the colours.
-constexpr int kMcDeps = 3;
+constexpr int kMcDeps = 4;
 constexpr int kMcWarps = 8;  // warps per CTA
 
 __device__ __forceinline__ unsigned mc_smem(const void* p) {
@@ -380,7 +380,7 @@ __device__ __forceinline__ unsigned mc_bulk(void* dst, const void* src, unsigned
 }
 
 template <int N, bool FWD>
-__global__ void __launch_bounds__(256, 3) k_mc_colour(int i0, int i1, const int* __restrict__ ro,
+__global__ void __launch_bounds__(256, 4) k_mc_colour(int i0, int i1, const int* __restrict__ ro,
                                                    const int* __restrict__ dg, const int* __restrict__ ci,
                                                    const double* __restrict__ v, const double* __restrict__ lu,
                                                    const double* __restrict__ rcp, const int* __restrict__ perm,
