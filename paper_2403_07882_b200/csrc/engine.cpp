@@ -1317,7 +1317,14 @@ void Engine::smootherApply(Level& L, const double* r, double* z, int accumulate)
         // performance mode: the multicolour DILU on the colour-permuted copy;
         // r in, result scattered back (and accumulated) in the level's numbering
         Level& M = *L.mc;
-        mc_vec_gather(n_, L.rows, L.mcPerm, r, M.r.p, stream_);
+        // one launch per colour: the gather of r and the scatter of z are fused
+        // into the first-colour forward and the backward colour kernels
+        static const bool fuseOn = [] {
+            const char* e = std::getenv("BCS_MC_FUSE");
+            return !e || std::atoi(e) != 0;
+        }();
+        const bool fused = M.colourSweep && !mcSweep_ && fuseOn;
+        if (!fused) mc_vec_gather(n_, L.rows, L.mcPerm, r, M.r.p, stream_);
         if (M.colourSweep) {
             // colour-synchronous sweeps: the forward reads the lower triangle,
             // the backward the upper one, each with the row's LU, input, output
@@ -1337,19 +1344,19 @@ void Engine::smootherApply(Level& L, const double* r, double* z, int accumulate)
                 const auto& co = L.mcColorOff;
                 if (kernelTiming_) timerBegin();
                 for (int c = 0; c < L.ncolors; ++c)
-                    mc_colour_sweep(n_, true, co[c], co[c + 1], M.ro, M.dg, M.ci, M.v, M.lu, M.rcp, M.perm, M.r,
-                                    M.y.p, stream_);
+                    mc_colour_sweep(n_, true, co[c], co[c + 1], M.ro, M.dg, M.ci, M.v, M.lu, M.rcp, M.perm,
+                                    fused ? r : M.r.p, M.y.p, fused ? L.mcPerm.p : nullptr, nullptr, 0, stream_);
                 if (kernelTiming_) timerEnd(1, per);
                 if (kernelTiming_) timerBegin();
                 for (int c = L.ncolors - 1; c >= 0; --c)
                     mc_colour_sweep(n_, false, co[c], co[c + 1], M.ro, M.dg, M.ci, M.v, M.lu, M.rcp, M.perm, M.y,
-                                    M.zb.p, stream_);
+                                    M.zb.p, fused ? L.mcPerm.p : nullptr, fused ? z : nullptr, accumulate, stream_);
                 if (kernelTiming_) timerEnd(1, per);
             }
         } else {
             smootherApply(M, M.r, M.zb.p, 0);
         }
-        mc_vec_scatter(n_, L.rows, L.mcPerm, M.zb, z, accumulate, stream_);
+        if (!fused) mc_vec_scatter(n_, L.rows, L.mcPerm, M.zb, z, accumulate, stream_);
         return;
     }
     const size_t N = static_cast<size_t>(L.rows) * n_;

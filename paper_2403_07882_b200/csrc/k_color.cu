@@ -379,12 +379,18 @@ __device__ __forceinline__ unsigned mc_bulk(void* dst, const void* src, unsigned
     return static_cast<unsigned>(s0 - lo);
 }
 
+// rowmap (the coloured level's new -> original row map), when given: the
+// forward reads its input r in the original numbering (the gather into the
+// coloured order fused), the backward also writes its result to zfinal in the
+// original numbering with k_vec_scatter's accumulate semantics (zacc; the
+// scatter fused).
 template <int N, bool FWD>
 __global__ void __launch_bounds__(256, 4) k_mc_colour(int i0, int i1, const int* __restrict__ ro,
                                                    const int* __restrict__ dg, const int* __restrict__ ci,
                                                    const double* __restrict__ v, const double* __restrict__ lu,
                                                    const double* __restrict__ rcp, const int* __restrict__ perm,
-                                                   const double* __restrict__ rin, double* out) {
+                                                   const double* __restrict__ rin, double* out,
+                                                   const int* __restrict__ rowmap, double* zfinal, int zacc) {
     constexpr int NN = N * N, G = 32 / N, RB = kMcWarps * G;  // rows per CTA
     // the CTA's rows' factors, reciprocals and permutations (contiguous in the
     // colour-ordered level) arrive by TMA while the warps fold their dependencies
@@ -414,8 +420,9 @@ __global__ void __launch_bounds__(256, 4) k_mc_colour(int i0, int i1, const int*
     const size_t ib = static_cast<size_t>(row ? i : c0row);
     double ri = 0.0;
     int kb = 0, cnt = 0;
+    const size_t orig = rowmap && row ? static_cast<size_t>(__ldg(&rowmap[ib])) : ib;  // original row
     if (row) {
-        ri = __ldg(&rin[ib * N + q]);
+        ri = FWD && rowmap ? __ldg(&rin[orig * N + q]) : __ldg(&rin[ib * N + q]);
         const int k0 = __ldg(&ro[ib]), kd = __ldg(&dg[ib]), k1 = __ldg(&ro[ib + 1]);
         kb = FWD ? k0 : k1 - 1;
         cnt = FWD ? kd - k0 : k1 - 1 - kd;
@@ -479,20 +486,27 @@ __global__ void __launch_bounds__(256, 4) k_mc_colour(int i0, int i1, const int*
     double mine = x[0];
 #pragma unroll
     for (int p = 1; p < N; ++p) mine = (q == p) ? x[p] : mine;
-    out[ib * N + q] = FWD ? mine : __dsub_rn(ri, mine);
+    const double res = FWD ? mine : __dsub_rn(ri, mine);
+    out[ib * N + q] = res;
+    if (!FWD && zfinal) {
+        const size_t o = orig * N + q;
+        zfinal[o] = zacc == 2 ? __dadd_rn(zfinal[o], res) : zacc == 1 ? __dadd_rn(0.0, res) : res;
+    }
 }
 
 void mc_colour_sweep(int n, bool fwd, int i0, int i1, const int* ro, const int* dg, const int* ci, const double* v,
                      const double* lu, const double* rcp, const int* perm, const double* rin, double* out,
-                     cudaStream_t s) {
+                     const int* rowmap, double* zfinal, int acc, cudaStream_t s) {
     if (i1 <= i0) return;
     const long long rb = static_cast<long long>(kMcWarps) * (32 / n);  // rows per CTA
     const unsigned g = static_cast<unsigned>((static_cast<long long>(i1 - i0) + rb - 1) / rb);
     switch (n) {
 #define BCS_MCC_CASE(NV)                                                                                        \
     case NV:                                                                                                    \
-        if (fwd) k_mc_colour<NV, true><<<g, 256, 0, s>>>(i0, i1, ro, dg, ci, v, lu, rcp, perm, rin, out);      \
-        else k_mc_colour<NV, false><<<g, 256, 0, s>>>(i0, i1, ro, dg, ci, v, lu, rcp, perm, rin, out);         \
+        if (fwd) k_mc_colour<NV, true><<<g, 256, 0, s>>>(i0, i1, ro, dg, ci, v, lu, rcp, perm, rin, out, rowmap,  \
+                                                         zfinal, acc);                                         \
+        else k_mc_colour<NV, false><<<g, 256, 0, s>>>(i0, i1, ro, dg, ci, v, lu, rcp, perm, rin, out, rowmap,  \
+                                                      zfinal, acc);                                            \
         break;
         BCS_MCC_CASE(1)
         BCS_MCC_CASE(2)

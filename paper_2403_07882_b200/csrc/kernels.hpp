@@ -64,9 +64,12 @@ void block_jacobi(int n, int rows, const double* lu, const double* rcp, const in
 // performance mode: one colour [i0, i1) of the colour-permuted level as a
 // streaming pass (rows of a colour are independent); forward colours in
 // increasing order, backward in decreasing order, one launch each
+// rowmap != null: the forward reads rin in the original numbering (fused
+// gather); the backward also writes zfinal[rowmap[i]] with k_vec_scatter's
+// acc semantics (fused scatter)
 void mc_colour_sweep(int n, bool fwd, int i0, int i1, const int* ro, const int* dg, const int* ci, const double* v,
                      const double* lu, const double* rcp, const int* perm, const double* rin, double* out,
-                     cudaStream_t s);
+                     const int* rowmap, double* zfinal, int acc, cudaStream_t s);
 void mc_sweep(int n, bool fwd, int rows, int ncol, const int* coff, const int* ro, const int* dg, const int* ci,
               const double* v, const double* lu, const double* rcp, const int* perm, const double* rin, double* out,
               cudaStream_t s);
