@@ -209,3 +209,28 @@ def test_dist_solve_parts_matches_dist_solve(ctx, maker, ranks, engines, mode):
     x, r = ctx.dist_solve_parts(parts, bnew.reshape(-1), xnew.reshape(-1), n, engines, r2e, ero, cfg)
     assert r.iterations == r_ref.iterations
     assert x.reshape(-1, n)[o2n].tobytes() == np.asarray(x_ref.values).tobytes()
+
+
+def test_dist_solve_parts_rejects_bad_plans(ctx):
+    """The reference's errors on bad consolidation plans (partition.cpp:184-199)
+    and rank lists, as invalid_argument -> ValueError, without touching the device state."""
+    s = gen.hex_euler(6)
+    A, n = s.A, s.A.n
+    P = bcs.Partition(A.n_cells, A.owner, A.neighbour, s.centroids, 2)
+    parts = []
+    for r in range(2):
+        d = P.part(r)
+        loc, halo = P.gather_values(r, A)
+        parts.append(dict(row_start=d["row_start"], row_end=d["row_end"], ro=d["ro"], ci=d["ci"], values=loc,
+                          halo_row=d["halo_row"], halo_col=d["halo_col"], halo_peer=d["halo_peer"], halo_values=halo))
+    cfg = bcs.SolverConfig(preconditioner=bcs.PrecondKind.AMG, relTol=1e-8, amg=bcs.AmgConfig(maxLevels=30, minCoarseRows=8))
+    b = np.ones(A.n_cells * n)
+    with pytest.raises(ValueError, match="makeConsolidationPlan"):
+        ctx.dist_solve_parts(parts, b, b * 0, n, 3, [0, 1], [0, 0], cfg)
+    with pytest.raises(ValueError, match="rank mapped to no engine"):
+        ctx.dist_solve_parts(parts, b, b * 0, n, 1, [0, 1], [0, 0], cfg)
+    with pytest.raises(ValueError, match="block size"):
+        ctx.dist_solve_parts(parts, b, b * 0, 7, 1, [0, 0], [0, 0], cfg)
+    # the context still solves afterwards
+    x, r = ctx.dist_solve_parts(parts, b, b * 0, n, 1, [0, 0], [0, parts[0]["row_end"] - parts[0]["row_start"]], cfg)
+    assert r.converged
